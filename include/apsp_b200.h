@@ -1,0 +1,125 @@
+/*
+ * apsp_b200.h -- C ABI of the B200-native dense APSP engine (libapsp_b200.so).
+ *
+ * Drop-in boundary for the reference's hot path (apsp 0.1.0, /root/reference/pkg/src/apsp):
+ * each entry point below replaces one reference function; the Python package
+ * paper_2310_03983_b200 binds them with ctypes and keeps the reference's Python API
+ * (fw_classic / rkleene / fw_squaring / minplus_product / minplus_accumulate).
+ *
+ * Conventions
+ *   - dtype: APSP_DTYPE_I32 (Infinity = 0x3FFFFFFF), APSP_DTYPE_F32 (Infinity = +inf),
+ *            APSP_DTYPE_I64 (Infinity = 2^61 = the reference's INF_RAW, core.py:19).
+ *   - index matrices (pred / via) are int32 on the device, -1 = None (core.py:233-272);
+ *     the host-level call can widen them to int64 like the reference's PredMatrix/ViaMatrix.
+ *   - matrices are row-major with a leading dimension (elements).
+ *   - device-level calls take device pointers and a cudaStream_t (NULL = legacy default
+ *     stream).  They are stream-ordered except for the small host reads the solver needs
+ *     to pick and certify a value tier (documented per call).  ws may be NULL: the library
+ *     then allocates stream-ordered scratch itself.
+ *   - every call returns an apsp_status; apsp_last_error() holds a thread-local message.
+ */
+#ifndef APSP_B200_H
+#define APSP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APSP_ABI_VERSION 1
+
+typedef enum {
+  APSP_OK = 0,
+  APSP_ERANGE = 1,      /* -> CostRangeError      (solvers.py:91-92,146-147; minplus.py:158-163) */
+  APSP_EINVAL = 2,      /* -> ParameterError      (solvers.py:131-132,227-230; minplus.py:181-183) */
+  APSP_ECUDA = 3,       /* CUDA runtime failure */
+  APSP_ENCCL = 4,       /* collective failure (multi-GPU path) */
+  APSP_ENEGATIVE = 5,   /* -> NegativeWeightError (solvers.py:70-71; minplus.py:153-155) */
+  APSP_EDIAGONAL = 6,   /* -> MalformedGraphError (solvers.py:72-73) */
+  APSP_EDIMENSION = 7,  /* -> DimensionError      (minplus.py:179-180,221-228) */
+  APSP_ECONVERGE = 8    /* -> ApspError           (solvers.py:195-196) */
+} apsp_status;
+
+typedef enum { APSP_DTYPE_I32 = 0, APSP_DTYPE_F32 = 1, APSP_DTYPE_I64 = 2 } apsp_dtype;
+
+/* Value tiers (in-HBM store formats); AUTO picks the narrowest exact one and certifies it. */
+typedef enum {
+  APSP_TIER_AUTO = -1,
+  APSP_TIER_U8 = 0,   /* uint8 store, 16-bit packed keys, VIADDMNMX.S16x2 */
+  APSP_TIER_W32 = 1,  /* int32 store (< 2^24), 32-bit keys, VIADD + VIMNMX3 */
+  APSP_TIER_I32 = 2,  /* exact int32 compare-select */
+  APSP_TIER_F32 = 3,  /* exact fp32 compare-select (continuous weights) */
+  APSP_TIER_I64 = 4   /* exact int64 compare-select (full reference range) */
+} apsp_tier;
+
+typedef enum { APSP_IDX_PRED = 0, APSP_IDX_VIA = 1 } apsp_idx_mode;
+
+typedef enum {
+  APSP_ALG_FW_BLOCKED = 0,  /* blocked 3-phase FW (replaces fw_classic, solvers.py:118) */
+  APSP_ALG_FW_CLASSIC = 1,  /* classic k-order FW, bit-exact pred (solvers.py:118-155) */
+  APSP_ALG_RKLEENE = 2,     /* recursive closure (solvers.py:207-296) */
+  APSP_ALG_FW_SQUARING = 3  /* repeated min-plus squaring (solvers.py:167-204) */
+} apsp_algorithm;
+
+typedef struct apsp_info {
+  int32_t tier;         /* tier that produced the returned result */
+  int32_t tiers_tried;  /* bitmask over apsp_tier values */
+  int32_t iterations;   /* fw_squaring rounds (solvers.py:186-194); 0 otherwise */
+  int32_t launches;     /* kernels launched by the call */
+  int64_t max_finite;   /* largest finite distance of the result (integer tiers) */
+  int64_t relaxations;  /* exact candidate count, the reference's relaxation_count */
+  double device_ms;     /* CUDA-event time of the solve (device-level calls) */
+  int32_t flags;        /* bit 0: zero-cost edges -> classic k order used for predecessors */
+  int32_t reserved;
+} apsp_info;
+
+const char* apsp_last_error(void);
+int apsp_abi_version(void);
+
+/* Scratch bytes the device-level calls need when ws != NULL. */
+size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block);
+
+/* Blocked three-phase Floyd-Warshall, in place on dist; pred (int32, n x n, ldp) receives
+ * predecessors (pred[i][j] = last vertex before j, -1 = None).
+ * Replaces fw_classic (solvers.py:118-155): same distances bit-exactly, pred a valid
+ * shortest-path tree (equal-length ties may pick another predecessor).
+ * block: pivot block size (128).  Host syncs: after the input scan, after the certificate. */
+int apsp_fw_blocked(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int block,
+                    int tier, void* ws, size_t ws_bytes, void* stream, apsp_info* info);
+
+/* Classic k-order Floyd-Warshall (one launch per k), in place; bit-exact dist and pred with
+ * fw_classic (solvers.py:77-95,134-147).  dtype = storage of dist (no tiering). */
+int apsp_fw_classic(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, void* stream,
+                    apsp_info* info);
+
+/* R-Kleene recursive closure (solvers.py:207-296), in place on dist; idx receives via (global
+ * intermediate vertex, APSP_IDX_VIA) or pred (APSP_IDX_PRED).
+ * aligned = 0: floor split and classic leaves at base_threshold -> via bit-exact with rkleene.
+ * aligned = 1: splits on 128-multiples, leaves of <= base_threshold closed by blocked FW. */
+int apsp_rkleene(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int64_t ldi, int idx_mode,
+                 int base_threshold, int aligned, int tier, void* ws, size_t ws_bytes, void* stream, apsp_info* info);
+
+/* Repeated squaring H <- min(H, H (x) H) until unchanged (solvers.py:167-204); via folded. */
+int apsp_fw_squaring(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, int64_t ldv, int tier, void* ws,
+                     size_t ws_bytes, void* stream, apsp_info* info);
+
+/* minplus_product (accumulate = 0; minplus.py:166-203, offsets = (row, inner, col)) and
+ * minplus_accumulate (accumulate = 1; minplus.py:206-252, z and via are the seeds).
+ * x: n1 x n2, y: n2 x n3, z: n1 x n3 (out; in for accumulate), via: n1 x n3 (out; in for accumulate). */
+int apsp_minplus(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, const void* x, int64_t ldx,
+                 const void* y, int64_t ldy, void* z, int64_t ldz, int32_t* via, int64_t ldv, int64_t row_off,
+                 int64_t inner_off, int64_t col_off, int tier, void* stream, apsp_info* info);
+
+/* Host-level call (reference-facing): host input h (n x n, dense, dtype), host outputs
+ * dist_out (dtype) and idx_out (idx_dtype = APSP_DTYPE_I32 or APSP_DTYPE_I64).  Copies in,
+ * solves on `device`, copies out; synchronous like the reference solvers.
+ * algorithm: apsp_algorithm; idx_mode: APSP_IDX_PRED / APSP_IDX_VIA (rkleene only). */
+int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* dist_out, void* idx_out, int idx_dtype,
+                    int idx_mode, int block, int base_threshold, int aligned, int tier, int device, apsp_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* APSP_B200_H */

@@ -1,0 +1,833 @@
+// C ABI and native orchestration: blocked FW rounds, R-Kleene recursion, squaring loop,
+// min-plus products, value-tier selection and certification, host-level entry.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+#include "../../include/apsp_b200.h"
+#include "launch.h"
+
+namespace apsp {
+const char* last_error();
+int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out,
+                         int64_t ldo, cudaStream_t s);
+}
+
+using namespace apsp;
+
+namespace {
+
+constexpr int DEFAULT_BLOCK = 128;
+constexpr int TILE_ALIGN = 128;
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+int tier_store(int tier) {
+  switch (tier) {
+    case APSP_TIER_U8: return STORE_U8;
+    case APSP_TIER_W32: return STORE_W32;
+    case APSP_TIER_I32: return STORE_I32;
+    case APSP_TIER_F32: return STORE_F32;
+    case APSP_TIER_I64: return STORE_I64;
+  }
+  return -1;
+}
+
+// Largest finite value a tier can hold.  A result is certified exact when
+// max_finite + w_max <= limit: every cell with true distance <= limit is computed exactly
+// (all partial sums of its shortest path are <= it), and a reachable cell beyond the limit
+// would force a cell within (limit - w_max, limit] along its shortest path.
+int64_t tier_limit(int tier) {
+  switch (tier) {
+    case APSP_TIER_U8: return U8_INF - 1;
+    case APSP_TIER_W32: return W32_INF - 1;
+    case APSP_TIER_I32: return INF32 - 1;
+    case APSP_TIER_I64: return MAX_FINITE_COST;
+  }
+  return INT64_MAX;
+}
+
+struct Scratch {
+  void* base = nullptr;
+  bool owned = false;
+  cudaStream_t s = nullptr;
+  ~Scratch() {
+    if (owned && base) cudaFreeAsync(base, s);
+  }
+  int acquire(void* ws, size_t ws_bytes, size_t need, cudaStream_t st) {
+    s = st;
+    if (ws) {
+      if (ws_bytes < need) return set_error(APSP_EINVAL, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+      base = ws;
+      return 0;
+    }
+    APSP_CUDA_TRY(cudaMallocAsync(&base, need, st));
+    owned = true;
+    return 0;
+  }
+};
+
+struct Header {   // first 256 bytes of every workspace
+  Status status;
+  ScanResult scan;
+  ScanResult cert;
+};
+
+int read_header(Header* dev, Header& host, cudaStream_t s) {
+  APSP_CUDA_TRY(cudaMemcpyAsync(&host, dev, sizeof(Header), cudaMemcpyDeviceToHost, s));
+  APSP_CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int check_scan(const ScanResult& sc) {
+  if (sc.negative) return set_error(APSP_ENEGATIVE, "solver input contains a negative finite cost");
+  if (sc.diag_nonzero) return set_error(APSP_EDIAGONAL, "solver input must have a zero diagonal");
+  return 0;
+}
+
+// Candidate tiers, narrowest first.
+std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced) {
+  const bool integral = dtype != APSP_DTYPE_F32 || !sc.non_integral;
+  const int64_t w = sc.max_finite;
+  if (forced >= 0) {
+    // a forced tier must be able to hold the input (the certificate covers the result)
+    bool fits = forced == APSP_TIER_U8 ? integral && w <= U8_INF - 1
+              : forced == APSP_TIER_W32 ? integral && w <= W32_INF - 1
+              : forced == APSP_TIER_I32 ? (dtype != APSP_DTYPE_F32 && w <= INF32 - 1)
+              : forced == APSP_TIER_F32 ? dtype == APSP_DTYPE_F32
+              : forced == APSP_TIER_I64 ? dtype == APSP_DTYPE_I64 : false;
+    if (!fits) return {};
+    return {forced};
+  }
+  std::vector<int> t;
+  if (integral && w <= U8_INF - 1) t.push_back(APSP_TIER_U8);
+  if (integral && w <= W32_INF - 1) t.push_back(APSP_TIER_W32);
+  if (dtype == APSP_DTYPE_F32) t.push_back(APSP_TIER_F32);
+  else if (dtype == APSP_DTYPE_I32) t.push_back(APSP_TIER_I32);
+  else t.push_back(APSP_TIER_I64);
+  return t;
+}
+
+size_t header_bytes() { return 256; }
+
+// ---- blocked FW on an m x m view (m multiple of b) -------------------------------------
+int fw_blocked_view(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t m, int b, int mode,
+                    int64_t via_off, Status* st, cudaStream_t s, int* launches) {
+  const size_t es = store_elem_size(store);
+  char* Dc = static_cast<char*>(D);
+  for (int64_t k0 = 0; k0 < m; k0 += b) {
+    int rc = launch_block_close(store, D, ld, k0, b, P, ldp, mode, via_off + k0, st, s);
+    if (rc) return rc;
+    rc = launch_fw_panels(store, D, ld, P, ldp, m, k0, b, mode, via_off, st, s);
+    if (rc) return rc;
+    MinplusArgs a{};
+    a.A = Dc + k0 * es; a.lda = ld;
+    a.B = Dc + k0 * ld * es; a.ldb = ld;
+    a.C = D; a.ldc = ld;
+    a.idx = P; a.ldi = ldp;
+    a.predB = P ? P + k0 * ldp : nullptr; a.ldp = ldp;
+    a.m = m; a.n = m; a.k = b;
+    a.inner_off = via_off + k0;
+    a.mode = mode;
+    a.skip_row_lo = k0; a.skip_row_hi = k0 + b;
+    a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
+    a.status = st;
+    rc = launch_minplus(store, a, s);
+    if (rc) return rc;
+    *launches += 4;
+  }
+  return 0;
+}
+
+int certify(int tier, int store, const void* D, int64_t ld, int64_t rows, int64_t cols, const ScanResult& sc,
+            Header* hdr_dev, Header& hdr, cudaStream_t s, bool& ok) {
+  int rc = launch_max_finite(store, D, ld, rows, cols, &hdr_dev->cert, s);
+  if (rc) return rc;
+  rc = read_header(hdr_dev, hdr, s);
+  if (rc) return rc;
+  ok = true;
+  if (hdr.status.overflow) {
+    if (tier == APSP_TIER_I64) return set_error(APSP_ERANGE, "shortest-path cost left the representable finite range");
+    ok = false;
+  }
+  if (tier == APSP_TIER_F32) return 0;
+  const int64_t M = hdr.cert.max_finite;
+  if (M >= 0 && M + sc.max_finite > tier_limit(tier)) {
+    if (tier == APSP_TIER_I64) {
+      if (M > MAX_FINITE_COST) return set_error(APSP_ERANGE, "shortest-path cost left the representable finite range");
+    } else {
+      ok = false;
+    }
+  }
+  return 0;
+}
+
+struct Timer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  cudaStream_t s;
+  explicit Timer(cudaStream_t st) : s(st) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+  }
+  double stop() {
+    float ms = 0;
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, cudaStream_t s,
+                    apsp_info* info);
+
+// Zero-cost edges let equal-distance vertices point at each other when many cells are
+// relaxed at once (blocked phase 3, R-Kleene products); only the classic k order keeps the
+// predecessor graph a tree then.  Such inputs are solved by the classic kernel, which is
+// bit-exact with the reference for both dist and pred.
+constexpr int32_t FLAG_CLASSIC_FOR_ZERO_EDGES = 1;
+
+size_t fw_ws_bytes(int dtype, int64_t n, int block) {
+  const int64_t N = round_up(std::max<int64_t>(n, 1), block);
+  const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
+  return header_bytes() + size_t(N) * N * (es + 4) + 256;
+}
+
+int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
+                    void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info) {
+  if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
+  if (b <= 0) b = DEFAULT_BLOCK;
+  if (b != 128) return set_error(APSP_EINVAL, "blocked FW supports block = 128 (got %d)", b);
+  const int64_t N = round_up(n, b);
+  Scratch sc;
+  int rc = sc.acquire(ws, ws_bytes, fw_ws_bytes(dtype, n, b), s);
+  if (rc) return rc;
+  Header* hdr_dev = static_cast<Header*>(sc.base);
+  int32_t* P = reinterpret_cast<int32_t*>(static_cast<char*>(sc.base) + header_bytes());
+  void* D = reinterpret_cast<char*>(P) + size_t(N) * N * 4;
+  Header hdr{};
+  Timer tm(s);
+  rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
+  if (!rc) rc = read_header(hdr_dev, hdr, s);
+  if (rc) return rc;
+  const ScanResult scan = hdr.scan;
+  rc = check_scan(scan);
+  if (rc) return rc;
+  if (scan.zero_offdiag && pred) {
+    rc = fw_classic_impl(dtype, n, dist, ld, pred, ldp, s, info);
+    if (!rc && info) info->flags |= FLAG_CLASSIC_FOR_ZERO_EDGES;
+    return rc;
+  }
+  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req);
+  if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
+  int launches = 2, used = -1, tried = 0;
+  for (int tier : tiers) {
+    const int store = tier_store(tier);
+    if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+    if (store == STORE_I64 && dtype != APSP_DTYPE_I64) return set_error(APSP_EINVAL, "int64 tier needs int64 input");
+    tried |= 1 << tier;
+    APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
+    rc = launch_to_store(dtype, dist, ld, n, store, D, N, N, P, N, 1, s);
+    if (!rc) rc = fw_blocked_view(store, D, N, P, N, N, b, IDX_PRED, 0, &hdr_dev->status, s, &launches);
+    bool ok = false;
+    if (!rc) rc = certify(tier, store, D, N, n, n, scan, hdr_dev, hdr, s, ok);
+    if (rc) return rc;
+    launches += 2;
+    if (ok) {
+      used = tier;
+      break;
+    }
+  }
+  if (used < 0) {
+    if (dtype == APSP_DTYPE_I32)
+      return set_error(APSP_ERANGE, "shortest-path cost left the representable int32 range");
+    return set_error(APSP_ERANGE, "no value tier could represent the result");
+  }
+  rc = launch_from_store(tier_store(used), D, N, n, n, dtype, dist, ld, s);
+  if (!rc && pred) rc = launch_copy_idx(P, N, n, n, APSP_DTYPE_I32, pred, ldp, s);
+  if (rc) return rc;
+  launches += 2;
+  const double ms = tm.stop();
+  if (info) {
+    info->tier = used;
+    info->tiers_tried = tried;
+    info->iterations = 0;
+    info->launches = launches;
+    info->max_finite = hdr.cert.max_finite;
+    info->relaxations = n * n * n;
+    info->device_ms = ms;
+    info->flags = 0;
+  }
+  return 0;
+}
+
+int api_store(int dtype) {
+  return dtype == APSP_DTYPE_I32 ? STORE_I32 : dtype == APSP_DTYPE_F32 ? STORE_F32 : STORE_I64;
+}
+
+int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, cudaStream_t s,
+                    apsp_info* info) {
+  if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
+  Scratch sc;
+  int rc = sc.acquire(nullptr, 0, header_bytes(), s);
+  if (rc) return rc;
+  Header* hdr_dev = static_cast<Header*>(sc.base);
+  Header hdr{};
+  Timer tm(s);
+  rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
+  if (!rc) rc = read_header(hdr_dev, hdr, s);
+  if (rc) return rc;
+  const ScanResult scan = hdr.scan;
+  rc = check_scan(scan);
+  if (rc) return rc;
+  const int store = api_store(dtype);
+  APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
+  // pred init in place (to_store with identical in/out is elementwise)
+  rc = launch_to_store(dtype, dist, ld, n, store, dist, ld, n, pred, ldp, 1, s);
+  for (int64_t k = 0; !rc && k < n; k++) rc = launch_fw_step(store, dist, ld, n, k, pred, ldp, IDX_PRED, 0, &hdr_dev->status, s);
+  if (rc) return rc;
+  const int tier = dtype == APSP_DTYPE_I32 ? APSP_TIER_I32 : dtype == APSP_DTYPE_F32 ? APSP_TIER_F32 : APSP_TIER_I64;
+  bool ok = false;
+  rc = certify(tier, store, dist, ld, n, n, scan, hdr_dev, hdr, s, ok);
+  if (rc) return rc;
+  if (!ok) return set_error(APSP_ERANGE, "shortest-path cost left the representable int32 range");
+  const double ms = tm.stop();
+  if (info) {
+    info->tier = tier;
+    info->tiers_tried = 1 << tier;
+    info->iterations = 0;
+    info->launches = int32_t(n + 3);
+    info->max_finite = hdr.cert.max_finite;
+    info->relaxations = n * n * n;
+    info->device_ms = ms;
+    info->flags = 0;
+  }
+  return 0;
+}
+
+// ---- R-Kleene ---------------------------------------------------------------------------
+struct RK {
+  int store;
+  size_t es;
+  char* D;
+  int64_t ld;
+  int32_t* P;     // idx matrix (pred or via), ld = ld
+  int mode;
+  int thr;
+  bool aligned;
+  char* sV;       // snapshot values (half x half)
+  int32_t* sP;    // snapshot idx
+  int64_t sld;
+  Status* st;
+  cudaStream_t s;
+  int launches = 0;
+
+  char* at(int64_t i, int64_t j) const { return D + (i * ld + j) * es; }
+  int32_t* pat(int64_t i, int64_t j) const { return P + i * ld + j; }
+
+  int mp(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t r0, int64_t c0, int64_t m, int64_t n,
+         int64_t k, const int32_t* predB, int64_t ldpb, int64_t inner_off) {
+    MinplusArgs a{};
+    a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
+    a.C = at(r0, c0); a.ldc = ld;
+    a.idx = pat(r0, c0); a.ldi = ld;
+    a.predB = predB; a.ldp = ldpb;
+    a.m = m; a.n = n; a.k = k;
+    a.inner_off = inner_off;
+    a.mode = mode;
+    a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
+    a.status = st;
+    launches++;
+    return launch_minplus(store, a, s);
+  }
+  int snap_vals(int64_t r0, int64_t c0, int64_t rows, int64_t cols) {
+    launches++;
+    return launch_copy_block(store, at(r0, c0), ld, sV, sld, rows, cols, s);
+  }
+  int snap_idx(int64_t r0, int64_t c0, int64_t rows, int64_t cols) {
+    if (rows <= 0 || cols <= 0) return 0;
+    launches++;
+    APSP_CUDA_TRY(cudaMemcpy2DAsync(sP, size_t(sld) * 4, pat(r0, c0), size_t(ld) * 4, size_t(cols) * 4, size_t(rows),
+                                    cudaMemcpyDeviceToDevice, s));
+    return 0;
+  }
+
+  int64_t split(int64_t m) const {
+    if (!aligned) return m / 2;
+    const int64_t tiles = m / TILE_ALIGN;
+    return ((tiles + 1) / 2) * TILE_ALIGN;
+  }
+
+  int leaf(int64_t lo, int64_t m) {
+    if (aligned && m > 128) {
+      return fw_blocked_view(store, at(lo, lo), ld, pat(lo, lo), ld, m, DEFAULT_BLOCK, mode, lo, st, s, &launches);
+    }
+    launches += int(m > 128 ? m : 1);
+    return launch_block_close(store, D, ld, lo, m, P, ld, mode, lo, st, s);
+  }
+
+  // solvers.py:239-286, every block op as C <- min(C, X (x) Y) with strict-improvement argmin
+  int close(int64_t lo, int64_t hi) {
+    const int64_t m = hi - lo;
+    if (m <= thr || (aligned && m <= TILE_ALIGN)) return leaf(lo, m);
+    const int64_t mid = lo + split(m);
+    const int64_t a = mid - lo, d = hi - mid;
+    const bool pred = mode == IDX_PRED;
+    int rc = close(lo, mid);
+    // B <- A (x) B   (B aliased: snapshot B values and, for pred, B's pred rows)
+    if (!rc) rc = snap_vals(lo, mid, a, d);
+    if (!rc && pred) rc = snap_idx(lo, mid, a, d);
+    if (!rc) rc = mp(at(lo, lo), ld, sV, sld, lo, mid, a, d, a, pred ? sP : nullptr, sld, lo);
+    // C <- C (x) A   (C aliased as the left operand)
+    if (!rc) rc = snap_vals(mid, lo, d, a);
+    if (!rc) rc = mp(sV, sld, at(lo, lo), ld, mid, lo, d, a, a, pat(lo, lo), ld, lo);
+    // D <- min(D, C (x) B)
+    if (!rc) rc = mp(at(mid, lo), ld, at(lo, mid), ld, mid, mid, d, d, a, pat(lo, mid), ld, lo);
+    if (!rc) rc = close(mid, hi);
+    // B <- B (x) D   (B aliased as the left operand)
+    if (!rc) rc = snap_vals(lo, mid, a, d);
+    if (!rc) rc = mp(sV, sld, at(mid, mid), ld, lo, mid, a, d, d, pat(mid, mid), ld, mid);
+    // C <- D (x) C   (C aliased as the right operand)
+    if (!rc) rc = snap_vals(mid, lo, d, a);
+    if (!rc && pred) rc = snap_idx(mid, lo, d, a);
+    if (!rc) rc = mp(at(mid, mid), ld, sV, sld, mid, lo, d, a, d, pred ? sP : nullptr, sld, mid);
+    // A <- min(A, B (x) C)
+    if (!rc) rc = mp(at(lo, mid), ld, at(mid, lo), ld, lo, lo, a, a, d, pat(mid, lo), ld, mid);
+    return rc;
+  }
+};
+
+// Largest block side below the root: floor split -> ceil(N/2); aligned split -> the first
+// half, ceil(tiles/2) tiles.
+int64_t rk_half(int64_t N, int aligned) {
+  return aligned ? ((N / TILE_ALIGN + 1) / 2) * TILE_ALIGN : N - N / 2;
+}
+
+size_t rk_ws_bytes(int dtype, int64_t n, int aligned) {
+  const int64_t N = aligned ? round_up(n, TILE_ALIGN) : n;
+  const int64_t h = rk_half(N, aligned);
+  const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
+  return header_bytes() + size_t(N) * N * (es + 4) + size_t(h + 8) * (h + 8) * (es + 4) + 1024;
+}
+
+int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int64_t ldi, int idx_mode, int thr,
+                 int aligned, int tier_req, void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info) {
+  if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
+  if (thr < 1) return set_error(APSP_EINVAL, "base_threshold must be >= 1, got %d", thr);
+  const int64_t N = aligned ? round_up(n, TILE_ALIGN) : n;
+  const int64_t h = rk_half(N, aligned);
+  Scratch sc;
+  int rc = sc.acquire(ws, ws_bytes, rk_ws_bytes(dtype, n, aligned), s);
+  if (rc) return rc;
+  Header* hdr_dev = static_cast<Header*>(sc.base);
+  char* p = static_cast<char*>(sc.base) + header_bytes();
+  int32_t* P = reinterpret_cast<int32_t*>(p);
+  p += size_t(N) * N * 4;
+  int32_t* sP = reinterpret_cast<int32_t*>(p);
+  p += size_t(h + 8) * (h + 8) * 4;
+  char* D = p;
+  p += size_t(N) * N * (dtype == APSP_DTYPE_I64 ? 8 : 4);
+  char* sV = p;
+  Header hdr{};
+  Timer tm(s);
+  rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
+  if (!rc) rc = read_header(hdr_dev, hdr, s);
+  if (rc) return rc;
+  const ScanResult scan = hdr.scan;
+  rc = check_scan(scan);
+  if (rc) return rc;
+  if (scan.zero_offdiag && idx_mode == IDX_PRED && idx) {
+    rc = fw_classic_impl(dtype, n, dist, ld, idx, ldi, s, info);
+    if (!rc && info) info->flags |= FLAG_CLASSIC_FOR_ZERO_EDGES;
+    return rc;
+  }
+  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req);
+  if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
+  int used = -1, tried = 0, launches = 2;
+  for (int tier : tiers) {
+    const int store = tier_store(tier);
+    if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+    if (store == STORE_I64 && dtype != APSP_DTYPE_I64) return set_error(APSP_EINVAL, "int64 tier needs int64 input");
+    tried |= 1 << tier;
+    APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
+    rc = launch_to_store(dtype, dist, ld, n, store, D, N, N, idx_mode == IDX_PRED ? P : nullptr, N, 1, s);
+    if (!rc && idx_mode == IDX_VIA) rc = launch_fill_idx(P, N, N, N, -1, s);
+    RK rk{store, store_elem_size(store), D, N, P, idx_mode, thr, aligned != 0, sV, sP, h, &hdr_dev->status, s};
+    if (!rc) rc = rk.close(0, N);
+    bool ok = false;
+    if (!rc) rc = certify(tier, store, D, N, n, n, scan, hdr_dev, hdr, s, ok);
+    if (rc) return rc;
+    launches += rk.launches + 3;
+    if (ok) {
+      used = tier;
+      break;
+    }
+  }
+  if (used < 0) {
+    if (dtype == APSP_DTYPE_I32) return set_error(APSP_ERANGE, "shortest-path cost left the representable int32 range");
+    return set_error(APSP_ERANGE, "no value tier could represent the result");
+  }
+  rc = launch_from_store(tier_store(used), D, N, n, n, dtype, dist, ld, s);
+  if (!rc && idx) rc = launch_copy_idx(P, N, n, n, APSP_DTYPE_I32, idx, ldi, s);
+  if (rc) return rc;
+  const double ms = tm.stop();
+  if (info) {
+    info->tier = used;
+    info->tiers_tried = tried;
+    info->iterations = 0;
+    info->launches = launches + 2;
+    info->max_finite = hdr.cert.max_finite;
+    info->relaxations = n * n * n;
+    info->device_ms = ms;
+    info->flags = 0;
+  }
+  return 0;
+}
+
+// ---- fw_squaring ----------------------------------------------------------------------------
+size_t sq_ws_bytes(int dtype, int64_t n) {
+  const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
+  return header_bytes() + 2 * size_t(n) * n * (es + 4) + 1024;
+}
+
+int squaring_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, int64_t ldv, int tier_req, void* ws,
+                  size_t ws_bytes, cudaStream_t s, apsp_info* info) {
+  if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
+  Scratch sc;
+  int rc = sc.acquire(ws, ws_bytes, sq_ws_bytes(dtype, n), s);
+  if (rc) return rc;
+  Header* hdr_dev = static_cast<Header*>(sc.base);
+  char* p = static_cast<char*>(sc.base) + header_bytes();
+  int32_t* P0 = reinterpret_cast<int32_t*>(p);
+  int32_t* P1 = P0 + n * n;
+  char* D0 = reinterpret_cast<char*>(P1 + n * n);
+  const size_t esmax = dtype == APSP_DTYPE_I64 ? 8 : 4;
+  char* D1 = D0 + size_t(n) * n * esmax;
+  Header hdr{};
+  Timer tm(s);
+  rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
+  if (!rc) rc = read_header(hdr_dev, hdr, s);
+  if (rc) return rc;
+  const ScanResult scan = hdr.scan;
+  rc = check_scan(scan);
+  if (rc) return rc;
+  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req);
+  if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
+  int used = -1, tried = 0, iters = 0, launches = 2;
+  char* cur = D0;
+  int32_t* curP = P0;
+  for (int tier : tiers) {
+    const int store = tier_store(tier);
+    if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+    if (store == STORE_I64 && dtype != APSP_DTYPE_I64) return set_error(APSP_EINVAL, "int64 tier needs int64 input");
+    tried |= 1 << tier;
+    const size_t es = store_elem_size(store);
+    cur = D0;
+    curP = P0;
+    char* nxt = D1;
+    int32_t* nxtP = P1;
+    APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
+    rc = launch_to_store(dtype, dist, ld, n, store, cur, n, n, nullptr, n, 0, s);
+    if (!rc) rc = launch_fill_idx(curP, n, n, n, -1, s);
+    if (rc) return rc;
+    iters = 0;
+    bool overflow = false;
+    while (true) {
+      APSP_CUDA_TRY(cudaMemcpyAsync(nxt, cur, size_t(n) * n * es, cudaMemcpyDeviceToDevice, s));
+      APSP_CUDA_TRY(cudaMemcpyAsync(nxtP, curP, size_t(n) * n * 4, cudaMemcpyDeviceToDevice, s));
+      APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status.changed, 0, sizeof(int32_t), s));
+      MinplusArgs a{};
+      a.A = cur; a.lda = n; a.B = cur; a.ldb = n; a.C = nxt; a.ldc = n; a.idx = nxtP; a.ldi = n;
+      a.predB = nullptr; a.ldp = n; a.m = n; a.n = n; a.k = n; a.inner_off = 0; a.mode = IDX_VIA;
+      a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
+      a.status = &hdr_dev->status;
+      rc = launch_minplus(store, a, s);
+      if (!rc) rc = read_header(hdr_dev, hdr, s);
+      if (rc) return rc;
+      launches += 4;
+      iters++;
+      std::swap(cur, nxt);
+      std::swap(curP, nxtP);
+      overflow |= hdr.status.overflow != 0;
+      if (!hdr.status.changed) break;
+      if (iters > n + 1) return set_error(APSP_ECONVERGE, "squaring failed to converge within %lld rounds", (long long)(n + 1));
+    }
+    bool ok = false;
+    rc = certify(tier, store, cur, n, n, n, scan, hdr_dev, hdr, s, ok);
+    if (rc) return rc;
+    if (ok) {
+      used = tier;
+      break;
+    }
+  }
+  if (used < 0) {
+    if (dtype == APSP_DTYPE_I32) return set_error(APSP_ERANGE, "shortest-path cost left the representable int32 range");
+    return set_error(APSP_ERANGE, "no value tier could represent the result");
+  }
+  rc = launch_from_store(tier_store(used), cur, n, n, n, dtype, dist, ld, s);
+  if (!rc && via) rc = launch_copy_idx(curP, n, n, n, APSP_DTYPE_I32, via, ldv, s);
+  if (rc) return rc;
+  const double ms = tm.stop();
+  if (info) {
+    info->tier = used;
+    info->tiers_tried = tried;
+    info->iterations = iters;
+    info->launches = launches + 2;
+    info->max_finite = hdr.cert.max_finite;
+    info->relaxations = int64_t(iters) * n * n * n;
+    info->device_ms = ms;
+    info->flags = 0;
+  }
+  return 0;
+}
+
+// ---- public min-plus product / accumulate ----------------------------------------------------
+int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, const void* x, int64_t ldx,
+                 const void* y, int64_t ldy, void* z, int64_t ldz, int32_t* via, int64_t ldv, int64_t row_off,
+                 int64_t inner_off, int64_t col_off, int tier_req, cudaStream_t s, apsp_info* info) {
+  if (n1 < 1 || n2 < 1 || n3 < 1) return set_error(APSP_EDIMENSION, "min-plus operands must be non-empty");
+  const size_t esmax = dtype == APSP_DTYPE_I64 ? 8 : 4;
+  const size_t need = header_bytes() + (size_t(n1) * n2 + size_t(n2) * n3 + size_t(n1) * n3) * esmax + 1024;
+  Scratch sc;
+  int rc = sc.acquire(nullptr, 0, need, s);
+  if (rc) return rc;
+  Header* hdr_dev = static_cast<Header*>(sc.base);
+  char* Xs = static_cast<char*>(sc.base) + header_bytes();
+  char* Ys = Xs + size_t(n1) * n2 * esmax;
+  char* Zs = Ys + size_t(n2) * n3 * esmax;
+  Header hdr{};
+  Timer tm(s);
+  // operand ranges: the tier must hold every partial sum x + y (and z)
+  ScanResult sx{}, sy{}, sz{};
+  rc = launch_scan(dtype, x, ldx, n1, n2, 0, &hdr_dev->scan, s);
+  if (!rc) rc = read_header(hdr_dev, hdr, s);
+  if (rc) return rc;
+  sx = hdr.scan;
+  rc = launch_scan(dtype, y, ldy, n2, n3, 0, &hdr_dev->scan, s);
+  if (!rc) rc = read_header(hdr_dev, hdr, s);
+  if (rc) return rc;
+  sy = hdr.scan;
+  if (accumulate) {
+    rc = launch_scan(dtype, z, ldz, n1, n3, 0, &hdr_dev->scan, s);
+    if (!rc) rc = read_header(hdr_dev, hdr, s);
+    if (rc) return rc;
+    sz = hdr.scan;
+  }
+  if (sx.negative) return set_error(APSP_ENEGATIVE, "left operand contains a negative finite cost");
+  if (sy.negative) return set_error(APSP_ENEGATIVE, "right operand contains a negative finite cost");
+  if (sz.negative) return set_error(APSP_ENEGATIVE, "accumulator contains a negative finite cost");
+  const bool integral = dtype != APSP_DTYPE_F32 || !(sx.non_integral || sy.non_integral || sz.non_integral);
+  const int64_t sum = std::max<int64_t>(sx.max_finite + sy.max_finite, sz.max_finite);
+  int tier = tier_req;
+  if (tier < 0) {
+    if (integral && sum <= U8_INF - 1) tier = APSP_TIER_U8;
+    else if (integral && sum <= W32_INF - 1) tier = APSP_TIER_W32;
+    else if (dtype == APSP_DTYPE_F32) tier = APSP_TIER_F32;
+    else if (dtype == APSP_DTYPE_I32) tier = APSP_TIER_I32;
+    else tier = APSP_TIER_I64;
+  }
+  const int store = tier_store(tier);
+  if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  rc = launch_to_store_rect(dtype, x, ldx, n1, n2, store, Xs, n2, s);
+  if (!rc) rc = launch_to_store_rect(dtype, y, ldy, n2, n3, store, Ys, n3, s);
+  if (rc) return rc;
+  if (accumulate) {
+    rc = launch_to_store_rect(dtype, z, ldz, n1, n3, store, Zs, n3, s);
+  } else {
+    // product: C starts at Infinity, via at None (minplus.py:398-400)
+    rc = launch_to_store_rect(dtype, nullptr, 0, n1, n3, store, Zs, n3, s);
+    if (!rc && via) rc = launch_fill_idx(via, ldv, n1, n3, -1, s);
+  }
+  if (rc) return rc;
+  APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
+  MinplusArgs a{};
+  a.A = Xs; a.lda = n2; a.B = Ys; a.ldb = n3; a.C = Zs; a.ldc = n3; a.idx = via; a.ldi = ldv;
+  a.predB = nullptr; a.ldp = 0; a.m = n1; a.n = n3; a.k = n2; a.inner_off = inner_off; a.mode = IDX_VIA;
+  a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
+  a.status = &hdr_dev->status;
+  rc = launch_minplus(store, a, s);
+  if (!rc && !accumulate && via)
+    rc = launch_witness_clear(store, Xs, n2, Ys, n3, Zs, n3, via, ldv, n1, n2, n3, row_off, inner_off, col_off, s);
+  if (!rc) rc = launch_max_finite(store, Zs, n3, n1, n3, &hdr_dev->cert, s);
+  if (!rc) rc = read_header(hdr_dev, hdr, s);
+  if (rc) return rc;
+  if (tier == APSP_TIER_I64 && hdr.cert.max_finite > MAX_FINITE_COST)
+    return set_error(APSP_ERANGE, "product cost left the representable finite range");
+  rc = launch_from_store(store, Zs, n3, n1, n3, dtype, z, ldz, s);
+  if (rc) return rc;
+  const double ms = tm.stop();
+  if (info) {
+    info->tier = tier;
+    info->tiers_tried = 1 << tier;
+    info->iterations = 0;
+    info->launches = 8;
+    info->max_finite = hdr.cert.max_finite;
+    info->relaxations = n1 * n2 * n3;
+    info->device_ms = ms;
+    info->flags = 0;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ---- conversion of a rectangular operand (no padding); h == nullptr fills Infinity --------
+namespace apsp {
+template <int D> struct ApiT;
+template <> struct ApiT<APSP_DTYPE_I32> { using T = int32_t; };
+template <> struct ApiT<APSP_DTYPE_F32> { using T = float; };
+template <> struct ApiT<APSP_DTYPE_I64> { using T = int64_t; };
+
+template <int D, int S>
+__global__ void to_store_rect_kernel(const typename ApiT<D>::T* h, int64_t ldh, int64_t rows, int64_t cols,
+                                     typename StoreT<S>::T* out, int64_t ldo) {
+  using TI = typename ApiT<D>::T;
+  using T = typename StoreT<S>::T;
+  const int64_t total = rows * cols;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    T o = store_inf<S>();
+    if (h) {
+      const TI v = h[i * ldh + j];
+      bool fin;
+      if constexpr (D == APSP_DTYPE_I32) fin = v != INF32;
+      else if constexpr (D == APSP_DTYPE_I64) fin = v != INF_RAW;
+      else fin = !isinf(v);
+      if (fin) o = T(v);
+    }
+    out[i * ldo + j] = o;
+  }
+}
+
+template <int D>
+static int rect_d(const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out, int64_t ldo,
+                  cudaStream_t s) {
+  using TI = typename ApiT<D>::T;
+  int64_t g = (rows * cols + 255) / 256;
+  g = std::min<int64_t>(std::max<int64_t>(g, 1), 148 * 16);
+  const TI* hh = static_cast<const TI*>(h);
+  switch (store) {
+    case STORE_U8: to_store_rect_kernel<D, STORE_U8><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (uint8_t*)out, ldo); break;
+    case STORE_W32: to_store_rect_kernel<D, STORE_W32><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (int32_t*)out, ldo); break;
+    case STORE_I32: to_store_rect_kernel<D, STORE_I32><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (int32_t*)out, ldo); break;
+    case STORE_F32: to_store_rect_kernel<D, STORE_F32><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (float*)out, ldo); break;
+    case STORE_I64: to_store_rect_kernel<D, STORE_I64><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (int64_t*)out, ldo); break;
+    default: return set_error(APSP_EINVAL, "unknown store %d", store);
+  }
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out,
+                         int64_t ldo, cudaStream_t s) {
+  switch (in_dtype) {
+    case APSP_DTYPE_I32: return rect_d<APSP_DTYPE_I32>(h, ldh, rows, cols, store, out, ldo, s);
+    case APSP_DTYPE_F32: return rect_d<APSP_DTYPE_F32>(h, ldh, rows, cols, store, out, ldo, s);
+    case APSP_DTYPE_I64: return rect_d<APSP_DTYPE_I64>(h, ldh, rows, cols, store, out, ldo, s);
+  }
+  return set_error(APSP_EINVAL, "unknown dtype %d", in_dtype);
+}
+}  // namespace apsp
+
+// =============================================================================================
+extern "C" {
+
+const char* apsp_last_error(void) { return apsp::last_error(); }
+int apsp_abi_version(void) { return APSP_ABI_VERSION; }
+
+size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block) {
+  switch (algorithm) {
+    case APSP_ALG_FW_BLOCKED: return fw_ws_bytes(dtype, n, block > 0 ? block : DEFAULT_BLOCK);
+    case APSP_ALG_RKLEENE: return std::max(rk_ws_bytes(dtype, n, 1), rk_ws_bytes(dtype, n, 0));
+    case APSP_ALG_FW_SQUARING: return sq_ws_bytes(dtype, n);
+    case APSP_ALG_FW_CLASSIC: return 0;
+  }
+  return 0;
+}
+
+int apsp_fw_blocked(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int block, int tier,
+                    void* ws, size_t ws_bytes, void* stream, apsp_info* info) {
+  return fw_blocked_impl(dtype, n, dist, ld, pred, ldp, block, tier, ws, ws_bytes, (cudaStream_t)stream, info);
+}
+
+int apsp_fw_classic(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, void* stream,
+                    apsp_info* info) {
+  return fw_classic_impl(dtype, n, dist, ld, pred, ldp, (cudaStream_t)stream, info);
+}
+
+int apsp_rkleene(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int64_t ldi, int idx_mode,
+                 int base_threshold, int aligned, int tier, void* ws, size_t ws_bytes, void* stream, apsp_info* info) {
+  return rkleene_impl(dtype, n, dist, ld, idx, ldi, idx_mode, base_threshold, aligned, tier, ws, ws_bytes,
+                      (cudaStream_t)stream, info);
+}
+
+int apsp_fw_squaring(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, int64_t ldv, int tier, void* ws,
+                     size_t ws_bytes, void* stream, apsp_info* info) {
+  return squaring_impl(dtype, n, dist, ld, via, ldv, tier, ws, ws_bytes, (cudaStream_t)stream, info);
+}
+
+int apsp_minplus(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, const void* x, int64_t ldx,
+                 const void* y, int64_t ldy, void* z, int64_t ldz, int32_t* via, int64_t ldv, int64_t row_off,
+                 int64_t inner_off, int64_t col_off, int tier, void* stream, apsp_info* info) {
+  return minplus_impl(dtype, accumulate, n1, n2, n3, x, ldx, y, ldy, z, ldz, via, ldv, row_off, inner_off, col_off,
+                      tier, (cudaStream_t)stream, info);
+}
+
+int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* dist_out, void* idx_out, int idx_dtype,
+                    int idx_mode, int block, int base_threshold, int aligned, int tier, int device, apsp_info* info) {
+  if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
+  if (idx_dtype != APSP_DTYPE_I32 && idx_dtype != APSP_DTYPE_I64)
+    return set_error(APSP_EINVAL, "index dtype must be int32 or int64");
+  APSP_CUDA_TRY(cudaSetDevice(device));
+  cudaStream_t s;
+  APSP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
+  const size_t bytes = size_t(n) * n * es;
+  void* d = nullptr;
+  int32_t* p = nullptr;
+  void* pw = nullptr;
+  int rc = 0;
+  auto fail = [&](int code) {
+    if (d) cudaFreeAsync(d, s);
+    if (p) cudaFreeAsync(p, s);
+    if (pw) cudaFreeAsync(pw, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return code;
+  };
+  cudaError_t e = cudaMallocAsync(&d, bytes, s);
+  if (e == cudaSuccess) e = cudaMallocAsync((void**)&p, size_t(n) * n * 4, s);
+  if (e == cudaSuccess && idx_dtype == APSP_DTYPE_I64 && idx_out) e = cudaMallocAsync(&pw, size_t(n) * n * 8, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return fail(set_cuda_error(e, "host staging", __FILE__, __LINE__));
+  switch (algorithm) {
+    case APSP_ALG_FW_BLOCKED: rc = fw_blocked_impl(dtype, n, d, n, p, n, block, tier, nullptr, 0, s, info); break;
+    case APSP_ALG_FW_CLASSIC: rc = fw_classic_impl(dtype, n, d, n, p, n, s, info); break;
+    case APSP_ALG_RKLEENE:
+      rc = rkleene_impl(dtype, n, d, n, p, n, idx_mode, base_threshold, aligned, tier, nullptr, 0, s, info);
+      break;
+    case APSP_ALG_FW_SQUARING: rc = squaring_impl(dtype, n, d, n, p, n, tier, nullptr, 0, s, info); break;
+    default: rc = set_error(APSP_EINVAL, "unknown algorithm %d", algorithm);
+  }
+  if (rc) return fail(rc);
+  e = cudaMemcpyAsync(dist_out, d, bytes, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && idx_out) {
+    if (idx_dtype == APSP_DTYPE_I64) {
+      rc = launch_copy_idx(p, n, n, n, APSP_DTYPE_I64, pw, n, s);
+      if (rc) return fail(rc);
+      e = cudaMemcpyAsync(idx_out, pw, size_t(n) * n * 8, cudaMemcpyDeviceToHost, s);
+    } else {
+      e = cudaMemcpyAsync(idx_out, p, size_t(n) * n * 4, cudaMemcpyDeviceToHost, s);
+    }
+  }
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(set_cuda_error(e, "host readback", __FILE__, __LINE__));
+  return fail(0);
+}
+
+}  // extern "C"

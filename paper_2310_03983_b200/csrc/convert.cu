@@ -1,0 +1,344 @@
+// Input scan (K7), API dtype <-> store conversion with padding and pred initialisation,
+// result certificate (max finite), index copies and the minplus_product witness clear.
+// All are HBM-bound elementwise kernels: grid-stride, 16B-friendly row-major sweeps.
+#include <cstdarg>
+#include <cstdio>
+#include "launch.h"
+
+namespace apsp {
+
+// API dtypes (apsp_b200.h): 0 = int32 (INF32), 1 = fp32 (+inf), 2 = int64 (INF_RAW)
+enum ApiDtype : int { API_I32 = 0, API_F32 = 1, API_I64 = 2 };
+
+size_t store_elem_size(int store) {
+  switch (store) {
+    case STORE_U8: return 1;
+    case STORE_W32: case STORE_I32: case STORE_F32: return 4;
+    case STORE_I64: return 8;
+  }
+  return 0;
+}
+
+template <int D> struct Api;
+template <> struct Api<API_I32> { using T = int32_t; __device__ static bool fin(T v) { return v != INF32; } };
+template <> struct Api<API_F32> { using T = float;   __device__ static bool fin(T v) { return !isinf(v) || v < 0; } };
+template <> struct Api<API_I64> { using T = int64_t; __device__ static bool fin(T v) { return v != INF_RAW; } };
+
+__device__ __forceinline__ void warp_or(int32_t* dst, bool v) {
+  if (__any_sync(0xffffffffu, v) && (threadIdx.x & 31) == 0) atomicOr(dst, 1);
+}
+
+template <int D>
+__global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t rows, int64_t cols, int check_diag,
+                            ScanResult* out) {
+  using T = typename Api<D>::T;
+  bool neg = false, diag = false, nonint = false, anyfin = false, zero = false;
+  long long mx = -1;
+  float mxf = -1.f;
+  const int64_t total = rows * cols;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    const T v = h[i * ld + j];
+    if (check_diag && i == j && v != T(0)) diag = true;
+    if (!Api<D>::fin(v)) continue;
+    anyfin = true;
+    if (v == T(0) && i != j) zero = true;
+    if constexpr (D == API_F32) {
+      if (isnan(v) || v < 0.f) { neg = true; continue; }
+      if (v != floorf(v)) nonint = true;
+      mxf = fmaxf(mxf, v);
+      mx = max(mx, (long long)fminf(v, 9.0e18f));
+    } else {
+      if (v < 0) { neg = true; continue; }
+      mx = max(mx, (long long)v);
+    }
+  }
+  warp_or(&out->negative, neg);
+  warp_or(&out->diag_nonzero, diag);
+  warp_or(&out->non_integral, nonint);
+  warp_or(&out->any_finite, anyfin);
+  warp_or(&out->zero_offdiag, zero);
+  for (int o = 16; o; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mx >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&out->max_finite), (unsigned long long)mx);
+    if (mxf >= 0.f) atomicMax(reinterpret_cast<int*>(&out->max_finite_f), __float_as_int(mxf));
+  }
+}
+
+static unsigned grid_for(int64_t total) {
+  int64_t g = (total + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (g < 1) g = 1;
+  return unsigned(g);
+}
+
+int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int check_diag,
+                ScanResult* out_dev, cudaStream_t s) {
+  APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
+  // max fields start at 0 after memset; negative sentinel not needed (values are >= 0)
+  const unsigned g = grid_for(rows * cols);
+  switch (in_dtype) {
+    case API_I32: scan_kernel<API_I32><<<g, 256, 0, s>>>((const int32_t*)h, ld, rows, cols, check_diag, out_dev); break;
+    case API_F32: scan_kernel<API_F32><<<g, 256, 0, s>>>((const float*)h, ld, rows, cols, check_diag, out_dev); break;
+    case API_I64: scan_kernel<API_I64><<<g, 256, 0, s>>>((const int64_t*)h, ld, rows, cols, check_diag, out_dev); break;
+    default: return set_error(2, "unknown dtype %d", in_dtype);
+  }
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---- conversion into a padded store ------------------------------------------------
+template <int D, int S>
+__global__ void to_store_kernel(const typename Api<D>::T* h, int64_t ldh, int64_t n, typename StoreT<S>::T* out,
+                                int64_t ld, int64_t N, int32_t* P, int64_t ldp, int pred_init) {
+  using T = typename StoreT<S>::T;
+  const int64_t total = N * N;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / N, j = e - i * N;
+    T o;
+    bool fin;
+    if (i < n && j < n) {
+      const typename Api<D>::T v = h[i * ldh + j];
+      fin = Api<D>::fin(v);
+      o = fin ? T(v) : store_inf<S>();
+    } else {
+      fin = (i == j);
+      o = fin ? T(0) : store_inf<S>();
+    }
+    out[i * ld + j] = o;
+    if (P) P[i * ldp + j] = (pred_init && fin && i != j && i < n && j < n) ? int32_t(i) : -1;
+  }
+}
+
+template <int D>
+static int to_store_d(const void* h, int64_t ldh, int64_t n, int store, void* Dp, int64_t ld, int64_t N, int32_t* P,
+                      int64_t ldp, int pred_init, cudaStream_t s) {
+  using TI = typename Api<D>::T;
+  const unsigned g = grid_for(N * N);
+  const TI* hh = static_cast<const TI*>(h);
+  switch (store) {
+    case STORE_U8: to_store_kernel<D, STORE_U8><<<g, 256, 0, s>>>(hh, ldh, n, (uint8_t*)Dp, ld, N, P, ldp, pred_init); break;
+    case STORE_W32: to_store_kernel<D, STORE_W32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init); break;
+    case STORE_I32: to_store_kernel<D, STORE_I32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init); break;
+    case STORE_F32: to_store_kernel<D, STORE_F32><<<g, 256, 0, s>>>(hh, ldh, n, (float*)Dp, ld, N, P, ldp, pred_init); break;
+    case STORE_I64: to_store_kernel<D, STORE_I64><<<g, 256, 0, s>>>(hh, ldh, n, (int64_t*)Dp, ld, N, P, ldp, pred_init); break;
+    default: return set_error(2, "unknown store %d", store);
+  }
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_to_store(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D, int64_t ld, int64_t N,
+                    int32_t* P, int64_t ldp, int pred_init, cudaStream_t s) {
+  switch (in_dtype) {
+    case API_I32: return to_store_d<API_I32>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, s);
+    case API_F32: return to_store_d<API_F32>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, s);
+    case API_I64: return to_store_d<API_I64>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, s);
+  }
+  return set_error(2, "unknown dtype %d", in_dtype);
+}
+
+// ---- conversion back -----------------------------------------------------------------
+template <int S, int D>
+__global__ void from_store_kernel(const typename StoreT<S>::T* in, int64_t ld, int64_t rows, int64_t cols,
+                                  typename Api<D>::T* out, int64_t ldo) {
+  using TO = typename Api<D>::T;
+  const int64_t total = rows * cols;
+  const typename StoreT<S>::T inf = store_inf<S>();
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    const auto v = in[i * ld + j];
+    TO o;
+    if constexpr (S == STORE_F32) {
+      o = TO(v);   // +inf maps to +inf (fp32 out) -- int outs never come from an fp32 store
+    } else {
+      if (v == inf) {
+        if constexpr (D == API_I32) o = INF32;
+        else if constexpr (D == API_I64) o = INF_RAW;
+        else o = __int_as_float(0x7f800000);
+      } else {
+        o = TO(v);
+      }
+    }
+    out[i * ldo + j] = o;
+  }
+}
+
+template <int S>
+static int from_store_s(const void* in, int64_t ld, int64_t rows, int64_t cols, int out_dtype, void* out, int64_t ldo,
+                        cudaStream_t s) {
+  using TI = typename StoreT<S>::T;
+  const unsigned g = grid_for(rows * cols);
+  const TI* ii = static_cast<const TI*>(in);
+  switch (out_dtype) {
+    case API_I32: from_store_kernel<S, API_I32><<<g, 256, 0, s>>>(ii, ld, rows, cols, (int32_t*)out, ldo); break;
+    case API_F32: from_store_kernel<S, API_F32><<<g, 256, 0, s>>>(ii, ld, rows, cols, (float*)out, ldo); break;
+    case API_I64: from_store_kernel<S, API_I64><<<g, 256, 0, s>>>(ii, ld, rows, cols, (int64_t*)out, ldo); break;
+    default: return set_error(2, "unknown dtype %d", out_dtype);
+  }
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_from_store(int store, const void* D, int64_t ld, int64_t rows, int64_t cols, int out_dtype, void* out,
+                      int64_t ldo, cudaStream_t s) {
+  switch (store) {
+    case STORE_U8: return from_store_s<STORE_U8>(D, ld, rows, cols, out_dtype, out, ldo, s);
+    case STORE_W32: return from_store_s<STORE_W32>(D, ld, rows, cols, out_dtype, out, ldo, s);
+    case STORE_I32: return from_store_s<STORE_I32>(D, ld, rows, cols, out_dtype, out, ldo, s);
+    case STORE_F32: return from_store_s<STORE_F32>(D, ld, rows, cols, out_dtype, out, ldo, s);
+    case STORE_I64: return from_store_s<STORE_I64>(D, ld, rows, cols, out_dtype, out, ldo, s);
+  }
+  return set_error(2, "unknown store %d", store);
+}
+
+// ---- index copies ----------------------------------------------------------------------
+template <typename TO>
+__global__ void copy_idx_kernel(const int32_t* P, int64_t ldp, int64_t rows, int64_t cols, TO* out, int64_t ldo) {
+  const int64_t total = rows * cols;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    out[i * ldo + j] = TO(P[i * ldp + j]);
+  }
+}
+
+int launch_copy_idx(const int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int out_dtype, void* out, int64_t ldo,
+                    cudaStream_t s) {
+  const unsigned g = grid_for(rows * cols);
+  if (out_dtype == API_I64) copy_idx_kernel<int64_t><<<g, 256, 0, s>>>(P, ldp, rows, cols, (int64_t*)out, ldo);
+  else copy_idx_kernel<int32_t><<<g, 256, 0, s>>>(P, ldp, rows, cols, (int32_t*)out, ldo);
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+__global__ void fill_idx_kernel(int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int32_t v) {
+  const int64_t total = rows * cols;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    P[i * ldp + j] = v;
+  }
+}
+
+int launch_fill_idx(int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int32_t v, cudaStream_t s) {
+  fill_idx_kernel<<<grid_for(rows * cols), 256, 0, s>>>(P, ldp, rows, cols, v);
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int launch_copy_block(int store, const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
+                      cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return 0;
+  const size_t es = store_elem_size(store);
+  APSP_CUDA_TRY(cudaMemcpy2DAsync(dst, size_t(ldd) * es, src, size_t(lds) * es, size_t(cols) * es, size_t(rows),
+                                  cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
+// ---- certificate: max finite value of a store ------------------------------------------
+template <int S>
+__global__ void max_finite_kernel(const typename StoreT<S>::T* D, int64_t ld, int64_t rows, int64_t cols,
+                                  ScanResult* out) {
+  const int64_t total = rows * cols;
+  const auto inf = store_inf<S>();
+  long long mx = -1;
+  float mxf = -1.f;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e - i * cols;
+    const auto v = D[i * ld + j];
+    if (v == inf) continue;
+    if constexpr (S == STORE_F32) mxf = fmaxf(mxf, v);
+    else mx = max(mx, (long long)v);
+  }
+  for (int o = 16; o; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (mx >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&out->max_finite), (unsigned long long)mx);
+    if (mxf >= 0.f) atomicMax(reinterpret_cast<int*>(&out->max_finite_f), __float_as_int(mxf));
+  }
+}
+
+int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_t cols, ScanResult* out_dev,
+                      cudaStream_t s) {
+  APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
+  const unsigned g = grid_for(rows * cols);
+  switch (store) {
+    case STORE_U8: max_finite_kernel<STORE_U8><<<g, 256, 0, s>>>((const uint8_t*)D, ld, rows, cols, out_dev); break;
+    case STORE_W32: max_finite_kernel<STORE_W32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev); break;
+    case STORE_I32: max_finite_kernel<STORE_I32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev); break;
+    case STORE_F32: max_finite_kernel<STORE_F32><<<g, 256, 0, s>>>((const float*)D, ld, rows, cols, out_dev); break;
+    case STORE_I64: max_finite_kernel<STORE_I64><<<g, 256, 0, s>>>((const int64_t*)D, ld, rows, cols, out_dev); break;
+    default: return set_error(2, "unknown store %d", store);
+  }
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---- minplus_product self-witness via clear (minplus.py:411-423) -----------------------
+template <int S>
+__global__ void witness_clear_kernel(const typename StoreT<S>::T* X, int64_t ldx, const typename StoreT<S>::T* Y,
+                                     int64_t ldy, const typename StoreT<S>::T* Dp, int64_t ldd, int32_t* via,
+                                     int64_t ldv, int64_t n1, int64_t n2, int64_t n3, int64_t row_off,
+                                     int64_t inner_off, int64_t col_off) {
+  using A = typename StoreT<S>::A;
+  const auto inf = store_inf<S>();
+  const int64_t total = n1 * n3;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / n3, j = e - i * n3;
+    const auto best = Dp[i * ldd + j];
+    if (best == inf) continue;
+    const int64_t ti = i + row_off - inner_off;
+    if (ti >= 0 && ti < n2 && X[i * ldx + ti] != inf && Y[ti * ldy + j] != inf &&
+        A(X[i * ldx + ti]) + A(Y[ti * ldy + j]) == A(best)) {
+      via[i * ldv + j] = -1;
+      continue;
+    }
+    const int64_t tj = j + col_off - inner_off;
+    if (tj >= 0 && tj < n2 && X[i * ldx + tj] != inf && Y[tj * ldy + j] != inf &&
+        A(X[i * ldx + tj]) + A(Y[tj * ldy + j]) == A(best))
+      via[i * ldv + j] = -1;
+  }
+}
+
+int launch_witness_clear(int store, const void* X, int64_t ldx, const void* Y, int64_t ldy, const void* Dp,
+                         int64_t ldd, int32_t* via, int64_t ldv, int64_t n1, int64_t n2, int64_t n3, int64_t row_off,
+                         int64_t inner_off, int64_t col_off, cudaStream_t s) {
+  const unsigned g = grid_for(n1 * n3);
+#define WC(S, T)                                                                                              \
+  witness_clear_kernel<S><<<g, 256, 0, s>>>((const T*)X, ldx, (const T*)Y, ldy, (const T*)Dp, ldd, via, ldv, n1, \
+                                            n2, n3, row_off, inner_off, col_off)
+  switch (store) {
+    case STORE_U8: WC(STORE_U8, uint8_t); break;
+    case STORE_W32: WC(STORE_W32, int32_t); break;
+    case STORE_I32: WC(STORE_I32, int32_t); break;
+    case STORE_F32: WC(STORE_F32, float); break;
+    case STORE_I64: WC(STORE_I64, int64_t); break;
+    default: return set_error(2, "unknown store %d", store);
+  }
+#undef WC
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ---- error state -------------------------------------------------------------------------
+static thread_local char g_err[512] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int set_cuda_error(cudaError_t e, const char* what, const char* file, int line) {
+  return set_error(3, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e), file, line, what);
+}
+
+const char* last_error() { return g_err; }
+
+}  // namespace apsp

@@ -1,0 +1,91 @@
+// Host-side launchers for the sm_100a kernels (one translation unit per kernel family).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "common.cuh"
+
+namespace apsp {
+
+// One min-plus tile update  C <- min(C, A (x) B)  with strict-improvement lexicographic
+// (value, smallest k) argmin, written to idx on improvement only.  Covers FW phase 3
+// (skip_row/col_tile = the pivot block) and every R-Kleene block product
+// (solvers.py:250-286; minplus.py:114-133).
+struct MinplusArgs {
+  const void* A; int64_t lda;     // m x k
+  const void* B; int64_t ldb;     // k x n
+  void* C; int64_t ldc;           // m x n, in/out
+  int32_t* idx; int64_t ldi;      // m x n, written where C strictly improves (may be null)
+  const int32_t* predB; int64_t ldp;  // k x n, IDX_PRED source rows (pred of B's rows)
+  int64_t m, n, k;
+  int64_t inner_off;              // IDX_VIA: global vertex of k = 0
+  int mode;                       // IdxMode
+  int64_t skip_row_lo, skip_row_hi;  // rows [lo,hi) and cols [lo,hi) form the FW pivot cross;
+  int64_t skip_col_lo, skip_col_hi;  // tiles entirely inside either band are skipped
+  Status* status;                 // optional: changed / overflow flags
+};
+
+int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s);
+
+// Closure of the diagonal block [lo, lo+m) (m <= 128) in classic k order, one CTA:
+// FW phase 1 and the R-Kleene leaf (_fw_via_block, solvers.py:98-115).
+int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m,
+                       int32_t* idx, int64_t ldi, int mode, int64_t via_off, Status* st,
+                       cudaStream_t s);
+
+// FW phase 2 for pivot block [k0, k0+b) of the N x N view D: row panel (rows of the pivot
+// block, all columns outside it) and column panel (all rows outside it, pivot columns),
+// each in classic k order against the closed diagonal block.
+// via_off = global vertex of row/column 0 of the view (pivot k gets via_off + k0 + k).
+int launch_fw_panels(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N,
+                     int64_t k0, int b, int mode, int64_t via_off, Status* st, cudaStream_t s);
+
+// Generalised panel update used by the sharded path: rows [r0,r1) x cols [c0,c1) of a
+// panel updated against the diagonal block (either its rows = pivot rows, or its cols).
+int launch_panel_rows(int store, const void* Dg, int64_t ldg, void* T, int64_t ldt, int32_t* PT,
+                      int64_t ldpt, int64_t b, int64_t ncols, int mode, int64_t via_off,
+                      Status* st, cudaStream_t s);
+int launch_panel_cols(int store, const void* Dg, int64_t ldg, const int32_t* PDg, int64_t ldpg,
+                      void* T, int64_t ldt, int32_t* PT, int64_t ldpt, int64_t b, int64_t nrows,
+                      int mode, int64_t via_off, Status* st, cudaStream_t s);
+
+// Classic per-k Floyd-Warshall step (K1): bit-exact pred/via parity with fw_classic
+// (solvers.py:77-95).  One launch per k; row k / column k are invariant in step k.
+int launch_fw_step(int store, void* D, int64_t ld, int64_t n, int64_t k, int32_t* idx,
+                   int64_t ldi, int mode, int64_t via_off, Status* st, cudaStream_t s);
+
+// Input scan (K7): negatives, nonzero diagonal, max finite, non-integral fp32.
+struct ScanResult {
+  int32_t negative;
+  int32_t diag_nonzero;
+  int32_t non_integral;
+  int32_t any_finite;
+  int64_t max_finite;      // integer domains (fp32: floor of max)
+  float max_finite_f;      // fp32 domain
+  int32_t zero_offdiag;    // a finite zero cost off the diagonal (zero-weight edge)
+};
+int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t cols,
+                int check_diag, ScanResult* out_dev, cudaStream_t s);
+
+// API dtype <-> store conversion, with padding to N (pad vertices are isolated) and the
+// FW pred initialisation pred[i][j] = i where h[i][j] finite and i != j (solvers.py:135-137).
+int launch_to_store(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D,
+                    int64_t ld, int64_t N, int32_t* P, int64_t ldp, int pred_init, cudaStream_t s);
+int launch_from_store(int store, const void* D, int64_t ld, int64_t rows, int64_t cols,
+                      int out_dtype, void* out, int64_t ldo, cudaStream_t s);
+int launch_copy_idx(const int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int out_dtype,
+                    void* out, int64_t ldo, cudaStream_t s);
+int launch_fill_idx(int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int32_t v, cudaStream_t s);
+int launch_copy_block(int store, const void* src, int64_t lds, void* dst, int64_t ldd,
+                      int64_t rows, int64_t cols, cudaStream_t s);
+int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_t cols,
+                      ScanResult* out_dev, cudaStream_t s);
+// Self-witness via clear of minplus_product (minplus.py:411-423).
+int launch_witness_clear(int store, const void* X, int64_t ldx, const void* Y, int64_t ldy,
+                         const void* Dp, int64_t ldd, int32_t* via, int64_t ldv, int64_t n1,
+                         int64_t n2, int64_t n3, int64_t row_off, int64_t inner_off,
+                         int64_t col_off, cudaStream_t s);
+
+size_t store_elem_size(int store);
+
+}  // namespace apsp

@@ -1,0 +1,299 @@
+"""GPU parity of the solvers against the reference (golden fixtures) and the CPU oracle.
+
+Parity bar:
+* distances: bit-exact for integer inputs;
+* fw_classic(method="classic") pred and rkleene(split="floor") via: bit-exact;
+* blocked-FW pred and R-Kleene pred: validated by the whole-matrix reconstruction
+  certificate (paths.check_pred_tree);
+* continuous fp32: within 1e-5 relative of a float64 Floyd-Warshall.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import INF_RAW, golden, random_graph_raw
+from oracle import oracle as orc
+
+import paper_2310_03983_b200 as ap
+from paper_2310_03983_b200.core import INF32
+
+pytestmark = pytest.mark.gpu
+
+
+def pred_ok(h, dist, pred, inf=INF_RAW):
+    ok, why = ap.check_pred_tree(h, dist, pred, inf)
+    assert ok, why
+
+
+# ---- Floyd-Warshall ------------------------------------------------------------------------
+
+def test_c1_blocked_and_classic(cuda):
+    g = golden("c1_fw.npz")
+    h = ap.CostMatrix(g["h"])
+    s = ap.fw_classic(h)                        # blocked (default)
+    assert np.array_equal(s.distances.raw, g["dist"])
+    pred_ok(g["h"], s.distances.raw, s.pred.raw)
+    assert s.info["tier"] == "u8"
+    c = ap.fw_classic(h, method="classic")      # classic order: pred bit-exact
+    assert np.array_equal(c.distances.raw, g["dist"])
+    assert np.array_equal(c.pred.raw, g["pred"])
+
+
+@pytest.mark.parametrize("tier", ["u8", "w32", "i64"])
+def test_c1_every_tier(cuda, tier):
+    g = golden("c1_fw.npz")
+    s = ap.fw_classic(ap.CostMatrix(g["h"]), tier=tier)
+    assert s.info["tier"] == tier
+    assert np.array_equal(s.distances.raw, g["dist"])
+    pred_ok(g["h"], s.distances.raw, s.pred.raw)
+
+
+def test_suite_graphs(cuda):
+    g = golden("suite.npz")
+    for i in range(int(g["count"])):
+        h = ap.CostMatrix(g[f"h{i}"])
+        s = ap.fw_classic(h)
+        assert np.array_equal(s.distances.raw, g[f"dist{i}"]), i
+        pred_ok(g[f"h{i}"], s.distances.raw, s.pred.raw)
+        c = ap.fw_classic(h, method="classic")
+        assert np.array_equal(c.pred.raw, g[f"pred{i}"]), i
+        r = ap.rkleene(h, base_threshold=16)
+        assert np.array_equal(r.distances.raw, g[f"dist{i}"]), i
+        assert np.array_equal(r.via.raw, g[f"rkvia{i}"]), i
+        q = ap.fw_squaring(h)
+        assert np.array_equal(q.distances.raw, g[f"dist{i}"]), i
+        assert np.array_equal(q.via.raw, g[f"sqvia{i}"]), i
+        assert q.iterations == int(g[f"sqit{i}"]), i
+
+
+def test_known_answers(cuda):
+    three = ap.cost_matrix_from_graph(ap.Graph(3, [(0, 1, 1), (1, 2, 2), (2, 0, 4)]))
+    for solver in ap.SOLVERS.values():
+        assert solver(three).distances.raw.tolist() == [[0, 1, 3], [6, 0, 2], [4, 5, 0]]
+    chain = ap.cost_matrix_from_graph(ap.Graph(3, [(0, 1, 3), (1, 2, 4), (0, 2, 10)]))
+    s = ap.fw_classic(chain)
+    assert s.distances[0, 2].value == 7 and s.pred[0, 2] == 1
+    one = ap.cost_matrix_from_graph(ap.Graph(3, [(0, 1, 3)]))
+    s = ap.fw_classic(one)
+    assert s.pred[0, 1] == 0 and s.pred[0, 2] is None and s.pred[0, 0] is None
+    edgeless = ap.cost_matrix_from_graph(ap.Graph(3, []))
+    s = ap.fw_classic(edgeless)
+    assert ap.matrices_equal(s.distances, ap.minplus_identity(3)) and (s.pred.raw == -1).all()
+    for n in (1, 2, 7, 33):
+        assert ap.fw_classic(ap.minplus_identity(n)).relaxation_count == n ** 3
+    path5 = ap.cost_matrix_from_graph(ap.Graph(5, [(i, i + 1, 1) for i in range(4)]))
+    assert ap.fw_squaring(path5).iterations == 3
+
+
+@pytest.mark.parametrize("n,density,wmax,seed", [(1, 1.0, 5, 1), (2, 1.0, 5, 2), (127, 0.1, 100, 3),
+                                                  (129, 0.05, 100, 4), (300, 0.02, 100, 5), (385, 1.0, 9, 6),
+                                                  (640, 0.01, 200, 7)])
+def test_fw_ragged_sizes_vs_oracle(cuda, n, density, wmax, seed):
+    raw = random_graph_raw(n, density, wmax, seed)
+    want_d, want_p = orc.fw_classic(raw)
+    s = ap.fw_classic(ap.CostMatrix(raw))
+    assert np.array_equal(s.distances.raw, want_d)
+    pred_ok(raw, s.distances.raw, s.pred.raw)
+    c = ap.fw_classic(ap.CostMatrix(raw), method="classic")
+    assert np.array_equal(c.distances.raw, want_d) and np.array_equal(c.pred.raw, want_p)
+
+
+def test_zero_weight_edges(cuda):
+    raw = random_graph_raw(257, 0.05, 20, 9, zero_frac=0.3)
+    want_d, _ = orc.fw_classic(raw)
+    s = ap.fw_classic(ap.CostMatrix(raw))
+    assert np.array_equal(s.distances.raw, want_d)
+    pred_ok(raw, s.distances.raw, s.pred.raw)
+    # zero-cost edges: predecessors come from the classic k order (a tree by construction)
+    assert s.info["classic_for_zero_edges"]
+    r = ap.rkleene(ap.CostMatrix(raw), track="pred", split="aligned", base_threshold=128)
+    assert np.array_equal(r.distances.raw, want_d)
+    pred_ok(raw, r.distances.raw, r.pred.raw)
+    v = ap.rkleene(ap.CostMatrix(raw))
+    assert np.array_equal(v.distances.raw, want_d)
+
+
+def test_tier_fallback_and_wide_costs(cuda):
+    # long paths: u8 certificate must fail and fall back to w32, results exact
+    n = 300
+    raw = np.full((n, n), INF_RAW, np.int64)
+    np.fill_diagonal(raw, 0)
+    for i in range(n - 1):
+        raw[i, i + 1] = 3
+    s = ap.fw_classic(ap.CostMatrix(raw))
+    assert s.info["tier"] == "w32" and "u8" in s.info["tiers_tried"]
+    want_d, _ = orc.fw_classic(raw)
+    assert np.array_equal(s.distances.raw, want_d)
+    pred_ok(raw, s.distances.raw, s.pred.raw)
+    # costs beyond 2^24: straight to the exact int64 tier
+    big = random_graph_raw(200, 0.1, 1 << 40, 11)
+    s = ap.fw_classic(ap.CostMatrix(big))
+    assert s.info["tier"] == "i64"
+    want_d, _ = orc.fw_classic(big)
+    assert np.array_equal(s.distances.raw, want_d)
+    pred_ok(big, s.distances.raw, s.pred.raw)
+
+
+def test_errors(cuda):
+    for solver in ap.SOLVERS.values():
+        with pytest.raises(ap.NegativeWeightError):
+            solver(ap.CostMatrix.from_rows([[0, -2], [1, 0]]))
+        with pytest.raises(ap.MalformedGraphError):
+            solver(ap.CostMatrix.from_rows([[0, 1], [1, 3]]))
+        with pytest.raises(ap.ParameterError):
+            solver(ap.minplus_identity(2), tile_size=0)
+        h = ap.cost_matrix_from_graph(ap.Graph(3, [(0, 1, 1), (1, 2, 2), (2, 0, 4)]))
+        before = h.raw.copy()
+        solver(h)
+        assert np.array_equal(h.raw, before)
+    with pytest.raises(ap.ParameterError):
+        ap.rkleene(ap.minplus_identity(2), base_threshold=0)
+    big = (1 << 60) - 2
+    m = ap.CostMatrix.from_rows([[0, big, ap.INF], [ap.INF, 0, big], [ap.INF, ap.INF, 0]])
+    with pytest.raises(ap.CostRangeError):
+        ap.fw_classic(m)
+    with pytest.raises(ap.CostRangeError):
+        ap.fw_classic(m, method="classic")
+
+
+def test_int32_and_fp32_dense_entry(cuda):
+    import torch
+
+    p = ap.GenParams(700, 0.1, 100, 707)
+    h64 = ap.dense_costs(p, np.int64)
+    want_d, _ = orc.fw_classic(h64)
+    h32 = ap.dense_costs(p, np.int32)
+    r = ap.solve(h32)
+    assert r.distances.dtype == np.int32
+    fin = want_d != INF_RAW
+    assert np.array_equal(r.distances[fin], want_d[fin]) and (r.distances[~fin] == INF32).all()
+    pred_ok(h32, r.distances, r.index, INF32)
+    hf = ap.dense_costs(p, np.float32)
+    rt = ap.solve(torch.from_numpy(hf).cuda())
+    df = rt.distances.cpu().numpy()
+    assert np.array_equal(df[fin], want_d[fin].astype(np.float32)) and np.isinf(df[~fin]).all()
+    assert rt.info["tier"] == "u8"
+
+
+def test_fp32_continuous_tolerance(cuda):
+    import torch
+
+    rng = np.random.default_rng(3)
+    n = 400
+    w = rng.uniform(1.0, 100.0, size=(n, n)).astype(np.float32)
+    w[rng.random((n, n)) > 0.05] = np.inf
+    np.fill_diagonal(w, 0.0)
+    ref = w.astype(np.float64)
+    for k in range(n):
+        np.minimum(ref, ref[:, k:k + 1] + ref[k:k + 1, :], out=ref)
+    for alg in ("fw_blocked", "fw_classic", "rkleene"):
+        r = ap.solve(torch.from_numpy(w).cuda(), alg)
+        assert r.info["tier"] == "f32"
+        d = r.distances.cpu().numpy().astype(np.float64)
+        fin = np.isfinite(ref)
+        assert (np.isfinite(d) == fin).all()
+        assert np.allclose(d[fin], ref[fin], rtol=1e-5, atol=0), alg
+
+
+# ---- R-Kleene -------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["rk_n300_t64.npz", "rk_n200_t16.npz", "rk_n130_t8.npz", "rk_n150_t1.npz"])
+def test_rkleene_via_bitwise(cuda, name):
+    g = golden(name)
+    r = ap.rkleene(ap.CostMatrix(g["h"]), base_threshold=int(g["thr"]))
+    assert np.array_equal(r.distances.raw, g["dist"])
+    assert np.array_equal(r.via.raw, g["via"])
+
+
+@pytest.mark.parametrize("split", ["floor", "aligned"])
+def test_rkleene_pred_and_aligned(cuda, split):
+    raw = random_graph_raw(777, 0.03, 100, 21)
+    want_d, _ = orc.fw_classic(raw)
+    r = ap.rkleene(ap.CostMatrix(raw), base_threshold=256, track="pred", split=split)
+    assert np.array_equal(r.distances.raw, want_d)
+    pred_ok(raw, r.distances.raw, r.pred.raw)
+    v = ap.rkleene(ap.CostMatrix(raw), base_threshold=256, split=split)
+    assert np.array_equal(v.distances.raw, want_d)
+    d, via = want_d, v.via.raw
+    rows, cols = np.nonzero(via >= 0)
+    mids = via[rows, cols]
+    assert (d[rows, mids] + d[mids, cols] == d[rows, cols]).all()
+    assert (mids != rows).all() and (mids != cols).all()
+
+
+# ---- min-plus products ----------------------------------------------------------------------
+
+def test_minplus_golden(cuda):
+    g = golden("minplus.npz")
+    for k in range(int(g["count"])):
+        x, y = ap.CostMatrix(g[f"p{k}_x"]), ap.CostMatrix(g[f"p{k}_y"])
+        r = ap.minplus_product(x, y, offsets=tuple(int(o) for o in g[f"p{k}_off"]))
+        assert np.array_equal(r.distances.raw, g[f"p{k}_dist"]), k
+        assert np.array_equal(r.via.raw, g[f"p{k}_via"]), k
+        a = ap.minplus_accumulate(ap.CostMatrix(g[f"a{k}_z"]), x, y, ap.ViaMatrix(g[f"a{k}_vin"]),
+                                  inner_offset=int(g[f"p{k}_off"][1]))
+        assert np.array_equal(a.distances.raw, g[f"a{k}_dist"]), k
+        assert np.array_equal(a.via.raw, g[f"a{k}_via"]), k
+
+
+def test_minplus_tiers_and_errors(cuda):
+    rng = np.random.default_rng(5)
+    x = rng.integers(0, 1 << 33, size=(70, 90)).astype(np.int64)
+    y = rng.integers(0, 1 << 33, size=(90, 50)).astype(np.int64)
+    x[rng.random(x.shape) < 0.2] = INF_RAW
+    want = orc.product(x, y)
+    r = ap.minplus_product(ap.CostMatrix(x), ap.CostMatrix(y))
+    assert np.array_equal(r.distances.raw, want[0]) and np.array_equal(r.via.raw, want[1])
+    with pytest.raises(ap.DimensionError):
+        ap.minplus_product(ap.CostMatrix(np.zeros((2, 3), np.int64)), ap.CostMatrix(np.zeros((2, 3), np.int64)))
+    big = (1 << 60) - 2
+    m = ap.CostMatrix.from_rows([[0, big, ap.INF], [ap.INF, 0, big], [ap.INF, ap.INF, 0]])
+    with pytest.raises(ap.CostRangeError):
+        ap.minplus_product(m, m)
+    with pytest.raises(ap.NegativeWeightError):
+        ap.minplus_product(ap.CostMatrix.from_rows([[0, -1], [1, 0]]), ap.minplus_identity(2))
+
+
+# ---- larger sizes: size-independent properties ---------------------------------------------
+
+def test_c2_shape_fw_equals_rkleene_and_oracle(cuda):
+    p = ap.GenParams(2048, 1.0, 100, 7 + 2048)
+    raw = ap.dense_costs(p, np.int64)
+    want_d, _ = orc.rkleene(raw, 64)
+    s = ap.fw_classic(ap.CostMatrix(raw))
+    assert np.array_equal(s.distances.raw, want_d)
+    pred_ok(raw, s.distances.raw, s.pred.raw)
+    r = ap.rkleene(ap.CostMatrix(raw), base_threshold=512, split="aligned", track="pred")
+    assert np.array_equal(r.distances.raw, want_d)
+    pred_ok(raw, r.distances.raw, r.pred.raw)
+
+
+def test_large_fw_device_properties(cuda):
+    import torch
+
+    p = ap.GenParams(8192, 0.1, 100, 7 + 8192)
+    h = torch.from_numpy(ap.dense_costs(p, np.int32)).cuda()
+    a = ap.solve(h, "fw_blocked")
+    b = ap.solve(h, "rkleene", track="pred", base_threshold=1024)
+    assert torch.equal(a.distances, b.distances)
+    w = ap.solve(h, "fw_blocked", tier="w32")
+    assert torch.equal(a.distances, w.distances)
+    ok, why = ap.check_pred_tree(h, a.distances, a.index, INF32)
+    assert ok, why
+    ok, why = ap.check_pred_tree(h, b.distances, b.index, INF32)
+    assert ok, why
+    # Bellman fixpoint on a row sample: with the pred certificate above (every distance is the
+    # length of a real path) this proves the sampled rows exact, independent of any CPU run.
+    H = h.to(torch.int64)
+    H = torch.where(h == INF32, torch.tensor(INF_RAW, device=h.device), H)
+    D = a.distances.to(torch.int64)
+    D = torch.where(a.distances == INF32, torch.tensor(INF_RAW, device=h.device), D)
+    for r in range(0, 8192, 1021):
+        best = H[r].clone()
+        for k0 in range(0, 8192, 1024):
+            cand = (D[r, k0:k0 + 1024, None] + H[k0:k0 + 1024, :]).amin(dim=0)
+            best = torch.minimum(best, cand)
+        best = torch.where(best >= INF_RAW, torch.tensor(INF_RAW, device=h.device), best)
+        assert torch.equal(best, D[r]), r
