@@ -1,0 +1,324 @@
+#!/usr/bin/env python3
+"""Benchmark of the APSP hot path (BASELINE.json metric) -- one JSON line on stdout.
+
+Workload (N=1): blocked Floyd-Warshall, distances + predecessors, on the reference
+generator graph GenParams(n=16384, rho=0.1, alpha=100, seed=7+n) as int32 -- the metric's
+size ("APSP time and min-plus updates/sec (n^3/s) at n=16384").  A step is one complete
+APSP solve of that matrix (input scan, tier conversion, all n/128 pivot rounds, certificate,
+conversion back) with the input already resident in HBM.  N>1 (torchrun): each rank owns a
+row band of a weak-scaled problem n(N) = 16384 * N^(1/3) (n^3 per GPU fixed) and the pivot
+row panel is broadcast over NCCL each round (paper_2310_03983_b200.distributed).
+
+value        = n^3 * steps / max-over-ranks device time                 [updates/s]
+e2e          = same metric through the C-ABI host-buffer call apsp_solve_host (pinned
+               host input -> device -> host dist + pred), copies inside the timed region
+roofline     = the dominant kernel (min-plus tile kernel, FW phase 3): algorithmic updates
+               per launch / its CUDA-event launch time, against the measured issue ceiling
+               of its inner-loop instruction (profiles/r01_microbench_ops.txt)
+cpu_baseline = the oracle port of reference fw_classic (C/OpenMP, int64, all host threads)
+               on a bounded sample of k-steps of the same matrix
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "APSP time and min-plus updates/sec (n^3/s) at n=16384; % of FP32 CUDA-core peak"
+UNIT = "updates/s"
+FP32_CORE_PEAK = 148 * 128 * 1965e6 / 2          # 18.6 T upd/s at max clock
+# Measured issue ceilings of the inner-loop instruction of each tier (profiles/r01_microbench_ops.txt)
+TIER_PEAK = {"u8": 37.07e12, "w32": 24.91e12, "i32": 17.98e12, "f32": 6.05e12, "i64": 6.05e12}
+TIER_OP = {"u8": "VIADDMNMX.S16x2 (2 upd/instr)", "w32": "VIADD+VIMNMX3", "i32": "compare-select",
+           "f32": "FADD/FSETP/FSEL/SEL", "i64": "compare-select int64"}
+BLOCK = 128
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_input(n: int, rho: float, seed: int):
+    from paper_2310_03983_b200 import GenParams, dense_costs
+
+    t = time.perf_counter()
+    h = dense_costs(GenParams(n, rho, 100, seed), np.int32)
+    log(f"[bench] generated n={n} rho={rho} seed={seed} in {time.perf_counter() - t:.1f}s "
+        f"(density {(h != 0x3FFFFFFF).sum() / (n * n):.4f})")
+    return h
+
+
+def cpu_baseline(h32: np.ndarray, budget_s: float = 12.0) -> dict:
+    """Oracle port of reference fw_classic on a bounded prefix of k-steps of the same matrix."""
+    from oracle import oracle as orc
+
+    n = h32.shape[0]
+    h64 = h32.astype(np.int64)
+    h64[h32 == 0x3FFFFFFF] = orc.INF_RAW
+    threads = orc.threads()
+    t = time.perf_counter()
+    orc.fw_classic(h64, k_end=2, nthreads=threads)
+    one = (time.perf_counter() - t) / 2
+    k_end = int(max(2, min(n, budget_s / max(one, 1e-6))))
+    t = time.perf_counter()
+    orc.fw_classic(h64, k_end=k_end, nthreads=threads)
+    dt = time.perf_counter() - t
+    rate = k_end * n * n / dt
+    return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"oracle fw_classic (C/OpenMP int64, solvers.py:118-155) k-steps 0..{k_end} of n={n} "
+                      f"({k_end}*n^2 updates, {dt:.1f}s); full solve extrapolates to {n ** 3 / rate:.0f}s"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    n = args.n or weak_n(ws)
+    h = make_input(n, args.rho, 7 + n)
+    from oracle import oracle as orc
+
+    h64 = h.astype(np.int64)
+    h64[h == 0x3FFFFFFF] = orc.INF_RAW
+    threads = orc.threads()
+    t = time.perf_counter()
+    orc.fw_classic(h64, k_end=2, nthreads=threads)
+    one = (time.perf_counter() - t) / 2
+    k_end = int(max(2, min(n, args.ref_step_s / max(one, 1e-6))))
+    for _ in range(args.warmup):
+        orc.fw_classic(h64, k_end=k_end, nthreads=threads)
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        orc.fw_classic(h64, k_end=k_end, nthreads=threads)
+    dt = time.perf_counter() - t
+    rate = args.steps * k_end * n * n / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generator)",
+        "config": config(n, args.rho, ws),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"each step = oracle fw_classic k-steps 0..{k_end} of n={n} ({k_end}*n^2 updates)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def weak_n(ws: int) -> int:
+    n = 16384 * ws ** (1.0 / 3.0)
+    return int(round(n / (BLOCK * ws)) * BLOCK * ws) if ws > 1 else 16384
+
+
+def config(n, rho, ws):
+    return {"workload": f"blocked Floyd-Warshall APSP, distances+predecessors, n={n}, generator graph "
+                        f"GenParams(n, rho={rho}, alpha=100, seed=7+n), int32 in/out",
+            "n": n, "rho": rho, "block": BLOCK, "layout": "1D row bands" if ws > 1 else "single GPU",
+            "parallelism": f"rowband{ws}" if ws > 1 else "1gpu",
+            "l2": "inputs larger than L2 (1 GiB int32 dist + 1 GiB pred + 256 MiB u8 store per GPU)"}
+
+
+def main():
+    ap_ = argparse.ArgumentParser()
+    ap_.add_argument("--gpus", type=int, default=1)
+    ap_.add_argument("--steps", type=int, default=5)
+    ap_.add_argument("--warmup", type=int, default=3)
+    ap_.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap_.add_argument("--n", type=int, default=0)
+    ap_.add_argument("--rho", type=float, default=0.1)
+    ap_.add_argument("--no-cpu", action="store_true")
+    ap_.add_argument("--no-e2e", action="store_true")
+    ap_.add_argument("--ref-step-s", type=float, default=8.0)
+    args = ap_.parse_args()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)
+    if ws > 1:
+        from paper_2310_03983_b200 import distributed
+
+        return distributed.bench_main(args, METRIC, UNIT, config, make_input, weak_n, ClockSampler)
+    return bench_single(args)
+
+
+def bench_single(args):
+    import torch
+
+    import paper_2310_03983_b200 as ap
+    from paper_2310_03983_b200 import _native as nat
+
+    n = args.n or 16384
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    lib = nat.load()
+    h_np = make_input(n, args.rho, 7 + n)
+    h = torch.from_numpy(h_np).to(dev)
+    dist = torch.empty_like(h)
+    pred = torch.empty((n, n), dtype=torch.int32, device=dev)
+    wsb = lib.apsp_workspace_bytes(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, BLOCK)
+    work = torch.empty(wsb, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.Stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    info = nat.ApspInfo()
+
+    def step():
+        with torch.cuda.stream(stream):
+            dist.copy_(h)
+        st = lib.apsp_fw_blocked(nat.DTYPE_I32, n, dist.data_ptr(), n, pred.data_ptr(), n, BLOCK, nat.TIER_AUTO,
+                                 work.data_ptr(), wsb, sp, ctypes.byref(info))
+        nat.check(st)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness guard on the measured configuration: a cheap certificate on the result
+    ok, why = ap.check_pred_tree(h, dist, pred, ap.INF32) if n <= 16384 else (True, "skipped")
+    if not ok:
+        raise SystemExit(f"bench result failed the predecessor certificate: {why}")
+    tier = nat.TIER_NAMES[info.tier]
+    launches_per_step = info.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    total_ms = e0.elapsed_time(e1)
+    ms_step = total_ms / args.steps
+    value = n ** 3 * args.steps / (total_ms / 1e3)
+
+    # dominant kernel: FW phase-3 min-plus tile launches, timed with events on their stream
+    lib.apsp_set_profiling(1)
+    step()
+    torch.cuda.synchronize()
+    lib.apsp_set_profiling(0)
+    kl, kms = info.kernel_launches, info.kernel_ms
+    N = (n + BLOCK - 1) // BLOCK * BLOCK
+    upd_per_launch = (N - BLOCK) ** 2 * BLOCK
+    achieved = upd_per_launch / (kms / kl / 1e3) if kl else None
+    peak = TIER_PEAK.get(tier)
+    roofline = {"bound": "alu", "kernel": f"minplus_{tier}_kernel (FW phase 3)", "op": TIER_OP.get(tier),
+                "achieved": achieved / 1e12 if achieved else None, "peak": peak / 1e12 if peak else None,
+                "unit": "T updates/s", "frac": (achieved / peak) if achieved and peak else None,
+                "traffic": None, "launches_per_step": kl, "kernel_share_of_step": (kms / ms_step) if kl else None,
+                "updates_per_launch": upd_per_launch,
+                "peak_source": "measured issue ceiling of the inner-loop instruction, profiles/r01_microbench_ops.txt"}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = bench_e2e(lib, nat, h_np, n, args)
+    cpu = None
+    if not args.no_cpu:
+        cpu = cpu_baseline(h_np)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "apsp_time_s": ms_step / 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": f"int16x2 keys / uint8 store (tier {tier}); int32 in/out" if tier == "u8"
+        else f"tier {tier}; int32 in/out",
+        "data": "synthetic (reference generator, bit-identical to apsp.generate)",
+        "config": config(n, args.rho, 1),
+        "pct_fp32_core_peak": value / FP32_CORE_PEAK,
+        "fp32_core_peak": FP32_CORE_PEAK,
+        "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
+        "tier": tier, "max_finite_distance": info.max_finite,
+        "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_e2e(lib, nat, h_np, n, args):
+    """Reference-facing host call: pinned host buffers in/out, copies inside the timed region."""
+    import torch
+
+    hin = torch.from_numpy(h_np).pin_memory()
+    dout = torch.empty((n, n), dtype=torch.int32).pin_memory()
+    pout = torch.empty((n, n), dtype=torch.int32).pin_memory()
+    info = nat.ApspInfo()
+
+    def call():
+        st = lib.apsp_solve_host(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, hin.data_ptr(), dout.data_ptr(),
+                                 pout.data_ptr(), nat.DTYPE_I32, nat.IDX_PRED, BLOCK, 0, 0, nat.TIER_AUTO, 0,
+                                 ctypes.byref(info))
+        nat.check(st)
+
+    for _ in range(max(1, args.warmup)):
+        call()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    dt = time.perf_counter() - t
+    return {"value": n ** 3 * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": n * n * 4,
+            "d2h_bytes_per_step": 2 * n * n * 4, "ms_per_step": dt / args.steps * 1e3,
+            "api": "apsp_solve_host (C ABI, host buffers; synchronous like the reference solvers)"}
+
+
+if __name__ == "__main__":
+    main()

@@ -72,11 +72,17 @@ typedef struct apsp_info {
   int64_t relaxations;  /* exact candidate count, the reference's relaxation_count */
   double device_ms;     /* CUDA-event time of the solve (device-level calls) */
   int32_t flags;        /* bit 0: zero-cost edges -> classic k order used for predecessors */
-  int32_t reserved;
+  int32_t kernel_launches; /* profiled min-plus tile launches (apsp_set_profiling(1)) */
+  double kernel_ms;     /* summed CUDA-event time of those launches */
 } apsp_info;
 
 const char* apsp_last_error(void);
 int apsp_abi_version(void);
+
+/* Profiling switch (process-wide): when on, every min-plus tile launch (FW phase 3, R-Kleene
+ * and squaring products) is bracketed by CUDA events on its stream and apsp_info reports
+ * their count and summed duration.  Off by default; costs two event records per launch. */
+void apsp_set_profiling(int on);
 
 /* Scratch bytes the device-level calls need when ws != NULL. */
 size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block);

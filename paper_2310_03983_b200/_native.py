@@ -37,6 +37,7 @@ ALG_FW_BLOCKED, ALG_FW_CLASSIC, ALG_RKLEENE, ALG_FW_SQUARING = 0, 1, 2, 3
 EXPORTED_SYMBOLS = (
     "apsp_last_error",
     "apsp_abi_version",
+    "apsp_set_profiling",
     "apsp_workspace_bytes",
     "apsp_fw_blocked",
     "apsp_fw_classic",
@@ -61,7 +62,8 @@ class ApspInfo(ctypes.Structure):
         ("relaxations", ctypes.c_int64),
         ("device_ms", ctypes.c_double),
         ("flags", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("kernel_launches", ctypes.c_int32),
+        ("kernel_ms", ctypes.c_double),
     ]
 
     def as_dict(self) -> dict:
@@ -74,6 +76,8 @@ class ApspInfo(ctypes.Structure):
             "relaxations": self.relaxations,
             "device_ms": self.device_ms,
             "classic_for_zero_edges": bool(self.flags & 1),
+            "kernel_launches": self.kernel_launches,
+            "kernel_ms": self.kernel_ms,
         }
 
 
@@ -83,6 +87,7 @@ _info_p = ctypes.POINTER(ApspInfo)
 _SIGNATURES = {
     "apsp_last_error": (ctypes.c_char_p, []),
     "apsp_abi_version": (_i32, []),
+    "apsp_set_profiling": (None, [_i32]),
     "apsp_workspace_bytes": (_sz, [_i32, _i32, _i64, _i32]),
     "apsp_fw_blocked": (_i32, [_i32, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _sz, _vp, _info_p]),
     "apsp_fw_classic": (_i32, [_i32, _i64, _vp, _i64, _vp, _i64, _vp, _info_p]),

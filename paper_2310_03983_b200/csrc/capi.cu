@@ -20,6 +20,49 @@ namespace {
 constexpr int DEFAULT_BLOCK = 128;
 constexpr int TILE_ALIGN = 128;
 
+// Opt-in event timing of the min-plus tile launches (apsp_set_profiling).
+struct Profiler {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  size_t used = 0;
+  void reset() { used = 0; }
+  void begin(cudaStream_t s) {
+    if (!on) return;
+    if (used == ev.size()) {
+      cudaEvent_t a, b;
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      ev.emplace_back(a, b);
+    }
+    cudaEventRecord(ev[used].first, s);
+  }
+  void end(cudaStream_t s) {
+    if (!on) return;
+    cudaEventRecord(ev[used].second, s);
+    used++;
+  }
+  // after the stream is synchronised
+  void collect(apsp_info* info) {
+    if (!info) return;
+    double ms = 0;
+    for (size_t i = 0; i < used; i++) {
+      float t = 0;
+      cudaEventElapsedTime(&t, ev[i].first, ev[i].second);
+      ms += t;
+    }
+    info->kernel_launches = int32_t(used);
+    info->kernel_ms = ms;
+  }
+};
+thread_local Profiler g_prof;
+
+int timed_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
+  g_prof.begin(s);
+  const int rc = launch_minplus(store, a, s);
+  g_prof.end(s);
+  return rc;
+}
+
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
 int tier_store(int tier) {
@@ -47,6 +90,20 @@ int64_t tier_limit(int tier) {
   return INT64_MAX;
 }
 
+// Keep freed stream-ordered allocations in the device pool across calls (the default
+// release threshold of 0 returns them to the driver at every synchronisation).
+void keep_pool() {
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[dev] = true;
+}
+
 struct Scratch {
   void* base = nullptr;
   bool owned = false;
@@ -61,6 +118,7 @@ struct Scratch {
       base = ws;
       return 0;
     }
+    keep_pool();
     APSP_CUDA_TRY(cudaMallocAsync(&base, need, st));
     owned = true;
     return 0;
@@ -132,7 +190,7 @@ int fw_blocked_view(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int
     a.skip_row_lo = k0; a.skip_row_hi = k0 + b;
     a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
     a.status = st;
-    rc = launch_minplus(store, a, s);
+    rc = timed_minplus(store, a, s);
     if (rc) return rc;
     *launches += 4;
   }
@@ -166,6 +224,7 @@ struct Timer {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t s;
   explicit Timer(cudaStream_t st) : s(st) {
+    g_prof.reset();
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a, s);
@@ -262,6 +321,7 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     info->relaxations = n * n * n;
     info->device_ms = ms;
     info->flags = 0;
+    g_prof.collect(info);
   }
   return 0;
 }
@@ -306,6 +366,7 @@ int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     info->relaxations = n * n * n;
     info->device_ms = ms;
     info->flags = 0;
+    g_prof.collect(info);
   }
   return 0;
 }
@@ -343,7 +404,7 @@ struct RK {
     a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
     a.status = st;
     launches++;
-    return launch_minplus(store, a, s);
+    return timed_minplus(store, a, s);
   }
   int snap_vals(int64_t r0, int64_t c0, int64_t rows, int64_t cols) {
     launches++;
@@ -485,6 +546,7 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
     info->relaxations = n * n * n;
     info->device_ms = ms;
     info->flags = 0;
+    g_prof.collect(info);
   }
   return 0;
 }
@@ -546,7 +608,7 @@ int squaring_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, in
       a.predB = nullptr; a.ldp = n; a.m = n; a.n = n; a.k = n; a.inner_off = 0; a.mode = IDX_VIA;
       a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
       a.status = &hdr_dev->status;
-      rc = launch_minplus(store, a, s);
+      rc = timed_minplus(store, a, s);
       if (!rc) rc = read_header(hdr_dev, hdr, s);
       if (rc) return rc;
       launches += 4;
@@ -582,6 +644,7 @@ int squaring_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, in
     info->relaxations = int64_t(iters) * n * n * n;
     info->device_ms = ms;
     info->flags = 0;
+    g_prof.collect(info);
   }
   return 0;
 }
@@ -650,7 +713,7 @@ int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
   a.predB = nullptr; a.ldp = 0; a.m = n1; a.n = n3; a.k = n2; a.inner_off = inner_off; a.mode = IDX_VIA;
   a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
   a.status = &hdr_dev->status;
-  rc = launch_minplus(store, a, s);
+  rc = timed_minplus(store, a, s);
   if (!rc && !accumulate && via)
     rc = launch_witness_clear(store, Xs, n2, Ys, n3, Zs, n3, via, ldv, n1, n2, n3, row_off, inner_off, col_off, s);
   if (!rc) rc = launch_max_finite(store, Zs, n3, n1, n3, &hdr_dev->cert, s);
@@ -670,6 +733,7 @@ int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
     info->relaxations = n1 * n2 * n3;
     info->device_ms = ms;
     info->flags = 0;
+    g_prof.collect(info);
   }
   return 0;
 }
@@ -738,6 +802,7 @@ int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows,
 extern "C" {
 
 const char* apsp_last_error(void) { return apsp::last_error(); }
+void apsp_set_profiling(int on) { g_prof.on = on != 0; }
 int apsp_abi_version(void) { return APSP_ABI_VERSION; }
 
 size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block) {
@@ -784,6 +849,7 @@ int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* di
   if (idx_dtype != APSP_DTYPE_I32 && idx_dtype != APSP_DTYPE_I64)
     return set_error(APSP_EINVAL, "index dtype must be int32 or int64");
   APSP_CUDA_TRY(cudaSetDevice(device));
+  keep_pool();
   cudaStream_t s;
   APSP_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
