@@ -195,6 +195,7 @@ def main():
     ap_.add_argument("--no-cpu", action="store_true")
     ap_.add_argument("--no-e2e", action="store_true")
     ap_.add_argument("--ref-step-s", type=float, default=8.0)
+    ap_.add_argument("--block", type=int, default=BLOCK)
     args = ap_.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":
@@ -213,6 +214,7 @@ def bench_single(args):
     from paper_2310_03983_b200 import _native as nat
 
     n = args.n or 16384
+    block = args.block
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     lib = nat.load()
@@ -220,7 +222,7 @@ def bench_single(args):
     h = torch.from_numpy(h_np).to(dev)
     dist = torch.empty_like(h)
     pred = torch.empty((n, n), dtype=torch.int32, device=dev)
-    wsb = lib.apsp_workspace_bytes(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, BLOCK)
+    wsb = lib.apsp_workspace_bytes(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, block)
     work = torch.empty(wsb, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
@@ -229,7 +231,7 @@ def bench_single(args):
     def step():
         with torch.cuda.stream(stream):
             dist.copy_(h)
-        st = lib.apsp_fw_blocked(nat.DTYPE_I32, n, dist.data_ptr(), n, pred.data_ptr(), n, BLOCK, nat.TIER_AUTO,
+        st = lib.apsp_fw_blocked(nat.DTYPE_I32, n, dist.data_ptr(), n, pred.data_ptr(), n, block, nat.TIER_AUTO,
                                  work.data_ptr(), wsb, sp, ctypes.byref(info))
         nat.check(st)
 
@@ -260,20 +262,22 @@ def bench_single(args):
     torch.cuda.synchronize()
     lib.apsp_set_profiling(0)
     kl, kms = info.kernel_launches, info.kernel_ms
-    N = (n + BLOCK - 1) // BLOCK * BLOCK
-    upd_per_launch = (N - BLOCK) ** 2 * BLOCK
-    achieved = upd_per_launch / (kms / kl / 1e3) if kl else None
+    N = (n + block - 1) // block * block
+    # phase 3 of one pivot round updates every tile outside the pivot cross: (N-b)^2 * b
+    # (3a + 3b launches together); a solve has N/b rounds
+    upd_phase3 = (N // block) * (N - block) ** 2 * block
+    achieved = upd_phase3 / (kms / 1e3) if kl else None
     peak = TIER_PEAK.get(tier)
     roofline = {"bound": "alu", "kernel": f"minplus_{tier}_kernel (FW phase 3)", "op": TIER_OP.get(tier),
                 "achieved": achieved / 1e12 if achieved else None, "peak": peak / 1e12 if peak else None,
                 "unit": "T updates/s", "frac": (achieved / peak) if achieved and peak else None,
                 "traffic": None, "launches_per_step": kl, "kernel_share_of_step": (kms / ms_step) if kl else None,
-                "updates_per_launch": upd_per_launch,
+                "updates_per_step": upd_phase3, "kernel_ms_per_step": kms,
                 "peak_source": "measured issue ceiling of the inner-loop instruction, profiles/r01_microbench_ops.txt"}
 
     e2e = None
     if not args.no_e2e:
-        e2e = bench_e2e(lib, nat, h_np, n, args)
+        e2e = bench_e2e(lib, nat, h_np, n, args, block)
     cpu = None
     if not args.no_cpu:
         cpu = cpu_baseline(h_np)
@@ -283,7 +287,7 @@ def bench_single(args):
         "vs_baseline": None, "dtype": f"int16x2 keys / uint8 store (tier {tier}); int32 in/out" if tier == "u8"
         else f"tier {tier}; int32 in/out",
         "data": "synthetic (reference generator, bit-identical to apsp.generate)",
-        "config": config(n, args.rho, 1),
+        "config": config(n, args.rho, 1) | {"block": block},
         "pct_fp32_core_peak": value / FP32_CORE_PEAK,
         "fp32_core_peak": FP32_CORE_PEAK,
         "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
@@ -293,7 +297,7 @@ def bench_single(args):
     print(json.dumps(line), flush=True)
 
 
-def bench_e2e(lib, nat, h_np, n, args):
+def bench_e2e(lib, nat, h_np, n, args, block):
     """Reference-facing host call: pinned host buffers in/out, copies inside the timed region."""
     import torch
 
@@ -304,7 +308,7 @@ def bench_e2e(lib, nat, h_np, n, args):
 
     def call():
         st = lib.apsp_solve_host(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, hin.data_ptr(), dout.data_ptr(),
-                                 pout.data_ptr(), nat.DTYPE_I32, nat.IDX_PRED, BLOCK, 0, 0, nat.TIER_AUTO, 0,
+                                 pout.data_ptr(), nat.DTYPE_I32, nat.IDX_PRED, block, 0, 0, nat.TIER_AUTO, 0,
                                  ctypes.byref(info))
         nat.check(st)
 

@@ -1,6 +1,7 @@
 // C ABI and native orchestration: blocked FW rounds, R-Kleene recursion, squaring loop,
 // min-plus products, value-tier selection and certification, host-level entry.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -169,32 +170,186 @@ std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced) {
 size_t header_bytes() { return 256; }
 
 // ---- blocked FW on an m x m view (m multiple of b) -------------------------------------
-int fw_blocked_view(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t m, int b, int mode,
-                    int64_t via_off, Status* st, cudaStream_t s, int* launches) {
-  const size_t es = store_elem_size(store);
-  char* Dc = static_cast<char*>(D);
-  for (int64_t k0 = 0; k0 < m; k0 += b) {
-    int rc = launch_block_close(store, D, ld, k0, b, P, ldp, mode, via_off + k0, st, s);
-    if (rc) return rc;
-    rc = launch_fw_panels(store, D, ld, P, ldp, m, k0, b, mode, via_off, st, s);
-    if (rc) return rc;
-    MinplusArgs a{};
-    a.A = Dc + k0 * es; a.lda = ld;
-    a.B = Dc + k0 * ld * es; a.ldb = ld;
-    a.C = D; a.ldc = ld;
-    a.idx = P; a.ldi = ldp;
-    a.predB = P ? P + k0 * ldp : nullptr; a.ldp = ldp;
-    a.m = m; a.n = m; a.k = b;
-    a.inner_off = via_off + k0;
-    a.mode = mode;
-    a.skip_row_lo = k0; a.skip_row_hi = k0 + b;
-    a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
-    a.status = st;
-    rc = timed_minplus(store, a, s);
-    if (rc) return rc;
-    *launches += 4;
+//
+// Round K (pivot block [k0, k0+b)):
+//   phase 1  close the diagonal block in classic k order (block_close; b > 128: blocked FW
+//            on the b x b sub-view)
+//   phase 2  row panel <- Dg (x) row panel, column panel <- column panel (x) Dg: one min-plus
+//            product each against the CLOSED diagonal block (equal distances to the classic
+//            in-block k loop); pred of the row panel is read from a snapshot because the
+//            product rewrites those rows
+//   phase 3  every other tile: C <- min(C, colpanel (x) rowpanel), pred <- pred[k*][j]
+// Lookahead: phase 3 of round K is split into (3a) the tiles of pivot cross K+1 and (3b) the
+// rest; phases 1-2 of round K+1 run on a high-priority side stream concurrently with 3b.
+// 3b never touches cross K+1 and phases 1-2 of K+1 never touch cross K, so the overlap is
+// race-free; round K+1's 3a waits for both.
+struct FwCtx {
+  int store = 0;
+  size_t es = 1;
+  char* D = nullptr;
+  int64_t ld = 0;
+  int32_t* P = nullptr;
+  int64_t ldp = 0;
+  int64_t m = 0;
+  int b = 128;
+  int mode = IDX_PRED;
+  int64_t via_off = 0;
+  Status* st = nullptr;
+  cudaStream_t side = nullptr;   // nullptr: no lookahead
+  int32_t* predsnap = nullptr;   // b x m
+  char* rowsnap = nullptr;       // b x m values (b > 128 only)
+  char* colsnap = nullptr;       // m x b values (b > 128 only)
+  int launches = 0;
+};
+
+size_t fw_scratch_bytes(int64_t m, int b, size_t es) {
+  size_t v = size_t(b) * m * 4 + 256;
+  if (b > TILE_ALIGN) v += 2 * size_t(b) * m * es + 256;
+  return v;
+}
+
+int fw_run(FwCtx& c, cudaStream_t s);
+
+int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s) {
+  c.launches++;
+  if (c.b <= TILE_ALIGN)
+    return launch_block_close(c.store, c.D, c.ld, k0, c.b, c.P, c.ldp, c.mode, c.via_off + k0, c.st, s);
+  FwCtx sub = c;
+  sub.D = c.D + (k0 * c.ld + k0) * c.es;
+  sub.P = c.P ? c.P + k0 * c.ldp + k0 : nullptr;
+  sub.m = c.b;
+  sub.b = TILE_ALIGN;
+  sub.via_off = c.via_off + k0;
+  sub.side = nullptr;
+  sub.rowsnap = sub.colsnap = nullptr;
+  sub.launches = 0;
+  const int rc = fw_run(sub, s);
+  c.launches += sub.launches;
+  return rc;
+}
+
+int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
+  const int64_t b = c.b, m = c.m;
+  char* Dg = c.D + (k0 * c.ld + k0) * c.es;
+  char* rowp = c.D + k0 * c.ld * c.es;
+  char* colp = c.D + k0 * c.es;
+  const bool snap = b > TILE_ALIGN;
+  if (c.P && c.mode == IDX_PRED) {
+    APSP_CUDA_TRY(cudaMemcpy2DAsync(c.predsnap, size_t(m) * 4, c.P + k0 * c.ldp, size_t(c.ldp) * 4, size_t(m) * 4,
+                                    size_t(b), cudaMemcpyDeviceToDevice, s));
   }
-  return 0;
+  if (snap) {
+    int rc = launch_copy_block(c.store, rowp, c.ld, c.rowsnap, m, b, m, s);
+    if (!rc) rc = launch_copy_block(c.store, colp, c.ld, c.colsnap, b, m, b, s);
+    if (rc) return rc;
+  }
+  MinplusArgs a = minplus_args();
+  a.A = Dg; a.lda = c.ld;
+  a.B = snap ? c.rowsnap : rowp; a.ldb = snap ? m : c.ld;
+  a.C = rowp; a.ldc = c.ld;
+  a.idx = c.P ? c.P + k0 * c.ldp : nullptr; a.ldi = c.ldp;
+  a.predB = c.predsnap; a.ldp = m;
+  a.m = b; a.n = m; a.k = b;
+  a.inner_off = c.via_off + k0;
+  a.mode = c.mode;
+  a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
+  a.status = c.st;
+  int rc = launch_minplus(c.store, a, s);
+  if (rc) return rc;
+  MinplusArgs q = minplus_args();
+  q.A = snap ? c.colsnap : colp; q.lda = snap ? b : c.ld;
+  q.B = Dg; q.ldb = c.ld;
+  q.C = colp; q.ldc = c.ld;
+  q.idx = c.P ? c.P + k0 : nullptr; q.ldi = c.ldp;
+  q.predB = c.P ? c.P + k0 * c.ldp + k0 : nullptr; q.ldp = c.ldp;
+  q.m = m; q.n = b; q.k = b;
+  q.inner_off = c.via_off + k0;
+  q.mode = c.mode;
+  q.skip_row_lo = k0; q.skip_row_hi = k0 + b;
+  q.status = c.st;
+  c.launches += 2;
+  return launch_minplus(c.store, q, s);
+}
+
+// phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
+// additionally skips cross skip_next.
+int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaStream_t s) {
+  MinplusArgs a = minplus_args();
+  a.A = c.D + k0 * c.es; a.lda = c.ld;
+  a.B = c.D + k0 * c.ld * c.es; a.ldb = c.ld;
+  a.C = c.D; a.ldc = c.ld;
+  a.idx = c.P; a.ldi = c.ldp;
+  a.predB = c.P ? c.P + k0 * c.ldp : nullptr; a.ldp = c.ldp;
+  a.m = c.m; a.n = c.m; a.k = c.b;
+  a.inner_off = c.via_off + k0;
+  a.mode = c.mode;
+  a.skip_row_lo = k0; a.skip_row_hi = k0 + c.b;
+  a.skip_col_lo = k0; a.skip_col_hi = k0 + c.b;
+  if (only_next >= 0) { a.only_lo = only_next; a.only_hi = only_next + c.b; }
+  if (skip_next >= 0) { a.skip2_lo = skip_next; a.skip2_hi = skip_next + c.b; }
+  a.status = c.st;
+  c.launches++;
+  return timed_minplus(c.store, a, s);
+}
+
+int fw_run(FwCtx& c, cudaStream_t s) {
+  const int64_t b = c.b;
+  int rc = fw_phase1(c, 0, s);
+  if (!rc) rc = fw_phase2(c, 0, s);
+  if (rc) return rc;
+  cudaEvent_t evA = nullptr, evB = nullptr;
+  if (c.side) {
+    APSP_CUDA_TRY(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
+    APSP_CUDA_TRY(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+  }
+  for (int64_t k0 = 0; !rc && k0 < c.m; k0 += b) {
+    const int64_t k1 = k0 + b;
+    if (k1 >= c.m) {
+      rc = fw_phase3(c, k0, -1, -1, s);
+    } else if (c.side) {
+      rc = fw_phase3(c, k0, k1, -1, s);                       // 3a: next pivot cross
+      if (!rc && cudaEventRecord(evA, s) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
+      if (!rc && cudaStreamWaitEvent(c.side, evA, 0) != cudaSuccess) rc = set_error(APSP_ECUDA, "stream wait");
+      if (!rc) rc = fw_phase1(c, k1, c.side);
+      if (!rc) rc = fw_phase2(c, k1, c.side);
+      if (!rc && cudaEventRecord(evB, c.side) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
+      if (!rc) rc = fw_phase3(c, k0, -1, k1, s);               // 3b: the rest
+      if (!rc && cudaStreamWaitEvent(s, evB, 0) != cudaSuccess) rc = set_error(APSP_ECUDA, "stream wait");
+    } else {
+      rc = fw_phase3(c, k0, -1, -1, s);
+      if (!rc) rc = fw_phase1(c, k1, s);
+      if (!rc) rc = fw_phase2(c, k1, s);
+    }
+  }
+  if (evA) cudaEventDestroy(evA);
+  if (evB) cudaEventDestroy(evB);
+  return rc;
+}
+
+// High-priority side stream of the current device (created once).
+cudaStream_t side_stream() {
+  static cudaStream_t streams[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!streams[dev]) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&streams[dev], cudaStreamNonBlocking, hi) != cudaSuccess) return nullptr;
+  }
+  return streams[dev];
+}
+
+// convenience for callers with a plain view (R-Kleene leaves): no lookahead
+int fw_blocked_view(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t m, int b, int mode,
+                    int64_t via_off, Status* st, cudaStream_t s, int* launches, int32_t* predsnap) {
+  FwCtx c;
+  c.store = store; c.es = store_elem_size(store);
+  c.D = static_cast<char*>(D); c.ld = ld; c.P = P; c.ldp = ldp;
+  c.m = m; c.b = b; c.mode = mode; c.via_off = via_off; c.st = st;
+  c.predsnap = predsnap;
+  const int rc = fw_run(c, s);
+  *launches += c.launches;
+  return rc;
 }
 
 int certify(int tier, int store, const void* D, int64_t ld, int64_t rows, int64_t cols, const ScanResult& sc,
@@ -254,21 +409,22 @@ constexpr int32_t FLAG_CLASSIC_FOR_ZERO_EDGES = 1;
 size_t fw_ws_bytes(int dtype, int64_t n, int block) {
   const int64_t N = round_up(std::max<int64_t>(n, 1), block);
   const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
-  return header_bytes() + size_t(N) * N * (es + 4) + 256;
+  return header_bytes() + size_t(N) * N * (es + 4) + 256 + fw_scratch_bytes(N, block, es);
 }
 
 int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
                     void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info) {
   if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
   if (b <= 0) b = DEFAULT_BLOCK;
-  if (b != 128) return set_error(APSP_EINVAL, "blocked FW supports block = 128 (got %d)", b);
+  if (b != 128 && b != 256) return set_error(APSP_EINVAL, "blocked FW supports block 128 or 256 (got %d)", b);
   const int64_t N = round_up(n, b);
   Scratch sc;
   int rc = sc.acquire(ws, ws_bytes, fw_ws_bytes(dtype, n, b), s);
   if (rc) return rc;
   Header* hdr_dev = static_cast<Header*>(sc.base);
   int32_t* P = reinterpret_cast<int32_t*>(static_cast<char*>(sc.base) + header_bytes());
-  void* D = reinterpret_cast<char*>(P) + size_t(N) * N * 4;
+  char* D = reinterpret_cast<char*>(P) + size_t(N) * N * 4;
+  char* scratch = D + size_t(N) * N * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 256;
   Header hdr{};
   Timer tm(s);
   rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
@@ -292,7 +448,20 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     tried |= 1 << tier;
     APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
     rc = launch_to_store(dtype, dist, ld, n, store, D, N, N, P, N, 1, s);
-    if (!rc) rc = fw_blocked_view(store, D, N, P, N, N, b, IDX_PRED, 0, &hdr_dev->status, s, &launches);
+    if (!rc) {
+      FwCtx c;
+      c.store = store; c.es = store_elem_size(store);
+      c.D = D; c.ld = N; c.P = P; c.ldp = N; c.m = N; c.b = b; c.mode = IDX_PRED; c.via_off = 0;
+      c.st = &hdr_dev->status;
+      c.side = getenv("APSP_NO_LOOKAHEAD") ? nullptr : side_stream();
+      c.predsnap = reinterpret_cast<int32_t*>(scratch);
+      if (b > TILE_ALIGN) {
+        c.rowsnap = scratch + size_t(b) * N * 4 + 256;
+        c.colsnap = c.rowsnap + size_t(b) * N * c.es + 128;
+      }
+      rc = fw_run(c, s);
+      launches += c.launches;
+    }
     bool ok = false;
     if (!rc) rc = certify(tier, store, D, N, n, n, scan, hdr_dev, hdr, s, ok);
     if (rc) return rc;
@@ -393,7 +562,7 @@ struct RK {
 
   int mp(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t r0, int64_t c0, int64_t m, int64_t n,
          int64_t k, const int32_t* predB, int64_t ldpb, int64_t inner_off) {
-    MinplusArgs a{};
+    MinplusArgs a = minplus_args();
     a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
     a.C = at(r0, c0); a.ldc = ld;
     a.idx = pat(r0, c0); a.ldi = ld;
@@ -401,7 +570,6 @@ struct RK {
     a.m = m; a.n = n; a.k = k;
     a.inner_off = inner_off;
     a.mode = mode;
-    a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
     a.status = st;
     launches++;
     return timed_minplus(store, a, s);
@@ -426,7 +594,8 @@ struct RK {
 
   int leaf(int64_t lo, int64_t m) {
     if (aligned && m > 128) {
-      return fw_blocked_view(store, at(lo, lo), ld, pat(lo, lo), ld, m, DEFAULT_BLOCK, mode, lo, st, s, &launches);
+      return fw_blocked_view(store, at(lo, lo), ld, pat(lo, lo), ld, m, DEFAULT_BLOCK, mode, lo, st, s, &launches,
+                             sP);
     }
     launches += int(m > 128 ? m : 1);
     return launch_block_close(store, D, ld, lo, m, P, ld, mode, lo, st, s);
@@ -603,11 +772,10 @@ int squaring_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, in
       APSP_CUDA_TRY(cudaMemcpyAsync(nxt, cur, size_t(n) * n * es, cudaMemcpyDeviceToDevice, s));
       APSP_CUDA_TRY(cudaMemcpyAsync(nxtP, curP, size_t(n) * n * 4, cudaMemcpyDeviceToDevice, s));
       APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status.changed, 0, sizeof(int32_t), s));
-      MinplusArgs a{};
+      MinplusArgs a = minplus_args();
       a.A = cur; a.lda = n; a.B = cur; a.ldb = n; a.C = nxt; a.ldc = n; a.idx = nxtP; a.ldi = n;
       a.predB = nullptr; a.ldp = n; a.m = n; a.n = n; a.k = n; a.inner_off = 0; a.mode = IDX_VIA;
-      a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
-      a.status = &hdr_dev->status;
+        a.status = &hdr_dev->status;
       rc = timed_minplus(store, a, s);
       if (!rc) rc = read_header(hdr_dev, hdr, s);
       if (rc) return rc;
@@ -708,10 +876,9 @@ int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
   }
   if (rc) return rc;
   APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
-  MinplusArgs a{};
+  MinplusArgs a = minplus_args();
   a.A = Xs; a.lda = n2; a.B = Ys; a.ldb = n3; a.C = Zs; a.ldc = n3; a.idx = via; a.ldi = ldv;
   a.predB = nullptr; a.ldp = 0; a.m = n1; a.n = n3; a.k = n2; a.inner_off = inner_off; a.mode = IDX_VIA;
-  a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
   a.status = &hdr_dev->status;
   rc = timed_minplus(store, a, s);
   if (!rc && !accumulate && via)

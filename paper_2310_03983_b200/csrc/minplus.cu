@@ -19,10 +19,34 @@ namespace apsp {
 
 constexpr int BM = 128, BN = 128, NT = 256;
 
+// Tile origin of this CTA.  Full grid: (blockIdx.y, blockIdx.x).  Cross-list mode
+// (only_lo < only_hi): blockIdx.x enumerates the tiles of rows band + cols band [lo, hi)
+// (band width w tiles): first the w full tile rows, then the remaining rows of the w columns.
+__device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn, int64_t& i0, int64_t& j0) {
+  if (p.only_lo < p.only_hi) {
+    const int64_t w = (p.only_hi - p.only_lo) / bm, lo_t = p.only_lo / bm;
+    const int64_t nt_c = (p.n + bn - 1) / bn;
+    const int64_t id = blockIdx.x;
+    if (id < w * nt_c) {
+      i0 = (lo_t + id / nt_c) * bm;
+      j0 = (id % nt_c) * bn;
+    } else {
+      const int64_t id2 = id - w * nt_c, rr = id2 / w, cc = id2 % w;
+      i0 = (rr < lo_t ? rr : rr + w) * bm;
+      j0 = (lo_t + cc) * bn;
+    }
+  } else {
+    i0 = int64_t(blockIdx.y) * bm;
+    j0 = int64_t(blockIdx.x) * bn;
+  }
+}
+
 __device__ __forceinline__ bool tile_skipped(const MinplusArgs& p, int64_t i0, int64_t j0, int bm, int bn) {
-  bool rin = i0 >= p.skip_row_lo && i0 + bm <= p.skip_row_hi;
-  bool cin = j0 >= p.skip_col_lo && j0 + bn <= p.skip_col_hi;
-  return rin || cin;
+  const bool rin = i0 >= p.skip_row_lo && i0 + bm <= p.skip_row_hi;
+  const bool cin = j0 >= p.skip_col_lo && j0 + bn <= p.skip_col_hi;
+  const bool r2 = i0 >= p.skip2_lo && i0 + bm <= p.skip2_hi;
+  const bool c2 = j0 >= p.skip2_lo && j0 + bn <= p.skip2_hi;
+  return rin || cin || r2 || c2;
 }
 
 __device__ __forceinline__ void emit_idx(const MinplusArgs& p, int64_t i, int64_t j, uint32_t kk) {
@@ -37,6 +61,7 @@ __device__ __forceinline__ void emit_idx(const MinplusArgs& p, int64_t i, int64_
 struct SmemU8 {
   uint32_t As[2][SUB][BM];   // replicated key pair (k0 | k0 << 16) per row
   uint16_t Bs[2][SUB][BN];   // tagged key per column
+  uint8_t Cs[BM][BN];        // old values of the tile (cp.async prefetch)
 };
 
 __device__ __forceinline__ void u8_load_chunk(const MinplusArgs& p, int64_t i0, int64_t j0, int64_t kc,
@@ -98,39 +123,41 @@ __device__ __forceinline__ void u8_store_chunk(SmemU8& sm, int buf, const uint4&
 }
 
 __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
-  __shared__ __align__(16) SmemU8 sm;
-  const int64_t i0 = int64_t(blockIdx.y) * BM, j0 = int64_t(blockIdx.x) * BN;
+  extern __shared__ __align__(16) unsigned char smraw_u8[];
+  SmemU8& sm = *reinterpret_cast<SmemU8*>(smraw_u8);
+  int64_t i0, j0;
+  tile_origin(p, BM, BN, i0, j0);
   if (tile_skipped(p, i0, j0, BM, BN)) return;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
 
   uint32_t acc[8][4];   // [row][pair]: pairs = cols {4tx,4tx+1},{4tx+2,4tx+3},{64+4tx..},{..}
   uint32_t kst[8][4];   // packed 16-bit k index (KNONE = untouched)
   const uint8_t* C = static_cast<const uint8_t*>(p.C);
-  const bool cfast = (i0 + BM <= p.m) && (j0 + BN <= p.n) && ((reinterpret_cast<uintptr_t>(C) & 3) == 0) &&
-                     ((p.ldc & 3) == 0);
+  const bool cfast = (i0 + BM <= p.m) && (j0 + BN <= p.n) && ((reinterpret_cast<uintptr_t>(C) & 15) == 0) &&
+                     ((p.ldc & 15) == 0);
+  {  // old values -> smem asynchronously (cp.async); merged after the first chunk
+    const int r = t >> 1, cb = 64 * (t & 1);
+    if (cfast) {
+      const uint8_t* src = C + (i0 + r) * p.ldc + j0 + cb;
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.Cs[r][cb]));
 #pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int64_t j = j0 + 64 * h + 4 * tx;
-      uint32_t w;
-      if (cfast) {
-        w = *reinterpret_cast<const uint32_t*>(C + i * p.ldc + j);
-      } else {
-        w = 0;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          uint32_t v = (i < p.m && j + q < p.n) ? C[i * p.ldc + j + q] : U8_INF;
-          w |= v << (8 * q);
-        }
+      for (int q = 0; q < 4; q++)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+      asm volatile("cp.async.commit_group;\n" ::);
+    } else {
+      for (int q = 0; q < 64; q++) {
+        const int64_t i = i0 + r, j = j0 + cb + q;
+        sm.Cs[r][cb + q] = (i < p.m && j < p.n) ? C[i * p.ldc + j] : uint8_t(U8_INF);
       }
-      acc[r][2 * h] = __byte_perm(w, 0, 0x4140) << TAG_BITS;
-      acc[r][2 * h + 1] = __byte_perm(w, 0, 0x4342) << TAG_BITS;
-      kst[r][2 * h] = 0xFFFFFFFFu;
-      kst[r][2 * h + 1] = 0xFFFFFFFFu;
     }
   }
+#pragma unroll
+  for (int r = 0; r < 8; r++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      acc[r][q] = K16_INF * 0x00010001u;
+      kst[r][q] = 0xFFFFFFFFu;
+    }
 
   const bool abfast_base = ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0) && ((p.lda & 15) == 0) &&
                            ((reinterpret_cast<uintptr_t>(p.B) & 15) == 0) && ((p.ldb & 15) == 0) &&
@@ -156,6 +183,22 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
       for (int r = 0; r < 8; r++)
 #pragma unroll
         for (int q = 0; q < 4; q++) acc[r][q] = viaddmin16x2(a[r], b[q], acc[r][q]);
+    }
+    if (c == 0) {
+      // merge the (prefetched) old values: an untagged old key wins value ties, so only a
+      // strictly improving candidate keeps its tag (strict-improvement rule)
+      asm volatile("cp.async.wait_all;\n" ::);
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
+          acc[r][2 * h] = __vmins2(acc[r][2 * h], __byte_perm(w, 0, 0x4140) << TAG_BITS);
+          acc[r][2 * h + 1] = __vmins2(acc[r][2 * h + 1], __byte_perm(w, 0, 0x4342) << TAG_BITS);
+        }
+      }
     }
     // decode tags of this chunk into k indices (relative to k = 0 of the product)
     uint32_t any = 0;
@@ -275,7 +318,8 @@ __device__ __forceinline__ void w32_store_chunk(SmemW32& sm, int buf, const int4
 __global__ void __launch_bounds__(NT, 1) minplus_w32_kernel(MinplusArgs p) {
   extern __shared__ __align__(16) unsigned char smraw[];
   SmemW32& sm = *reinterpret_cast<SmemW32*>(smraw);
-  const int64_t i0 = int64_t(blockIdx.y) * BM, j0 = int64_t(blockIdx.x) * BN;
+  int64_t i0, j0;
+  tile_origin(p, BM, BN, i0, j0);
   if (tile_skipped(p, i0, j0, BM, BN)) return;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
 
@@ -406,7 +450,8 @@ __global__ void __launch_bounds__(NT) minplus_exact_kernel(MinplusArgs p) {
   using T = typename StoreT<S>::T;
   __shared__ T As[SUB][EM + 1];
   __shared__ T Bs[SUB][EN];
-  const int64_t i0 = int64_t(blockIdx.y) * EM, j0 = int64_t(blockIdx.x) * EN;
+  int64_t i0, j0;
+  tile_origin(p, EM, EN, i0, j0);
   if (tile_skipped(p, i0, j0, EM, EN)) return;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
   const T inf = store_inf<S>();
@@ -474,14 +519,33 @@ __global__ void __launch_bounds__(NT) minplus_exact_kernel(MinplusArgs p) {
   }
 }
 
+static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
+  if (a.only_lo < a.only_hi) {
+    const int64_t w = (a.only_hi - a.only_lo) / bm;
+    const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
+    return dim3(unsigned(w * nt_c + (nt_r - w) * w), 1);
+  }
+  return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
+}
+
 int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
   if (a.m <= 0 || a.n <= 0) return 0;
   if (a.k <= 0) return 0;
   if (a.k > 65535) return set_error(2, "min-plus inner dimension %lld exceeds 65535", (long long)a.k);
+  if (a.only_lo < a.only_hi) {
+    const int tb = (store == STORE_U8 || store == STORE_W32) ? BM : EM;
+    if (a.only_lo % tb || a.only_hi % tb || a.m != a.n)
+      return set_error(2, "cross-list mode needs tile-aligned bands on a square view");
+  }
   switch (store) {
     case STORE_U8: {
-      dim3 grid(unsigned((a.n + BN - 1) / BN), unsigned((a.m + BM - 1) / BM));
-      minplus_u8_kernel<<<grid, NT, 0, s>>>(a);
+      static bool attr = false;
+      if (!attr) {
+        APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(sizeof(SmemU8))));
+        attr = true;
+      }
+      minplus_u8_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemU8), s>>>(a);
       break;
     }
     case STORE_W32: {
@@ -491,14 +555,13 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
                                            int(sizeof(SmemW32))));
         attr = true;
       }
-      dim3 grid(unsigned((a.n + BN - 1) / BN), unsigned((a.m + BM - 1) / BM));
-      minplus_w32_kernel<<<grid, NT, sizeof(SmemW32), s>>>(a);
+      minplus_w32_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemW32), s>>>(a);
       break;
     }
     case STORE_I32:
     case STORE_F32:
     case STORE_I64: {
-      dim3 grid(unsigned((a.n + EN - 1) / EN), unsigned((a.m + EM - 1) / EM));
+      const dim3 grid = grid_for(a, EM, EN);
       if (store == STORE_I32) minplus_exact_kernel<STORE_I32><<<grid, NT, 0, s>>>(a);
       else if (store == STORE_F32) minplus_exact_kernel<STORE_F32><<<grid, NT, 0, s>>>(a);
       else minplus_exact_kernel<STORE_I64><<<grid, NT, 0, s>>>(a);
