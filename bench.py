@@ -43,7 +43,7 @@ FP32_CORE_PEAK = 148 * 128 * 1965e6 / 2          # 18.6 T upd/s 
 TIER_PEAK = {"u8": 37.07e12, "w32": 24.91e12, "i32": 17.98e12, "f32": 6.05e12, "i64": 6.05e12}
 TIER_OP = {"u8": "VIADDMNMX.S16x2 (2 upd/instr)", "w32": "VIADD+VIMNMX3", "i32": "compare-select",
            "f32": "FADD/FSETP/FSEL/SEL", "i64": "compare-select int64"}
-BLOCK = 128
+BLOCK = 256
 
 
 def log(*a):
@@ -125,9 +125,7 @@ def cpu_baseline(h32: np.ndarray, budget_s: float = 12.0) -> dict:
     h64 = h32.astype(np.int64)
     h64[h32 == 0x3FFFFFFF] = orc.INF_RAW
     threads = orc.threads()
-    t = time.perf_counter()
-    orc.fw_classic(h64, k_end=2, nthreads=threads)
-    one = (time.perf_counter() - t) / 2
+    one = _cpu_step_time(orc, h64, threads)
     k_end = int(max(2, min(n, budget_s / max(one, 1e-6))))
     t = time.perf_counter()
     orc.fw_classic(h64, k_end=k_end, nthreads=threads)
@@ -136,6 +134,16 @@ def cpu_baseline(h32: np.ndarray, budget_s: float = 12.0) -> dict:
     return {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"oracle fw_classic (C/OpenMP int64, solvers.py:118-155) k-steps 0..{k_end} of n={n} "
                       f"({k_end}*n^2 updates, {dt:.1f}s); full solve extrapolates to {n ** 3 / rate:.0f}s"}
+
+
+def _cpu_step_time(orc, h64, threads) -> float:
+    """Seconds per k-step of the oracle FW (pred initialisation excluded)."""
+    t = time.perf_counter()
+    orc.fw_classic(h64, k_end=0, nthreads=threads)
+    t0 = time.perf_counter() - t
+    t = time.perf_counter()
+    orc.fw_classic(h64, k_end=4, nthreads=threads)
+    return max((time.perf_counter() - t - t0) / 4, 1e-6)
 
 
 def run_reference(args, ws, rank):
@@ -148,9 +156,7 @@ def run_reference(args, ws, rank):
     h64 = h.astype(np.int64)
     h64[h == 0x3FFFFFFF] = orc.INF_RAW
     threads = orc.threads()
-    t = time.perf_counter()
-    orc.fw_classic(h64, k_end=2, nthreads=threads)
-    one = (time.perf_counter() - t) / 2
+    one = _cpu_step_time(orc, h64, threads)
     k_end = int(max(2, min(n, args.ref_step_s / max(one, 1e-6))))
     for _ in range(args.warmup):
         orc.fw_classic(h64, k_end=k_end, nthreads=threads)
@@ -195,7 +201,7 @@ def main():
     ap_.add_argument("--no-cpu", action="store_true")
     ap_.add_argument("--no-e2e", action="store_true")
     ap_.add_argument("--ref-step-s", type=float, default=8.0)
-    ap_.add_argument("--block", type=int, default=BLOCK)
+    ap_.add_argument("--block", type=int, default=BLOCK, help="pivot block (128 or 256)")
     args = ap_.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":

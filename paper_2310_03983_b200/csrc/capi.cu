@@ -7,6 +7,7 @@
 #include <vector>
 #include "../../include/apsp_b200.h"
 #include "launch.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace apsp {
 const char* last_error();
@@ -210,7 +211,14 @@ size_t fw_scratch_bytes(int64_t m, int b, size_t es) {
 
 int fw_run(FwCtx& c, cudaStream_t s);
 
+// NVTX ranges name the phases for nsys/ncu (`ncu --nvtx --nvtx-include "apsp.fw.phase3/"`).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s) {
+  NvtxRange r("apsp.fw.phase1");
   c.launches++;
   if (c.b <= TILE_ALIGN)
     return launch_block_close(c.store, c.D, c.ld, k0, c.b, c.P, c.ldp, c.mode, c.via_off + k0, c.st, s);
@@ -229,6 +237,7 @@ int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s) {
 }
 
 int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
+  NvtxRange r("apsp.fw.phase2");
   const int64_t b = c.b, m = c.m;
   char* Dg = c.D + (k0 * c.ld + k0) * c.es;
   char* rowp = c.D + k0 * c.ld * c.es;
@@ -274,6 +283,7 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
 // additionally skips cross skip_next.
 int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaStream_t s) {
+  NvtxRange r(only_next >= 0 ? "apsp.fw.phase3a" : skip_next >= 0 ? "apsp.fw.phase3b" : "apsp.fw.phase3");
   MinplusArgs a = minplus_args();
   a.A = c.D + k0 * c.es; a.lda = c.ld;
   a.B = c.D + k0 * c.ld * c.es; a.ldb = c.ld;
@@ -415,7 +425,7 @@ size_t fw_ws_bytes(int dtype, int64_t n, int block) {
 int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
                     void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info) {
   if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
-  if (b <= 0) b = DEFAULT_BLOCK;
+  if (b <= 0) b = n >= 2048 ? 256 : DEFAULT_BLOCK;   // 256: half the phase-3 traffic and prologues
   if (b != 128 && b != 256) return set_error(APSP_EINVAL, "blocked FW supports block 128 or 256 (got %d)", b);
   const int64_t N = round_up(n, b);
   Scratch sc;
@@ -562,6 +572,7 @@ struct RK {
 
   int mp(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t r0, int64_t c0, int64_t m, int64_t n,
          int64_t k, const int32_t* predB, int64_t ldpb, int64_t inner_off) {
+    NvtxRange r("apsp.rkleene.product");
     MinplusArgs a = minplus_args();
     a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
     a.C = at(r0, c0); a.ldc = ld;
@@ -776,6 +787,7 @@ int squaring_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, in
       a.A = cur; a.lda = n; a.B = cur; a.ldb = n; a.C = nxt; a.ldc = n; a.idx = nxtP; a.ldi = n;
       a.predB = nullptr; a.ldp = n; a.m = n; a.n = n; a.k = n; a.inner_off = 0; a.mode = IDX_VIA;
         a.status = &hdr_dev->status;
+      a.track_changed = 1;
       rc = timed_minplus(store, a, s);
       if (!rc) rc = read_header(hdr_dev, hdr, s);
       if (rc) return rc;
@@ -974,7 +986,8 @@ int apsp_abi_version(void) { return APSP_ABI_VERSION; }
 
 size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block) {
   switch (algorithm) {
-    case APSP_ALG_FW_BLOCKED: return fw_ws_bytes(dtype, n, block > 0 ? block : DEFAULT_BLOCK);
+    case APSP_ALG_FW_BLOCKED: return std::max(fw_ws_bytes(dtype, n, block > 0 ? block : 256),
+                                              fw_ws_bytes(dtype, n, block > 0 ? block : DEFAULT_BLOCK));
     case APSP_ALG_RKLEENE: return std::max(rk_ws_bytes(dtype, n, 1), rk_ws_bytes(dtype, n, 0));
     case APSP_ALG_FW_SQUARING: return sq_ws_bytes(dtype, n);
     case APSP_ALG_FW_CLASSIC: return 0;

@@ -24,7 +24,8 @@ struct MinplusArgs {
   int64_t skip_col_lo, skip_col_hi;  // tiles entirely inside either band are skipped
   int64_t skip2_lo, skip2_hi;     // a second cross (rows and cols [lo,hi)) to skip (lookahead rest)
   int64_t only_lo, only_hi;       // if lo < hi: the grid enumerates only the tiles of this cross
-  Status* status;                 // optional: changed / overflow flags
+  Status* status;                 // optional: overflow flag (+ changed flag if track_changed)
+  int track_changed;              // set status->changed on any strict improvement (squaring)
 };
 
 // Default-initialised args: nothing skipped, full grid.

@@ -55,6 +55,14 @@ __device__ __forceinline__ void emit_idx(const MinplusArgs& p, int64_t i, int64_
   p.idx[i * p.ldi + j] = v;
 }
 
+// 0xFFFF in each 16-bit half whose bit 15 is set, else 0 (PTX prmt sign replication; the
+// CUDA __byte_perm intrinsic masks selectors to 3 bits and cannot express it).
+__device__ __forceinline__ uint32_t prmt_sign_halves(uint32_t x) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(x));
+  return d;
+}
+
 // ------------------------------------------------------------------------------------
 // narrow tier: uint8 store, packed 16-bit keys
 // ------------------------------------------------------------------------------------
@@ -156,7 +164,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       acc[r][q] = K16_INF * 0x00010001u;
-      kst[r][q] = 0xFFFFFFFFu;
+      kst[r][q] = 0u;
     }
 
   const bool abfast_base = ((reinterpret_cast<uintptr_t>(p.A) & 15) == 0) && ((p.lda & 15) == 0) &&
@@ -200,27 +208,25 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
         }
       }
     }
-    // decode tags of this chunk into k indices (relative to k = 0 of the product)
+    // decode tags of this chunk into 1-based k indices (0 = untouched), branch-free:
+    //   tg   = tags of the pair;  tg + 0x7FFF per half sets bit 15 iff the tag is nonzero
+    //   mask = PRMT sign-replication of bytes 1/3 -> 0xFFFF per half with a tag
+    //   kst  = mask ? (c*32 + tg) : kst          (one LOP3; no cross-half carry: all >= 0)
     uint32_t any = 0;
 #pragma unroll
     for (int r = 0; r < 8; r++)
 #pragma unroll
       for (int q = 0; q < 4; q++) any |= acc[r][q];
-    if (any & TAGMASK2) {
-      const uint32_t kb = uint32_t(c * SUB) - 1u;
+    if (__any_sync(0xffffffffu, any & TAGMASK2)) {
+      const uint32_t kb2 = uint32_t(c * SUB) * 0x00010001u;
 #pragma unroll
       for (int r = 0; r < 8; r++)
 #pragma unroll
         for (int q = 0; q < 4; q++) {
           const uint32_t tg = acc[r][q] & TAGMASK2;
-          if (tg) {
-            acc[r][q] ^= tg;
-            const uint32_t lo = tg & 0xFFFF, hi = tg >> 16;
-            uint32_t ks = kst[r][q];
-            if (lo) ks = (ks & 0xFFFF0000u) | ((kb + lo) & 0xFFFF);
-            if (hi) ks = (ks & 0x0000FFFFu) | ((kb + hi) << 16);
-            kst[r][q] = ks;
-          }
+          const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
+          kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
+          acc[r][q] ^= tg;
         }
     }
     if (more) u8_store_chunk(sm, buf ^ 1, ra, rb);
@@ -236,7 +242,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
-      if ((k0 & k1) == 0xFFFFFFFFu) continue;
+      if ((k0 | k1) == 0u) continue;
       changed = true;
       const int64_t j = j0 + 64 * h + 4 * tx;
       const uint32_t w = __byte_perm(acc[r][2 * h] >> TAG_BITS, acc[r][2 * h + 1] >> TAG_BITS, 0x6420);
@@ -251,11 +257,11 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
         const uint32_t ks[4] = {k0 & 0xFFFF, k0 >> 16, k1 & 0xFFFF, k1 >> 16};
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          if (ks[q] != KNONE && j + q < p.n) emit_idx(p, i, j + q, ks[q]);
+          if (ks[q] != 0u && j + q < p.n) emit_idx(p, i, j + q, ks[q] - 1u);
       }
     }
   }
-  if (p.status && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
 }
 
 // ------------------------------------------------------------------------------------
@@ -437,7 +443,7 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32_kernel(MinplusArgs p) {
       }
     }
   }
-  if (p.status && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
 }
 
 // ------------------------------------------------------------------------------------
@@ -515,7 +521,7 @@ __global__ void __launch_bounds__(NT) minplus_exact_kernel(MinplusArgs p) {
     }
   if (p.status) {
     if (overflow) p.status->overflow = 1;
-    if (__syncthreads_or(changed) && t == 0) p.status->changed = 1;
+    if (p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
   }
 }
 
