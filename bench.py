@@ -202,11 +202,12 @@ def main():
     ap_.add_argument("--no-e2e", action="store_true")
     ap_.add_argument("--ref-step-s", type=float, default=8.0)
     ap_.add_argument("--block", type=int, default=BLOCK, help="pivot block (128 or 256)")
+    ap_.add_argument("--sharded", action="store_true", help="use the multi-GPU row-band path even at N=1")
     args = ap_.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, ws, rank)
-    if ws > 1:
+    if ws > 1 or args.sharded:
         from paper_2310_03983_b200 import distributed
 
         return distributed.bench_main(args, METRIC, UNIT, config, make_input, weak_n, ClockSampler)

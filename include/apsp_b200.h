@@ -125,6 +125,39 @@ int apsp_minplus(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
 int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* dist_out, void* idx_out, int idx_dtype,
                     int idx_mode, int block, int base_threshold, int aligned, int tier, int device, apsp_info* info);
 
+/* ---- building blocks: input scan and row-band shards of the blocked FW (multi-GPU) ----------
+ * The sharded solver (paper_2310_03983_b200.distributed) runs one process per GPU; rank r owns
+ * rows [row0, row0 + rows) of the N x N padded matrix (rows a multiple of block).  Per pivot
+ * block k0 the owner calls apsp_shard_pivot, broadcasts the b x N row panel (values + pred)
+ * with NCCL, and every rank calls apsp_shard_update with the received panel.  tier must be the
+ * same on all ranks (chosen from the all-reduced apsp_scan results). */
+typedef struct apsp_scan_result {
+  int32_t negative;      /* a finite cost < 0 (or NaN) */
+  int32_t diag_nonzero;  /* a diagonal cell != 0 */
+  int32_t non_integral;  /* fp32 input with a non-integral finite cost */
+  int32_t any_finite;
+  int64_t max_finite;    /* largest finite cost (integer view) */
+  float max_finite_f;    /* largest finite cost (fp32 input) */
+  int32_t zero_offdiag;  /* a zero-cost edge off the diagonal */
+} apsp_scan_result;
+
+/* diag_off: cell (i, i + diag_off) is diagonal (0 whole matrix, row0 for a shard, -1 none). Syncs. */
+int apsp_scan(int dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
+              apsp_scan_result* out, void* stream);
+size_t apsp_shard_scratch_bytes(int tier, int64_t N, int64_t rows, int block);
+int apsp_shard_prepare(int dtype, int tier, int64_t n, int64_t N, int64_t row0, int64_t rows, const void* h,
+                       int64_t ldh, void* D, int64_t ld, int32_t* P, int64_t ldp, void* stream);
+int apsp_shard_pivot(int tier, int64_t N, int block, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
+                     int64_t k0, void* scratch, size_t scratch_bytes, void* stream);
+int apsp_shard_update(int tier, int64_t N, int block, int64_t rows, void* D, int64_t ld, int32_t* P, int64_t ldp,
+                      const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0, int64_t lrow,
+                      void* scratch, size_t scratch_bytes, void* stream);
+/* Converts rows x n back to dtype (dist) and copies pred; *max_finite = largest finite local
+ * distance (for the cross-rank certificate), -1 if none.  Syncs. */
+int apsp_shard_finish(int tier, int dtype, int64_t rows, int64_t n, const void* D, int64_t ld, const int32_t* P,
+                      int64_t ldp, void* dist, int64_t ldd, int32_t* pred, int64_t ldpo, int64_t* max_finite,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

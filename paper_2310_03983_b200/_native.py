@@ -45,6 +45,12 @@ EXPORTED_SYMBOLS = (
     "apsp_fw_squaring",
     "apsp_minplus",
     "apsp_solve_host",
+    "apsp_scan",
+    "apsp_shard_scratch_bytes",
+    "apsp_shard_prepare",
+    "apsp_shard_pivot",
+    "apsp_shard_update",
+    "apsp_shard_finish",
 )
 
 
@@ -81,8 +87,21 @@ class ApspInfo(ctypes.Structure):
         }
 
 
+class ScanResult(ctypes.Structure):
+    _fields_ = [
+        ("negative", ctypes.c_int32),
+        ("diag_nonzero", ctypes.c_int32),
+        ("non_integral", ctypes.c_int32),
+        ("any_finite", ctypes.c_int32),
+        ("max_finite", ctypes.c_int64),
+        ("max_finite_f", ctypes.c_float),
+        ("zero_offdiag", ctypes.c_int32),
+    ]
+
+
 _i32, _i64, _vp, _sz = ctypes.c_int, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
 _info_p = ctypes.POINTER(ApspInfo)
+_scan_p = ctypes.POINTER(ScanResult)
 
 _SIGNATURES = {
     "apsp_last_error": (ctypes.c_char_p, []),
@@ -97,6 +116,14 @@ _SIGNATURES = {
                             _i64, _i64, _i64, _i32, _vp, _info_p]),
     "apsp_solve_host": (_i32, [_i32, _i32, _i64, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
                                _info_p]),
+    "apsp_scan": (_i32, [_i32, _vp, _i64, _i64, _i64, _i64, _scan_p, _vp]),
+    "apsp_shard_scratch_bytes": (_sz, [_i32, _i64, _i64, _i32]),
+    "apsp_shard_prepare": (_i32, [_i32, _i32, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "apsp_shard_pivot": (_i32, [_i32, _i64, _i32, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
+    "apsp_shard_update": (_i32, [_i32, _i64, _i32, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64,
+                                 _vp, _sz, _vp]),
+    "apsp_shard_finish": (_i32, [_i32, _i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
+                                 ctypes.POINTER(ctypes.c_int64), _vp]),
 }
 
 _lib = None

@@ -437,7 +437,7 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   char* scratch = D + size_t(N) * N * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 256;
   Header hdr{};
   Timer tm(s);
-  rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
+  rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
   if (!rc) rc = read_header(hdr_dev, hdr, s);
   if (rc) return rc;
   const ScanResult scan = hdr.scan;
@@ -518,7 +518,7 @@ int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   Header* hdr_dev = static_cast<Header*>(sc.base);
   Header hdr{};
   Timer tm(s);
-  rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
+  rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
   if (!rc) rc = read_header(hdr_dev, hdr, s);
   if (rc) return rc;
   const ScanResult scan = hdr.scan;
@@ -676,7 +676,7 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
   char* sV = p;
   Header hdr{};
   Timer tm(s);
-  rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
+  rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
   if (!rc) rc = read_header(hdr_dev, hdr, s);
   if (rc) return rc;
   const ScanResult scan = hdr.scan;
@@ -752,7 +752,7 @@ int squaring_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, in
   char* D1 = D0 + size_t(n) * n * esmax;
   Header hdr{};
   Timer tm(s);
-  rc = launch_scan(dtype, dist, ld, n, n, 1, &hdr_dev->scan, s);
+  rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
   if (!rc) rc = read_header(hdr_dev, hdr, s);
   if (rc) return rc;
   const ScanResult scan = hdr.scan;
@@ -847,16 +847,16 @@ int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
   Timer tm(s);
   // operand ranges: the tier must hold every partial sum x + y (and z)
   ScanResult sx{}, sy{}, sz{};
-  rc = launch_scan(dtype, x, ldx, n1, n2, 0, &hdr_dev->scan, s);
+  rc = launch_scan(dtype, x, ldx, n1, n2, -1, &hdr_dev->scan, s);
   if (!rc) rc = read_header(hdr_dev, hdr, s);
   if (rc) return rc;
   sx = hdr.scan;
-  rc = launch_scan(dtype, y, ldy, n2, n3, 0, &hdr_dev->scan, s);
+  rc = launch_scan(dtype, y, ldy, n2, n3, -1, &hdr_dev->scan, s);
   if (!rc) rc = read_header(hdr_dev, hdr, s);
   if (rc) return rc;
   sy = hdr.scan;
   if (accumulate) {
-    rc = launch_scan(dtype, z, ldz, n1, n3, 0, &hdr_dev->scan, s);
+    rc = launch_scan(dtype, z, ldz, n1, n3, -1, &hdr_dev->scan, s);
     if (!rc) rc = read_header(hdr_dev, hdr, s);
     if (rc) return rc;
     sz = hdr.scan;
@@ -977,11 +977,162 @@ int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows,
 }
 }  // namespace apsp
 
+// ---- row-band shards of a blocked FW (multi-GPU building blocks) ---------------------------
+//
+// Rank r owns rows [row0, row0 + R) of the padded N x N matrix (R a multiple of b).  Per
+// pivot block [k0, k0 + b) with owner o (local pivot rows [lrow, lrow + b) on o):
+//   owner:     shard_pivot  = phase 1 on the diagonal block + row panel <- Dg (x) row panel
+//   broadcast  row panel values (b x N) and pred (b x N) from o        (NCCL, caller)
+//   everyone:  shard_update = column panel <- colpanel (x) Dg; phase 3 on the local rows
+// The arithmetic is exactly the single-GPU schedule, so results are bit-identical to one GPU
+// at the same b.
+namespace {
+
+size_t shard_scratch_bytes(int64_t N, int64_t R, int b, size_t es) {
+  size_t v = size_t(b) * N * 4 + 256;                   // pred row-panel snapshot
+  if (b > TILE_ALIGN) v += size_t(b) * N * es + size_t(R) * b * es + 512;   // value snapshots
+  return v;
+}
+
+int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
+                     int64_t k0, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  const int store = tier_store(tier);
+  if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  const size_t es = store_elem_size(store);
+  if (scratch_bytes < shard_scratch_bytes(N, b, b, es)) return set_error(APSP_EINVAL, "shard scratch too small");
+  char* D = static_cast<char*>(Dv);
+  FwCtx c;
+  c.store = store; c.es = es;
+  c.D = D + (lrow * ld + k0) * es; c.ld = ld;
+  c.P = P ? P + lrow * ldp + k0 : nullptr; c.ldp = ldp;
+  c.m = b; c.b = b; c.mode = IDX_PRED; c.via_off = k0;
+  c.predsnap = static_cast<int32_t*>(scratch);
+  int rc = fw_phase1(c, 0, s);                           // diagonal block, classic order
+  if (rc) return rc;
+  char* rowp = D + lrow * ld * es;
+  const bool snap = b > TILE_ALIGN;
+  char* rowsnap = static_cast<char*>(scratch) + size_t(b) * N * 4 + 256;
+  if (P) APSP_CUDA_TRY(cudaMemcpy2DAsync(c.predsnap, size_t(N) * 4, P + lrow * ldp, size_t(ldp) * 4, size_t(N) * 4,
+                                         size_t(b), cudaMemcpyDeviceToDevice, s));
+  if (snap && (rc = launch_copy_block(store, rowp, ld, rowsnap, N, b, N, s))) return rc;
+  MinplusArgs a = minplus_args();
+  a.A = c.D; a.lda = ld;
+  a.B = snap ? rowsnap : rowp; a.ldb = snap ? N : ld;
+  a.C = rowp; a.ldc = ld;
+  a.idx = P ? P + lrow * ldp : nullptr; a.ldi = ldp;
+  a.predB = c.predsnap; a.ldp = N;
+  a.m = b; a.n = N; a.k = b; a.inner_off = k0; a.mode = IDX_PRED;
+  a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
+  return launch_minplus(store, a, s);
+}
+
+int shard_update_impl(int tier, int64_t N, int b, int64_t R, void* Dv, int64_t ld, int32_t* P, int64_t ldp,
+                      const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0, int64_t lrow,
+                      void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  const int store = tier_store(tier);
+  if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  const size_t es = store_elem_size(store);
+  if (scratch_bytes < shard_scratch_bytes(N, R, b, es)) return set_error(APSP_EINVAL, "shard scratch too small");
+  char* D = static_cast<char*>(Dv);
+  const char* pv = static_cast<const char*>(panel);
+  const bool snap = b > TILE_ALIGN;
+  char* colsnap = static_cast<char*>(scratch) + size_t(b) * N * 4 + 256 + size_t(b) * N * es + 256;
+  int rc = 0;
+  if (snap && (rc = launch_copy_block(store, D + k0 * es, ld, colsnap, b, R, b, s))) return rc;
+  // column panel of the local rows against the (received) closed diagonal block
+  MinplusArgs q = minplus_args();
+  q.A = snap ? colsnap : D + k0 * es; q.lda = snap ? b : ld;
+  q.B = pv + k0 * es; q.ldb = ldpv;
+  q.C = D + k0 * es; q.ldc = ld;
+  q.idx = P ? P + k0 : nullptr; q.ldi = ldp;
+  q.predB = ppanel ? ppanel + k0 : nullptr; q.ldp = ldpp;
+  q.m = R; q.n = b; q.k = b; q.inner_off = k0; q.mode = IDX_PRED;
+  if (lrow >= 0) { q.skip_row_lo = lrow; q.skip_row_hi = lrow + b; }
+  if ((rc = launch_minplus(store, q, s))) return rc;
+  // phase 3 of the local rows
+  MinplusArgs a = minplus_args();
+  a.A = D + k0 * es; a.lda = ld;
+  a.B = pv; a.ldb = ldpv;
+  a.C = D; a.ldc = ld;
+  a.idx = P; a.ldi = ldp;
+  a.predB = ppanel; a.ldp = ldpp;
+  a.m = R; a.n = N; a.k = b; a.inner_off = k0; a.mode = IDX_PRED;
+  if (lrow >= 0) { a.skip_row_lo = lrow; a.skip_row_hi = lrow + b; }
+  a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
+  return timed_minplus(store, a, s);
+}
+
+}  // namespace
+
 // =============================================================================================
 extern "C" {
 
 const char* apsp_last_error(void) { return apsp::last_error(); }
 void apsp_set_profiling(int on) { g_prof.on = on != 0; }
+
+int apsp_scan(int dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
+              apsp_scan_result* out, void* stream) {
+  static_assert(sizeof(apsp_scan_result) == sizeof(ScanResult), "scan result layout");
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch sc;
+  int rc = sc.acquire(nullptr, 0, sizeof(ScanResult), s);
+  if (rc) return rc;
+  rc = launch_scan(dtype, h, ld, rows, cols, diag_off, static_cast<ScanResult*>(sc.base), s);
+  if (rc) return rc;
+  APSP_CUDA_TRY(cudaMemcpyAsync(out, sc.base, sizeof(ScanResult), cudaMemcpyDeviceToHost, s));
+  APSP_CUDA_TRY(cudaStreamSynchronize(s));
+  return 0;
+}
+
+size_t apsp_shard_scratch_bytes(int tier, int64_t N, int64_t rows, int block) {
+  const int store = tier_store(tier);
+  return shard_scratch_bytes(N, rows, block, store < 0 ? 8 : store_elem_size(store));
+}
+
+int apsp_shard_prepare(int dtype, int tier, int64_t n, int64_t N, int64_t row0, int64_t rows, const void* h,
+                       int64_t ldh, void* D, int64_t ld, int32_t* P, int64_t ldp, void* stream) {
+  const int store = tier_store(tier);
+  if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  return launch_to_store_rows(dtype, h, ldh, n, store, D, ld, N, P, ldp, 1, row0, rows, (cudaStream_t)stream);
+}
+
+int apsp_shard_pivot(int tier, int64_t N, int block, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
+                     int64_t k0, void* scratch, size_t scratch_bytes, void* stream) {
+  return shard_pivot_impl(tier, N, block, D, ld, P, ldp, lrow, k0, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int apsp_shard_update(int tier, int64_t N, int block, int64_t rows, void* D, int64_t ld, int32_t* P, int64_t ldp,
+                      const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0, int64_t lrow,
+                      void* scratch, size_t scratch_bytes, void* stream) {
+  return shard_update_impl(tier, N, block, rows, D, ld, P, ldp, panel, ldpv, ppanel, ldpp, k0, lrow, scratch,
+                           scratch_bytes, (cudaStream_t)stream);
+}
+
+int apsp_shard_finish(int tier, int dtype, int64_t rows, int64_t n, const void* D, int64_t ld, const int32_t* P,
+                      int64_t ldp, void* dist, int64_t ldd, int32_t* pred, int64_t ldpo, int64_t* max_finite,
+                      void* stream) {
+  const int store = tier_store(tier);
+  if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  cudaStream_t s = (cudaStream_t)stream;
+  Scratch sc;
+  int rc = sc.acquire(nullptr, 0, sizeof(ScanResult), s);
+  if (rc) return rc;
+  ScanResult* r = static_cast<ScanResult*>(sc.base);
+  if (rows > 0) {
+    rc = launch_max_finite(store, D, ld, rows, n, r, s);
+    if (!rc && dist) rc = launch_from_store(store, D, ld, rows, n, dtype, dist, ldd, s);
+    if (!rc && pred && P) rc = launch_copy_idx(P, ldp, rows, n, APSP_DTYPE_I32, pred, ldpo, s);
+    if (rc) return rc;
+  } else {
+    APSP_CUDA_TRY(cudaMemsetAsync(r, 0, sizeof(ScanResult), s));
+  }
+  ScanResult h{};
+  APSP_CUDA_TRY(cudaMemcpyAsync(&h, r, sizeof(ScanResult), cudaMemcpyDeviceToHost, s));
+  APSP_CUDA_TRY(cudaStreamSynchronize(s));
+  if (max_finite) *max_finite = rows > 0 && h.max_finite >= 0 ? h.max_finite : -1;
+  return 0;
+}
+
 int apsp_abi_version(void) { return APSP_ABI_VERSION; }
 
 size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block) {

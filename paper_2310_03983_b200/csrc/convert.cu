@@ -29,7 +29,7 @@ __device__ __forceinline__ void warp_or(int32_t* dst, bool v) {
 }
 
 template <int D>
-__global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t rows, int64_t cols, int check_diag,
+__global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
                             ScanResult* out) {
   using T = typename Api<D>::T;
   bool neg = false, diag = false, nonint = false, anyfin = false, zero = false;
@@ -39,10 +39,11 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e / cols, j = e - i * cols;
     const T v = h[i * ld + j];
-    if (check_diag && i == j && v != T(0)) diag = true;
+    const bool on_diag = diag_off >= 0 && j == i + diag_off;
+    if (on_diag && v != T(0)) diag = true;
     if (!Api<D>::fin(v)) continue;
     anyfin = true;
-    if (v == T(0) && i != j) zero = true;
+    if (v == T(0) && !on_diag) zero = true;
     if constexpr (D == API_F32) {
       if (isnan(v) || v < 0.f) { neg = true; continue; }
       if (v != floorf(v)) nonint = true;
@@ -75,15 +76,15 @@ static unsigned grid_for(int64_t total) {
   return unsigned(g);
 }
 
-int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int check_diag,
+int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
                 ScanResult* out_dev, cudaStream_t s) {
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
   // max fields start at 0 after memset; negative sentinel not needed (values are >= 0)
   const unsigned g = grid_for(rows * cols);
   switch (in_dtype) {
-    case API_I32: scan_kernel<API_I32><<<g, 256, 0, s>>>((const int32_t*)h, ld, rows, cols, check_diag, out_dev); break;
-    case API_F32: scan_kernel<API_F32><<<g, 256, 0, s>>>((const float*)h, ld, rows, cols, check_diag, out_dev); break;
-    case API_I64: scan_kernel<API_I64><<<g, 256, 0, s>>>((const int64_t*)h, ld, rows, cols, check_diag, out_dev); break;
+    case API_I32: scan_kernel<API_I32><<<g, 256, 0, s>>>((const int32_t*)h, ld, rows, cols, diag_off, out_dev); break;
+    case API_F32: scan_kernel<API_F32><<<g, 256, 0, s>>>((const float*)h, ld, rows, cols, diag_off, out_dev); break;
+    case API_I64: scan_kernel<API_I64><<<g, 256, 0, s>>>((const int64_t*)h, ld, rows, cols, diag_off, out_dev); break;
     default: return set_error(2, "unknown dtype %d", in_dtype);
   }
   APSP_CUDA_TRY(cudaGetLastError());
@@ -91,54 +92,61 @@ int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t c
 }
 
 // ---- conversion into a padded store ------------------------------------------------
+// rows [row0, row0 + R) of the padded N x N matrix (R = N, row0 = 0 for a whole matrix)
 template <int D, int S>
 __global__ void to_store_kernel(const typename Api<D>::T* h, int64_t ldh, int64_t n, typename StoreT<S>::T* out,
-                                int64_t ld, int64_t N, int32_t* P, int64_t ldp, int pred_init) {
+                                int64_t ld, int64_t N, int32_t* P, int64_t ldp, int pred_init, int64_t row0,
+                                int64_t R) {
   using T = typename StoreT<S>::T;
-  const int64_t total = N * N;
+  const int64_t total = R * N;
   for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / N, j = e - i * N;
+    const int64_t il = e / N, j = e - il * N, i = row0 + il;
     T o;
     bool fin;
     if (i < n && j < n) {
-      const typename Api<D>::T v = h[i * ldh + j];
+      const typename Api<D>::T v = h[il * ldh + j];
       fin = Api<D>::fin(v);
       o = fin ? T(v) : store_inf<S>();
     } else {
       fin = (i == j);
       o = fin ? T(0) : store_inf<S>();
     }
-    out[i * ld + j] = o;
-    if (P) P[i * ldp + j] = (pred_init && fin && i != j && i < n && j < n) ? int32_t(i) : -1;
+    out[il * ld + j] = o;
+    if (P) P[il * ldp + j] = (pred_init && fin && i != j && i < n && j < n) ? int32_t(i) : -1;
   }
 }
 
 template <int D>
 static int to_store_d(const void* h, int64_t ldh, int64_t n, int store, void* Dp, int64_t ld, int64_t N, int32_t* P,
-                      int64_t ldp, int pred_init, cudaStream_t s) {
+                      int64_t ldp, int pred_init, int64_t row0, int64_t R, cudaStream_t s) {
   using TI = typename Api<D>::T;
-  const unsigned g = grid_for(N * N);
+  const unsigned g = grid_for(R * N);
   const TI* hh = static_cast<const TI*>(h);
   switch (store) {
-    case STORE_U8: to_store_kernel<D, STORE_U8><<<g, 256, 0, s>>>(hh, ldh, n, (uint8_t*)Dp, ld, N, P, ldp, pred_init); break;
-    case STORE_W32: to_store_kernel<D, STORE_W32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init); break;
-    case STORE_I32: to_store_kernel<D, STORE_I32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init); break;
-    case STORE_F32: to_store_kernel<D, STORE_F32><<<g, 256, 0, s>>>(hh, ldh, n, (float*)Dp, ld, N, P, ldp, pred_init); break;
-    case STORE_I64: to_store_kernel<D, STORE_I64><<<g, 256, 0, s>>>(hh, ldh, n, (int64_t*)Dp, ld, N, P, ldp, pred_init); break;
+    case STORE_U8: to_store_kernel<D, STORE_U8><<<g, 256, 0, s>>>(hh, ldh, n, (uint8_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
+    case STORE_W32: to_store_kernel<D, STORE_W32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
+    case STORE_I32: to_store_kernel<D, STORE_I32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
+    case STORE_F32: to_store_kernel<D, STORE_F32><<<g, 256, 0, s>>>(hh, ldh, n, (float*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
+    case STORE_I64: to_store_kernel<D, STORE_I64><<<g, 256, 0, s>>>(hh, ldh, n, (int64_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
     default: return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
-int launch_to_store(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D, int64_t ld, int64_t N,
-                    int32_t* P, int64_t ldp, int pred_init, cudaStream_t s) {
+int launch_to_store_rows(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D, int64_t ld,
+                         int64_t N, int32_t* P, int64_t ldp, int pred_init, int64_t row0, int64_t R, cudaStream_t s) {
   switch (in_dtype) {
-    case API_I32: return to_store_d<API_I32>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, s);
-    case API_F32: return to_store_d<API_F32>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, s);
-    case API_I64: return to_store_d<API_I64>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, s);
+    case API_I32: return to_store_d<API_I32>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, row0, R, s);
+    case API_F32: return to_store_d<API_F32>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, row0, R, s);
+    case API_I64: return to_store_d<API_I64>(h, ldh, n, store, D, ld, N, P, ldp, pred_init, row0, R, s);
   }
   return set_error(2, "unknown dtype %d", in_dtype);
+}
+
+int launch_to_store(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D, int64_t ld, int64_t N,
+                    int32_t* P, int64_t ldp, int pred_init, cudaStream_t s) {
+  return launch_to_store_rows(in_dtype, h, ldh, n, store, D, ld, N, P, ldp, pred_init, 0, N, s);
 }
 
 // ---- conversion back -----------------------------------------------------------------

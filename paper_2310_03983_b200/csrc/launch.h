@@ -76,13 +76,18 @@ struct ScanResult {
   float max_finite_f;      // fp32 domain
   int32_t zero_offdiag;    // a finite zero cost off the diagonal (zero-weight edge)
 };
+// diag_off: cell (i, i + diag_off) is a diagonal cell (0 for a whole matrix, row0 for a
+// row shard, -1: no diagonal check)
 int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t cols,
-                int check_diag, ScanResult* out_dev, cudaStream_t s);
+                int64_t diag_off, ScanResult* out_dev, cudaStream_t s);
 
 // API dtype <-> store conversion, with padding to N (pad vertices are isolated) and the
 // FW pred initialisation pred[i][j] = i where h[i][j] finite and i != j (solvers.py:135-137).
 int launch_to_store(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D,
                     int64_t ld, int64_t N, int32_t* P, int64_t ldp, int pred_init, cudaStream_t s);
+// the same for rows [row0, row0 + R) of the padded matrix (h holds those rows of the input)
+int launch_to_store_rows(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D, int64_t ld,
+                         int64_t N, int32_t* P, int64_t ldp, int pred_init, int64_t row0, int64_t R, cudaStream_t s);
 int launch_from_store(int store, const void* D, int64_t ld, int64_t rows, int64_t cols,
                       int out_dtype, void* out, int64_t ldo, cudaStream_t s);
 int launch_copy_idx(const int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int out_dtype,

@@ -1,0 +1,412 @@
+"""Multi-GPU blocked Floyd-Warshall: one process per GPU, 1D row bands, NCCL panel broadcast.
+
+SURVEY.md 8(e): FW shards naturally with one exchange step per pivot block.  Rank r owns rows
+[r*R, (r+1)*R) of the padded N x N matrix (R = N / world, a multiple of the pivot block b, so a
+pivot block never straddles ranks).  Per pivot block [k0, k0+b), owned by rank o:
+
+  1. o      apsp_shard_pivot: close the b x b diagonal block (classic order), then
+            row panel <- Dg (x) row panel                      (both on o's rows only)
+  2. all    broadcast the b x N row panel -- values and predecessors -- from o (NCCL over
+            NVLink/NVSwitch; ~b*N*(1+4) bytes per round)
+  3. all    apsp_shard_update: column panel <- colpanel (x) Dg (Dg = columns k0.. of the
+            received panel), then phase 3 on the local rows with the received panel as B
+
+A row-band layout needs one broadcast per round (the column panel is local to every rank);
+on NVSwitch every GPU has full bandwidth to every peer, so the 2D grid of the survey buys no
+bandwidth, only smaller messages.  The arithmetic is the single-GPU schedule exactly, so the
+distances are bit-identical to one GPU and the predecessors identical at the same b.
+
+The schedule is written once over abstract per-rank ``ops`` and a ``bcast`` hook:
+* ``CudaShardOps`` + ``TorchComm`` (NCCL, torchrun)      -- the product path;
+* ``CudaShardOps`` + in-process emulation of all ranks on one GPU (tests);
+* CPU ops in tests/ + ``TorchComm`` over gloo            -- the world_size-2 CPU tests.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import json
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as nat
+from .core import (
+    INF32,
+    INF_RAW,
+    ApspError,
+    CostRangeError,
+    MalformedGraphError,
+    NegativeWeightError,
+    ParameterError,
+)
+
+U8_LIMIT, W32_LIMIT = 254, (1 << 24) - 2
+TIER_LIMIT = {nat.TIER_U8: U8_LIMIT, nat.TIER_W32: W32_LIMIT, nat.TIER_I32: INF32 - 1,
+              nat.TIER_I64: (1 << 60) - 1}
+
+
+def round_up(v: int, m: int) -> int:
+    return (v + m - 1) // m * m
+
+
+def layout(n: int, world: int, block: int) -> tuple[int, int]:
+    """(N, R): padded order and rows per rank (R a multiple of block)."""
+    N = round_up(max(n, 1), block * world)
+    return N, N // world
+
+
+def pick_tiers(dtype_code: int, scan: dict) -> list[int]:
+    """Narrowest exact tier first (mirror of capi.cu pick_tiers)."""
+    integral = dtype_code != nat.DTYPE_F32 or not scan["non_integral"]
+    w = scan["max_finite"]
+    t = []
+    if integral and w <= U8_LIMIT:
+        t.append(nat.TIER_U8)
+    if integral and w <= W32_LIMIT:
+        t.append(nat.TIER_W32)
+    t.append({nat.DTYPE_F32: nat.TIER_F32, nat.DTYPE_I32: nat.TIER_I32}.get(dtype_code, nat.TIER_I64))
+    return t
+
+
+def merge_scans(scans: list[dict]) -> dict:
+    out = {k: 0 for k in ("negative", "diag_nonzero", "non_integral", "zero_offdiag")}
+    out["max_finite"] = -1
+    for s in scans:
+        for k in out:
+            out[k] = max(out[k], int(s[k]))
+    return out
+
+
+def check_scan(scan: dict) -> None:
+    if scan["negative"]:
+        raise NegativeWeightError("solver input contains a negative finite cost")
+    if scan["diag_nonzero"]:
+        raise MalformedGraphError("solver input must have a zero diagonal")
+    if scan["zero_offdiag"]:
+        raise ParameterError("zero-cost edges need the classic k order for predecessors; "
+                             "use fw_classic(method='classic') on one GPU")
+
+
+# ---- the schedule --------------------------------------------------------------------------
+
+@dataclass
+class RankState:
+    rank: int
+    row0: int
+    rows_valid: int
+    state: object = None
+
+
+def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, bcast, dtype_code: int,
+                 h_locals: list, tier_req: int | None = None, allreduce_max=None):
+    """Solve with the given local ranks; returns (tier, global max finite, per-rank outputs)."""
+    N, R = layout(n, world, block)
+    scan = merged_scan(ranks, ops, h_locals, n, allreduce_max)
+    tiers = [tier_req] if tier_req is not None else pick_tiers(dtype_code, scan)
+    for tier in tiers:
+        for rk, h in zip(ranks, h_locals):
+            rk.state = ops.alloc(tier, R, N)
+            ops.prepare(rk.state, h, n, rk.row0, dtype_code)
+        for k0 in range(0, N, block):
+            owner = k0 // R
+            lrow = k0 - owner * R
+            owner_panels = None
+            for rk in ranks:
+                if rk.rank == owner:
+                    owner_panels = ops.pivot(rk.state, lrow, k0)
+            panels = bcast(ranks, owner, owner_panels, ops)
+            for rk, (pv, pp) in zip(ranks, panels):
+                ops.update(rk.state, pv, pp, k0, lrow if rk.rank == owner else -1)
+        local_max = max(ops.max_finite(rk.state, rk.rows_valid, n) for rk in ranks)
+        gmax = allreduce_max(local_max) if allreduce_max else local_max
+        if tier == nat.TIER_F32:
+            return tier, gmax
+        if gmax < 0 or gmax + scan["max_finite"] <= TIER_LIMIT[tier]:
+            return tier, gmax
+    if dtype_code == nat.DTYPE_I32:
+        raise CostRangeError("shortest-path cost left the representable int32 range")
+    raise CostRangeError("no value tier could represent the result")
+
+
+def merged_scan(ranks, ops, h_locals, n, allreduce_max):
+    scans = [ops.scan(h, rk.row0, rk.rows_valid, n) for rk, h in zip(ranks, h_locals)]
+    scan = merge_scans(scans)
+    if allreduce_max is not None:
+        scan = {k: allreduce_max(v) for k, v in scan.items()}
+    check_scan(scan)
+    for rk in ranks:
+        rk.scan = scan
+    return scan
+
+
+# ---- CUDA shard ops --------------------------------------------------------------------------
+
+_TORCH_STORE = {nat.TIER_U8: "uint8", nat.TIER_W32: "int32", nat.TIER_I32: "int32", nat.TIER_F32: "float32",
+                nat.TIER_I64: "int64"}
+
+
+@dataclass
+class CudaShard:
+    tier: int
+    R: int
+    N: int
+    D: object
+    P: object
+    scratch: object
+    stream: object
+    pv: object = None      # receive buffers for the broadcast panel
+    pp: object = None
+
+
+class CudaShardOps:
+    """Per-rank device state and the C-ABI shard calls, on torch's current stream."""
+
+    def __init__(self, device, block: int):
+        import torch
+
+        self.torch = torch
+        self.device = torch.device(device)
+        self.block = block
+        self.lib = nat.load()
+
+    def _stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def scan(self, h, row0: int, rows_valid: int, n: int) -> dict:
+        r = nat.ScanResult()
+        if rows_valid > 0:
+            nat.check(self.lib.apsp_scan(_dtype_of(h), h.data_ptr(), n, rows_valid, n, row0, ctypes.byref(r),
+                                         self._stream()))
+        mx = int(r.max_finite) if r.any_finite else -1
+        return {"negative": r.negative, "diag_nonzero": r.diag_nonzero, "non_integral": r.non_integral,
+                "zero_offdiag": r.zero_offdiag, "max_finite": mx}
+
+    def alloc(self, tier: int, R: int, N: int) -> CudaShard:
+        t = self.torch
+        dt = getattr(t, _TORCH_STORE[tier])
+        sb = self.lib.apsp_shard_scratch_bytes(tier, N, R, self.block)
+        return CudaShard(tier, R, N, t.empty((R, N), dtype=dt, device=self.device),
+                         t.empty((R, N), dtype=t.int32, device=self.device),
+                         t.empty(sb, dtype=t.uint8, device=self.device), None,
+                         t.empty((self.block, N), dtype=dt, device=self.device),
+                         t.empty((self.block, N), dtype=t.int32, device=self.device))
+
+    def prepare(self, st: CudaShard, h, n: int, row0: int, dtype_code: int) -> None:
+        hp = h.data_ptr() if h is not None and h.numel() else None
+        nat.check(self.lib.apsp_shard_prepare(dtype_code, st.tier, n, st.N, row0, st.R, hp, n, st.D.data_ptr(),
+                                              st.N, st.P.data_ptr(), st.N, self._stream()))
+
+    def pivot(self, st: CudaShard, lrow: int, k0: int):
+        nat.check(self.lib.apsp_shard_pivot(st.tier, st.N, self.block, st.D.data_ptr(), st.N, st.P.data_ptr(), st.N,
+                                            lrow, k0, st.scratch.data_ptr(), st.scratch.numel(), self._stream()))
+        return st.D[lrow:lrow + self.block], st.P[lrow:lrow + self.block]
+
+    def recv_buffers(self, st: CudaShard):
+        return st.pv, st.pp
+
+    def update(self, st: CudaShard, pv, pp, k0: int, lrow: int) -> None:
+        nat.check(self.lib.apsp_shard_update(st.tier, st.N, self.block, st.R, st.D.data_ptr(), st.N,
+                                             st.P.data_ptr(), st.N, pv.data_ptr(), st.N, pp.data_ptr(), st.N, k0,
+                                             lrow, st.scratch.data_ptr(), st.scratch.numel(), self._stream()))
+
+    def max_finite(self, st: CudaShard, rows_valid: int, n: int) -> int:
+        mx = ctypes.c_int64(-1)
+        nat.check(self.lib.apsp_shard_finish(st.tier, nat.DTYPE_I32, rows_valid, n, st.D.data_ptr(), st.N,
+                                             None, st.N, None, n, None, n, ctypes.byref(mx), self._stream()))
+        return int(mx.value)
+
+    def finish(self, st: CudaShard, rows_valid: int, n: int, dtype_code: int, dist, pred) -> None:
+        mx = ctypes.c_int64(-1)
+        nat.check(self.lib.apsp_shard_finish(st.tier, dtype_code, rows_valid, n, st.D.data_ptr(), st.N,
+                                             st.P.data_ptr(), st.N, dist.data_ptr(), n, pred.data_ptr(), n,
+                                             ctypes.byref(mx), self._stream()))
+
+
+def _dtype_of(t) -> int:
+    s = str(t.dtype)
+    return {"torch.int32": nat.DTYPE_I32, "torch.float32": nat.DTYPE_F32, "torch.int64": nat.DTYPE_I64}[s]
+
+
+# ---- communicators ---------------------------------------------------------------------------
+
+class TorchComm:
+    """torch.distributed (NCCL on GPUs, gloo on CPU): this process is one rank."""
+
+    def __init__(self, device=None, group=None):
+        import torch
+        import torch.distributed as dist
+
+        self.torch, self.dist, self.group = torch, dist, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.device(device) if device is not None else torch.device("cpu")
+
+    def allreduce_max(self, v: int) -> int:
+        t = self.torch.tensor([int(v)], dtype=self.torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+    def bcast(self, ranks, owner: int, owner_panels, ops):
+        (rk,) = ranks
+        if rk.rank == owner:
+            pv, pp = owner_panels
+        else:
+            pv, pp = ops.recv_buffers(rk.state)
+        self.dist.broadcast(pv, src=owner, group=self.group)
+        self.dist.broadcast(pp, src=owner, group=self.group)
+        return [(pv, pp)]
+
+
+def emulated_bcast(ranks, owner: int, owner_panels, ops):
+    """All ranks in this process on one device: every rank reads the owner's panel directly."""
+    return [owner_panels for _ in ranks]
+
+
+# ---- public entry points ---------------------------------------------------------------------
+
+@dataclass
+class ShardedResult:
+    distances: object        # local rows [row0, row0 + rows_valid) x n (device tensor)
+    pred: object
+    row0: int
+    rows_valid: int
+    info: dict = field(default_factory=dict)
+
+
+def fw_blocked_sharded(h_local, n: int, *, comm: TorchComm, block: int = 256, tier=None, ops=None):
+    """SPMD entry: this rank's rows of the input (torch CUDA tensor, rows x n) -> its rows of
+    dist / pred.  Must be called by every rank of ``comm`` with the same n and block."""
+    import torch
+
+    world, rank = comm.world, comm.rank
+    N, R = layout(n, world, block)
+    row0 = rank * R
+    rows_valid = max(0, min(R, n - row0))
+    if h_local is not None and tuple(h_local.shape) != (rows_valid, n):
+        raise ParameterError(f"rank {rank} expects {rows_valid} x {n} input rows, got {tuple(h_local.shape)}")
+    ops = ops or CudaShardOps(h_local.device, block)
+    rs = RankState(rank, row0, rows_valid)
+    dtype_code = _dtype_of(h_local)
+    t0 = time.perf_counter()
+    tier, gmax = run_schedule([rs], world, n, block, ops, comm.bcast, dtype_code, [h_local],
+                              None if tier is None else tier, comm.allreduce_max)
+    dist = torch.empty((rows_valid, n), dtype=h_local.dtype, device=h_local.device)
+    pred = torch.empty((rows_valid, n), dtype=torch.int32, device=h_local.device)
+    if rows_valid:
+        ops.finish(rs.state, rows_valid, n, dtype_code, dist, pred)
+    return ShardedResult(dist, pred, row0, rows_valid,
+                         {"tier": nat.TIER_NAMES[tier], "max_finite": gmax, "world": world, "N": N, "R": R,
+                          "block": block, "host_s": time.perf_counter() - t0})
+
+
+def fw_blocked_emulated(h, world: int, *, block: int = 256, tier=None):
+    """All ``world`` ranks of the row-band schedule in this process on h's device (sequential;
+    no rank waits on another).  Returns full (dist, pred) tensors.  Used to test the sharded
+    path on one GPU."""
+    import torch
+
+    n = h.shape[0]
+    N, R = layout(n, world, block)
+    ops = CudaShardOps(h.device, block)
+    ranks, hs = [], []
+    for r in range(world):
+        row0 = r * R
+        rv = max(0, min(R, n - row0))
+        ranks.append(RankState(r, row0, rv))
+        hs.append(h[row0:row0 + rv].contiguous() if rv else h[:0])
+    tier_code, gmax = run_schedule(ranks, world, n, block, ops, emulated_bcast, _dtype_of(h), hs,
+                                   None if tier is None else tier, None)
+    dist = torch.empty_like(h)
+    pred = torch.empty((n, n), dtype=torch.int32, device=h.device)
+    for rk in ranks:
+        if rk.rows_valid:
+            ops.finish(rk.state, rk.rows_valid, n, _dtype_of(h), dist[rk.row0:rk.row0 + rk.rows_valid],
+                       pred[rk.row0:rk.row0 + rk.rows_valid])
+    return dist, pred, {"tier": nat.TIER_NAMES[tier_code], "max_finite": gmax}
+
+
+# ---- multi-GPU bench leg (torchrun) ----------------------------------------------------------
+
+def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
+    """bench.py --gpus N under torchrun: weak-scaled n, row bands, max-over-ranks device time."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = TorchComm(dev)
+    world, rank = comm.world, comm.rank
+    block = args.block
+    n = args.n or weak_n(world)
+    N, R = layout(n, world, block)
+    row0 = rank * R
+    rv = max(0, min(R, n - row0))
+    from .graphgen import GenParams, dense_costs
+
+    t = time.perf_counter()
+    h_np = dense_costs(GenParams(n, args.rho, 100, 7 + n), np.int32, rows=(row0, row0 + rv))
+    if rank == 0:
+        print(f"[bench] rank0 generated rows {row0}..{row0 + rv} of n={n} in {time.perf_counter() - t:.1f}s",
+              file=__import__("sys").stderr, flush=True)
+    h = torch.from_numpy(h_np).to(dev)
+    ops = CudaShardOps(dev, block)
+    lib = ops.lib
+
+    def step():
+        return fw_blocked_sharded(h, n, comm=comm, block=block, ops=ops)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        for _ in range(args.steps):
+            res = step()
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    value = n ** 3 * args.steps / (total_ms / 1e3)
+    # e2e: pinned host rows in, device solve, host rows out, all ranks
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.from_numpy(h_np).pin_memory()
+        dout = torch.empty_like(hin).pin_memory()
+        pout = torch.empty(hin.shape, dtype=torch.int32).pin_memory()
+        dist.barrier()
+        t = time.perf_counter()
+        for _ in range(args.steps):
+            hd = hin.to(dev, non_blocking=True)
+            r = fw_blocked_sharded(hd, n, comm=comm, block=block, ops=ops)
+            dout.copy_(r.distances, non_blocking=True)
+            pout.copy_(r.pred, non_blocking=True)
+            torch.cuda.synchronize()
+        dist.barrier()
+        dt = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=dev)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": n ** 3 * args.steps / float(dt.item()), "unit": unit,
+               "h2d_bytes_per_step": n * n * 4, "d2h_bytes_per_step": 2 * n * n * 4,
+               "api": "paper_2310_03983_b200.distributed.fw_blocked_sharded from pinned host rows"}
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": f"tier {res.info['tier']}; int32 in/out",
+                "data": "synthetic (reference generator, bit-identical to apsp.generate)",
+                "config": config(n, args.rho, world) | {"block": block, "rows_per_rank": R},
+                "clocks": clk.summary(), "gpu_launches": None, "e2e": e2e, "cpu_baseline": None,
+                "tier": res.info["tier"]}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()

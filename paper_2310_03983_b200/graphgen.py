@@ -119,13 +119,17 @@ class _LemireStream:
         return out
 
 
-def dense_costs(params: GenParams, dtype=np.int64, chunk_rows: int = 512) -> np.ndarray:
+def dense_costs(params: GenParams, dtype=np.int64, chunk_rows: int = 512,
+                rows: tuple[int, int] | None = None) -> np.ndarray:
     """Dense cost matrix of ``generate(params)`` (zero diagonal, Infinity elsewhere).
 
     dtype int64 -> INF_RAW, int32 -> INF32, float32 -> +inf.  Equal to
-    ``cost_matrix_from_graph(generate(params)).raw`` after sentinel mapping.
+    ``cost_matrix_from_graph(generate(params)).raw`` after sentinel mapping.  ``rows=(r0, r1)``
+    returns only those rows (a rank's row band): the uniform streams jump straight to row r0;
+    the weight stream is replayed up to r0 to count Lemire rejections exactly.
     """
     v, seed = params.v, params.seed
+    r_lo, r_hi = (0, v) if rows is None else (max(0, rows[0]), min(v, rows[1]))
     dtype = np.dtype(dtype)
     if dtype == np.int64:
         inf = INF_RAW
@@ -137,25 +141,32 @@ def dense_costs(params: GenParams, dtype=np.int64, chunk_rows: int = 512) -> np.
         inf = np.inf
     else:
         raise ParameterError(f"unsupported dtype {dtype}")
-    out = np.empty((v, v), dtype=dtype)
-    g_prob = np.random.Generator(_stream_at(seed, 0))
-    g_pres = np.random.Generator(_stream_at(seed, v * v))
+    out = np.empty((max(0, r_hi - r_lo), v), dtype=dtype)
+    if r_hi <= r_lo:
+        return out
+    g_prob = np.random.Generator(_stream_at(seed, r_lo * v))
+    g_pres = np.random.Generator(_stream_at(seed, v * v + r_lo * v))
     rng = params.alpha - 1
     lemire = None
     if 0 < rng < 0xFFFFFFFF:
         lemire = _LemireStream(_stream_at(seed, 2 * v * v), rng)
+        done = 0
+        while done < r_lo * v:                     # replay (rejections shift the stream)
+            step = min(r_lo * v - done, chunk_rows * v)
+            lemire.take(step)
+            done += step
     elif rng != 0:
         mask, weights = _monolithic_draws(params)   # 64-bit weight path: rare, do it whole
-        out[...] = np.where(mask, weights, inf).astype(dtype)
-        np.fill_diagonal(out, 0)
-        return out
-    for r0 in range(0, v, chunk_rows):
-        r1 = min(v, r0 + chunk_rows)
+        full = np.where(mask, weights, inf).astype(dtype)
+        np.fill_diagonal(full, 0)
+        return full[r_lo:r_hi].copy()
+    for r0 in range(r_lo, r_hi, chunk_rows):
+        r1 = min(r_hi, r0 + chunk_rows)
         prob = g_prob.random((r1 - r0, v))
         pres = g_pres.random((r1 - r0, v))
         w = (lemire.take((r1 - r0) * v).reshape(r1 - r0, v) + 1) if lemire else np.ones((r1 - r0, v), np.int64)
         mask = pres < np.clip(params.rho * prob, 0.0, 1.0)
-        block = out[r0:r1]
+        block = out[r0 - r_lo:r1 - r_lo]
         block[...] = inf
         block[mask] = w[mask].astype(dtype)
         idx = np.arange(r0, r1)

@@ -1,0 +1,97 @@
+"""World-size-2 tests of the multi-GPU row-band schedule over gloo on CPU.
+
+The schedule (ownership, panel broadcast, tier agreement, certificate) is the product code in
+paper_2310_03983_b200.distributed; the per-shard arithmetic is the exact CPU stand-in in
+tests/shard_ops_cpu.py.  Distances must equal the oracle bit-for-bit and the predecessors must
+pass the reconstruction certificate -- for every split of the rows across the two ranks.
+"""
+
+from __future__ import annotations
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import INF_RAW, random_graph_raw
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, h, block, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from shard_ops_cpu import CpuShardOps
+
+        from paper_2310_03983_b200 import _native as nat
+        from paper_2310_03983_b200.distributed import RankState, TorchComm, layout, run_schedule
+
+        n = h.shape[0]
+        comm = TorchComm(torch.device("cpu"))
+        N, R = layout(n, world, block)
+        row0 = rank * R
+        rv = max(0, min(R, n - row0))
+        hl = torch.from_numpy(h[row0:row0 + rv].copy())
+        ops = CpuShardOps(block)
+        rs = RankState(rank, row0, rv)
+        tier, gmax = run_schedule([rs], world, n, block, ops, comm.bcast, nat.DTYPE_I64, [hl], None,
+                                  comm.allreduce_max)
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), d=rs.state.D.numpy()[:rv, :n], p=rs.state.P.numpy()[:rv, :n],
+                 tier=tier, gmax=gmax)
+    finally:
+        dist.destroy_process_group()
+
+
+def _solve(h, world, block):
+    with tempfile.TemporaryDirectory() as td:
+        mp.spawn(_worker, args=(world, _free_port(), h, block, td), nprocs=world, join=True)
+        parts = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(world)]
+        d = np.concatenate([p["d"] for p in parts])
+        pr = np.concatenate([p["p"] for p in parts])
+        return d, pr, int(parts[0]["tier"]), [int(p["gmax"]) for p in parts]
+
+
+@pytest.mark.parametrize("n,block,density", [(200, 64, 0.05), (60, 64, 0.2), (256, 32, 0.02), (97, 16, 0.1)])
+def test_two_ranks_match_oracle(n, block, density):
+    from oracle import oracle as orc
+
+    import paper_2310_03983_b200 as ap
+
+    h = random_graph_raw(n, density, 100, seed=n + block)
+    want_d, _ = orc.fw_classic(h)
+    d, pred, tier, gmaxes = _solve(h, 2, block)
+    assert np.array_equal(d, want_d)
+    ok, why = ap.check_pred_tree(h, d, pred.astype(np.int64), INF_RAW)
+    assert ok, why
+    assert len(set(gmaxes)) == 1            # every rank agreed on the certificate input
+
+
+def test_layout_rows_are_block_multiples():
+    from paper_2310_03983_b200.distributed import layout
+
+    for n in (1, 60, 200, 16384, 32768, 20000):
+        for world in (1, 2, 4, 8):
+            for block in (128, 256):
+                N, R = layout(n, world, block)
+                assert N >= n and R * world == N and R % block == 0
+
+
+def test_tier_selection_mirrors_library():
+    from paper_2310_03983_b200 import _native as nat
+    from paper_2310_03983_b200.distributed import pick_tiers
+
+    base = {"non_integral": 0, "max_finite": 100}
+    assert pick_tiers(nat.DTYPE_I32, base) == [nat.TIER_U8, nat.TIER_W32, nat.TIER_I32]
+    assert pick_tiers(nat.DTYPE_I64, base | {"max_finite": 1 << 30}) == [nat.TIER_I64]
+    assert pick_tiers(nat.DTYPE_F32, base | {"non_integral": 1}) == [nat.TIER_F32]
