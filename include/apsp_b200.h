@@ -149,9 +149,13 @@ int apsp_shard_prepare(int dtype, int tier, int64_t n, int64_t N, int64_t row0, 
                        int64_t ldh, void* D, int64_t ld, int32_t* P, int64_t ldp, void* stream);
 int apsp_shard_pivot(int tier, int64_t N, int block, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
                      int64_t k0, void* scratch, size_t scratch_bytes, void* stream);
-int apsp_shard_update(int tier, int64_t N, int block, int64_t rows, void* D, int64_t ld, int32_t* P, int64_t ldp,
-                      const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0, int64_t lrow,
-                      void* scratch, size_t scratch_bytes, void* stream);
+/* Updates local rows [row_lo, row_hi) with the received panel; rows [skip_lo, skip_hi) (the
+ * caller's own pivot rows, -1 if none) are left alone. */
+int apsp_shard_update(int tier, int64_t N, int block, int64_t row_lo, int64_t row_hi, void* D, int64_t ld, int32_t* P,
+                      int64_t ldp, const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0,
+                      int64_t skip_lo, int64_t skip_hi, void* scratch, size_t scratch_bytes, void* stream);
+/* The library's high-priority side stream of the current device (lookahead pivots). */
+void* apsp_side_stream(void);
 /* Converts rows x n back to dtype (dist) and copies pred; *max_finite = largest finite local
  * distance (for the cross-rank certificate), -1 if none.  Syncs. */
 int apsp_shard_finish(int tier, int dtype, int64_t rows, int64_t n, const void* D, int64_t ld, const int32_t* P,

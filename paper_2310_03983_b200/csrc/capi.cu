@@ -1026,38 +1026,42 @@ int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* 
   return launch_minplus(store, a, s);
 }
 
-int shard_update_impl(int tier, int64_t N, int b, int64_t R, void* Dv, int64_t ld, int32_t* P, int64_t ldp,
-                      const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0, int64_t lrow,
-                      void* scratch, size_t scratch_bytes, cudaStream_t s) {
+int shard_update_impl(int tier, int64_t N, int b, int64_t row_lo, int64_t row_hi, void* Dv, int64_t ld, int32_t* P,
+                      int64_t ldp, const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0,
+                      int64_t skip_lo, int64_t skip_hi, void* scratch, size_t scratch_bytes, cudaStream_t s) {
   const int store = tier_store(tier);
   if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  const int64_t R = row_hi - row_lo;
+  if (R <= 0) return 0;
   const size_t es = store_elem_size(store);
   if (scratch_bytes < shard_scratch_bytes(N, R, b, es)) return set_error(APSP_EINVAL, "shard scratch too small");
-  char* D = static_cast<char*>(Dv);
+  char* D = static_cast<char*>(Dv) + row_lo * ld * es;      // the processed row range
+  int32_t* Pr = P ? P + row_lo * ldp : nullptr;
   const char* pv = static_cast<const char*>(panel);
   const bool snap = b > TILE_ALIGN;
+  const bool skip = skip_lo >= 0 && skip_hi > skip_lo;
   char* colsnap = static_cast<char*>(scratch) + size_t(b) * N * 4 + 256 + size_t(b) * N * es + 256;
   int rc = 0;
   if (snap && (rc = launch_copy_block(store, D + k0 * es, ld, colsnap, b, R, b, s))) return rc;
-  // column panel of the local rows against the (received) closed diagonal block
+  // column panel of the rows against the (received) closed diagonal block
   MinplusArgs q = minplus_args();
   q.A = snap ? colsnap : D + k0 * es; q.lda = snap ? b : ld;
   q.B = pv + k0 * es; q.ldb = ldpv;
   q.C = D + k0 * es; q.ldc = ld;
-  q.idx = P ? P + k0 : nullptr; q.ldi = ldp;
+  q.idx = Pr ? Pr + k0 : nullptr; q.ldi = ldp;
   q.predB = ppanel ? ppanel + k0 : nullptr; q.ldp = ldpp;
   q.m = R; q.n = b; q.k = b; q.inner_off = k0; q.mode = IDX_PRED;
-  if (lrow >= 0) { q.skip_row_lo = lrow; q.skip_row_hi = lrow + b; }
+  if (skip) { q.skip_row_lo = skip_lo - row_lo; q.skip_row_hi = skip_hi - row_lo; }
   if ((rc = launch_minplus(store, q, s))) return rc;
-  // phase 3 of the local rows
+  // phase 3 of the rows
   MinplusArgs a = minplus_args();
   a.A = D + k0 * es; a.lda = ld;
   a.B = pv; a.ldb = ldpv;
   a.C = D; a.ldc = ld;
-  a.idx = P; a.ldi = ldp;
+  a.idx = Pr; a.ldi = ldp;
   a.predB = ppanel; a.ldp = ldpp;
   a.m = R; a.n = N; a.k = b; a.inner_off = k0; a.mode = IDX_PRED;
-  if (lrow >= 0) { a.skip_row_lo = lrow; a.skip_row_hi = lrow + b; }
+  if (skip) { a.skip_row_lo = skip_lo - row_lo; a.skip_row_hi = skip_hi - row_lo; }
   a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
   return timed_minplus(store, a, s);
 }
@@ -1101,12 +1105,14 @@ int apsp_shard_pivot(int tier, int64_t N, int block, void* D, int64_t ld, int32_
   return shard_pivot_impl(tier, N, block, D, ld, P, ldp, lrow, k0, scratch, scratch_bytes, (cudaStream_t)stream);
 }
 
-int apsp_shard_update(int tier, int64_t N, int block, int64_t rows, void* D, int64_t ld, int32_t* P, int64_t ldp,
-                      const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0, int64_t lrow,
-                      void* scratch, size_t scratch_bytes, void* stream) {
-  return shard_update_impl(tier, N, block, rows, D, ld, P, ldp, panel, ldpv, ppanel, ldpp, k0, lrow, scratch,
-                           scratch_bytes, (cudaStream_t)stream);
+int apsp_shard_update(int tier, int64_t N, int block, int64_t row_lo, int64_t row_hi, void* D, int64_t ld, int32_t* P,
+                      int64_t ldp, const void* panel, int64_t ldpv, const int32_t* ppanel, int64_t ldpp, int64_t k0,
+                      int64_t skip_lo, int64_t skip_hi, void* scratch, size_t scratch_bytes, void* stream) {
+  return shard_update_impl(tier, N, block, row_lo, row_hi, D, ld, P, ldp, panel, ldpv, ppanel, ldpp, k0, skip_lo,
+                           skip_hi, scratch, scratch_bytes, (cudaStream_t)stream);
 }
+
+void* apsp_side_stream(void) { return side_stream(); }
 
 int apsp_shard_finish(int tier, int dtype, int64_t rows, int64_t n, const void* D, int64_t ld, const int32_t* P,
                       int64_t ldp, void* dist, int64_t ldd, int32_t* pred, int64_t ldpo, int64_t* max_finite,

@@ -99,9 +99,9 @@ class RankState:
     state: object = None
 
 
-def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, bcast, dtype_code: int,
+def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, comm, dtype_code: int,
                  h_locals: list, tier_req: int | None = None, allreduce_max=None):
-    """Solve with the given local ranks; returns (tier, global max finite, per-rank outputs)."""
+    """Solve with the given local ranks; returns (tier, global max finite)."""
     N, R = layout(n, world, block)
     scan = merged_scan(ranks, ops, h_locals, n, allreduce_max)
     tiers = [tier_req] if tier_req is not None else pick_tiers(dtype_code, scan)
@@ -109,16 +109,7 @@ def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, bc
         for rk, h in zip(ranks, h_locals):
             rk.state = ops.alloc(tier, R, N)
             ops.prepare(rk.state, h, n, rk.row0, dtype_code)
-        for k0 in range(0, N, block):
-            owner = k0 // R
-            lrow = k0 - owner * R
-            owner_panels = None
-            for rk in ranks:
-                if rk.rank == owner:
-                    owner_panels = ops.pivot(rk.state, lrow, k0)
-            panels = bcast(ranks, owner, owner_panels, ops)
-            for rk, (pv, pp) in zip(ranks, panels):
-                ops.update(rk.state, pv, pp, k0, lrow if rk.rank == owner else -1)
+        run_rounds(ranks, N, R, block, ops, comm)
         local_max = max(ops.max_finite(rk.state, rk.rows_valid, n) for rk in ranks)
         gmax = allreduce_max(local_max) if allreduce_max else local_max
         if tier == nat.TIER_F32:
@@ -128,6 +119,48 @@ def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, bc
     if dtype_code == nat.DTYPE_I32:
         raise CostRangeError("shortest-path cost left the representable int32 range")
     raise CostRangeError("no value tier could represent the result")
+
+
+def run_rounds(ranks: list[RankState], N: int, R: int, b: int, ops, comm) -> None:
+    """The pivot rounds with one-block lookahead.
+
+    Round K (pivot rows owned by o, local rows [lr, lr+b)):
+      * wait for panel K
+      * owner o' of block K+1: finish round K on its rows [lr', lr'+b) first, then run the
+        K+1 pivot on the high-priority side stream and start broadcasting panel K+1
+        (asynchronously, into the other receive slot)
+      * everyone: round K on all remaining local rows, concurrent with pivot / broadcast K+1
+    """
+    nblocks = N // b
+
+    def owner(k0):
+        o = k0 // R
+        return o, k0 - o * R
+
+    o, lr = owner(0)
+    panels = None
+    for rk in ranks:
+        if rk.rank == o:
+            panels = ops.pivot(rk.state, lr, 0, side=False)
+    handle = comm.bcast_start(ranks, o, panels, 0, ops)
+    for K in range(nblocks):
+        k0 = K * b
+        o, lr = owner(k0)
+        cur = comm.bcast_wait(handle, ranks, ops)
+        nxt = K + 1 < nblocks
+        o1, lr1 = owner(k0 + b) if nxt else (-1, -1)
+        if nxt:
+            nxt_panels = None
+            for rk, (pv, pp) in zip(ranks, cur):
+                if rk.rank == o1:
+                    ops.update(rk.state, pv, pp, k0, lr1, lr1 + b, -1, -1)
+                    nxt_panels = ops.pivot(rk.state, lr1, k0 + b, side=True)
+            handle = comm.bcast_start(ranks, o1, nxt_panels, (K + 1) % 2, ops)
+        for rk, (pv, pp) in zip(ranks, cur):
+            lo, hi = (lr, lr + b) if rk.rank == o else (-1, -1)
+            if rk.rank == o1:              # its K+1 pivot rows are done already (adjacent bands merge)
+                lo, hi = (lr1, lr1 + b) if lo < 0 else (min(lo, lr1), max(hi, lr1 + b))
+            ops.update(rk.state, pv, pp, k0, 0, R, lo, hi)
 
 
 def merged_scan(ranks, ops, h_locals, n, allreduce_max):
@@ -156,7 +189,7 @@ class CudaShard:
     P: object
     scratch: object
     stream: object
-    pv: object = None      # receive buffers for the broadcast panel
+    pv: object = None      # two receive slots for the broadcast panel (values, pred)
     pp: object = None
 
 
@@ -170,6 +203,7 @@ class CudaShardOps:
         self.device = torch.device(device)
         self.block = block
         self.lib = nat.load()
+        self.side = torch.cuda.Stream(self.device, priority=-100)   # lookahead pivots
 
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
@@ -189,27 +223,41 @@ class CudaShardOps:
         sb = self.lib.apsp_shard_scratch_bytes(tier, N, R, self.block)
         return CudaShard(tier, R, N, t.empty((R, N), dtype=dt, device=self.device),
                          t.empty((R, N), dtype=t.int32, device=self.device),
-                         t.empty(sb, dtype=t.uint8, device=self.device), None,
-                         t.empty((self.block, N), dtype=dt, device=self.device),
-                         t.empty((self.block, N), dtype=t.int32, device=self.device))
+                         t.empty(sb, dtype=t.uint8, device=self.device),
+                         t.empty(sb, dtype=t.uint8, device=self.device),      # side-stream scratch
+                         [t.empty((self.block, N), dtype=dt, device=self.device) for _ in range(2)],
+                         [t.empty((self.block, N), dtype=t.int32, device=self.device) for _ in range(2)])
 
     def prepare(self, st: CudaShard, h, n: int, row0: int, dtype_code: int) -> None:
         hp = h.data_ptr() if h is not None and h.numel() else None
         nat.check(self.lib.apsp_shard_prepare(dtype_code, st.tier, n, st.N, row0, st.R, hp, n, st.D.data_ptr(),
                                               st.N, st.P.data_ptr(), st.N, self._stream()))
 
-    def pivot(self, st: CudaShard, lrow: int, k0: int):
+    def pivot(self, st: CudaShard, lrow: int, k0: int, side: bool):
+        """Pivot of block k0 (its rows are local rows [lrow, lrow+b)); side=True runs it on the
+        high-priority side stream after the work already queued on the current stream."""
+        t = self.torch
+        if side:
+            self.side.wait_stream(t.cuda.current_stream(self.device))
+            stream, scratch = self.side, st.stream
+        else:
+            stream, scratch = t.cuda.current_stream(self.device), st.scratch
         nat.check(self.lib.apsp_shard_pivot(st.tier, st.N, self.block, st.D.data_ptr(), st.N, st.P.data_ptr(), st.N,
-                                            lrow, k0, st.scratch.data_ptr(), st.scratch.numel(), self._stream()))
-        return st.D[lrow:lrow + self.block], st.P[lrow:lrow + self.block]
+                                            lrow, k0, scratch.data_ptr(), scratch.numel(),
+                                            ctypes.c_void_p(stream.cuda_stream)))
+        return st.D[lrow:lrow + self.block], st.P[lrow:lrow + self.block], (stream if side else None)
 
-    def recv_buffers(self, st: CudaShard):
-        return st.pv, st.pp
+    def recv_buffers(self, st: CudaShard, slot: int):
+        return st.pv[slot], st.pp[slot]
 
-    def update(self, st: CudaShard, pv, pp, k0: int, lrow: int) -> None:
-        nat.check(self.lib.apsp_shard_update(st.tier, st.N, self.block, st.R, st.D.data_ptr(), st.N,
+    def join_side(self) -> None:
+        self.torch.cuda.current_stream(self.device).wait_stream(self.side)
+
+    def update(self, st: CudaShard, pv, pp, k0: int, row_lo: int, row_hi: int, skip_lo: int, skip_hi: int) -> None:
+        nat.check(self.lib.apsp_shard_update(st.tier, st.N, self.block, row_lo, row_hi, st.D.data_ptr(), st.N,
                                              st.P.data_ptr(), st.N, pv.data_ptr(), st.N, pp.data_ptr(), st.N, k0,
-                                             lrow, st.scratch.data_ptr(), st.scratch.numel(), self._stream()))
+                                             skip_lo, skip_hi, st.scratch.data_ptr(), st.scratch.numel(),
+                                             self._stream()))
 
     def max_finite(self, st: CudaShard, rows_valid: int, n: int) -> int:
         mx = ctypes.c_int64(-1)
@@ -248,20 +296,48 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return int(t.item())
 
-    def bcast(self, ranks, owner: int, owner_panels, ops):
+    def bcast_start(self, ranks, owner: int, owner_panels, slot: int, ops):
+        """Asynchronous broadcast of panel (values, pred) from owner into receive slot `slot`.
+        On the owner the collective is issued on the stream that produced the panel."""
         (rk,) = ranks
         if rk.rank == owner:
-            pv, pp = owner_panels
+            pv, pp, stream = owner_panels
         else:
-            pv, pp = ops.recv_buffers(rk.state)
-        self.dist.broadcast(pv, src=owner, group=self.group)
-        self.dist.broadcast(pp, src=owner, group=self.group)
-        return [(pv, pp)]
+            (pv, pp), stream = ops.recv_buffers(rk.state, slot), None
+        ctx = self.torch.cuda.stream(stream) if stream is not None else _null_ctx()
+        with ctx:
+            works = [self.dist.broadcast(pv, src=owner, group=self.group, async_op=True),
+                     self.dist.broadcast(pp, src=owner, group=self.group, async_op=True)]
+        return works, [(pv, pp)], rk.rank == owner
+
+    def bcast_wait(self, handle, ranks, ops):
+        works, panels, is_owner = handle
+        for w in works:
+            w.wait()
+        if is_owner and hasattr(ops, "join_side"):
+            ops.join_side()
+        return panels
 
 
-def emulated_bcast(ranks, owner: int, owner_panels, ops):
+class _null_ctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+class EmulatedComm:
     """All ranks in this process on one device: every rank reads the owner's panel directly."""
-    return [owner_panels for _ in ranks]
+
+    def bcast_start(self, ranks, owner: int, owner_panels, slot: int, ops):
+        pv, pp, _ = owner_panels
+        return [(pv, pp) for _ in ranks]
+
+    def bcast_wait(self, handle, ranks, ops):
+        if hasattr(ops, "join_side"):
+            ops.join_side()
+        return handle
 
 
 # ---- public entry points ---------------------------------------------------------------------
@@ -290,7 +366,7 @@ def fw_blocked_sharded(h_local, n: int, *, comm: TorchComm, block: int = 256, ti
     rs = RankState(rank, row0, rows_valid)
     dtype_code = _dtype_of(h_local)
     t0 = time.perf_counter()
-    tier, gmax = run_schedule([rs], world, n, block, ops, comm.bcast, dtype_code, [h_local],
+    tier, gmax = run_schedule([rs], world, n, block, ops, comm, dtype_code, [h_local],
                               None if tier is None else tier, comm.allreduce_max)
     dist = torch.empty((rows_valid, n), dtype=h_local.dtype, device=h_local.device)
     pred = torch.empty((rows_valid, n), dtype=torch.int32, device=h_local.device)
@@ -316,7 +392,7 @@ def fw_blocked_emulated(h, world: int, *, block: int = 256, tier=None):
         rv = max(0, min(R, n - row0))
         ranks.append(RankState(r, row0, rv))
         hs.append(h[row0:row0 + rv].contiguous() if rv else h[:0])
-    tier_code, gmax = run_schedule(ranks, world, n, block, ops, emulated_bcast, _dtype_of(h), hs,
+    tier_code, gmax = run_schedule(ranks, world, n, block, ops, EmulatedComm(), _dtype_of(h), hs,
                                    None if tier is None else tier, None)
     dist = torch.empty_like(h)
     pred = torch.empty((n, n), dtype=torch.int32, device=h.device)

@@ -19,8 +19,8 @@ class CpuShard:
     N: int
     D: torch.Tensor
     P: torch.Tensor
-    pv: torch.Tensor
-    pp: torch.Tensor
+    pv: list
+    pp: list
 
 
 class CpuShardOps:
@@ -41,7 +41,8 @@ class CpuShardOps:
         b = self.block
         return CpuShard(tier, R, N, torch.full((R, N), INF_RAW, dtype=torch.int64),
                         torch.full((R, N), -1, dtype=torch.int32),
-                        torch.empty((b, N), dtype=torch.int64), torch.empty((b, N), dtype=torch.int32))
+                        [torch.empty((b, N), dtype=torch.int64) for _ in range(2)],
+                        [torch.empty((b, N), dtype=torch.int32) for _ in range(2)])
 
     def prepare(self, st, h, n, row0, dtype_code):
         D, P = st.D.numpy(), st.P.numpy()
@@ -72,7 +73,7 @@ class CpuShardOps:
         C[imp] = best[imp]
         PC[imp] = newp[imp]
 
-    def pivot(self, st, lrow, k0):
+    def pivot(self, st, lrow, k0, side=False):
         b = self.block
         D, P = st.D.numpy(), st.P.numpy()
         G = D[lrow:lrow + b, k0:k0 + b]
@@ -85,16 +86,16 @@ class CpuShardOps:
         T = D[lrow:lrow + b]
         snap = P[lrow:lrow + b].copy()
         self._product(T, P[lrow:lrow + b], G.copy(), T.copy(), snap, skip_cols=(k0, k0 + b))
-        return st.D[lrow:lrow + b], st.P[lrow:lrow + b]
+        return st.D[lrow:lrow + b], st.P[lrow:lrow + b], None
 
-    def recv_buffers(self, st):
-        return st.pv, st.pp
+    def recv_buffers(self, st, slot):
+        return st.pv[slot], st.pp[slot]
 
-    def update(self, st, pv, pp, k0, lrow):
+    def update(self, st, pv, pp, k0, row_lo, row_hi, skip_lo, skip_hi):
         b = self.block
-        D, P = st.D.numpy(), st.P.numpy()
+        D, P = st.D.numpy()[row_lo:row_hi], st.P.numpy()[row_lo:row_hi]
         pvn, ppn = pv.numpy(), pp.numpy()
-        skip = (lrow, lrow + b) if lrow >= 0 else None
+        skip = (skip_lo - row_lo, skip_hi - row_lo) if skip_lo >= 0 else None
         self._product(D[:, k0:k0 + b], P[:, k0:k0 + b], D[:, k0:k0 + b].copy(), pvn[:, k0:k0 + b],
                       ppn[:, k0:k0 + b], skip_rows=skip)
         self._product(D, P, D[:, k0:k0 + b].copy(), pvn, ppn, skip_rows=skip, skip_cols=(k0, k0 + b))

@@ -45,7 +45,7 @@ def _worker(rank, world, port, h, block, out_dir):
         hl = torch.from_numpy(h[row0:row0 + rv].copy())
         ops = CpuShardOps(block)
         rs = RankState(rank, row0, rv)
-        tier, gmax = run_schedule([rs], world, n, block, ops, comm.bcast, nat.DTYPE_I64, [hl], None,
+        tier, gmax = run_schedule([rs], world, n, block, ops, comm, nat.DTYPE_I64, [hl], None,
                                   comm.allreduce_max)
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), d=rs.state.D.numpy()[:rv, :n], p=rs.state.P.numpy()[:rv, :n],
                  tier=tier, gmax=gmax)
@@ -62,7 +62,8 @@ def _solve(h, world, block):
         return d, pr, int(parts[0]["tier"]), [int(p["gmax"]) for p in parts]
 
 
-@pytest.mark.parametrize("n,block,density", [(200, 64, 0.05), (60, 64, 0.2), (256, 32, 0.02), (97, 16, 0.1)])
+@pytest.mark.parametrize("n,block,density", [(200, 64, 0.05), (60, 64, 0.2), (256, 32, 0.02), (97, 16, 0.1),
+                                             (130, 16, 0.03)])
 def test_two_ranks_match_oracle(n, block, density):
     from oracle import oracle as orc
 
