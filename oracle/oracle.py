@@ -40,6 +40,7 @@ def _load():
         i64, p, i = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
         lib.oracle_fw_classic.argtypes = [i64, p, p, i64, i]
         lib.oracle_fw_via_block.argtypes = [i64, p, p, i64, i64]
+        lib.oracle_fw_steps.argtypes = [i64, p, p, i64, i64, i]
         lib.oracle_product.argtypes = [i64, i64, i64, p, i64, p, i64, p, p, i64, i64, i64, i64]
         lib.oracle_accumulate.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64, p, i64, p, p, i64, i64]
         lib.oracle_rkleene.argtypes = [i64, p, p, i64, i]
@@ -70,6 +71,12 @@ def fw_classic(h, k_end: int = -1, nthreads: int | None = None):
     pred = np.empty_like(d)
     _check(_load().oracle_fw_classic(n, d.ctypes.data, pred.ctypes.data, k_end, nthreads or threads()))
     return d, pred
+
+
+def fw_steps(d: np.ndarray, pred: np.ndarray, k0: int, k1: int, nthreads: int | None = None) -> None:
+    """In place: steps [k0, k1) of fw_classic on an initialised (d, pred) state."""
+    assert d.dtype == np.int64 and pred.dtype == np.int64 and d.flags.c_contiguous and pred.flags.c_contiguous
+    _check(_load().oracle_fw_steps(d.shape[0], d.ctypes.data, pred.ctypes.data, k0, k1, nthreads or threads()))
 
 
 def rkleene(h, base_threshold: int = 64, nthreads: int | None = None):
@@ -116,5 +123,5 @@ def accumulate(z, x, y, via=None, inner_offset: int = 0):
     return d, v
 
 
-__all__ = ["INF_RAW", "OracleRangeError", "accumulate", "build", "fw_classic", "fw_squaring", "product",
+__all__ = ["INF_RAW", "OracleRangeError", "accumulate", "build", "fw_classic", "fw_squaring", "fw_steps", "product",
            "rkleene", "threads"]
