@@ -425,7 +425,7 @@ size_t fw_ws_bytes(int dtype, int64_t n, int block) {
 int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
                     void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info) {
   if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
-  if (b <= 0) b = n >= 2048 ? 256 : DEFAULT_BLOCK;   // 256: half the phase-3 traffic and prologues
+  if (b <= 0) b = n > 6144 ? 256 : DEFAULT_BLOCK;   // 256 halves phase-3 traffic/prologues; 128 keeps phase 1 short
   if (b != 128 && b != 256) return set_error(APSP_EINVAL, "blocked FW supports block 128 or 256 (got %d)", b);
   const int64_t N = round_up(n, b);
   Scratch sc;

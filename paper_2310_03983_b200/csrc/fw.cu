@@ -69,41 +69,97 @@ int launch_fw_step(int store, void* D, int64_t ld, int64_t n, int64_t k, int32_t
 // ------------------------------------------------------------------------------------
 constexpr int MAXB = 128;
 
+// Register-resident closure: 512 threads, thread (ty, tx) of 16x32 owns cells i = ty + 16a
+// (a < 8), j = tx + 32c (c < 4).  Step k: the owners of row k / column k have published them
+// into a double-buffered smem row/column (values, and pred for row k); one barrier; every
+// thread relaxes its 32 cells; the owners of row / column k+1 publish them right away.
+constexpr int CR = 8, CC = 4;
 template <int S>
-__global__ void __launch_bounds__(1024) block_close_kernel(typename StoreT<S>::T* D, int64_t ld, int64_t lo, int m,
-                                                           int32_t* idx, int64_t ldi, int mode, int64_t via_off,
-                                                           Status* st) {
+__global__ void __launch_bounds__(512) block_close_kernel(typename StoreT<S>::T* D, int64_t ld, int64_t lo, int m,
+                                                          int32_t* idx, int64_t ldi, int mode, int64_t via_off,
+                                                          Status* st) {
   using T = typename StoreT<S>::T;
   using A = typename StoreT<S>::A;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  A* V = reinterpret_cast<A*>(smraw);                        // m x m
-  int32_t* I = reinterpret_cast<int32_t*>(V + m * m);        // m x m
+  __shared__ A rowk[2][MAXB];
+  __shared__ A colk[2][MAXB];
+  __shared__ int32_t prowk[2][MAXB];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int i = ty; i < m; i += 32)
-    for (int j = tx; j < m; j += 32) {
-      V[i * m + j] = A(D[(lo + i) * ld + lo + j]);
-      I[i * m + j] = idx ? idx[(lo + i) * ldi + lo + j] : -1;
+  const A inf = A(store_inf<S>());
+  A v[CR][CC];
+  int32_t p[CR][CC];
+#pragma unroll
+  for (int a = 0; a < CR; a++)
+#pragma unroll
+    for (int c = 0; c < CC; c++) {
+      const int i = ty + 16 * a, j = tx + 32 * c;
+      const bool in = i < m && j < m;
+      v[a][c] = in ? A(D[(lo + i) * ld + lo + j]) : inf;
+      p[a][c] = (in && idx) ? idx[(lo + i) * ldi + lo + j] : -1;
     }
+// publish row / column KK of the register tile (select chains: no dynamic register indexing)
+#define APSP_PUBLISH(KK, BUF)                                        \
+  do {                                                               \
+    const int pk_ = (KK), pb_ = (BUF);                               \
+    if (ty == (pk_ & 15)) {                                          \
+      const int sa_ = pk_ >> 4;                                      \
+      _Pragma("unroll") for (int c = 0; c < CC; c++) {               \
+        A rv_ = v[0][c];                                             \
+        int32_t rp_ = p[0][c];                                       \
+        _Pragma("unroll") for (int a = 1; a < CR; a++) {             \
+          rv_ = (a == sa_) ? v[a][c] : rv_;                          \
+          rp_ = (a == sa_) ? p[a][c] : rp_;                          \
+        }                                                            \
+        rowk[pb_][tx + 32 * c] = rv_;                                \
+        prowk[pb_][tx + 32 * c] = rp_;                               \
+      }                                                              \
+    }                                                                \
+    if (tx == (pk_ & 31)) {                                          \
+      const int sc_ = pk_ >> 5;                                      \
+      _Pragma("unroll") for (int a = 0; a < CR; a++) {               \
+        A cv_ = v[a][0];                                             \
+        _Pragma("unroll") for (int c = 1; c < CC; c++)               \
+          cv_ = (c == sc_) ? v[a][c] : cv_;                          \
+        colk[pb_][ty + 16 * a] = cv_;                                \
+      }                                                              \
+    }                                                                \
+  } while (0)
+  APSP_PUBLISH(0, 0);
   bool overflow = false;
   for (int k = 0; k < m; k++) {
     __syncthreads();
-    for (int i = ty; i < m; i += 32) {
-      const A dik = V[i * m + k];
-      for (int j = tx; j < m; j += 32) {
-        const A c = dik + V[k * m + j];
-        if (c < V[i * m + j]) {
-          overflow |= range_overflow<S>(c);
-          V[i * m + j] = c;
-          I[i * m + j] = (mode == IDX_PRED) ? I[k * m + j] : int32_t(via_off + k);
+    const int b = k & 1;
+    A dkj[CC], dik[CR];
+    int32_t pkj[CC];
+#pragma unroll
+    for (int c = 0; c < CC; c++) {
+      dkj[c] = rowk[b][tx + 32 * c];
+      pkj[c] = prowk[b][tx + 32 * c];
+    }
+#pragma unroll
+    for (int a = 0; a < CR; a++) dik[a] = colk[b][ty + 16 * a];
+    const int32_t vk = int32_t(via_off + k);
+#pragma unroll
+    for (int a = 0; a < CR; a++)
+#pragma unroll
+      for (int c = 0; c < CC; c++) {
+        const A cand = dik[a] + dkj[c];
+        if (cand < v[a][c]) {
+          overflow |= range_overflow<S>(cand);
+          v[a][c] = cand;
+          p[a][c] = (mode == IDX_PRED) ? pkj[c] : vk;
         }
       }
-    }
+    if (k + 1 < m) APSP_PUBLISH(k + 1, b ^ 1);
   }
-  __syncthreads();
-  for (int i = ty; i < m; i += 32)
-    for (int j = tx; j < m; j += 32) {
-      D[(lo + i) * ld + lo + j] = T(V[i * m + j]);
-      if (idx) idx[(lo + i) * ldi + lo + j] = I[i * m + j];
+#pragma unroll
+  for (int a = 0; a < CR; a++)
+#pragma unroll
+    for (int c = 0; c < CC; c++) {
+      const int i = ty + 16 * a, j = tx + 32 * c;
+      if (i < m && j < m) {
+        D[(lo + i) * ld + lo + j] = T(v[a][c]);
+        if (idx) idx[(lo + i) * ldi + lo + j] = p[a][c];
+      }
     }
   if (st && overflow) st->overflow = 1;
 }
@@ -111,16 +167,8 @@ __global__ void __launch_bounds__(1024) block_close_kernel(typename StoreT<S>::T
 template <int S>
 static int close_impl(void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi, int mode,
                       int64_t via_off, Status* st, cudaStream_t s) {
-  using A = typename StoreT<S>::A;
-  const size_t smem = size_t(m) * m * (sizeof(A) + sizeof(int32_t));
-  static bool attr = false;
-  if (!attr) {
-    APSP_CUDA_TRY(cudaFuncSetAttribute(block_close_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(MAXB * MAXB * (sizeof(A) + sizeof(int32_t)))));
-    attr = true;
-  }
-  block_close_kernel<S><<<1, 1024, smem, s>>>(static_cast<typename StoreT<S>::T*>(D), ld, lo, int(m), idx, ldi, mode,
-                                              via_off, st);
+  block_close_kernel<S><<<1, 512, 0, s>>>(static_cast<typename StoreT<S>::T*>(D), ld, lo, int(m), idx, ldi, mode,
+                                           via_off, st);
   APSP_CUDA_TRY(cudaGetLastError());
   return 0;
 }

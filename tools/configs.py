@@ -1,0 +1,115 @@
+#!/usr/bin/env python3
+"""Measure the BASELINE.json configs other than the headline (bench.py) on one B200.
+
+C1  FW n=256 generator (rho 0.1) int32, dist+pred, parity with the oracle
+C2  blocked FW n=4096 rho=1.0 as fp32 (integral -> u8 tier) + a continuous-weight fp32 variant
+C3  R-Kleene n=8192 rho=1.0 fp32, semiring-GEMM recursion (aligned split, pred)
+C5  density/scale sweep n in {1024..16384} x rho in {0.002,0.01,0.1,0.5,1.0}: FW vs R-Kleene
+
+Times are CUDA-event device times of the solve with the input resident (median of --reps after
+one warm-up).  Writes a markdown table and a JSON file.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_2310_03983_b200 as ap  # noqa: E402
+
+
+def timed(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return statistics.median(ts), out
+
+
+def gen(n, rho, dtype):
+    return torch.from_numpy(ap.dense_costs(ap.GenParams(n, rho, 100, 7 + n), dtype)).cuda()
+
+
+def row(rows, name, n, rho, alg, ms, info, extra=""):
+    rate = n ** 3 / (ms / 1e3)
+    rows.append({"config": name, "n": n, "rho": rho, "alg": alg, "ms": ms, "upd_per_s": rate,
+                 "tier": info.get("tier"), "extra": extra})
+    print(f"{name:4s} n={n:6d} rho={rho:<6} {alg:28s} {ms:10.2f} ms {rate / 1e12:7.2f} T upd/s "
+          f"tier={info.get('tier')} {extra}", flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--reps", type=int, default=3)
+    p.add_argument("--sweep-max", type=int, default=16384)
+    p.add_argument("--out", default=str(ROOT / "gpurun_out" / "configs.json"))
+    a = p.parse_args()
+    rows = []
+    # C1
+    from oracle import oracle as orc
+
+    h = gen(256, 0.1, np.int32)
+    ms, r = timed(lambda: ap.solve(h, "fw_blocked"), a.reps)
+    h64 = h.cpu().numpy().astype(np.int64)
+    h64[h64 == ap.INF32] = ap.INF_RAW
+    want, _ = orc.fw_classic(h64)
+    d = r.distances.cpu().numpy().astype(np.int64)
+    d[d == ap.INF32] = ap.INF_RAW
+    row(rows, "C1", 256, 0.1, "fw_blocked", ms, r.info, f"bitwise_vs_oracle={np.array_equal(d, want)}")
+    ms, r = timed(lambda: ap.solve(h, "fw_classic"), a.reps)
+    row(rows, "C1", 256, 0.1, "fw_classic (K1)", ms, r.info)
+    # C2
+    h = gen(4096, 1.0, np.float32)
+    ms, r = timed(lambda: ap.solve(h, "fw_blocked"), a.reps)
+    row(rows, "C2", 4096, 1.0, "fw_blocked fp32 (integral)", ms, r.info)
+    rng = np.random.default_rng(4096)
+    hc = h.cpu().numpy().copy()
+    fin = np.isfinite(hc) & (hc > 0)
+    hc[fin] = rng.uniform(1.0, 100.0, size=int(fin.sum())).astype(np.float32)
+    hc = torch.from_numpy(hc).cuda()
+    ms, r = timed(lambda: ap.solve(hc, "fw_blocked"), a.reps)
+    row(rows, "C2", 4096, 1.0, "fw_blocked fp32 continuous", ms, r.info)
+    ms, r = timed(lambda: ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=1024), a.reps)
+    row(rows, "C2", 4096, 1.0, "rkleene fp32 (aligned, pred)", ms, r.info)
+    # C3
+    h = gen(8192, 1.0, np.float32)
+    for thr in (512, 1024, 2048):
+        ms, r = timed(lambda: ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=thr), a.reps)
+        row(rows, "C3", 8192, 1.0, f"rkleene fp32 aligned thr={thr}", ms, r.info)
+    ms, r = timed(lambda: ap.solve(h, "fw_blocked"), a.reps)
+    row(rows, "C3", 8192, 1.0, "fw_blocked fp32", ms, r.info)
+    # C5
+    for n in (1024, 2048, 4096, 8192, 16384):
+        if n > a.sweep_max:
+            break
+        for rho in (0.002, 0.01, 0.1, 0.5, 1.0):
+            h = gen(n, rho, np.int32)
+            ms, r = timed(lambda: ap.solve(h, "fw_blocked"), max(1, a.reps - 1))
+            row(rows, "C5", n, rho, "fw_blocked int32", ms, r.info, f"maxd={r.info['max_finite']}")
+            ms, r = timed(lambda: ap.solve(h, "rkleene", track="pred", split="aligned",
+                                           base_threshold=min(1024, n // 2)), max(1, a.reps - 1))
+            row(rows, "C5", n, rho, "rkleene int32 (aligned, pred)", ms, r.info)
+            del h
+            torch.cuda.empty_cache()
+    Path(a.out).parent.mkdir(parents=True, exist_ok=True)
+    Path(a.out).write_text(json.dumps(rows, indent=1))
+
+
+if __name__ == "__main__":
+    main()
