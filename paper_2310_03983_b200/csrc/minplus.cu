@@ -18,6 +18,10 @@
 namespace apsp {
 
 constexpr int BM = 128, BN = 128, NT = 256;
+#ifndef APSP_U8_UNROLL
+#define APSP_U8_UNROLL 32
+#endif
+constexpr int kU8Unroll = APSP_U8_UNROLL;
 
 // Tile origin of this CTA.  Full grid: (blockIdx.y, blockIdx.x).  Cross-list mode
 // (only_lo < only_hi): blockIdx.x enumerates the tiles of rows band + cols band [lo, hi)
@@ -53,6 +57,16 @@ __device__ __forceinline__ void emit_idx(const MinplusArgs& p, int64_t i, int64_
   if (p.idx == nullptr) return;
   int32_t v = (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(kk) * p.ldp + j) : int32_t(p.inner_off + kk);
   p.idx[i * p.ldi + j] = v;
+}
+
+// u8 tier keys: 16-bit UNSIGNED, key = value << 7 | tag, tag = 1..64 over a 64-k decode window
+// (two 32-k chunks).  INF key = 255 << 7 = 32640; the largest sum INF + INF + tag = 65407 < 2^16.
+constexpr int U8_TAG = 7;
+constexpr uint32_t U8_KINF = uint32_t(U8_INF) << U8_TAG;
+constexpr uint32_t U8_TAGMASK2 = 0x007F007Fu;
+
+__device__ __forceinline__ uint32_t viaddmin_u16x2(uint32_t a, uint32_t b, uint32_t c) {
+  return __viaddmin_u16x2(a, b, c);
 }
 
 // 0xFFFF in each 16-bit half whose bit 15 is set, else 0 (PTX prmt sign replication; the
@@ -103,7 +117,7 @@ __device__ __forceinline__ void u8_load_chunk(const MinplusArgs& p, int64_t i0, 
   }
 }
 
-__device__ __forceinline__ void u8_store_chunk(SmemU8& sm, int buf, const uint4& ra, const uint4& rb) {
+__device__ __forceinline__ void u8_store_chunk(SmemU8& sm, int buf, const uint4& ra, const uint4& rb, int tagbase) {
   const int t = threadIdx.x;
   {
     const int r = t & 127, kb = 16 * (t >> 7);
@@ -111,18 +125,18 @@ __device__ __forceinline__ void u8_store_chunk(SmemU8& sm, int buf, const uint4&
 #pragma unroll
     for (int q = 0; q < 16; q++) {
       uint32_t v = (w[q >> 2] >> (8 * (q & 3))) & 0xFF;
-      sm.As[buf][kb + q][r] = v * 0x00400040u;   // (v<<6) in both halves
+      sm.As[buf][kb + q][r] = v * 0x00800080u;   // (v<<7) in both halves
     }
   }
   {
     const int kk = t >> 3, cb = 16 * (t & 7);
-    const uint32_t tag = uint32_t(kk + 1) * 0x00010001u;
+    const uint32_t tag = uint32_t(tagbase + kk + 1) * 0x00010001u;
     uint32_t w[4] = {rb.x, rb.y, rb.z, rb.w};
     uint32_t o[8];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      o[2 * q] = (__byte_perm(w[q], 0, 0x4140) << TAG_BITS) | tag;
-      o[2 * q + 1] = (__byte_perm(w[q], 0, 0x4342) << TAG_BITS) | tag;
+      o[2 * q] = (__byte_perm(w[q], 0, 0x4140) << U8_TAG) | tag;
+      o[2 * q + 1] = (__byte_perm(w[q], 0, 0x4342) << U8_TAG) | tag;
     }
     uint4* dst = reinterpret_cast<uint4*>(&sm.Bs[buf][kk][cb]);
     dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
@@ -163,7 +177,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
   for (int r = 0; r < 8; r++)
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      acc[r][q] = K16_INF * 0x00010001u;
+      acc[r][q] = U8_KINF * 0x00010001u;
       kst[r][q] = 0u;
     }
 
@@ -173,13 +187,13 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
   const int64_t nchunks = (p.k + SUB - 1) / SUB;
   uint4 ra, rb;
   u8_load_chunk(p, i0, j0, 0, abfast_base && SUB <= p.k, ra, rb);
-  u8_store_chunk(sm, 0, ra, rb);
+  u8_store_chunk(sm, 0, ra, rb, 0);
   __syncthreads();
   for (int64_t c = 0; c < nchunks; c++) {
     const int buf = int(c & 1);
     const bool more = c + 1 < nchunks;
     if (more) u8_load_chunk(p, i0, j0, (c + 1) * SUB, abfast_base && (c + 2) * SUB <= p.k, ra, rb);
-#pragma unroll 4
+#pragma unroll kU8Unroll
     for (int kk = 0; kk < SUB; kk++) {
       const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[buf][kk][4 * ty]);
       const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[buf][kk][64 + 4 * ty]);
@@ -190,7 +204,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
 #pragma unroll
       for (int r = 0; r < 8; r++)
 #pragma unroll
-        for (int q = 0; q < 4; q++) acc[r][q] = viaddmin16x2(a[r], b[q], acc[r][q]);
+        for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
     }
     if (c == 0) {
       // merge the (prefetched) old values: an untagged old key wins value ties, so only a
@@ -203,49 +217,72 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
-          acc[r][2 * h] = __vmins2(acc[r][2 * h], __byte_perm(w, 0, 0x4140) << TAG_BITS);
-          acc[r][2 * h + 1] = __vmins2(acc[r][2 * h + 1], __byte_perm(w, 0, 0x4342) << TAG_BITS);
+          acc[r][2 * h] = __vminu2(acc[r][2 * h], __byte_perm(w, 0, 0x4140) << U8_TAG);
+          acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], __byte_perm(w, 0, 0x4342) << U8_TAG);
         }
       }
     }
-    // decode tags of this chunk into 1-based k indices (0 = untouched), branch-free:
+    // decode the tags of the 64-k window (after every second chunk and the last one) into
+    // 1-based k indices (0 = untouched), branch-free:
     //   tg   = tags of the pair;  tg + 0x7FFF per half sets bit 15 iff the tag is nonzero
     //   mask = PRMT sign-replication of bytes 1/3 -> 0xFFFF per half with a tag
-    //   kst  = mask ? (c*32 + tg) : kst          (one LOP3; no cross-half carry: all >= 0)
-    uint32_t any = 0;
-#pragma unroll
-    for (int r = 0; r < 8; r++)
-#pragma unroll
-      for (int q = 0; q < 4; q++) any |= acc[r][q];
-    if (__any_sync(0xffffffffu, any & TAGMASK2)) {
-      const uint32_t kb2 = uint32_t(c * SUB) * 0x00010001u;
+    //   kst  = mask ? (window base + tg) : kst   (one LOP3; no cross-half carry: all >= 0)
+    if ((c & 1) || !more) {
+      uint32_t any = 0;
 #pragma unroll
       for (int r = 0; r < 8; r++)
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const uint32_t tg = acc[r][q] & TAGMASK2;
-          const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
-          kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
-          acc[r][q] ^= tg;
-        }
+        for (int q = 0; q < 4; q++) any |= acc[r][q];
+      if (__any_sync(0xffffffffu, any & U8_TAGMASK2)) {
+        const uint32_t kb2 = uint32_t((c & ~int64_t(1)) * SUB) * 0x00010001u;
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const uint32_t tg = acc[r][q] & U8_TAGMASK2;
+            const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
+            kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
+            acc[r][q] ^= tg;
+          }
+      }
     }
-    if (more) u8_store_chunk(sm, buf ^ 1, ra, rb);
+    if (more) u8_store_chunk(sm, buf ^ 1, ra, rb, int((c + 1) & 1) * SUB);
     __syncthreads();
   }
 
-  // epilogue: values of improved row segments, then idx of improved cells
+  // epilogue: values of improved row segments, then idx of improved cells.  The pred gathers
+  // of a row are issued back to back (restrict: idx rows never alias the predB rows a tile
+  // reads -- the pivot cross is skipped / snapshotted), then stored, 16B when all 4 improved.
   bool changed = false;
   uint8_t* Cw = static_cast<uint8_t*>(p.C);
+  const int32_t* __restrict__ pb = p.predB;
+  int32_t* __restrict__ out = p.idx;
+  const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
 #pragma unroll
   for (int r = 0; r < 8; r++) {
     const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+    int32_t pv[2][4];
+    uint32_t ks[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+      ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
+      const int64_t j = j0 + 64 * h + 4 * tx;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        pv[h][q] = 0;
+        if (out && ks[h][q] != 0u && i < p.m && j + q < p.n)
+          pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
+                                          : int32_t(p.inner_off + ks[h][q] - 1u);
+      }
+    }
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
       if ((k0 | k1) == 0u) continue;
       changed = true;
       const int64_t j = j0 + 64 * h + 4 * tx;
-      const uint32_t w = __byte_perm(acc[r][2 * h] >> TAG_BITS, acc[r][2 * h + 1] >> TAG_BITS, 0x6420);
+      const uint32_t w = __byte_perm(acc[r][2 * h] >> U8_TAG, acc[r][2 * h + 1] >> U8_TAG, 0x6420);
       if (cfast) {
         *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) = w;
       } else {
@@ -253,11 +290,14 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
         for (int q = 0; q < 4; q++)
           if (i < p.m && j + q < p.n) Cw[i * p.ldc + j + q] = uint8_t(w >> (8 * q));
       }
-      if (i < p.m) {
-        const uint32_t ks[4] = {k0 & 0xFFFF, k0 >> 16, k1 & 0xFFFF, k1 >> 16};
+      if (!out || i >= p.m) continue;
+      const bool all4 = ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3];
+      if (all4 && idx_vec && cfast) {
+        *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+      } else {
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          if (ks[q] != 0u && j + q < p.n) emit_idx(p, i, j + q, ks[q] - 1u);
+          if (ks[h][q] != 0u && j + q < p.n) out[i * p.ldi + j + q] = pv[h][q];
       }
     }
   }
