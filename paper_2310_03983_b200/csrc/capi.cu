@@ -200,13 +200,36 @@ struct FwCtx {
   int32_t* predsnap = nullptr;   // b x m
   char* rowsnap = nullptr;       // b x m values (b > 128 only)
   char* colsnap = nullptr;       // m x b values (b > 128 only)
+  char* prep[2] = {nullptr, nullptr};  // u8 tier: bulk-copy layouts of the panels, by round parity
   int launches = 0;
 };
 
 size_t fw_scratch_bytes(int64_t m, int b, size_t es) {
   size_t v = size_t(b) * m * 4 + 256;
   if (b > TILE_ALIGN) v += 2 * size_t(b) * m * es + 256;
+  v += 2 * (prep_u8_bytes(m, m, b) + 256);
   return v;
+}
+
+// carve the scratch of fw_scratch_bytes
+void fw_carve(FwCtx& c, char* scratch, int64_t N) {
+  char* p = scratch;
+  c.predsnap = reinterpret_cast<int32_t*>(p);
+  p += size_t(c.b) * N * 4 + 256;
+  if (c.b > TILE_ALIGN) {
+    c.rowsnap = p;
+    c.colsnap = p + size_t(c.b) * N * c.es + 128;
+    p += 2 * size_t(c.b) * N * c.es + 256;
+  }
+  for (int q = 0; q < 2; q++) {
+    c.prep[q] = p;
+    p += prep_u8_bytes(N, N, c.b) + 256;
+  }
+}
+
+uint32_t* prep_a(char* slot) { return reinterpret_cast<uint32_t*>(slot); }
+uint16_t* prep_b(char* slot, int64_t m, int64_t k) {
+  return reinterpret_cast<uint16_t*>(slot + ((size_t(m) * k * 4 + 255) / 256) * 256);
 }
 
 int fw_run(FwCtx& c, cudaStream_t s);
@@ -277,7 +300,11 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   q.skip_row_lo = k0; q.skip_row_hi = k0 + b;
   q.status = c.st;
   c.launches += 2;
-  return launch_minplus(c.store, q, s);
+  rc = launch_minplus(c.store, q, s);
+  if (rc || !c.prep[0] || c.store != STORE_U8) return rc;
+  char* slot = c.prep[(k0 / b) & 1];
+  c.launches += 2;
+  return launch_prep_u8(colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
 }
 
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
@@ -298,6 +325,11 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   if (only_next >= 0) { a.only_lo = only_next; a.only_hi = only_next + c.b; }
   if (skip_next >= 0) { a.skip2_lo = skip_next; a.skip2_hi = skip_next + c.b; }
   a.status = c.st;
+  if (c.prep[0] && c.store == STORE_U8) {
+    char* slot = c.prep[(k0 / c.b) & 1];
+    a.Aprep = prep_a(slot);
+    a.Bprep = prep_b(slot, c.m, c.b);
+  }
   c.launches++;
   return timed_minplus(c.store, a, s);
 }
@@ -464,11 +496,8 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
       c.D = D; c.ld = N; c.P = P; c.ldp = N; c.m = N; c.b = b; c.mode = IDX_PRED; c.via_off = 0;
       c.st = &hdr_dev->status;
       c.side = getenv("APSP_NO_LOOKAHEAD") ? nullptr : side_stream();
-      c.predsnap = reinterpret_cast<int32_t*>(scratch);
-      if (b > TILE_ALIGN) {
-        c.rowsnap = scratch + size_t(b) * N * 4 + 256;
-        c.colsnap = c.rowsnap + size_t(b) * N * c.es + 128;
-      }
+      fw_carve(c, scratch, N);
+      if (getenv("APSP_NO_BULK")) c.prep[0] = c.prep[1] = nullptr;
       rc = fw_run(c, s);
       launches += c.launches;
     }

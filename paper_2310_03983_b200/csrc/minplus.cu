@@ -305,6 +305,229 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
 }
 
 // ------------------------------------------------------------------------------------
+// narrow tier with pre-laid-out panels: cp.async.bulk (TMA bulk copy) + mbarrier 3-stage ring
+// ------------------------------------------------------------------------------------
+constexpr int U8_STAGES = 3;
+constexpr uint32_t U8_CHUNK_A = SUB * BM * 4, U8_CHUNK_B = SUB * BN * 2;
+struct SmemU8T {
+  uint32_t As[U8_STAGES][SUB][BM];
+  uint16_t Bs[U8_STAGES][SUB][BN];
+  uint8_t Cs[BM][BN];
+  unsigned long long bar[U8_STAGES];
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+__device__ __forceinline__ void u8t_issue(SmemU8T& sm, const MinplusArgs& p, int64_t rt, int64_t ct, int64_t nch,
+                                          int64_t c, int slot) {
+  mbar_expect_tx(&sm.bar[slot], U8_CHUNK_A + U8_CHUNK_B);
+  bulk_g2s(&sm.As[slot][0][0], p.Aprep + (rt * nch + c) * (SUB * BM), U8_CHUNK_A, &sm.bar[slot]);
+  bulk_g2s(&sm.Bs[slot][0][0], p.Bprep + (ct * nch + c) * (SUB * BN), U8_CHUNK_B, &sm.bar[slot]);
+}
+
+__global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p) {
+  extern __shared__ __align__(128) unsigned char smraw_u8t[];
+  SmemU8T& sm = *reinterpret_cast<SmemU8T*>(smraw_u8t);
+  int64_t i0, j0;
+  tile_origin(p, BM, BN, i0, j0);
+  if (tile_skipped(p, i0, j0, BM, BN)) return;
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int64_t rt = i0 / BM, ct = j0 / BN, nch = p.k / SUB;
+  if (t == 0) {
+    for (int s = 0; s < U8_STAGES; s++) mbar_init(&sm.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (t == 0)
+    for (int s = 0; s < U8_STAGES && s < nch; s++) u8t_issue(sm, p, rt, ct, nch, s, s);
+
+  uint32_t acc[8][4];
+  uint32_t kst[8][4];
+  const uint8_t* C = static_cast<const uint8_t*>(p.C);
+  {
+    const int r = t >> 1, cb = 64 * (t & 1);
+    const uint8_t* src = C + (i0 + r) * p.ldc + j0 + cb;
+    const uint32_t dst = smem_u32(&sm.Cs[r][cb]);
+#pragma unroll
+    for (int q = 0; q < 4; q++)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+#pragma unroll
+  for (int r = 0; r < 8; r++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      acc[r][q] = U8_KINF * 0x00010001u;
+      kst[r][q] = 0u;
+    }
+  for (int64_t c = 0; c < nch; c++) {
+    const int slot = int(c % U8_STAGES);
+    mbar_wait(&sm.bar[slot], uint32_t((c / U8_STAGES) & 1));
+#pragma unroll kU8Unroll
+    for (int kk = 0; kk < SUB; kk++) {
+      const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
+      const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
+      const uint2 b0 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][4 * tx]);
+      const uint2 b1 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][64 + 4 * tx]);
+      const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
+    }
+    const bool more = c + 1 < nch;
+    if (c == 0) {
+      asm volatile("cp.async.wait_all;\n" ::);
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
+          acc[r][2 * h] = __vminu2(acc[r][2 * h], __byte_perm(w, 0, 0x4140) << U8_TAG);
+          acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], __byte_perm(w, 0, 0x4342) << U8_TAG);
+        }
+      }
+    }
+    if ((c & 1) || !more) {
+      uint32_t any = 0;
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) any |= acc[r][q];
+      if (__any_sync(0xffffffffu, any & U8_TAGMASK2)) {
+        const uint32_t kb2 = uint32_t((c & ~int64_t(1)) * SUB) * 0x00010001u;
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const uint32_t tg = acc[r][q] & U8_TAGMASK2;
+            const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
+            kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
+            acc[r][q] ^= tg;
+          }
+      }
+    }
+    __syncthreads();   // every warp is done with this slot
+    if (t == 0 && c + U8_STAGES < nch) u8t_issue(sm, p, rt, ct, nch, c + U8_STAGES, slot);
+  }
+
+  bool changed = false;
+  uint8_t* Cw = static_cast<uint8_t*>(p.C);
+  const int32_t* __restrict__ pb = p.predB;
+  int32_t* __restrict__ out = p.idx;
+  const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+    int32_t pv[2][4];
+    uint32_t ks[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+      ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
+      const int64_t j = j0 + 64 * h + 4 * tx;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        pv[h][q] = 0;
+        if (out && ks[h][q] != 0u)
+          pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
+                                          : int32_t(p.inner_off + ks[h][q] - 1u);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+      if ((k0 | k1) == 0u) continue;
+      changed = true;
+      const int64_t j = j0 + 64 * h + 4 * tx;
+      *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) =
+          __byte_perm(acc[r][2 * h] >> U8_TAG, acc[r][2 * h + 1] >> U8_TAG, 0x6420);
+      if (!out) continue;
+      if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
+        *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (ks[h][q] != 0u) out[i * p.ldi + j + q] = pv[h][q];
+      }
+    }
+  }
+  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+}
+
+// panel layout kernels
+__global__ void prep_u8_a_kernel(const uint8_t* A, int64_t lda, int64_t nch, uint32_t* Aprep) {
+  const int64_t rt = blockIdx.y, c = blockIdx.x;
+  const int t = threadIdx.x, r = t & 127, kb = 16 * (t >> 7);
+  const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(A + (rt * BM + r) * lda + c * SUB + kb));
+  const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+  uint32_t* dst = Aprep + (rt * nch + c) * (SUB * BM);
+#pragma unroll
+  for (int q = 0; q < 16; q++) dst[(kb + q) * BM + r] = ((w[q >> 2] >> (8 * (q & 3))) & 0xFF) * 0x00800080u;
+}
+
+__global__ void prep_u8_b_kernel(const uint8_t* B, int64_t ldb, int64_t nch, uint16_t* Bprep) {
+  const int64_t ct = blockIdx.y, c = blockIdx.x;
+  const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
+  const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(B + (c * SUB + kk) * ldb + ct * BN + cb));
+  const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+  const uint32_t tag = uint32_t(SUB * (c & 1) + kk + 1) * 0x00010001u;
+  uint32_t o[8];
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    o[2 * q] = (__byte_perm(w[q], 0, 0x4140) << U8_TAG) | tag;
+    o[2 * q + 1] = (__byte_perm(w[q], 0, 0x4342) << U8_TAG) | tag;
+  }
+  uint4* dst = reinterpret_cast<uint4*>(Bprep + (ct * nch + c) * (SUB * BN) + kk * BN + cb);
+  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+size_t prep_u8_bytes(int64_t m, int64_t n, int64_t k) { return size_t(m) * k * 4 + size_t(k) * n * 2 + 256; }
+
+int launch_prep_u8(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n, int64_t k,
+                   uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s) {
+  if (m % BM || n % BN || k % SUB || (lda & 15) || (ldb & 15) || (reinterpret_cast<uintptr_t>(A) & 15) ||
+      (reinterpret_cast<uintptr_t>(B) & 15))
+    return set_error(2, "prep_u8 needs 128-multiple m/n, 32-multiple k and 16-byte aligned panels");
+  const int64_t nch = k / SUB;
+  prep_u8_a_kernel<<<dim3(unsigned(nch), unsigned(m / BM)), NT, 0, s>>>(static_cast<const uint8_t*>(A), lda, nch,
+                                                                         Aprep);
+  prep_u8_b_kernel<<<dim3(unsigned(nch), unsigned(n / BN)), NT, 0, s>>>(static_cast<const uint8_t*>(B), ldb, nch,
+                                                                         Bprep);
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------
 // wide tier: int32 store (< 2^24), int32 keys, VIADD + VIMNMX3 over k pairs
 // ------------------------------------------------------------------------------------
 struct SmemW32 {
@@ -585,6 +808,18 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
   }
   switch (store) {
     case STORE_U8: {
+      if (a.Aprep && a.Bprep) {
+        static bool attr_t = false;
+        if (!attr_t) {
+          APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_u8_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(sizeof(SmemU8T))));
+          attr_t = true;
+        }
+        if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc & 15))
+          return set_error(2, "bulk-staged u8 tiles need full 128 x 128 tiles and 32-multiple k");
+        minplus_u8_tma_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemU8T), s>>>(a);
+        break;
+      }
       static bool attr = false;
       if (!attr) {
         APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
