@@ -5,6 +5,7 @@
 //
 // Race freedom in all three: with a zero diagonal and nonnegative costs, row k and column k
 // are invariant during step k (solvers.py:79-81), so one barrier per k suffices.
+#include <cstdlib>
 #include "launch.h"
 
 namespace apsp {
@@ -164,6 +165,179 @@ __global__ void __launch_bounds__(512) block_close_kernel(typename StoreT<S>::T*
   if (st && overflow) st->overflow = 1;
 }
 
+// ------------------------------------------------------------------------------------
+// u8 tier closure of an m <= 128 diagonal block: packed 16-bit DPX keys.
+//   key = value << 7 | tag, tag = 1 + (k mod 64), decoded every 64 steps into the last
+//   improving k per cell (8 bits, 1-based).  Row / column k are published tag-free.
+//   pred is deferred: with k* the last improving step of (i,j), pred[k*][j] never changes after
+//   step k* (else (i,j) would improve again), so pred_final[i][j] = pred_final[k*][j]; the
+//   chains k* -> kst(k*, j) -> ... strictly decrease and are resolved by pointer jumping.
+//   The result equals the classic in-block order exactly (values, pred and via).
+// 512 threads: thread (ty, tx) owns rows ty + 16a (a < 8) x column pairs 2tx + 64c (c < 2).
+// ------------------------------------------------------------------------------------
+struct CloseU8Smem {
+  uint32_t rowk[2][64];       // row k as tag-free key pairs
+  uint32_t colk[2][MAXB];     // column k as replicated tag-free keys
+  int32_t P[MAXB][MAXB];      // pred resolution
+  uint8_t K[MAXB][MAXB];      // 1-based last improving k (0 = none)
+};
+
+__device__ __forceinline__ uint32_t u8c_strip(uint32_t x) { return x & 0xFF80FF80u; }
+
+__global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t ld, int64_t lo, int m, int32_t* idx,
+                                                             int64_t ldi, int mode, int64_t via_off) {
+  extern __shared__ __align__(16) unsigned char smraw_cu8[];
+  CloseU8Smem& sm = *reinterpret_cast<CloseU8Smem*>(smraw_cu8);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  constexpr uint32_t KINF2 = (255u << 7) * 0x00010001u;
+  uint32_t acc[8][2];
+  uint32_t kst[8];            // byte q of kst[a] = cell (a, q): q = 2c + half
+#pragma unroll
+  for (int a = 0; a < 8; a++) {
+    const int i = ty + 16 * a;
+    kst[a] = 0;
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      const int j = 2 * tx + 64 * c;
+      uint32_t lo16 = 255, hi16 = 255;
+      if (i < m && j < m) lo16 = D[(lo + i) * ld + lo + j];
+      if (i < m && j + 1 < m) hi16 = D[(lo + i) * ld + lo + j + 1];
+      acc[a][c] = ((hi16 << 16) | lo16) << 7;
+    }
+  }
+  // publish helpers (select chains: no dynamic register indexing)
+#define CU8_PUBLISH(KK, BUF)                                                              \
+  do {                                                                                    \
+    const int pk_ = (KK), pb_ = (BUF);                                                    \
+    if (ty == (pk_ & 15)) {                                                               \
+      const int sa_ = pk_ >> 4;                                                           \
+      _Pragma("unroll") for (int c = 0; c < 2; c++) {                                     \
+        uint32_t r_ = acc[0][c];                                                          \
+        _Pragma("unroll") for (int a = 1; a < 8; a++) r_ = (a == sa_) ? acc[a][c] : r_;  \
+        sm.rowk[pb_][tx + 32 * c] = u8c_strip(r_);                                        \
+      }                                                                                   \
+    }                                                                                     \
+    if (tx == ((pk_ & 63) >> 1)) {                                                        \
+      const int sc_ = pk_ >> 6, sh_ = pk_ & 1;                                            \
+      _Pragma("unroll") for (int a = 0; a < 8; a++) {                                     \
+        const uint32_t x_ = sc_ ? acc[a][1] : acc[a][0];                                  \
+        const uint32_t h_ = (sh_ ? (x_ >> 16) : x_) & 0xFF80u;                            \
+        sm.colk[pb_][ty + 16 * a] = h_ * 0x00010001u;                                     \
+      }                                                                                   \
+    }                                                                                     \
+  } while (0)
+  CU8_PUBLISH(0, 0);
+  for (int k = 0; k < m; k++) {
+    __syncthreads();
+    const int b = k & 1;
+    const uint32_t tag2 = uint32_t((k & 63) + 1) * 0x00010001u;
+    uint32_t dkj[2], dik[8];
+#pragma unroll
+    for (int c = 0; c < 2; c++) dkj[c] = sm.rowk[b][tx + 32 * c] + tag2;
+#pragma unroll
+    for (int a = 0; a < 8; a++) dik[a] = sm.colk[b][ty + 16 * a];
+#pragma unroll
+    for (int a = 0; a < 8; a++)
+#pragma unroll
+      for (int c = 0; c < 2; c++) acc[a][c] = __viaddmin_u16x2(dik[a], dkj[c], acc[a][c]);
+    if ((k & 63) == 63 || k + 1 == m) {   // decode this 64-step window
+      const uint32_t wbase = uint32_t(k & ~63);
+#pragma unroll
+      for (int a = 0; a < 8; a++) {
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          const uint32_t tg = acc[a][c] & 0x007F007Fu;
+          acc[a][c] ^= tg;
+          const uint32_t tlo = tg & 0xFF, thi = tg >> 16;
+          const int sh0 = 8 * (2 * c), sh1 = 8 * (2 * c + 1);
+          if (tlo) kst[a] = (kst[a] & ~(0xFFu << sh0)) | ((wbase + tlo) << sh0);
+          if (thi) kst[a] = (kst[a] & ~(0xFFu << sh1)) | ((wbase + thi) << sh1);
+        }
+      }
+    }
+    if (k + 1 < m) CU8_PUBLISH(k + 1, b ^ 1);
+  }
+#undef CU8_PUBLISH
+  // values back
+#pragma unroll
+  for (int a = 0; a < 8; a++) {
+    const int i = ty + 16 * a;
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      const int j = 2 * tx + 64 * c;
+      const uint32_t v = acc[a][c] >> 7;
+      if (i < m && j < m) D[(lo + i) * ld + lo + j] = uint8_t(v & 0xFF);
+      if (i < m && j + 1 < m) D[(lo + i) * ld + lo + j + 1] = uint8_t(v >> 16);
+    }
+  }
+  if (!idx) return;
+  if (mode == IDX_VIA) {
+#pragma unroll
+    for (int a = 0; a < 8; a++) {
+      const int i = ty + 16 * a;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
+        const uint32_t kk = (kst[a] >> (8 * q)) & 0xFF;
+        if (kk && i < m && j < m) idx[(lo + i) * ldi + lo + j] = int32_t(via_off + kk - 1);
+      }
+    }
+    return;
+  }
+  // pred: stage P_init and the 0-based k* rows, then pointer-jump the chains
+#pragma unroll
+  for (int a = 0; a < 8; a++) {
+    const int i = ty + 16 * a;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
+      sm.K[i][j] = uint8_t((kst[a] >> (8 * q)) & 0xFF);
+      sm.P[i][j] = (i < m && j < m) ? idx[(lo + i) * ldi + lo + j] : -1;
+    }
+  }
+  __syncthreads();
+  for (int round = 0; round < 7; round++) {   // chains have length < 128 = 2^7
+    int32_t np[8][4];
+    uint8_t nk[8][4];
+#pragma unroll
+    for (int a = 0; a < 8; a++) {
+      const int i = ty + 16 * a;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
+        const uint8_t kk = sm.K[i][j];
+        np[a][q] = sm.P[i][j];
+        nk[a][q] = kk;
+        if (kk) {
+          np[a][q] = sm.P[kk - 1][j];
+          nk[a][q] = sm.K[kk - 1][j];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 8; a++) {
+      const int i = ty + 16 * a;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
+        sm.P[i][j] = np[a][q];
+        sm.K[i][j] = nk[a][q];
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 8; a++) {
+    const int i = ty + 16 * a;
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
+      if (i < m && j < m) idx[(lo + i) * ldi + lo + j] = sm.P[i][j];
+    }
+  }
+}
+
 template <int S>
 static int close_impl(void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi, int mode,
                       int64_t via_off, Status* st, cudaStream_t s) {
@@ -183,6 +357,18 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
                               idx ? idx + lo * ldi + lo : nullptr, ldi, mode, via_off, st, s);
       if (rc) return rc;
     }
+    return 0;
+  }
+  if (store == STORE_U8 && !getenv("APSP_SLOW_CLOSE")) {
+    static bool attr = false;
+    if (!attr) {
+      APSP_CUDA_TRY(cudaFuncSetAttribute(block_close_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(sizeof(CloseU8Smem))));
+      attr = true;
+    }
+    block_close_u8_kernel<<<1, 512, sizeof(CloseU8Smem), s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
+                                                              mode, via_off);
+    APSP_CUDA_TRY(cudaGetLastError());
     return 0;
   }
   switch (store) {

@@ -100,6 +100,18 @@ def test_fw_ragged_sizes_vs_oracle(cuda, n, density, wmax, seed):
     assert np.array_equal(c.distances.raw, want_d) and np.array_equal(c.pred.raw, want_p)
 
 
+@pytest.mark.parametrize("n,density", [(50, 0.1), (100, 0.05), (128, 0.03), (128, 1.0), (77, 0.2)])
+def test_single_block_closure_is_classic_order(cuda, n, density):
+    # n <= 128: the blocked solve is one phase-1 closure, whose deferred-pred u8 kernel must
+    # reproduce the classic k order bit-for-bit (dist and pred), like reference fw_classic
+    raw = random_graph_raw(n, density, 9, seed=1000 + n)
+    want_d, want_p = orc.fw_classic(raw)
+    s = ap.fw_classic(ap.CostMatrix(raw))
+    assert s.info["tier"] == "u8"
+    assert np.array_equal(s.distances.raw, want_d)
+    assert np.array_equal(s.pred.raw, want_p)
+
+
 def test_zero_weight_edges(cuda):
     raw = random_graph_raw(257, 0.05, 20, 9, zero_frac=0.3)
     want_d, _ = orc.fw_classic(raw)
