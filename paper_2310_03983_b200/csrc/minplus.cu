@@ -13,6 +13,7 @@
 // keys is the lexicographic (value, smallest k) min; an untagged (old) key wins ties, so a
 // tag survives only on strict improvement (minplus.py:80-82,128-133).  Every 32 k-steps the
 // tags are decoded into a 16-bit k index per cell and cleared.
+#include <cstdlib>
 #include "launch.h"
 
 namespace apsp {
@@ -350,133 +351,191 @@ __device__ __forceinline__ void u8t_issue(SmemU8T& sm, const MinplusArgs& p, int
   bulk_g2s(&sm.Bs[slot][0][0], p.Bprep + (ct * nch + c) * (SUB * BN), U8_CHUNK_B, &sm.bar[slot]);
 }
 
-__global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p) {
+// Tile origin of virtual tile index v (the 2D grid flattened row-major, or the cross list).
+__device__ __forceinline__ void tile_at(const MinplusArgs& p, int64_t v, int bm, int bn, int64_t& i0, int64_t& j0) {
+  if (p.only_lo < p.only_hi) {
+    const int64_t w = (p.only_hi - p.only_lo) / bm, lo_t = p.only_lo / bm;
+    const int64_t nt_c = (p.n + bn - 1) / bn;
+    if (v < w * nt_c) {
+      i0 = (lo_t + v / nt_c) * bm;
+      j0 = (v % nt_c) * bn;
+    } else {
+      const int64_t id2 = v - w * nt_c, rr = id2 / w, cc = id2 % w;
+      i0 = (rr < lo_t ? rr : rr + w) * bm;
+      j0 = (lo_t + cc) * bn;
+    }
+  } else {
+    const int64_t nt_c = (p.n + bn - 1) / bn;
+    i0 = (v / nt_c) * bm;
+    j0 = (v % nt_c) * bn;
+  }
+}
+
+__device__ __forceinline__ int64_t tile_count(const MinplusArgs& p, int bm, int bn) {
+  const int64_t nt_r = (p.m + bm - 1) / bm, nt_c = (p.n + bn - 1) / bn;
+  if (p.only_lo < p.only_hi) {
+    const int64_t w = (p.only_hi - p.only_lo) / bm;
+    return w * nt_c + (nt_r - w) * w;
+  }
+  return nt_r * nt_c;
+}
+
+constexpr int U8_TPC_MAX = 8;       // tiles per CTA (ring and C prefetch run across tiles)
+constexpr int U8_DEC_CHUNKS = 3;    // decode window: 3 chunks = 96 k, tags 1..96 (7 bits)
+
+__global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, int tpc) {
   extern __shared__ __align__(128) unsigned char smraw_u8t[];
   SmemU8T& sm = *reinterpret_cast<SmemU8T*>(smraw_u8t);
-  int64_t i0, j0;
-  tile_origin(p, BM, BN, i0, j0);
-  if (tile_skipped(p, i0, j0, BM, BN)) return;
+  __shared__ int64_t tiles_i0[U8_TPC_MAX], tiles_j0[U8_TPC_MAX];
+  __shared__ int ntiles;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  const int64_t rt = i0 / BM, ct = j0 / BN, nch = p.k / SUB;
+  const int64_t nch = p.k / SUB;
   if (t == 0) {
+    const int64_t total = tile_count(p, BM, BN), v0 = int64_t(blockIdx.x) * tpc;
+    int cnt = 0;
+    for (int64_t v = v0; v < v0 + tpc && v < total; v++) {
+      int64_t i0, j0;
+      tile_at(p, v, BM, BN, i0, j0);
+      if (tile_skipped(p, i0, j0, BM, BN)) continue;
+      tiles_i0[cnt] = i0;
+      tiles_j0[cnt] = j0;
+      cnt++;
+    }
+    ntiles = cnt;
     for (int s = 0; s < U8_STAGES; s++) mbar_init(&sm.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const int nt = ntiles;
+  if (nt == 0) return;
+  const int64_t total_g = int64_t(nt) * nch;
+  auto issue = [&](int64_t g) {
+    const int tt = int(g / nch);
+    const int64_t c = g - int64_t(tt) * nch;
+    u8t_issue(sm, p, tiles_i0[tt] / BM, tiles_j0[tt] / BN, nch, c, int(g % U8_STAGES));
+  };
   if (t == 0)
-    for (int s = 0; s < U8_STAGES && s < nch; s++) u8t_issue(sm, p, rt, ct, nch, s, s);
-
-  uint32_t acc[8][4];
-  uint32_t kst[8][4];
+    for (int64_t g = 0; g < U8_STAGES && g < total_g; g++) issue(g);
   const uint8_t* C = static_cast<const uint8_t*>(p.C);
-  {
+  auto prefetch_c = [&](int tt) {
     const int r = t >> 1, cb = 64 * (t & 1);
-    const uint8_t* src = C + (i0 + r) * p.ldc + j0 + cb;
+    const uint8_t* src = C + (tiles_i0[tt] + r) * p.ldc + tiles_j0[tt] + cb;
     const uint32_t dst = smem_u32(&sm.Cs[r][cb]);
 #pragma unroll
     for (int q = 0; q < 4; q++)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
     asm volatile("cp.async.commit_group;\n" ::);
-  }
+  };
+  prefetch_c(0);
+  bool changed = false;
+  const int32_t* __restrict__ pb = p.predB;
+  int32_t* __restrict__ out = p.idx;
+  uint8_t* Cw = static_cast<uint8_t*>(p.C);
+  const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
+
+  for (int tt = 0; tt < nt; tt++) {
+    const int64_t i0 = tiles_i0[tt], j0 = tiles_j0[tt];
+    uint32_t acc[8][4];
+    uint32_t kst[8][4];
 #pragma unroll
-  for (int r = 0; r < 8; r++)
+    for (int r = 0; r < 8; r++)
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      acc[r][q] = U8_KINF * 0x00010001u;
-      kst[r][q] = 0u;
-    }
-  for (int64_t c = 0; c < nch; c++) {
-    const int slot = int(c % U8_STAGES);
-    mbar_wait(&sm.bar[slot], uint32_t((c / U8_STAGES) & 1));
-#pragma unroll kU8Unroll
-    for (int kk = 0; kk < SUB; kk++) {
-      const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
-      const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
-      const uint2 b0 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][4 * tx]);
-      const uint2 b1 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][64 + 4 * tx]);
-      const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
-#pragma unroll
-      for (int r = 0; r < 8; r++)
-#pragma unroll
-        for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
-    }
-    const bool more = c + 1 < nch;
-    if (c == 0) {
-      asm volatile("cp.async.wait_all;\n" ::);
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < 8; r++) {
-        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
-          acc[r][2 * h] = __vminu2(acc[r][2 * h], __byte_perm(w, 0, 0x4140) << U8_TAG);
-          acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], __byte_perm(w, 0, 0x4342) << U8_TAG);
-        }
+      for (int q = 0; q < 4; q++) {
+        acc[r][q] = U8_KINF * 0x00010001u;
+        kst[r][q] = 0u;
       }
-    }
-    if ((c & 1) || !more) {
-      uint32_t any = 0;
-#pragma unroll
-      for (int r = 0; r < 8; r++)
-#pragma unroll
-        for (int q = 0; q < 4; q++) any |= acc[r][q];
-      if (__any_sync(0xffffffffu, any & U8_TAGMASK2)) {
-        const uint32_t kb2 = uint32_t((c & ~int64_t(1)) * SUB) * 0x00010001u;
+    for (int64_t c = 0; c < nch; c++) {
+      const int64_t g = int64_t(tt) * nch + c;
+      const int slot = int(g % U8_STAGES);
+      mbar_wait(&sm.bar[slot], uint32_t((g / U8_STAGES) & 1));
+      const int64_t wc = c % U8_DEC_CHUNKS;   // chunk position inside the decode window
+#pragma unroll kU8Unroll
+      for (int kk = 0; kk < SUB; kk++) {
+        const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
+        const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
+        const uint2 b0 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][4 * tx]);
+        const uint2 b1 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][64 + 4 * tx]);
+        const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
         for (int r = 0; r < 8; r++)
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const uint32_t tg = acc[r][q] & U8_TAGMASK2;
-            const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
-            kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
-            acc[r][q] ^= tg;
+          for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
+      }
+      const bool more = c + 1 < nch;
+      if (c == 0) {
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 8; r++) {
+          const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
+            acc[r][2 * h] = __vminu2(acc[r][2 * h], __byte_perm(w, 0, 0x4140) << U8_TAG);
+            acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], __byte_perm(w, 0, 0x4342) << U8_TAG);
           }
+        }
+        __syncthreads();                      // Cs consumed: prefetch the next tile's C
+        if (tt + 1 < nt) prefetch_c(tt + 1);
       }
-    }
-    __syncthreads();   // every warp is done with this slot
-    if (t == 0 && c + U8_STAGES < nch) u8t_issue(sm, p, rt, ct, nch, c + U8_STAGES, slot);
-  }
-
-  bool changed = false;
-  uint8_t* Cw = static_cast<uint8_t*>(p.C);
-  const int32_t* __restrict__ pb = p.predB;
-  int32_t* __restrict__ out = p.idx;
-  const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
+      if (wc == U8_DEC_CHUNKS - 1 || !more) {
+        uint32_t any = 0;
 #pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
-    int32_t pv[2][4];
-    uint32_t ks[2][4];
+        for (int r = 0; r < 8; r++)
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
-      ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
-      const int64_t j = j0 + 64 * h + 4 * tx;
+          for (int q = 0; q < 4; q++) any |= acc[r][q];
+        if (__any_sync(0xffffffffu, any & U8_TAGMASK2)) {
+          const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
-        pv[h][q] = 0;
-        if (out && ks[h][q] != 0u)
-          pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
-                                          : int32_t(p.inner_off + ks[h][q] - 1u);
+          for (int r = 0; r < 8; r++)
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+              const uint32_t tg = acc[r][q] & U8_TAGMASK2;
+              const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
+              kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
+              acc[r][q] -= tg;
+            }
+        }
       }
+      __syncthreads();   // every warp is done with this slot
+      if (t == 0 && g + U8_STAGES < total_g) issue(g + U8_STAGES);
     }
+    // epilogue of tile tt (the next tile's first chunks and C are already in flight)
 #pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
-      if ((k0 | k1) == 0u) continue;
-      changed = true;
-      const int64_t j = j0 + 64 * h + 4 * tx;
-      *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) =
-          __byte_perm(acc[r][2 * h] >> U8_TAG, acc[r][2 * h + 1] >> U8_TAG, 0x6420);
-      if (!out) continue;
-      if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
-        *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
-      } else {
+    for (int r = 0; r < 8; r++) {
+      const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+      int32_t pv[2][4];
+      uint32_t ks[2][4];
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-          if (ks[h][q] != 0u) out[i * p.ldi + j + q] = pv[h][q];
+      for (int h = 0; h < 2; h++) {
+        const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+        ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
+        const int64_t j = j0 + 64 * h + 4 * tx;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          pv[h][q] = 0;
+          if (out && ks[h][q] != 0u)
+            pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
+                                            : int32_t(p.inner_off + ks[h][q] - 1u);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+        if ((k0 | k1) == 0u) continue;
+        changed = true;
+        const int64_t j = j0 + 64 * h + 4 * tx;
+        *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) =
+            __byte_perm(acc[r][2 * h] >> U8_TAG, acc[r][2 * h + 1] >> U8_TAG, 0x6420);
+        if (!out) continue;
+        if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
+          *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            if (ks[h][q] != 0u) out[i * p.ldi + j + q] = pv[h][q];
+        }
       }
     }
   }
@@ -499,7 +558,7 @@ __global__ void prep_u8_b_kernel(const uint8_t* B, int64_t ldb, int64_t nch, uin
   const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
   const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(B + (c * SUB + kk) * ldb + ct * BN + cb));
   const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-  const uint32_t tag = uint32_t(SUB * (c & 1) + kk + 1) * 0x00010001u;
+  const uint32_t tag = uint32_t(SUB * (c % U8_DEC_CHUNKS) + kk + 1) * 0x00010001u;   // 1..96 per window
   uint32_t o[8];
 #pragma unroll
   for (int q = 0; q < 4; q++) {
@@ -817,7 +876,16 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
         }
         if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc & 15))
           return set_error(2, "bulk-staged u8 tiles need full 128 x 128 tiles and 32-multiple k");
-        minplus_u8_tma_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemU8T), s>>>(a);
+        static int tpc = -1;
+        if (tpc < 0) {
+          const char* e = getenv("APSP_U8_TPC");
+          tpc = e ? atoi(e) : 1;   // >1 delays the lookahead side stream (measured slower)
+          if (tpc < 1) tpc = 1;
+          if (tpc > U8_TPC_MAX) tpc = U8_TPC_MAX;
+        }
+        const dim3 g2 = grid_for(a, BM, BN);
+        const int64_t tiles = int64_t(g2.x) * g2.y;
+        minplus_u8_tma_kernel<<<unsigned((tiles + tpc - 1) / tpc), NT, sizeof(SmemU8T), s>>>(a, tpc);
         break;
       }
       static bool attr = false;
