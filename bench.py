@@ -40,8 +40,9 @@ METRIC = "APSP time and min-plus updates/sec (n^3/s) at n=16384; % of FP32 CUDA-
 UNIT = "updates/s"
 FP32_CORE_PEAK = 148 * 128 * 1965e6 / 2          # 18.6 T upd/s at max clock
 # Measured issue ceilings of the inner-loop instruction of each tier (profiles/r01_microbench_ops.txt)
-TIER_PEAK = {"u8": 37.07e12, "w32": 24.91e12, "i32": 17.98e12, "f32": 6.05e12, "i64": 6.05e12}
-TIER_OP = {"u8": "VIADDMNMX.S16x2 (2 upd/instr)", "w32": "VIADD+VIMNMX3", "i32": "compare-select",
+TIER_PEAK = {"u8": 37.07e12, "u16": 37.07e12, "w32": 24.91e12, "i32": 17.98e12, "f32": 6.05e12, "i64": 6.05e12}
+TIER_OP = {"u8": "VIADDMNMX.U16x2 (2 upd/instr)", "u16": "VIADDMNMX.U16x2 (2 upd/instr)",
+           "w32": "VIADD+VIMNMX3", "i32": "compare-select",
            "f32": "FADD/FSETP/FSEL/SEL", "i64": "compare-select int64"}
 BLOCK = 256
 
@@ -287,7 +288,9 @@ def bench_single(args):
     upd_phase3 = (N // block) * (N - block) ** 2 * block
     achieved = upd_phase3 / (kms / 1e3) if kl else None
     peak = TIER_PEAK.get(tier)
-    roofline = {"bound": "alu", "kernel": f"minplus_{tier}_kernel (FW phase 3)", "op": TIER_OP.get(tier),
+    kname = f"minplus_nt_kernel<{tier}> (FW phase 3, bulk-staged)" if tier in ("u8", "u16") else \
+        f"minplus_{tier}_kernel (FW phase 3)"
+    roofline = {"bound": "alu", "kernel": kname, "op": TIER_OP.get(tier),
                 "achieved": achieved / 1e12 if achieved else None, "peak": peak / 1e12 if peak else None,
                 "unit": "T updates/s", "frac": (achieved / peak) if achieved and peak else None,
                 "traffic": None, "launches_per_step": kl, "kernel_share_of_step": (kms / ms_step) if kl else None,

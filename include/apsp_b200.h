@@ -47,11 +47,12 @@ typedef enum { APSP_DTYPE_I32 = 0, APSP_DTYPE_F32 = 1, APSP_DTYPE_I64 = 2 } apsp
 /* Value tiers (in-HBM store formats); AUTO picks the narrowest exact one and certifies it. */
 typedef enum {
   APSP_TIER_AUTO = -1,
-  APSP_TIER_U8 = 0,   /* uint8 store, 16-bit packed keys, VIADDMNMX.S16x2 */
+  APSP_TIER_U8 = 0,   /* uint8 store (values < 255), 16-bit packed keys, VIADDMNMX.U16x2 */
   APSP_TIER_W32 = 1,  /* int32 store (< 2^24), 32-bit keys, VIADD + VIMNMX3 */
   APSP_TIER_I32 = 2,  /* exact int32 compare-select */
   APSP_TIER_F32 = 3,  /* exact fp32 compare-select (continuous weights) */
-  APSP_TIER_I64 = 4   /* exact int64 compare-select (full reference range) */
+  APSP_TIER_I64 = 4,  /* exact int64 compare-select (full reference range) */
+  APSP_TIER_U16 = 5   /* uint16 store (values < 511), 16-bit packed keys, VIADDMNMX.U16x2 (aligned products) */
 } apsp_tier;
 
 typedef enum { APSP_IDX_PRED = 0, APSP_IDX_VIA = 1 } apsp_idx_mode;

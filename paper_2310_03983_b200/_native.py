@@ -27,8 +27,8 @@ OK, ERANGE, EINVAL, ECUDA, ENCCL, ENEGATIVE, EDIAGONAL, EDIMENSION, ECONVERGE = 
 # apsp_dtype
 DTYPE_I32, DTYPE_F32, DTYPE_I64 = 0, 1, 2
 # apsp_tier
-TIER_AUTO, TIER_U8, TIER_W32, TIER_I32, TIER_F32, TIER_I64 = -1, 0, 1, 2, 3, 4
-TIER_NAMES = {TIER_U8: "u8", TIER_W32: "w32", TIER_I32: "i32", TIER_F32: "f32", TIER_I64: "i64"}
+TIER_AUTO, TIER_U8, TIER_W32, TIER_I32, TIER_F32, TIER_I64, TIER_U16 = -1, 0, 1, 2, 3, 4, 5
+TIER_NAMES = {TIER_U8: "u8", TIER_U16: "u16", TIER_W32: "w32", TIER_I32: "i32", TIER_F32: "f32", TIER_I64: "i64"}
 # apsp_idx_mode
 IDX_PRED, IDX_VIA = 0, 1
 # apsp_algorithm

@@ -70,6 +70,7 @@ int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 int tier_store(int tier) {
   switch (tier) {
     case APSP_TIER_U8: return STORE_U8;
+    case APSP_TIER_U16: return STORE_U16;
     case APSP_TIER_W32: return STORE_W32;
     case APSP_TIER_I32: return STORE_I32;
     case APSP_TIER_F32: return STORE_F32;
@@ -85,6 +86,7 @@ int tier_store(int tier) {
 int64_t tier_limit(int tier) {
   switch (tier) {
     case APSP_TIER_U8: return U8_INF - 1;
+    case APSP_TIER_U16: return U16_INF - 1;
     case APSP_TIER_W32: return W32_INF - 1;
     case APSP_TIER_I32: return INF32 - 1;
     case APSP_TIER_I64: return MAX_FINITE_COST;
@@ -145,13 +147,17 @@ int check_scan(const ScanResult& sc) {
   return 0;
 }
 
-// Candidate tiers, narrowest first.
-std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced) {
+bool narrow_store(int store) { return store == STORE_U8 || store == STORE_U16; }
+
+// Candidate tiers, narrowest first.  allow_u16: the caller runs only aligned products (the
+// u16 tier exists only as bulk-staged tiles).
+std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced, bool allow_u16 = true) {
   const bool integral = dtype != APSP_DTYPE_F32 || !sc.non_integral;
   const int64_t w = sc.max_finite;
   if (forced >= 0) {
     // a forced tier must be able to hold the input (the certificate covers the result)
     bool fits = forced == APSP_TIER_U8 ? integral && w <= U8_INF - 1
+              : forced == APSP_TIER_U16 ? allow_u16 && integral && w <= U16_INF - 1
               : forced == APSP_TIER_W32 ? integral && w <= W32_INF - 1
               : forced == APSP_TIER_I32 ? (dtype != APSP_DTYPE_F32 && w <= INF32 - 1)
               : forced == APSP_TIER_F32 ? dtype == APSP_DTYPE_F32
@@ -161,6 +167,7 @@ std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced) {
   }
   std::vector<int> t;
   if (integral && w <= U8_INF - 1) t.push_back(APSP_TIER_U8);
+  if (allow_u16 && integral && w <= U16_INF - 1) t.push_back(APSP_TIER_U16);
   if (integral && w <= W32_INF - 1) t.push_back(APSP_TIER_W32);
   if (dtype == APSP_DTYPE_F32) t.push_back(APSP_TIER_F32);
   else if (dtype == APSP_DTYPE_I32) t.push_back(APSP_TIER_I32);
@@ -200,14 +207,18 @@ struct FwCtx {
   int32_t* predsnap = nullptr;   // b x m
   char* rowsnap = nullptr;       // b x m values (b > 128 only)
   char* colsnap = nullptr;       // m x b values (b > 128 only)
-  char* prep[2] = {nullptr, nullptr};  // u8 tier: bulk-copy layouts of the panels, by round parity
+  char* prep[2] = {nullptr, nullptr};  // narrow tiers: bulk-copy layouts of the panels, by round parity
+  char* p2prep = nullptr;        // narrow tiers: bulk-copy layouts of the phase-2 operands
+  char* sub = nullptr;           // scratch of the phase-1 sub-run when b > 128
   int launches = 0;
 };
 
 size_t fw_scratch_bytes(int64_t m, int b, size_t es) {
-  size_t v = size_t(b) * m * 4 + 256;
-  if (b > TILE_ALIGN) v += 2 * size_t(b) * m * es + 256;
-  v += 2 * (prep_u8_bytes(m, m, b) + 256);
+  size_t v = size_t(b) * m * 4 + 256;                      // pred row-panel snapshot
+  if (b > TILE_ALIGN) v += 2 * size_t(b) * m * es + 256;   // value snapshots (non-narrow tiers)
+  v += 2 * (prep_u8_bytes(m, m, b) + 256);                 // phase-3 panel layouts (double buffered)
+  v += prep_u8_bytes(m, b, b) + 256;                       // phase-2 layouts (max of row/col product)
+  if (b > TILE_ALIGN) v += fw_scratch_bytes(b, TILE_ALIGN, es) + 256;   // phase-1 sub-run
   return v;
 }
 
@@ -225,6 +236,9 @@ void fw_carve(FwCtx& c, char* scratch, int64_t N) {
     c.prep[q] = p;
     p += prep_u8_bytes(N, N, c.b) + 256;
   }
+  c.p2prep = p;
+  p += prep_u8_bytes(N, c.b, c.b) + 256;
+  if (c.b > TILE_ALIGN) c.sub = p;
 }
 
 uint32_t* prep_a(char* slot) { return reinterpret_cast<uint32_t*>(slot); }
@@ -253,6 +267,8 @@ int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s) {
   sub.via_off = c.via_off + k0;
   sub.side = nullptr;
   sub.rowsnap = sub.colsnap = nullptr;
+  sub.prep[0] = sub.prep[1] = sub.p2prep = sub.sub = nullptr;
+  if (c.sub) fw_carve(sub, c.sub, c.b);
   sub.launches = 0;
   const int rc = fw_run(sub, s);
   c.launches += sub.launches;
@@ -265,13 +281,15 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   char* Dg = c.D + (k0 * c.ld + k0) * c.es;
   char* rowp = c.D + k0 * c.ld * c.es;
   char* colp = c.D + k0 * c.es;
-  const bool snap = b > TILE_ALIGN;
+  const bool nt = narrow_store(c.store) && c.p2prep;   // bulk-staged narrow tiles (prep = snapshot)
+  const bool snap = !nt && b > TILE_ALIGN;
   if (c.P && c.mode == IDX_PRED) {
     APSP_CUDA_TRY(cudaMemcpy2DAsync(c.predsnap, size_t(m) * 4, c.P + k0 * c.ldp, size_t(c.ldp) * 4, size_t(m) * 4,
                                     size_t(b), cudaMemcpyDeviceToDevice, s));
   }
+  int rc = 0;
   if (snap) {
-    int rc = launch_copy_block(c.store, rowp, c.ld, c.rowsnap, m, b, m, s);
+    rc = launch_copy_block(c.store, rowp, c.ld, c.rowsnap, m, b, m, s);
     if (!rc) rc = launch_copy_block(c.store, colp, c.ld, c.colsnap, b, m, b, s);
     if (rc) return rc;
   }
@@ -286,7 +304,14 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   a.mode = c.mode;
   a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
   a.status = c.st;
-  int rc = launch_minplus(c.store, a, s);
+  if (nt) {
+    rc = launch_prep_narrow(c.store, Dg, c.ld, rowp, c.ld, b, m, b, prep_a(c.p2prep), prep_b(c.p2prep, b, b), s);
+    if (rc) return rc;
+    a.Aprep = prep_a(c.p2prep);
+    a.Bprep = prep_b(c.p2prep, b, b);
+    c.launches += 2;
+  }
+  rc = launch_minplus(c.store, a, s);
   if (rc) return rc;
   MinplusArgs q = minplus_args();
   q.A = snap ? c.colsnap : colp; q.lda = snap ? b : c.ld;
@@ -299,12 +324,19 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   q.mode = c.mode;
   q.skip_row_lo = k0; q.skip_row_hi = k0 + b;
   q.status = c.st;
+  if (nt) {
+    rc = launch_prep_narrow(c.store, colp, c.ld, Dg, c.ld, m, b, b, prep_a(c.p2prep), prep_b(c.p2prep, m, b), s);
+    if (rc) return rc;
+    q.Aprep = prep_a(c.p2prep);
+    q.Bprep = prep_b(c.p2prep, m, b);
+    c.launches += 2;
+  }
   c.launches += 2;
   rc = launch_minplus(c.store, q, s);
-  if (rc || !c.prep[0] || c.store != STORE_U8) return rc;
+  if (rc || !c.prep[0] || !narrow_store(c.store)) return rc;
   char* slot = c.prep[(k0 / b) & 1];
   c.launches += 2;
-  return launch_prep_u8(colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
+  return launch_prep_narrow(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
 }
 
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
@@ -325,7 +357,7 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   if (only_next >= 0) { a.only_lo = only_next; a.only_hi = only_next + c.b; }
   if (skip_next >= 0) { a.skip2_lo = skip_next; a.skip2_hi = skip_next + c.b; }
   a.status = c.st;
-  if (c.prep[0] && c.store == STORE_U8) {
+  if (c.prep[0] && narrow_store(c.store)) {
     char* slot = c.prep[(k0 / c.b) & 1];
     a.Aprep = prep_a(slot);
     a.Bprep = prep_b(slot, c.m, c.b);
@@ -381,14 +413,17 @@ cudaStream_t side_stream() {
   return streams[dev];
 }
 
-// convenience for callers with a plain view (R-Kleene leaves): no lookahead
+// convenience for callers with a plain view (R-Kleene leaves): no lookahead; scratch laid out
+// by fw_carve (fw_scratch_bytes(m, b, es) bytes) or, if null, only a pred snapshot
 int fw_blocked_view(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t m, int b, int mode,
-                    int64_t via_off, Status* st, cudaStream_t s, int* launches, int32_t* predsnap) {
+                    int64_t via_off, Status* st, cudaStream_t s, int* launches, int32_t* predsnap,
+                    char* scratch = nullptr) {
   FwCtx c;
   c.store = store; c.es = store_elem_size(store);
   c.D = static_cast<char*>(D); c.ld = ld; c.P = P; c.ldp = ldp;
   c.m = m; c.b = b; c.mode = mode; c.via_off = via_off; c.st = st;
-  c.predsnap = predsnap;
+  if (scratch) fw_carve(c, scratch, m);
+  else c.predsnap = predsnap;
   const int rc = fw_run(c, s);
   *launches += c.launches;
   return rc;
@@ -594,6 +629,8 @@ struct RK {
   int64_t sld;
   Status* st;
   cudaStream_t s;
+  char* prep = nullptr;     // narrow tiers, aligned split: bulk-copy operand layouts (half x half)
+  char* leafws = nullptr;   // aligned leaves: fw_scratch_bytes(thr, 128, es)
   int launches = 0;
 
   char* at(int64_t i, int64_t j) const { return D + (i * ld + j) * es; }
@@ -612,6 +649,13 @@ struct RK {
     a.mode = mode;
     a.status = st;
     launches++;
+    if (prep && narrow_store(store) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
+      int rc = launch_prep_narrow(store, A, lda, B, ldb, m, n, k, prep_a(prep), prep_b(prep, m, k), s);
+      if (rc) return rc;
+      a.Aprep = prep_a(prep);
+      a.Bprep = prep_b(prep, m, k);
+      launches += 2;
+    }
     return timed_minplus(store, a, s);
   }
   int snap_vals(int64_t r0, int64_t c0, int64_t rows, int64_t cols) {
@@ -635,7 +679,7 @@ struct RK {
   int leaf(int64_t lo, int64_t m) {
     if (aligned && m > 128) {
       return fw_blocked_view(store, at(lo, lo), ld, pat(lo, lo), ld, m, DEFAULT_BLOCK, mode, lo, st, s, &launches,
-                             sP);
+                             sP, leafws);
     }
     launches += int(m > 128 ? m : 1);
     return launch_block_close(store, D, ld, lo, m, P, ld, mode, lo, st, s);
@@ -678,11 +722,19 @@ int64_t rk_half(int64_t N, int aligned) {
   return aligned ? ((N / TILE_ALIGN + 1) / 2) * TILE_ALIGN : N - N / 2;
 }
 
-size_t rk_ws_bytes(int dtype, int64_t n, int aligned) {
+size_t rk_extra_bytes(int64_t N, int aligned, int thr) {
+  if (!aligned) return 0;
+  const int64_t h = rk_half(N, aligned);
+  const int64_t leaf = std::max<int64_t>(round_up(std::min<int64_t>(thr, N), TILE_ALIGN), TILE_ALIGN);
+  return prep_u8_bytes(h, h, h) + 512 + fw_scratch_bytes(leaf, TILE_ALIGN, 4) + 512;
+}
+
+size_t rk_ws_bytes(int dtype, int64_t n, int aligned, int thr = 1 << 30) {
   const int64_t N = aligned ? round_up(n, TILE_ALIGN) : n;
   const int64_t h = rk_half(N, aligned);
   const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
-  return header_bytes() + size_t(N) * N * (es + 4) + size_t(h + 8) * (h + 8) * (es + 4) + 1024;
+  return header_bytes() + size_t(N) * N * (es + 4) + size_t(h + 8) * (h + 8) * (es + 4) + 1024 +
+         rk_extra_bytes(N, aligned, thr);
 }
 
 int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int64_t ldi, int idx_mode, int thr,
@@ -692,7 +744,7 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
   const int64_t N = aligned ? round_up(n, TILE_ALIGN) : n;
   const int64_t h = rk_half(N, aligned);
   Scratch sc;
-  int rc = sc.acquire(ws, ws_bytes, rk_ws_bytes(dtype, n, aligned), s);
+  int rc = sc.acquire(ws, ws_bytes, rk_ws_bytes(dtype, n, aligned, thr), s);
   if (rc) return rc;
   Header* hdr_dev = static_cast<Header*>(sc.base);
   char* p = static_cast<char*>(sc.base) + header_bytes();
@@ -703,6 +755,9 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
   char* D = p;
   p += size_t(N) * N * (dtype == APSP_DTYPE_I64 ? 8 : 4);
   char* sV = p;
+  p += size_t(h + 8) * (h + 8) * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 512;
+  char* rkprep = aligned ? p : nullptr;
+  char* leafws = aligned ? p + ((prep_u8_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
   Header hdr{};
   Timer tm(s);
   rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
@@ -716,7 +771,7 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
     if (!rc && info) info->flags |= FLAG_CLASSIC_FOR_ZERO_EDGES;
     return rc;
   }
-  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req);
+  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, aligned != 0);
   if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
   int used = -1, tried = 0, launches = 2;
   for (int tier : tiers) {
@@ -728,6 +783,8 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
     rc = launch_to_store(dtype, dist, ld, n, store, D, N, N, idx_mode == IDX_PRED ? P : nullptr, N, 1, s);
     if (!rc && idx_mode == IDX_VIA) rc = launch_fill_idx(P, N, N, N, -1, s);
     RK rk{store, store_elem_size(store), D, N, P, idx_mode, thr, aligned != 0, sV, sP, h, &hdr_dev->status, s};
+    rk.prep = rkprep;
+    rk.leafws = leafws;
     if (!rc) rc = rk.close(0, N);
     bool ok = false;
     if (!rc) rc = certify(tier, store, D, N, n, n, scan, hdr_dev, hdr, s, ok);
@@ -787,7 +844,7 @@ int squaring_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, in
   const ScanResult scan = hdr.scan;
   rc = check_scan(scan);
   if (rc) return rc;
-  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req);
+  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, false);
   if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
   int used = -1, tried = 0, iters = 0, launches = 2;
   char* cur = D0;
@@ -904,7 +961,7 @@ int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
     else tier = APSP_TIER_I64;
   }
   const int store = tier_store(tier);
-  if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  if (store < 0 || store == STORE_U16) return set_error(APSP_EINVAL, "tier %d not available for products", tier);
   rc = launch_to_store_rect(dtype, x, ldx, n1, n2, store, Xs, n2, s);
   if (!rc) rc = launch_to_store_rect(dtype, y, ldy, n2, n3, store, Ys, n3, s);
   if (rc) return rc;
@@ -989,6 +1046,7 @@ static int rect_d(const void* h, int64_t ldh, int64_t rows, int64_t cols, int st
     case STORE_I32: to_store_rect_kernel<D, STORE_I32><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (int32_t*)out, ldo); break;
     case STORE_F32: to_store_rect_kernel<D, STORE_F32><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (float*)out, ldo); break;
     case STORE_I64: to_store_rect_kernel<D, STORE_I64><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (int64_t*)out, ldo); break;
+    case STORE_U16: to_store_rect_kernel<D, STORE_U16><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (uint16_t*)out, ldo); break;
     default: return set_error(APSP_EINVAL, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
@@ -1018,9 +1076,35 @@ int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows,
 namespace {
 
 size_t shard_scratch_bytes(int64_t N, int64_t R, int b, size_t es) {
-  size_t v = size_t(b) * N * 4 + 256;                   // pred row-panel snapshot
-  if (b > TILE_ALIGN) v += size_t(b) * N * es + size_t(R) * b * es + 512;   // value snapshots
+  size_t v = size_t(b) * N * 4 + 256;                                         // pred row-panel snapshot
+  if (b > TILE_ALIGN) v += size_t(b) * N * es + size_t(R) * b * es + 512;     // value snapshots
+  v += std::max(prep_u8_bytes(b, N, b), prep_u8_bytes(std::max<int64_t>(R, b), N, b)) + 256;   // panel layouts
+  if (b > TILE_ALIGN) v += fw_scratch_bytes(b, TILE_ALIGN, es) + 256;        // phase-1 sub-run
   return v;
+}
+
+struct ShardScratch {
+  int32_t* predsnap;
+  char* rowsnap;
+  char* colsnap;
+  char* prep;
+  char* sub;
+};
+
+ShardScratch shard_carve(void* scratch, int64_t N, int64_t R, int b, size_t es) {
+  ShardScratch c{};
+  char* p = static_cast<char*>(scratch);
+  c.predsnap = reinterpret_cast<int32_t*>(p);
+  p += size_t(b) * N * 4 + 256;
+  if (b > TILE_ALIGN) {
+    c.rowsnap = p;
+    c.colsnap = p + size_t(b) * N * es + 256;
+    p += size_t(b) * N * es + size_t(R) * b * es + 512;
+  }
+  c.prep = p;
+  p += std::max(prep_u8_bytes(b, N, b), prep_u8_bytes(std::max<int64_t>(R, b), N, b)) + 256;
+  if (b > TILE_ALIGN) c.sub = p;
+  return c;
 }
 
 int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
@@ -1029,29 +1113,37 @@ int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* 
   if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
   const size_t es = store_elem_size(store);
   if (scratch_bytes < shard_scratch_bytes(N, b, b, es)) return set_error(APSP_EINVAL, "shard scratch too small");
+  const ShardScratch sc = shard_carve(scratch, N, b, b, es);
   char* D = static_cast<char*>(Dv);
   FwCtx c;
   c.store = store; c.es = es;
   c.D = D + (lrow * ld + k0) * es; c.ld = ld;
   c.P = P ? P + lrow * ldp + k0 : nullptr; c.ldp = ldp;
   c.m = b; c.b = b; c.mode = IDX_PRED; c.via_off = k0;
-  c.predsnap = static_cast<int32_t*>(scratch);
+  c.predsnap = sc.predsnap;
+  c.sub = sc.sub;
   int rc = fw_phase1(c, 0, s);                           // diagonal block, classic order
   if (rc) return rc;
   char* rowp = D + lrow * ld * es;
-  const bool snap = b > TILE_ALIGN;
-  char* rowsnap = static_cast<char*>(scratch) + size_t(b) * N * 4 + 256;
-  if (P) APSP_CUDA_TRY(cudaMemcpy2DAsync(c.predsnap, size_t(N) * 4, P + lrow * ldp, size_t(ldp) * 4, size_t(N) * 4,
+  const bool nt = narrow_store(store);
+  const bool snap = !nt && b > TILE_ALIGN;
+  if (P) APSP_CUDA_TRY(cudaMemcpy2DAsync(sc.predsnap, size_t(N) * 4, P + lrow * ldp, size_t(ldp) * 4, size_t(N) * 4,
                                          size_t(b), cudaMemcpyDeviceToDevice, s));
-  if (snap && (rc = launch_copy_block(store, rowp, ld, rowsnap, N, b, N, s))) return rc;
+  if (snap && (rc = launch_copy_block(store, rowp, ld, sc.rowsnap, N, b, N, s))) return rc;
   MinplusArgs a = minplus_args();
   a.A = c.D; a.lda = ld;
-  a.B = snap ? rowsnap : rowp; a.ldb = snap ? N : ld;
+  a.B = snap ? sc.rowsnap : rowp; a.ldb = snap ? N : ld;
   a.C = rowp; a.ldc = ld;
   a.idx = P ? P + lrow * ldp : nullptr; a.ldi = ldp;
-  a.predB = c.predsnap; a.ldp = N;
+  a.predB = sc.predsnap; a.ldp = N;
   a.m = b; a.n = N; a.k = b; a.inner_off = k0; a.mode = IDX_PRED;
   a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
+  if (nt) {
+    if ((rc = launch_prep_narrow(store, c.D, ld, rowp, ld, b, N, b, prep_a(sc.prep), prep_b(sc.prep, b, b), s)))
+      return rc;
+    a.Aprep = prep_a(sc.prep);
+    a.Bprep = prep_b(sc.prep, b, b);
+  }
   return launch_minplus(store, a, s);
 }
 
@@ -1064,23 +1156,31 @@ int shard_update_impl(int tier, int64_t N, int b, int64_t row_lo, int64_t row_hi
   if (R <= 0) return 0;
   const size_t es = store_elem_size(store);
   if (scratch_bytes < shard_scratch_bytes(N, R, b, es)) return set_error(APSP_EINVAL, "shard scratch too small");
+  const ShardScratch sc = shard_carve(scratch, N, R, b, es);
   char* D = static_cast<char*>(Dv) + row_lo * ld * es;      // the processed row range
   int32_t* Pr = P ? P + row_lo * ldp : nullptr;
   const char* pv = static_cast<const char*>(panel);
-  const bool snap = b > TILE_ALIGN;
+  const bool nt = narrow_store(store);
+  const bool snap = !nt && b > TILE_ALIGN;
   const bool skip = skip_lo >= 0 && skip_hi > skip_lo;
-  char* colsnap = static_cast<char*>(scratch) + size_t(b) * N * 4 + 256 + size_t(b) * N * es + 256;
   int rc = 0;
-  if (snap && (rc = launch_copy_block(store, D + k0 * es, ld, colsnap, b, R, b, s))) return rc;
+  if (snap && (rc = launch_copy_block(store, D + k0 * es, ld, sc.colsnap, b, R, b, s))) return rc;
   // column panel of the rows against the (received) closed diagonal block
   MinplusArgs q = minplus_args();
-  q.A = snap ? colsnap : D + k0 * es; q.lda = snap ? b : ld;
+  q.A = snap ? sc.colsnap : D + k0 * es; q.lda = snap ? b : ld;
   q.B = pv + k0 * es; q.ldb = ldpv;
   q.C = D + k0 * es; q.ldc = ld;
   q.idx = Pr ? Pr + k0 : nullptr; q.ldi = ldp;
   q.predB = ppanel ? ppanel + k0 : nullptr; q.ldp = ldpp;
   q.m = R; q.n = b; q.k = b; q.inner_off = k0; q.mode = IDX_PRED;
   if (skip) { q.skip_row_lo = skip_lo - row_lo; q.skip_row_hi = skip_hi - row_lo; }
+  if (nt) {
+    if ((rc = launch_prep_narrow(store, D + k0 * es, ld, pv + k0 * es, ldpv, R, b, b, prep_a(sc.prep),
+                                 prep_b(sc.prep, R, b), s)))
+      return rc;
+    q.Aprep = prep_a(sc.prep);
+    q.Bprep = prep_b(sc.prep, R, b);
+  }
   if ((rc = launch_minplus(store, q, s))) return rc;
   // phase 3 of the rows
   MinplusArgs a = minplus_args();
@@ -1092,6 +1192,13 @@ int shard_update_impl(int tier, int64_t N, int b, int64_t row_lo, int64_t row_hi
   a.m = R; a.n = N; a.k = b; a.inner_off = k0; a.mode = IDX_PRED;
   if (skip) { a.skip_row_lo = skip_lo - row_lo; a.skip_row_hi = skip_hi - row_lo; }
   a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
+  if (nt) {
+    if ((rc = launch_prep_narrow(store, D + k0 * es, ld, pv, ldpv, R, N, b, prep_a(sc.prep), prep_b(sc.prep, R, b),
+                                 s)))
+      return rc;
+    a.Aprep = prep_a(sc.prep);
+    a.Bprep = prep_b(sc.prep, R, b);
+  }
   return timed_minplus(store, a, s);
 }
 
@@ -1174,7 +1281,7 @@ size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block) {
   switch (algorithm) {
     case APSP_ALG_FW_BLOCKED: return std::max(fw_ws_bytes(dtype, n, block > 0 ? block : 256),
                                               fw_ws_bytes(dtype, n, block > 0 ? block : DEFAULT_BLOCK));
-    case APSP_ALG_RKLEENE: return std::max(rk_ws_bytes(dtype, n, 1), rk_ws_bytes(dtype, n, 0));
+    case APSP_ALG_RKLEENE: return std::max(rk_ws_bytes(dtype, n, 1, 1 << 30), rk_ws_bytes(dtype, n, 0));
     case APSP_ALG_FW_SQUARING: return sq_ws_bytes(dtype, n);
     case APSP_ALG_FW_CLASSIC: return 0;
   }

@@ -5,7 +5,8 @@
 // makes "strict c < d" saturate at Infinity with no branch (the reference gets the same
 // effect from INF_RAW = 2^61, core.py:19-20):
 //
-//   STORE_U8    uint8_t  finite 0..254, INF 255      narrow tier (keys are 16-bit, s16x2 DPX)
+//   STORE_U8    uint8_t  finite 0..254, INF 255      narrow tier (16-bit keys, 7-bit tags, u16x2 DPX)
+//   STORE_U16   uint16_t finite 0..510, INF 511      narrow tier (16-bit keys, 6-bit tags, u16x2 DPX)
 //   STORE_W32   int32_t  finite 0..2^24-2, INF 2^24-1 wide tier   (keys are 32-bit)
 //   STORE_I32   int32_t  finite 0..2^30-2, INF 0x3FFFFFFF   exact int32 (API format)
 //   STORE_F32   float    finite >= 0, INF +inf             exact fp32 (API format)
@@ -21,7 +22,7 @@
 
 namespace apsp {
 
-enum Store : int { STORE_U8 = 0, STORE_W32 = 1, STORE_I32 = 2, STORE_F32 = 3, STORE_I64 = 4 };
+enum Store : int { STORE_U8 = 0, STORE_W32 = 1, STORE_I32 = 2, STORE_F32 = 3, STORE_I64 = 4, STORE_U16 = 5 };
 
 constexpr int32_t INF32 = 0x3FFFFFFF;
 constexpr int64_t INF_RAW = int64_t(1) << 61;
@@ -30,6 +31,7 @@ constexpr int64_t MAX_FINITE_COST = (int64_t(1) << 60) - 1;
 constexpr int TAG_BITS = 6;
 constexpr int SUB = 32;                 // k-steps between argmin decodes (tags 1..32)
 constexpr int U8_INF = 255;
+constexpr int U16_INF = 511;
 constexpr int32_t W32_INF = 0x00FFFFFF;
 constexpr uint32_t K16_INF = uint32_t(U8_INF) << TAG_BITS;      // 16320; 2*K16_INF+32 < 2^15
 constexpr int32_t K32_INF = W32_INF << TAG_BITS;                 // 0x3FFFFFC0
@@ -42,6 +44,7 @@ template <> struct StoreT<STORE_W32> { using T = int32_t;  using A = int32_t; st
 template <> struct StoreT<STORE_I32> { using T = int32_t;  using A = int32_t; static constexpr bool keyed = false; };
 template <> struct StoreT<STORE_F32> { using T = float;    using A = float;   static constexpr bool keyed = false; };
 template <> struct StoreT<STORE_I64> { using T = int64_t;  using A = int64_t; static constexpr bool keyed = false; };
+template <> struct StoreT<STORE_U16> { using T = uint16_t; using A = int32_t; static constexpr bool keyed = true; };
 
 template <int S> __host__ __device__ inline typename StoreT<S>::T store_inf();
 template <> __host__ __device__ inline uint8_t store_inf<STORE_U8>() { return U8_INF; }
@@ -49,6 +52,7 @@ template <> __host__ __device__ inline int32_t store_inf<STORE_W32>() { return W
 template <> __host__ __device__ inline int32_t store_inf<STORE_I32>() { return INF32; }
 template <> __host__ __device__ inline float store_inf<STORE_F32>() { return __builtin_huge_valf(); }
 template <> __host__ __device__ inline int64_t store_inf<STORE_I64>() { return INF_RAW; }
+template <> __host__ __device__ inline uint16_t store_inf<STORE_U16>() { return U16_INF; }
 
 // Overflow rule of the int64 domain (solvers.py:91-92): a strictly improving finite sum
 // above MAX_FINITE_COST is a range error.  The narrower domains never report it: their

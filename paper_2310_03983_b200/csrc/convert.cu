@@ -15,6 +15,7 @@ size_t store_elem_size(int store) {
     case STORE_U8: return 1;
     case STORE_W32: case STORE_I32: case STORE_F32: return 4;
     case STORE_I64: return 8;
+    case STORE_U16: return 2;
   }
   return 0;
 }
@@ -128,6 +129,7 @@ static int to_store_d(const void* h, int64_t ldh, int64_t n, int store, void* Dp
     case STORE_I32: to_store_kernel<D, STORE_I32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
     case STORE_F32: to_store_kernel<D, STORE_F32><<<g, 256, 0, s>>>(hh, ldh, n, (float*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
     case STORE_I64: to_store_kernel<D, STORE_I64><<<g, 256, 0, s>>>(hh, ldh, n, (int64_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
+    case STORE_U16: to_store_kernel<D, STORE_U16><<<g, 256, 0, s>>>(hh, ldh, n, (uint16_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
     default: return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
@@ -199,6 +201,7 @@ int launch_from_store(int store, const void* D, int64_t ld, int64_t rows, int64_
     case STORE_I32: return from_store_s<STORE_I32>(D, ld, rows, cols, out_dtype, out, ldo, s);
     case STORE_F32: return from_store_s<STORE_F32>(D, ld, rows, cols, out_dtype, out, ldo, s);
     case STORE_I64: return from_store_s<STORE_I64>(D, ld, rows, cols, out_dtype, out, ldo, s);
+    case STORE_U16: return from_store_s<STORE_U16>(D, ld, rows, cols, out_dtype, out, ldo, s);
   }
   return set_error(2, "unknown store %d", store);
 }
@@ -280,6 +283,7 @@ int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_
     case STORE_I32: max_finite_kernel<STORE_I32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev); break;
     case STORE_F32: max_finite_kernel<STORE_F32><<<g, 256, 0, s>>>((const float*)D, ld, rows, cols, out_dev); break;
     case STORE_I64: max_finite_kernel<STORE_I64><<<g, 256, 0, s>>>((const int64_t*)D, ld, rows, cols, out_dev); break;
+    case STORE_U16: max_finite_kernel<STORE_U16><<<g, 256, 0, s>>>((const uint16_t*)D, ld, rows, cols, out_dev); break;
     default: return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
@@ -325,6 +329,7 @@ int launch_witness_clear(int store, const void* X, int64_t ldx, const void* Y, i
     case STORE_I32: WC(STORE_I32, int32_t); break;
     case STORE_F32: WC(STORE_F32, float); break;
     case STORE_I64: WC(STORE_I64, int64_t); break;
+    case STORE_U16: WC(STORE_U16, uint16_t); break;
     default: return set_error(2, "unknown store %d", store);
   }
 #undef WC

@@ -57,6 +57,7 @@ int launch_fw_step(int store, void* D, int64_t ld, int64_t n, int64_t k, int32_t
     case STORE_I32: fw_step_kernel<STORE_I32><<<grid, 256, 0, s>>>((int32_t*)D, ld, n, k, idx, ldi, mode, via_off, st); break;
     case STORE_F32: fw_step_kernel<STORE_F32><<<grid, 256, 0, s>>>((float*)D, ld, n, k, idx, ldi, mode, via_off, st); break;
     case STORE_I64: fw_step_kernel<STORE_I64><<<grid, 256, 0, s>>>((int64_t*)D, ld, n, k, idx, ldi, mode, via_off, st); break;
+    case STORE_U16: fw_step_kernel<STORE_U16><<<grid, 256, 0, s>>>((uint16_t*)D, ld, n, k, idx, ldi, mode, via_off, st); break;
     case STORE_U8: fw_step_kernel<STORE_U8><<<grid, 256, 0, s>>>((uint8_t*)D, ld, n, k, idx, ldi, mode, via_off, st); break;
     case STORE_W32: fw_step_kernel<STORE_W32><<<grid, 256, 0, s>>>((int32_t*)D, ld, n, k, idx, ldi, mode, via_off, st); break;
     default: return set_error(2, "unknown store %d", store);
@@ -377,6 +378,7 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
     case STORE_I32: return close_impl<STORE_I32>(D, ld, lo, m, idx, ldi, mode, via_off, st, s);
     case STORE_F32: return close_impl<STORE_F32>(D, ld, lo, m, idx, ldi, mode, via_off, st, s);
     case STORE_I64: return close_impl<STORE_I64>(D, ld, lo, m, idx, ldi, mode, via_off, st, s);
+    case STORE_U16: return close_impl<STORE_U16>(D, ld, lo, m, idx, ldi, mode, via_off, st, s);
   }
   return set_error(2, "unknown store %d", store);
 }
@@ -543,6 +545,7 @@ static int panel_cols_impl(const void* Dg, int64_t ldg, const int32_t* PDg, int6
     case STORE_I32: return CALL(STORE_I32);                    \
     case STORE_F32: return CALL(STORE_F32);                    \
     case STORE_I64: return CALL(STORE_I64);                    \
+    case STORE_U16: return CALL(STORE_U16);                    \
     default: return set_error(2, "unknown store %d", store);   \
   }
 

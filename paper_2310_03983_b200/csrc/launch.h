@@ -37,6 +37,8 @@ struct MinplusArgs {
 size_t prep_u8_bytes(int64_t m, int64_t n, int64_t k);
 int launch_prep_u8(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n, int64_t k,
                    uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s);
+int launch_prep_narrow(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
+                       int64_t k, uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s);
 
 // Default-initialised args: nothing skipped, full grid.
 inline MinplusArgs minplus_args() {

@@ -306,14 +306,30 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
 }
 
 // ------------------------------------------------------------------------------------
-// narrow tier with pre-laid-out panels: cp.async.bulk (TMA bulk copy) + mbarrier 3-stage ring
+// narrow tiers with pre-laid-out panels: cp.async.bulk (TMA bulk copy) + mbarrier 3-stage ring
+//   u8  : uint8 store,  values 0..254, key = v << 7 | tag, decode window 3 chunks (tags 1..96)
+//   u16 : uint16 store, values 0..510, key = v << 6 | tag, decode window 1 chunk  (tags 1..32)
+// Keys are unsigned 16-bit: INF + INF + tag < 2^16 in both (VIADDMNMX.U16x2).
 // ------------------------------------------------------------------------------------
+template <int S> struct Narrow;
+template <> struct Narrow<STORE_U8> {
+  using T = uint8_t;
+  static constexpr int TAG = 7, WIN = 3;
+  static constexpr uint32_t INF = U8_INF;
+};
+template <> struct Narrow<STORE_U16> {
+  using T = uint16_t;
+  static constexpr int TAG = 6, WIN = 1;
+  static constexpr uint32_t INF = U16_INF;
+};
+
 constexpr int U8_STAGES = 3;
 constexpr uint32_t U8_CHUNK_A = SUB * BM * 4, U8_CHUNK_B = SUB * BN * 2;
-struct SmemU8T {
+template <int S>
+struct SmemNT {
   uint32_t As[U8_STAGES][SUB][BM];
   uint16_t Bs[U8_STAGES][SUB][BN];
-  uint8_t Cs[BM][BN];
+  typename Narrow<S>::T Cs[BM][BN];
   unsigned long long bar[U8_STAGES];
 };
 
@@ -342,13 +358,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(b))
       : "memory");
-}
-
-__device__ __forceinline__ void u8t_issue(SmemU8T& sm, const MinplusArgs& p, int64_t rt, int64_t ct, int64_t nch,
-                                          int64_t c, int slot) {
-  mbar_expect_tx(&sm.bar[slot], U8_CHUNK_A + U8_CHUNK_B);
-  bulk_g2s(&sm.As[slot][0][0], p.Aprep + (rt * nch + c) * (SUB * BM), U8_CHUNK_A, &sm.bar[slot]);
-  bulk_g2s(&sm.Bs[slot][0][0], p.Bprep + (ct * nch + c) * (SUB * BN), U8_CHUNK_B, &sm.bar[slot]);
 }
 
 // Tile origin of virtual tile index v (the 2D grid flattened row-major, or the cross list).
@@ -381,11 +390,17 @@ __device__ __forceinline__ int64_t tile_count(const MinplusArgs& p, int bm, int 
 }
 
 constexpr int U8_TPC_MAX = 8;       // tiles per CTA (ring and C prefetch run across tiles)
-constexpr int U8_DEC_CHUNKS = 3;    // decode window: 3 chunks = 96 k, tags 1..96 (7 bits)
 
-__global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, int tpc) {
-  extern __shared__ __align__(128) unsigned char smraw_u8t[];
-  SmemU8T& sm = *reinterpret_cast<SmemU8T*>(smraw_u8t);
+template <int S>
+__global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p, int tpc) {
+  using NR = Narrow<S>;
+  using T = typename NR::T;
+  constexpr int TAG = NR::TAG, WIN = NR::WIN;
+  constexpr uint32_t KINF2 = (NR::INF << TAG) * 0x00010001u;
+  constexpr uint32_t TMASK2 = ((1u << TAG) - 1u) * 0x00010001u;
+  constexpr int CB = BN * int(sizeof(T)) / 2;     // C bytes per thread-half-row
+  extern __shared__ __align__(128) unsigned char smraw_nt[];
+  SmemNT<S>& sm = *reinterpret_cast<SmemNT<S>*>(smraw_nt);
   __shared__ int64_t tiles_i0[U8_TPC_MAX], tiles_j0[U8_TPC_MAX];
   __shared__ int ntiles;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
@@ -412,17 +427,20 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, in
   auto issue = [&](int64_t g) {
     const int tt = int(g / nch);
     const int64_t c = g - int64_t(tt) * nch;
-    u8t_issue(sm, p, tiles_i0[tt] / BM, tiles_j0[tt] / BN, nch, c, int(g % U8_STAGES));
+    const int slot = int(g % U8_STAGES);
+    mbar_expect_tx(&sm.bar[slot], U8_CHUNK_A + U8_CHUNK_B);
+    bulk_g2s(&sm.As[slot][0][0], p.Aprep + ((tiles_i0[tt] / BM) * nch + c) * (SUB * BM), U8_CHUNK_A, &sm.bar[slot]);
+    bulk_g2s(&sm.Bs[slot][0][0], p.Bprep + ((tiles_j0[tt] / BN) * nch + c) * (SUB * BN), U8_CHUNK_B, &sm.bar[slot]);
   };
   if (t == 0)
     for (int64_t g = 0; g < U8_STAGES && g < total_g; g++) issue(g);
-  const uint8_t* C = static_cast<const uint8_t*>(p.C);
+  const char* C = static_cast<const char*>(p.C);
   auto prefetch_c = [&](int tt) {
-    const int r = t >> 1, cb = 64 * (t & 1);
-    const uint8_t* src = C + (tiles_i0[tt] + r) * p.ldc + tiles_j0[tt] + cb;
-    const uint32_t dst = smem_u32(&sm.Cs[r][cb]);
+    const int r = t >> 1;
+    const char* src = C + ((tiles_i0[tt] + r) * p.ldc + tiles_j0[tt]) * int64_t(sizeof(T)) + CB * (t & 1);
+    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r][0]) + CB * (t & 1));
 #pragma unroll
-    for (int q = 0; q < 4; q++)
+    for (int q = 0; q < CB / 16; q++)
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
     asm volatile("cp.async.commit_group;\n" ::);
   };
@@ -430,7 +448,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, in
   bool changed = false;
   const int32_t* __restrict__ pb = p.predB;
   int32_t* __restrict__ out = p.idx;
-  uint8_t* Cw = static_cast<uint8_t*>(p.C);
+  T* Cw = static_cast<T*>(p.C);
   const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
 
   for (int tt = 0; tt < nt; tt++) {
@@ -441,14 +459,13 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, in
     for (int r = 0; r < 8; r++)
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        acc[r][q] = U8_KINF * 0x00010001u;
+        acc[r][q] = KINF2;
         kst[r][q] = 0u;
       }
     for (int64_t c = 0; c < nch; c++) {
       const int64_t g = int64_t(tt) * nch + c;
       const int slot = int(g % U8_STAGES);
       mbar_wait(&sm.bar[slot], uint32_t((g / U8_STAGES) & 1));
-      const int64_t wc = c % U8_DEC_CHUNKS;   // chunk position inside the decode window
 #pragma unroll kU8Unroll
       for (int kk = 0; kk < SUB; kk++) {
         const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
@@ -463,6 +480,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, in
           for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
       }
       const bool more = c + 1 < nch;
+      const int64_t wc = c % WIN;   // chunk position inside the decode window
       if (c == 0) {
         asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
@@ -471,27 +489,36 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, in
           const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
-            acc[r][2 * h] = __vminu2(acc[r][2 * h], __byte_perm(w, 0, 0x4140) << U8_TAG);
-            acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], __byte_perm(w, 0, 0x4342) << U8_TAG);
+            uint32_t p0, p1;   // old values of the two column pairs, as key pairs
+            if constexpr (sizeof(T) == 1) {
+              const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
+              p0 = __byte_perm(w, 0, 0x4140) << TAG;
+              p1 = __byte_perm(w, 0, 0x4342) << TAG;
+            } else {
+              const uint2 w = *reinterpret_cast<const uint2*>(&sm.Cs[ri][64 * h + 4 * tx]);
+              p0 = w.x << TAG;
+              p1 = w.y << TAG;
+            }
+            acc[r][2 * h] = __vminu2(acc[r][2 * h], p0);
+            acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], p1);
           }
         }
         __syncthreads();                      // Cs consumed: prefetch the next tile's C
         if (tt + 1 < nt) prefetch_c(tt + 1);
       }
-      if (wc == U8_DEC_CHUNKS - 1 || !more) {
+      if (wc == WIN - 1 || !more) {
         uint32_t any = 0;
 #pragma unroll
         for (int r = 0; r < 8; r++)
 #pragma unroll
           for (int q = 0; q < 4; q++) any |= acc[r][q];
-        if (__any_sync(0xffffffffu, any & U8_TAGMASK2)) {
+        if (__any_sync(0xffffffffu, any & TMASK2)) {
           const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
 #pragma unroll
           for (int r = 0; r < 8; r++)
 #pragma unroll
             for (int q = 0; q < 4; q++) {
-              const uint32_t tg = acc[r][q] & U8_TAGMASK2;
+              const uint32_t tg = acc[r][q] & TMASK2;
               const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
               kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
               acc[r][q] -= tg;
@@ -526,8 +553,12 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, in
         if ((k0 | k1) == 0u) continue;
         changed = true;
         const int64_t j = j0 + 64 * h + 4 * tx;
-        *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) =
-            __byte_perm(acc[r][2 * h] >> U8_TAG, acc[r][2 * h + 1] >> U8_TAG, 0x6420);
+        if constexpr (sizeof(T) == 1) {
+          *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) =
+              __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
+        } else {
+          *reinterpret_cast<uint2*>(Cw + i * p.ldc + j) = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
+        }
         if (!out) continue;
         if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
           *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
@@ -542,29 +573,37 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_tma_kernel(MinplusArgs p, in
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
 }
 
-// panel layout kernels
-__global__ void prep_u8_a_kernel(const uint8_t* A, int64_t lda, int64_t nch, uint32_t* Aprep) {
+// panel layout kernels (one CTA per (tile, chunk); thread = one row x 16 k, or one k x 16 columns)
+template <int S>
+__global__ void prep_nt_a_kernel(const typename Narrow<S>::T* A, int64_t lda, int64_t nch, uint32_t* Aprep) {
+  using T = typename Narrow<S>::T;
+  constexpr int TAG = Narrow<S>::TAG;
   const int64_t rt = blockIdx.y, c = blockIdx.x;
   const int t = threadIdx.x, r = t & 127, kb = 16 * (t >> 7);
-  const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(A + (rt * BM + r) * lda + c * SUB + kb));
-  const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+  const T* src = A + (rt * BM + r) * lda + c * SUB + kb;
   uint32_t* dst = Aprep + (rt * nch + c) * (SUB * BM);
+  T v[16];
+  *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(src));
+  if constexpr (sizeof(T) == 2) *reinterpret_cast<uint4*>(v + 8) = __ldg(reinterpret_cast<const uint4*>(src) + 1);
 #pragma unroll
-  for (int q = 0; q < 16; q++) dst[(kb + q) * BM + r] = ((w[q >> 2] >> (8 * (q & 3))) & 0xFF) * 0x00800080u;
+  for (int q = 0; q < 16; q++) dst[(kb + q) * BM + r] = (uint32_t(v[q]) << TAG) * 0x00010001u;
 }
 
-__global__ void prep_u8_b_kernel(const uint8_t* B, int64_t ldb, int64_t nch, uint16_t* Bprep) {
+template <int S>
+__global__ void prep_nt_b_kernel(const typename Narrow<S>::T* B, int64_t ldb, int64_t nch, uint16_t* Bprep) {
+  using T = typename Narrow<S>::T;
+  constexpr int TAG = Narrow<S>::TAG, WIN = Narrow<S>::WIN;
   const int64_t ct = blockIdx.y, c = blockIdx.x;
   const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
-  const uint4 w4 = __ldg(reinterpret_cast<const uint4*>(B + (c * SUB + kk) * ldb + ct * BN + cb));
-  const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
-  const uint32_t tag = uint32_t(SUB * (c % U8_DEC_CHUNKS) + kk + 1) * 0x00010001u;   // 1..96 per window
+  const T* src = B + (c * SUB + kk) * ldb + ct * BN + cb;
+  T v[16];
+  *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(src));
+  if constexpr (sizeof(T) == 2) *reinterpret_cast<uint4*>(v + 8) = __ldg(reinterpret_cast<const uint4*>(src) + 1);
+  const uint32_t tag = uint32_t(SUB * (c % WIN) + kk + 1);   // 1..32*WIN inside a decode window
   uint32_t o[8];
 #pragma unroll
-  for (int q = 0; q < 4; q++) {
-    o[2 * q] = (__byte_perm(w[q], 0, 0x4140) << U8_TAG) | tag;
-    o[2 * q + 1] = (__byte_perm(w[q], 0, 0x4342) << U8_TAG) | tag;
-  }
+  for (int q = 0; q < 8; q++)
+    o[q] = ((uint32_t(v[2 * q]) << TAG) | tag) | (((uint32_t(v[2 * q + 1]) << TAG) | tag) << 16);
   uint4* dst = reinterpret_cast<uint4*>(Bprep + (ct * nch + c) * (SUB * BN) + kk * BN + cb);
   dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
   dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
@@ -572,17 +611,62 @@ __global__ void prep_u8_b_kernel(const uint8_t* B, int64_t ldb, int64_t nch, uin
 
 size_t prep_u8_bytes(int64_t m, int64_t n, int64_t k) { return size_t(m) * k * 4 + size_t(k) * n * 2 + 256; }
 
+int launch_prep_narrow(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
+                       int64_t k, uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s) {
+  const size_t es = store == STORE_U16 ? 2 : 1;
+  if (m % BM || n % BN || k % SUB || (lda * es) % 16 || (ldb * es) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
+      (reinterpret_cast<uintptr_t>(B) & 15))
+    return set_error(2, "panel prep needs 128-multiple m/n, 32-multiple k and 16-byte aligned panels");
+  const int64_t nch = k / SUB;
+  const dim3 ga(unsigned(nch), unsigned(m / BM)), gb(unsigned(nch), unsigned(n / BN));
+  if (store == STORE_U8) {
+    prep_nt_a_kernel<STORE_U8><<<ga, NT, 0, s>>>(static_cast<const uint8_t*>(A), lda, nch, Aprep);
+    prep_nt_b_kernel<STORE_U8><<<gb, NT, 0, s>>>(static_cast<const uint8_t*>(B), ldb, nch, Bprep);
+  } else if (store == STORE_U16) {
+    prep_nt_a_kernel<STORE_U16><<<ga, NT, 0, s>>>(static_cast<const uint16_t*>(A), lda, nch, Aprep);
+    prep_nt_b_kernel<STORE_U16><<<gb, NT, 0, s>>>(static_cast<const uint16_t*>(B), ldb, nch, Bprep);
+  } else {
+    return set_error(2, "panel prep is for the narrow tiers");
+  }
+  APSP_CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int launch_prep_u8(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n, int64_t k,
                    uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s) {
-  if (m % BM || n % BN || k % SUB || (lda & 15) || (ldb & 15) || (reinterpret_cast<uintptr_t>(A) & 15) ||
-      (reinterpret_cast<uintptr_t>(B) & 15))
-    return set_error(2, "prep_u8 needs 128-multiple m/n, 32-multiple k and 16-byte aligned panels");
-  const int64_t nch = k / SUB;
-  prep_u8_a_kernel<<<dim3(unsigned(nch), unsigned(m / BM)), NT, 0, s>>>(static_cast<const uint8_t*>(A), lda, nch,
-                                                                         Aprep);
-  prep_u8_b_kernel<<<dim3(unsigned(nch), unsigned(n / BN)), NT, 0, s>>>(static_cast<const uint8_t*>(B), ldb, nch,
-                                                                         Bprep);
-  APSP_CUDA_TRY(cudaGetLastError());
+  return launch_prep_narrow(STORE_U8, A, lda, B, ldb, m, n, k, Aprep, Bprep, s);
+}
+
+static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
+  if (a.only_lo < a.only_hi) {
+    const int64_t w = (a.only_hi - a.only_lo) / bm;
+    const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
+    return dim3(unsigned(w * nt_c + (nt_r - w) * w), 1);
+  }
+  return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
+}
+
+template <int S>
+static int launch_nt(const MinplusArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_nt_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(sizeof(SmemNT<S>))));
+    attr = true;
+  }
+  const size_t es = sizeof(typename Narrow<S>::T);
+  if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
+    return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
+  static int tpc = -1;
+  if (tpc < 0) {
+    const char* e = getenv("APSP_U8_TPC");
+    tpc = e ? atoi(e) : 1;   // >1 delays the lookahead side stream (measured slower)
+    if (tpc < 1) tpc = 1;
+    if (tpc > U8_TPC_MAX) tpc = U8_TPC_MAX;
+  }
+  const dim3 g2 = grid_for(a, BM, BN);
+  const int64_t tiles = int64_t(g2.x) * g2.y;
+  minplus_nt_kernel<S><<<unsigned((tiles + tpc - 1) / tpc), NT, sizeof(SmemNT<S>), s>>>(a, tpc);
   return 0;
 }
 
@@ -847,15 +931,6 @@ __global__ void __launch_bounds__(NT) minplus_exact_kernel(MinplusArgs p) {
   }
 }
 
-static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
-  if (a.only_lo < a.only_hi) {
-    const int64_t w = (a.only_hi - a.only_lo) / bm;
-    const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
-    return dim3(unsigned(w * nt_c + (nt_r - w) * w), 1);
-  }
-  return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
-}
-
 int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
   if (a.m <= 0 || a.n <= 0) return 0;
   if (a.k <= 0) return 0;
@@ -868,24 +943,8 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
   switch (store) {
     case STORE_U8: {
       if (a.Aprep && a.Bprep) {
-        static bool attr_t = false;
-        if (!attr_t) {
-          APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_u8_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(sizeof(SmemU8T))));
-          attr_t = true;
-        }
-        if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc & 15))
-          return set_error(2, "bulk-staged u8 tiles need full 128 x 128 tiles and 32-multiple k");
-        static int tpc = -1;
-        if (tpc < 0) {
-          const char* e = getenv("APSP_U8_TPC");
-          tpc = e ? atoi(e) : 1;   // >1 delays the lookahead side stream (measured slower)
-          if (tpc < 1) tpc = 1;
-          if (tpc > U8_TPC_MAX) tpc = U8_TPC_MAX;
-        }
-        const dim3 g2 = grid_for(a, BM, BN);
-        const int64_t tiles = int64_t(g2.x) * g2.y;
-        minplus_u8_tma_kernel<<<unsigned((tiles + tpc - 1) / tpc), NT, sizeof(SmemU8T), s>>>(a, tpc);
+        const int rc = launch_nt<STORE_U8>(a, s);
+        if (rc) return rc;
         break;
       }
       static bool attr = false;
@@ -905,6 +964,12 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
         attr = true;
       }
       minplus_w32_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemW32), s>>>(a);
+      break;
+    }
+    case STORE_U16: {
+      if (!(a.Aprep && a.Bprep)) return set_error(2, "the u16 tier needs pre-laid-out panels (aligned products)");
+      const int rc = launch_nt<STORE_U16>(a, s);
+      if (rc) return rc;
       break;
     }
     case STORE_I32:

@@ -42,8 +42,8 @@ from .core import (
     ParameterError,
 )
 
-U8_LIMIT, W32_LIMIT = 254, (1 << 24) - 2
-TIER_LIMIT = {nat.TIER_U8: U8_LIMIT, nat.TIER_W32: W32_LIMIT, nat.TIER_I32: INF32 - 1,
+U8_LIMIT, U16_LIMIT, W32_LIMIT = 254, 510, (1 << 24) - 2
+TIER_LIMIT = {nat.TIER_U8: U8_LIMIT, nat.TIER_U16: U16_LIMIT, nat.TIER_W32: W32_LIMIT, nat.TIER_I32: INF32 - 1,
               nat.TIER_I64: (1 << 60) - 1}
 
 
@@ -64,6 +64,8 @@ def pick_tiers(dtype_code: int, scan: dict) -> list[int]:
     t = []
     if integral and w <= U8_LIMIT:
         t.append(nat.TIER_U8)
+    if integral and w <= U16_LIMIT:
+        t.append(nat.TIER_U16)
     if integral and w <= W32_LIMIT:
         t.append(nat.TIER_W32)
     t.append({nat.DTYPE_F32: nat.TIER_F32, nat.DTYPE_I32: nat.TIER_I32}.get(dtype_code, nat.TIER_I64))
@@ -176,7 +178,7 @@ def merged_scan(ranks, ops, h_locals, n, allreduce_max):
 
 # ---- CUDA shard ops --------------------------------------------------------------------------
 
-_TORCH_STORE = {nat.TIER_U8: "uint8", nat.TIER_W32: "int32", nat.TIER_I32: "int32", nat.TIER_F32: "float32",
+_TORCH_STORE = {nat.TIER_U8: "uint8", nat.TIER_U16: "uint16", nat.TIER_W32: "int32", nat.TIER_I32: "int32", nat.TIER_F32: "float32",
                 nat.TIER_I64: "int64"}
 
 
@@ -305,8 +307,9 @@ class TorchComm:
         else:
             (pv, pp), stream = ops.recv_buffers(rk.state, slot), None
         ctx = self.torch.cuda.stream(stream) if stream is not None else _null_ctx()
+        wire = pv.view(self.torch.int16) if pv.dtype == self.torch.uint16 else pv   # NCCL has no uint16
         with ctx:
-            works = [self.dist.broadcast(pv, src=owner, group=self.group, async_op=True),
+            works = [self.dist.broadcast(wire, src=owner, group=self.group, async_op=True),
                      self.dist.broadcast(pp, src=owner, group=self.group, async_op=True)]
         return works, [(pv, pp)], rk.rank == owner
 

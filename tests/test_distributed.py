@@ -93,6 +93,7 @@ def test_tier_selection_mirrors_library():
     from paper_2310_03983_b200.distributed import pick_tiers
 
     base = {"non_integral": 0, "max_finite": 100}
-    assert pick_tiers(nat.DTYPE_I32, base) == [nat.TIER_U8, nat.TIER_W32, nat.TIER_I32]
+    assert pick_tiers(nat.DTYPE_I32, base) == [nat.TIER_U8, nat.TIER_U16, nat.TIER_W32, nat.TIER_I32]
+    assert pick_tiers(nat.DTYPE_I32, base | {"max_finite": 300}) == [nat.TIER_U16, nat.TIER_W32, nat.TIER_I32]
     assert pick_tiers(nat.DTYPE_I64, base | {"max_finite": 1 << 30}) == [nat.TIER_I64]
     assert pick_tiers(nat.DTYPE_F32, base | {"non_integral": 1}) == [nat.TIER_F32]

@@ -41,7 +41,7 @@ def test_c1_blocked_and_classic(cuda):
     assert np.array_equal(c.pred.raw, g["pred"])
 
 
-@pytest.mark.parametrize("tier", ["u8", "w32", "i64"])
+@pytest.mark.parametrize("tier", ["u8", "u16", "w32", "i64"])
 def test_c1_every_tier(cuda, tier):
     g = golden("c1_fw.npz")
     s = ap.fw_classic(ap.CostMatrix(g["h"]), tier=tier)
@@ -127,15 +127,45 @@ def test_zero_weight_edges(cuda):
     assert np.array_equal(v.distances.raw, want_d)
 
 
+def ring_with_chords(n, step, seed):
+    """Unit ring i -> i+1 plus weight-2 chords i -> i+step: max distance ~ 2n/step (known range)."""
+    rng = np.random.default_rng(seed)
+    raw = np.full((n, n), INF_RAW, np.int64)
+    idx = np.arange(n)
+    raw[idx, (idx + 1) % n] = 1
+    keep = rng.random(n) < 0.9
+    raw[idx[keep], (idx[keep] + step) % n] = 2
+    np.fill_diagonal(raw, 0)
+    return raw
+
+
+@pytest.mark.parametrize("n,step,b", [(384, 3, 128), (1000, 7, 256), (2048, 13, 256)])
+def test_u16_tier_fw_and_rkleene(cuda, n, step, b):
+    # max distance in (254, 508]: u8 cannot certify, u16 can; forced and auto both exact
+    raw = ring_with_chords(n, step, seed=n)
+    want_d, _ = orc.rkleene(raw, 64)
+    m = want_d[want_d != INF_RAW].max()
+    assert 254 < m + 2 <= 510
+    for tier in ("u16", None):
+        s = ap.fw_classic(ap.CostMatrix(raw), tier=tier, block=b)
+        assert s.info["tier"] == "u16"
+        assert np.array_equal(s.distances.raw, want_d)
+        pred_ok(raw, s.distances.raw, s.pred.raw)
+    r = ap.rkleene(ap.CostMatrix(raw), split="aligned", track="pred", base_threshold=256, tier="u16")
+    assert r.info["tier"] == "u16"
+    assert np.array_equal(r.distances.raw, want_d)
+    pred_ok(raw, r.distances.raw, r.pred.raw)
+
+
 def test_tier_fallback_and_wide_costs(cuda):
-    # long paths: u8 certificate must fail and fall back to w32, results exact
+    # long paths: u8 and u16 certificates must fail and fall back to w32, results exact
     n = 300
     raw = np.full((n, n), INF_RAW, np.int64)
     np.fill_diagonal(raw, 0)
     for i in range(n - 1):
         raw[i, i + 1] = 3
     s = ap.fw_classic(ap.CostMatrix(raw))
-    assert s.info["tier"] == "w32" and "u8" in s.info["tiers_tried"]
+    assert s.info["tier"] == "w32" and "u8" in s.info["tiers_tried"] and "u16" in s.info["tiers_tried"]
     want_d, _ = orc.fw_classic(raw)
     assert np.array_equal(s.distances.raw, want_d)
     pred_ok(raw, s.distances.raw, s.pred.raw)
