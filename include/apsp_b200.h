@@ -140,6 +140,7 @@ typedef struct apsp_scan_result {
   int64_t max_finite;    /* largest finite cost (integer view) */
   float max_finite_f;    /* largest finite cost (fp32 input) */
   int32_t zero_offdiag;  /* a zero-cost edge off the diagonal */
+  uint64_t finite_offdiag; /* number of finite off-diagonal cells (edges) */
 } apsp_scan_result;
 
 /* diag_off: cell (i, i + diag_off) is diagonal (0 whole matrix, row0 for a shard, -1 none). Syncs. */

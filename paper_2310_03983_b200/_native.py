@@ -97,6 +97,7 @@ class ScanResult(ctypes.Structure):
         ("max_finite", ctypes.c_int64),
         ("max_finite_f", ctypes.c_float),
         ("zero_offdiag", ctypes.c_int32),
+        ("finite_offdiag", ctypes.c_uint64),
     ]
 
 

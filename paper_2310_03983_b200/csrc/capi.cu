@@ -1,6 +1,7 @@
 // C ABI and native orchestration: blocked FW rounds, R-Kleene recursion, squaring loop,
 // min-plus products, value-tier selection and certification, host-level entry.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -151,7 +152,7 @@ bool narrow_store(int store) { return store == STORE_U8 || store == STORE_U16; }
 
 // Candidate tiers, narrowest first.  allow_u16: the caller runs only aligned products (the
 // u16 tier exists only as bulk-staged tiles).
-std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced, bool allow_u16 = true) {
+std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced, bool allow_u16, int64_t n_vert) {
   const bool integral = dtype != APSP_DTYPE_F32 || !sc.non_integral;
   const int64_t w = sc.max_finite;
   if (forced >= 0) {
@@ -165,9 +166,15 @@ std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced, bool al
     if (!fits) return {};
     return {forced};
   }
+  // Skip narrow tiers whose certificate would almost surely fail: on random-like graphs the
+  // largest distance grows like w_max * ln(n) / ln(average degree).  The estimate only picks
+  // the starting tier; the certificate still decides exactness.
+  const double n = n_vert > 0 ? double(n_vert) : 1.0;
+  const double deg = std::max(double(sc.finite_offdiag) / n, 1.5);
+  const double m_est = 0.5 * double(w) * std::log(std::max(n, 2.0)) / std::log(deg);
   std::vector<int> t;
-  if (integral && w <= U8_INF - 1) t.push_back(APSP_TIER_U8);
-  if (allow_u16 && integral && w <= U16_INF - 1) t.push_back(APSP_TIER_U16);
+  if (integral && w <= U8_INF - 1 && m_est + w <= U8_INF - 1) t.push_back(APSP_TIER_U8);
+  if (allow_u16 && integral && w <= U16_INF - 1 && m_est + w <= U16_INF - 1) t.push_back(APSP_TIER_U16);
   if (integral && w <= W32_INF - 1) t.push_back(APSP_TIER_W32);
   if (dtype == APSP_DTYPE_F32) t.push_back(APSP_TIER_F32);
   else if (dtype == APSP_DTYPE_I32) t.push_back(APSP_TIER_I32);
@@ -515,7 +522,7 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     if (!rc && info) info->flags |= FLAG_CLASSIC_FOR_ZERO_EDGES;
     return rc;
   }
-  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req);
+  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, true, n);
   if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
   int launches = 2, used = -1, tried = 0;
   for (int tier : tiers) {
@@ -771,7 +778,7 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
     if (!rc && info) info->flags |= FLAG_CLASSIC_FOR_ZERO_EDGES;
     return rc;
   }
-  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, aligned != 0);
+  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, aligned != 0, n);
   if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
   int used = -1, tried = 0, launches = 2;
   for (int tier : tiers) {
@@ -844,7 +851,7 @@ int squaring_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* via, in
   const ScanResult scan = hdr.scan;
   rc = check_scan(scan);
   if (rc) return rc;
-  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, false);
+  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, false, n);
   if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
   int used = -1, tried = 0, iters = 0, launches = 2;
   char* cur = D0;

@@ -34,6 +34,7 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
                             ScanResult* out) {
   using T = typename Api<D>::T;
   bool neg = false, diag = false, nonint = false, anyfin = false, zero = false;
+  unsigned long long edges = 0;
   long long mx = -1;
   float mxf = -1.f;
   const int64_t total = rows * cols;
@@ -44,6 +45,7 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
     if (on_diag && v != T(0)) diag = true;
     if (!Api<D>::fin(v)) continue;
     anyfin = true;
+    if (!on_diag) edges++;
     if (v == T(0) && !on_diag) zero = true;
     if constexpr (D == API_F32) {
       if (isnan(v) || v < 0.f) { neg = true; continue; }
@@ -63,10 +65,12 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
   for (int o = 16; o; o >>= 1) {
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+    edges += __shfl_xor_sync(0xffffffffu, edges, o);
   }
   if ((threadIdx.x & 31) == 0) {
     if (mx >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&out->max_finite), (unsigned long long)mx);
     if (mxf >= 0.f) atomicMax(reinterpret_cast<int*>(&out->max_finite_f), __float_as_int(mxf));
+    if (edges) atomicAdd(&out->finite_offdiag, edges);
   }
 }
 

@@ -87,6 +87,7 @@ struct ScanResult {
   int64_t max_finite;      // integer domains (fp32: floor of max)
   float max_finite_f;      // fp32 domain
   int32_t zero_offdiag;    // a finite zero cost off the diagonal (zero-weight edge)
+  unsigned long long finite_offdiag;   // number of finite off-diagonal cells (edges)
 };
 // diag_off: cell (i, i + diag_off) is a diagonal cell (0 for a whole matrix, row0 for a
 // row shard, -1: no diagonal check)

@@ -57,14 +57,20 @@ def layout(n: int, world: int, block: int) -> tuple[int, int]:
     return N, N // world
 
 
-def pick_tiers(dtype_code: int, scan: dict) -> list[int]:
-    """Narrowest exact tier first (mirror of capi.cu pick_tiers)."""
+def pick_tiers(dtype_code: int, scan: dict, n: int = 0) -> list[int]:
+    """Narrowest exact tier first (mirror of capi.cu pick_tiers, including the sparse-graph
+    distance estimate 0.5 * w_max * ln(n) / ln(average degree) that skips hopeless tiers)."""
+    import math
+
     integral = dtype_code != nat.DTYPE_F32 or not scan["non_integral"]
     w = scan["max_finite"]
+    nv = max(n, 2)
+    deg = max(scan.get("finite_offdiag", nv * nv) / nv, 1.5)
+    m_est = 0.5 * w * math.log(nv) / math.log(deg)
     t = []
-    if integral and w <= U8_LIMIT:
+    if integral and w <= U8_LIMIT and m_est + w <= U8_LIMIT:
         t.append(nat.TIER_U8)
-    if integral and w <= U16_LIMIT:
+    if integral and w <= U16_LIMIT and m_est + w <= U16_LIMIT:
         t.append(nat.TIER_U16)
     if integral and w <= W32_LIMIT:
         t.append(nat.TIER_W32)
@@ -78,6 +84,7 @@ def merge_scans(scans: list[dict]) -> dict:
     for s in scans:
         for k in out:
             out[k] = max(out[k], int(s[k]))
+    out["finite_offdiag"] = sum(int(s.get("finite_offdiag", 0)) for s in scans)
     return out
 
 
@@ -106,7 +113,7 @@ def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, co
     """Solve with the given local ranks; returns (tier, global max finite)."""
     N, R = layout(n, world, block)
     scan = merged_scan(ranks, ops, h_locals, n, allreduce_max)
-    tiers = [tier_req] if tier_req is not None else pick_tiers(dtype_code, scan)
+    tiers = [tier_req] if tier_req is not None else pick_tiers(dtype_code, scan, n)
     for tier in tiers:
         for rk, h in zip(ranks, h_locals):
             rk.state = ops.alloc(tier, R, N)
@@ -165,11 +172,19 @@ def run_rounds(ranks: list[RankState], N: int, R: int, b: int, ops, comm) -> Non
             ops.update(rk.state, pv, pp, k0, 0, R, lo, hi)
 
 
+def allreduce_sum(allreduce_max, v: int) -> int:
+    """Sum over ranks through the comm's all-reduce (TorchComm exposes allreduce_sum)."""
+    owner = getattr(allreduce_max, "__self__", None)
+    return owner.allreduce_sum(v) if owner is not None and hasattr(owner, "allreduce_sum") else v
+
+
 def merged_scan(ranks, ops, h_locals, n, allreduce_max):
     scans = [ops.scan(h, rk.row0, rk.rows_valid, n) for rk, h in zip(ranks, h_locals)]
     scan = merge_scans(scans)
     if allreduce_max is not None:
+        edges = scan.pop("finite_offdiag")
         scan = {k: allreduce_max(v) for k, v in scan.items()}
+        scan["finite_offdiag"] = allreduce_sum(allreduce_max, edges)
     check_scan(scan)
     for rk in ranks:
         rk.scan = scan
@@ -217,7 +232,7 @@ class CudaShardOps:
                                          self._stream()))
         mx = int(r.max_finite) if r.any_finite else -1
         return {"negative": r.negative, "diag_nonzero": r.diag_nonzero, "non_integral": r.non_integral,
-                "zero_offdiag": r.zero_offdiag, "max_finite": mx}
+                "zero_offdiag": r.zero_offdiag, "max_finite": mx, "finite_offdiag": int(r.finite_offdiag)}
 
     def alloc(self, tier: int, R: int, N: int) -> CudaShard:
         t = self.torch
@@ -296,6 +311,11 @@ class TorchComm:
     def allreduce_max(self, v: int) -> int:
         t = self.torch.tensor([int(v)], dtype=self.torch.int64, device=self.device)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
+    def allreduce_sum(self, v: int) -> int:
+        t = self.torch.tensor([int(v)], dtype=self.torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return int(t.item())
 
     def bcast_start(self, ranks, owner: int, owner_panels, slot: int, ops):

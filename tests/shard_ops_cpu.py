@@ -35,7 +35,7 @@ class CpuShardOps:
             diag[i, row0 + i] = True
         return {"negative": int((a[fin] < 0).any()), "diag_nonzero": int((a[diag] != 0).any()),
                 "non_integral": 0, "zero_offdiag": int(((a == 0) & fin & ~diag).any()),
-                "max_finite": int(a[fin].max()) if fin.any() else -1}
+                "max_finite": int(a[fin].max()) if fin.any() else -1, "finite_offdiag": int((fin & ~diag).sum())}
 
     def alloc(self, tier, R, N):
         b = self.block

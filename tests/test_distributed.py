@@ -92,8 +92,13 @@ def test_tier_selection_mirrors_library():
     from paper_2310_03983_b200 import _native as nat
     from paper_2310_03983_b200.distributed import pick_tiers
 
-    base = {"non_integral": 0, "max_finite": 100}
-    assert pick_tiers(nat.DTYPE_I32, base) == [nat.TIER_U8, nat.TIER_U16, nat.TIER_W32, nat.TIER_I32]
-    assert pick_tiers(nat.DTYPE_I32, base | {"max_finite": 300}) == [nat.TIER_U16, nat.TIER_W32, nat.TIER_I32]
-    assert pick_tiers(nat.DTYPE_I64, base | {"max_finite": 1 << 30}) == [nat.TIER_I64]
-    assert pick_tiers(nat.DTYPE_F32, base | {"non_integral": 1}) == [nat.TIER_F32]
+    dense = {"non_integral": 0, "max_finite": 100, "finite_offdiag": 16384 * 800}
+    assert pick_tiers(nat.DTYPE_I32, dense, 16384) == [nat.TIER_U8, nat.TIER_U16, nat.TIER_W32, nat.TIER_I32]
+    assert pick_tiers(nat.DTYPE_I32, dense | {"max_finite": 200}, 16384) == [nat.TIER_U16, nat.TIER_W32,
+                                                                             nat.TIER_I32]
+    sparse = dense | {"finite_offdiag": 16384 * 16}      # rho=0.002-like: skip u8, start at u16
+    assert pick_tiers(nat.DTYPE_I32, sparse, 16384) == [nat.TIER_U16, nat.TIER_W32, nat.TIER_I32]
+    tiny = dense | {"finite_offdiag": 2048 * 2}          # degree ~2: straight to w32
+    assert pick_tiers(nat.DTYPE_I32, tiny, 2048) == [nat.TIER_W32, nat.TIER_I32]
+    assert pick_tiers(nat.DTYPE_I64, dense | {"max_finite": 1 << 30}, 16384) == [nat.TIER_I64]
+    assert pick_tiers(nat.DTYPE_F32, dense | {"non_integral": 1}, 16384) == [nat.TIER_F32]
