@@ -44,7 +44,7 @@ TIER_PEAK = {"u8": 37.07e12, "u16": 37.07e12, "w32": 24.91e12, "i32": 17.98e12, 
 TIER_OP = {"u8": "VIADDMNMX.U16x2 (2 upd/instr)", "u16": "VIADDMNMX.U16x2 (2 upd/instr)",
            "w32": "VIADD+VIMNMX3", "i32": "compare-select",
            "f32": "FADD/FSETP/FSEL/SEL", "i64": "compare-select int64"}
-BLOCK = 256
+BLOCK = 0          # 0: the library's size-aware default (apsp_info.block reports it)
 
 
 def log(*a):
@@ -192,13 +192,13 @@ def run_reference(args, ws, rank):
 
 def weak_n(ws: int) -> int:
     n = 16384 * ws ** (1.0 / 3.0)
-    return int(round(n / (BLOCK * ws)) * BLOCK * ws) if ws > 1 else 16384
+    return int(round(n / (256 * ws)) * 256 * ws) if ws > 1 else 16384
 
 
 def config(n, rho, ws):
     return {"workload": f"blocked Floyd-Warshall APSP, distances+predecessors, n={n}, generator graph "
                         f"GenParams(n, rho={rho}, alpha=100, seed=7+n), int32 in/out",
-            "n": n, "rho": rho, "block": BLOCK, "layout": "1D row bands" if ws > 1 else "single GPU",
+            "n": n, "rho": rho, "layout": "1D row bands" if ws > 1 else "single GPU",
             "parallelism": f"rowband{ws}" if ws > 1 else "1gpu",
             "l2": "inputs larger than L2 (1 GiB int32 dist + 1 GiB pred + 256 MiB u8 store per GPU)"}
 
@@ -214,7 +214,7 @@ def main():
     ap_.add_argument("--no-cpu", action="store_true")
     ap_.add_argument("--no-e2e", action="store_true")
     ap_.add_argument("--ref-step-s", type=float, default=8.0)
-    ap_.add_argument("--block", type=int, default=BLOCK, help="pivot block (128 or 256)")
+    ap_.add_argument("--block", type=int, default=BLOCK, help="pivot block (multiple of 128; 0 = library default)")
     ap_.add_argument("--sharded", action="store_true", help="use the multi-GPU row-band path even at N=1")
     args = ap_.parse_args()
     ws, rank, local = dist_env()
@@ -264,6 +264,7 @@ def bench_single(args):
         raise SystemExit(f"bench result failed the predecessor certificate: {why}")
     tier = nat.TIER_NAMES[info.tier]
     launches_per_step = info.launches
+    block = info.block or block
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     with ClockSampler(0) as clk:

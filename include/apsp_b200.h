@@ -75,6 +75,8 @@ typedef struct apsp_info {
   int32_t flags;        /* bit 0: zero-cost edges -> classic k order used for predecessors */
   int32_t kernel_launches; /* profiled min-plus tile launches (apsp_set_profiling(1)) */
   double kernel_ms;     /* summed CUDA-event time of those launches */
+  int32_t block;        /* pivot block used by the blocked FW (0 otherwise) */
+  int32_t reserved;
 } apsp_info;
 
 const char* apsp_last_error(void);

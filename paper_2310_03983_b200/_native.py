@@ -71,6 +71,8 @@ class ApspInfo(ctypes.Structure):
         ("flags", ctypes.c_int32),
         ("kernel_launches", ctypes.c_int32),
         ("kernel_ms", ctypes.c_double),
+        ("block", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -85,6 +87,7 @@ class ApspInfo(ctypes.Structure):
             "classic_for_zero_edges": bool(self.flags & 1),
             "kernel_launches": self.kernel_launches,
             "kernel_ms": self.kernel_ms,
+            "block": self.block,
         }
 
 

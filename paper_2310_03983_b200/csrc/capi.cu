@@ -490,6 +490,15 @@ int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
 // bit-exact with the reference for both dist and pred.
 constexpr int32_t FLAG_CLASSIC_FOR_ZERO_EDGES = 1;
 
+// Pivot block by size (measured on B200, profiles/r01_summary.md): small n is bound by the
+// phase-1 chain (b = 128), large n by per-tile overheads that a longer k amortises
+// (n=16384: b=1024 145 ms vs 256 161 ms; n=32768: b=2048).  Padding waste is kept below ~1%.
+int default_block(int64_t n) {
+  int b = n <= 6144 ? 128 : n <= 12288 ? 256 : n <= 24576 ? 1024 : 2048;
+  while (b > 128 && double(round_up(n, b)) > 1.01 * double(round_up(n, 128))) b /= 2;
+  return b;
+}
+
 size_t fw_ws_bytes(int dtype, int64_t n, int block) {
   const int64_t N = round_up(std::max<int64_t>(n, 1), block);
   const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
@@ -499,8 +508,8 @@ size_t fw_ws_bytes(int dtype, int64_t n, int block) {
 int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
                     void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info) {
   if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
-  if (b <= 0) b = n > 6144 ? 256 : DEFAULT_BLOCK;   // 256 halves phase-3 traffic/prologues; 128 keeps phase 1 short
-  if (b != 128 && b != 256) return set_error(APSP_EINVAL, "blocked FW supports block 128 or 256 (got %d)", b);
+  if (b <= 0) b = default_block(n);
+  if (b % 128 || b < 128 || b > 4096) return set_error(APSP_EINVAL, "blocked FW block must be a multiple of 128 in [128, 4096] (got %d)", b);
   const int64_t N = round_up(n, b);
   Scratch sc;
   int rc = sc.acquire(ws, ws_bytes, fw_ws_bytes(dtype, n, b), s);
@@ -563,6 +572,7 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   launches += 2;
   const double ms = tm.stop();
   if (info) {
+    info->block = b;
     info->tier = used;
     info->tiers_tried = tried;
     info->iterations = 0;
@@ -1286,8 +1296,7 @@ int apsp_abi_version(void) { return APSP_ABI_VERSION; }
 
 size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block) {
   switch (algorithm) {
-    case APSP_ALG_FW_BLOCKED: return std::max(fw_ws_bytes(dtype, n, block > 0 ? block : 256),
-                                              fw_ws_bytes(dtype, n, block > 0 ? block : DEFAULT_BLOCK));
+    case APSP_ALG_FW_BLOCKED: return fw_ws_bytes(dtype, n, block > 0 ? block : default_block(n));
     case APSP_ALG_RKLEENE: return std::max(rk_ws_bytes(dtype, n, 1, 1 << 30), rk_ws_bytes(dtype, n, 0));
     case APSP_ALG_FW_SQUARING: return sq_ws_bytes(dtype, n);
     case APSP_ALG_FW_CLASSIC: return 0;

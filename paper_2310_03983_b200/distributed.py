@@ -51,6 +51,15 @@ def round_up(v: int, m: int) -> int:
     return (v + m - 1) // m * m
 
 
+def shard_block(n: int, world: int) -> int:
+    """Pivot block for the sharded solve: the single-GPU size rule (capi.cu default_block),
+    lowered until a rank's row band holds a whole number of blocks without extra padding."""
+    b = 128 if n <= 6144 else 256 if n <= 12288 else 1024 if n <= 24576 else 2048
+    while b > 128 and layout(n, world, b)[0] > 1.01 * layout(n, world, 128)[0]:
+        b //= 2
+    return b
+
+
 def layout(n: int, world: int, block: int) -> tuple[int, int]:
     """(N, R): padded order and rows per rank (R a multiple of block)."""
     N = round_up(max(n, 1), block * world)
@@ -441,8 +450,8 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
     dist.init_process_group("nccl", device_id=dev)
     comm = TorchComm(dev)
     world, rank = comm.world, comm.rank
-    block = args.block
     n = args.n or weak_n(world)
+    block = args.block or shard_block(n, world)
     N, R = layout(n, world, block)
     row0 = rank * R
     rv = max(0, min(R, n - row0))
