@@ -166,6 +166,14 @@ int apsp_shard_finish(int tier, int dtype, int64_t rows, int64_t n, const void* 
                       int64_t ldp, void* dist, int64_t ldd, int32_t* pred, int64_t ldpo, int64_t* max_finite,
                       void* stream);
 
+/* ---- host-side matrix wire format of the reference (textio.py:70-119), multi-threaded ----------
+ * apsp_format_matrix_i64: writes "n\n" + n rows of n fields (integer or INF) into out; returns
+ * the byte count, or the required capacity when out is NULL / cap is too small, -2 for a
+ * negative cell.  apsp_parse_matrix_i64: parses the n body lines (after the header) into out;
+ * 0 ok, -(1 + row) for a malformed row (*bad_col = field), -(1 + n) for a wrong line count. */
+int64_t apsp_format_matrix_i64(const int64_t* m, int64_t n, char* out, int64_t cap);
+int64_t apsp_parse_matrix_i64(const char* text, int64_t len, int64_t n, int64_t* out, int64_t* bad_col);
+
 #ifdef __cplusplus
 }
 #endif

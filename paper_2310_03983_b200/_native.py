@@ -52,6 +52,8 @@ EXPORTED_SYMBOLS = (
     "apsp_shard_update",
     "apsp_shard_finish",
     "apsp_side_stream",
+    "apsp_format_matrix_i64",
+    "apsp_parse_matrix_i64",
 )
 
 
@@ -128,6 +130,8 @@ _SIGNATURES = {
     "apsp_shard_update": (_i32, [_i32, _i64, _i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64,
                                  _i64, _i64, _vp, _sz, _vp]),
     "apsp_side_stream": (_vp, []),
+    "apsp_format_matrix_i64": (_i64, [_vp, _i64, _vp, _i64]),
+    "apsp_parse_matrix_i64": (_i64, [_vp, _i64, _i64, _vp, ctypes.POINTER(ctypes.c_int64)]),
     "apsp_shard_finish": (_i32, [_i32, _i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
                                  ctypes.POINTER(ctypes.c_int64), _vp]),
 }
