@@ -168,6 +168,28 @@ def cpu_baseline(h32: np.ndarray, budget_s: float = 12.0) -> dict:
             "sample": s.describe() + f"; {dt:.1f}s; full solve extrapolates to {s.n ** 3 / rate:.0f}s"}
 
 
+def networkx_baseline(n: int = 1024, rho: float = 0.1) -> dict | None:
+    """NetworkX floyd_warshall_numpy (float64, distances only, single thread), a full solve of
+    GenParams(n, rho, 100, 7+n) -- the survey's third comparison point."""
+    try:
+        import networkx as nx
+    except ImportError:
+        return None
+    from paper_2310_03983_b200 import GenParams, generate
+
+    g = generate(GenParams(n, rho, 100, 7 + n))
+    G = nx.DiGraph()
+    G.add_nodes_from(range(n))
+    G.add_weighted_edges_from(g.edges)
+    t = time.perf_counter()
+    nx.floyd_warshall_numpy(G)
+    dt = time.perf_counter() - t
+    rate = n ** 3 / dt
+    return {"value": rate, "unit": UNIT, "cores": 1, "kind": "networkx",
+            "sample": f"networkx {nx.__version__} floyd_warshall_numpy full solve n={n} rho={rho} ({dt:.2f}s, "
+                      f"distances only); n=16384 extrapolates to {16384 ** 3 / rate / 3600:.1f} h"}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
@@ -301,9 +323,10 @@ def bench_single(args):
     e2e = None
     if not args.no_e2e:
         e2e = bench_e2e(lib, nat, h_np, n, args, block)
-    cpu = None
+    cpu = nxb = None
     if not args.no_cpu:
         cpu = cpu_baseline(h_np)
+        nxb = networkx_baseline()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "apsp_time_s": ms_step / 1e3, "higher_is_better": True, "scaling": "weak",
@@ -315,7 +338,7 @@ def bench_single(args):
         "fp32_core_peak": FP32_CORE_PEAK,
         "clocks": clk.summary(), "gpu_launches": launches_per_step * args.steps,
         "tier": tier, "max_finite_distance": info.max_finite,
-        "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+        "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "networkx_baseline": nxb,
     }
     print(json.dumps(line), flush=True)
 
