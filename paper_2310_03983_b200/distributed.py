@@ -52,9 +52,15 @@ def round_up(v: int, m: int) -> int:
 
 
 def shard_block(n: int, world: int) -> int:
-    """Pivot block for the sharded solve: the single-GPU size rule (capi.cu default_block),
-    lowered until a rank's row band holds a whole number of blocks without extra padding."""
+    """Pivot block for the sharded solve.
+
+    Starts from the single-GPU size rule (capi.cu default_block).  The owner of a pivot block
+    does its b^2*N pivot work alone while every rank does (N/P)*N*b of phase 3, so the owner's
+    extra share is b*P/N: b is capped at N/(16 P) (~6%).  Then lowered until a rank's row band
+    holds whole blocks without extra padding."""
     b = 128 if n <= 6144 else 256 if n <= 12288 else 1024 if n <= 24576 else 2048
+    while b > 128 and b > n / (16 * world):
+        b //= 2
     while b > 128 and layout(n, world, b)[0] > 1.01 * layout(n, world, 128)[0]:
         b //= 2
     return b
@@ -331,6 +337,9 @@ class TorchComm:
         """Asynchronous broadcast of panel (values, pred) from owner into receive slot `slot`.
         On the owner the collective is issued on the stream that produced the panel."""
         (rk,) = ranks
+        if self.world == 1:                  # nothing to send (NCCL would still copy 5*b*N bytes)
+            pv, pp, _ = owner_panels
+            return [], [(pv, pp)], True
         if rk.rank == owner:
             pv, pp, stream = owner_panels
         else:
@@ -445,6 +454,7 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    os.environ.setdefault("NCCL_DEBUG", "WARN")     # keep stdout to the one JSON line
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)

@@ -88,6 +88,18 @@ def test_layout_rows_are_block_multiples():
                 assert N >= n and R * world == N and R % block == 0
 
 
+def test_shard_block_rule():
+    from paper_2310_03983_b200.distributed import layout, shard_block
+
+    assert shard_block(16384, 1) == 1024          # single rank: the single-GPU rule
+    assert shard_block(32768, 8) == 256           # owner pivot share capped at N/(16P)
+    assert shard_block(4096, 2) == 128
+    for n, w in [(20480, 2), (26112, 4), (32768, 8), (1000, 3)]:
+        b = shard_block(n, w)
+        N, R = layout(n, w, b)
+        assert R % b == 0 and b % 128 == 0
+
+
 def test_tier_selection_mirrors_library():
     from paper_2310_03983_b200 import _native as nat
     from paper_2310_03983_b200.distributed import pick_tiers
