@@ -87,6 +87,9 @@ int apsp_abi_version(void);
  * their count and summed duration.  Off by default; costs two event records per launch. */
 void apsp_set_profiling(int on);
 
+/* Number of kernels this library has launched in the process (all devices, all calls). */
+long long apsp_launch_count(void);
+
 /* Scratch bytes the device-level calls need when ws != NULL. */
 size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block);
 

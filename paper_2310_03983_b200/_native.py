@@ -38,6 +38,7 @@ EXPORTED_SYMBOLS = (
     "apsp_last_error",
     "apsp_abi_version",
     "apsp_set_profiling",
+    "apsp_launch_count",
     "apsp_workspace_bytes",
     "apsp_fw_blocked",
     "apsp_fw_classic",
@@ -114,6 +115,7 @@ _SIGNATURES = {
     "apsp_last_error": (ctypes.c_char_p, []),
     "apsp_abi_version": (_i32, []),
     "apsp_set_profiling": (None, [_i32]),
+    "apsp_launch_count": (ctypes.c_longlong, []),
     "apsp_workspace_bytes": (_sz, [_i32, _i32, _i64, _i32]),
     "apsp_fw_blocked": (_i32, [_i32, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _sz, _vp, _info_p]),
     "apsp_fw_classic": (_i32, [_i32, _i64, _vp, _i64, _vp, _i64, _vp, _info_p]),

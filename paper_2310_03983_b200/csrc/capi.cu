@@ -12,6 +12,7 @@
 
 namespace apsp {
 const char* last_error();
+long long launch_count();
 int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out,
                          int64_t ldo, cudaStream_t s);
 }
@@ -1067,6 +1068,7 @@ static int rect_d(const void* h, int64_t ldh, int64_t rows, int64_t cols, int st
     default: return set_error(APSP_EINVAL, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -1226,6 +1228,7 @@ extern "C" {
 
 const char* apsp_last_error(void) { return apsp::last_error(); }
 void apsp_set_profiling(int on) { g_prof.on = on != 0; }
+long long apsp_launch_count(void) { return apsp::launch_count(); }
 
 int apsp_scan(int dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
               apsp_scan_result* out, void* stream) {

@@ -83,5 +83,6 @@ __device__ __forceinline__ int32_t vimin3(int32_t a, int32_t b, int32_t c) { ret
 
 int set_cuda_error(cudaError_t e, const char* what, const char* file, int line);
 int set_error(int code, const char* fmt, ...);
+void count_launches(long long k);   // process-wide kernel launch counter (apsp_launch_count)
 
 }  // namespace apsp

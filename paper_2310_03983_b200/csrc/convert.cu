@@ -1,6 +1,7 @@
 // Input scan (K7), API dtype <-> store conversion with padding and pred initialisation,
 // result certificate (max finite), index copies and the minplus_product witness clear.
 // All are HBM-bound elementwise kernels: grid-stride, 16B-friendly row-major sweeps.
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include "launch.h"
@@ -93,6 +94,7 @@ int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t c
     default: return set_error(2, "unknown dtype %d", in_dtype);
   }
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -137,6 +139,7 @@ static int to_store_d(const void* h, int64_t ldh, int64_t n, int store, void* Dp
     default: return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -194,6 +197,7 @@ static int from_store_s(const void* in, int64_t ld, int64_t rows, int64_t cols, 
     default: return set_error(2, "unknown dtype %d", out_dtype);
   }
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -226,6 +230,7 @@ int launch_copy_idx(const int32_t* P, int64_t ldp, int64_t rows, int64_t cols, i
   if (out_dtype == API_I64) copy_idx_kernel<int64_t><<<g, 256, 0, s>>>(P, ldp, rows, cols, (int64_t*)out, ldo);
   else copy_idx_kernel<int32_t><<<g, 256, 0, s>>>(P, ldp, rows, cols, (int32_t*)out, ldo);
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -240,6 +245,7 @@ __global__ void fill_idx_kernel(int32_t* P, int64_t ldp, int64_t rows, int64_t c
 int launch_fill_idx(int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int32_t v, cudaStream_t s) {
   fill_idx_kernel<<<grid_for(rows * cols), 256, 0, s>>>(P, ldp, rows, cols, v);
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -291,6 +297,7 @@ int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_
     default: return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -338,6 +345,7 @@ int launch_witness_clear(int store, const void* X, int64_t ldx, const void* Y, i
   }
 #undef WC
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -357,5 +365,9 @@ int set_cuda_error(cudaError_t e, const char* what, const char* file, int line) 
 }
 
 const char* last_error() { return g_err; }
+
+static std::atomic<long long> g_launches{0};
+void count_launches(long long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 }  // namespace apsp

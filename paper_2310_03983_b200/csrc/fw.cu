@@ -63,6 +63,7 @@ int launch_fw_step(int store, void* D, int64_t ld, int64_t n, int64_t k, int32_t
     default: return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -345,6 +346,7 @@ static int close_impl(void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, 
   block_close_kernel<S><<<1, 512, 0, s>>>(static_cast<typename StoreT<S>::T*>(D), ld, lo, int(m), idx, ldi, mode,
                                            via_off, st);
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -370,6 +372,7 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
     block_close_u8_kernel<<<1, 512, sizeof(CloseU8Smem), s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
                                                               mode, via_off);
     APSP_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
     return 0;
   }
   switch (store) {
@@ -515,6 +518,7 @@ static int panel_rows_impl(const void* Dg, int64_t ldg, void* T_, int64_t ldt, i
                                                                ldt, PT, ldpt, int(b), ncols, mode, via_off, skip_lo,
                                                                skip_hi, st);
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 
@@ -535,6 +539,7 @@ static int panel_cols_impl(const void* Dg, int64_t ldg, const int32_t* PDg, int6
                                                                static_cast<T*>(T_), ldt, PT, ldpt, int(b), nrows, mode,
                                                                via_off, skip_lo, skip_hi, st);
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 

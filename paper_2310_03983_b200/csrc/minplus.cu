@@ -629,6 +629,7 @@ int launch_prep_narrow(int store, const void* A, int64_t lda, const void* B, int
     return set_error(2, "panel prep is for the narrow tiers");
   }
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(2);
   return 0;
 }
 
@@ -985,6 +986,7 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
       return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
   return 0;
 }
 

@@ -484,6 +484,7 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.apsp_launch_count()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         dist.barrier()
@@ -493,6 +494,7 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
         e1.record()
         torch.cuda.synchronize()
         dist.barrier()
+    launches = comm.allreduce_sum(lib.apsp_launch_count() - launches0)   # all ranks' kernels
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
@@ -523,7 +525,7 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
                 "scaling": "weak", "vs_baseline": None, "dtype": f"tier {res.info['tier']}; int32 in/out",
                 "data": "synthetic (reference generator, bit-identical to apsp.generate)",
                 "config": config(n, args.rho, world) | {"block": block, "rows_per_rank": R},
-                "clocks": clk.summary(), "gpu_launches": None, "e2e": e2e, "cpu_baseline": None,
+                "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e, "cpu_baseline": None,
                 "tier": res.info["tier"]}
         print(json.dumps(line), flush=True)
     dist.barrier()

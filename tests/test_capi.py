@@ -18,7 +18,7 @@ from paper_2310_03983_b200 import _native as nat
 
 def declared_symbols():
     text = (ROOT / "include" / "apsp_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\*?\s+\*?(apsp_[a-z_0-9]+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:[a-z_0-9]+\*?\s+)+\*?(apsp_[a-z_0-9]+)\s*\(", text, re.M)))
 
 
 def test_header_and_binding_agree():
