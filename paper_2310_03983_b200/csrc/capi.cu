@@ -149,7 +149,7 @@ int check_scan(const ScanResult& sc) {
   return 0;
 }
 
-bool narrow_store(int store) { return store == STORE_U8 || store == STORE_U16; }
+bool bulk_store(int store) { return store == STORE_U8 || store == STORE_U16 || store == STORE_W32; }
 
 // Candidate tiers, narrowest first.  allow_u16: the caller runs only aligned products (the
 // u16 tier exists only as bulk-staged tiles).
@@ -168,11 +168,13 @@ std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced, bool al
     return {forced};
   }
   // Skip narrow tiers whose certificate would almost surely fail: on random-like graphs the
-  // largest distance grows like w_max * ln(n) / ln(average degree).  The estimate only picks
-  // the starting tier; the certificate still decides exactness.
+  // largest distance grows like w_max * ln(n) / ln(average degree), with a larger constant on
+  // very sparse graphs (degree < 8: the diameter's long tails; fitted on the generator sweep,
+  // profiles/r01_configs_sparse.json).  The estimate only picks the starting tier; the
+  // certificate still decides exactness.
   const double n = n_vert > 0 ? double(n_vert) : 1.0;
   const double deg = std::max(double(sc.finite_offdiag) / n, 1.5);
-  const double m_est = 0.5 * double(w) * std::log(std::max(n, 2.0)) / std::log(deg);
+  const double m_est = (deg < 8.0 ? 0.8 : 0.5) * double(w) * std::log(std::max(n, 2.0)) / std::log(deg);
   std::vector<int> t;
   if (integral && w <= U8_INF - 1 && m_est + w <= U8_INF - 1) t.push_back(APSP_TIER_U8);
   if (allow_u16 && integral && w <= U16_INF - 1 && m_est + w <= U16_INF - 1) t.push_back(APSP_TIER_U16);
@@ -224,8 +226,8 @@ struct FwCtx {
 size_t fw_scratch_bytes(int64_t m, int b, size_t es) {
   size_t v = size_t(b) * m * 4 + 256;                      // pred row-panel snapshot
   if (b > TILE_ALIGN) v += 2 * size_t(b) * m * es + 256;   // value snapshots (non-narrow tiers)
-  v += 2 * (prep_u8_bytes(m, m, b) + 256);                 // phase-3 panel layouts (double buffered)
-  v += prep_u8_bytes(m, b, b) + 256;                       // phase-2 layouts (max of row/col product)
+  v += 2 * (prep_bytes(m, m, b) + 256);                 // phase-3 panel layouts (double buffered)
+  v += prep_bytes(m, b, b) + 256;                       // phase-2 layouts (max of row/col product)
   if (b > TILE_ALIGN) v += fw_scratch_bytes(b, TILE_ALIGN, es) + 256;   // phase-1 sub-run
   return v;
 }
@@ -242,10 +244,10 @@ void fw_carve(FwCtx& c, char* scratch, int64_t N) {
   }
   for (int q = 0; q < 2; q++) {
     c.prep[q] = p;
-    p += prep_u8_bytes(N, N, c.b) + 256;
+    p += prep_bytes(N, N, c.b) + 256;
   }
   c.p2prep = p;
-  p += prep_u8_bytes(N, c.b, c.b) + 256;
+  p += prep_bytes(N, c.b, c.b) + 256;
   if (c.b > TILE_ALIGN) c.sub = p;
 }
 
@@ -289,7 +291,7 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   char* Dg = c.D + (k0 * c.ld + k0) * c.es;
   char* rowp = c.D + k0 * c.ld * c.es;
   char* colp = c.D + k0 * c.es;
-  const bool nt = narrow_store(c.store) && c.p2prep;   // bulk-staged narrow tiles (prep = snapshot)
+  const bool nt = bulk_store(c.store) && c.p2prep;   // bulk-staged narrow tiles (prep = snapshot)
   const bool snap = !nt && b > TILE_ALIGN;
   if (c.P && c.mode == IDX_PRED) {
     APSP_CUDA_TRY(cudaMemcpy2DAsync(c.predsnap, size_t(m) * 4, c.P + k0 * c.ldp, size_t(c.ldp) * 4, size_t(m) * 4,
@@ -313,7 +315,7 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
   a.status = c.st;
   if (nt) {
-    rc = launch_prep_narrow(c.store, Dg, c.ld, rowp, c.ld, b, m, b, prep_a(c.p2prep), prep_b(c.p2prep, b, b), s);
+    rc = launch_prep_bulk(c.store, Dg, c.ld, rowp, c.ld, b, m, b, prep_a(c.p2prep), prep_b(c.p2prep, b, b), s);
     if (rc) return rc;
     a.Aprep = prep_a(c.p2prep);
     a.Bprep = prep_b(c.p2prep, b, b);
@@ -333,7 +335,7 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   q.skip_row_lo = k0; q.skip_row_hi = k0 + b;
   q.status = c.st;
   if (nt) {
-    rc = launch_prep_narrow(c.store, colp, c.ld, Dg, c.ld, m, b, b, prep_a(c.p2prep), prep_b(c.p2prep, m, b), s);
+    rc = launch_prep_bulk(c.store, colp, c.ld, Dg, c.ld, m, b, b, prep_a(c.p2prep), prep_b(c.p2prep, m, b), s);
     if (rc) return rc;
     q.Aprep = prep_a(c.p2prep);
     q.Bprep = prep_b(c.p2prep, m, b);
@@ -341,10 +343,10 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   }
   c.launches += 2;
   rc = launch_minplus(c.store, q, s);
-  if (rc || !c.prep[0] || !narrow_store(c.store)) return rc;
+  if (rc || !c.prep[0] || !bulk_store(c.store)) return rc;
   char* slot = c.prep[(k0 / b) & 1];
   c.launches += 2;
-  return launch_prep_narrow(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
+  return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
 }
 
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
@@ -365,7 +367,7 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   if (only_next >= 0) { a.only_lo = only_next; a.only_hi = only_next + c.b; }
   if (skip_next >= 0) { a.skip2_lo = skip_next; a.skip2_hi = skip_next + c.b; }
   a.status = c.st;
-  if (c.prep[0] && narrow_store(c.store)) {
+  if (c.prep[0] && bulk_store(c.store)) {
     char* slot = c.prep[(k0 / c.b) & 1];
     a.Aprep = prep_a(slot);
     a.Bprep = prep_b(slot, c.m, c.b);
@@ -667,8 +669,8 @@ struct RK {
     a.mode = mode;
     a.status = st;
     launches++;
-    if (prep && narrow_store(store) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
-      int rc = launch_prep_narrow(store, A, lda, B, ldb, m, n, k, prep_a(prep), prep_b(prep, m, k), s);
+    if (prep && bulk_store(store) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
+      int rc = launch_prep_bulk(store, A, lda, B, ldb, m, n, k, prep_a(prep), prep_b(prep, m, k), s);
       if (rc) return rc;
       a.Aprep = prep_a(prep);
       a.Bprep = prep_b(prep, m, k);
@@ -744,7 +746,7 @@ size_t rk_extra_bytes(int64_t N, int aligned, int thr) {
   if (!aligned) return 0;
   const int64_t h = rk_half(N, aligned);
   const int64_t leaf = std::max<int64_t>(round_up(std::min<int64_t>(thr, N), TILE_ALIGN), TILE_ALIGN);
-  return prep_u8_bytes(h, h, h) + 512 + fw_scratch_bytes(leaf, TILE_ALIGN, 4) + 512;
+  return prep_bytes(h, h, h) + 512 + fw_scratch_bytes(leaf, TILE_ALIGN, 4) + 512;
 }
 
 size_t rk_ws_bytes(int dtype, int64_t n, int aligned, int thr = 1 << 30) {
@@ -775,7 +777,7 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
   char* sV = p;
   p += size_t(h + 8) * (h + 8) * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 512;
   char* rkprep = aligned ? p : nullptr;
-  char* leafws = aligned ? p + ((prep_u8_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
+  char* leafws = aligned ? p + ((prep_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
   Header hdr{};
   Timer tm(s);
   rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
@@ -1097,7 +1099,7 @@ namespace {
 size_t shard_scratch_bytes(int64_t N, int64_t R, int b, size_t es) {
   size_t v = size_t(b) * N * 4 + 256;                                         // pred row-panel snapshot
   if (b > TILE_ALIGN) v += size_t(b) * N * es + size_t(R) * b * es + 512;     // value snapshots
-  v += std::max(prep_u8_bytes(b, N, b), prep_u8_bytes(std::max<int64_t>(R, b), N, b)) + 256;   // panel layouts
+  v += std::max(prep_bytes(b, N, b), prep_bytes(std::max<int64_t>(R, b), N, b)) + 256;   // panel layouts
   if (b > TILE_ALIGN) v += fw_scratch_bytes(b, TILE_ALIGN, es) + 256;        // phase-1 sub-run
   return v;
 }
@@ -1121,7 +1123,7 @@ ShardScratch shard_carve(void* scratch, int64_t N, int64_t R, int b, size_t es) 
     p += size_t(b) * N * es + size_t(R) * b * es + 512;
   }
   c.prep = p;
-  p += std::max(prep_u8_bytes(b, N, b), prep_u8_bytes(std::max<int64_t>(R, b), N, b)) + 256;
+  p += std::max(prep_bytes(b, N, b), prep_bytes(std::max<int64_t>(R, b), N, b)) + 256;
   if (b > TILE_ALIGN) c.sub = p;
   return c;
 }
@@ -1144,7 +1146,7 @@ int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* 
   int rc = fw_phase1(c, 0, s);                           // diagonal block, classic order
   if (rc) return rc;
   char* rowp = D + lrow * ld * es;
-  const bool nt = narrow_store(store);
+  const bool nt = bulk_store(store);
   const bool snap = !nt && b > TILE_ALIGN;
   if (P) APSP_CUDA_TRY(cudaMemcpy2DAsync(sc.predsnap, size_t(N) * 4, P + lrow * ldp, size_t(ldp) * 4, size_t(N) * 4,
                                          size_t(b), cudaMemcpyDeviceToDevice, s));
@@ -1158,7 +1160,7 @@ int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* 
   a.m = b; a.n = N; a.k = b; a.inner_off = k0; a.mode = IDX_PRED;
   a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
   if (nt) {
-    if ((rc = launch_prep_narrow(store, c.D, ld, rowp, ld, b, N, b, prep_a(sc.prep), prep_b(sc.prep, b, b), s)))
+    if ((rc = launch_prep_bulk(store, c.D, ld, rowp, ld, b, N, b, prep_a(sc.prep), prep_b(sc.prep, b, b), s)))
       return rc;
     a.Aprep = prep_a(sc.prep);
     a.Bprep = prep_b(sc.prep, b, b);
@@ -1179,7 +1181,7 @@ int shard_update_impl(int tier, int64_t N, int b, int64_t row_lo, int64_t row_hi
   char* D = static_cast<char*>(Dv) + row_lo * ld * es;      // the processed row range
   int32_t* Pr = P ? P + row_lo * ldp : nullptr;
   const char* pv = static_cast<const char*>(panel);
-  const bool nt = narrow_store(store);
+  const bool nt = bulk_store(store);
   const bool snap = !nt && b > TILE_ALIGN;
   const bool skip = skip_lo >= 0 && skip_hi > skip_lo;
   int rc = 0;
@@ -1194,7 +1196,7 @@ int shard_update_impl(int tier, int64_t N, int b, int64_t row_lo, int64_t row_hi
   q.m = R; q.n = b; q.k = b; q.inner_off = k0; q.mode = IDX_PRED;
   if (skip) { q.skip_row_lo = skip_lo - row_lo; q.skip_row_hi = skip_hi - row_lo; }
   if (nt) {
-    if ((rc = launch_prep_narrow(store, D + k0 * es, ld, pv + k0 * es, ldpv, R, b, b, prep_a(sc.prep),
+    if ((rc = launch_prep_bulk(store, D + k0 * es, ld, pv + k0 * es, ldpv, R, b, b, prep_a(sc.prep),
                                  prep_b(sc.prep, R, b), s)))
       return rc;
     q.Aprep = prep_a(sc.prep);
@@ -1212,7 +1214,7 @@ int shard_update_impl(int tier, int64_t N, int b, int64_t row_lo, int64_t row_hi
   if (skip) { a.skip_row_lo = skip_lo - row_lo; a.skip_row_hi = skip_hi - row_lo; }
   a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
   if (nt) {
-    if ((rc = launch_prep_narrow(store, D + k0 * es, ld, pv, ldpv, R, N, b, prep_a(sc.prep), prep_b(sc.prep, R, b),
+    if ((rc = launch_prep_bulk(store, D + k0 * es, ld, pv, ldpv, R, N, b, prep_a(sc.prep), prep_b(sc.prep, R, b),
                                  s)))
       return rc;
     a.Aprep = prep_a(sc.prep);

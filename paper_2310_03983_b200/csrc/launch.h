@@ -26,19 +26,18 @@ struct MinplusArgs {
   int64_t only_lo, only_hi;       // if lo < hi: the grid enumerates only the tiles of this cross
   Status* status;                 // optional: overflow flag (+ changed flag if track_changed)
   int track_changed;              // set status->changed on any strict improvement (squaring)
-  // u8 tier only: operand panels pre-laid-out by launch_prep_u8 (bulk-copy staging); null = off
-  const uint32_t* Aprep;          // [m/128][k/32][32][128] replicated keys
-  const uint16_t* Bprep;          // [n/128][k/32][32][128] tagged keys
+  // u8 / u16 / w32 tiers: operand panels pre-laid-out by launch_prep_bulk (bulk-copy staging);
+  // null = off.  Bprep is uint16 keys for u8/u16 and uint32 keys for w32.
+  const uint32_t* Aprep;          // [m/128][k/32][32][128] keys (u8/u16: replicated into both halves)
+  const void* Bprep;              // [n/128][k/32][32][128] tagged keys
 };
 
 // Lay the u8 operand panels out in the tile kernel's shared-memory format, once per product:
 // A (m x k) -> replicated 16-bit key pairs, B (k x n) -> tagged 16-bit keys.  m, n multiples of
 // 128 and k a multiple of 32 (the FW phase-3 case).
-size_t prep_u8_bytes(int64_t m, int64_t n, int64_t k);
-int launch_prep_u8(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n, int64_t k,
-                   uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s);
-int launch_prep_narrow(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
-                       int64_t k, uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s);
+size_t prep_bytes(int64_t m, int64_t n, int64_t k);
+int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
+                       int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s);
 
 // Default-initialised args: nothing skipped, full grid.
 inline MinplusArgs minplus_args() {

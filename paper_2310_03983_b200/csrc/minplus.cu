@@ -430,7 +430,8 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p, int tp
     const int slot = int(g % U8_STAGES);
     mbar_expect_tx(&sm.bar[slot], U8_CHUNK_A + U8_CHUNK_B);
     bulk_g2s(&sm.As[slot][0][0], p.Aprep + ((tiles_i0[tt] / BM) * nch + c) * (SUB * BM), U8_CHUNK_A, &sm.bar[slot]);
-    bulk_g2s(&sm.Bs[slot][0][0], p.Bprep + ((tiles_j0[tt] / BN) * nch + c) * (SUB * BN), U8_CHUNK_B, &sm.bar[slot]);
+    bulk_g2s(&sm.Bs[slot][0][0], static_cast<const uint16_t*>(p.Bprep) + ((tiles_j0[tt] / BN) * nch + c) * (SUB * BN),
+             U8_CHUNK_B, &sm.bar[slot]);
   };
   if (t == 0)
     for (int64_t g = 0; g < U8_STAGES && g < total_g; g++) issue(g);
@@ -609,11 +610,205 @@ __global__ void prep_nt_b_kernel(const typename Narrow<S>::T* B, int64_t ldb, in
   dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
 }
 
-size_t prep_u8_bytes(int64_t m, int64_t n, int64_t k) { return size_t(m) * k * 4 + size_t(k) * n * 2 + 256; }
+// ------------------------------------------------------------------------------------
+// w32 tier with pre-laid-out panels: int32 store (< 2^24 - 1), unsigned 32-bit keys
+// key = v << 7 | tag, decode window 3 chunks (tags 1..96).  INF + INF + tag < 2^32, so the
+// sums never wrap.  ptxas turns min3(acc, a0 + b0, a1 + b1) into two VIADDMNMX.U32 (ALU, one
+// update per instruction, 18.6 T upd/s ceiling); forcing the sums onto the FMA pipe as IMAD +
+// VIMNMX3 measured slower (341 vs 293 ms, n = 16384).  Same staging as the narrow kernel:
+// cp.async.bulk + mbarrier ring for A/B, cp.async for C.
+// ------------------------------------------------------------------------------------
+constexpr int W32_TAG = 7, W32_WIN = 3, W32_STAGES = 3;
 
-int launch_prep_narrow(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
-                       int64_t k, uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s) {
-  const size_t es = store == STORE_U16 ? 2 : 1;
+constexpr uint32_t W32_CHUNK = SUB * BM * 4;   // A and B chunk bytes (128 x 32 keys each)
+struct SmemW32NT {
+  uint32_t As[W32_STAGES][SUB][BM];
+  uint32_t Bs[W32_STAGES][SUB][BN];
+  int32_t Cs[BM][BN];
+  unsigned long long bar[W32_STAGES];
+};
+
+__global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
+  constexpr uint32_t KINF = uint32_t(W32_INF) << W32_TAG;
+  constexpr uint32_t TMASK = (1u << W32_TAG) - 1u;
+  extern __shared__ __align__(128) unsigned char smraw_w32[];
+  SmemW32NT& sm = *reinterpret_cast<SmemW32NT*>(smraw_w32);
+  int64_t i0, j0;
+  tile_origin(p, BM, BN, i0, j0);
+  if (tile_skipped(p, i0, j0, BM, BN)) return;
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int64_t nch = p.k / SUB;
+  const uint32_t* Ap = p.Aprep + (i0 / BM) * nch * (SUB * BM);
+  const uint32_t* Bp = static_cast<const uint32_t*>(p.Bprep) + (j0 / BN) * nch * (SUB * BN);
+  if (t == 0) {
+    for (int s = 0; s < W32_STAGES; s++) mbar_init(&sm.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t c) {
+    const int slot = int(c % W32_STAGES);
+    mbar_expect_tx(&sm.bar[slot], 2 * W32_CHUNK);
+    bulk_g2s(&sm.As[slot][0][0], Ap + c * (SUB * BM), W32_CHUNK, &sm.bar[slot]);
+    bulk_g2s(&sm.Bs[slot][0][0], Bp + c * (SUB * BN), W32_CHUNK, &sm.bar[slot]);
+  };
+  if (t == 0)
+    for (int64_t c = 0; c < W32_STAGES && c < nch; c++) issue(c);
+  {  // C tile -> smem (merged after chunk 0)
+    const int r = t >> 1;
+    const char* src = reinterpret_cast<const char*>(static_cast<const int32_t*>(p.C) + (i0 + r) * p.ldc + j0) +
+                      256 * (t & 1);
+    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r][0]) + 256 * (t & 1));
+#pragma unroll
+    for (int q = 0; q < 16; q++)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  uint32_t acc[8][8];
+  uint32_t kst[8][4];
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) acc[r][q] = KINF;
+#pragma unroll
+    for (int q = 0; q < 4; q++) kst[r][q] = 0u;
+  }
+  for (int64_t c = 0; c < nch; c++) {
+    const int slot = int(c % W32_STAGES);
+    mbar_wait(&sm.bar[slot], uint32_t((c / W32_STAGES) & 1));
+#pragma unroll 4
+    for (int kk = 0; kk < SUB; kk += 2) {
+      uint32_t a0[8], a1[8], b0[8], b1[8];
+      *reinterpret_cast<uint4*>(a0) = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
+      *reinterpret_cast<uint4*>(a0 + 4) = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
+      *reinterpret_cast<uint4*>(a1) = *reinterpret_cast<const uint4*>(&sm.As[slot][kk + 1][4 * ty]);
+      *reinterpret_cast<uint4*>(a1 + 4) = *reinterpret_cast<const uint4*>(&sm.As[slot][kk + 1][64 + 4 * ty]);
+      *reinterpret_cast<uint4*>(b0) = *reinterpret_cast<const uint4*>(&sm.Bs[slot][kk][4 * tx]);
+      *reinterpret_cast<uint4*>(b0 + 4) = *reinterpret_cast<const uint4*>(&sm.Bs[slot][kk][64 + 4 * tx]);
+      *reinterpret_cast<uint4*>(b1) = *reinterpret_cast<const uint4*>(&sm.Bs[slot][kk + 1][4 * tx]);
+      *reinterpret_cast<uint4*>(b1 + 4) = *reinterpret_cast<const uint4*>(&sm.Bs[slot][kk + 1][64 + 4 * tx]);
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int q = 0; q < 8; q++) acc[r][q] = __vimin3_u32(acc[r][q], a0[r] + b0[q], a1[r] + b1[q]);
+    }
+    const int64_t wc = c % W32_WIN;
+    if (c == 0) {
+      asm volatile("cp.async.wait_all;\n" ::);
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const uint4 w = *reinterpret_cast<const uint4*>(&sm.Cs[ri][64 * h + 4 * tx]);
+          acc[r][4 * h] = min(acc[r][4 * h], w.x << W32_TAG);
+          acc[r][4 * h + 1] = min(acc[r][4 * h + 1], w.y << W32_TAG);
+          acc[r][4 * h + 2] = min(acc[r][4 * h + 2], w.z << W32_TAG);
+          acc[r][4 * h + 3] = min(acc[r][4 * h + 3], w.w << W32_TAG);
+        }
+      }
+    }
+    if (wc == W32_WIN - 1 || c + 1 == nch) {
+      uint32_t any = 0;
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int q = 0; q < 8; q++) any |= acc[r][q];
+      if (__any_sync(0xffffffffu, any & TMASK)) {
+        const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const uint32_t t0 = acc[r][2 * q] & TMASK, t1 = acc[r][2 * q + 1] & TMASK;
+            const uint32_t tg = __byte_perm(t0, t1, 0x5410);
+            const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
+            kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
+            acc[r][2 * q] -= t0;
+            acc[r][2 * q + 1] -= t1;
+          }
+      }
+    }
+    __syncthreads();   // every warp is done with this slot
+    if (t == 0 && c + W32_STAGES < nch) issue(c + W32_STAGES);
+  }
+  bool changed = false;
+  const int32_t* __restrict__ pb = p.predB;
+  int32_t* __restrict__ out = p.idx;
+  int32_t* Cw = static_cast<int32_t*>(p.C);
+  const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+    int32_t pv[2][4];
+    uint32_t ks[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+      ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
+      const int64_t j = j0 + 64 * h + 4 * tx;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        pv[h][q] = 0;
+        if (out && ks[h][q] != 0u)
+          pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
+                                          : int32_t(p.inner_off + ks[h][q] - 1u);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      if ((kst[r][2 * h] | kst[r][2 * h + 1]) == 0u) continue;
+      changed = true;
+      const int64_t j = j0 + 64 * h + 4 * tx;
+      *reinterpret_cast<int4*>(Cw + i * p.ldc + j) =
+          make_int4(int32_t(acc[r][4 * h] >> W32_TAG), int32_t(acc[r][4 * h + 1] >> W32_TAG),
+                    int32_t(acc[r][4 * h + 2] >> W32_TAG), int32_t(acc[r][4 * h + 3] >> W32_TAG));
+      if (!out) continue;
+      if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
+        *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          if (ks[h][q] != 0u) out[i * p.ldi + j + q] = pv[h][q];
+      }
+    }
+  }
+  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+}
+
+__global__ void prep_w32_a_kernel(const int32_t* A, int64_t lda, int64_t nch, uint32_t* Aprep) {
+  const int64_t rt = blockIdx.y, c = blockIdx.x;
+  const int t = threadIdx.x, r = t & 127, kb = 16 * (t >> 7);
+  const int4* src = reinterpret_cast<const int4*>(A + (rt * BM + r) * lda + c * SUB + kb);
+  uint32_t* dst = Aprep + (rt * nch + c) * (SUB * BM);
+  int32_t v[16];
+#pragma unroll
+  for (int q = 0; q < 4; q++) reinterpret_cast<int4*>(v)[q] = __ldg(src + q);
+#pragma unroll
+  for (int q = 0; q < 16; q++) dst[(kb + q) * BM + r] = uint32_t(v[q]) << W32_TAG;
+}
+
+__global__ void prep_w32_b_kernel(const int32_t* B, int64_t ldb, int64_t nch, uint32_t* Bprep) {
+  const int64_t ct = blockIdx.y, c = blockIdx.x;
+  const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
+  const int4* src = reinterpret_cast<const int4*>(B + (c * SUB + kk) * ldb + ct * BN + cb);
+  const uint32_t tag = uint32_t(SUB * (c % W32_WIN) + kk + 1);   // 1..96 inside a decode window
+  uint4* dst = reinterpret_cast<uint4*>(Bprep + (ct * nch + c) * (SUB * BN) + kk * BN + cb);
+#pragma unroll
+  for (int q = 0; q < 4; q++) {
+    const int4 v = __ldg(src + q);
+    dst[q] = make_uint4((uint32_t(v.x) << W32_TAG) | tag, (uint32_t(v.y) << W32_TAG) | tag,
+                        (uint32_t(v.z) << W32_TAG) | tag, (uint32_t(v.w) << W32_TAG) | tag);
+  }
+}
+
+size_t prep_bytes(int64_t m, int64_t n, int64_t k) {   // A keys + B keys (uint32 B keys for w32)
+  return ((size_t(m) * k * 4 + 255) / 256) * 256 + size_t(k) * n * 4 + 256;
+}
+
+int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
+                     int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s) {
+  const size_t es = store == STORE_W32 ? 4 : store == STORE_U16 ? 2 : 1;
   if (m % BM || n % BN || k % SUB || (lda * es) % 16 || (ldb * es) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
     return set_error(2, "panel prep needs 128-multiple m/n, 32-multiple k and 16-byte aligned panels");
@@ -621,21 +816,20 @@ int launch_prep_narrow(int store, const void* A, int64_t lda, const void* B, int
   const dim3 ga(unsigned(nch), unsigned(m / BM)), gb(unsigned(nch), unsigned(n / BN));
   if (store == STORE_U8) {
     prep_nt_a_kernel<STORE_U8><<<ga, NT, 0, s>>>(static_cast<const uint8_t*>(A), lda, nch, Aprep);
-    prep_nt_b_kernel<STORE_U8><<<gb, NT, 0, s>>>(static_cast<const uint8_t*>(B), ldb, nch, Bprep);
+    prep_nt_b_kernel<STORE_U8><<<gb, NT, 0, s>>>(static_cast<const uint8_t*>(B), ldb, nch, static_cast<uint16_t*>(Bprep));
   } else if (store == STORE_U16) {
     prep_nt_a_kernel<STORE_U16><<<ga, NT, 0, s>>>(static_cast<const uint16_t*>(A), lda, nch, Aprep);
-    prep_nt_b_kernel<STORE_U16><<<gb, NT, 0, s>>>(static_cast<const uint16_t*>(B), ldb, nch, Bprep);
+    prep_nt_b_kernel<STORE_U16><<<gb, NT, 0, s>>>(static_cast<const uint16_t*>(B), ldb, nch,
+                                                  static_cast<uint16_t*>(Bprep));
+  } else if (store == STORE_W32) {
+    prep_w32_a_kernel<<<ga, NT, 0, s>>>(static_cast<const int32_t*>(A), lda, nch, Aprep);
+    prep_w32_b_kernel<<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep));
   } else {
-    return set_error(2, "panel prep is for the narrow tiers");
+    return set_error(2, "panel prep is for the u8 / u16 / w32 tiers");
   }
   APSP_CUDA_TRY(cudaGetLastError());
   count_launches(2);
   return 0;
-}
-
-int launch_prep_u8(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n, int64_t k,
-                   uint32_t* Aprep, uint16_t* Bprep, cudaStream_t s) {
-  return launch_prep_narrow(STORE_U8, A, lda, B, ldb, m, n, k, Aprep, Bprep, s);
 }
 
 static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
@@ -645,6 +839,19 @@ static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
     return dim3(unsigned(w * nt_c + (nt_r - w) * w), 1);
   }
   return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
+}
+
+static int launch_w32nt(const MinplusArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_w32nt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(sizeof(SmemW32NT))));
+    attr = true;
+  }
+  if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * 4) % 16)
+    return set_error(2, "bulk-staged w32 tiles need full 128 x 128 tiles and 32-multiple k");
+  minplus_w32nt_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemW32NT), s>>>(a);
+  return 0;
 }
 
 template <int S>
@@ -958,6 +1165,11 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
       break;
     }
     case STORE_W32: {
+      if (a.Aprep && a.Bprep) {
+        const int rc = launch_w32nt(a, s);
+        if (rc) return rc;
+        break;
+      }
       static bool attr = false;
       if (!attr) {
         APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_w32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -81,7 +81,7 @@ def pick_tiers(dtype_code: int, scan: dict, n: int = 0) -> list[int]:
     w = scan["max_finite"]
     nv = max(n, 2)
     deg = max(scan.get("finite_offdiag", nv * nv) / nv, 1.5)
-    m_est = 0.5 * w * math.log(nv) / math.log(deg)
+    m_est = (0.8 if deg < 8 else 0.5) * w * math.log(nv) / math.log(deg)
     t = []
     if integral and w <= U8_LIMIT and m_est + w <= U8_LIMIT:
         t.append(nat.TIER_U8)

@@ -339,3 +339,19 @@ def test_large_fw_device_properties(cuda):
             best = torch.minimum(best, cand)
         best = torch.where(best >= INF_RAW, torch.tensor(INF_RAW, device=h.device), best)
         assert torch.equal(best, D[r]), r
+
+
+@pytest.mark.parametrize("block", [0, 128, 256])
+def test_w32_bulk_tier_wide_weights(cuda, block):
+    # weights up to 50000: only w32 / i64 certify; the w32 tier runs the bulk-staged kernel
+    # (7-bit tags, 3-chunk decode windows) in phases 2/3 and in the R-Kleene products
+    raw = random_graph_raw(777, 0.05, 50000, 5)
+    want_d, _ = orc.fw_classic(raw)
+    s = ap.fw_classic(ap.CostMatrix(raw), block=block)
+    assert s.info["tier"] == "w32"
+    assert np.array_equal(s.distances.raw, want_d)
+    pred_ok(raw, s.distances.raw, s.pred.raw)
+    r = ap.rkleene(ap.CostMatrix(raw), split="aligned", track="pred", base_threshold=256)
+    assert r.info["tier"] == "w32"
+    assert np.array_equal(r.distances.raw, want_d)
+    pred_ok(raw, r.distances.raw, r.pred.raw)
