@@ -169,6 +169,21 @@ int apsp_shard_finish(int tier, int dtype, int64_t rows, int64_t n, const void* 
                       int64_t ldp, void* dist, int64_t ldd, int32_t* pred, int64_t ldpo, int64_t* max_finite,
                       void* stream);
 
+/* ---- sharded R-Kleene: replicated matrix, products split by output row bands --
+ * Every rank holds the whole padded N x N store matrix D and pred P (apsp_shard_prepare with
+ * row0 = 0, rows = N; N a multiple of 128).  The host recursion (distributed.py run_rkleene,
+ * the order of solvers.py:239-286 with the 128-aligned split) calls apsp_rk_shard_leaf for the
+ * diagonal leaves (every rank, redundantly) and apsp_rk_shard_product for its band of output
+ * rows of each block product C <- min(C, A (x) B) (pred <- pred_b[k*][j]); the caller then
+ * all-gathers the bands.  Replaces the band loop of rkleene (solvers.py:239-286) across GPUs. */
+size_t apsp_rk_shard_scratch_bytes(int64_t N, int thr);
+int apsp_rk_shard_leaf(int tier, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lo, int64_t m, int thr,
+                       void* scratch, size_t scratch_bytes, void* stream);
+int apsp_rk_shard_product(int tier, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                          int32_t* idx, int64_t ldi, const int32_t* pred_b, int64_t ldpb, int64_t m, int64_t n,
+                          int64_t k, int64_t inner_off, int64_t N, int thr, void* scratch, size_t scratch_bytes,
+                          void* stream);
+
 /* ---- host-side matrix wire format of the reference (textio.py:70-119), multi-threaded ----------
  * apsp_format_matrix_i64: writes "n\n" + n rows of n fields (integer or INF) into out; returns
  * the byte count, or the required capacity when out is NULL / cap is too small, -2 for a

@@ -53,6 +53,9 @@ EXPORTED_SYMBOLS = (
     "apsp_shard_update",
     "apsp_shard_finish",
     "apsp_side_stream",
+    "apsp_rk_shard_scratch_bytes",
+    "apsp_rk_shard_leaf",
+    "apsp_rk_shard_product",
     "apsp_format_matrix_i64",
     "apsp_parse_matrix_i64",
 )
@@ -132,6 +135,10 @@ _SIGNATURES = {
     "apsp_shard_update": (_i32, [_i32, _i64, _i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64,
                                  _i64, _i64, _vp, _sz, _vp]),
     "apsp_side_stream": (_vp, []),
+    "apsp_rk_shard_scratch_bytes": (_sz, [_i64, _i32]),
+    "apsp_rk_shard_leaf": (_i32, [_i32, _vp, _i64, _vp, _i64, _i64, _i64, _i32, _vp, _sz, _vp]),
+    "apsp_rk_shard_product": (_i32, [_i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64,
+                                     _i64, _i64, _i64, _i32, _vp, _sz, _vp]),
     "apsp_format_matrix_i64": (_i64, [_vp, _i64, _vp, _i64]),
     "apsp_parse_matrix_i64": (_i64, [_vp, _i64, _i64, _vp, ctypes.POINTER(ctypes.c_int64)]),
     "apsp_shard_finish": (_i32, [_i32, _i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,

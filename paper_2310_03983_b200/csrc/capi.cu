@@ -1223,6 +1223,63 @@ int shard_update_impl(int tier, int64_t N, int b, int64_t row_lo, int64_t row_hi
   return timed_minplus(store, a, s);
 }
 
+// ---- sharded R-Kleene: replicated matrix, every block product split by output row bands ----
+// Every rank holds the whole N x N store matrix (N a multiple of 128, aligned split).  The host
+// schedule (distributed.py run_rkleene) mirrors RK::close; each of the six block products is
+// computed by every rank on its band of output rows (rk_shard_product) and the bands are then
+// all-gathered; the diagonal leaves are closed redundantly on every rank (rk_shard_leaf), so all
+// replicas stay bit-identical to the single-GPU aligned R-Kleene.
+size_t rk_shard_scratch_bytes(int64_t N, int thr) {
+  const int64_t h = rk_half(N, 1);
+  const int64_t leaf = std::max<int64_t>(round_up(std::min<int64_t>(thr, N), TILE_ALIGN), TILE_ALIGN);
+  return 256 + prep_bytes(h, h, h) + 512 + fw_scratch_bytes(leaf, TILE_ALIGN, 4) + 512;
+}
+
+int rk_shard_leaf_impl(int tier, void* Dv, int64_t ld, int32_t* P, int64_t ldp, int64_t lo, int64_t m, int thr,
+                       void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  const int store = tier_store(tier);
+  if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  if (lo % TILE_ALIGN || m % TILE_ALIGN || m <= 0) return set_error(APSP_EINVAL, "leaf blocks must be 128-aligned");
+  const int64_t N = ld;
+  if (scratch_bytes < rk_shard_scratch_bytes(N, thr)) return set_error(APSP_EINVAL, "rk shard scratch too small");
+  Status* st = static_cast<Status*>(scratch);
+  char* leafws = static_cast<char*>(scratch) + 256 + ((prep_bytes(rk_half(N, 1), rk_half(N, 1), rk_half(N, 1)) + 511) / 256) * 256;
+  char* D = static_cast<char*>(Dv);
+  const size_t es = store_elem_size(store);
+  int launches = 0;
+  if (m > TILE_ALIGN)
+    return fw_blocked_view(store, D + (lo * ld + lo) * es, ld, P + lo * ldp + lo, ldp, m, DEFAULT_BLOCK, IDX_PRED, lo,
+                           st, s, &launches, nullptr, leafws);
+  return launch_block_close(store, D, ld, lo, m, P, ldp, IDX_PRED, lo, st, s);
+}
+
+int rk_shard_product_impl(int tier, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                          int32_t* idx, int64_t ldi, const int32_t* predB, int64_t ldpb, int64_t m, int64_t n,
+                          int64_t k, int64_t inner_off, int64_t N, int thr, void* scratch, size_t scratch_bytes,
+                          cudaStream_t s) {
+  const int store = tier_store(tier);
+  if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
+  if (m <= 0 || n <= 0 || k <= 0) return 0;
+  if (scratch_bytes < rk_shard_scratch_bytes(N, thr)) return set_error(APSP_EINVAL, "rk shard scratch too small");
+  char* prep = static_cast<char*>(scratch) + 256;
+  MinplusArgs a = minplus_args();
+  a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
+  a.C = C; a.ldc = ldc;
+  a.idx = idx; a.ldi = ldi;
+  a.predB = predB; a.ldp = ldpb;
+  a.m = m; a.n = n; a.k = k;
+  a.inner_off = inner_off;
+  a.mode = IDX_PRED;
+  a.status = static_cast<Status*>(scratch);
+  if (bulk_store(store) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {   // as RK::mp
+    int rc = launch_prep_bulk(store, A, lda, B, ldb, m, n, k, prep_a(prep), prep_b(prep, m, k), s);
+    if (rc) return rc;
+    a.Aprep = prep_a(prep);
+    a.Bprep = prep_b(prep, m, k);
+  }
+  return timed_minplus(store, a, s);
+}
+
 }  // namespace
 
 // =============================================================================================
@@ -1295,6 +1352,21 @@ int apsp_shard_finish(int tier, int dtype, int64_t rows, int64_t n, const void* 
   APSP_CUDA_TRY(cudaStreamSynchronize(s));
   if (max_finite) *max_finite = rows > 0 && h.max_finite >= 0 ? h.max_finite : -1;
   return 0;
+}
+
+size_t apsp_rk_shard_scratch_bytes(int64_t N, int thr) { return rk_shard_scratch_bytes(N, thr); }
+
+int apsp_rk_shard_leaf(int tier, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lo, int64_t m, int thr,
+                       void* scratch, size_t scratch_bytes, void* stream) {
+  return rk_shard_leaf_impl(tier, D, ld, P, ldp, lo, m, thr, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int apsp_rk_shard_product(int tier, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                          int32_t* idx, int64_t ldi, const int32_t* pred_b, int64_t ldpb, int64_t m, int64_t n,
+                          int64_t k, int64_t inner_off, int64_t N, int thr, void* scratch, size_t scratch_bytes,
+                          void* stream) {
+  return rk_shard_product_impl(tier, A, lda, B, ldb, C, ldc, idx, ldi, pred_b, ldpb, m, n, k, inner_off, N, thr,
+                               scratch, scratch_bytes, (cudaStream_t)stream);
 }
 
 int apsp_abi_version(void) { return APSP_ABI_VERSION; }

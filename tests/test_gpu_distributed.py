@@ -4,6 +4,8 @@
   rank waits on another) and must be bit-identical -- distances AND predecessors -- to the
   single-GPU solver at the same pivot block.
 * fw_blocked_sharded is exercised end to end over a 1-rank NCCL process group.
+* rkleene_emulated / rkleene_sharded (replicated matrix, products split by output row bands)
+  must equal the single-GPU aligned R-Kleene bit for bit, on every replica.
 """
 
 from __future__ import annotations
@@ -60,10 +62,17 @@ def _nccl_worker(rank, port, out):
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     from paper_2310_03983_b200.distributed import TorchComm, fw_blocked_sharded
 
+    from paper_2310_03983_b200.distributed_rk import rkleene_sharded
+
     h = torch.from_numpy(ap.dense_costs(ap.GenParams(512, 0.1, 100, 3), np.int32)).cuda()
-    r = fw_blocked_sharded(h, 512, comm=TorchComm(torch.device("cuda", 0)), block=128)
+    comm = TorchComm(torch.device("cuda", 0))
+    r = fw_blocked_sharded(h, 512, comm=comm, block=128)
     single = ap.solve(h, "fw_blocked", block=128)
-    out.put(bool(torch.equal(r.distances, single.distances) and torch.equal(r.pred, single.index)))
+    ok = bool(torch.equal(r.distances, single.distances) and torch.equal(r.pred, single.index))
+    k = rkleene_sharded(h, 512, comm=comm, base_threshold=128)
+    ks = ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=128)
+    ok = ok and bool(torch.equal(k.distances, ks.distances) and torch.equal(k.pred, ks.index))
+    out.put(ok)
     dist.destroy_process_group()
 
 
@@ -80,3 +89,33 @@ def test_sharded_entry_over_nccl(cuda):
     proc.join(timeout=300)
     assert proc.exitcode == 0
     assert q.get(timeout=5)
+
+
+@pytest.mark.parametrize("n,world,thr,rho", [(1000, 2, 256, 0.05), (2048, 3, 512, 0.1), (700, 4, 128, 0.02),
+                                             (1500, 2, 2048, 0.1)])
+def test_rkleene_emulated_ranks_bitwise_equal_single_gpu(cuda, n, world, thr, rho):
+    from paper_2310_03983_b200.distributed_rk import rkleene_emulated
+
+    h = torch.from_numpy(ap.dense_costs(ap.GenParams(n, rho, 100, n + 1), np.int32)).cuda()
+    single = ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=thr)
+    d, p, info = rkleene_emulated(h, world, base_threshold=thr)
+    assert info["replicas_equal"]
+    assert info["tier"] == single.info["tier"]
+    assert torch.equal(d, single.distances)
+    assert torch.equal(p, single.index)
+    ok, why = ap.check_pred_tree(h, d, p, INF32)
+    assert ok, why
+
+
+def test_rkleene_emulated_tier_fallback(cuda):
+    from paper_2310_03983_b200.distributed_rk import rkleene_emulated
+
+    n = 600
+    raw = np.full((n, n), INF32, np.int32)
+    np.fill_diagonal(raw, 0)
+    raw[np.arange(n - 1), np.arange(1, n)] = 2          # a long path: u8 certificate must fail
+    h = torch.from_numpy(raw).cuda()
+    d, p, info = rkleene_emulated(h, 3, base_threshold=128)
+    assert info["tier"] == "w32" and info["replicas_equal"]
+    single = ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=128)
+    assert torch.equal(d, single.distances) and torch.equal(p, single.index)
