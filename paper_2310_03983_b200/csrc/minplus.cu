@@ -28,17 +28,17 @@ constexpr int kU8Unroll = APSP_U8_UNROLL;
 // (only_lo < only_hi): blockIdx.x enumerates the tiles of rows band + cols band [lo, hi)
 // (band width w tiles): first the w full tile rows, then the remaining rows of the w columns.
 __device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn, int64_t& i0, int64_t& j0) {
-  if (p.only_lo < p.only_hi) {
-    const int64_t w = (p.only_hi - p.only_lo) / bm, lo_t = p.only_lo / bm;
-    const int64_t nt_c = (p.n + bn - 1) / bn;
-    const int64_t id = blockIdx.x;
+  if (p.only_lo < p.only_hi) {   // tile counts fit 32 bits: 32-bit division (a 64-bit one is ~100 instr)
+    const int w = int((p.only_hi - p.only_lo) / bm), lo_t = int(p.only_lo / bm);
+    const int nt_c = int((p.n + bn - 1) / bn);
+    const int id = int(blockIdx.x);
     if (id < w * nt_c) {
-      i0 = (lo_t + id / nt_c) * bm;
-      j0 = (id % nt_c) * bn;
+      i0 = int64_t(lo_t + id / nt_c) * bm;
+      j0 = int64_t(id % nt_c) * bn;
     } else {
-      const int64_t id2 = id - w * nt_c, rr = id2 / w, cc = id2 % w;
-      i0 = (rr < lo_t ? rr : rr + w) * bm;
-      j0 = (lo_t + cc) * bn;
+      const int id2 = id - w * nt_c, rr = id2 / w, cc = id2 % w;
+      i0 = int64_t(rr < lo_t ? rr : rr + w) * bm;
+      j0 = int64_t(lo_t + cc) * bn;
     }
   } else {
     i0 = int64_t(blockIdx.y) * bm;
@@ -314,23 +314,23 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
 template <int S> struct Narrow;
 template <> struct Narrow<STORE_U8> {
   using T = uint8_t;
-  static constexpr int TAG = 7, WIN = 3;
+  static constexpr int TAG = 7, WIN = 3, STAGES = 3;
   static constexpr uint32_t INF = U8_INF;
 };
 template <> struct Narrow<STORE_U16> {
   using T = uint16_t;
-  static constexpr int TAG = 6, WIN = 1;
+  static constexpr int TAG = 6, WIN = 1, STAGES = 3;
   static constexpr uint32_t INF = U16_INF;
 };
 
-constexpr int U8_STAGES = 3;
 constexpr uint32_t U8_CHUNK_A = SUB * BM * 4, U8_CHUNK_B = SUB * BN * 2;
 template <int S>
-struct SmemNT {
-  uint32_t As[U8_STAGES][SUB][BM];
-  uint16_t Bs[U8_STAGES][SUB][BN];
+struct SmemNT {   // u8: 4 x 24 KB ring + 16 KB C = 112 KB (2 CTAs / SM); u16: 3 x 24 KB + 32 KB
+  uint32_t As[Narrow<S>::STAGES][SUB][BM];
+  uint16_t Bs[Narrow<S>::STAGES][SUB][BN];
   typename Narrow<S>::T Cs[BM][BN];
-  unsigned long long bar[U8_STAGES];
+  unsigned long long full[Narrow<S>::STAGES];   // bulk copy landed (tx count)
+  unsigned int done[Narrow<S>::STAGES];         // warps finished with the slot's chunk
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -342,6 +342,9 @@ __device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count)
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -351,6 +354,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity)
+      : "memory");
+}
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes instead
+// of re-issuing the probe (a spinning producer warp steals issue slots from the ALU-bound
+// consumers on its SM sub-partition)
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(1000000u)
       : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b) {
@@ -380,198 +397,192 @@ __device__ __forceinline__ void tile_at(const MinplusArgs& p, int64_t v, int bm,
   }
 }
 
-__device__ __forceinline__ int64_t tile_count(const MinplusArgs& p, int bm, int bn) {
-  const int64_t nt_r = (p.m + bm - 1) / bm, nt_c = (p.n + bn - 1) / bn;
-  if (p.only_lo < p.only_hi) {
-    const int64_t w = (p.only_hi - p.only_lo) / bm;
-    return w * nt_c + (nt_r - w) * w;
-  }
-  return nt_r * nt_c;
-}
-
-constexpr int U8_TPC_MAX = 8;       // tiles per CTA (ring and C prefetch run across tiles)
-
+// One 128 x 128 tile per CTA (8 warps, 8 x 8 cells per thread).  The pre-laid-out A/B chunks
+// stream through a STAGES-slot ring with cp.async.bulk (full mbarriers carry the tx count).
+// No barrier sits in the k loop: each warp counts itself out of a slot when it has consumed
+// it, and the LAST warp out refills the slot with chunk c + STAGES -- no warp ever waits for
+// another, only for data.  Each thread prefetches exactly its own 8 x 8 C cells (cp.async),
+// so the merge after chunk 0 needs no barrier either.
 template <int S>
-__global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p, int tpc) {
+__global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   using NR = Narrow<S>;
   using T = typename NR::T;
-  constexpr int TAG = NR::TAG, WIN = NR::WIN;
+  constexpr int TAG = NR::TAG, WIN = NR::WIN, STAGES = NR::STAGES;
   constexpr uint32_t KINF2 = (NR::INF << TAG) * 0x00010001u;
   constexpr uint32_t TMASK2 = ((1u << TAG) - 1u) * 0x00010001u;
-  constexpr int CB = BN * int(sizeof(T)) / 2;     // C bytes per thread-half-row
+  constexpr int CW = 4 * int(sizeof(T));          // bytes of one 4-cell C segment
   extern __shared__ __align__(128) unsigned char smraw_nt[];
   SmemNT<S>& sm = *reinterpret_cast<SmemNT<S>*>(smraw_nt);
-  __shared__ int64_t tiles_i0[U8_TPC_MAX], tiles_j0[U8_TPC_MAX];
-  __shared__ int ntiles;
-  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  const int64_t nch = p.k / SUB;
+  int64_t i0, j0;
+  tile_origin(p, BM, BN, i0, j0);
+  if (tile_skipped(p, i0, j0, BM, BN)) return;
+  const int t = threadIdx.x;
+  const int nch = int(p.k / SUB);
+  const uint32_t* Ap = p.Aprep + (i0 / BM) * int64_t(nch) * (SUB * BM);
+  const uint16_t* Bp = static_cast<const uint16_t*>(p.Bprep) + (j0 / BN) * int64_t(nch) * (SUB * BN);
+  auto issue = [&](int c, int slot) {
+    mbar_expect_tx(&sm.full[slot], U8_CHUNK_A + U8_CHUNK_B);
+    bulk_g2s(&sm.As[slot][0][0], Ap + int64_t(c) * (SUB * BM), U8_CHUNK_A, &sm.full[slot]);
+    bulk_g2s(&sm.Bs[slot][0][0], Bp + int64_t(c) * (SUB * BN), U8_CHUNK_B, &sm.full[slot]);
+  };
   if (t == 0) {
-    const int64_t total = tile_count(p, BM, BN), v0 = int64_t(blockIdx.x) * tpc;
-    int cnt = 0;
-    for (int64_t v = v0; v < v0 + tpc && v < total; v++) {
-      int64_t i0, j0;
-      tile_at(p, v, BM, BN, i0, j0);
-      if (tile_skipped(p, i0, j0, BM, BN)) continue;
-      tiles_i0[cnt] = i0;
-      tiles_j0[cnt] = j0;
-      cnt++;
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&sm.full[s], 1);
+      sm.done[s] = 0;
     }
-    ntiles = cnt;
-    for (int s = 0; s < U8_STAGES; s++) mbar_init(&sm.bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int c = 0; c < STAGES && c < nch; c++) issue(c, c);
   }
   __syncthreads();
-  const int nt = ntiles;
-  if (nt == 0) return;
-  const int64_t total_g = int64_t(nt) * nch;
-  auto issue = [&](int64_t g) {
-    const int tt = int(g / nch);
-    const int64_t c = g - int64_t(tt) * nch;
-    const int slot = int(g % U8_STAGES);
-    mbar_expect_tx(&sm.bar[slot], U8_CHUNK_A + U8_CHUNK_B);
-    bulk_g2s(&sm.As[slot][0][0], p.Aprep + ((tiles_i0[tt] / BM) * nch + c) * (SUB * BM), U8_CHUNK_A, &sm.bar[slot]);
-    bulk_g2s(&sm.Bs[slot][0][0], static_cast<const uint16_t*>(p.Bprep) + ((tiles_j0[tt] / BN) * nch + c) * (SUB * BN),
-             U8_CHUNK_B, &sm.bar[slot]);
-  };
-  if (t == 0)
-    for (int64_t g = 0; g < U8_STAGES && g < total_g; g++) issue(g);
-  const char* C = static_cast<const char*>(p.C);
-  auto prefetch_c = [&](int tt) {
-    const int r = t >> 1;
-    const char* src = C + ((tiles_i0[tt] + r) * p.ldc + tiles_j0[tt]) * int64_t(sizeof(T)) + CB * (t & 1);
-    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r][0]) + CB * (t & 1));
+  const int tx = t & 15, ty = t >> 4, lane = t & 31;
+  {  // own C cells -> smem (cp.async, 4 or 8 bytes per 4-cell segment)
+    const char* C = static_cast<const char*>(p.C);
 #pragma unroll
-    for (int q = 0; q < CB / 16; q++)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+    for (int r = 0; r < 8; r++) {
+      const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const char* src = C + ((i0 + ri) * p.ldc + j0 + 64 * h + 4 * tx) * int64_t(sizeof(T));
+        const uint32_t dst = smem_u32(&sm.Cs[ri][64 * h + 4 * tx]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst), "l"(src), "n"(CW));
+      }
+    }
     asm volatile("cp.async.commit_group;\n" ::);
-  };
-  prefetch_c(0);
+  }
   bool changed = false;
   const int32_t* __restrict__ pb = p.predB;
   int32_t* __restrict__ out = p.idx;
   T* Cw = static_cast<T*>(p.C);
   const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
 
-  for (int tt = 0; tt < nt; tt++) {
-    const int64_t i0 = tiles_i0[tt], j0 = tiles_j0[tt];
-    uint32_t acc[8][4];
-    uint32_t kst[8][4];
+  uint32_t acc[8][4];
+  uint32_t kst[8][4];
 #pragma unroll
-    for (int r = 0; r < 8; r++)
+  for (int r = 0; r < 8; r++)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      acc[r][q] = KINF2;
+      kst[r][q] = 0u;
+    }
+  int slot = 0, wc = 0;
+  uint32_t ph = 0;
+  for (int c = 0; c < nch; c++) {
+    mbar_wait(&sm.full[slot], ph);
+#pragma unroll kU8Unroll
+    for (int kk = 0; kk < SUB; kk++) {
+      const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
+      const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
+      const uint2 b0 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][4 * tx]);
+      const uint2 b1 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][64 + 4 * tx]);
+      const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
+    }
+    __syncwarp();
+    if (lane == 0) {   // count this warp out of the slot; the last one refills it
+      __threadfence_block();
+      if (atomicAdd(&sm.done[slot], 1u) == NT / 32 - 1) {
+        __threadfence_block();
+        sm.done[slot] = 0;
+        if (c + STAGES < nch) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(c + STAGES, slot);
+        }
+      }
+    }
+    if (++slot == STAGES) {
+      slot = 0;
+      ph ^= 1u;
+    }
+    if (c == 0) {   // merge the old C (own cells only: no barrier)
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          uint32_t p0, p1;   // old values of the two column pairs, as key pairs
+          if constexpr (sizeof(T) == 1) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
+            p0 = __byte_perm(w, 0, 0x4140) << TAG;
+            p1 = __byte_perm(w, 0, 0x4342) << TAG;
+          } else {
+            const uint2 w = *reinterpret_cast<const uint2*>(&sm.Cs[ri][64 * h + 4 * tx]);
+            p0 = w.x << TAG;
+            p1 = w.y << TAG;
+          }
+          acc[r][2 * h] = __vminu2(acc[r][2 * h], p0);
+          acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], p1);
+        }
+      }
+    }
+    if (wc == WIN - 1 || c + 1 == nch) {
+      uint32_t any = 0;
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int q = 0; q < 4; q++) any |= acc[r][q];
+      if (__any_sync(0xffffffffu, any & TMASK2)) {
+        const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
+#pragma unroll
+        for (int r = 0; r < 8; r++)
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const uint32_t tg = acc[r][q] & TMASK2;
+            const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
+            kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
+            acc[r][q] -= tg;
+          }
+      }
+    }
+    if (++wc == WIN) wc = 0;
+  }
+  // epilogue
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+    int32_t pv[2][4];
+    uint32_t ks[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+      ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
+      const int64_t j = j0 + 64 * h + 4 * tx;
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        acc[r][q] = KINF2;
-        kst[r][q] = 0u;
+        pv[h][q] = 0;
+        if (out && ks[h][q] != 0u)
+          pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
+                                          : int32_t(p.inner_off + ks[h][q] - 1u);
       }
-    for (int64_t c = 0; c < nch; c++) {
-      const int64_t g = int64_t(tt) * nch + c;
-      const int slot = int(g % U8_STAGES);
-      mbar_wait(&sm.bar[slot], uint32_t((g / U8_STAGES) & 1));
-#pragma unroll kU8Unroll
-      for (int kk = 0; kk < SUB; kk++) {
-        const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
-        const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
-        const uint2 b0 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][4 * tx]);
-        const uint2 b1 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][64 + 4 * tx]);
-        const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
-#pragma unroll
-        for (int r = 0; r < 8; r++)
-#pragma unroll
-          for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
-      }
-      const bool more = c + 1 < nch;
-      const int64_t wc = c % WIN;   // chunk position inside the decode window
-      if (c == 0) {
-        asm volatile("cp.async.wait_all;\n" ::);
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < 8; r++) {
-          const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            uint32_t p0, p1;   // old values of the two column pairs, as key pairs
-            if constexpr (sizeof(T) == 1) {
-              const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
-              p0 = __byte_perm(w, 0, 0x4140) << TAG;
-              p1 = __byte_perm(w, 0, 0x4342) << TAG;
-            } else {
-              const uint2 w = *reinterpret_cast<const uint2*>(&sm.Cs[ri][64 * h + 4 * tx]);
-              p0 = w.x << TAG;
-              p1 = w.y << TAG;
-            }
-            acc[r][2 * h] = __vminu2(acc[r][2 * h], p0);
-            acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], p1);
-          }
-        }
-        __syncthreads();                      // Cs consumed: prefetch the next tile's C
-        if (tt + 1 < nt) prefetch_c(tt + 1);
-      }
-      if (wc == WIN - 1 || !more) {
-        uint32_t any = 0;
-#pragma unroll
-        for (int r = 0; r < 8; r++)
-#pragma unroll
-          for (int q = 0; q < 4; q++) any |= acc[r][q];
-        if (__any_sync(0xffffffffu, any & TMASK2)) {
-          const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
-#pragma unroll
-          for (int r = 0; r < 8; r++)
-#pragma unroll
-            for (int q = 0; q < 4; q++) {
-              const uint32_t tg = acc[r][q] & TMASK2;
-              const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
-              kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
-              acc[r][q] -= tg;
-            }
-        }
-      }
-      __syncthreads();   // every warp is done with this slot
-      if (t == 0 && g + U8_STAGES < total_g) issue(g + U8_STAGES);
     }
-    // epilogue of tile tt (the next tile's first chunks and C are already in flight)
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
-      const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
-      int32_t pv[2][4];
-      uint32_t ks[2][4];
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
-        ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
-        const int64_t j = j0 + 64 * h + 4 * tx;
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          pv[h][q] = 0;
-          if (out && ks[h][q] != 0u)
-            pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
-                                            : int32_t(p.inner_off + ks[h][q] - 1u);
-        }
+    for (int h = 0; h < 2; h++) {
+      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+      if ((k0 | k1) == 0u) continue;
+      changed = true;
+      const int64_t j = j0 + 64 * h + 4 * tx;
+      if constexpr (sizeof(T) == 1) {
+        *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) =
+            __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
+      } else {
+        *reinterpret_cast<uint2*>(Cw + i * p.ldc + j) = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
       }
+      if (!out) continue;
+      if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
+        *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+      } else {
 #pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
-        if ((k0 | k1) == 0u) continue;
-        changed = true;
-        const int64_t j = j0 + 64 * h + 4 * tx;
-        if constexpr (sizeof(T) == 1) {
-          *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) =
-              __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
-        } else {
-          *reinterpret_cast<uint2*>(Cw + i * p.ldc + j) = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
-        }
-        if (!out) continue;
-        if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
-          *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; q++)
-            if (ks[h][q] != 0u) out[i * p.ldi + j + q] = pv[h][q];
-        }
+        for (int q = 0; q < 4; q++)
+          if (ks[h][q] != 0u) out[i * p.ldi + j + q] = pv[h][q];
       }
     }
   }
-  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+  // one flag write per warp that changed (no CTA barrier needed)
+  if (p.status && p.track_changed && __any_sync(0xffffffffu, changed) && lane == 0) p.status->changed = 1;
 }
 
 // panel layout kernels (one CTA per (tile, chunk); thread = one row x 16 k, or one k x 16 columns)
@@ -865,16 +876,7 @@ static int launch_nt(const MinplusArgs& a, cudaStream_t s) {
   const size_t es = sizeof(typename Narrow<S>::T);
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
     return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
-  static int tpc = -1;
-  if (tpc < 0) {
-    const char* e = getenv("APSP_U8_TPC");
-    tpc = e ? atoi(e) : 1;   // >1 delays the lookahead side stream (measured slower)
-    if (tpc < 1) tpc = 1;
-    if (tpc > U8_TPC_MAX) tpc = U8_TPC_MAX;
-  }
-  const dim3 g2 = grid_for(a, BM, BN);
-  const int64_t tiles = int64_t(g2.x) * g2.y;
-  minplus_nt_kernel<S><<<unsigned((tiles + tpc - 1) / tpc), NT, sizeof(SmemNT<S>), s>>>(a, tpc);
+  minplus_nt_kernel<S><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
   return 0;
 }
 
