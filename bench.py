@@ -321,6 +321,15 @@ def bench_single(args):
                 "traffic": None, "launches_per_step": kl, "kernel_share_of_step": (kms / ms_step) if kl else None,
                 "updates_per_step": upd_phase3, "kernel_ms_per_step": kms,
                 "peak_source": "measured issue ceiling of the inner-loop instruction, profiles/r01_microbench_ops.txt"}
+    # DRAM traffic of one phase-3b launch from the committed ncu --set full capture of this
+    # configuration (profiles/ncu_phase3b.json, tools/ncu_summary.py); null for other configs
+    cap = Path(__file__).resolve().parent / "profiles" / "ncu_phase3b.json"
+    if cap.exists() and tier == "u8" and n == 16384 and block == 1024:
+        c = json.loads(cap.read_text())
+        roofline["traffic"] = c["traffic_bytes"]
+        roofline["traffic_launch"] = {"updates": c["updates"], "duration_ms_isolated": c["duration_ms"],
+                                      "achieved_isolated": c["achieved_T"], "frac_isolated": c["frac_of_dpx_ceiling"],
+                                      "source": "profiles/ncu_phase3b.json (ncu --set full, round-7 phase-3b launch)"}
 
     e2e = None
     if not args.no_e2e:
