@@ -13,8 +13,6 @@
 namespace apsp {
 const char* last_error();
 long long launch_count();
-int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out,
-                         int64_t ldo, cudaStream_t s);
 }
 
 using namespace apsp;
@@ -536,6 +534,13 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   }
   std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, true, n);
   if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
+  // no padding: solve straight into the caller's pred matrix (saves an N^2 int32 copy)
+  int32_t* Pw = P;
+  int64_t ldpw = N;
+  if (pred && N == n && ldp >= n && ldp % 4 == 0 && (reinterpret_cast<uintptr_t>(pred) & 15) == 0) {
+    Pw = pred;
+    ldpw = ldp;
+  }
   int launches = 2, used = -1, tried = 0;
   for (int tier : tiers) {
     const int store = tier_store(tier);
@@ -543,11 +548,11 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     if (store == STORE_I64 && dtype != APSP_DTYPE_I64) return set_error(APSP_EINVAL, "int64 tier needs int64 input");
     tried |= 1 << tier;
     APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
-    rc = launch_to_store(dtype, dist, ld, n, store, D, N, N, P, N, 1, s);
+    rc = launch_to_store(dtype, dist, ld, n, store, D, N, N, Pw, ldpw, 1, s);
     if (!rc) {
       FwCtx c;
       c.store = store; c.es = store_elem_size(store);
-      c.D = D; c.ld = N; c.P = P; c.ldp = N; c.m = N; c.b = b; c.mode = IDX_PRED; c.via_off = 0;
+      c.D = D; c.ld = N; c.P = Pw; c.ldp = ldpw; c.m = N; c.b = b; c.mode = IDX_PRED; c.via_off = 0;
       c.st = &hdr_dev->status;
       c.side = getenv("APSP_NO_LOOKAHEAD") ? nullptr : side_stream();
       fw_carve(c, scratch, N);
@@ -570,9 +575,12 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     return set_error(APSP_ERANGE, "no value tier could represent the result");
   }
   rc = launch_from_store(tier_store(used), D, N, n, n, dtype, dist, ld, s);
-  if (!rc && pred) rc = launch_copy_idx(P, N, n, n, APSP_DTYPE_I32, pred, ldp, s);
+  if (!rc && pred && Pw != pred) {
+    rc = launch_copy_idx(P, N, n, n, APSP_DTYPE_I32, pred, ldp, s);
+    launches++;
+  }
   if (rc) return rc;
-  launches += 2;
+  launches++;
   const double ms = tm.stop();
   if (info) {
     info->block = b;
@@ -1025,65 +1033,6 @@ int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
 
 }  // namespace
 
-// ---- conversion of a rectangular operand (no padding); h == nullptr fills Infinity --------
-namespace apsp {
-template <int D> struct ApiT;
-template <> struct ApiT<APSP_DTYPE_I32> { using T = int32_t; };
-template <> struct ApiT<APSP_DTYPE_F32> { using T = float; };
-template <> struct ApiT<APSP_DTYPE_I64> { using T = int64_t; };
-
-template <int D, int S>
-__global__ void to_store_rect_kernel(const typename ApiT<D>::T* h, int64_t ldh, int64_t rows, int64_t cols,
-                                     typename StoreT<S>::T* out, int64_t ldo) {
-  using TI = typename ApiT<D>::T;
-  using T = typename StoreT<S>::T;
-  const int64_t total = rows * cols;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / cols, j = e - i * cols;
-    T o = store_inf<S>();
-    if (h) {
-      const TI v = h[i * ldh + j];
-      bool fin;
-      if constexpr (D == APSP_DTYPE_I32) fin = v != INF32;
-      else if constexpr (D == APSP_DTYPE_I64) fin = v != INF_RAW;
-      else fin = !isinf(v);
-      if (fin) o = T(v);
-    }
-    out[i * ldo + j] = o;
-  }
-}
-
-template <int D>
-static int rect_d(const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out, int64_t ldo,
-                  cudaStream_t s) {
-  using TI = typename ApiT<D>::T;
-  int64_t g = (rows * cols + 255) / 256;
-  g = std::min<int64_t>(std::max<int64_t>(g, 1), 148 * 16);
-  const TI* hh = static_cast<const TI*>(h);
-  switch (store) {
-    case STORE_U8: to_store_rect_kernel<D, STORE_U8><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (uint8_t*)out, ldo); break;
-    case STORE_W32: to_store_rect_kernel<D, STORE_W32><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (int32_t*)out, ldo); break;
-    case STORE_I32: to_store_rect_kernel<D, STORE_I32><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (int32_t*)out, ldo); break;
-    case STORE_F32: to_store_rect_kernel<D, STORE_F32><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (float*)out, ldo); break;
-    case STORE_I64: to_store_rect_kernel<D, STORE_I64><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (int64_t*)out, ldo); break;
-    case STORE_U16: to_store_rect_kernel<D, STORE_U16><<<unsigned(g), 256, 0, s>>>(hh, ldh, rows, cols, (uint16_t*)out, ldo); break;
-    default: return set_error(APSP_EINVAL, "unknown store %d", store);
-  }
-  APSP_CUDA_TRY(cudaGetLastError());
-  count_launches(1);
-  return 0;
-}
-
-int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out,
-                         int64_t ldo, cudaStream_t s) {
-  switch (in_dtype) {
-    case APSP_DTYPE_I32: return rect_d<APSP_DTYPE_I32>(h, ldh, rows, cols, store, out, ldo, s);
-    case APSP_DTYPE_F32: return rect_d<APSP_DTYPE_F32>(h, ldh, rows, cols, store, out, ldo, s);
-    case APSP_DTYPE_I64: return rect_d<APSP_DTYPE_I64>(h, ldh, rows, cols, store, out, ldo, s);
-  }
-  return set_error(APSP_EINVAL, "unknown dtype %d", in_dtype);
-}
-}  // namespace apsp
 
 // ---- row-band shards of a blocked FW (multi-GPU building blocks) ---------------------------
 //

@@ -1,6 +1,7 @@
 // Input scan (K7), API dtype <-> store conversion with padding and pred initialisation,
 // result certificate (max finite), index copies and the minplus_product witness clear.
-// All are HBM-bound elementwise kernels: grid-stride, 16B-friendly row-major sweeps.
+// All are HBM-bound elementwise kernels: 2D grid-stride sweeps (rows over blockIdx.y, columns
+// over threads) -- no per-element 64-bit index division, coalesced along rows.
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -26,6 +27,22 @@ template <> struct Api<API_I32> { using T = int32_t; __device__ static bool fin(
 template <> struct Api<API_F32> { using T = float;   __device__ static bool fin(T v) { return !isinf(v) || v < 0; } };
 template <> struct Api<API_I64> { using T = int64_t; __device__ static bool fin(T v) { return v != INF_RAW; } };
 
+// rows over blockIdx.y (grid-stride), columns over blockIdx.x * blockDim.x + threadIdx.x
+#define FOR_2D(i, j, rows, cols)                                                                         \
+  for (int64_t i = blockIdx.y; i < (rows); i += gridDim.y)                                               \
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < (cols); j += int64_t(gridDim.x) * blockDim.x)
+
+static dim3 grid_2d(int64_t rows, int64_t cols) {
+  int64_t gx = (cols + 255) / 256;
+  if (gx > 16) gx = 16;
+  if (gx < 1) gx = 1;
+  int64_t gy = (148 * 16 + gx - 1) / gx;
+  if (gy > rows) gy = rows;
+  if (gy > 65535) gy = 65535;
+  if (gy < 1) gy = 1;
+  return dim3(unsigned(gx), unsigned(gy));
+}
+
 __device__ __forceinline__ void warp_or(int32_t* dst, bool v) {
   if (__any_sync(0xffffffffu, v) && (threadIdx.x & 31) == 0) atomicOr(dst, 1);
 }
@@ -38,9 +55,7 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
   unsigned long long edges = 0;
   long long mx = -1;
   float mxf = -1.f;
-  const int64_t total = rows * cols;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / cols, j = e - i * cols;
+  FOR_2D(i, j, rows, cols) {
     const T v = h[i * ld + j];
     const bool on_diag = diag_off >= 0 && j == i + diag_off;
     if (on_diag && v != T(0)) diag = true;
@@ -75,18 +90,11 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
   }
 }
 
-static unsigned grid_for(int64_t total) {
-  int64_t g = (total + 255) / 256;
-  if (g > 148 * 16) g = 148 * 16;
-  if (g < 1) g = 1;
-  return unsigned(g);
-}
-
 int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
                 ScanResult* out_dev, cudaStream_t s) {
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
   // max fields start at 0 after memset; negative sentinel not needed (values are >= 0)
-  const unsigned g = grid_for(rows * cols);
+  const dim3 g = grid_2d(rows, cols);
   switch (in_dtype) {
     case API_I32: scan_kernel<API_I32><<<g, 256, 0, s>>>((const int32_t*)h, ld, rows, cols, diag_off, out_dev); break;
     case API_F32: scan_kernel<API_F32><<<g, 256, 0, s>>>((const float*)h, ld, rows, cols, diag_off, out_dev); break;
@@ -105,9 +113,8 @@ __global__ void to_store_kernel(const typename Api<D>::T* h, int64_t ldh, int64_
                                 int64_t ld, int64_t N, int32_t* P, int64_t ldp, int pred_init, int64_t row0,
                                 int64_t R) {
   using T = typename StoreT<S>::T;
-  const int64_t total = R * N;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t il = e / N, j = e - il * N, i = row0 + il;
+  FOR_2D(il, j, R, N) {
+    const int64_t i = row0 + il;
     T o;
     bool fin;
     if (i < n && j < n) {
@@ -127,7 +134,7 @@ template <int D>
 static int to_store_d(const void* h, int64_t ldh, int64_t n, int store, void* Dp, int64_t ld, int64_t N, int32_t* P,
                       int64_t ldp, int pred_init, int64_t row0, int64_t R, cudaStream_t s) {
   using TI = typename Api<D>::T;
-  const unsigned g = grid_for(R * N);
+  const dim3 g = grid_2d(R, N);
   const TI* hh = static_cast<const TI*>(h);
   switch (store) {
     case STORE_U8: to_store_kernel<D, STORE_U8><<<g, 256, 0, s>>>(hh, ldh, n, (uint8_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
@@ -158,15 +165,58 @@ int launch_to_store(int in_dtype, const void* h, int64_t ldh, int64_t n, int sto
   return launch_to_store_rows(in_dtype, h, ldh, n, store, D, ld, N, P, ldp, pred_init, 0, N, s);
 }
 
+// ---- conversion of a rectangular operand (no padding); h == nullptr fills Infinity -------
+template <int D, int S>
+__global__ void to_store_rect_kernel(const typename Api<D>::T* h, int64_t ldh, int64_t rows, int64_t cols,
+                                     typename StoreT<S>::T* out, int64_t ldo) {
+  using T = typename StoreT<S>::T;
+  FOR_2D(i, j, rows, cols) {
+    T o = store_inf<S>();
+    if (h) {
+      const typename Api<D>::T v = h[i * ldh + j];
+      if (Api<D>::fin(v)) o = T(v);
+    }
+    out[i * ldo + j] = o;
+  }
+}
+
+template <int D>
+static int rect_d(const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out, int64_t ldo,
+                  cudaStream_t s) {
+  using TI = typename Api<D>::T;
+  const dim3 g = grid_2d(rows, cols);
+  const TI* hh = static_cast<const TI*>(h);
+  switch (store) {
+    case STORE_U8: to_store_rect_kernel<D, STORE_U8><<<g, 256, 0, s>>>(hh, ldh, rows, cols, (uint8_t*)out, ldo); break;
+    case STORE_W32: to_store_rect_kernel<D, STORE_W32><<<g, 256, 0, s>>>(hh, ldh, rows, cols, (int32_t*)out, ldo); break;
+    case STORE_I32: to_store_rect_kernel<D, STORE_I32><<<g, 256, 0, s>>>(hh, ldh, rows, cols, (int32_t*)out, ldo); break;
+    case STORE_F32: to_store_rect_kernel<D, STORE_F32><<<g, 256, 0, s>>>(hh, ldh, rows, cols, (float*)out, ldo); break;
+    case STORE_I64: to_store_rect_kernel<D, STORE_I64><<<g, 256, 0, s>>>(hh, ldh, rows, cols, (int64_t*)out, ldo); break;
+    case STORE_U16: to_store_rect_kernel<D, STORE_U16><<<g, 256, 0, s>>>(hh, ldh, rows, cols, (uint16_t*)out, ldo); break;
+    default: return set_error(2, "unknown store %d", store);
+  }
+  APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
+  return 0;
+}
+
+int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out,
+                         int64_t ldo, cudaStream_t s) {
+  switch (in_dtype) {
+    case API_I32: return rect_d<API_I32>(h, ldh, rows, cols, store, out, ldo, s);
+    case API_F32: return rect_d<API_F32>(h, ldh, rows, cols, store, out, ldo, s);
+    case API_I64: return rect_d<API_I64>(h, ldh, rows, cols, store, out, ldo, s);
+  }
+  return set_error(2, "unknown dtype %d", in_dtype);
+}
+
 // ---- conversion back -----------------------------------------------------------------
 template <int S, int D>
 __global__ void from_store_kernel(const typename StoreT<S>::T* in, int64_t ld, int64_t rows, int64_t cols,
                                   typename Api<D>::T* out, int64_t ldo) {
   using TO = typename Api<D>::T;
-  const int64_t total = rows * cols;
   const typename StoreT<S>::T inf = store_inf<S>();
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / cols, j = e - i * cols;
+  FOR_2D(i, j, rows, cols) {
     const auto v = in[i * ld + j];
     TO o;
     if constexpr (S == STORE_F32) {
@@ -188,7 +238,7 @@ template <int S>
 static int from_store_s(const void* in, int64_t ld, int64_t rows, int64_t cols, int out_dtype, void* out, int64_t ldo,
                         cudaStream_t s) {
   using TI = typename StoreT<S>::T;
-  const unsigned g = grid_for(rows * cols);
+  const dim3 g = grid_2d(rows, cols);
   const TI* ii = static_cast<const TI*>(in);
   switch (out_dtype) {
     case API_I32: from_store_kernel<S, API_I32><<<g, 256, 0, s>>>(ii, ld, rows, cols, (int32_t*)out, ldo); break;
@@ -217,16 +267,12 @@ int launch_from_store(int store, const void* D, int64_t ld, int64_t rows, int64_
 // ---- index copies ----------------------------------------------------------------------
 template <typename TO>
 __global__ void copy_idx_kernel(const int32_t* P, int64_t ldp, int64_t rows, int64_t cols, TO* out, int64_t ldo) {
-  const int64_t total = rows * cols;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / cols, j = e - i * cols;
-    out[i * ldo + j] = TO(P[i * ldp + j]);
-  }
+  FOR_2D(i, j, rows, cols) out[i * ldo + j] = TO(P[i * ldp + j]);
 }
 
 int launch_copy_idx(const int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int out_dtype, void* out, int64_t ldo,
                     cudaStream_t s) {
-  const unsigned g = grid_for(rows * cols);
+  const dim3 g = grid_2d(rows, cols);
   if (out_dtype == API_I64) copy_idx_kernel<int64_t><<<g, 256, 0, s>>>(P, ldp, rows, cols, (int64_t*)out, ldo);
   else copy_idx_kernel<int32_t><<<g, 256, 0, s>>>(P, ldp, rows, cols, (int32_t*)out, ldo);
   APSP_CUDA_TRY(cudaGetLastError());
@@ -235,15 +281,11 @@ int launch_copy_idx(const int32_t* P, int64_t ldp, int64_t rows, int64_t cols, i
 }
 
 __global__ void fill_idx_kernel(int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int32_t v) {
-  const int64_t total = rows * cols;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / cols, j = e - i * cols;
-    P[i * ldp + j] = v;
-  }
+  FOR_2D(i, j, rows, cols) P[i * ldp + j] = v;
 }
 
 int launch_fill_idx(int32_t* P, int64_t ldp, int64_t rows, int64_t cols, int32_t v, cudaStream_t s) {
-  fill_idx_kernel<<<grid_for(rows * cols), 256, 0, s>>>(P, ldp, rows, cols, v);
+  fill_idx_kernel<<<grid_2d(rows, cols), 256, 0, s>>>(P, ldp, rows, cols, v);
   APSP_CUDA_TRY(cudaGetLastError());
   count_launches(1);
   return 0;
@@ -262,12 +304,10 @@ int launch_copy_block(int store, const void* src, int64_t lds, void* dst, int64_
 template <int S>
 __global__ void max_finite_kernel(const typename StoreT<S>::T* D, int64_t ld, int64_t rows, int64_t cols,
                                   ScanResult* out) {
-  const int64_t total = rows * cols;
   const auto inf = store_inf<S>();
   long long mx = -1;
   float mxf = -1.f;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / cols, j = e - i * cols;
+  FOR_2D(i, j, rows, cols) {
     const auto v = D[i * ld + j];
     if (v == inf) continue;
     if constexpr (S == STORE_F32) mxf = fmaxf(mxf, v);
@@ -286,7 +326,7 @@ __global__ void max_finite_kernel(const typename StoreT<S>::T* D, int64_t ld, in
 int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_t cols, ScanResult* out_dev,
                       cudaStream_t s) {
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
-  const unsigned g = grid_for(rows * cols);
+  const dim3 g = grid_2d(rows, cols);
   switch (store) {
     case STORE_U8: max_finite_kernel<STORE_U8><<<g, 256, 0, s>>>((const uint8_t*)D, ld, rows, cols, out_dev); break;
     case STORE_W32: max_finite_kernel<STORE_W32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev); break;
@@ -309,9 +349,7 @@ __global__ void witness_clear_kernel(const typename StoreT<S>::T* X, int64_t ldx
                                      int64_t inner_off, int64_t col_off) {
   using A = typename StoreT<S>::A;
   const auto inf = store_inf<S>();
-  const int64_t total = n1 * n3;
-  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = e / n3, j = e - i * n3;
+  FOR_2D(i, j, n1, n3) {
     const auto best = Dp[i * ldd + j];
     if (best == inf) continue;
     const int64_t ti = i + row_off - inner_off;
@@ -330,7 +368,7 @@ __global__ void witness_clear_kernel(const typename StoreT<S>::T* X, int64_t ldx
 int launch_witness_clear(int store, const void* X, int64_t ldx, const void* Y, int64_t ldy, const void* Dp,
                          int64_t ldd, int32_t* via, int64_t ldv, int64_t n1, int64_t n2, int64_t n3, int64_t row_off,
                          int64_t inner_off, int64_t col_off, cudaStream_t s) {
-  const unsigned g = grid_for(n1 * n3);
+  const dim3 g = grid_2d(n1, n3);
 #define WC(S, T)                                                                                              \
   witness_clear_kernel<S><<<g, 256, 0, s>>>((const T*)X, ldx, (const T*)Y, ldy, (const T*)Dp, ldd, via, ldv, n1, \
                                             n2, n3, row_off, inner_off, col_off)

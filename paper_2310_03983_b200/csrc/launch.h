@@ -98,6 +98,9 @@ int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t c
 int launch_to_store(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D,
                     int64_t ld, int64_t N, int32_t* P, int64_t ldp, int pred_init, cudaStream_t s);
 // the same for rows [row0, row0 + R) of the padded matrix (h holds those rows of the input)
+// rectangular operand (no padding, no pred); h == nullptr fills Infinity
+int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows, int64_t cols, int store, void* out,
+                         int64_t ldo, cudaStream_t s);
 int launch_to_store_rows(int in_dtype, const void* h, int64_t ldh, int64_t n, int store, void* D, int64_t ld,
                          int64_t N, int32_t* P, int64_t ldp, int pred_init, int64_t row0, int64_t R, cudaStream_t s);
 int launch_from_store(int store, const void* D, int64_t ld, int64_t rows, int64_t cols,
