@@ -425,11 +425,12 @@ cudaStream_t side_stream() {
 // by fw_carve (fw_scratch_bytes(m, b, es) bytes) or, if null, only a pred snapshot
 int fw_blocked_view(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t m, int b, int mode,
                     int64_t via_off, Status* st, cudaStream_t s, int* launches, int32_t* predsnap,
-                    char* scratch = nullptr) {
+                    char* scratch = nullptr, cudaStream_t side = nullptr) {
   FwCtx c;
   c.store = store; c.es = store_elem_size(store);
   c.D = static_cast<char*>(D); c.ld = ld; c.P = P; c.ldp = ldp;
   c.m = m; c.b = b; c.mode = mode; c.via_off = via_off; c.st = st;
+  c.side = side;
   if (scratch) fw_carve(c, scratch, m);
   else c.predsnap = predsnap;
   const int rc = fw_run(c, s);
@@ -706,8 +707,9 @@ struct RK {
 
   int leaf(int64_t lo, int64_t m) {
     if (aligned && m > 128) {
+      // leaves run the lookahead schedule too (phases 1-2 of K+1 beside phase 3 of K)
       return fw_blocked_view(store, at(lo, lo), ld, pat(lo, lo), ld, m, DEFAULT_BLOCK, mode, lo, st, s, &launches,
-                             sP, leafws);
+                             sP, leafws, getenv("APSP_NO_LOOKAHEAD") ? nullptr : side_stream());
     }
     launches += int(m > 128 ? m : 1);
     return launch_block_close(store, D, ld, lo, m, P, ld, mode, lo, st, s);
@@ -1198,7 +1200,7 @@ int rk_shard_leaf_impl(int tier, void* Dv, int64_t ld, int32_t* P, int64_t ldp, 
   int launches = 0;
   if (m > TILE_ALIGN)
     return fw_blocked_view(store, D + (lo * ld + lo) * es, ld, P + lo * ldp + lo, ldp, m, DEFAULT_BLOCK, IDX_PRED, lo,
-                           st, s, &launches, nullptr, leafws);
+                           st, s, &launches, nullptr, leafws, getenv("APSP_NO_LOOKAHEAD") ? nullptr : side_stream());
   return launch_block_close(store, D, ld, lo, m, P, ldp, IDX_PRED, lo, st, s);
 }
 
