@@ -178,8 +178,8 @@ __global__ void __launch_bounds__(512) block_close_kernel(typename StoreT<S>::T*
 // 512 threads: thread (ty, tx) owns rows ty + 16a (a < 8) x column pairs 2tx + 64c (c < 2).
 // ------------------------------------------------------------------------------------
 struct CloseU8Smem {
-  uint32_t rowk[2][64];       // row k as tag-free key pairs
-  uint32_t colk[2][MAXB];     // column k as replicated tag-free keys
+  uint32_t rowk[2][64];       // row k as tag-free key pairs, [2 * tx + c]: one 8-byte read per lane
+  uint32_t colk[2][MAXB];     // column k as replicated tag-free keys, [8 * ty + a]: 2 x 16-byte reads
   int32_t P[MAXB][MAXB];      // pred resolution
   uint8_t K[MAXB][MAXB];      // 1-based last improving k (0 = none)
 };
@@ -211,21 +211,23 @@ __global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t
 #define CU8_PUBLISH(KK, BUF)                                                              \
   do {                                                                                    \
     const int pk_ = (KK), pb_ = (BUF);                                                    \
-    if (ty == (pk_ & 15)) {                                                               \
+    if (ty == (pk_ & 15)) {   /* one warp: row pk_ = register row pk_ >> 4 */            \
       const int sa_ = pk_ >> 4;                                                           \
-      _Pragma("unroll") for (int c = 0; c < 2; c++) {                                     \
-        uint32_t r_ = acc[0][c];                                                          \
-        _Pragma("unroll") for (int a = 1; a < 8; a++) r_ = (a == sa_) ? acc[a][c] : r_;  \
-        sm.rowk[pb_][tx + 32 * c] = u8c_strip(r_);                                        \
+      uint32_t r0_ = acc[0][0], r1_ = acc[0][1];                                          \
+      _Pragma("unroll") for (int a = 1; a < 8; a++) {                                     \
+        r0_ = (a == sa_) ? acc[a][0] : r0_;                                               \
+        r1_ = (a == sa_) ? acc[a][1] : r1_;                                               \
       }                                                                                   \
+      *reinterpret_cast<uint2*>(&sm.rowk[pb_][2 * tx]) = make_uint2(u8c_strip(r0_), u8c_strip(r1_)); \
     }                                                                                     \
-    if (tx == ((pk_ & 63) >> 1)) {                                                        \
-      const int sc_ = pk_ >> 6, sh_ = pk_ & 1;                                            \
-      _Pragma("unroll") for (int a = 0; a < 8; a++) {                                     \
-        const uint32_t x_ = sc_ ? acc[a][1] : acc[a][0];                                  \
-        const uint32_t h_ = (sh_ ? (x_ >> 16) : x_) & 0xFF80u;                            \
-        sm.colk[pb_][ty + 16 * a] = h_ * 0x00010001u;                                     \
-      }                                                                                   \
+    if (tx == ((pk_ & 63) >> 1)) {   /* one lane per warp: column pk_, 8 rows */          \
+      const int sc_ = pk_ >> 6;                                                           \
+      const uint32_t sel_ = (pk_ & 1) ? 0x3232u : 0x1010u;   /* replicate the half */     \
+      uint32_t v_[8];                                                                     \
+      _Pragma("unroll") for (int a = 0; a < 8; a++)                                       \
+        v_[a] = __byte_perm(sc_ ? acc[a][1] : acc[a][0], 0, sel_) & 0xFF80FF80u;          \
+      *reinterpret_cast<uint4*>(&sm.colk[pb_][8 * ty]) = make_uint4(v_[0], v_[1], v_[2], v_[3]); \
+      *reinterpret_cast<uint4*>(&sm.colk[pb_][8 * ty + 4]) = make_uint4(v_[4], v_[5], v_[6], v_[7]); \
     }                                                                                     \
   } while (0)
   CU8_PUBLISH(0, 0);
@@ -234,10 +236,15 @@ __global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t
     const int b = k & 1;
     const uint32_t tag2 = uint32_t((k & 63) + 1) * 0x00010001u;
     uint32_t dkj[2], dik[8];
-#pragma unroll
-    for (int c = 0; c < 2; c++) dkj[c] = sm.rowk[b][tx + 32 * c] + tag2;
-#pragma unroll
-    for (int a = 0; a < 8; a++) dik[a] = sm.colk[b][ty + 16 * a];
+    {
+      const uint2 r = *reinterpret_cast<const uint2*>(&sm.rowk[b][2 * tx]);
+      dkj[0] = r.x + tag2;
+      dkj[1] = r.y + tag2;
+      const uint4 c0 = *reinterpret_cast<const uint4*>(&sm.colk[b][8 * ty]);
+      const uint4 c1 = *reinterpret_cast<const uint4*>(&sm.colk[b][8 * ty + 4]);
+      dik[0] = c0.x; dik[1] = c0.y; dik[2] = c0.z; dik[3] = c0.w;
+      dik[4] = c1.x; dik[5] = c1.y; dik[6] = c1.z; dik[7] = c1.w;
+    }
 #pragma unroll
     for (int a = 0; a < 8; a++)
 #pragma unroll

@@ -69,7 +69,7 @@ def _single(h, thr):
     return rs.state.D.numpy()[:n, :n], rs.state.P.numpy()[:n, :n]
 
 
-@pytest.mark.parametrize("n,thr,density", [(300, 128, 0.03), (200, 100, 0.1), (520, 128, 0.01)])
+@pytest.mark.parametrize("n,thr,density", [(300, 128, 0.03), (200, 100, 0.1), (390, 128, 0.01)])
 def test_two_ranks_replicas_match_one_rank_and_oracle(n, thr, density):
     from oracle import oracle as orc
 
