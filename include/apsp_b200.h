@@ -183,6 +183,15 @@ int apsp_rk_shard_product(int tier, const void* A, int64_t lda, const void* B, i
                           int32_t* idx, int64_t ldi, const int32_t* pred_b, int64_t ldpb, int64_t m, int64_t n,
                           int64_t k, int64_t inner_off, int64_t N, int thr, void* scratch, size_t scratch_bytes,
                           void* stream);
+/* Fused exchange: the same product, whose epilogue also stores every improved C / pred segment
+ * at the same position of npeers (<= 7) peer replicas -- address + peer_dc[r] / peer_di[r]
+ * bytes, peer memory mapped into this process (CUDA IPC over NVLink) -- so the band reaches every
+ * GPU while the other tiles still compute; the caller then only needs a barrier instead of an
+ * all-gather.  u8 / u16 / w32 tiers (bulk-staged tiles) only. */
+int apsp_rk_shard_product_fused(int tier, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                                int32_t* idx, int64_t ldi, const int32_t* pred_b, int64_t ldpb, int64_t m, int64_t n,
+                                int64_t k, int64_t inner_off, int64_t N, int thr, int npeers, const int64_t* peer_dc,
+                                const int64_t* peer_di, void* scratch, size_t scratch_bytes, void* stream);
 
 /* ---- host-side matrix wire format of the reference (textio.py:70-119), multi-threaded ----------
  * apsp_format_matrix_i64: writes "n\n" + n rows of n fields (integer or INF) into out; returns

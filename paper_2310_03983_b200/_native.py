@@ -56,6 +56,7 @@ EXPORTED_SYMBOLS = (
     "apsp_rk_shard_scratch_bytes",
     "apsp_rk_shard_leaf",
     "apsp_rk_shard_product",
+    "apsp_rk_shard_product_fused",
     "apsp_format_matrix_i64",
     "apsp_parse_matrix_i64",
 )
@@ -139,6 +140,8 @@ _SIGNATURES = {
     "apsp_rk_shard_leaf": (_i32, [_i32, _vp, _i64, _vp, _i64, _i64, _i64, _i32, _vp, _sz, _vp]),
     "apsp_rk_shard_product": (_i32, [_i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64,
                                      _i64, _i64, _i64, _i32, _vp, _sz, _vp]),
+    "apsp_rk_shard_product_fused": (_i32, [_i32, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64,
+                                           _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
     "apsp_format_matrix_i64": (_i64, [_vp, _i64, _vp, _i64]),
     "apsp_parse_matrix_i64": (_i64, [_vp, _i64, _i64, _vp, ctypes.POINTER(ctypes.c_int64)]),
     "apsp_shard_finish": (_i32, [_i32, _i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,

@@ -1207,7 +1207,8 @@ int rk_shard_leaf_impl(int tier, void* Dv, int64_t ld, int32_t* P, int64_t ldp, 
 int rk_shard_product_impl(int tier, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                           int32_t* idx, int64_t ldi, const int32_t* predB, int64_t ldpb, int64_t m, int64_t n,
                           int64_t k, int64_t inner_off, int64_t N, int thr, void* scratch, size_t scratch_bytes,
-                          cudaStream_t s) {
+                          cudaStream_t s, int npeers = 0, const int64_t* peer_dc = nullptr,
+                          const int64_t* peer_di = nullptr) {
   const int store = tier_store(tier);
   if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
   if (m <= 0 || n <= 0 || k <= 0) return 0;
@@ -1222,6 +1223,12 @@ int rk_shard_product_impl(int tier, const void* A, int64_t lda, const void* B, i
   a.inner_off = inner_off;
   a.mode = IDX_PRED;
   a.status = static_cast<Status*>(scratch);
+  if (npeers < 0 || npeers > MAX_PEERS) return set_error(APSP_EINVAL, "npeers %d outside [0, %d]", npeers, MAX_PEERS);
+  a.npeers = npeers;
+  for (int r = 0; r < npeers; r++) {
+    a.peer_dC[r] = peer_dc[r];
+    a.peer_dI[r] = peer_di[r];
+  }
   if (bulk_store(store) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {   // as RK::mp
     int rc = launch_prep_bulk(store, A, lda, B, ldb, m, n, k, prep_a(prep), prep_b(prep, m, k), s);
     if (rc) return rc;
@@ -1306,6 +1313,14 @@ int apsp_shard_finish(int tier, int dtype, int64_t rows, int64_t n, const void* 
 }
 
 size_t apsp_rk_shard_scratch_bytes(int64_t N, int thr) { return rk_shard_scratch_bytes(N, thr); }
+
+int apsp_rk_shard_product_fused(int tier, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
+                                int32_t* idx, int64_t ldi, const int32_t* pred_b, int64_t ldpb, int64_t m, int64_t n,
+                                int64_t k, int64_t inner_off, int64_t N, int thr, int npeers, const int64_t* peer_dc,
+                                const int64_t* peer_di, void* scratch, size_t scratch_bytes, void* stream) {
+  return rk_shard_product_impl(tier, A, lda, B, ldb, C, ldc, idx, ldi, pred_b, ldpb, m, n, k, inner_off, N, thr,
+                               scratch, scratch_bytes, (cudaStream_t)stream, npeers, peer_dc, peer_di);
+}
 
 int apsp_rk_shard_leaf(int tier, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lo, int64_t m, int thr,
                        void* scratch, size_t scratch_bytes, void* stream) {

@@ -11,6 +11,8 @@ namespace apsp {
 // (value, smallest k) argmin, written to idx on improvement only.  Covers FW phase 3
 // (skip_row/col_tile = the pivot block) and every R-Kleene block product
 // (solvers.py:250-286; minplus.py:114-133).
+constexpr int MAX_PEERS = 7;      // 8 GPUs per NVSwitch node
+
 struct MinplusArgs {
   const void* A; int64_t lda;     // m x k
   const void* B; int64_t ldb;     // k x n
@@ -30,6 +32,13 @@ struct MinplusArgs {
   // null = off.  Bprep is uint16 keys for u8/u16 and uint32 keys for w32.
   const uint32_t* Aprep;          // [m/128][k/32][32][128] keys (u8/u16: replicated into both halves)
   const void* Bprep;              // [n/128][k/32][32][128] tagged keys
+  // Fused exchange (bulk-staged kernels only): every improved C / idx segment is also stored at
+  // the same position of up to MAX_PEERS peer replicas -- address + peer_dC[r] / peer_dI[r]
+  // bytes (peer memory mapped over NVLink), so the product's output reaches every GPU while the
+  // remaining tiles compute.
+  int npeers;
+  int64_t peer_dC[MAX_PEERS];
+  int64_t peer_dI[MAX_PEERS];
 };
 
 // Lay the u8 operand panels out in the tile kernel's shared-memory format, once per product:

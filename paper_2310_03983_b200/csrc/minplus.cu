@@ -403,7 +403,7 @@ __device__ __forceinline__ void tile_at(const MinplusArgs& p, int64_t v, int bm,
 // it, and the LAST warp out refills the slot with chunk c + STAGES -- no warp ever waits for
 // another, only for data.  Each thread prefetches exactly its own 8 x 8 C cells (cp.async),
 // so the merge after chunk 0 needs no barrier either.
-template <int S>
+template <int S, bool PEERS>
 __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   using NR = Narrow<S>;
   using T = typename NR::T;
@@ -566,18 +566,38 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
       changed = true;
       const int64_t j = j0 + 64 * h + 4 * tx;
       if constexpr (sizeof(T) == 1) {
-        *reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j) =
-            __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
+        const uint32_t w = __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j);
+        *dst = w;
+        if constexpr (PEERS)
+          for (int pr = 0; pr < p.npeers; pr++)
+            *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
       } else {
-        *reinterpret_cast<uint2*>(Cw + i * p.ldc + j) = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
+        const uint2 w = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
+        uint2* dst = reinterpret_cast<uint2*>(Cw + i * p.ldc + j);
+        *dst = w;
+        if constexpr (PEERS)
+          for (int pr = 0; pr < p.npeers; pr++)
+            *reinterpret_cast<uint2*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
       }
       if (!out) continue;
       if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
-        *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+        const int4 w = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+        int4* dst = reinterpret_cast<int4*>(out + i * p.ldi + j);
+        *dst = w;
+        if constexpr (PEERS)
+          for (int pr = 0; pr < p.npeers; pr++)
+            *reinterpret_cast<int4*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = w;
       } else {
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          if (ks[h][q] != 0u) out[i * p.ldi + j + q] = pv[h][q];
+          if (ks[h][q] != 0u) {
+            int32_t* dst = out + i * p.ldi + j + q;
+            *dst = pv[h][q];
+            if constexpr (PEERS)
+              for (int pr = 0; pr < p.npeers; pr++)
+                *reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = pv[h][q];
+          }
       }
     }
   }
@@ -771,16 +791,28 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
       if ((kst[r][2 * h] | kst[r][2 * h + 1]) == 0u) continue;
       changed = true;
       const int64_t j = j0 + 64 * h + 4 * tx;
-      *reinterpret_cast<int4*>(Cw + i * p.ldc + j) =
-          make_int4(int32_t(acc[r][4 * h] >> W32_TAG), int32_t(acc[r][4 * h + 1] >> W32_TAG),
-                    int32_t(acc[r][4 * h + 2] >> W32_TAG), int32_t(acc[r][4 * h + 3] >> W32_TAG));
+      const int4 wv = make_int4(int32_t(acc[r][4 * h] >> W32_TAG), int32_t(acc[r][4 * h + 1] >> W32_TAG),
+                                int32_t(acc[r][4 * h + 2] >> W32_TAG), int32_t(acc[r][4 * h + 3] >> W32_TAG));
+      int4* dstv = reinterpret_cast<int4*>(Cw + i * p.ldc + j);
+      *dstv = wv;
+      for (int pr = 0; pr < p.npeers; pr++)
+        *reinterpret_cast<int4*>(reinterpret_cast<char*>(dstv) + p.peer_dC[pr]) = wv;
       if (!out) continue;
       if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
-        *reinterpret_cast<int4*>(out + i * p.ldi + j) = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+        const int4 w = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
+        int4* dst = reinterpret_cast<int4*>(out + i * p.ldi + j);
+        *dst = w;
+        for (int pr = 0; pr < p.npeers; pr++)
+          *reinterpret_cast<int4*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = w;
       } else {
 #pragma unroll
         for (int q = 0; q < 4; q++)
-          if (ks[h][q] != 0u) out[i * p.ldi + j + q] = pv[h][q];
+          if (ks[h][q] != 0u) {
+            int32_t* dst = out + i * p.ldi + j + q;
+            *dst = pv[h][q];
+            for (int pr = 0; pr < p.npeers; pr++)
+              *reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = pv[h][q];
+          }
       }
     }
   }
@@ -869,14 +901,17 @@ template <int S>
 static int launch_nt(const MinplusArgs& a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_nt_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_nt_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(sizeof(SmemNT<S>))));
+    APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_nt_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        int(sizeof(SmemNT<S>))));
     attr = true;
   }
   const size_t es = sizeof(typename Narrow<S>::T);
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
     return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
-  minplus_nt_kernel<S><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
+  if (a.npeers) minplus_nt_kernel<S, true><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
+  else minplus_nt_kernel<S, false><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
   return 0;
 }
 
@@ -1143,6 +1178,9 @@ __global__ void __launch_bounds__(NT) minplus_exact_kernel(MinplusArgs p) {
 
 int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
   if (a.m <= 0 || a.n <= 0) return 0;
+  if (a.npeers < 0 || a.npeers > MAX_PEERS) return set_error(2, "npeers %d outside [0, %d]", a.npeers, MAX_PEERS);
+  if (a.npeers && !(a.Aprep && a.Bprep && (store == STORE_U8 || store == STORE_U16 || store == STORE_W32)))
+    return set_error(2, "fused peer stores need a bulk-staged tier (u8 / u16 / w32) with prepared panels");
   if (a.k <= 0) return 0;
   if (a.k > 65535) return set_error(2, "min-plus inner dimension %lld exceeds 65535", (long long)a.k);
   if (a.only_lo < a.only_hi) {

@@ -18,6 +18,12 @@ Work per rank is (products / P) + leaves; exchange per product is its output blo
 (m * n * (store bytes + 4)), e.g. 16384^2 * 5 B = 1.3 GiB for a top-level product at n = 32768
 against ~18 ms of 8-GPU compute.
 
+Fused exchange (``fused=True``, bulk-staged tiers u8/u16/w32): instead of all-gathering the bands
+after a product, the product kernel's epilogue stores every improved segment into every peer's
+replica as well (peer memory mapped with CUDA IPC, NVLink/NVSwitch stores), so the exchange
+overlaps the remaining tiles and the host only adds a 4-byte all-reduce as the per-product
+barrier.  Emulated ranks on one GPU exercise the same kernel path with in-process replicas.
+
 The schedule is written once over per-rank ``ops`` and a comm with ``gather_bands``:
 * ``CudaRkOps`` + ``TorchComm``            -- the product path (torchrun, one process per GPU);
 * ``CudaRkOps`` + ``EmulatedComm``         -- all ranks in one process on one GPU (tests);
@@ -28,7 +34,7 @@ from __future__ import annotations
 
 import ctypes
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 from . import _native as nat
 from .core import CostRangeError, ParameterError
@@ -66,17 +72,24 @@ def run_rkleene(ranks: list[RankState], world: int, N: int, thr: int, ops, comm)
     Operand specs: ("D", i, j) the matrix, ("S", 0, 0) the value snapshot, ("P", i, j) the pred
     matrix, ("SP", 0, 0) the pred snapshot (the aliasing rules of solvers.py:250-286)."""
 
+    fused = bool(getattr(ops, "fused_for", lambda st: False)(ranks[0].state))
+
     def product(A, B, r0, c0, m, n, k, PB, inner_off):
         bands = row_bands(m, world)
         for rk in ranks:
             lo, hi = bands[rk.rank]
             if hi > lo:
                 ops.product(rk.state, A, B, r0, c0, lo, hi, n, k, PB, inner_off)
-        comm.gather_bands(ranks, ops, r0, c0, n, bands)
+        if fused:
+            comm.product_barrier(ranks, ops)      # bands already stored into every replica
+        else:
+            comm.gather_bands(ranks, ops, r0, c0, n, bands)
 
     def snap(i, j, rows, cols, idx):
         for rk in ranks:
             ops.snap(rk.state, i, j, rows, cols, idx)
+        if fused:   # the snapshot's source is the next product's output: no peer may store into
+            comm.product_barrier(ranks, ops)      # it before every rank has taken its copy
 
     def close(lo, hi):
         m = hi - lo
@@ -113,6 +126,9 @@ def run_rk_schedule(ranks, world, n, thr, ops, comm, dtype_code, h_fulls, tier_r
         for rk, h in zip(ranks, h_fulls):
             rk.state = ops.alloc(tier, N, thr)
             ops.prepare(rk.state, h, n, dtype_code)
+        if getattr(ops, "fused_for", lambda st: False)(ranks[0].state):
+            comm.connect_replicas(ranks, ops)
+            comm.product_barrier(ranks, ops)      # every replica prepared before any peer store
         run_rkleene(ranks, world, N, thr, ops, comm)
         gmax = ops.max_finite(ranks[0].state, n)
         if allreduce_max is not None:
@@ -137,17 +153,36 @@ class CudaRk:
     S: object
     SP: object
     scratch: object
+    peer_dc: object = None      # ctypes int64 arrays: byte deltas to the peer replicas (fused)
+    peer_di: object = None
+    npeers: int = 0
+    peer_views: list = field(default_factory=list)   # keeps IPC mappings alive
 
 
 class CudaRkOps:
     """One replica per rank and the C-ABI R-Kleene shard calls, on torch's current stream."""
 
-    def __init__(self, device):
+    def __init__(self, device, fused: bool = False):
         import torch
 
         self.torch = torch
         self.device = torch.device(device)
         self.lib = nat.load()
+        self.fused = fused
+
+    def fused_for(self, st) -> bool:
+        """Fused peer stores are available for the bulk-staged tiers."""
+        return self.fused and st.tier in (nat.TIER_U8, nat.TIER_U16, nat.TIER_W32)
+
+    def set_peers(self, st: CudaRk, peer_D: list, peer_P: list, keep=()) -> None:
+        """Peer replicas (tensors aliasing peer memory, same layout): byte deltas for the epilogue."""
+        n = len(peer_D)
+        if n > 7:
+            raise ParameterError("fused exchange supports at most 8 ranks")
+        st.npeers = n
+        st.peer_dc = (ctypes.c_int64 * max(n, 1))(*[d.data_ptr() - st.D.data_ptr() for d in peer_D])
+        st.peer_di = (ctypes.c_int64 * max(n, 1))(*[p.data_ptr() - st.P.data_ptr() for p in peer_P])
+        st.peer_views = list(keep)
 
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
@@ -194,6 +229,11 @@ class CudaRkOps:
         pb, ldpb = self._ptr(st, PB)
         c = st.D.data_ptr() + ((r0 + lo) * st.N + c0) * st.es
         p = st.P.data_ptr() + ((r0 + lo) * st.N + c0) * 4
+        if self.fused_for(st) and st.peer_dc is not None:
+            nat.check(self.lib.apsp_rk_shard_product_fused(
+                st.tier, a, lda, b, ldb, c, st.N, p, st.N, pb, ldpb, hi - lo, n, k, inner_off, st.N, st.thr,
+                st.npeers, st.peer_dc, st.peer_di, st.scratch.data_ptr(), st.scratch.numel(), self._stream()))
+            return
         nat.check(self.lib.apsp_rk_shard_product(st.tier, a, lda, b, ldb, c, st.N, p, st.N, pb, ldpb, hi - lo, n, k,
                                                  inner_off, st.N, st.thr, st.scratch.data_ptr(), st.scratch.numel(),
                                                  self._stream()))
@@ -264,13 +304,58 @@ def _emulated_gather_bands(self: EmulatedComm, ranks, ops, r0, c0, n, bands):
                 dst[1].copy_(src[1])
 
 
+def _torch_connect_replicas(self: TorchComm, ranks, ops):
+    """Map every peer's replica into this process (CUDA IPC handles exchanged over the process
+    group) and hand the byte deltas to the ops; world 1 has no peers."""
+    (rk,) = ranks
+    st = rk.state
+    if self.world == 1:
+        ops.set_peers(st, [], [])
+        return
+    from torch.multiprocessing.reductions import reduce_tensor
+
+    mine = (reduce_tensor(st.D), reduce_tensor(st.P))
+    every = [None] * self.world
+    self.dist.all_gather_object(every, mine, group=self.group)
+    peer_D, peer_P = [], []
+    for r, ((fd, ad), (fp, ap_)) in enumerate(every):
+        if r != rk.rank:
+            peer_D.append(fd(*ad))
+            peer_P.append(fp(*ap_))
+    ops.set_peers(st, peer_D, peer_P, keep=peer_D + peer_P)
+
+
+def _torch_product_barrier(self: TorchComm, ranks, ops):
+    """Every rank's fused product has landed in every replica: a 4-byte all-reduce on the
+    compute stream orders the next product after all peers' stores."""
+    if self.world == 1:
+        return
+    t = self.torch.zeros(1, dtype=self.torch.int32, device=self.device)
+    self.dist.all_reduce(t, group=self.group)
+
+
+def _emulated_connect_replicas(self: EmulatedComm, ranks, ops):
+    for rk in ranks:
+        others = [o.state for o in ranks if o is not rk]
+        ops.set_peers(rk.state, [o.D for o in others], [o.P for o in others])
+
+
+def _emulated_product_barrier(self: EmulatedComm, ranks, ops):
+    return None   # one stream, one process: stream order is the barrier
+
+
 TorchComm.gather_bands = _torch_gather_bands
 EmulatedComm.gather_bands = _emulated_gather_bands
+TorchComm.connect_replicas = _torch_connect_replicas
+EmulatedComm.connect_replicas = _emulated_connect_replicas
+TorchComm.product_barrier = _torch_product_barrier
+EmulatedComm.product_barrier = _emulated_product_barrier
 
 
 # ---- public entry points ------------------------------------------------------------------------
 
-def rkleene_sharded(h, n: int, *, comm: TorchComm, base_threshold: int = 1024, tier=None, ops=None):
+def rkleene_sharded(h, n: int, *, comm: TorchComm, base_threshold: int = 1024, tier=None, ops=None,
+                    fused: bool = True):
     """SPMD entry: every rank passes the full input (torch CUDA tensor, n x n, int32 or fp32)
     and receives the full (dist, pred) -- bit-identical to the one-GPU aligned R-Kleene."""
     import torch
@@ -279,7 +364,7 @@ def rkleene_sharded(h, n: int, *, comm: TorchComm, base_threshold: int = 1024, t
         raise ParameterError(f"rank {comm.rank} expects the full {n} x {n} input, got {tuple(h.shape)}")
     if base_threshold < 1:
         raise ParameterError(f"base_threshold must be >= 1, got {base_threshold}")
-    ops = ops or CudaRkOps(h.device)
+    ops = ops or CudaRkOps(h.device, fused=fused)
     rs = RankState(comm.rank, 0, n)
     dtype_code = _dtype_of(h)
     t0 = time.perf_counter()
@@ -293,13 +378,13 @@ def rkleene_sharded(h, n: int, *, comm: TorchComm, base_threshold: int = 1024, t
                                             "host_s": time.perf_counter() - t0})
 
 
-def rkleene_emulated(h, world: int, *, base_threshold: int = 1024, tier=None):
+def rkleene_emulated(h, world: int, *, base_threshold: int = 1024, tier=None, fused: bool = False):
     """All ``world`` ranks in this process on h's device (one replica each; sequential, no rank
     waits on another).  Returns (dist, pred, info) of rank 0's replica."""
     import torch
 
     n = h.shape[0]
-    ops = CudaRkOps(h.device)
+    ops = CudaRkOps(h.device, fused=fused)
     ranks = [RankState(r, 0, n) for r in range(world)]
     tier_code, gmax = run_rk_schedule(ranks, world, n, base_threshold, ops, EmulatedComm(), _dtype_of(h),
                                       [h] * world, tier, None)
@@ -308,4 +393,5 @@ def rkleene_emulated(h, world: int, *, base_threshold: int = 1024, tier=None):
     ops.finish(ranks[0].state, n, _dtype_of(h), dist, pred)
     replicas_equal = all(torch.equal(ranks[0].state.D, rk.state.D) and torch.equal(ranks[0].state.P, rk.state.P)
                          for rk in ranks[1:])
-    return dist, pred, {"tier": nat.TIER_NAMES[tier_code], "max_finite": gmax, "replicas_equal": replicas_equal}
+    return dist, pred, {"tier": nat.TIER_NAMES[tier_code], "max_finite": gmax, "replicas_equal": replicas_equal,
+                        "fused": ops.fused_for(ranks[0].state)}

@@ -119,3 +119,58 @@ def test_rkleene_emulated_tier_fallback(cuda):
     assert info["tier"] == "w32" and info["replicas_equal"]
     single = ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=128)
     assert torch.equal(d, single.distances) and torch.equal(p, single.index)
+
+
+@pytest.mark.parametrize("n,world,thr,rho", [(1000, 3, 256, 0.05), (2048, 4, 512, 0.1)])
+def test_rkleene_fused_peer_stores_emulated(cuda, n, world, thr, rho):
+    """Fused exchange: each rank's product epilogue writes its band into every replica."""
+    from paper_2310_03983_b200.distributed_rk import rkleene_emulated
+
+    h = torch.from_numpy(ap.dense_costs(ap.GenParams(n, rho, 100, n + 2), np.int32)).cuda()
+    single = ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=thr)
+    d, p, info = rkleene_emulated(h, world, base_threshold=thr, fused=True)
+    assert info["fused"] and info["replicas_equal"]
+    assert torch.equal(d, single.distances) and torch.equal(p, single.index)
+
+
+def _ipc_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2310_03983_b200.distributed import TorchComm
+        from paper_2310_03983_b200.distributed_rk import rkleene_sharded
+
+        n = 900
+        h = torch.from_numpy(ap.dense_costs(ap.GenParams(n, 0.05, 100, 77), np.int32)).cuda()
+        r = rkleene_sharded(h, n, comm=TorchComm(torch.device("cuda", 0)), base_threshold=256, fused=True)
+        torch.cuda.synchronize()
+        if rank == 0:
+            single = ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=256)
+            out.put(bool(torch.equal(r.distances, single.distances) and torch.equal(r.pred, single.index)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_rkleene_fused_ipc_two_processes_one_gpu(cuda):
+    """Two processes, one GPU: replicas mapped with CUDA IPC, bands pushed by the product
+    kernel's peer stores, gloo all-reduce as the per-product barrier (host-side; no kernel waits
+    on another)."""
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=5)
