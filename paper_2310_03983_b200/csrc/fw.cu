@@ -1,10 +1,11 @@
-// Floyd-Warshall kernels whose order of k matters: the classic per-k step (K1), the
-// diagonal-block closure (blocked phase 1 and the R-Kleene leaf) and the pivot panels
-// (blocked phase 2).  All use the strict-improvement rule of solvers.py:89-94 and write
-// idx as pred[k][j] (FW rule) or as the global k (via rule, solvers.py:109-114).
+// Floyd-Warshall kernels whose order of k matters: the classic per-k step (K1) and the
+// diagonal-block closure (blocked phase 1 and the R-Kleene leaf).  Both use the
+// strict-improvement rule of solvers.py:89-94 and write idx as pred[k][j] (FW rule) or as the
+// global k (via rule, solvers.py:109-114).  Phase 2 runs as min-plus products against the
+// closed diagonal block (minplus.cu).
 //
-// Race freedom in all three: with a zero diagonal and nonnegative costs, row k and column k
-// are invariant during step k (solvers.py:79-81), so one barrier per k suffices.
+// Race freedom: with a zero diagonal and nonnegative costs, row k and column k are invariant
+// during step k (solvers.py:79-81), so one barrier per k suffices.
 #include <cstdlib>
 #include "launch.h"
 
@@ -391,208 +392,6 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
     case STORE_U16: return close_impl<STORE_U16>(D, ld, lo, m, idx, ldi, mode, via_off, st, s);
   }
   return set_error(2, "unknown store %d", store);
-}
-
-// ------------------------------------------------------------------------------------
-// Phase 2 panels against a closed b x b diagonal block Dg (b <= 128).
-//   rows kernel: T is b x ncols (the pivot rows);   T[i][j] = min(T, Dg[i][k] + T[k][j])
-//                idx rule pred: PT[i][j] <- PT[k][j] (same panel, kept in smem)
-//   cols kernel: T is nrows x b (the pivot columns); T[i][j] = min(T, T[i][k] + Dg[k][j])
-//                idx rule pred: PT[i][j] <- PDg[k*][j] (diag pred is final: gather at end)
-// Each CTA owns a 32-wide strip (columns for rows kernel, rows for cols kernel).
-// ------------------------------------------------------------------------------------
-constexpr int PW = 32;
-
-template <int S>
-__global__ void __launch_bounds__(256) panel_rows_kernel(const typename StoreT<S>::T* Dg, int64_t ldg,
-                                                         typename StoreT<S>::T* T_, int64_t ldt, int32_t* PT,
-                                                         int64_t ldpt, int b, int64_t ncols, int mode,
-                                                         int64_t via_off, int64_t skip_lo, int64_t skip_hi,
-                                                         Status* st) {
-  using T = typename StoreT<S>::T;
-  using A = typename StoreT<S>::A;
-  const int64_t c0 = int64_t(blockIdx.x) * PW;
-  if (c0 >= skip_lo && c0 + PW <= skip_hi) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  A* G = reinterpret_cast<A*>(smraw);        // b x b
-  A* V = G + b * b;                           // b x PW
-  int32_t* I = reinterpret_cast<int32_t*>(V + b * PW);   // b x PW
-  const T inf = store_inf<S>();
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t j = c0 + tx;
-  for (int i = ty; i < b; i += 8) {
-    for (int q = tx; q < b; q += 32) G[i * b + q] = A(Dg[i * ldg + q]);
-    V[i * PW + tx] = A(j < ncols ? T_[i * ldt + j] : inf);
-    I[i * PW + tx] = (PT && j < ncols) ? PT[i * ldpt + j] : -1;
-  }
-  bool overflow = false;
-  uint32_t changed_rows = 0;
-  for (int k = 0; k < b; k++) {
-    __syncthreads();
-    const A vkj = V[k * PW + tx];
-    const int32_t ikj = I[k * PW + tx];
-    for (int i = ty, q = 0; i < b; i += 8, q++) {
-      const A c = G[i * b + k] + vkj;
-      if (c < V[i * PW + tx]) {
-        overflow |= range_overflow<S>(c);
-        V[i * PW + tx] = c;
-        I[i * PW + tx] = (mode == IDX_PRED) ? ikj : int32_t(via_off + k);
-        changed_rows |= 1u << q;
-      }
-    }
-  }
-  __syncthreads();
-  if (j < ncols)
-    for (int i = ty, q = 0; i < b; i += 8, q++)
-      if (changed_rows & (1u << q)) {
-        T_[i * ldt + j] = T(V[i * PW + tx]);
-        if (PT) PT[i * ldpt + j] = I[i * PW + tx];
-      }
-  if (st && overflow) st->overflow = 1;
-}
-
-template <int S>
-__global__ void __launch_bounds__(256) panel_cols_kernel(const typename StoreT<S>::T* Dg, int64_t ldg,
-                                                         const int32_t* PDg, int64_t ldpg,
-                                                         typename StoreT<S>::T* T_, int64_t ldt, int32_t* PT,
-                                                         int64_t ldpt, int b, int64_t nrows, int mode,
-                                                         int64_t via_off, int64_t skip_lo, int64_t skip_hi,
-                                                         Status* st) {
-  using T = typename StoreT<S>::T;
-  using A = typename StoreT<S>::A;
-  const int64_t r0 = int64_t(blockIdx.x) * PW;
-  if (r0 >= skip_lo && r0 + PW <= skip_hi) return;
-  extern __shared__ __align__(16) unsigned char smraw[];
-  A* G = reinterpret_cast<A*>(smraw);        // b x b
-  A* V = G + b * b;                           // PW x b
-  int16_t* K = reinterpret_cast<int16_t*>(V + PW * b);   // PW x b
-  const T inf = store_inf<S>();
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int i = ty; i < b; i += 8)
-    for (int q = tx; q < b; q += 32) G[i * b + q] = A(Dg[i * ldg + q]);
-  for (int i = ty; i < PW; i += 8)
-    for (int q = tx; q < b; q += 32) {
-      V[i * b + q] = A(r0 + i < nrows ? T_[(r0 + i) * ldt + q] : inf);
-      K[i * b + q] = -1;
-    }
-  bool overflow = false;
-  for (int k = 0; k < b; k++) {
-    __syncthreads();
-    for (int i = ty; i < PW; i += 8) {
-      const A vik = V[i * b + k];
-      for (int q = tx; q < b; q += 32) {
-        const A c = vik + G[k * b + q];
-        if (c < V[i * b + q]) {
-          overflow |= range_overflow<S>(c);
-          V[i * b + q] = c;
-          K[i * b + q] = int16_t(k);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int i = ty; i < PW; i += 8) {
-    if (r0 + i >= nrows) break;
-    for (int q = tx; q < b; q += 32) {
-      const int kk = K[i * b + q];
-      if (kk < 0) continue;
-      T_[(r0 + i) * ldt + q] = T(V[i * b + q]);
-      if (PT) PT[(r0 + i) * ldpt + q] = (mode == IDX_PRED) ? PDg[int64_t(kk) * ldpg + q] : int32_t(via_off + kk);
-    }
-  }
-  if (st && overflow) st->overflow = 1;
-}
-
-template <int S>
-static size_t rows_smem(int b) { return size_t(b) * b * sizeof(typename StoreT<S>::A) + size_t(b) * PW * (sizeof(typename StoreT<S>::A) + 4); }
-template <int S>
-static size_t cols_smem(int b) { return size_t(b) * b * sizeof(typename StoreT<S>::A) + size_t(b) * PW * (sizeof(typename StoreT<S>::A) + 2); }
-
-template <int S>
-static int panel_rows_impl(const void* Dg, int64_t ldg, void* T_, int64_t ldt, int32_t* PT, int64_t ldpt, int64_t b,
-                           int64_t ncols, int mode, int64_t via_off, int64_t skip_lo, int64_t skip_hi, Status* st,
-                           cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    APSP_CUDA_TRY(cudaFuncSetAttribute(panel_rows_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(rows_smem<S>(MAXB))));
-    attr = true;
-  }
-  using T = typename StoreT<S>::T;
-  const unsigned grid = unsigned((ncols + PW - 1) / PW);
-  if (grid == 0) return 0;
-  panel_rows_kernel<S><<<grid, 256, rows_smem<S>(int(b)), s>>>(static_cast<const T*>(Dg), ldg, static_cast<T*>(T_),
-                                                               ldt, PT, ldpt, int(b), ncols, mode, via_off, skip_lo,
-                                                               skip_hi, st);
-  APSP_CUDA_TRY(cudaGetLastError());
-  count_launches(1);
-  return 0;
-}
-
-template <int S>
-static int panel_cols_impl(const void* Dg, int64_t ldg, const int32_t* PDg, int64_t ldpg, void* T_, int64_t ldt,
-                           int32_t* PT, int64_t ldpt, int64_t b, int64_t nrows, int mode, int64_t via_off,
-                           int64_t skip_lo, int64_t skip_hi, Status* st, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    APSP_CUDA_TRY(cudaFuncSetAttribute(panel_cols_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(cols_smem<S>(MAXB))));
-    attr = true;
-  }
-  using T = typename StoreT<S>::T;
-  const unsigned grid = unsigned((nrows + PW - 1) / PW);
-  if (grid == 0) return 0;
-  panel_cols_kernel<S><<<grid, 256, cols_smem<S>(int(b)), s>>>(static_cast<const T*>(Dg), ldg, PDg, ldpg,
-                                                               static_cast<T*>(T_), ldt, PT, ldpt, int(b), nrows, mode,
-                                                               via_off, skip_lo, skip_hi, st);
-  APSP_CUDA_TRY(cudaGetLastError());
-  count_launches(1);
-  return 0;
-}
-
-#define APSP_STORE_DISPATCH(store, CALL)                       \
-  switch (store) {                                             \
-    case STORE_U8: return CALL(STORE_U8);                      \
-    case STORE_W32: return CALL(STORE_W32);                    \
-    case STORE_I32: return CALL(STORE_I32);                    \
-    case STORE_F32: return CALL(STORE_F32);                    \
-    case STORE_I64: return CALL(STORE_I64);                    \
-    case STORE_U16: return CALL(STORE_U16);                    \
-    default: return set_error(2, "unknown store %d", store);   \
-  }
-
-int launch_panel_rows(int store, const void* Dg, int64_t ldg, void* T_, int64_t ldt, int32_t* PT, int64_t ldpt,
-                      int64_t b, int64_t ncols, int mode, int64_t via_off, Status* st, cudaStream_t s) {
-  if (b > MAXB) return set_error(2, "panel block %lld exceeds %d", (long long)b, MAXB);
-#define CALL(S) panel_rows_impl<S>(Dg, ldg, T_, ldt, PT, ldpt, b, ncols, mode, via_off, -1, -1, st, s)
-  APSP_STORE_DISPATCH(store, CALL)
-#undef CALL
-}
-
-int launch_panel_cols(int store, const void* Dg, int64_t ldg, const int32_t* PDg, int64_t ldpg, void* T_, int64_t ldt,
-                      int32_t* PT, int64_t ldpt, int64_t b, int64_t nrows, int mode, int64_t via_off, Status* st,
-                      cudaStream_t s) {
-  if (b > MAXB) return set_error(2, "panel block %lld exceeds %d", (long long)b, MAXB);
-#define CALL(S) panel_cols_impl<S>(Dg, ldg, PDg, ldpg, T_, ldt, PT, ldpt, b, nrows, mode, via_off, -1, -1, st, s)
-  APSP_STORE_DISPATCH(store, CALL)
-#undef CALL
-}
-
-int launch_fw_panels(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, int64_t k0, int b, int mode,
-                     int64_t via_off, Status* st, cudaStream_t s) {
-  if (b > MAXB) return set_error(2, "panel block %d exceeds %d", b, MAXB);
-  const size_t es = store_elem_size(store);
-  char* Dc = static_cast<char*>(D);
-  const void* Dg = Dc + (k0 * ld + k0) * es;
-  // row panel: rows [k0,k0+b), all columns, pivot strip skipped
-  // column panel: all rows, columns [k0,k0+b), pivot strip skipped
-#define CALL(S)                                                                                                   \
-  (panel_rows_impl<S>(Dg, ld, Dc + k0 * ld * es, ld, P ? P + k0 * ldp : nullptr, ldp, b, N, mode, via_off + k0, \
-                      k0, k0 + b, st, s) ||                                                                       \
-   panel_cols_impl<S>(Dg, ld, P ? P + k0 * ldp + k0 : nullptr, ldp, Dc + k0 * es, ld, P ? P + k0 : nullptr, ldp, \
-                      b, N, mode, via_off + k0, k0, k0 + b, st, s))
-  APSP_STORE_DISPATCH(store, CALL)
-#undef CALL
 }
 
 }  // namespace apsp

@@ -65,22 +65,6 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m,
                        int32_t* idx, int64_t ldi, int mode, int64_t via_off, Status* st,
                        cudaStream_t s);
 
-// FW phase 2 for pivot block [k0, k0+b) of the N x N view D: row panel (rows of the pivot
-// block, all columns outside it) and column panel (all rows outside it, pivot columns),
-// each in classic k order against the closed diagonal block.
-// via_off = global vertex of row/column 0 of the view (pivot k gets via_off + k0 + k).
-int launch_fw_panels(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N,
-                     int64_t k0, int b, int mode, int64_t via_off, Status* st, cudaStream_t s);
-
-// Generalised panel update used by the sharded path: rows [r0,r1) x cols [c0,c1) of a
-// panel updated against the diagonal block (either its rows = pivot rows, or its cols).
-int launch_panel_rows(int store, const void* Dg, int64_t ldg, void* T, int64_t ldt, int32_t* PT,
-                      int64_t ldpt, int64_t b, int64_t ncols, int mode, int64_t via_off,
-                      Status* st, cudaStream_t s);
-int launch_panel_cols(int store, const void* Dg, int64_t ldg, const int32_t* PDg, int64_t ldpg,
-                      void* T, int64_t ldt, int32_t* PT, int64_t ldpt, int64_t b, int64_t nrows,
-                      int mode, int64_t via_off, Status* st, cudaStream_t s);
-
 // Classic per-k Floyd-Warshall step (K1): bit-exact pred/via parity with fw_classic
 // (solvers.py:77-95).  One launch per k; row k / column k are invariant in step k.
 int launch_fw_step(int store, void* D, int64_t ld, int64_t n, int64_t k, int32_t* idx,

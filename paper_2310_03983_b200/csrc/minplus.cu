@@ -377,26 +377,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Tile origin of virtual tile index v (the 2D grid flattened row-major, or the cross list).
-__device__ __forceinline__ void tile_at(const MinplusArgs& p, int64_t v, int bm, int bn, int64_t& i0, int64_t& j0) {
-  if (p.only_lo < p.only_hi) {
-    const int64_t w = (p.only_hi - p.only_lo) / bm, lo_t = p.only_lo / bm;
-    const int64_t nt_c = (p.n + bn - 1) / bn;
-    if (v < w * nt_c) {
-      i0 = (lo_t + v / nt_c) * bm;
-      j0 = (v % nt_c) * bn;
-    } else {
-      const int64_t id2 = v - w * nt_c, rr = id2 / w, cc = id2 % w;
-      i0 = (rr < lo_t ? rr : rr + w) * bm;
-      j0 = (lo_t + cc) * bn;
-    }
-  } else {
-    const int64_t nt_c = (p.n + bn - 1) / bn;
-    i0 = (v / nt_c) * bm;
-    j0 = (v % nt_c) * bn;
-  }
-}
-
 // One 128 x 128 tile per CTA (8 warps, 8 x 8 cells per thread).  The pre-laid-out A/B chunks
 // stream through a STAGES-slot ring with cp.async.bulk (full mbarriers carry the tx count).
 // No barrier sits in the k loop: each warp counts itself out of a slot when it has consumed
