@@ -371,12 +371,8 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
     return 0;
   }
   if (store == STORE_U8 && !getenv("APSP_SLOW_CLOSE")) {
-    static bool attr = false;
-    if (!attr) {
-      APSP_CUDA_TRY(cudaFuncSetAttribute(block_close_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(sizeof(CloseU8Smem))));
-      attr = true;
-    }
+    static std::atomic<unsigned long long> attr{0};
+    APSP_CUDA_TRY(smem_optin(block_close_u8_kernel, int(sizeof(CloseU8Smem)), attr));
     block_close_u8_kernel<<<1, 512, sizeof(CloseU8Smem), s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
                                                               mode, via_off);
     APSP_CUDA_TRY(cudaGetLastError());

@@ -1,11 +1,26 @@
 // Host-side launchers for the sm_100a kernels (one translation unit per kernel family).
 #pragma once
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "common.cuh"
 
 namespace apsp {
+
+// Opt a kernel into more than 48 KB of dynamic shared memory, once per device (the attribute is
+// per device; a process may drive several GPUs through apsp_solve_host's device argument).
+template <typename K>
+inline cudaError_t smem_optin(K* kernel, int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 // One min-plus tile update  C <- min(C, A (x) B)  with strict-improvement lexicographic
 // (value, smallest k) argmin, written to idx on improvement only.  Covers FW phase 3

@@ -865,12 +865,8 @@ static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
 }
 
 static int launch_w32nt(const MinplusArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_w32nt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(sizeof(SmemW32NT))));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  APSP_CUDA_TRY(smem_optin(minplus_w32nt_kernel, int(sizeof(SmemW32NT)), attr));
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * 4) % 16)
     return set_error(2, "bulk-staged w32 tiles need full 128 x 128 tiles and 32-multiple k");
   minplus_w32nt_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemW32NT), s>>>(a);
@@ -879,14 +875,9 @@ static int launch_w32nt(const MinplusArgs& a, cudaStream_t s) {
 
 template <int S>
 static int launch_nt(const MinplusArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_nt_kernel<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(sizeof(SmemNT<S>))));
-    APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_nt_kernel<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(sizeof(SmemNT<S>))));
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr0{0}, attr1{0};
+  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, false>, int(sizeof(SmemNT<S>)), attr0));
+  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, true>, int(sizeof(SmemNT<S>)), attr1));
   const size_t es = sizeof(typename Narrow<S>::T);
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
     return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
@@ -1175,12 +1166,8 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
         if (rc) return rc;
         break;
       }
-      static bool attr = false;
-      if (!attr) {
-        APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(sizeof(SmemU8))));
-        attr = true;
-      }
+      static std::atomic<unsigned long long> attr{0};
+      APSP_CUDA_TRY(smem_optin(minplus_u8_kernel, int(sizeof(SmemU8)), attr));
       minplus_u8_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemU8), s>>>(a);
       break;
     }
@@ -1190,12 +1177,8 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
         if (rc) return rc;
         break;
       }
-      static bool attr = false;
-      if (!attr) {
-        APSP_CUDA_TRY(cudaFuncSetAttribute(minplus_w32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(sizeof(SmemW32))));
-        attr = true;
-      }
+      static std::atomic<unsigned long long> attr{0};
+      APSP_CUDA_TRY(smem_optin(minplus_w32_kernel, int(sizeof(SmemW32)), attr));
       minplus_w32_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemW32), s>>>(a);
       break;
     }
