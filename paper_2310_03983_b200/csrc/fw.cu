@@ -171,137 +171,152 @@ __global__ void __launch_bounds__(512) block_close_kernel(typename StoreT<S>::T*
 // ------------------------------------------------------------------------------------
 // u8 tier closure of an m <= 128 diagonal block: packed 16-bit DPX keys.
 //   key = value << 7 | tag, tag = 1 + (k mod 64), decoded every 64 steps into the last
-//   improving k per cell (8 bits, 1-based).  Row / column k are published tag-free.
+//   improving k per cell (8 bits, 1-based).  Row / column k are used tag-free.
 //   pred is deferred: with k* the last improving step of (i,j), pred[k*][j] never changes after
 //   step k* (else (i,j) would improve again), so pred_final[i][j] = pred_final[k*][j]; the
 //   chains k* -> kst(k*, j) -> ... strictly decrease and are resolved by pointer jumping.
 //   The result equals the classic in-block order exactly (values, pred and via).
-// 512 threads: thread (ty, tx) owns rows ty + 16a (a < 8) x column pairs 2tx + 64c (c < 2).
+// 512 threads: warp w owns columns 8w..8w+7 of every row, lane l owns rows 4l..4l+3, so a
+// thread holds rows 4l + r (r < 4) x column pairs 8w + 2p (p < 4).  Row k of a warp's columns
+// lives in lane k >> 2 of the same warp and is broadcast by shuffle; column k lives in warp
+// k >> 3 (all lanes) and goes through shared memory, one 16-byte store per lane.  The k loop
+// is unrolled by 8, so every register index is a compile-time constant (no select chains).
 // ------------------------------------------------------------------------------------
 struct CloseU8Smem {
-  uint32_t rowk[2][64];       // row k as tag-free key pairs, [2 * tx + c]: one 8-byte read per lane
-  uint32_t colk[2][MAXB];     // column k as replicated tag-free keys, [8 * ty + a]: 2 x 16-byte reads
+  uint32_t colk[2][MAXB];     // column k as replicated tag-free keys, by row (16-byte lane slots)
   int32_t P[MAXB][MAXB];      // pred resolution
   uint8_t K[MAXB][MAXB];      // 1-based last improving k (0 = none)
 };
-
-__device__ __forceinline__ uint32_t u8c_strip(uint32_t x) { return x & 0xFF80FF80u; }
 
 __global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t ld, int64_t lo, int m, int32_t* idx,
                                                              int64_t ldi, int mode, int64_t via_off) {
   extern __shared__ __align__(16) unsigned char smraw_cu8[];
   CloseU8Smem& sm = *reinterpret_cast<CloseU8Smem*>(smraw_cu8);
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  constexpr uint32_t KINF2 = (255u << 7) * 0x00010001u;
-  uint32_t acc[8][2];
-  uint32_t kst[8];            // byte q of kst[a] = cell (a, q): q = 2c + half
-#pragma unroll
-  for (int a = 0; a < 8; a++) {
-    const int i = ty + 16 * a;
-    kst[a] = 0;
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-      const int j = 2 * tx + 64 * c;
-      uint32_t lo16 = 255, hi16 = 255;
-      if (i < m && j < m) lo16 = D[(lo + i) * ld + lo + j];
-      if (i < m && j + 1 < m) hi16 = D[(lo + i) * ld + lo + j + 1];
-      acc[a][c] = ((hi16 << 16) | lo16) << 7;
+  const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t acc[4][4];   // [row r][pair p]: columns (8w + 2p, 8w + 2p + 1)
+  uint32_t kst[4][2];   // byte 2 * (p & 1) + h of kst[r][p >> 1] = cell (r, 8w + 2p + h)
+  // coalesced load through the K staging area (lanes over columns), then each thread picks
+  // its 4 rows x 8 bytes
+  const bool vec = m == MAXB && ((reinterpret_cast<uintptr_t>(D + lo * ld + lo) | uintptr_t(ld)) & 15) == 0;
+  if (vec) {   // full aligned block (every FW phase 1): 16-byte rows segments
+    for (int e = threadIdx.x; e < MAXB * MAXB / 16; e += blockDim.x) {
+      const int i = e >> 3, j = 16 * (e & 7);
+      *reinterpret_cast<uint4*>(&sm.K[i][j]) = *reinterpret_cast<const uint4*>(D + (lo + i) * ld + lo + j);
+    }
+  } else {
+    for (int e = threadIdx.x; e < MAXB * MAXB; e += blockDim.x) {
+      const int i = e >> 7, j = e & 127;
+      sm.K[i][j] = (i < m && j < m) ? D[(lo + i) * ld + lo + j] : uint8_t(255);
     }
   }
-  // publish helpers (select chains: no dynamic register indexing)
-#define CU8_PUBLISH(KK, BUF)                                                              \
-  do {                                                                                    \
-    const int pk_ = (KK), pb_ = (BUF);                                                    \
-    if (ty == (pk_ & 15)) {   /* one warp: row pk_ = register row pk_ >> 4 */            \
-      const int sa_ = pk_ >> 4;                                                           \
-      uint32_t r0_ = acc[0][0], r1_ = acc[0][1];                                          \
-      _Pragma("unroll") for (int a = 1; a < 8; a++) {                                     \
-        r0_ = (a == sa_) ? acc[a][0] : r0_;                                               \
-        r1_ = (a == sa_) ? acc[a][1] : r1_;                                               \
-      }                                                                                   \
-      *reinterpret_cast<uint2*>(&sm.rowk[pb_][2 * tx]) = make_uint2(u8c_strip(r0_), u8c_strip(r1_)); \
-    }                                                                                     \
-    if (tx == ((pk_ & 63) >> 1)) {   /* one lane per warp: column pk_, 8 rows */          \
-      const int sc_ = pk_ >> 6;                                                           \
-      const uint32_t sel_ = (pk_ & 1) ? 0x3232u : 0x1010u;   /* replicate the half */     \
-      uint32_t v_[8];                                                                     \
-      _Pragma("unroll") for (int a = 0; a < 8; a++)                                       \
-        v_[a] = __byte_perm(sc_ ? acc[a][1] : acc[a][0], 0, sel_) & 0xFF80FF80u;          \
-      *reinterpret_cast<uint4*>(&sm.colk[pb_][8 * ty]) = make_uint4(v_[0], v_[1], v_[2], v_[3]); \
-      *reinterpret_cast<uint4*>(&sm.colk[pb_][8 * ty + 4]) = make_uint4(v_[4], v_[5], v_[6], v_[7]); \
-    }                                                                                     \
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    const uint2 v = *reinterpret_cast<const uint2*>(&sm.K[4 * l + r][8 * w]);
+    kst[r][0] = kst[r][1] = 0;
+    acc[r][0] = __byte_perm(v.x, 0, 0x4140) << 7;
+    acc[r][1] = __byte_perm(v.x, 0, 0x4342) << 7;
+    acc[r][2] = __byte_perm(v.y, 0, 0x4140) << 7;
+    acc[r][3] = __byte_perm(v.y, 0, 0x4342) << 7;
+  }
+  // column KC (its low 3 bits KL static) of the owner warp into buffer BUF
+#define CU8_PUBCOL(KC, KL, BUF)                                                                  \
+  do {                                                                                           \
+    if (w == ((KC) >> 3)) {                                                                      \
+      const int pp_ = ((KL) & 7) >> 1;                                                       \
+      const uint32_t sel_ = ((KL) & 1) ? 0x3232u : 0x1010u; /* replicate the half */        \
+      *reinterpret_cast<uint4*>(&sm.colk[BUF][4 * l]) =                                          \
+          make_uint4(__byte_perm(acc[0][pp_], 0, sel_) & 0xFF80FF80u,                            \
+                     __byte_perm(acc[1][pp_], 0, sel_) & 0xFF80FF80u,                            \
+                     __byte_perm(acc[2][pp_], 0, sel_) & 0xFF80FF80u,                            \
+                     __byte_perm(acc[3][pp_], 0, sel_) & 0xFF80FF80u);                           \
+    }                                                                                            \
   } while (0)
-  CU8_PUBLISH(0, 0);
-  for (int k = 0; k < m; k++) {
-    __syncthreads();
-    const int b = k & 1;
-    const uint32_t tag2 = uint32_t((k & 63) + 1) * 0x00010001u;
-    uint32_t dkj[2], dik[8];
-    {
-      const uint2 r = *reinterpret_cast<const uint2*>(&sm.rowk[b][2 * tx]);
-      dkj[0] = r.x + tag2;
-      dkj[1] = r.y + tag2;
-      const uint4 c0 = *reinterpret_cast<const uint4*>(&sm.colk[b][8 * ty]);
-      const uint4 c1 = *reinterpret_cast<const uint4*>(&sm.colk[b][8 * ty + 4]);
-      dik[0] = c0.x; dik[1] = c0.y; dik[2] = c0.z; dik[3] = c0.w;
-      dik[4] = c1.x; dik[5] = c1.y; dik[6] = c1.z; dik[7] = c1.w;
-    }
+  CU8_PUBCOL(0, 0, 0);
+  for (int k0 = 0; k0 < m; k0 += 8) {
 #pragma unroll
-    for (int a = 0; a < 8; a++)
+    for (int kk = 0; kk < 8; kk++) {
+      const int k = k0 + kk;
+      if (k < m) {
+        __syncthreads();
+        const uint4 c4 = *reinterpret_cast<const uint4*>(&sm.colk[kk & 1][4 * l]);
+        const uint32_t dik[4] = {c4.x, c4.y, c4.z, c4.w};
+        const uint32_t tag2 = uint32_t((k & 63) + 1) * 0x00010001u;
+        uint32_t dkj[4];
 #pragma unroll
-      for (int c = 0; c < 2; c++) acc[a][c] = __viaddmin_u16x2(dik[a], dkj[c], acc[a][c]);
-    if ((k & 63) == 63 || k + 1 == m) {   // decode this 64-step window
-      const uint32_t wbase = uint32_t(k & ~63);
+        for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[kk & 3][p], k >> 2) & 0xFF80FF80u) + tag2;
 #pragma unroll
-      for (int a = 0; a < 8; a++) {
+        for (int r = 0; r < 4; r++)
 #pragma unroll
-        for (int c = 0; c < 2; c++) {
-          const uint32_t tg = acc[a][c] & 0x007F007Fu;
-          acc[a][c] ^= tg;
-          const uint32_t tlo = tg & 0xFF, thi = tg >> 16;
-          const int sh0 = 8 * (2 * c), sh1 = 8 * (2 * c + 1);
-          if (tlo) kst[a] = (kst[a] & ~(0xFFu << sh0)) | ((wbase + tlo) << sh0);
-          if (thi) kst[a] = (kst[a] & ~(0xFFu << sh1)) | ((wbase + thi) << sh1);
+          for (int p = 0; p < 4; p++) acc[r][p] = __viaddmin_u16x2(dik[r], dkj[p], acc[r][p]);
+        if ((k & 63) == 63 || k + 1 == m) {   // decode this 64-step window
+          const uint32_t wbase = uint32_t(k & ~63);
+#pragma unroll
+          for (int r = 0; r < 4; r++) {
+#pragma unroll
+            for (int p = 0; p < 4; p++) {
+              const uint32_t tg = acc[r][p] & 0x007F007Fu;
+              acc[r][p] ^= tg;
+              const uint32_t tlo = tg & 0xFF, thi = tg >> 16;
+              const int sh0 = 8 * (2 * (p & 1)), sh1 = sh0 + 8;
+              uint32_t& ks = kst[r][p >> 1];
+              if (tlo) ks = (ks & ~(0xFFu << sh0)) | ((wbase + tlo) << sh0);
+              if (thi) ks = (ks & ~(0xFFu << sh1)) | ((wbase + thi) << sh1);
+            }
+          }
         }
+        if (k + 1 < m) CU8_PUBCOL(k + 1, kk + 1, (kk + 1) & 1);
       }
     }
-    if (k + 1 < m) CU8_PUBLISH(k + 1, b ^ 1);
   }
-#undef CU8_PUBLISH
-  // values back
+#undef CU8_PUBCOL
+  // values back (through the staging area) and the 1-based k* bytes
+  __syncthreads();   // every thread has read its cells and column k of the last step
 #pragma unroll
-  for (int a = 0; a < 8; a++) {
-    const int i = ty + 16 * a;
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-      const int j = 2 * tx + 64 * c;
-      const uint32_t v = acc[a][c] >> 7;
-      if (i < m && j < m) D[(lo + i) * ld + lo + j] = uint8_t(v & 0xFF);
-      if (i < m && j + 1 < m) D[(lo + i) * ld + lo + j + 1] = uint8_t(v >> 16);
+  for (int r = 0; r < 4; r++) {
+    const uint32_t v0 = __byte_perm(acc[r][0] >> 7, acc[r][1] >> 7, 0x6420);
+    const uint32_t v1 = __byte_perm(acc[r][2] >> 7, acc[r][3] >> 7, 0x6420);
+    *reinterpret_cast<uint2*>(&sm.K[4 * l + r][8 * w]) = make_uint2(v0, v1);
+  }
+  __syncthreads();
+  if (vec) {
+    for (int e = threadIdx.x; e < MAXB * MAXB / 16; e += blockDim.x) {
+      const int i = e >> 3, j = 16 * (e & 7);
+      *reinterpret_cast<uint4*>(D + (lo + i) * ld + lo + j) = *reinterpret_cast<const uint4*>(&sm.K[i][j]);
+    }
+  } else {
+    for (int e = threadIdx.x; e < MAXB * MAXB; e += blockDim.x) {
+      const int i = e >> 7, j = e & 127;
+      if (i < m && j < m) D[(lo + i) * ld + lo + j] = sm.K[i][j];
     }
   }
   if (!idx) return;
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 4; r++)
+    *reinterpret_cast<uint2*>(&sm.K[4 * l + r][8 * w]) = make_uint2(kst[r][0], kst[r][1]);
+  __syncthreads();
+  // pred / via resolution in a bank-conflict-free mapping: lanes over columns
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   if (mode == IDX_VIA) {
 #pragma unroll
     for (int a = 0; a < 8; a++) {
       const int i = ty + 16 * a;
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
-        const uint32_t kk = (kst[a] >> (8 * q)) & 0xFF;
+        const int j = tx + 32 * q;
+        const uint32_t kk = sm.K[i][j];
         if (kk && i < m && j < m) idx[(lo + i) * ldi + lo + j] = int32_t(via_off + kk - 1);
       }
     }
     return;
   }
-  // pred: stage P_init and the 0-based k* rows, then pointer-jump the chains
 #pragma unroll
   for (int a = 0; a < 8; a++) {
     const int i = ty + 16 * a;
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
-      sm.K[i][j] = uint8_t((kst[a] >> (8 * q)) & 0xFF);
+      const int j = tx + 32 * q;
       sm.P[i][j] = (i < m && j < m) ? idx[(lo + i) * ldi + lo + j] : -1;
     }
   }
@@ -309,40 +324,44 @@ __global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t
   for (int round = 0; round < 7; round++) {   // chains have length < 128 = 2^7
     int32_t np[8][4];
     uint8_t nk[8][4];
+    bool live = false;
 #pragma unroll
     for (int a = 0; a < 8; a++) {
       const int i = ty + 16 * a;
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
+        const int j = tx + 32 * q;
         const uint8_t kk = sm.K[i][j];
         np[a][q] = sm.P[i][j];
         nk[a][q] = kk;
         if (kk) {
           np[a][q] = sm.P[kk - 1][j];
           nk[a][q] = sm.K[kk - 1][j];
+          live |= nk[a][q] != 0;
         }
       }
     }
-    __syncthreads();
+    // chains are usually a few hops long: stop as soon as none has a next hop left
+    const bool more = __syncthreads_or(live);
 #pragma unroll
     for (int a = 0; a < 8; a++) {
       const int i = ty + 16 * a;
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
+        const int j = tx + 32 * q;
         sm.P[i][j] = np[a][q];
         sm.K[i][j] = nk[a][q];
       }
     }
     __syncthreads();
+    if (!more) break;
   }
 #pragma unroll
   for (int a = 0; a < 8; a++) {
     const int i = ty + 16 * a;
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      const int j = 2 * tx + 64 * (q >> 1) + (q & 1);
+      const int j = tx + 32 * q;
       if (i < m && j < m) idx[(lo + i) * ldi + lo + j] = sm.P[i][j];
     }
   }
