@@ -184,40 +184,71 @@ __global__ void __launch_bounds__(512) block_close_kernel(typename StoreT<S>::T*
 // ------------------------------------------------------------------------------------
 struct CloseU8Smem {
   uint32_t colk[2][MAXB];     // column k as replicated tag-free keys, by row (16-byte lane slots)
-  int32_t P[MAXB][MAXB];      // pred resolution
+  int32_t P[MAXB][MAXB];      // pred resolution (and the value staging area before it)
   uint8_t K[MAXB][MAXB];      // 1-based last improving k (0 = none)
 };
 
-__global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t ld, int64_t lo, int m, int32_t* idx,
-                                                             int64_t ldi, int mode, int64_t via_off) {
+// Key formats of the packed closure: u8 values << 7 with 64-step tag windows, u16 values << 6
+// with 32-step windows (INF + INF + tag < 2^16 in both).
+template <int S> struct CloseKeys;
+template <> struct CloseKeys<STORE_U8> {
+  using T = uint8_t;
+  static constexpr int TAG = 7, WIN = 64;
+  static constexpr uint32_t INF = U8_INF;
+};
+template <> struct CloseKeys<STORE_U16> {
+  using T = uint16_t;
+  static constexpr int TAG = 6, WIN = 32;
+  static constexpr uint32_t INF = U16_INF;
+};
+
+template <int S>
+__global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo,
+                                                              int m, int32_t* idx, int64_t ldi, int mode,
+                                                              int64_t via_off) {
+  using CK = CloseKeys<S>;
+  using T = typename CK::T;
+  constexpr int TAG = CK::TAG, WIN = CK::WIN, VB = int(sizeof(T));
+  constexpr uint32_t TMASK2 = ((1u << TAG) - 1u) * 0x00010001u;   // tag bits of both halves
+  constexpr uint32_t STRIP2 = ~TMASK2;
   extern __shared__ __align__(16) unsigned char smraw_cu8[];
   CloseU8Smem& sm = *reinterpret_cast<CloseU8Smem*>(smraw_cu8);
+  T (*stage)[MAXB] = reinterpret_cast<T (*)[MAXB]>(&sm.P[0][0]);   // value staging (aliases P)
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t acc[4][4];   // [row r][pair p]: columns (8w + 2p, 8w + 2p + 1)
   uint32_t kst[4][2];   // byte 2 * (p & 1) + h of kst[r][p >> 1] = cell (r, 8w + 2p + h)
   // coalesced load through the K staging area (lanes over columns), then each thread picks
   // its 4 rows x 8 bytes
-  const bool vec = m == MAXB && ((reinterpret_cast<uintptr_t>(D + lo * ld + lo) | uintptr_t(ld)) & 15) == 0;
-  if (vec) {   // full aligned block (every FW phase 1): 16-byte rows segments
-    for (int e = threadIdx.x; e < MAXB * MAXB / 16; e += blockDim.x) {
-      const int i = e >> 3, j = 16 * (e & 7);
-      *reinterpret_cast<uint4*>(&sm.K[i][j]) = *reinterpret_cast<const uint4*>(D + (lo + i) * ld + lo + j);
+  constexpr int SEG = 16 / VB;   // values per 16-byte segment
+  const bool vec = m == MAXB && ((reinterpret_cast<uintptr_t>(D + lo * ld + lo) | uintptr_t(ld * VB)) & 15) == 0;
+  if (vec) {   // full aligned block (every FW phase 1): 16-byte row segments
+    for (int e = threadIdx.x; e < MAXB * MAXB / SEG; e += blockDim.x) {
+      const int i = e / (MAXB / SEG), j = SEG * (e % (MAXB / SEG));
+      *reinterpret_cast<uint4*>(&stage[i][j]) = *reinterpret_cast<const uint4*>(D + (lo + i) * ld + lo + j);
     }
   } else {
     for (int e = threadIdx.x; e < MAXB * MAXB; e += blockDim.x) {
       const int i = e >> 7, j = e & 127;
-      sm.K[i][j] = (i < m && j < m) ? D[(lo + i) * ld + lo + j] : uint8_t(255);
+      stage[i][j] = (i < m && j < m) ? D[(lo + i) * ld + lo + j] : T(CK::INF);
     }
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < 4; r++) {
-    const uint2 v = *reinterpret_cast<const uint2*>(&sm.K[4 * l + r][8 * w]);
     kst[r][0] = kst[r][1] = 0;
-    acc[r][0] = __byte_perm(v.x, 0, 0x4140) << 7;
-    acc[r][1] = __byte_perm(v.x, 0, 0x4342) << 7;
-    acc[r][2] = __byte_perm(v.y, 0, 0x4140) << 7;
-    acc[r][3] = __byte_perm(v.y, 0, 0x4342) << 7;
+    if constexpr (VB == 1) {
+      const uint2 v = *reinterpret_cast<const uint2*>(&stage[4 * l + r][8 * w]);
+      acc[r][0] = __byte_perm(v.x, 0, 0x4140) << TAG;
+      acc[r][1] = __byte_perm(v.x, 0, 0x4342) << TAG;
+      acc[r][2] = __byte_perm(v.y, 0, 0x4140) << TAG;
+      acc[r][3] = __byte_perm(v.y, 0, 0x4342) << TAG;
+    } else {
+      const uint4 v = *reinterpret_cast<const uint4*>(&stage[4 * l + r][8 * w]);
+      acc[r][0] = v.x << TAG;
+      acc[r][1] = v.y << TAG;
+      acc[r][2] = v.z << TAG;
+      acc[r][3] = v.w << TAG;
+    }
   }
   // column KC (its low 3 bits KL static) of the owner warp into buffer BUF
 #define CU8_PUBCOL(KC, KL, BUF)                                                                  \
@@ -226,10 +257,10 @@ __global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t
       const int pp_ = ((KL) & 7) >> 1;                                                       \
       const uint32_t sel_ = ((KL) & 1) ? 0x3232u : 0x1010u; /* replicate the half */        \
       *reinterpret_cast<uint4*>(&sm.colk[BUF][4 * l]) =                                          \
-          make_uint4(__byte_perm(acc[0][pp_], 0, sel_) & 0xFF80FF80u,                            \
-                     __byte_perm(acc[1][pp_], 0, sel_) & 0xFF80FF80u,                            \
-                     __byte_perm(acc[2][pp_], 0, sel_) & 0xFF80FF80u,                            \
-                     __byte_perm(acc[3][pp_], 0, sel_) & 0xFF80FF80u);                           \
+          make_uint4(__byte_perm(acc[0][pp_], 0, sel_) & STRIP2,                                 \
+                     __byte_perm(acc[1][pp_], 0, sel_) & STRIP2,                                 \
+                     __byte_perm(acc[2][pp_], 0, sel_) & STRIP2,                                 \
+                     __byte_perm(acc[3][pp_], 0, sel_) & STRIP2);                                \
     }                                                                                            \
   } while (0)
   CU8_PUBCOL(0, 0, 0);
@@ -241,21 +272,21 @@ __global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t
         __syncthreads();
         const uint4 c4 = *reinterpret_cast<const uint4*>(&sm.colk[kk & 1][4 * l]);
         const uint32_t dik[4] = {c4.x, c4.y, c4.z, c4.w};
-        const uint32_t tag2 = uint32_t((k & 63) + 1) * 0x00010001u;
+        const uint32_t tag2 = uint32_t((k & (WIN - 1)) + 1) * 0x00010001u;
         uint32_t dkj[4];
 #pragma unroll
-        for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[kk & 3][p], k >> 2) & 0xFF80FF80u) + tag2;
+        for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[kk & 3][p], k >> 2) & STRIP2) + tag2;
 #pragma unroll
         for (int r = 0; r < 4; r++)
 #pragma unroll
           for (int p = 0; p < 4; p++) acc[r][p] = __viaddmin_u16x2(dik[r], dkj[p], acc[r][p]);
-        if ((k & 63) == 63 || k + 1 == m) {   // decode this 64-step window
-          const uint32_t wbase = uint32_t(k & ~63);
+        if ((k & (WIN - 1)) == WIN - 1 || k + 1 == m) {   // decode this tag window
+          const uint32_t wbase = uint32_t(k & ~(WIN - 1));
 #pragma unroll
           for (int r = 0; r < 4; r++) {
 #pragma unroll
             for (int p = 0; p < 4; p++) {
-              const uint32_t tg = acc[r][p] & 0x007F007Fu;
+              const uint32_t tg = acc[r][p] & TMASK2;
               acc[r][p] ^= tg;
               const uint32_t tlo = tg & 0xFF, thi = tg >> 16;
               const int sh0 = 8 * (2 * (p & 1)), sh1 = sh0 + 8;
@@ -274,20 +305,25 @@ __global__ void __launch_bounds__(512) block_close_u8_kernel(uint8_t* D, int64_t
   __syncthreads();   // every thread has read its cells and column k of the last step
 #pragma unroll
   for (int r = 0; r < 4; r++) {
-    const uint32_t v0 = __byte_perm(acc[r][0] >> 7, acc[r][1] >> 7, 0x6420);
-    const uint32_t v1 = __byte_perm(acc[r][2] >> 7, acc[r][3] >> 7, 0x6420);
-    *reinterpret_cast<uint2*>(&sm.K[4 * l + r][8 * w]) = make_uint2(v0, v1);
+    if constexpr (VB == 1) {
+      const uint32_t v0 = __byte_perm(acc[r][0] >> TAG, acc[r][1] >> TAG, 0x6420);
+      const uint32_t v1 = __byte_perm(acc[r][2] >> TAG, acc[r][3] >> TAG, 0x6420);
+      *reinterpret_cast<uint2*>(&stage[4 * l + r][8 * w]) = make_uint2(v0, v1);
+    } else {
+      *reinterpret_cast<uint4*>(&stage[4 * l + r][8 * w]) =
+          make_uint4(acc[r][0] >> TAG, acc[r][1] >> TAG, acc[r][2] >> TAG, acc[r][3] >> TAG);
+    }
   }
   __syncthreads();
   if (vec) {
-    for (int e = threadIdx.x; e < MAXB * MAXB / 16; e += blockDim.x) {
-      const int i = e >> 3, j = 16 * (e & 7);
-      *reinterpret_cast<uint4*>(D + (lo + i) * ld + lo + j) = *reinterpret_cast<const uint4*>(&sm.K[i][j]);
+    for (int e = threadIdx.x; e < MAXB * MAXB / SEG; e += blockDim.x) {
+      const int i = e / (MAXB / SEG), j = SEG * (e % (MAXB / SEG));
+      *reinterpret_cast<uint4*>(D + (lo + i) * ld + lo + j) = *reinterpret_cast<const uint4*>(&stage[i][j]);
     }
   } else {
     for (int e = threadIdx.x; e < MAXB * MAXB; e += blockDim.x) {
       const int i = e >> 7, j = e & 127;
-      if (i < m && j < m) D[(lo + i) * ld + lo + j] = sm.K[i][j];
+      if (i < m && j < m) D[(lo + i) * ld + lo + j] = stage[i][j];
     }
   }
   if (!idx) return;
@@ -389,11 +425,17 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
     }
     return 0;
   }
-  if (store == STORE_U8 && !getenv("APSP_SLOW_CLOSE")) {
-    static std::atomic<unsigned long long> attr{0};
-    APSP_CUDA_TRY(smem_optin(block_close_u8_kernel, int(sizeof(CloseU8Smem)), attr));
-    block_close_u8_kernel<<<1, 512, sizeof(CloseU8Smem), s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
-                                                              mode, via_off);
+  if ((store == STORE_U8 || store == STORE_U16) && !getenv("APSP_SLOW_CLOSE")) {
+    static std::atomic<unsigned long long> attr8{0}, attr16{0};
+    if (store == STORE_U8) {
+      APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8>, int(sizeof(CloseU8Smem)), attr8));
+      block_close_dpx_kernel<STORE_U8><<<1, 512, sizeof(CloseU8Smem), s>>>(static_cast<uint8_t*>(D), ld, lo, int(m),
+                                                                           idx, ldi, mode, via_off);
+    } else {
+      APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16>, int(sizeof(CloseU8Smem)), attr16));
+      block_close_dpx_kernel<STORE_U16><<<1, 512, sizeof(CloseU8Smem), s>>>(static_cast<uint16_t*>(D), ld, lo,
+                                                                            int(m), idx, ldi, mode, via_off);
+    }
     APSP_CUDA_TRY(cudaGetLastError());
     count_launches(1);
     return 0;
