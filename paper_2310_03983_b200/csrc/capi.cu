@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <atomic>
+#include <mutex>
 #include <vector>
 #include "../../include/apsp_b200.h"
 #include "launch.h"
@@ -96,16 +98,18 @@ int64_t tier_limit(int tier) {
 
 // Keep freed stream-ordered allocations in the device pool across calls (the default
 // release threshold of 0 returns them to the driver at every synchronisation).
+// The library's scratch comes from the device's default stream-ordered pool; keep freed blocks
+// reserved (release threshold = max) so repeated solves do not remap GBs of workspace.
 void keep_pool() {
-  static bool done[64] = {};
+  static std::atomic<bool> done[64] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev].load()) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
   }
-  done[dev] = true;
+  done[dev].store(true);
 }
 
 struct Scratch {
@@ -381,8 +385,12 @@ int fw_run(FwCtx& c, cudaStream_t s) {
   if (rc) return rc;
   cudaEvent_t evA = nullptr, evB = nullptr;
   if (c.side) {
-    APSP_CUDA_TRY(cudaEventCreateWithFlags(&evA, cudaEventDisableTiming));
-    APSP_CUDA_TRY(cudaEventCreateWithFlags(&evB, cudaEventDisableTiming));
+    cudaError_t e = cudaEventCreateWithFlags(&evA, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&evB, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      if (evA) cudaEventDestroy(evA);
+      return set_cuda_error(e, "lookahead events", __FILE__, __LINE__);
+    }
   }
   for (int64_t k0 = 0; !rc && k0 < c.m; k0 += b) {
     const int64_t k1 = k0 + b;
@@ -408,11 +416,13 @@ int fw_run(FwCtx& c, cudaStream_t s) {
   return rc;
 }
 
-// High-priority side stream of the current device (created once).
+// High-priority side stream of the current device (created once per device, thread-safe).
 cudaStream_t side_stream() {
   static cudaStream_t streams[64] = {};
+  static std::mutex mu;
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
   if (!streams[dev]) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -421,8 +431,9 @@ cudaStream_t side_stream() {
   return streams[dev];
 }
 
-// convenience for callers with a plain view (R-Kleene leaves): no lookahead; scratch laid out
-// by fw_carve (fw_scratch_bytes(m, b, es) bytes) or, if null, only a pred snapshot
+// convenience for callers with a plain view (R-Kleene leaves): lookahead when `side` is given;
+// scratch laid out by fw_carve (fw_scratch_bytes(m, b, es) bytes) or, if null, only a pred
+// snapshot
 int fw_blocked_view(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t m, int b, int mode,
                     int64_t via_off, Status* st, cudaStream_t s, int* launches, int32_t* predsnap,
                     char* scratch = nullptr, cudaStream_t side = nullptr) {
