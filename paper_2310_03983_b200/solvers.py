@@ -38,7 +38,7 @@ from .core import (
 from .minplus import DEFAULT_TILE_SIZE, _resolve_workers
 
 DEFAULT_BASE_THRESHOLD = 64
-DEFAULT_BLOCK = 0   # 0: the library picks (256 for n >= 2048, else 128)
+DEFAULT_BLOCK = 0   # 0: the library picks by n (capi.cu default_block: 128 ... 2048)
 
 
 @dataclass(frozen=True)
