@@ -151,7 +151,13 @@ int check_scan(const ScanResult& sc) {
   return 0;
 }
 
-bool bulk_store(int store) { return store == STORE_U8 || store == STORE_U16 || store == STORE_W32; }
+// Bulk-staged (pre-laid-out panel) products for this tier and inner length k.  The exact fp32
+// kernel (1 CTA / SM, compare-select) only pays off on long products: k >= 256 (measured
+// n=8192 FW 119 vs 126 ms; at k = 128 the 64 x 64 register-staged kernel is faster).
+bool bulk_store(int store, int64_t k) {
+  static const bool f32 = !getenv("APSP_F32_BULK") || atoi(getenv("APSP_F32_BULK")) != 0;
+  return store == STORE_U8 || store == STORE_U16 || store == STORE_W32 || (store == STORE_F32 && f32 && k >= 256);
+}
 
 // Candidate tiers, narrowest first.  allow_u16: the caller runs only aligned products (the
 // u16 tier exists only as bulk-staged tiles).
@@ -293,7 +299,7 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   char* Dg = c.D + (k0 * c.ld + k0) * c.es;
   char* rowp = c.D + k0 * c.ld * c.es;
   char* colp = c.D + k0 * c.es;
-  const bool nt = bulk_store(c.store) && c.p2prep;   // bulk-staged narrow tiles (prep = snapshot)
+  const bool nt = bulk_store(c.store, c.b) && c.p2prep;   // bulk-staged tiles (prep = snapshot)
   const bool snap = !nt && b > TILE_ALIGN;
   if (c.P && c.mode == IDX_PRED) {
     APSP_CUDA_TRY(cudaMemcpy2DAsync(c.predsnap, size_t(m) * 4, c.P + k0 * c.ldp, size_t(c.ldp) * 4, size_t(m) * 4,
@@ -345,7 +351,7 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   }
   c.launches += 2;
   rc = launch_minplus(c.store, q, s);
-  if (rc || !c.prep[0] || !bulk_store(c.store)) return rc;
+  if (rc || !c.prep[0] || !bulk_store(c.store, c.b)) return rc;
   char* slot = c.prep[(k0 / b) & 1];
   c.launches += 2;
   return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
@@ -369,7 +375,7 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   if (only_next >= 0) { a.only_lo = only_next; a.only_hi = only_next + c.b; }
   if (skip_next >= 0) { a.skip2_lo = skip_next; a.skip2_hi = skip_next + c.b; }
   a.status = c.st;
-  if (c.prep[0] && bulk_store(c.store)) {
+  if (c.prep[0] && bulk_store(c.store, c.b)) {
     char* slot = c.prep[(k0 / c.b) & 1];
     a.Aprep = prep_a(slot);
     a.Bprep = prep_b(slot, c.m, c.b);
@@ -689,7 +695,7 @@ struct RK {
     a.mode = mode;
     a.status = st;
     launches++;
-    if (prep && bulk_store(store) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
+    if (prep && bulk_store(store, k) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
       int rc = launch_prep_bulk(store, A, lda, B, ldb, m, n, k, prep_a(prep), prep_b(prep, m, k), s);
       if (rc) return rc;
       a.Aprep = prep_a(prep);
@@ -1108,7 +1114,7 @@ int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* 
   int rc = fw_phase1(c, 0, s);                           // diagonal block, classic order
   if (rc) return rc;
   char* rowp = D + lrow * ld * es;
-  const bool nt = bulk_store(store);
+  const bool nt = bulk_store(store, b);
   const bool snap = !nt && b > TILE_ALIGN;
   if (P) APSP_CUDA_TRY(cudaMemcpy2DAsync(sc.predsnap, size_t(N) * 4, P + lrow * ldp, size_t(ldp) * 4, size_t(N) * 4,
                                          size_t(b), cudaMemcpyDeviceToDevice, s));
@@ -1143,7 +1149,7 @@ int shard_update_impl(int tier, int64_t N, int b, int64_t row_lo, int64_t row_hi
   char* D = static_cast<char*>(Dv) + row_lo * ld * es;      // the processed row range
   int32_t* Pr = P ? P + row_lo * ldp : nullptr;
   const char* pv = static_cast<const char*>(panel);
-  const bool nt = bulk_store(store);
+  const bool nt = bulk_store(store, b);
   const bool snap = !nt && b > TILE_ALIGN;
   const bool skip = skip_lo >= 0 && skip_hi > skip_lo;
   int rc = 0;
@@ -1240,7 +1246,7 @@ int rk_shard_product_impl(int tier, const void* A, int64_t lda, const void* B, i
     a.peer_dC[r] = peer_dc[r];
     a.peer_dI[r] = peer_di[r];
   }
-  if (bulk_store(store) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {   // as RK::mp
+  if (bulk_store(store, k) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {   // as RK::mp
     int rc = launch_prep_bulk(store, A, lda, B, ldb, m, n, k, prep_a(prep), prep_b(prep, m, k), s);
     if (rc) return rc;
     a.Aprep = prep_a(prep);

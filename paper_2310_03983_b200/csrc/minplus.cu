@@ -799,6 +799,8 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
 }
 
+// RAW: plain 32-bit copies in the same layout (the exact fp32 tier); else w32 keys v << 7
+template <bool RAW>
 __global__ void prep_w32_a_kernel(const int32_t* A, int64_t lda, int64_t nch, uint32_t* Aprep) {
   const int64_t rt = blockIdx.y, c = blockIdx.x;
   const int t = threadIdx.x, r = t & 127, kb = 16 * (t >> 7);
@@ -808,9 +810,10 @@ __global__ void prep_w32_a_kernel(const int32_t* A, int64_t lda, int64_t nch, ui
 #pragma unroll
   for (int q = 0; q < 4; q++) reinterpret_cast<int4*>(v)[q] = __ldg(src + q);
 #pragma unroll
-  for (int q = 0; q < 16; q++) dst[(kb + q) * BM + r] = uint32_t(v[q]) << W32_TAG;
+  for (int q = 0; q < 16; q++) dst[(kb + q) * BM + r] = RAW ? uint32_t(v[q]) : uint32_t(v[q]) << W32_TAG;
 }
 
+template <bool RAW>
 __global__ void prep_w32_b_kernel(const int32_t* B, int64_t ldb, int64_t nch, uint32_t* Bprep) {
   const int64_t ct = blockIdx.y, c = blockIdx.x;
   const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
@@ -820,8 +823,10 @@ __global__ void prep_w32_b_kernel(const int32_t* B, int64_t ldb, int64_t nch, ui
 #pragma unroll
   for (int q = 0; q < 4; q++) {
     const int4 v = __ldg(src + q);
-    dst[q] = make_uint4((uint32_t(v.x) << W32_TAG) | tag, (uint32_t(v.y) << W32_TAG) | tag,
-                        (uint32_t(v.z) << W32_TAG) | tag, (uint32_t(v.w) << W32_TAG) | tag);
+    if constexpr (RAW) dst[q] = make_uint4(uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w));
+    else
+      dst[q] = make_uint4((uint32_t(v.x) << W32_TAG) | tag, (uint32_t(v.y) << W32_TAG) | tag,
+                          (uint32_t(v.z) << W32_TAG) | tag, (uint32_t(v.w) << W32_TAG) | tag);
   }
 }
 
@@ -831,7 +836,7 @@ size_t prep_bytes(int64_t m, int64_t n, int64_t k) {   // A keys + B keys (uint3
 
 int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
                      int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s) {
-  const size_t es = store == STORE_W32 ? 4 : store == STORE_U16 ? 2 : 1;
+  const size_t es = (store == STORE_W32 || store == STORE_F32) ? 4 : store == STORE_U16 ? 2 : 1;
   if (m % BM || n % BN || k % SUB || (lda * es) % 16 || (ldb * es) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
     return set_error(2, "panel prep needs 128-multiple m/n, 32-multiple k and 16-byte aligned panels");
@@ -845,10 +850,13 @@ int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64
     prep_nt_b_kernel<STORE_U16><<<gb, NT, 0, s>>>(static_cast<const uint16_t*>(B), ldb, nch,
                                                   static_cast<uint16_t*>(Bprep));
   } else if (store == STORE_W32) {
-    prep_w32_a_kernel<<<ga, NT, 0, s>>>(static_cast<const int32_t*>(A), lda, nch, Aprep);
-    prep_w32_b_kernel<<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep));
+    prep_w32_a_kernel<false><<<ga, NT, 0, s>>>(static_cast<const int32_t*>(A), lda, nch, Aprep);
+    prep_w32_b_kernel<false><<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep));
+  } else if (store == STORE_F32) {
+    prep_w32_a_kernel<true><<<ga, NT, 0, s>>>(static_cast<const int32_t*>(A), lda, nch, Aprep);
+    prep_w32_b_kernel<true><<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep));
   } else {
-    return set_error(2, "panel prep is for the u8 / u16 / w32 tiers");
+    return set_error(2, "panel prep is for the u8 / u16 / w32 / f32 tiers");
   }
   APSP_CUDA_TRY(cudaGetLastError());
   count_launches(2);
@@ -862,6 +870,141 @@ static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
     return dim3(unsigned(w * nt_c + (nt_r - w) * w), 1);
   }
   return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
+}
+
+// ------------------------------------------------------------------------------------
+// exact fp32 tier with pre-laid-out panels (continuous weights): compare-select per update,
+// strict < keeps the smallest k.  8 x 8 cells per thread with a 32-bit k per cell; same
+// cp.async.bulk ring as the w32 tier; 1 CTA / SM.
+// ------------------------------------------------------------------------------------
+struct SmemF32NT {
+  float As[W32_STAGES][SUB][BM];
+  float Bs[W32_STAGES][SUB][BN];
+  float Cs[BM][BN];
+  unsigned long long bar[W32_STAGES];
+};
+
+__global__ void __launch_bounds__(NT, 1) minplus_f32nt_kernel(MinplusArgs p) {
+  extern __shared__ __align__(128) unsigned char smraw_f32[];
+  SmemF32NT& sm = *reinterpret_cast<SmemF32NT*>(smraw_f32);
+  int64_t i0, j0;
+  tile_origin(p, BM, BN, i0, j0);
+  if (tile_skipped(p, i0, j0, BM, BN)) return;
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  const int64_t nch = p.k / SUB;
+  const float* Ap = reinterpret_cast<const float*>(p.Aprep) + (i0 / BM) * nch * (SUB * BM);
+  const float* Bp = static_cast<const float*>(p.Bprep) + (j0 / BN) * nch * (SUB * BN);
+  if (t == 0) {
+    for (int s = 0; s < W32_STAGES; s++) mbar_init(&sm.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t c) {
+    const int slot = int(c % W32_STAGES);
+    mbar_expect_tx(&sm.bar[slot], 2 * W32_CHUNK);
+    bulk_g2s(&sm.As[slot][0][0], Ap + c * (SUB * BM), W32_CHUNK, &sm.bar[slot]);
+    bulk_g2s(&sm.Bs[slot][0][0], Bp + c * (SUB * BN), W32_CHUNK, &sm.bar[slot]);
+  };
+  if (t == 0)
+    for (int64_t c = 0; c < W32_STAGES && c < nch; c++) issue(c);
+  {  // C tile -> smem (merged after chunk 0)
+    const int r = t >> 1;
+    const char* src = reinterpret_cast<const char*>(static_cast<const float*>(p.C) + (i0 + r) * p.ldc + j0) +
+                      256 * (t & 1);
+    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r][0]) + 256 * (t & 1));
+#pragma unroll
+    for (int q = 0; q < 16; q++)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+  float acc[8][8];
+  int32_t kid[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; r++)
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      acc[r][q] = __int_as_float(0x7f800000);
+      kid[r][q] = -1;
+    }
+  for (int64_t c = 0; c < nch; c++) {
+    const int slot = int(c % W32_STAGES);
+    mbar_wait(&sm.bar[slot], uint32_t((c / W32_STAGES) & 1));
+    const int kb = int(c) * SUB;
+#pragma unroll 4
+    for (int kk = 0; kk < SUB; kk++) {
+      float a[8], b[8];
+      *reinterpret_cast<float4*>(a) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][4 * ty]);
+      *reinterpret_cast<float4*>(a + 4) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][64 + 4 * ty]);
+      *reinterpret_cast<float4*>(b) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][4 * tx]);
+      *reinterpret_cast<float4*>(b + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][64 + 4 * tx]);
+      const int kg = kb + kk;
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const float sv = a[r] + b[q];
+          if (sv < acc[r][q]) {
+            acc[r][q] = sv;
+            kid[r][q] = kg;
+          }
+        }
+    }
+    if (c == 0) {   // the old C wins ties: strict improvement only
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const float4 w = *reinterpret_cast<const float4*>(&sm.Cs[ri][64 * h + 4 * tx]);
+          const float cv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            if (!(acc[r][4 * h + q] < cv[q])) {
+              acc[r][4 * h + q] = cv[q];
+              kid[r][4 * h + q] = -1;
+            }
+        }
+      }
+    }
+    __syncthreads();   // every warp is done with this slot
+    if (t == 0 && c + W32_STAGES < nch) issue(c + W32_STAGES);
+  }
+  bool changed = false;
+  float* Cw = static_cast<float*>(p.C);
+#pragma unroll
+  for (int r = 0; r < 8; r++) {
+    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int64_t j = j0 + 64 * h + 4 * tx;
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q < 4; q++) any |= kid[r][4 * h + q] >= 0;
+      if (!any) continue;
+      changed = true;
+#pragma unroll
+      for (int q = 0; q < 4; q++) {
+        const int32_t k = kid[r][4 * h + q];
+        if (k < 0) continue;
+        Cw[i * p.ldc + j + q] = acc[r][4 * h + q];
+        if (p.idx)
+          p.idx[i * p.ldi + j + q] =
+              (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(k) * p.ldp + j + q) : int32_t(p.inner_off + k);
+      }
+    }
+  }
+  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+}
+
+static int launch_f32nt(const MinplusArgs& a, cudaStream_t s) {
+  static std::atomic<unsigned long long> attr{0};
+  APSP_CUDA_TRY(smem_optin(minplus_f32nt_kernel, int(sizeof(SmemF32NT)), attr));
+  if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * 4) % 16)
+    return set_error(2, "bulk-staged f32 tiles need full 128 x 128 tiles and 32-multiple k");
+  minplus_f32nt_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemF32NT), s>>>(a);
+  return 0;
 }
 
 static int launch_w32nt(const MinplusArgs& a, cudaStream_t s) {
@@ -1188,8 +1331,14 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
       if (rc) return rc;
       break;
     }
-    case STORE_I32:
     case STORE_F32:
+      if (a.Aprep && a.Bprep) {
+        const int rc = launch_f32nt(a, s);
+        if (rc) return rc;
+        break;
+      }
+      [[fallthrough]];
+    case STORE_I32:
     case STORE_I64: {
       const dim3 grid = grid_for(a, EM, EN);
       if (store == STORE_I32) minplus_exact_kernel<STORE_I32><<<grid, NT, 0, s>>>(a);

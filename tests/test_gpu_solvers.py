@@ -239,6 +239,35 @@ def test_fp32_continuous_tolerance(cuda):
         assert np.allclose(d[fin], ref[fin], rtol=1e-5, atol=0), alg
 
 
+def test_fp32_continuous_bulk_kernel(cuda):
+    # block 256 / long R-Kleene products: the bulk-staged fp32 kernel (k >= 256); tolerance vs
+    # float64, and blocked FW == R-Kleene within the same tolerance; predecessors certified
+    import torch
+
+    rng = np.random.default_rng(5)
+    n = 1000
+    w = rng.uniform(1.0, 100.0, size=(n, n)).astype(np.float32)
+    w[rng.random((n, n)) > 0.02] = np.inf
+    np.fill_diagonal(w, 0.0)
+    ref = w.astype(np.float64)
+    for k in range(n):
+        np.minimum(ref, ref[:, k:k + 1] + ref[k:k + 1, :], out=ref)
+    fin = np.isfinite(ref)
+    h = torch.from_numpy(w).cuda()
+    for r in (ap.solve(h, "fw_blocked", block=256),
+              ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=256)):
+        assert r.info["tier"] == "f32"
+        d = r.distances.cpu().numpy().astype(np.float64)
+        assert (np.isfinite(d) == fin).all()
+        assert np.allclose(d[fin], ref[fin], rtol=1e-5, atol=0)
+        p = r.index.cpu().numpy()
+        # every finite off-diagonal cell's pred is a real last hop: d[i][p] + w[p][j] == d[i][j]
+        ii, jj = np.nonzero(fin & ~np.eye(n, dtype=bool))
+        pp = p[ii, jj].astype(np.int64)
+        assert (pp >= 0).all()
+        assert np.allclose(d[ii, pp] + w[pp, jj].astype(np.float64), d[ii, jj], rtol=1e-5)
+
+
 # ---- R-Kleene -------------------------------------------------------------------------------
 
 @pytest.mark.parametrize("name", ["rk_n300_t64.npz", "rk_n200_t16.npz", "rk_n130_t8.npz", "rk_n150_t1.npz"])
