@@ -301,25 +301,46 @@ def bench_single(args):
     ms_step = total_ms / args.steps
     value = n ** 3 * args.steps / (total_ms / 1e3)
 
-    # dominant kernel: FW phase-3 min-plus tile launches, timed with events on their stream
-    lib.apsp_set_profiling(1)
-    step()
-    torch.cuda.synchronize()
-    lib.apsp_set_profiling(0)
-    kl, kms = info.kernel_launches, info.kernel_ms
+    # dominant kernel: FW phase-3 min-plus tile launches, timed with CUDA events on their stream
+    # (apsp_set_profiling) in two extra, untimed solves:
+    #   * without the lookahead stream, so no phase-1/2 kernel shares the SMs with a phase-3
+    #     launch: the kernel's own rate ("achieved");
+    #   * as in the timed steps, where phase-3 launches share SMs with the lookahead stream
+    #     ("achieved_in_step", the same launches stretched by the concurrent work).
+    def profile(no_lookahead: bool):
+        if no_lookahead:
+            os.environ["APSP_NO_LOOKAHEAD"] = "1"
+        try:
+            lib.apsp_set_profiling(1)
+            step()
+            torch.cuda.synchronize()
+            lib.apsp_set_profiling(0)
+        finally:
+            os.environ.pop("APSP_NO_LOOKAHEAD", None)
+        return info.kernel_launches, info.kernel_ms
+
     N = (n + block - 1) // block * block
     # phase 3 of one pivot round updates every tile outside the pivot cross: (N-b)^2 * b
     # (3a + 3b launches together); a solve has N/b rounds
     upd_phase3 = (N // block) * (N - block) ** 2 * block
+    kl, kms = profile(no_lookahead=True)
+    kl2, kms2 = profile(no_lookahead=False)
     achieved = upd_phase3 / (kms / 1e3) if kl else None
+    achieved_step = upd_phase3 / (kms2 / 1e3) if kl2 else None
     peak = TIER_PEAK.get(tier)
     kname = f"minplus_nt_kernel<{tier}> (FW phase 3, bulk-staged)" if tier in ("u8", "u16") else \
         f"minplus_{tier}_kernel (FW phase 3)"
     roofline = {"bound": "alu", "kernel": kname, "op": TIER_OP.get(tier),
                 "achieved": achieved / 1e12 if achieved else None, "peak": peak / 1e12 if peak else None,
                 "unit": "T updates/s", "frac": (achieved / peak) if achieved and peak else None,
-                "traffic": None, "launches_per_step": kl, "kernel_share_of_step": (kms / ms_step) if kl else None,
-                "updates_per_step": upd_phase3, "kernel_ms_per_step": kms,
+                "traffic": None, "launches_per_step": kl, "kernel_ms_per_step": kms,
+                "updates_per_step": upd_phase3,
+                "measurement": "CUDA events around every phase-3 launch on its stream, one extra solve without the "
+                               "lookahead stream (no concurrent kernels)",
+                "achieved_in_step": achieved_step / 1e12 if achieved_step else None,
+                "frac_in_step": (achieved_step / peak) if achieved_step and peak else None,
+                "kernel_share_of_step": (kms2 / ms_step) if kl2 else None,
+                "step_frac": value / peak if peak else None,
                 "peak_source": "measured issue ceiling of the inner-loop instruction, profiles/r01_microbench_ops.txt"}
     # DRAM traffic of one phase-3b launch from the committed ncu --set full capture of this
     # configuration (profiles/ncu_phase3b.json, tools/ncu_summary.py); null for other configs
