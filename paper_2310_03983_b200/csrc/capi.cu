@@ -306,6 +306,34 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
                                     size_t(b), cudaMemcpyDeviceToDevice, s));
   }
   int rc = 0;
+  if (nt && c.prep[0]) {
+    // Both panels in ONE cross-list launch: the tiles of the pivot row band compute
+    // Dg (x) row panel and those of the pivot column band column panel (x) Dg, because the
+    // A / B layouts are the full column / row panels (their pivot rows / columns are Dg).  The
+    // diagonal tiles compute Dg (x) Dg, which never strictly improves a closed block.  The
+    // layouts live in this round's phase-3 slot (free: its last reader, phase 3 two rounds
+    // back, is ordered before us) and are rebuilt from the updated panels right after.
+    char* slot = c.prep[(k0 / b) & 1];
+    rc = launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
+    if (rc) return rc;
+    MinplusArgs x = minplus_args();
+    x.A = colp; x.lda = c.ld;
+    x.B = rowp; x.ldb = c.ld;
+    x.C = c.D; x.ldc = c.ld;
+    x.idx = c.P; x.ldi = c.ldp;
+    x.predB = c.predsnap; x.ldp = m;
+    x.m = m; x.n = m; x.k = b;
+    x.inner_off = c.via_off + k0;
+    x.mode = c.mode;
+    x.only_lo = k0; x.only_hi = k0 + b;
+    x.status = c.st;
+    x.Aprep = prep_a(slot);
+    x.Bprep = prep_b(slot, m, b);
+    c.launches += 5;
+    rc = launch_minplus(c.store, x, s);
+    if (rc) return rc;
+    return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
+  }
   if (snap) {
     rc = launch_copy_block(c.store, rowp, c.ld, c.rowsnap, m, b, m, s);
     if (!rc) rc = launch_copy_block(c.store, colp, c.ld, c.colsnap, b, m, b, s);
