@@ -705,6 +705,12 @@ struct RK {
   cudaStream_t s;
   char* prep = nullptr;     // narrow tiers, aligned split: bulk-copy operand layouts (half x half)
   char* leafws = nullptr;   // aligned leaves: fw_scratch_bytes(thr, 128, es)
+  // aligned split: the two independent products of each half (B and C updates) run
+  // concurrently on a second stream, with their own snapshot / layout buffers
+  char* sV2 = nullptr;
+  char* prep2 = nullptr;
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t evFork = nullptr, evJoin = nullptr;
   int launches = 0;
 
   char* at(int64_t i, int64_t j) const { return D + (i * ld + j) * es; }
@@ -712,6 +718,10 @@ struct RK {
 
   int mp(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t r0, int64_t c0, int64_t m, int64_t n,
          int64_t k, const int32_t* predB, int64_t ldpb, int64_t inner_off) {
+    return mp_on(s, prep, A, lda, B, ldb, r0, c0, m, n, k, predB, ldpb, inner_off);
+  }
+  int mp_on(cudaStream_t st_, char* prep_, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t r0,
+            int64_t c0, int64_t m, int64_t n, int64_t k, const int32_t* predB, int64_t ldpb, int64_t inner_off) {
     NvtxRange r("apsp.rkleene.product");
     MinplusArgs a = minplus_args();
     a.A = A; a.lda = lda; a.B = B; a.ldb = ldb;
@@ -723,24 +733,35 @@ struct RK {
     a.mode = mode;
     a.status = st;
     launches++;
-    if (prep && bulk_store(store, k) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
-      int rc = launch_prep_bulk(store, A, lda, B, ldb, m, n, k, prep_a(prep), prep_b(prep, m, k), s);
+    if (prep_ && bulk_store(store, k) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
+      int rc = launch_prep_bulk(store, A, lda, B, ldb, m, n, k, prep_a(prep_), prep_b(prep_, m, k), st_);
       if (rc) return rc;
-      a.Aprep = prep_a(prep);
-      a.Bprep = prep_b(prep, m, k);
+      a.Aprep = prep_a(prep_);
+      a.Bprep = prep_b(prep_, m, k);
       launches += 2;
     }
-    return timed_minplus(store, a, s);
+    return timed_minplus(store, a, st_);
   }
-  int snap_vals(int64_t r0, int64_t c0, int64_t rows, int64_t cols) {
+  int snap_vals(int64_t r0, int64_t c0, int64_t rows, int64_t cols, char* dst = nullptr) {
     launches++;
-    return launch_copy_block(store, at(r0, c0), ld, sV, sld, rows, cols, s);
+    return launch_copy_block(store, at(r0, c0), ld, dst ? dst : sV, sld, rows, cols, s);
   }
   int snap_idx(int64_t r0, int64_t c0, int64_t rows, int64_t cols) {
     if (rows <= 0 || cols <= 0) return 0;
     launches++;
     APSP_CUDA_TRY(cudaMemcpy2DAsync(sP, size_t(sld) * 4, pat(r0, c0), size_t(ld) * 4, size_t(cols) * 4, size_t(rows),
                                     cudaMemcpyDeviceToDevice, s));
+    return 0;
+  }
+  bool pairs() const { return aligned && s2 && sV2 && prep2 && evFork && evJoin; }
+  int fork() {
+    APSP_CUDA_TRY(cudaEventRecord(evFork, s));
+    APSP_CUDA_TRY(cudaStreamWaitEvent(s2, evFork, 0));
+    return 0;
+  }
+  int join() {
+    APSP_CUDA_TRY(cudaEventRecord(evJoin, s2));
+    APSP_CUDA_TRY(cudaStreamWaitEvent(s, evJoin, 0));
     return 0;
   }
 
@@ -768,23 +789,45 @@ struct RK {
     const int64_t a = mid - lo, d = hi - mid;
     const bool pred = mode == IDX_PRED;
     int rc = close(lo, mid);
-    // B <- A (x) B   (B aliased: snapshot B values and, for pred, B's pred rows)
-    if (!rc) rc = snap_vals(lo, mid, a, d);
-    if (!rc && pred) rc = snap_idx(lo, mid, a, d);
-    if (!rc) rc = mp(at(lo, lo), ld, sV, sld, lo, mid, a, d, a, pred ? sP : nullptr, sld, lo);
-    // C <- C (x) A   (C aliased as the left operand)
-    if (!rc) rc = snap_vals(mid, lo, d, a);
-    if (!rc) rc = mp(sV, sld, at(lo, lo), ld, mid, lo, d, a, a, pat(lo, lo), ld, lo);
+    if (pairs()) {
+      // B <- A (x) B and C <- C (x) A read only A and their own snapshots: run them side by side
+      if (!rc) rc = snap_vals(lo, mid, a, d);
+      if (!rc && pred) rc = snap_idx(lo, mid, a, d);
+      if (!rc) rc = snap_vals(mid, lo, d, a, sV2);
+      if (!rc) rc = fork();
+      if (!rc) rc = mp_on(s2, prep2, sV2, sld, at(lo, lo), ld, mid, lo, d, a, a, pat(lo, lo), ld, lo);
+      if (!rc) rc = mp(at(lo, lo), ld, sV, sld, lo, mid, a, d, a, pred ? sP : nullptr, sld, lo);
+      if (!rc) rc = join();
+    } else {
+      // B <- A (x) B   (B aliased: snapshot B values and, for pred, B's pred rows)
+      if (!rc) rc = snap_vals(lo, mid, a, d);
+      if (!rc && pred) rc = snap_idx(lo, mid, a, d);
+      if (!rc) rc = mp(at(lo, lo), ld, sV, sld, lo, mid, a, d, a, pred ? sP : nullptr, sld, lo);
+      // C <- C (x) A   (C aliased as the left operand)
+      if (!rc) rc = snap_vals(mid, lo, d, a);
+      if (!rc) rc = mp(sV, sld, at(lo, lo), ld, mid, lo, d, a, a, pat(lo, lo), ld, lo);
+    }
     // D <- min(D, C (x) B)
     if (!rc) rc = mp(at(mid, lo), ld, at(lo, mid), ld, mid, mid, d, d, a, pat(lo, mid), ld, lo);
     if (!rc) rc = close(mid, hi);
-    // B <- B (x) D   (B aliased as the left operand)
-    if (!rc) rc = snap_vals(lo, mid, a, d);
-    if (!rc) rc = mp(sV, sld, at(mid, mid), ld, lo, mid, a, d, d, pat(mid, mid), ld, mid);
-    // C <- D (x) C   (C aliased as the right operand)
-    if (!rc) rc = snap_vals(mid, lo, d, a);
-    if (!rc && pred) rc = snap_idx(mid, lo, d, a);
-    if (!rc) rc = mp(at(mid, mid), ld, sV, sld, mid, lo, d, a, d, pred ? sP : nullptr, sld, mid);
+    if (pairs()) {
+      // B <- B (x) D and C <- D (x) C read only D and their own snapshots
+      if (!rc) rc = snap_vals(lo, mid, a, d);
+      if (!rc) rc = snap_vals(mid, lo, d, a, sV2);
+      if (!rc && pred) rc = snap_idx(mid, lo, d, a);
+      if (!rc) rc = fork();
+      if (!rc) rc = mp_on(s2, prep2, sV, sld, at(mid, mid), ld, lo, mid, a, d, d, pat(mid, mid), ld, mid);
+      if (!rc) rc = mp(at(mid, mid), ld, sV2, sld, mid, lo, d, a, d, pred ? sP : nullptr, sld, mid);
+      if (!rc) rc = join();
+    } else {
+      // B <- B (x) D   (B aliased as the left operand)
+      if (!rc) rc = snap_vals(lo, mid, a, d);
+      if (!rc) rc = mp(sV, sld, at(mid, mid), ld, lo, mid, a, d, d, pat(mid, mid), ld, mid);
+      // C <- D (x) C   (C aliased as the right operand)
+      if (!rc) rc = snap_vals(mid, lo, d, a);
+      if (!rc && pred) rc = snap_idx(mid, lo, d, a);
+      if (!rc) rc = mp(at(mid, mid), ld, sV, sld, mid, lo, d, a, d, pred ? sP : nullptr, sld, mid);
+    }
     // A <- min(A, B (x) C)
     if (!rc) rc = mp(at(lo, mid), ld, at(mid, lo), ld, lo, lo, a, a, d, pat(mid, lo), ld, mid);
     return rc;
@@ -801,7 +844,9 @@ size_t rk_extra_bytes(int64_t N, int aligned, int thr) {
   if (!aligned) return 0;
   const int64_t h = rk_half(N, aligned);
   const int64_t leaf = std::max<int64_t>(round_up(std::min<int64_t>(thr, N), TILE_ALIGN), TILE_ALIGN);
-  return prep_bytes(h, h, h) + 512 + fw_scratch_bytes(leaf, TILE_ALIGN, 4) + 512;
+  // prep + prep2 (concurrent product pair), leaf FW scratch, second value snapshot (<= 8 B / cell)
+  return 2 * (prep_bytes(h, h, h) + 512) + fw_scratch_bytes(leaf, TILE_ALIGN, 4) + 512 +
+         size_t(h + 8) * (h + 8) * 8 + 512;
 }
 
 size_t rk_ws_bytes(int dtype, int64_t n, int aligned, int thr = 1 << 30) {
@@ -832,7 +877,26 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
   char* sV = p;
   p += size_t(h + 8) * (h + 8) * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 512;
   char* rkprep = aligned ? p : nullptr;
-  char* leafws = aligned ? p + ((prep_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
+  char* rkprep2 = aligned ? rkprep + ((prep_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
+  char* sV2 = aligned ? rkprep2 + ((prep_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
+  char* leafws = aligned ? sV2 + ((size_t(h + 8) * (h + 8) * 8 + 511) / 256) * 256 : nullptr;
+  cudaStream_t s2 = (aligned && !getenv("APSP_NO_LOOKAHEAD")) ? side_stream() : nullptr;
+  cudaEvent_t evs[2] = {nullptr, nullptr};
+  if (s2) {
+    cudaError_t e = cudaEventCreateWithFlags(&evs[0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&evs[1], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      if (evs[0]) cudaEventDestroy(evs[0]);
+      return set_cuda_error(e, "product-pair events", __FILE__, __LINE__);
+    }
+  }
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      if (e[0]) cudaEventDestroy(e[0]);
+      if (e[1]) cudaEventDestroy(e[1]);
+    }
+  } ev_guard{evs};
   Header hdr{};
   Timer tm(s);
   rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
@@ -860,6 +924,11 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
     RK rk{store, store_elem_size(store), D, N, P, idx_mode, thr, aligned != 0, sV, sP, h, &hdr_dev->status, s};
     rk.prep = rkprep;
     rk.leafws = leafws;
+    rk.prep2 = rkprep2;
+    rk.sV2 = sV2;
+    rk.s2 = s2;
+    rk.evFork = evs[0];
+    rk.evJoin = evs[1];
     if (!rc) rc = rk.close(0, N);
     bool ok = false;
     if (!rc) rc = certify(tier, store, D, N, n, n, scan, hdr_dev, hdr, s, ok);
