@@ -384,3 +384,37 @@ def test_w32_bulk_tier_wide_weights(cuda, block):
     assert r.info["tier"] == "w32"
     assert np.array_equal(r.distances.raw, want_d)
     pred_ok(raw, r.distances.raw, r.pred.raw)
+
+
+def test_graph_replay_with_changing_inputs(cuda):
+    """Repeated solves of one shape on the same buffers replay a CUDA graph (N <= 2048): every
+    call must still read the current input (different graphs, reused buffers)."""
+    import torch
+
+    n = 1500
+    dist = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    pred = torch.empty((n, n), dtype=torch.int32, device="cuda")
+    lib = ap._native.load()
+    ws_n = lib.apsp_workspace_bytes(ap._native.ALG_FW_BLOCKED, ap._native.DTYPE_I32, n, 0)
+    ws = torch.empty(ws_n, dtype=torch.uint8, device="cuda")
+    import ctypes
+
+    stream = torch.cuda.current_stream()
+    for it in range(6):                       # sightings 1 (plain), 2 (capture), 3+ (replay)
+        seed = 100 + it
+        h = ap.dense_costs(ap.GenParams(n, 0.02 if it % 2 else 0.1, 100, seed), np.int32)
+        dist.copy_(torch.from_numpy(h))
+        info = ap._native.ApspInfo()
+        st = lib.apsp_fw_blocked(ap._native.DTYPE_I32, n, dist.data_ptr(), n, pred.data_ptr(), n, 0,
+                                 ap._native.TIER_AUTO, ws.data_ptr(), ws.numel(), ctypes.c_void_p(stream.cuda_stream),
+                                 ctypes.byref(info))
+        ap._native.check(st)
+        torch.cuda.synchronize()
+        h64 = h.astype(np.int64)
+        h64[h64 == INF32] = INF_RAW
+        want, _ = orc.fw_classic(h64)
+        got = dist.cpu().numpy().astype(np.int64)
+        got[got == INF32] = INF_RAW
+        assert np.array_equal(got, want), it
+        ok, why = ap.check_pred_tree(h64, got, pred.cpu().numpy().astype(np.int64), INF_RAW)
+        assert ok, (it, why)
