@@ -520,7 +520,10 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   a.skip_row_lo = k0; a.skip_row_hi = k0 + c.b;
   a.skip_col_lo = k0; a.skip_col_hi = k0 + c.b;
   if (only_next >= 0) { a.only_lo = only_next; a.only_hi = only_next + c.b; }
-  if (skip_next >= 0) { a.skip2_lo = skip_next; a.skip2_hi = skip_next + c.b; }
+  if (skip_next >= 0) {   // 3b: disjoint from the 3a launch queued just before it
+    a.skip2_lo = skip_next; a.skip2_hi = skip_next + c.b;
+    a.pdl = getenv("APSP_NO_PDL") ? 0 : 1;
+  }
   a.status = c.st;
   if (c.prep[0] && bulk_store(c.store, c.b)) {
     char* slot = c.prep[(k0 / c.b) & 1];

@@ -393,6 +393,8 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   constexpr int CW = 4 * int(sizeof(T));          // bytes of one 4-cell C segment
   extern __shared__ __align__(128) unsigned char smraw_nt[];
   SmemNT<S>& sm = *reinterpret_cast<SmemNT<S>*>(smraw_nt);
+  // a dependent launch queued behind this kernel (pdl) may start as soon as every CTA is running
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int64_t i0, j0;
   tile_origin(p, BM, BN, i0, j0);
   if (tile_skipped(p, i0, j0, BM, BN)) return;
@@ -1024,8 +1026,23 @@ static int launch_nt(const MinplusArgs& a, cudaStream_t s) {
   const size_t es = sizeof(typename Narrow<S>::T);
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
     return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
-  if (a.npeers) minplus_nt_kernel<S, true><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
-  else minplus_nt_kernel<S, false><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
+  if (a.npeers) {
+    minplus_nt_kernel<S, true><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
+  } else if (a.pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid_for(a, BM, BN);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = sizeof(SmemNT<S>);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    APSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, minplus_nt_kernel<S, false>, a));
+  } else {
+    minplus_nt_kernel<S, false><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
+  }
   return 0;
 }
 
