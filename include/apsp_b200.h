@@ -156,6 +156,13 @@ int apsp_shard_prepare(int dtype, int tier, int64_t n, int64_t N, int64_t row0, 
                        int64_t ldh, void* D, int64_t ld, int32_t* P, int64_t ldp, void* stream);
 int apsp_shard_pivot(int tier, int64_t N, int block, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
                      int64_t k0, void* scratch, size_t scratch_bytes, void* stream);
+/* Fused variant: the pivot's row-panel product also stores the whole b x N panel (values and
+ * pred, every cell) into npeers (<= 7) peer receive slots -- address + peer_dv[r] / peer_dp[r]
+ * bytes from the local panel rows, IPC-mapped over NVLink -- replacing the NCCL broadcast with
+ * the kernel's own peer stores.  u8 / u16 tiers. */
+int apsp_shard_pivot_fused(int tier, int64_t N, int block, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
+                           int64_t k0, int npeers, const int64_t* peer_dv, const int64_t* peer_dp, void* scratch,
+                           size_t scratch_bytes, void* stream);
 /* Updates local rows [row_lo, row_hi) with the received panel; rows [skip_lo, skip_hi) (the
  * caller's own pivot rows, -1 if none) are left alone. */
 int apsp_shard_update(int tier, int64_t N, int block, int64_t row_lo, int64_t row_hi, void* D, int64_t ld, int32_t* P,

@@ -50,6 +50,7 @@ EXPORTED_SYMBOLS = (
     "apsp_shard_scratch_bytes",
     "apsp_shard_prepare",
     "apsp_shard_pivot",
+    "apsp_shard_pivot_fused",
     "apsp_shard_update",
     "apsp_shard_finish",
     "apsp_side_stream",
@@ -133,6 +134,8 @@ _SIGNATURES = {
     "apsp_shard_scratch_bytes": (_sz, [_i32, _i64, _i64, _i32]),
     "apsp_shard_prepare": (_i32, [_i32, _i32, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "apsp_shard_pivot": (_i32, [_i32, _i64, _i32, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _sz, _vp]),
+    "apsp_shard_pivot_fused": (_i32, [_i32, _i64, _i32, _vp, _i64, _vp, _i64, _i64, _i64, _i32, _vp, _vp, _vp, _sz,
+                                      _vp]),
     "apsp_shard_update": (_i32, [_i32, _i64, _i32, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64,
                                  _i64, _i64, _vp, _sz, _vp]),
     "apsp_side_stream": (_vp, []),

@@ -1325,7 +1325,8 @@ ShardScratch shard_carve(void* scratch, int64_t N, int64_t R, int b, size_t es) 
 }
 
 int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
-                     int64_t k0, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+                     int64_t k0, void* scratch, size_t scratch_bytes, cudaStream_t s, int npeers = 0,
+                     const int64_t* peer_dv = nullptr, const int64_t* peer_dp = nullptr) {
   const int store = tier_store(tier);
   if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
   const size_t es = store_elem_size(store);
@@ -1354,7 +1355,22 @@ int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* 
   a.idx = P ? P + lrow * ldp : nullptr; a.ldi = ldp;
   a.predB = sc.predsnap; a.ldp = N;
   a.m = b; a.n = N; a.k = b; a.inner_off = k0; a.mode = IDX_PRED;
-  a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
+  if (npeers > 0) {
+    // fused panel push: the product also covers the diagonal tiles (Dg (x) Dg never improves a
+    // closed block) and stores every cell of the b x N panel, values and pred, into each
+    // peer's receive slot (address + peer_dv / peer_dp bytes, IPC-mapped over NVLink)
+    if (!nt || !(store == STORE_U8 || store == STORE_U16))
+      return set_error(APSP_EINVAL, "the fused panel push needs the u8 / u16 tier");
+    if (npeers > MAX_PEERS) return set_error(APSP_EINVAL, "npeers %d outside [0, %d]", npeers, MAX_PEERS);
+    a.npeers = npeers;
+    a.push_all = 1;
+    for (int r = 0; r < npeers; r++) {
+      a.peer_dC[r] = peer_dv[r];
+      a.peer_dI[r] = peer_dp[r];
+    }
+  } else {
+    a.skip_col_lo = k0; a.skip_col_hi = k0 + b;
+  }
   if (nt) {
     if ((rc = launch_prep_bulk(store, c.D, ld, rowp, ld, b, N, b, prep_a(sc.prep), prep_b(sc.prep, b, b), s)))
       return rc;
@@ -1528,6 +1544,13 @@ int apsp_shard_update(int tier, int64_t N, int block, int64_t row_lo, int64_t ro
                       int64_t skip_lo, int64_t skip_hi, void* scratch, size_t scratch_bytes, void* stream) {
   return shard_update_impl(tier, N, block, row_lo, row_hi, D, ld, P, ldp, panel, ldpv, ppanel, ldpp, k0, skip_lo,
                            skip_hi, scratch, scratch_bytes, (cudaStream_t)stream);
+}
+
+int apsp_shard_pivot_fused(int tier, int64_t N, int block, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t lrow,
+                           int64_t k0, int npeers, const int64_t* peer_dv, const int64_t* peer_dp, void* scratch,
+                           size_t scratch_bytes, void* stream) {
+  return shard_pivot_impl(tier, N, block, D, ld, P, ldp, lrow, k0, scratch, scratch_bytes, (cudaStream_t)stream,
+                          npeers, peer_dv, peer_dp);
 }
 
 void* apsp_side_stream(void) { return side_stream(); }

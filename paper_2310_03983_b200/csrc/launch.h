@@ -54,6 +54,7 @@ struct MinplusArgs {
   int npeers;
   int64_t peer_dC[MAX_PEERS];
   int64_t peer_dI[MAX_PEERS];
+  int push_all;                   // peer-store every cell of each tile, not only improved ones
   // Programmatic dependent launch: this launch has no data dependency on the kernel queued
   // right before it on the stream (FW phase 3b after 3a: disjoint tiles), so its CTAs may start
   // while that kernel's last wave drains.

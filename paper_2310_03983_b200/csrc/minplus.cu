@@ -383,7 +383,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // it, and the LAST warp out refills the slot with chunk c + STAGES -- no warp ever waits for
 // another, only for data.  Each thread prefetches exactly its own 8 x 8 C cells (cp.async),
 // so the merge after chunk 0 needs no barrier either.
-template <int S, bool PEERS>
+// PEERS: 0 no peer stores; 1 improved segments also stored into the peer replicas (R-Kleene);
+// 2 every cell of the tile (values and pred, improved or not) stored into the peers' receive
+// slots (the FW pivot panel push).
+template <int S, int PEERS>
 __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   using NR = Narrow<S>;
   using T = typename NR::T;
@@ -544,6 +547,38 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
+      if constexpr (PEERS == 2) {   // push the whole segment; local stores only where improved
+        const int64_t j = j0 + 64 * h + 4 * tx;
+        const bool imp = (k0 | k1) != 0u;
+        changed |= imp;
+        if constexpr (sizeof(T) == 1) {
+          const uint32_t w = __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j);
+          if (imp) *dst = w;
+          for (int pr = 0; pr < p.npeers; pr++)
+            *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
+        } else {
+          const uint2 w = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
+          uint2* dst = reinterpret_cast<uint2*>(Cw + i * p.ldc + j);
+          if (imp) *dst = w;
+          for (int pr = 0; pr < p.npeers; pr++)
+            *reinterpret_cast<uint2*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
+        }
+        if (!out) continue;
+        int32_t* dst = out + i * p.ldi + j;
+        int32_t full[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          full[q] = ks[h][q] != 0u ? pv[h][q] : dst[q];   // unimproved: the current pred
+          if (ks[h][q] != 0u) dst[q] = pv[h][q];
+        }
+        for (int pr = 0; pr < p.npeers; pr++) {
+          int32_t* pd = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) pd[q] = full[q];
+        }
+        continue;
+      }
       if ((k0 | k1) == 0u) continue;
       changed = true;
       const int64_t j = j0 + 64 * h + 4 * tx;
@@ -551,14 +586,14 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
         const uint32_t w = __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
         uint32_t* dst = reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j);
         *dst = w;
-        if constexpr (PEERS)
+        if constexpr (PEERS != 0)
           for (int pr = 0; pr < p.npeers; pr++)
             *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
       } else {
         const uint2 w = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
         uint2* dst = reinterpret_cast<uint2*>(Cw + i * p.ldc + j);
         *dst = w;
-        if constexpr (PEERS)
+        if constexpr (PEERS != 0)
           for (int pr = 0; pr < p.npeers; pr++)
             *reinterpret_cast<uint2*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
       }
@@ -567,7 +602,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
         const int4 w = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
         int4* dst = reinterpret_cast<int4*>(out + i * p.ldi + j);
         *dst = w;
-        if constexpr (PEERS)
+        if constexpr (PEERS != 0)
           for (int pr = 0; pr < p.npeers; pr++)
             *reinterpret_cast<int4*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = w;
       } else {
@@ -576,13 +611,15 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
           if (ks[h][q] != 0u) {
             int32_t* dst = out + i * p.ldi + j + q;
             *dst = pv[h][q];
-            if constexpr (PEERS)
+            if constexpr (PEERS != 0)
               for (int pr = 0; pr < p.npeers; pr++)
                 *reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = pv[h][q];
           }
       }
     }
   }
+  // peer stores are ordered before anything the host signals after this kernel
+  if constexpr (PEERS != 0) __threadfence_system();
   // one flag write per warp that changed (no CTA barrier needed)
   if (p.status && p.track_changed && __any_sync(0xffffffffu, changed) && lane == 0) p.status->changed = 1;
 }
@@ -1020,14 +1057,17 @@ static int launch_w32nt(const MinplusArgs& a, cudaStream_t s) {
 
 template <int S>
 static int launch_nt(const MinplusArgs& a, cudaStream_t s) {
-  static std::atomic<unsigned long long> attr0{0}, attr1{0};
-  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, false>, int(sizeof(SmemNT<S>)), attr0));
-  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, true>, int(sizeof(SmemNT<S>)), attr1));
+  static std::atomic<unsigned long long> attr0{0}, attr1{0}, attr2{0};
+  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 0>, int(sizeof(SmemNT<S>)), attr0));
+  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 1>, int(sizeof(SmemNT<S>)), attr1));
+  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 2>, int(sizeof(SmemNT<S>)), attr2));
   const size_t es = sizeof(typename Narrow<S>::T);
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
     return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
-  if (a.npeers) {
-    minplus_nt_kernel<S, true><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
+  if (a.npeers && a.push_all) {
+    minplus_nt_kernel<S, 2><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
+  } else if (a.npeers) {
+    minplus_nt_kernel<S, 1><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
   } else if (a.pdl) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid_for(a, BM, BN);
@@ -1039,9 +1079,9 @@ static int launch_nt(const MinplusArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    APSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, minplus_nt_kernel<S, false>, a));
+    APSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, minplus_nt_kernel<S, 0>, a));
   } else {
-    minplus_nt_kernel<S, false><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
+    minplus_nt_kernel<S, 0><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
   }
   return 0;
 }
@@ -1312,6 +1352,8 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
   if (a.npeers < 0 || a.npeers > MAX_PEERS) return set_error(2, "npeers %d outside [0, %d]", a.npeers, MAX_PEERS);
   if (a.npeers && !(a.Aprep && a.Bprep && (store == STORE_U8 || store == STORE_U16 || store == STORE_W32)))
     return set_error(2, "fused peer stores need a bulk-staged tier (u8 / u16 / w32) with prepared panels");
+  if (a.push_all && !(a.npeers && (store == STORE_U8 || store == STORE_U16)))
+    return set_error(2, "whole-panel peer pushes need the u8 / u16 tier and peers");
   if (a.k <= 0) return 0;
   if (a.k > 65535) return set_error(2, "min-plus inner dimension %lld exceeds 65535", (long long)a.k);
   if (a.only_lo < a.only_hi) {

@@ -161,12 +161,17 @@ def run_rounds(ranks: list[RankState], N: int, R: int, b: int, ops, comm) -> Non
         o = k0 // R
         return o, k0 - o * R
 
+    # fused panel push (u8/u16, CudaShardOps(fused=True)): the owner's pivot kernel stores the
+    # whole panel into every peer's receive slot; the comm only adds tiny barriers
+    fused = bool(getattr(ops, "fused_for", lambda st: False)(ranks[0].state))
+    if fused:
+        comm.connect_slots(ranks, ops)
     o, lr = owner(0)
     panels = None
     for rk in ranks:
         if rk.rank == o:
-            panels = ops.pivot(rk.state, lr, 0, side=False)
-    handle = comm.bcast_start(ranks, o, panels, 0, ops)
+            panels = ops.pivot(rk.state, lr, 0, side=False, slot=0)
+    handle = comm.bcast_start(ranks, o, panels, 0, ops, fused=fused)
     for K in range(nblocks):
         k0 = K * b
         o, lr = owner(k0)
@@ -174,12 +179,14 @@ def run_rounds(ranks: list[RankState], N: int, R: int, b: int, ops, comm) -> Non
         nxt = K + 1 < nblocks
         o1, lr1 = owner(k0 + b) if nxt else (-1, -1)
         if nxt:
+            if fused:   # every rank is done with slot (K+1) % 2 (read by round K-1) before the push
+                comm.slot_barrier(ranks, ops)
             nxt_panels = None
             for rk, (pv, pp) in zip(ranks, cur):
                 if rk.rank == o1:
                     ops.update(rk.state, pv, pp, k0, lr1, lr1 + b, -1, -1)
-                    nxt_panels = ops.pivot(rk.state, lr1, k0 + b, side=True)
-            handle = comm.bcast_start(ranks, o1, nxt_panels, (K + 1) % 2, ops)
+                    nxt_panels = ops.pivot(rk.state, lr1, k0 + b, side=True, slot=(K + 1) % 2)
+            handle = comm.bcast_start(ranks, o1, nxt_panels, (K + 1) % 2, ops, fused=fused)
         for rk, (pv, pp) in zip(ranks, cur):
             lo, hi = (lr, lr + b) if rk.rank == o else (-1, -1)
             if rk.rank == o1:              # its K+1 pivot rows are done already (adjacent bands merge)
@@ -223,12 +230,15 @@ class CudaShard:
     stream: object
     pv: object = None      # two receive slots for the broadcast panel (values, pred)
     pp: object = None
+    peer_pv: list = field(default_factory=list)   # fused push: peers' receive slots [peer][slot]
+    peer_pp: list = field(default_factory=list)
+    peer_keep: list = field(default_factory=list)  # IPC mappings kept alive
 
 
 class CudaShardOps:
     """Per-rank device state and the C-ABI shard calls, on torch's current stream."""
 
-    def __init__(self, device, block: int):
+    def __init__(self, device, block: int, fused: bool = False):
         import torch
 
         self.torch = torch
@@ -236,6 +246,16 @@ class CudaShardOps:
         self.block = block
         self.lib = nat.load()
         self.side = torch.cuda.Stream(self.device, priority=-100)   # lookahead pivots
+        self.fused = fused
+
+    def fused_for(self, st) -> bool:
+        """Fused panel push (the pivot kernel's own peer stores) for the u8 / u16 tiers."""
+        return self.fused and st.tier in (nat.TIER_U8, nat.TIER_U16)
+
+    def set_peer_slots(self, st: CudaShard, peer_pv: list, peer_pp: list, keep=()) -> None:
+        if len(peer_pv) > 7:
+            raise ParameterError("the fused panel push supports at most 8 ranks")
+        st.peer_pv, st.peer_pp, st.peer_keep = list(peer_pv), list(peer_pp), list(keep)
 
     def _stream(self):
         return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
@@ -265,15 +285,28 @@ class CudaShardOps:
         nat.check(self.lib.apsp_shard_prepare(dtype_code, st.tier, n, st.N, row0, st.R, hp, n, st.D.data_ptr(),
                                               st.N, st.P.data_ptr(), st.N, self._stream()))
 
-    def pivot(self, st: CudaShard, lrow: int, k0: int, side: bool):
+    def pivot(self, st: CudaShard, lrow: int, k0: int, side: bool, slot: int | None = None):
         """Pivot of block k0 (its rows are local rows [lrow, lrow+b)); side=True runs it on the
-        high-priority side stream after the work already queued on the current stream."""
+        high-priority side stream after the work already queued on the current stream.  Fused:
+        the pivot kernel also stores the whole panel into every peer's receive slot ``slot``."""
         t = self.torch
         if side:
             self.side.wait_stream(t.cuda.current_stream(self.device))
             stream, scratch = self.side, st.stream
         else:
             stream, scratch = t.cuda.current_stream(self.device), st.scratch
+        if self.fused_for(st) and st.peer_pv and slot is not None:
+            es = st.D.element_size()
+            base_v = st.D.data_ptr() + lrow * st.N * es
+            base_p = st.P.data_ptr() + lrow * st.N * 4
+            npr = len(st.peer_pv)
+            dv = (ctypes.c_int64 * npr)(*[pv[slot].data_ptr() - base_v for pv in st.peer_pv])
+            dp = (ctypes.c_int64 * npr)(*[pp[slot].data_ptr() - base_p for pp in st.peer_pp])
+            nat.check(self.lib.apsp_shard_pivot_fused(st.tier, st.N, self.block, st.D.data_ptr(), st.N,
+                                                      st.P.data_ptr(), st.N, lrow, k0, npr, dv, dp,
+                                                      scratch.data_ptr(), scratch.numel(),
+                                                      ctypes.c_void_p(stream.cuda_stream)))
+            return st.D[lrow:lrow + self.block], st.P[lrow:lrow + self.block], (stream if side else None)
         nat.check(self.lib.apsp_shard_pivot(st.tier, st.N, self.block, st.D.data_ptr(), st.N, st.P.data_ptr(), st.N,
                                             lrow, k0, scratch.data_ptr(), scratch.numel(),
                                             ctypes.c_void_p(stream.cuda_stream)))
@@ -333,13 +366,57 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return int(t.item())
 
-    def bcast_start(self, ranks, owner: int, owner_panels, slot: int, ops):
+    def _flag(self, stream=None):
+        """A 4-byte all-reduce issued on `stream` (default: current): the collective's
+        completion orders every rank's queued work before whatever waits on the handle."""
+        t = self.torch.zeros(1, dtype=self.torch.int32, device=self.device)
+        ctx = self.torch.cuda.stream(stream) if stream is not None else _null_ctx()
+        with ctx:
+            return self.dist.all_reduce(t, group=self.group, async_op=True)
+
+    def connect_slots(self, ranks, ops):
+        """Fused panel push: map every peer's two receive slots (values, pred) into this process
+        with CUDA IPC handles exchanged over the process group."""
+        (rk,) = ranks
+        st = rk.state
+        if self.world == 1:
+            ops.set_peer_slots(st, [], [])
+            return
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        mine = [reduce_tensor(x) for x in (st.pv[0], st.pv[1], st.pp[0], st.pp[1])]
+        every = [None] * self.world
+        self.dist.all_gather_object(every, mine, group=self.group)
+        peer_pv, peer_pp, keep = [], [], []
+        for r, handles in enumerate(every):
+            if r == rk.rank:
+                continue
+            v0, v1, p0, p1 = (f(*a) for f, a in handles)
+            peer_pv.append([v0, v1])
+            peer_pp.append([p0, p1])
+            keep += [v0, v1, p0, p1]
+        ops.set_peer_slots(st, peer_pv, peer_pp, keep=keep)
+        self._flag().wait()
+
+    def slot_barrier(self, ranks, ops):
+        if self.world > 1:
+            self._flag().wait()
+
+    def bcast_start(self, ranks, owner: int, owner_panels, slot: int, ops, fused: bool = False):
         """Asynchronous broadcast of panel (values, pred) from owner into receive slot `slot`.
-        On the owner the collective is issued on the stream that produced the panel."""
+        On the owner the collective is issued on the stream that produced the panel.  Fused:
+        the owner's pivot kernel already stored the panel into every receive slot; a 4-byte
+        all-reduce after it (on the pivot's stream) is the readiness signal."""
         (rk,) = ranks
         if self.world == 1:                  # nothing to send (NCCL would still copy 5*b*N bytes)
             pv, pp, _ = owner_panels
             return [], [(pv, pp)], True
+        if fused:
+            if rk.rank == owner:
+                pv, pp, stream = owner_panels
+            else:
+                (pv, pp), stream = ops.recv_buffers(rk.state, slot), None
+            return [self._flag(stream)], [(pv, pp)], rk.rank == owner
         if rk.rank == owner:
             pv, pp, stream = owner_panels
         else:
@@ -369,10 +446,21 @@ class _null_ctx:
 
 
 class EmulatedComm:
-    """All ranks in this process on one device: every rank reads the owner's panel directly."""
+    """All ranks in this process on one device: every rank reads the owner's panel directly
+    (fused: each rank reads its own receive slot, filled by the owner's pivot kernel)."""
 
-    def bcast_start(self, ranks, owner: int, owner_panels, slot: int, ops):
+    def connect_slots(self, ranks, ops):
+        for rk in ranks:
+            others = [o.state for o in ranks if o is not rk]
+            ops.set_peer_slots(rk.state, [o.pv for o in others], [o.pp for o in others])
+
+    def slot_barrier(self, ranks, ops):
+        return None   # one process, stream order: the side-stream pivot follows all queued updates
+
+    def bcast_start(self, ranks, owner: int, owner_panels, slot: int, ops, fused: bool = False):
         pv, pp, _ = owner_panels
+        if fused:
+            return [(pv, pp) if rk.rank == owner else ops.recv_buffers(rk.state, slot) for rk in ranks]
         return [(pv, pp) for _ in ranks]
 
     def bcast_wait(self, handle, ranks, ops):
@@ -392,7 +480,8 @@ class ShardedResult:
     info: dict = field(default_factory=dict)
 
 
-def fw_blocked_sharded(h_local, n: int, *, comm: TorchComm, block: int = 256, tier=None, ops=None):
+def fw_blocked_sharded(h_local, n: int, *, comm: TorchComm, block: int = 256, tier=None, ops=None,
+                       fused: bool = True):
     """SPMD entry: this rank's rows of the input (torch CUDA tensor, rows x n) -> its rows of
     dist / pred.  Must be called by every rank of ``comm`` with the same n and block."""
     import torch
@@ -403,7 +492,7 @@ def fw_blocked_sharded(h_local, n: int, *, comm: TorchComm, block: int = 256, ti
     rows_valid = max(0, min(R, n - row0))
     if h_local is not None and tuple(h_local.shape) != (rows_valid, n):
         raise ParameterError(f"rank {rank} expects {rows_valid} x {n} input rows, got {tuple(h_local.shape)}")
-    ops = ops or CudaShardOps(h_local.device, block)
+    ops = ops or CudaShardOps(h_local.device, block, fused=fused)
     rs = RankState(rank, row0, rows_valid)
     dtype_code = _dtype_of(h_local)
     t0 = time.perf_counter()
@@ -418,7 +507,7 @@ def fw_blocked_sharded(h_local, n: int, *, comm: TorchComm, block: int = 256, ti
                           "block": block, "host_s": time.perf_counter() - t0})
 
 
-def fw_blocked_emulated(h, world: int, *, block: int = 256, tier=None):
+def fw_blocked_emulated(h, world: int, *, block: int = 256, tier=None, fused: bool = False):
     """All ``world`` ranks of the row-band schedule in this process on h's device (sequential;
     no rank waits on another).  Returns full (dist, pred) tensors.  Used to test the sharded
     path on one GPU."""
@@ -426,7 +515,7 @@ def fw_blocked_emulated(h, world: int, *, block: int = 256, tier=None):
 
     n = h.shape[0]
     N, R = layout(n, world, block)
-    ops = CudaShardOps(h.device, block)
+    ops = CudaShardOps(h.device, block, fused=fused)
     ranks, hs = [], []
     for r in range(world):
         row0 = r * R
@@ -473,7 +562,7 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
         print(f"[bench] rank0 generated rows {row0}..{row0 + rv} of n={n} in {time.perf_counter() - t:.1f}s",
               file=__import__("sys").stderr, flush=True)
     h = torch.from_numpy(h_np).to(dev)
-    ops = CudaShardOps(dev, block)
+    ops = CudaShardOps(dev, block, fused=os.environ.get("APSP_FUSED_PUSH", "1") != "0")
     lib = ops.lib
 
     def step():

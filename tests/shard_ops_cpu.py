@@ -73,7 +73,7 @@ class CpuShardOps:
         C[imp] = best[imp]
         PC[imp] = newp[imp]
 
-    def pivot(self, st, lrow, k0, side=False):
+    def pivot(self, st, lrow, k0, side=False, slot=None):
         b = self.block
         D, P = st.D.numpy(), st.P.numpy()
         G = D[lrow:lrow + b, k0:k0 + b]

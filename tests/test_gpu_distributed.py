@@ -174,3 +174,63 @@ def test_rkleene_fused_ipc_two_processes_one_gpu(cuda):
         p.join(timeout=300)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5)
+
+
+@pytest.mark.parametrize("n,world,block", [(1000, 3, 128), (2048, 4, 256), (777, 2, 256)])
+def test_fused_panel_push_emulated(cuda, n, world, block):
+    """FW fused panel push: the owner's pivot kernel stores the whole panel into every other
+    rank's receive slot; receivers read only their own slots."""
+    from paper_2310_03983_b200.distributed import fw_blocked_emulated
+
+    h = torch.from_numpy(ap.dense_costs(ap.GenParams(n, 0.05, 100, n + 5), np.int32)).cuda()
+    single = ap.solve(h, "fw_blocked", block=block)
+    d, p, info = fw_blocked_emulated(h, world, block=block, fused=True)
+    assert info["tier"] == single.info["tier"]
+    assert torch.equal(d, single.distances) and torch.equal(p, single.index)
+
+
+def _fw_ipc_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2310_03983_b200.distributed import TorchComm, fw_blocked_sharded, layout
+
+        n, block = 1100, 128
+        h = torch.from_numpy(ap.dense_costs(ap.GenParams(n, 0.05, 100, 91), np.int32)).cuda()
+        N, R = layout(n, world, block)
+        row0 = rank * R
+        rv = max(0, min(R, n - row0))
+        r = fw_blocked_sharded(h[row0:row0 + rv].contiguous(), n, comm=TorchComm(torch.device("cuda", 0)),
+                               block=block, fused=True)
+        torch.cuda.synchronize()
+        single = ap.solve(h, "fw_blocked", block=block)
+        ok = bool(torch.equal(r.distances, single.distances[row0:row0 + rv]) and
+                  torch.equal(r.pred, single.index[row0:row0 + rv]))
+        out.put((rank, ok))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_panel_push_ipc_two_processes_one_gpu(cuda):
+    """Two processes, one GPU: receive slots mapped with CUDA IPC, panels pushed by the pivot
+    kernel's peer stores, gloo all-reduces as the slot / readiness barriers (host-side)."""
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fw_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+    assert all(p.exitcode == 0 for p in procs)
+    res = dict(q.get(timeout=5) for _ in range(2))
+    assert res[0] and res[1]
