@@ -6,8 +6,10 @@ pivot block never straddles ranks).  Per pivot block [k0, k0+b), owned by rank o
 
   1. o      apsp_shard_pivot: close the b x b diagonal block (classic order), then
             row panel <- Dg (x) row panel                      (both on o's rows only)
-  2. all    broadcast the b x N row panel -- values and predecessors -- from o (NCCL over
-            NVLink/NVSwitch; ~b*N*(1+4) bytes per round)
+  2. all    the b x N row panel -- values and predecessors, ~b*N*(1+4) bytes per round --
+            reaches every rank: fused (u8/u16): the owner's pivot kernel stores it into each
+            peer's receive slot over NVLink (CUDA IPC), with 4-byte all-reduces as barriers;
+            otherwise an NCCL broadcast
   3. all    apsp_shard_update: column panel <- colpanel (x) Dg (Dg = columns k0.. of the
             received panel), then phase 3 on the local rows with the received panel as B
 
