@@ -154,9 +154,10 @@ int check_scan(const ScanResult& sc) {
 // Bulk-staged (pre-laid-out panel) products for this tier and inner length k.  The exact fp32
 // kernel (1 CTA / SM, compare-select) only pays off on long products: k >= 256 (measured
 // n=8192 FW 119 vs 126 ms; at k = 128 the 64 x 64 register-staged kernel is faster).
+int64_t kF32MinK = getenv("APSP_F32_MINK") ? atoll(getenv("APSP_F32_MINK")) : 128;
 bool bulk_store(int store, int64_t k) {
   static const bool f32 = !getenv("APSP_F32_BULK") || atoi(getenv("APSP_F32_BULK")) != 0;
-  return store == STORE_U8 || store == STORE_U16 || store == STORE_W32 || (store == STORE_F32 && f32 && k >= 256);
+  return store == STORE_U8 || store == STORE_U16 || store == STORE_W32 || (store == STORE_F32 && f32 && k >= kF32MinK);
 }
 
 // Candidate tiers, narrowest first.  allow_u16: the caller runs only aligned products (the

@@ -14,6 +14,7 @@
 // tag survives only on strict improvement (minplus.py:80-82,128-133).  Every 32 k-steps the
 // tags are decoded into a 16-bit k index per cell and cleared.
 #include <cstdlib>
+#include <string>
 #include "launch.h"
 
 namespace apsp {
@@ -29,16 +30,17 @@ constexpr int kU8Unroll = APSP_U8_UNROLL;
 // (band width w tiles): first the w full tile rows, then the remaining rows of the w columns.
 __device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn, int64_t& i0, int64_t& j0) {
   if (p.only_lo < p.only_hi) {   // tile counts fit 32 bits: 32-bit division (a 64-bit one is ~100 instr)
-    const int w = int((p.only_hi - p.only_lo) / bm), lo_t = int(p.only_lo / bm);
+    const int wr = int((p.only_hi - p.only_lo) / bm), lo_r = int(p.only_lo / bm);   // row band, in row tiles
+    const int wc = int((p.only_hi - p.only_lo) / bn), lo_c = int(p.only_lo / bn);   // col band, in col tiles
     const int nt_c = int((p.n + bn - 1) / bn);
     const int id = int(blockIdx.x);
-    if (id < w * nt_c) {
-      i0 = int64_t(lo_t + id / nt_c) * bm;
+    if (id < wr * nt_c) {
+      i0 = int64_t(lo_r + id / nt_c) * bm;
       j0 = int64_t(id % nt_c) * bn;
     } else {
-      const int id2 = id - w * nt_c, rr = id2 / w, cc = id2 % w;
-      i0 = int64_t(rr < lo_t ? rr : rr + w) * bm;
-      j0 = int64_t(lo_t + cc) * bn;
+      const int id2 = id - wr * nt_c, rr = id2 / wc, cc = id2 % wc;
+      i0 = int64_t(rr < lo_r ? rr : rr + wr) * bm;
+      j0 = int64_t(lo_c + cc) * bn;
     }
   } else {
     i0 = int64_t(blockIdx.y) * bm;
@@ -869,6 +871,192 @@ __global__ void prep_w32_b_kernel(const int32_t* B, int64_t ldb, int64_t nch, ui
   }
 }
 
+// 3-input fp32 min (FMNMX3 on sm_100)
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// ------------------------------------------------------------------------------------
+// exact fp32 tier, deferred argmin: per 32-k chunk the min runs as FADD + FMNMX3 (1.5 instr per
+// update, no compare-select); cells whose value improved in the chunk then rescan that chunk
+// -- still in shared memory -- for the FIRST k whose (bitwise identical) sum equals the new min.
+// Strict improvement across chunks keeps the older k on ties, so the result equals the
+// compare-select kernel exactly.  The rescan is a per-lane loop over the improved cells
+// (targets and k staged in shared memory, so no dynamic register indexing).
+// Tile 128 x 64, 256 threads, 4 x 8 cells each; 1 CTA / SM.
+// ------------------------------------------------------------------------------------
+constexpr int DM_BN = 64, DM_STAGES = 2;
+constexpr uint32_t DM_CHUNK_A = SUB * BM * 4, DM_CHUNK_B = SUB * DM_BN * 4;
+struct SmemF32DM {   // 96 KB: 2 CTAs / SM
+  float As[DM_STAGES][SUB][BM];
+  float Bs[DM_STAGES][SUB][DM_BN];
+  float Cs[BM * DM_BN];         // the old C tile; after the chunk-0 merge, the rescan targets
+  uint16_t kid[NT][32];         // 0-based k of the last strict improvement, 0xFFFF = none
+  unsigned long long bar[DM_STAGES];
+  unsigned int done[DM_STAGES];  // warps finished with the slot's chunk
+};
+// rescan target slot of (thread, cell): swizzled so the 32 lanes hit 32 banks for a common cell
+__device__ __forceinline__ int dm_tgt(int t, int cell) { return t * 32 + ((cell + t) & 31); }
+
+__global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
+  extern __shared__ __align__(128) unsigned char smraw_dm[];
+  SmemF32DM& sm = *reinterpret_cast<SmemF32DM*>(smraw_dm);
+  int64_t i0, j0;
+  tile_origin(p, BM, DM_BN, i0, j0);
+  if (tile_skipped(p, i0, j0, BM, DM_BN)) return;
+  const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
+  const int64_t nch = p.k / SUB;
+  const float* Ap = reinterpret_cast<const float*>(p.Aprep) + (i0 / BM) * nch * (SUB * BM);
+  const float* Bp = static_cast<const float*>(p.Bprep) + (j0 / DM_BN) * nch * (SUB * DM_BN);
+  auto issue = [&](int64_t c) {
+    const int slot = int(c % DM_STAGES);
+    mbar_expect_tx(&sm.bar[slot], DM_CHUNK_A + DM_CHUNK_B);
+    bulk_g2s(&sm.As[slot][0][0], Ap + c * (SUB * BM), DM_CHUNK_A, &sm.bar[slot]);
+    bulk_g2s(&sm.Bs[slot][0][0], Bp + c * (SUB * DM_BN), DM_CHUNK_B, &sm.bar[slot]);
+  };
+  if (t == 0) {
+    for (int s = 0; s < DM_STAGES; s++) {
+      mbar_init(&sm.bar[s], 1);
+      sm.done[s] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int64_t c = 0; c < DM_STAGES && c < nch; c++) issue(c);
+  }
+  __syncthreads();
+  {  // C tile -> smem (merged after chunk 0): row t >> 1, half (t & 1) of 64 floats
+    const int r = t >> 1;
+    const char* src = reinterpret_cast<const char*>(static_cast<const float*>(p.C) + (i0 + r) * p.ldc + j0) +
+                      128 * (t & 1);
+    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r * DM_BN]) + 128 * (t & 1));
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
+    asm volatile("cp.async.commit_group;\n" ::);
+  }
+#pragma unroll
+  for (int c = 0; c < 32; c++) sm.kid[t][c] = 0xFFFF;
+  float acc[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; r++)
+#pragma unroll
+    for (int q = 0; q < 8; q++) acc[r][q] = __int_as_float(0x7f800000);
+  for (int64_t c = 0; c < nch; c++) {
+    const int slot = int(c % DM_STAGES);
+    mbar_wait(&sm.bar[slot], uint32_t((c / DM_STAGES) & 1));
+    float old[4][8];
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+#pragma unroll
+      for (int q = 0; q < 8; q++) old[r][q] = acc[r][q];
+#pragma unroll 4
+    for (int kk = 0; kk < SUB; kk += 2) {
+      float a0[4], a1[4], b0[8], b1[8];
+      *reinterpret_cast<float4*>(a0) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][4 * ty]);
+      *reinterpret_cast<float4*>(a1) = *reinterpret_cast<const float4*>(&sm.As[slot][kk + 1][4 * ty]);
+      *reinterpret_cast<float4*>(b0) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][8 * tx]);
+      *reinterpret_cast<float4*>(b0 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][8 * tx + 4]);
+      *reinterpret_cast<float4*>(b1) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][8 * tx]);
+      *reinterpret_cast<float4*>(b1 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][8 * tx + 4]);
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int q = 0; q < 8; q++) acc[r][q] = fmin3(acc[r][q], a0[r] + b0[q], a1[r] + b1[q]);
+    }
+    uint32_t mask = 0;
+    if (c == 0) {   // improvement is against the old C (which wins ties)
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const float4 w0 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 8 * tx]);
+        const float4 w1 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 8 * tx + 4]);
+        const float cv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          if (acc[r][q] < cv[q]) mask |= 1u << (8 * r + q);
+          else acc[r][q] = cv[q];
+        }
+      }
+      __syncthreads();   // the C tile is consumed: its space now holds the rescan targets
+    } else {
+#pragma unroll
+      for (int r = 0; r < 4; r++)
+#pragma unroll
+        for (int q = 0; q < 8; q++)
+          if (acc[r][q] < old[r][q]) mask |= 1u << (8 * r + q);
+    }
+    if (__any_sync(0xffffffffu, mask != 0u)) {
+      if (mask) {
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+          for (int q = 0; q < 8; q++) sm.Cs[dm_tgt(t, 8 * r + q)] = acc[r][q];
+      }
+      const int kb = int(c) * SUB;
+      while (mask) {   // per-lane loop over this lane's improved cells
+        const int cell = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int row = 4 * ty + (cell >> 3), col = 8 * tx + (cell & 7);
+        const float target = sm.Cs[dm_tgt(t, cell)];
+        int found = 0;
+        for (int kk = 0; kk < SUB; kk++)
+          if (sm.As[slot][kk][row] + sm.Bs[slot][kk][col] == target) {
+            found = kk;
+            break;
+          }
+        sm.kid[t][cell] = uint16_t(kb + found);
+      }
+    }
+    __syncwarp();
+    if ((t & 31) == 0) {   // count this warp out of the slot; the last one refills it
+      __threadfence_block();
+      if (atomicAdd(&sm.done[slot], 1u) == NT / 32 - 1) {
+        __threadfence_block();
+        sm.done[slot] = 0;
+        if (c + DM_STAGES < nch) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(c + DM_STAGES);
+        }
+      }
+    }
+  }
+  bool changed = false;
+  float* Cw = static_cast<float*>(p.C);
+#pragma unroll
+  for (int r = 0; r < 4; r++) {
+    const int64_t i = i0 + 4 * ty + r;
+#pragma unroll
+    for (int q = 0; q < 8; q++) {
+      const uint32_t k = sm.kid[t][8 * r + q];
+      if (k == 0xFFFFu) continue;
+      changed = true;
+      const int64_t j = j0 + 8 * tx + q;
+      Cw[i * p.ldc + j] = acc[r][q];
+      if (p.idx)
+        p.idx[i * p.ldi + j] =
+            (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(k) * p.ldp + j) : int32_t(p.inner_off + k);
+    }
+  }
+  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+}
+
+// B (k x n) fp32 -> [n/64][k/32][32][64] for the deferred-argmin kernel
+__global__ void prep_f32_b64_kernel(const float* B, int64_t ldb, int64_t nch, float* Bprep) {
+  const int64_t ct = blockIdx.y, c = blockIdx.x;
+  const int t = threadIdx.x, kk = t >> 3, cb = 8 * (t & 7);
+  const float4* src = reinterpret_cast<const float4*>(B + (c * SUB + kk) * ldb + ct * DM_BN + cb);
+  float4* dst = reinterpret_cast<float4*>(Bprep + (ct * nch + c) * (SUB * DM_BN) + kk * DM_BN + cb);
+  dst[0] = __ldg(src);
+  dst[1] = __ldg(src + 1);
+}
+
+bool f32_deferred() {
+  static const bool on = !getenv("APSP_F32_KERNEL") || std::string(getenv("APSP_F32_KERNEL")) != "nt";
+  return on;
+}
+
 size_t prep_bytes(int64_t m, int64_t n, int64_t k) {   // A keys + B keys (uint32 B keys for w32)
   return ((size_t(m) * k * 4 + 255) / 256) * 256 + size_t(k) * n * 4 + 256;
 }
@@ -893,7 +1081,12 @@ int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64
     prep_w32_b_kernel<false><<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep));
   } else if (store == STORE_F32) {
     prep_w32_a_kernel<true><<<ga, NT, 0, s>>>(static_cast<const int32_t*>(A), lda, nch, Aprep);
-    prep_w32_b_kernel<true><<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep));
+    if (f32_deferred())
+      prep_f32_b64_kernel<<<dim3(unsigned(nch), unsigned(n / DM_BN)), NT, 0, s>>>(static_cast<const float*>(B), ldb,
+                                                                                  nch, static_cast<float*>(Bprep));
+    else
+      prep_w32_b_kernel<true><<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch,
+                                                 static_cast<uint32_t*>(Bprep));
   } else {
     return set_error(2, "panel prep is for the u8 / u16 / w32 / f32 tiers");
   }
@@ -903,10 +1096,10 @@ int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64
 }
 
 static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
-  if (a.only_lo < a.only_hi) {
-    const int64_t w = (a.only_hi - a.only_lo) / bm;
+  if (a.only_lo < a.only_hi) {   // the cross of rows and columns [lo, hi) (tile_origin's enumeration)
+    const int64_t wr = (a.only_hi - a.only_lo) / bm, wc = (a.only_hi - a.only_lo) / bn;
     const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
-    return dim3(unsigned(w * nt_c + (nt_r - w) * w), 1);
+    return dim3(unsigned(wr * nt_c + (nt_r - wr) * wc), 1);
   }
   return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
 }
@@ -1035,6 +1228,16 @@ __global__ void __launch_bounds__(NT, 1) minplus_f32nt_kernel(MinplusArgs p) {
     }
   }
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+}
+
+static int launch_f32dm(const MinplusArgs& a, cudaStream_t s) {
+  static std::atomic<unsigned long long> attr{0};
+  APSP_CUDA_TRY(smem_optin(minplus_f32dm_kernel, int(sizeof(SmemF32DM)), attr));
+  if (a.m % BM || a.n % DM_BN || a.k % SUB || a.k > 65535 || (reinterpret_cast<uintptr_t>(a.C) & 15) ||
+      (a.ldc * 4) % 16)
+    return set_error(2, "deferred-argmin f32 tiles need 128 x 64 tiles and 32-multiple k");
+  minplus_f32dm_kernel<<<grid_for(a, BM, DM_BN), NT, sizeof(SmemF32DM), s>>>(a);
+  return 0;
 }
 
 static int launch_f32nt(const MinplusArgs& a, cudaStream_t s) {
@@ -1392,7 +1595,7 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
     }
     case STORE_F32:
       if (a.Aprep && a.Bprep) {
-        const int rc = launch_f32nt(a, s);
+        const int rc = f32_deferred() ? launch_f32dm(a, s) : launch_f32nt(a, s);
         if (rc) return rc;
         break;
       }
