@@ -418,3 +418,21 @@ def test_graph_replay_with_changing_inputs(cuda):
         assert np.array_equal(got, want), it
         ok, why = ap.check_pred_tree(h64, got, pred.cpu().numpy().astype(np.int64), INF_RAW)
         assert ok, (it, why)
+
+
+def test_results_independent_of_tile_size_and_workers(cuda):
+    """Reference determinism-under-parallelism criterion (test_solvers.py:195-210,
+    test_acceptance.py:53-71): identical dist / pred / via for every tile_size and worker count
+    (both are accepted and validated; neither changes the GPU grid)."""
+    raw = random_graph_raw(300, 0.08, 50, 17)
+    h = ap.CostMatrix(raw)
+    base_f = ap.fw_classic(h)
+    base_r = ap.rkleene(h, base_threshold=16)
+    for tile_size in (1, 8, 16, 64, 1024):
+        for workers in (1, 2, 3, 4, None):
+            f = ap.fw_classic(h, tile_size=tile_size, workers=workers)
+            assert np.array_equal(f.distances.raw, base_f.distances.raw)
+            assert np.array_equal(f.pred.raw, base_f.pred.raw)
+    for tile_size in (1, 64):
+        r = ap.rkleene(h, base_threshold=16, tile_size=tile_size, workers=2)
+        assert np.array_equal(r.via.raw, base_r.via.raw)
