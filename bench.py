@@ -238,6 +238,8 @@ def main():
     ap_.add_argument("--ref-step-s", type=float, default=8.0)
     ap_.add_argument("--block", type=int, default=BLOCK, help="pivot block (multiple of 128; 0 = library default)")
     ap_.add_argument("--sharded", action="store_true", help="use the multi-GPU row-band path even at N=1")
+    ap_.add_argument("--alg", default="fw", choices=["fw", "rkleene"],
+                     help="multi-GPU leg: row-band FW (default) or replicated R-Kleene with row-band products")
     args = ap_.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":

@@ -558,17 +558,29 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
     rv = max(0, min(R, n - row0))
     from .graphgen import GenParams, dense_costs
 
+    rk = getattr(args, "alg", "fw") == "rkleene"
+    fused = os.environ.get("APSP_FUSED_PUSH", "1") != "0"
+    if rk:   # replicated matrix: every rank generates (and holds) the whole input
+        row0, rv = 0, n
     t = time.perf_counter()
     h_np = dense_costs(GenParams(n, args.rho, 100, 7 + n), np.int32, rows=(row0, row0 + rv))
     if rank == 0:
         print(f"[bench] rank0 generated rows {row0}..{row0 + rv} of n={n} in {time.perf_counter() - t:.1f}s",
               file=__import__("sys").stderr, flush=True)
     h = torch.from_numpy(h_np).to(dev)
-    ops = CudaShardOps(dev, block, fused=os.environ.get("APSP_FUSED_PUSH", "1") != "0")
-    lib = ops.lib
+    if rk:
+        from .distributed_rk import CudaRkOps, rkleene_sharded
 
-    def step():
-        return fw_blocked_sharded(h, n, comm=comm, block=block, ops=ops)
+        ops = CudaRkOps(dev, fused=fused)
+
+        def step():
+            return rkleene_sharded(h, n, comm=comm, base_threshold=2048, ops=ops)
+    else:
+        ops = CudaShardOps(dev, block, fused=fused)
+
+        def step():
+            return fw_blocked_sharded(h, n, comm=comm, block=block, ops=ops)
+    lib = ops.lib
 
     for _ in range(args.warmup):
         res = step()
@@ -600,22 +612,32 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
         t = time.perf_counter()
         for _ in range(args.steps):
             hd = hin.to(dev, non_blocking=True)
-            r = fw_blocked_sharded(hd, n, comm=comm, block=block, ops=ops)
-            dout.copy_(r.distances, non_blocking=True)
-            pout.copy_(r.pred, non_blocking=True)
+            if rk:
+                r = rkleene_sharded(hd, n, comm=comm, base_threshold=2048, ops=ops)
+            else:
+                r = fw_blocked_sharded(hd, n, comm=comm, block=block, ops=ops)
+            if not rk or rank == 0:   # R-Kleene: every replica holds the result; rank 0 reads it
+                dout.copy_(r.distances, non_blocking=True)
+                pout.copy_(r.pred, non_blocking=True)
             torch.cuda.synchronize()
         dist.barrier()
         dt = torch.tensor([time.perf_counter() - t], dtype=torch.float64, device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": n ** 3 * args.steps / float(dt.item()), "unit": unit,
-               "h2d_bytes_per_step": n * n * 4, "d2h_bytes_per_step": 2 * n * n * 4,
-               "api": "paper_2310_03983_b200.distributed.fw_blocked_sharded from pinned host rows"}
+               "h2d_bytes_per_step": n * n * 4 * (world if rk else 1), "d2h_bytes_per_step": 2 * n * n * 4,
+               "api": ("paper_2310_03983_b200.distributed_rk.rkleene_sharded from pinned host matrices" if rk else
+                       "paper_2310_03983_b200.distributed.fw_blocked_sharded from pinned host rows")}
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": f"tier {res.info['tier']}; int32 in/out",
                 "data": "synthetic (reference generator, bit-identical to apsp.generate)",
-                "config": config(n, args.rho, world) | {"block": block, "rows_per_rank": R},
+                "config": config(n, args.rho, world) | (
+                    {"workload": f"aligned R-Kleene APSP (replicated matrix, row-band products), distances+"
+                                 f"predecessors, n={n}, generator graph GenParams(n, rho={args.rho}, alpha=100, "
+                                 f"seed=7+n), int32 in/out", "alg": "rkleene", "base_threshold": 2048,
+                     "fused_exchange": fused} if rk else
+                    {"block": block, "rows_per_rank": R, "fused_exchange": fused}),
                 "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e, "cpu_baseline": None,
                 "tier": res.info["tier"]}
         print(json.dumps(line), flush=True)
