@@ -13,6 +13,7 @@
 // keys is the lexicographic (value, smallest k) min; an untagged (old) key wins ties, so a
 // tag survives only on strict improvement (minplus.py:80-82,128-133).  Every 32 k-steps the
 // tags are decoded into a 16-bit k index per cell and cleared.
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 #include "launch.h"
@@ -628,10 +629,10 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
 
 // panel layout kernels (one CTA per (tile, chunk); thread = one row x 16 k, or one k x 16 columns)
 template <int S>
-__global__ void prep_nt_a_kernel(const typename Narrow<S>::T* A, int64_t lda, int64_t nch, uint32_t* Aprep) {
+__device__ __forceinline__ void prep_nt_a_body(const typename Narrow<S>::T* A, int64_t lda, int64_t nch,
+                                               uint32_t* Aprep, int64_t rt, int64_t c) {
   using T = typename Narrow<S>::T;
   constexpr int TAG = Narrow<S>::TAG;
-  const int64_t rt = blockIdx.y, c = blockIdx.x;
   const int t = threadIdx.x, r = t & 127, kb = 16 * (t >> 7);
   const T* src = A + (rt * BM + r) * lda + c * SUB + kb;
   uint32_t* dst = Aprep + (rt * nch + c) * (SUB * BM);
@@ -643,10 +644,10 @@ __global__ void prep_nt_a_kernel(const typename Narrow<S>::T* A, int64_t lda, in
 }
 
 template <int S>
-__global__ void prep_nt_b_kernel(const typename Narrow<S>::T* B, int64_t ldb, int64_t nch, uint16_t* Bprep) {
+__device__ __forceinline__ void prep_nt_b_body(const typename Narrow<S>::T* B, int64_t ldb, int64_t nch,
+                                               uint16_t* Bprep, int64_t ct, int64_t c) {
   using T = typename Narrow<S>::T;
   constexpr int TAG = Narrow<S>::TAG, WIN = Narrow<S>::WIN;
-  const int64_t ct = blockIdx.y, c = blockIdx.x;
   const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
   const T* src = B + (c * SUB + kk) * ldb + ct * BN + cb;
   T v[16];
@@ -842,8 +843,8 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
 
 // RAW: plain 32-bit copies in the same layout (the exact fp32 tier); else w32 keys v << 7
 template <bool RAW>
-__global__ void prep_w32_a_kernel(const int32_t* A, int64_t lda, int64_t nch, uint32_t* Aprep) {
-  const int64_t rt = blockIdx.y, c = blockIdx.x;
+__device__ __forceinline__ void prep_w32_a_body(const int32_t* A, int64_t lda, int64_t nch, uint32_t* Aprep,
+                                                int64_t rt, int64_t c) {
   const int t = threadIdx.x, r = t & 127, kb = 16 * (t >> 7);
   const int4* src = reinterpret_cast<const int4*>(A + (rt * BM + r) * lda + c * SUB + kb);
   uint32_t* dst = Aprep + (rt * nch + c) * (SUB * BM);
@@ -855,8 +856,8 @@ __global__ void prep_w32_a_kernel(const int32_t* A, int64_t lda, int64_t nch, ui
 }
 
 template <bool RAW>
-__global__ void prep_w32_b_kernel(const int32_t* B, int64_t ldb, int64_t nch, uint32_t* Bprep) {
-  const int64_t ct = blockIdx.y, c = blockIdx.x;
+__device__ __forceinline__ void prep_w32_b_body(const int32_t* B, int64_t ldb, int64_t nch, uint32_t* Bprep,
+                                                int64_t ct, int64_t c) {
   const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
   const int4* src = reinterpret_cast<const int4*>(B + (c * SUB + kk) * ldb + ct * BN + cb);
   const uint32_t tag = uint32_t(SUB * (c % W32_WIN) + kk + 1);   // 1..96 inside a decode window
@@ -1043,8 +1044,8 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
 }
 
 // B (k x n) fp32 -> [n/64][k/32][32][64] for the deferred-argmin kernel
-__global__ void prep_f32_b64_kernel(const float* B, int64_t ldb, int64_t nch, float* Bprep) {
-  const int64_t ct = blockIdx.y, c = blockIdx.x;
+__device__ __forceinline__ void prep_f32_b64_body(const float* B, int64_t ldb, int64_t nch, float* Bprep,
+                                                  int64_t ct, int64_t c) {
   const int t = threadIdx.x, kk = t >> 3, cb = 8 * (t & 7);
   const float4* src = reinterpret_cast<const float4*>(B + (c * SUB + kk) * ldb + ct * DM_BN + cb);
   float4* dst = reinterpret_cast<float4*>(Bprep + (ct * nch + c) * (SUB * DM_BN) + kk * DM_BN + cb);
@@ -1061,37 +1062,58 @@ size_t prep_bytes(int64_t m, int64_t n, int64_t k) {   // A keys + B keys (uint3
   return ((size_t(m) * k * 4 + 255) / 256) * 256 + size_t(k) * n * 4 + 256;
 }
 
+// Both panel layouts in ONE launch (one dependent launch fewer on the per-round chain):
+// blockIdx = (chunk, tile, part) with part 0 the A rows and part 1 the B columns.
+enum PrepKind : int { PREP_U8 = 0, PREP_U16 = 1, PREP_W32 = 2, PREP_F32 = 3, PREP_F32_DM = 4 };
+template <int KIND>
+__global__ void __launch_bounds__(NT) prep_pair_kernel(const void* A, int64_t lda, const void* B, int64_t ldb,
+                                                       int64_t nch, int64_t nta, int64_t ntb, uint32_t* Aprep,
+                                                       void* Bprep) {
+  const int64_t c = blockIdx.x, tile = blockIdx.y;
+  if (blockIdx.z == 0) {
+    if (tile >= nta) return;
+    if constexpr (KIND == PREP_U8) prep_nt_a_body<STORE_U8>(static_cast<const uint8_t*>(A), lda, nch, Aprep, tile, c);
+    else if constexpr (KIND == PREP_U16)
+      prep_nt_a_body<STORE_U16>(static_cast<const uint16_t*>(A), lda, nch, Aprep, tile, c);
+    else if constexpr (KIND == PREP_W32) prep_w32_a_body<false>(static_cast<const int32_t*>(A), lda, nch, Aprep, tile, c);
+    else prep_w32_a_body<true>(static_cast<const int32_t*>(A), lda, nch, Aprep, tile, c);
+  } else {
+    if (tile >= ntb) return;
+    if constexpr (KIND == PREP_U8)
+      prep_nt_b_body<STORE_U8>(static_cast<const uint8_t*>(B), ldb, nch, static_cast<uint16_t*>(Bprep), tile, c);
+    else if constexpr (KIND == PREP_U16)
+      prep_nt_b_body<STORE_U16>(static_cast<const uint16_t*>(B), ldb, nch, static_cast<uint16_t*>(Bprep), tile, c);
+    else if constexpr (KIND == PREP_W32)
+      prep_w32_b_body<false>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep), tile, c);
+    else if constexpr (KIND == PREP_F32)
+      prep_w32_b_body<true>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep), tile, c);
+    else prep_f32_b64_body(static_cast<const float*>(B), ldb, nch, static_cast<float*>(Bprep), tile, c);
+  }
+}
+
 int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
                      int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s) {
   const size_t es = (store == STORE_W32 || store == STORE_F32) ? 4 : store == STORE_U16 ? 2 : 1;
   if (m % BM || n % BN || k % SUB || (lda * es) % 16 || (ldb * es) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
     return set_error(2, "panel prep needs 128-multiple m/n, 32-multiple k and 16-byte aligned panels");
-  const int64_t nch = k / SUB;
-  const dim3 ga(unsigned(nch), unsigned(m / BM)), gb(unsigned(nch), unsigned(n / BN));
-  if (store == STORE_U8) {
-    prep_nt_a_kernel<STORE_U8><<<ga, NT, 0, s>>>(static_cast<const uint8_t*>(A), lda, nch, Aprep);
-    prep_nt_b_kernel<STORE_U8><<<gb, NT, 0, s>>>(static_cast<const uint8_t*>(B), ldb, nch, static_cast<uint16_t*>(Bprep));
-  } else if (store == STORE_U16) {
-    prep_nt_a_kernel<STORE_U16><<<ga, NT, 0, s>>>(static_cast<const uint16_t*>(A), lda, nch, Aprep);
-    prep_nt_b_kernel<STORE_U16><<<gb, NT, 0, s>>>(static_cast<const uint16_t*>(B), ldb, nch,
-                                                  static_cast<uint16_t*>(Bprep));
-  } else if (store == STORE_W32) {
-    prep_w32_a_kernel<false><<<ga, NT, 0, s>>>(static_cast<const int32_t*>(A), lda, nch, Aprep);
-    prep_w32_b_kernel<false><<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep));
-  } else if (store == STORE_F32) {
-    prep_w32_a_kernel<true><<<ga, NT, 0, s>>>(static_cast<const int32_t*>(A), lda, nch, Aprep);
-    if (f32_deferred())
-      prep_f32_b64_kernel<<<dim3(unsigned(nch), unsigned(n / DM_BN)), NT, 0, s>>>(static_cast<const float*>(B), ldb,
-                                                                                  nch, static_cast<float*>(Bprep));
-    else
-      prep_w32_b_kernel<true><<<gb, NT, 0, s>>>(static_cast<const int32_t*>(B), ldb, nch,
-                                                 static_cast<uint32_t*>(Bprep));
-  } else {
-    return set_error(2, "panel prep is for the u8 / u16 / w32 / f32 tiers");
+  const int64_t nch = k / SUB, nta = m / BM;
+  const bool dm = store == STORE_F32 && f32_deferred();
+  const int64_t ntb = n / (dm ? DM_BN : BN);
+  const dim3 g(unsigned(nch), unsigned(std::max(nta, ntb)), 2);
+  switch (store) {
+    case STORE_U8: prep_pair_kernel<PREP_U8><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
+    case STORE_U16: prep_pair_kernel<PREP_U16><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
+    case STORE_W32: prep_pair_kernel<PREP_W32><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
+    case STORE_F32:
+      if (dm) prep_pair_kernel<PREP_F32_DM><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep);
+      else prep_pair_kernel<PREP_F32><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep);
+      break;
+    default:
+      return set_error(2, "panel prep is for the u8 / u16 / w32 / f32 tiers");
   }
   APSP_CUDA_TRY(cudaGetLastError());
-  count_launches(2);
+  count_launches(1);
   return 0;
 }
 
