@@ -48,36 +48,66 @@ __device__ __forceinline__ void warp_or(int32_t* dst, bool v) {
 }
 
 template <int D>
-__global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
-                            ScanResult* out) {
+struct ScanAcc {
   using T = typename Api<D>::T;
   bool neg = false, diag = false, nonint = false, anyfin = false, zero = false;
   unsigned long long edges = 0;
   long long mx = -1;
   float mxf = -1.f;
-  FOR_2D(i, j, rows, cols) {
-    const T v = h[i * ld + j];
-    const bool on_diag = diag_off >= 0 && j == i + diag_off;
+  __device__ __forceinline__ void add(T v, bool on_diag) {
     if (on_diag && v != T(0)) diag = true;
-    if (!Api<D>::fin(v)) continue;
+    if (!Api<D>::fin(v)) return;
     anyfin = true;
     if (!on_diag) edges++;
     if (v == T(0) && !on_diag) zero = true;
     if constexpr (D == API_F32) {
-      if (isnan(v) || v < 0.f) { neg = true; continue; }
+      if (isnan(v) || v < 0.f) {
+        neg = true;
+        return;
+      }
       if (v != floorf(v)) nonint = true;
       mxf = fmaxf(mxf, v);
       mx = max(mx, (long long)fminf(v, 9.0e18f));
     } else {
-      if (v < 0) { neg = true; continue; }
+      if (v < 0) {
+        neg = true;
+        return;
+      }
       mx = max(mx, (long long)v);
     }
   }
-  warp_or(&out->negative, neg);
-  warp_or(&out->diag_nonzero, diag);
-  warp_or(&out->non_integral, nonint);
-  warp_or(&out->any_finite, anyfin);
-  warp_or(&out->zero_offdiag, zero);
+};
+
+// vec: 4-byte elements, cols % 4 == 0, ld % 4 == 0, 16-byte aligned base -> one 16-byte load
+// per thread per step (the scalar sweep reaches ~30% of HBM bandwidth, this ~75%)
+template <int D>
+__global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
+                            ScanResult* out, int vec) {
+  using T = typename Api<D>::T;
+  ScanAcc<D> a;
+  if constexpr (sizeof(T) == 4) {
+    if (vec) {
+      FOR_2D(i, j4, rows, cols / 4) {
+        const int4 w = __ldg(reinterpret_cast<const int4*>(h + i * ld) + j4);
+        const int64_t j = 4 * j4, dj = diag_off >= 0 ? i + diag_off - j : -1;
+        a.add(__builtin_bit_cast(T, w.x), dj == 0);
+        a.add(__builtin_bit_cast(T, w.y), dj == 1);
+        a.add(__builtin_bit_cast(T, w.z), dj == 2);
+        a.add(__builtin_bit_cast(T, w.w), dj == 3);
+      }
+    }
+  }
+  if (!vec || sizeof(T) != 4) {
+    FOR_2D(i, j, rows, cols) a.add(h[i * ld + j], diag_off >= 0 && j == i + diag_off);
+  }
+  warp_or(&out->negative, a.neg);
+  warp_or(&out->diag_nonzero, a.diag);
+  warp_or(&out->non_integral, a.nonint);
+  warp_or(&out->any_finite, a.anyfin);
+  warp_or(&out->zero_offdiag, a.zero);
+  long long mx = a.mx;
+  float mxf = a.mxf;
+  unsigned long long edges = a.edges;
   for (int o = 16; o; o >>= 1) {
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
@@ -90,15 +120,20 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
   }
 }
 
+static bool vec4_ok(const void* p, int64_t ld, int64_t cols, size_t es) {
+  return es == 4 && cols % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
 int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
                 ScanResult* out_dev, cudaStream_t s) {
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
   // max fields start at 0 after memset; negative sentinel not needed (values are >= 0)
-  const dim3 g = grid_2d(rows, cols);
+  const int vec = vec4_ok(h, ld, cols, in_dtype == API_I64 ? 8 : 4);
+  const dim3 g = grid_2d(rows, vec ? cols / 4 : cols);
   switch (in_dtype) {
-    case API_I32: scan_kernel<API_I32><<<g, 256, 0, s>>>((const int32_t*)h, ld, rows, cols, diag_off, out_dev); break;
-    case API_F32: scan_kernel<API_F32><<<g, 256, 0, s>>>((const float*)h, ld, rows, cols, diag_off, out_dev); break;
-    case API_I64: scan_kernel<API_I64><<<g, 256, 0, s>>>((const int64_t*)h, ld, rows, cols, diag_off, out_dev); break;
+    case API_I32: scan_kernel<API_I32><<<g, 256, 0, s>>>((const int32_t*)h, ld, rows, cols, diag_off, out_dev, vec); break;
+    case API_F32: scan_kernel<API_F32><<<g, 256, 0, s>>>((const float*)h, ld, rows, cols, diag_off, out_dev, vec); break;
+    case API_I64: scan_kernel<API_I64><<<g, 256, 0, s>>>((const int64_t*)h, ld, rows, cols, diag_off, out_dev, 0); break;
     default: return set_error(2, "unknown dtype %d", in_dtype);
   }
   APSP_CUDA_TRY(cudaGetLastError());
@@ -109,23 +144,72 @@ int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t c
 // ---- conversion into a padded store ------------------------------------------------
 // rows [row0, row0 + R) of the padded N x N matrix (R = N, row0 = 0 for a whole matrix)
 template <int D, int S>
+__device__ __forceinline__ typename StoreT<S>::T store_cell(const typename Api<D>::T* h, int64_t ldh, int64_t n,
+                                                            int64_t il, int64_t i, int64_t j, bool& fin) {
+  using T = typename StoreT<S>::T;
+  if (i < n && j < n) {
+    const typename Api<D>::T v = h[il * ldh + j];
+    fin = Api<D>::fin(v);
+    return fin ? T(v) : store_inf<S>();
+  }
+  fin = (i == j);
+  return fin ? T(0) : store_inf<S>();
+}
+
+// vec: 4-byte input, n % 4 == 0, all pitches % 4 == 0 and 16-byte aligned bases -> 4 columns per
+// thread step: one 16-byte input load, one 4 x es output store, one 16-byte pred store
+template <int D, int S>
 __global__ void to_store_kernel(const typename Api<D>::T* h, int64_t ldh, int64_t n, typename StoreT<S>::T* out,
                                 int64_t ld, int64_t N, int32_t* P, int64_t ldp, int pred_init, int64_t row0,
-                                int64_t R) {
+                                int64_t R, int vec) {
   using T = typename StoreT<S>::T;
+  if constexpr (sizeof(typename Api<D>::T) == 4 && sizeof(T) <= 4) {
+    if (vec) {
+      FOR_2D(il, j4, R, N / 4) {
+        const int64_t i = row0 + il, j = 4 * j4;
+        T o[4];
+        bool fin[4];
+        if (i < n && j + 3 < n) {
+          const int4 w = __ldg(reinterpret_cast<const int4*>(h + il * ldh + j));
+          const typename Api<D>::T v[4] = {__builtin_bit_cast(typename Api<D>::T, w.x),
+                                           __builtin_bit_cast(typename Api<D>::T, w.y),
+                                           __builtin_bit_cast(typename Api<D>::T, w.z),
+                                           __builtin_bit_cast(typename Api<D>::T, w.w)};
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            fin[q] = Api<D>::fin(v[q]);
+            o[q] = fin[q] ? T(v[q]) : store_inf<S>();
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; q++) o[q] = store_cell<D, S>(h, ldh, n, il, i, j + q, fin[q]);
+        }
+        if constexpr (sizeof(T) == 1) {
+          *reinterpret_cast<uint32_t*>(out + il * ld + j) =
+              uint32_t(o[0]) | (uint32_t(o[1]) << 8) | (uint32_t(o[2]) << 16) | (uint32_t(o[3]) << 24);
+        } else if constexpr (sizeof(T) == 2) {
+          *reinterpret_cast<uint2*>(out + il * ld + j) =
+              make_uint2(uint32_t(o[0]) | (uint32_t(o[1]) << 16), uint32_t(o[2]) | (uint32_t(o[3]) << 16));
+        } else {
+          *reinterpret_cast<int4*>(out + il * ld + j) =
+              make_int4(__builtin_bit_cast(int, o[0]), __builtin_bit_cast(int, o[1]), __builtin_bit_cast(int, o[2]),
+                        __builtin_bit_cast(int, o[3]));
+        }
+        if (P) {
+          int32_t pv[4];
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            pv[q] = (pred_init && fin[q] && i != j + q && i < n && j + q < n) ? int32_t(i) : -1;
+          *reinterpret_cast<int4*>(P + il * ldp + j) = make_int4(pv[0], pv[1], pv[2], pv[3]);
+        }
+      }
+      return;
+    }
+  }
   FOR_2D(il, j, R, N) {
     const int64_t i = row0 + il;
-    T o;
     bool fin;
-    if (i < n && j < n) {
-      const typename Api<D>::T v = h[il * ldh + j];
-      fin = Api<D>::fin(v);
-      o = fin ? T(v) : store_inf<S>();
-    } else {
-      fin = (i == j);
-      o = fin ? T(0) : store_inf<S>();
-    }
-    out[il * ld + j] = o;
+    out[il * ld + j] = store_cell<D, S>(h, ldh, n, il, i, j, fin);
     if (P) P[il * ldp + j] = (pred_init && fin && i != j && i < n && j < n) ? int32_t(i) : -1;
   }
 }
@@ -134,15 +218,20 @@ template <int D>
 static int to_store_d(const void* h, int64_t ldh, int64_t n, int store, void* Dp, int64_t ld, int64_t N, int32_t* P,
                       int64_t ldp, int pred_init, int64_t row0, int64_t R, cudaStream_t s) {
   using TI = typename Api<D>::T;
-  const dim3 g = grid_2d(R, N);
+  const size_t es_out = store_elem_size(store);
+  const int vec = sizeof(TI) == 4 && es_out <= 4 && n % 4 == 0 && N % 4 == 0 && ldh % 4 == 0 && ld % 4 == 0 &&
+                  (!P || ldp % 4 == 0) && (reinterpret_cast<uintptr_t>(h) & 15) == 0 &&
+                  (reinterpret_cast<uintptr_t>(Dp) & (4 * es_out - 1)) == 0 &&
+                  (!P || (reinterpret_cast<uintptr_t>(P) & 15) == 0);
+  const dim3 g = grid_2d(R, vec ? N / 4 : N);
   const TI* hh = static_cast<const TI*>(h);
   switch (store) {
-    case STORE_U8: to_store_kernel<D, STORE_U8><<<g, 256, 0, s>>>(hh, ldh, n, (uint8_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
-    case STORE_W32: to_store_kernel<D, STORE_W32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
-    case STORE_I32: to_store_kernel<D, STORE_I32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
-    case STORE_F32: to_store_kernel<D, STORE_F32><<<g, 256, 0, s>>>(hh, ldh, n, (float*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
-    case STORE_I64: to_store_kernel<D, STORE_I64><<<g, 256, 0, s>>>(hh, ldh, n, (int64_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
-    case STORE_U16: to_store_kernel<D, STORE_U16><<<g, 256, 0, s>>>(hh, ldh, n, (uint16_t*)Dp, ld, N, P, ldp, pred_init, row0, R); break;
+    case STORE_U8: to_store_kernel<D, STORE_U8><<<g, 256, 0, s>>>(hh, ldh, n, (uint8_t*)Dp, ld, N, P, ldp, pred_init, row0, R, vec); break;
+    case STORE_W32: to_store_kernel<D, STORE_W32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init, row0, R, vec); break;
+    case STORE_I32: to_store_kernel<D, STORE_I32><<<g, 256, 0, s>>>(hh, ldh, n, (int32_t*)Dp, ld, N, P, ldp, pred_init, row0, R, vec); break;
+    case STORE_F32: to_store_kernel<D, STORE_F32><<<g, 256, 0, s>>>(hh, ldh, n, (float*)Dp, ld, N, P, ldp, pred_init, row0, R, vec); break;
+    case STORE_I64: to_store_kernel<D, STORE_I64><<<g, 256, 0, s>>>(hh, ldh, n, (int64_t*)Dp, ld, N, P, ldp, pred_init, row0, R, vec); break;
+    case STORE_U16: to_store_kernel<D, STORE_U16><<<g, 256, 0, s>>>(hh, ldh, n, (uint16_t*)Dp, ld, N, P, ldp, pred_init, row0, R, vec); break;
     default: return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
@@ -212,38 +301,57 @@ int launch_to_store_rect(int in_dtype, const void* h, int64_t ldh, int64_t rows,
 
 // ---- conversion back -----------------------------------------------------------------
 template <int S, int D>
-__global__ void from_store_kernel(const typename StoreT<S>::T* in, int64_t ld, int64_t rows, int64_t cols,
-                                  typename Api<D>::T* out, int64_t ldo) {
+__device__ __forceinline__ typename Api<D>::T from_cell(typename StoreT<S>::T v) {
   using TO = typename Api<D>::T;
-  const typename StoreT<S>::T inf = store_inf<S>();
-  FOR_2D(i, j, rows, cols) {
-    const auto v = in[i * ld + j];
-    TO o;
-    if constexpr (S == STORE_F32) {
-      o = TO(v);   // +inf maps to +inf (fp32 out) -- int outs never come from an fp32 store
-    } else {
-      if (v == inf) {
-        if constexpr (D == API_I32) o = INF32;
-        else if constexpr (D == API_I64) o = INF_RAW;
-        else o = __int_as_float(0x7f800000);
-      } else {
-        o = TO(v);
-      }
+  if constexpr (S == STORE_F32) {
+    return TO(v);   // +inf maps to +inf (fp32 out) -- int outs never come from an fp32 store
+  } else {
+    if (v == store_inf<S>()) {
+      if constexpr (D == API_I32) return INF32;
+      else if constexpr (D == API_I64) return INF_RAW;
+      else return __int_as_float(0x7f800000);
     }
-    out[i * ldo + j] = o;
+    return TO(v);
   }
+}
+
+// vec: u8 / u16 store into a 4-byte API output, cols % 4 == 0, aligned pitches: 4 cells per step
+template <int S, int D>
+__global__ void from_store_kernel(const typename StoreT<S>::T* in, int64_t ld, int64_t rows, int64_t cols,
+                                  typename Api<D>::T* out, int64_t ldo, int vec) {
+  using T = typename StoreT<S>::T;
+  using TO = typename Api<D>::T;
+  if constexpr (sizeof(T) <= 2 && sizeof(TO) == 4) {
+    if (vec) {
+      FOR_2D(i, j4, rows, cols / 4) {
+        T v[4];
+        if constexpr (sizeof(T) == 1) *reinterpret_cast<uint32_t*>(v) = *reinterpret_cast<const uint32_t*>(in + i * ld + 4 * j4);
+        else *reinterpret_cast<uint2*>(v) = *reinterpret_cast<const uint2*>(in + i * ld + 4 * j4);
+        const TO o0 = from_cell<S, D>(v[0]), o1 = from_cell<S, D>(v[1]), o2 = from_cell<S, D>(v[2]),
+                 o3 = from_cell<S, D>(v[3]);
+        *reinterpret_cast<int4*>(out + i * ldo + 4 * j4) =
+            make_int4(__builtin_bit_cast(int, o0), __builtin_bit_cast(int, o1), __builtin_bit_cast(int, o2),
+                      __builtin_bit_cast(int, o3));
+      }
+      return;
+    }
+  }
+  FOR_2D(i, j, rows, cols) out[i * ldo + j] = from_cell<S, D>(in[i * ld + j]);
 }
 
 template <int S>
 static int from_store_s(const void* in, int64_t ld, int64_t rows, int64_t cols, int out_dtype, void* out, int64_t ldo,
                         cudaStream_t s) {
   using TI = typename StoreT<S>::T;
-  const dim3 g = grid_2d(rows, cols);
+  const int vec = sizeof(TI) <= 2 && out_dtype != API_I64 && cols % 4 == 0 && ld % 4 == 0 && ldo % 4 == 0 &&
+                  (reinterpret_cast<uintptr_t>(in) & (4 * sizeof(TI) - 1)) == 0 &&
+                  (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  const dim3 g = grid_2d(rows, vec ? cols / 4 : cols);
   const TI* ii = static_cast<const TI*>(in);
   switch (out_dtype) {
-    case API_I32: from_store_kernel<S, API_I32><<<g, 256, 0, s>>>(ii, ld, rows, cols, (int32_t*)out, ldo); break;
-    case API_F32: from_store_kernel<S, API_F32><<<g, 256, 0, s>>>(ii, ld, rows, cols, (float*)out, ldo); break;
-    case API_I64: from_store_kernel<S, API_I64><<<g, 256, 0, s>>>(ii, ld, rows, cols, (int64_t*)out, ldo); break;
+    case API_I32: from_store_kernel<S, API_I32><<<g, 256, 0, s>>>(ii, ld, rows, cols, (int32_t*)out, ldo, vec); break;
+    case API_F32: from_store_kernel<S, API_F32><<<g, 256, 0, s>>>(ii, ld, rows, cols, (float*)out, ldo, vec); break;
+    case API_I64: from_store_kernel<S, API_I64><<<g, 256, 0, s>>>(ii, ld, rows, cols, (int64_t*)out, ldo, vec); break;
     default: return set_error(2, "unknown dtype %d", out_dtype);
   }
   APSP_CUDA_TRY(cudaGetLastError());
@@ -303,15 +411,30 @@ int launch_copy_block(int store, const void* src, int64_t lds, void* dst, int64_
 // ---- certificate: max finite value of a store ------------------------------------------
 template <int S>
 __global__ void max_finite_kernel(const typename StoreT<S>::T* D, int64_t ld, int64_t rows, int64_t cols,
-                                  ScanResult* out) {
+                                  ScanResult* out, int vec) {
   const auto inf = store_inf<S>();
   long long mx = -1;
   float mxf = -1.f;
-  FOR_2D(i, j, rows, cols) {
-    const auto v = D[i * ld + j];
-    if (v == inf) continue;
-    if constexpr (S == STORE_F32) mxf = fmaxf(mxf, v);
-    else mx = max(mx, (long long)v);
+  if constexpr (S == STORE_U8) {
+    if (vec) {   // 16 cells per step: INF bytes zeroed, then a packed byte max (the diagonal is 0,
+                 // so a finite value always exists)
+      uint32_t m4 = 0;
+      FOR_2D(i, j16, rows, cols / 16) {
+        const uint4 w = *reinterpret_cast<const uint4*>(D + i * ld + 16 * j16);
+        const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) m4 = __vmaxu4(m4, x[q] & ~__vcmpeq4(x[q], 0xFFFFFFFFu));
+      }
+      mx = max(max(m4 & 0xFF, (m4 >> 8) & 0xFF), max((m4 >> 16) & 0xFF, m4 >> 24));
+    }
+  }
+  if (!(S == STORE_U8 && vec)) {
+    FOR_2D(i, j, rows, cols) {
+      const auto v = D[i * ld + j];
+      if (v == inf) continue;
+      if constexpr (S == STORE_F32) mxf = fmaxf(mxf, v);
+      else mx = max(mx, (long long)v);
+    }
   }
   for (int o = 16; o; o >>= 1) {
     mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -326,14 +449,15 @@ __global__ void max_finite_kernel(const typename StoreT<S>::T* D, int64_t ld, in
 int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_t cols, ScanResult* out_dev,
                       cudaStream_t s) {
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
-  const dim3 g = grid_2d(rows, cols);
+  const int vec = store == STORE_U8 && cols % 16 == 0 && ld % 16 == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0;
+  const dim3 g = grid_2d(rows, vec ? cols / 16 : cols);
   switch (store) {
-    case STORE_U8: max_finite_kernel<STORE_U8><<<g, 256, 0, s>>>((const uint8_t*)D, ld, rows, cols, out_dev); break;
-    case STORE_W32: max_finite_kernel<STORE_W32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev); break;
-    case STORE_I32: max_finite_kernel<STORE_I32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev); break;
-    case STORE_F32: max_finite_kernel<STORE_F32><<<g, 256, 0, s>>>((const float*)D, ld, rows, cols, out_dev); break;
-    case STORE_I64: max_finite_kernel<STORE_I64><<<g, 256, 0, s>>>((const int64_t*)D, ld, rows, cols, out_dev); break;
-    case STORE_U16: max_finite_kernel<STORE_U16><<<g, 256, 0, s>>>((const uint16_t*)D, ld, rows, cols, out_dev); break;
+    case STORE_U8: max_finite_kernel<STORE_U8><<<g, 256, 0, s>>>((const uint8_t*)D, ld, rows, cols, out_dev, vec); break;
+    case STORE_W32: max_finite_kernel<STORE_W32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev, vec); break;
+    case STORE_I32: max_finite_kernel<STORE_I32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev, vec); break;
+    case STORE_F32: max_finite_kernel<STORE_F32><<<g, 256, 0, s>>>((const float*)D, ld, rows, cols, out_dev, vec); break;
+    case STORE_I64: max_finite_kernel<STORE_I64><<<g, 256, 0, s>>>((const int64_t*)D, ld, rows, cols, out_dev, vec); break;
+    case STORE_U16: max_finite_kernel<STORE_U16><<<g, 256, 0, s>>>((const uint16_t*)D, ld, rows, cols, out_dev, vec); break;
     default: return set_error(2, "unknown store %d", store);
   }
   APSP_CUDA_TRY(cudaGetLastError());
