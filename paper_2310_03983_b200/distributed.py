@@ -56,7 +56,7 @@ def round_up(v: int, m: int) -> int:
 def shard_block(n: int, world: int) -> int:
     """Pivot block for the sharded solve.
 
-    Starts from the single-GPU size rule (capi.cu default_block).  The owner of a pivot block
+    Starts from the single-GPU size rule (fw_sched.cu default_block).  The owner of a pivot block
     does its b^2*N pivot work alone while every rank does (N/P)*N*b of phase 3, so the owner's
     extra share is b*P/N: b is capped at N/(16 P) (~6%).  Then lowered until a rank's row band
     holds whole blocks without extra padding."""
@@ -75,7 +75,7 @@ def layout(n: int, world: int, block: int) -> tuple[int, int]:
 
 
 def pick_tiers(dtype_code: int, scan: dict, n: int = 0) -> list[int]:
-    """Narrowest exact tier first (mirror of capi.cu pick_tiers, including the sparse-graph
+    """Narrowest exact tier first (mirror of engine.cu pick_tiers, including the sparse-graph
     distance estimate 0.5 * w_max * ln(n) / ln(average degree) that skips hopeless tiers)."""
     import math
 

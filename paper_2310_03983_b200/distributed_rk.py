@@ -55,7 +55,7 @@ TILE = 128
 
 
 def rk_split(m: int) -> int:
-    """Size of the first half of an m-block (capi.cu RK::split, aligned): ceil(tiles / 2) tiles."""
+    """Size of the first half of an m-block (rkleene.cu RK::split, aligned): ceil(tiles / 2) tiles."""
     return ((m // TILE + 1) // 2) * TILE
 
 
@@ -67,7 +67,7 @@ def row_bands(m: int, world: int) -> list[tuple[int, int]]:
 
 
 def run_rkleene(ranks: list[RankState], world: int, N: int, thr: int, ops, comm) -> None:
-    """The recursion of capi.cu RK::close on every local rank's replica.
+    """The recursion of rkleene.cu RK::close on every local rank's replica.
 
     Operand specs: ("D", i, j) the matrix, ("S", 0, 0) the value snapshot, ("P", i, j) the pred
     matrix, ("SP", 0, 0) the pred snapshot (the aliasing rules of solvers.py:250-286)."""

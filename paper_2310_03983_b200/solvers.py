@@ -38,7 +38,7 @@ from .core import (
 from .minplus import DEFAULT_TILE_SIZE, _resolve_workers
 
 DEFAULT_BASE_THRESHOLD = 64
-DEFAULT_BLOCK = 0   # 0: the library picks by n (capi.cu default_block: 128 ... 2048)
+DEFAULT_BLOCK = 0   # 0: the library picks by n (fw_sched.cu default_block: 128 ... 2048)
 
 
 @dataclass(frozen=True)
