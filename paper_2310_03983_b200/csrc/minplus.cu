@@ -1,85 +1,21 @@
 // Min-plus tile kernels:  C <- min(C, A (x) B)  with argmin -> idx on strict improvement.
 //
-// This is the bulk of the work for both solvers: FW phase 3 (the "remaining tiles" of each
-// pivot block) and every block product of the R-Kleene recursion.  Three variants:
+// This is the bulk of the work for both solvers: FW phases 2-3 and every block product of the
+// R-Kleene recursion.  Keyed tiers carry the argmin inside the value: key(x) = x << tag_bits,
+// the right operand carries tag = 1 + (k mod window); the min over keys is the lexicographic
+// (value, smallest k) min and an untagged (old) key wins ties, so a tag survives only on
+// strict improvement (minplus.py:80-82,128-133).  Tags are decoded into a 16-bit k index per
+// cell once per window and cleared.
 //
-//  * u8  (narrow tier)  store uint8, keys 16-bit packed two per register; the inner loop is
-//    one VIADDMNMX.S16x2 per two updates (DPX, measured 128 upd/clk/SM on B200).
-//  * w32 (wide tier)    store int32 < 2^24, keys int32; inner loop VIADD + VIMNMX3 over a pair
-//    of k (1.5 instr/update, measured 85 upd/clk/SM).
-//  * exact              int32 / fp32 / int64 compare-select (continuous weights, huge costs).
-//
-// Keyed tiers:  key(x) = x << 6, right operand carries tag = 1 + (k mod 32).  The min over
-// keys is the lexicographic (value, smallest k) min; an untagged (old) key wins ties, so a
-// tag survives only on strict improvement (minplus.py:80-82,128-133).  Every 32 k-steps the
-// tags are decoded into a 16-bit k index per cell and cleared.
+//  * minplus_bulk.cu: the bulk-staged kernels on pre-laid-out panels (u8/u16 VIADDMNMX.U16x2,
+//    w32 VIADDMNMX.U32, exact fp32 deferred-argmin and compare-select) and the panel layouts.
+//  * here: register-staged kernels for unaligned shapes (u8, w32), the exact compare-select
+//    kernel (int32 / fp32 / int64) and the launch dispatch.
 #include <algorithm>
 #include <cstdlib>
-#include <string>
-#include "launch.h"
+#include "tiles.cuh"
 
 namespace apsp {
-
-constexpr int BM = 128, BN = 128, NT = 256;
-#ifndef APSP_U8_UNROLL
-#define APSP_U8_UNROLL 32
-#endif
-constexpr int kU8Unroll = APSP_U8_UNROLL;
-
-// Tile origin of this CTA.  Full grid: (blockIdx.y, blockIdx.x).  Cross-list mode
-// (only_lo < only_hi): blockIdx.x enumerates the tiles of rows band + cols band [lo, hi)
-// (band width w tiles): first the w full tile rows, then the remaining rows of the w columns.
-__device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn, int64_t& i0, int64_t& j0) {
-  if (p.only_lo < p.only_hi) {   // tile counts fit 32 bits: 32-bit division (a 64-bit one is ~100 instr)
-    const int wr = int((p.only_hi - p.only_lo) / bm), lo_r = int(p.only_lo / bm);   // row band, in row tiles
-    const int wc = int((p.only_hi - p.only_lo) / bn), lo_c = int(p.only_lo / bn);   // col band, in col tiles
-    const int nt_c = int((p.n + bn - 1) / bn);
-    const int id = int(blockIdx.x);
-    if (id < wr * nt_c) {
-      i0 = int64_t(lo_r + id / nt_c) * bm;
-      j0 = int64_t(id % nt_c) * bn;
-    } else {
-      const int id2 = id - wr * nt_c, rr = id2 / wc, cc = id2 % wc;
-      i0 = int64_t(rr < lo_r ? rr : rr + wr) * bm;
-      j0 = int64_t(lo_c + cc) * bn;
-    }
-  } else {
-    i0 = int64_t(blockIdx.y) * bm;
-    j0 = int64_t(blockIdx.x) * bn;
-  }
-}
-
-__device__ __forceinline__ bool tile_skipped(const MinplusArgs& p, int64_t i0, int64_t j0, int bm, int bn) {
-  const bool rin = i0 >= p.skip_row_lo && i0 + bm <= p.skip_row_hi;
-  const bool cin = j0 >= p.skip_col_lo && j0 + bn <= p.skip_col_hi;
-  const bool r2 = i0 >= p.skip2_lo && i0 + bm <= p.skip2_hi;
-  const bool c2 = j0 >= p.skip2_lo && j0 + bn <= p.skip2_hi;
-  return rin || cin || r2 || c2;
-}
-
-__device__ __forceinline__ void emit_idx(const MinplusArgs& p, int64_t i, int64_t j, uint32_t kk) {
-  if (p.idx == nullptr) return;
-  int32_t v = (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(kk) * p.ldp + j) : int32_t(p.inner_off + kk);
-  p.idx[i * p.ldi + j] = v;
-}
-
-// u8 tier keys: 16-bit UNSIGNED, key = value << 7 | tag, tag = 1..64 over a 64-k decode window
-// (two 32-k chunks).  INF key = 255 << 7 = 32640; the largest sum INF + INF + tag = 65407 < 2^16.
-constexpr int U8_TAG = 7;
-constexpr uint32_t U8_KINF = uint32_t(U8_INF) << U8_TAG;
-constexpr uint32_t U8_TAGMASK2 = 0x007F007Fu;
-
-__device__ __forceinline__ uint32_t viaddmin_u16x2(uint32_t a, uint32_t b, uint32_t c) {
-  return __viaddmin_u16x2(a, b, c);
-}
-
-// 0xFFFF in each 16-bit half whose bit 15 is set, else 0 (PTX prmt sign replication; the
-// CUDA __byte_perm intrinsic masks selectors to 3 bits and cannot express it).
-__device__ __forceinline__ uint32_t prmt_sign_halves(uint32_t x) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(x));
-  return d;
-}
 
 // ------------------------------------------------------------------------------------
 // narrow tier: uint8 store, packed 16-bit keys
@@ -306,1009 +242,6 @@ __global__ void __launch_bounds__(NT, 2) minplus_u8_kernel(MinplusArgs p) {
     }
   }
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
-}
-
-// ------------------------------------------------------------------------------------
-// narrow tiers with pre-laid-out panels: cp.async.bulk (TMA bulk copy) + mbarrier 3-stage ring
-//   u8  : uint8 store,  values 0..254, key = v << 7 | tag, decode window 3 chunks (tags 1..96)
-//   u16 : uint16 store, values 0..510, key = v << 6 | tag, decode window 1 chunk  (tags 1..32)
-// Keys are unsigned 16-bit: INF + INF + tag < 2^16 in both (VIADDMNMX.U16x2).
-// ------------------------------------------------------------------------------------
-template <int S> struct Narrow;
-template <> struct Narrow<STORE_U8> {
-  using T = uint8_t;
-  static constexpr int TAG = 7, WIN = 3, STAGES = 3;
-  static constexpr uint32_t INF = U8_INF;
-};
-template <> struct Narrow<STORE_U16> {
-  using T = uint16_t;
-  static constexpr int TAG = 6, WIN = 1, STAGES = 3;
-  static constexpr uint32_t INF = U16_INF;
-};
-
-constexpr uint32_t U8_CHUNK_A = SUB * BM * 4, U8_CHUNK_B = SUB * BN * 2;
-template <int S>
-struct SmemNT {   // u8: 4 x 24 KB ring + 16 KB C = 112 KB (2 CTAs / SM); u16: 3 x 24 KB + 32 KB
-  uint32_t As[Narrow<S>::STAGES][SUB][BM];
-  uint16_t Bs[Narrow<S>::STAGES][SUB][BN];
-  typename Narrow<S>::T Cs[BM][BN];
-  unsigned long long full[Narrow<S>::STAGES];   // bulk copy landed (tx count)
-  unsigned int done[Narrow<S>::STAGES];         // warps finished with the slot's chunk
-};
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-// try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes instead
-// of re-issuing the probe (a spinning producer warp steals issue slots from the ALU-bound
-// consumers on its SM sub-partition)
-__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* b, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity), "r"(1000000u)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-
-// One 128 x 128 tile per CTA (8 warps, 8 x 8 cells per thread).  The pre-laid-out A/B chunks
-// stream through a STAGES-slot ring with cp.async.bulk (full mbarriers carry the tx count).
-// No barrier sits in the k loop: each warp counts itself out of a slot when it has consumed
-// it, and the LAST warp out refills the slot with chunk c + STAGES -- no warp ever waits for
-// another, only for data.  Each thread prefetches exactly its own 8 x 8 C cells (cp.async),
-// so the merge after chunk 0 needs no barrier either.
-// PEERS: 0 no peer stores; 1 improved segments also stored into the peer replicas (R-Kleene);
-// 2 every cell of the tile (values and pred, improved or not) stored into the peers' receive
-// slots (the FW pivot panel push).
-template <int S, int PEERS>
-__global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
-  using NR = Narrow<S>;
-  using T = typename NR::T;
-  constexpr int TAG = NR::TAG, WIN = NR::WIN, STAGES = NR::STAGES;
-  constexpr uint32_t KINF2 = (NR::INF << TAG) * 0x00010001u;
-  constexpr uint32_t TMASK2 = ((1u << TAG) - 1u) * 0x00010001u;
-  constexpr int CW = 4 * int(sizeof(T));          // bytes of one 4-cell C segment
-  extern __shared__ __align__(128) unsigned char smraw_nt[];
-  SmemNT<S>& sm = *reinterpret_cast<SmemNT<S>*>(smraw_nt);
-  // a dependent launch queued behind this kernel (pdl) may start as soon as every CTA is running
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  int64_t i0, j0;
-  tile_origin(p, BM, BN, i0, j0);
-  if (tile_skipped(p, i0, j0, BM, BN)) return;
-  const int t = threadIdx.x;
-  const int nch = int(p.k / SUB);
-  const uint32_t* Ap = p.Aprep + (i0 / BM) * int64_t(nch) * (SUB * BM);
-  const uint16_t* Bp = static_cast<const uint16_t*>(p.Bprep) + (j0 / BN) * int64_t(nch) * (SUB * BN);
-  auto issue = [&](int c, int slot) {
-    mbar_expect_tx(&sm.full[slot], U8_CHUNK_A + U8_CHUNK_B);
-    bulk_g2s(&sm.As[slot][0][0], Ap + int64_t(c) * (SUB * BM), U8_CHUNK_A, &sm.full[slot]);
-    bulk_g2s(&sm.Bs[slot][0][0], Bp + int64_t(c) * (SUB * BN), U8_CHUNK_B, &sm.full[slot]);
-  };
-  if (t == 0) {
-    for (int s = 0; s < STAGES; s++) {
-      mbar_init(&sm.full[s], 1);
-      sm.done[s] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int c = 0; c < STAGES && c < nch; c++) issue(c, c);
-  }
-  __syncthreads();
-  const int tx = t & 15, ty = t >> 4, lane = t & 31;
-  {  // own C cells -> smem (cp.async, 4 or 8 bytes per 4-cell segment)
-    const char* C = static_cast<const char*>(p.C);
-#pragma unroll
-    for (int r = 0; r < 8; r++) {
-      const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const char* src = C + ((i0 + ri) * p.ldc + j0 + 64 * h + 4 * tx) * int64_t(sizeof(T));
-        const uint32_t dst = smem_u32(&sm.Cs[ri][64 * h + 4 * tx]);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"(dst), "l"(src), "n"(CW));
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
-  bool changed = false;
-  const int32_t* __restrict__ pb = p.predB;
-  int32_t* __restrict__ out = p.idx;
-  T* Cw = static_cast<T*>(p.C);
-  const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
-
-  uint32_t acc[8][4];
-  uint32_t kst[8][4];
-#pragma unroll
-  for (int r = 0; r < 8; r++)
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      acc[r][q] = KINF2;
-      kst[r][q] = 0u;
-    }
-  int slot = 0, wc = 0;
-  uint32_t ph = 0;
-  for (int c = 0; c < nch; c++) {
-    mbar_wait(&sm.full[slot], ph);
-#pragma unroll kU8Unroll
-    for (int kk = 0; kk < SUB; kk++) {
-      const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
-      const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
-      const uint2 b0 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][4 * tx]);
-      const uint2 b1 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][64 + 4 * tx]);
-      const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
-#pragma unroll
-      for (int r = 0; r < 8; r++)
-#pragma unroll
-        for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
-    }
-    __syncwarp();
-    if (lane == 0) {   // count this warp out of the slot; the last one refills it
-      __threadfence_block();
-      if (atomicAdd(&sm.done[slot], 1u) == NT / 32 - 1) {
-        __threadfence_block();
-        sm.done[slot] = 0;
-        if (c + STAGES < nch) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(c + STAGES, slot);
-        }
-      }
-    }
-    if (++slot == STAGES) {
-      slot = 0;
-      ph ^= 1u;
-    }
-    if (c == 0) {   // merge the old C (own cells only: no barrier)
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-#pragma unroll
-      for (int r = 0; r < 8; r++) {
-        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          uint32_t p0, p1;   // old values of the two column pairs, as key pairs
-          if constexpr (sizeof(T) == 1) {
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]);
-            p0 = __byte_perm(w, 0, 0x4140) << TAG;
-            p1 = __byte_perm(w, 0, 0x4342) << TAG;
-          } else {
-            const uint2 w = *reinterpret_cast<const uint2*>(&sm.Cs[ri][64 * h + 4 * tx]);
-            p0 = w.x << TAG;
-            p1 = w.y << TAG;
-          }
-          acc[r][2 * h] = __vminu2(acc[r][2 * h], p0);
-          acc[r][2 * h + 1] = __vminu2(acc[r][2 * h + 1], p1);
-        }
-      }
-    }
-    if (wc == WIN - 1 || c + 1 == nch) {
-      uint32_t any = 0;
-#pragma unroll
-      for (int r = 0; r < 8; r++)
-#pragma unroll
-        for (int q = 0; q < 4; q++) any |= acc[r][q];
-      if (__any_sync(0xffffffffu, any & TMASK2)) {
-        const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
-#pragma unroll
-        for (int r = 0; r < 8; r++)
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const uint32_t tg = acc[r][q] & TMASK2;
-            const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
-            kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
-            acc[r][q] -= tg;
-          }
-      }
-    }
-    if (++wc == WIN) wc = 0;
-  }
-  // epilogue
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
-    int32_t pv[2][4];
-    uint32_t ks[2][4];
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
-      ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
-      const int64_t j = j0 + 64 * h + 4 * tx;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        pv[h][q] = 0;
-        if (out && ks[h][q] != 0u)
-          pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
-                                          : int32_t(p.inner_off + ks[h][q] - 1u);
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
-      if constexpr (PEERS == 2) {   // push the whole segment; local stores only where improved
-        const int64_t j = j0 + 64 * h + 4 * tx;
-        const bool imp = (k0 | k1) != 0u;
-        changed |= imp;
-        if constexpr (sizeof(T) == 1) {
-          const uint32_t w = __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
-          uint32_t* dst = reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j);
-          if (imp) *dst = w;
-          for (int pr = 0; pr < p.npeers; pr++)
-            *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
-        } else {
-          const uint2 w = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
-          uint2* dst = reinterpret_cast<uint2*>(Cw + i * p.ldc + j);
-          if (imp) *dst = w;
-          for (int pr = 0; pr < p.npeers; pr++)
-            *reinterpret_cast<uint2*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
-        }
-        if (!out) continue;
-        int32_t* dst = out + i * p.ldi + j;
-        int32_t full[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          full[q] = ks[h][q] != 0u ? pv[h][q] : dst[q];   // unimproved: the current pred
-          if (ks[h][q] != 0u) dst[q] = pv[h][q];
-        }
-        for (int pr = 0; pr < p.npeers; pr++) {
-          int32_t* pd = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]);
-#pragma unroll
-          for (int q = 0; q < 4; q++) pd[q] = full[q];
-        }
-        continue;
-      }
-      if ((k0 | k1) == 0u) continue;
-      changed = true;
-      const int64_t j = j0 + 64 * h + 4 * tx;
-      if constexpr (sizeof(T) == 1) {
-        const uint32_t w = __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(Cw + i * p.ldc + j);
-        *dst = w;
-        if constexpr (PEERS != 0)
-          for (int pr = 0; pr < p.npeers; pr++)
-            *reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
-      } else {
-        const uint2 w = make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
-        uint2* dst = reinterpret_cast<uint2*>(Cw + i * p.ldc + j);
-        *dst = w;
-        if constexpr (PEERS != 0)
-          for (int pr = 0; pr < p.npeers; pr++)
-            *reinterpret_cast<uint2*>(reinterpret_cast<char*>(dst) + p.peer_dC[pr]) = w;
-      }
-      if (!out) continue;
-      if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
-        const int4 w = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
-        int4* dst = reinterpret_cast<int4*>(out + i * p.ldi + j);
-        *dst = w;
-        if constexpr (PEERS != 0)
-          for (int pr = 0; pr < p.npeers; pr++)
-            *reinterpret_cast<int4*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-          if (ks[h][q] != 0u) {
-            int32_t* dst = out + i * p.ldi + j + q;
-            *dst = pv[h][q];
-            if constexpr (PEERS != 0)
-              for (int pr = 0; pr < p.npeers; pr++)
-                *reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = pv[h][q];
-          }
-      }
-    }
-  }
-  // peer stores are ordered before anything the host signals after this kernel
-  if constexpr (PEERS != 0) __threadfence_system();
-  // one flag write per warp that changed (no CTA barrier needed)
-  if (p.status && p.track_changed && __any_sync(0xffffffffu, changed) && lane == 0) p.status->changed = 1;
-}
-
-// panel layout kernels (one CTA per (tile, chunk); thread = one row x 16 k, or one k x 16 columns)
-template <int S>
-__device__ __forceinline__ void prep_nt_a_body(const typename Narrow<S>::T* A, int64_t lda, int64_t nch,
-                                               uint32_t* Aprep, int64_t rt, int64_t c) {
-  using T = typename Narrow<S>::T;
-  constexpr int TAG = Narrow<S>::TAG;
-  const int t = threadIdx.x, r = t & 127, kb = 16 * (t >> 7);
-  const T* src = A + (rt * BM + r) * lda + c * SUB + kb;
-  uint32_t* dst = Aprep + (rt * nch + c) * (SUB * BM);
-  T v[16];
-  *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(src));
-  if constexpr (sizeof(T) == 2) *reinterpret_cast<uint4*>(v + 8) = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-#pragma unroll
-  for (int q = 0; q < 16; q++) dst[(kb + q) * BM + r] = (uint32_t(v[q]) << TAG) * 0x00010001u;
-}
-
-template <int S>
-__device__ __forceinline__ void prep_nt_b_body(const typename Narrow<S>::T* B, int64_t ldb, int64_t nch,
-                                               uint16_t* Bprep, int64_t ct, int64_t c) {
-  using T = typename Narrow<S>::T;
-  constexpr int TAG = Narrow<S>::TAG, WIN = Narrow<S>::WIN;
-  const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
-  const T* src = B + (c * SUB + kk) * ldb + ct * BN + cb;
-  T v[16];
-  *reinterpret_cast<uint4*>(v) = __ldg(reinterpret_cast<const uint4*>(src));
-  if constexpr (sizeof(T) == 2) *reinterpret_cast<uint4*>(v + 8) = __ldg(reinterpret_cast<const uint4*>(src) + 1);
-  const uint32_t tag = uint32_t(SUB * (c % WIN) + kk + 1);   // 1..32*WIN inside a decode window
-  uint32_t o[8];
-#pragma unroll
-  for (int q = 0; q < 8; q++)
-    o[q] = ((uint32_t(v[2 * q]) << TAG) | tag) | (((uint32_t(v[2 * q + 1]) << TAG) | tag) << 16);
-  uint4* dst = reinterpret_cast<uint4*>(Bprep + (ct * nch + c) * (SUB * BN) + kk * BN + cb);
-  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
-}
-
-// ------------------------------------------------------------------------------------
-// w32 tier with pre-laid-out panels: int32 store (< 2^24 - 1), unsigned 32-bit keys
-// key = v << 7 | tag, decode window 3 chunks (tags 1..96).  INF + INF + tag < 2^32, so the
-// sums never wrap.  ptxas turns min3(acc, a0 + b0, a1 + b1) into two VIADDMNMX.U32 (ALU, one
-// update per instruction, 18.6 T upd/s ceiling); forcing the sums onto the FMA pipe as IMAD +
-// VIMNMX3 measured slower (341 vs 293 ms, n = 16384).  Same staging as the narrow kernel:
-// cp.async.bulk + mbarrier ring for A/B, cp.async for C.
-// ------------------------------------------------------------------------------------
-constexpr int W32_TAG = 7, W32_WIN = 3, W32_STAGES = 3;
-
-constexpr uint32_t W32_CHUNK = SUB * BM * 4;   // A and B chunk bytes (128 x 32 keys each)
-struct SmemW32NT {
-  uint32_t As[W32_STAGES][SUB][BM];
-  uint32_t Bs[W32_STAGES][SUB][BN];
-  int32_t Cs[BM][BN];
-  unsigned long long bar[W32_STAGES];
-};
-
-__global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
-  constexpr uint32_t KINF = uint32_t(W32_INF) << W32_TAG;
-  constexpr uint32_t TMASK = (1u << W32_TAG) - 1u;
-  extern __shared__ __align__(128) unsigned char smraw_w32[];
-  SmemW32NT& sm = *reinterpret_cast<SmemW32NT*>(smraw_w32);
-  int64_t i0, j0;
-  tile_origin(p, BM, BN, i0, j0);
-  if (tile_skipped(p, i0, j0, BM, BN)) return;
-  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  const int64_t nch = p.k / SUB;
-  const uint32_t* Ap = p.Aprep + (i0 / BM) * nch * (SUB * BM);
-  const uint32_t* Bp = static_cast<const uint32_t*>(p.Bprep) + (j0 / BN) * nch * (SUB * BN);
-  if (t == 0) {
-    for (int s = 0; s < W32_STAGES; s++) mbar_init(&sm.bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int64_t c) {
-    const int slot = int(c % W32_STAGES);
-    mbar_expect_tx(&sm.bar[slot], 2 * W32_CHUNK);
-    bulk_g2s(&sm.As[slot][0][0], Ap + c * (SUB * BM), W32_CHUNK, &sm.bar[slot]);
-    bulk_g2s(&sm.Bs[slot][0][0], Bp + c * (SUB * BN), W32_CHUNK, &sm.bar[slot]);
-  };
-  if (t == 0)
-    for (int64_t c = 0; c < W32_STAGES && c < nch; c++) issue(c);
-  {  // C tile -> smem (merged after chunk 0)
-    const int r = t >> 1;
-    const char* src = reinterpret_cast<const char*>(static_cast<const int32_t*>(p.C) + (i0 + r) * p.ldc + j0) +
-                      256 * (t & 1);
-    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r][0]) + 256 * (t & 1));
-#pragma unroll
-    for (int q = 0; q < 16; q++)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
-  uint32_t acc[8][8];
-  uint32_t kst[8][4];
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-#pragma unroll
-    for (int q = 0; q < 8; q++) acc[r][q] = KINF;
-#pragma unroll
-    for (int q = 0; q < 4; q++) kst[r][q] = 0u;
-  }
-  for (int64_t c = 0; c < nch; c++) {
-    const int slot = int(c % W32_STAGES);
-    mbar_wait(&sm.bar[slot], uint32_t((c / W32_STAGES) & 1));
-#pragma unroll 4
-    for (int kk = 0; kk < SUB; kk += 2) {
-      uint32_t a0[8], a1[8], b0[8], b1[8];
-      *reinterpret_cast<uint4*>(a0) = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
-      *reinterpret_cast<uint4*>(a0 + 4) = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
-      *reinterpret_cast<uint4*>(a1) = *reinterpret_cast<const uint4*>(&sm.As[slot][kk + 1][4 * ty]);
-      *reinterpret_cast<uint4*>(a1 + 4) = *reinterpret_cast<const uint4*>(&sm.As[slot][kk + 1][64 + 4 * ty]);
-      *reinterpret_cast<uint4*>(b0) = *reinterpret_cast<const uint4*>(&sm.Bs[slot][kk][4 * tx]);
-      *reinterpret_cast<uint4*>(b0 + 4) = *reinterpret_cast<const uint4*>(&sm.Bs[slot][kk][64 + 4 * tx]);
-      *reinterpret_cast<uint4*>(b1) = *reinterpret_cast<const uint4*>(&sm.Bs[slot][kk + 1][4 * tx]);
-      *reinterpret_cast<uint4*>(b1 + 4) = *reinterpret_cast<const uint4*>(&sm.Bs[slot][kk + 1][64 + 4 * tx]);
-#pragma unroll
-      for (int r = 0; r < 8; r++)
-#pragma unroll
-        for (int q = 0; q < 8; q++) acc[r][q] = __vimin3_u32(acc[r][q], a0[r] + b0[q], a1[r] + b1[q]);
-    }
-    const int64_t wc = c % W32_WIN;
-    if (c == 0) {
-      asm volatile("cp.async.wait_all;\n" ::);
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < 8; r++) {
-        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const uint4 w = *reinterpret_cast<const uint4*>(&sm.Cs[ri][64 * h + 4 * tx]);
-          acc[r][4 * h] = min(acc[r][4 * h], w.x << W32_TAG);
-          acc[r][4 * h + 1] = min(acc[r][4 * h + 1], w.y << W32_TAG);
-          acc[r][4 * h + 2] = min(acc[r][4 * h + 2], w.z << W32_TAG);
-          acc[r][4 * h + 3] = min(acc[r][4 * h + 3], w.w << W32_TAG);
-        }
-      }
-    }
-    if (wc == W32_WIN - 1 || c + 1 == nch) {
-      uint32_t any = 0;
-#pragma unroll
-      for (int r = 0; r < 8; r++)
-#pragma unroll
-        for (int q = 0; q < 8; q++) any |= acc[r][q];
-      if (__any_sync(0xffffffffu, any & TMASK)) {
-        const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
-#pragma unroll
-        for (int r = 0; r < 8; r++)
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const uint32_t t0 = acc[r][2 * q] & TMASK, t1 = acc[r][2 * q + 1] & TMASK;
-            const uint32_t tg = __byte_perm(t0, t1, 0x5410);
-            const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
-            kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
-            acc[r][2 * q] -= t0;
-            acc[r][2 * q + 1] -= t1;
-          }
-      }
-    }
-    __syncthreads();   // every warp is done with this slot
-    if (t == 0 && c + W32_STAGES < nch) issue(c + W32_STAGES);
-  }
-  bool changed = false;
-  const int32_t* __restrict__ pb = p.predB;
-  int32_t* __restrict__ out = p.idx;
-  int32_t* Cw = static_cast<int32_t*>(p.C);
-  const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
-    int32_t pv[2][4];
-    uint32_t ks[2][4];
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const uint32_t k0 = kst[r][2 * h], k1 = kst[r][2 * h + 1];
-      ks[h][0] = k0 & 0xFFFF; ks[h][1] = k0 >> 16; ks[h][2] = k1 & 0xFFFF; ks[h][3] = k1 >> 16;
-      const int64_t j = j0 + 64 * h + 4 * tx;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        pv[h][q] = 0;
-        if (out && ks[h][q] != 0u)
-          pv[h][q] = (p.mode == IDX_PRED) ? __ldg(pb + int64_t(ks[h][q] - 1u) * p.ldp + j + q)
-                                          : int32_t(p.inner_off + ks[h][q] - 1u);
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      if ((kst[r][2 * h] | kst[r][2 * h + 1]) == 0u) continue;
-      changed = true;
-      const int64_t j = j0 + 64 * h + 4 * tx;
-      const int4 wv = make_int4(int32_t(acc[r][4 * h] >> W32_TAG), int32_t(acc[r][4 * h + 1] >> W32_TAG),
-                                int32_t(acc[r][4 * h + 2] >> W32_TAG), int32_t(acc[r][4 * h + 3] >> W32_TAG));
-      int4* dstv = reinterpret_cast<int4*>(Cw + i * p.ldc + j);
-      *dstv = wv;
-      for (int pr = 0; pr < p.npeers; pr++)
-        *reinterpret_cast<int4*>(reinterpret_cast<char*>(dstv) + p.peer_dC[pr]) = wv;
-      if (!out) continue;
-      if (ks[h][0] && ks[h][1] && ks[h][2] && ks[h][3] && idx_vec) {
-        const int4 w = make_int4(pv[h][0], pv[h][1], pv[h][2], pv[h][3]);
-        int4* dst = reinterpret_cast<int4*>(out + i * p.ldi + j);
-        *dst = w;
-        for (int pr = 0; pr < p.npeers; pr++)
-          *reinterpret_cast<int4*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = w;
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; q++)
-          if (ks[h][q] != 0u) {
-            int32_t* dst = out + i * p.ldi + j + q;
-            *dst = pv[h][q];
-            for (int pr = 0; pr < p.npeers; pr++)
-              *reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]) = pv[h][q];
-          }
-      }
-    }
-  }
-  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
-}
-
-// RAW: plain 32-bit copies in the same layout (the exact fp32 tier); else w32 keys v << 7
-template <bool RAW>
-__device__ __forceinline__ void prep_w32_a_body(const int32_t* A, int64_t lda, int64_t nch, uint32_t* Aprep,
-                                                int64_t rt, int64_t c) {
-  const int t = threadIdx.x, r = t & 127, kb = 16 * (t >> 7);
-  const int4* src = reinterpret_cast<const int4*>(A + (rt * BM + r) * lda + c * SUB + kb);
-  uint32_t* dst = Aprep + (rt * nch + c) * (SUB * BM);
-  int32_t v[16];
-#pragma unroll
-  for (int q = 0; q < 4; q++) reinterpret_cast<int4*>(v)[q] = __ldg(src + q);
-#pragma unroll
-  for (int q = 0; q < 16; q++) dst[(kb + q) * BM + r] = RAW ? uint32_t(v[q]) : uint32_t(v[q]) << W32_TAG;
-}
-
-template <bool RAW>
-__device__ __forceinline__ void prep_w32_b_body(const int32_t* B, int64_t ldb, int64_t nch, uint32_t* Bprep,
-                                                int64_t ct, int64_t c) {
-  const int t = threadIdx.x, kk = t >> 3, cb = 16 * (t & 7);
-  const int4* src = reinterpret_cast<const int4*>(B + (c * SUB + kk) * ldb + ct * BN + cb);
-  const uint32_t tag = uint32_t(SUB * (c % W32_WIN) + kk + 1);   // 1..96 inside a decode window
-  uint4* dst = reinterpret_cast<uint4*>(Bprep + (ct * nch + c) * (SUB * BN) + kk * BN + cb);
-#pragma unroll
-  for (int q = 0; q < 4; q++) {
-    const int4 v = __ldg(src + q);
-    if constexpr (RAW) dst[q] = make_uint4(uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w));
-    else
-      dst[q] = make_uint4((uint32_t(v.x) << W32_TAG) | tag, (uint32_t(v.y) << W32_TAG) | tag,
-                          (uint32_t(v.z) << W32_TAG) | tag, (uint32_t(v.w) << W32_TAG) | tag);
-  }
-}
-
-// 3-input fp32 min (FMNMX3 on sm_100)
-__device__ __forceinline__ float fmin3(float a, float b, float c) {
-  float d;
-  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-
-// ------------------------------------------------------------------------------------
-// exact fp32 tier, deferred argmin: per 32-k chunk the min runs as FADD + FMNMX3 (1.5 instr per
-// update, no compare-select); cells whose value improved in the chunk then rescan that chunk
-// -- still in shared memory -- for the FIRST k whose (bitwise identical) sum equals the new min.
-// Strict improvement across chunks keeps the older k on ties, so the result equals the
-// compare-select kernel exactly.  The rescan is a per-lane loop over the improved cells
-// (targets and k staged in shared memory, so no dynamic register indexing).
-// Tile 128 x 64, 256 threads, 4 x 8 cells each; 1 CTA / SM.
-// ------------------------------------------------------------------------------------
-constexpr int DM_BN = 64, DM_STAGES = 2;
-constexpr uint32_t DM_CHUNK_A = SUB * BM * 4, DM_CHUNK_B = SUB * DM_BN * 4;
-struct SmemF32DM {   // 96 KB: 2 CTAs / SM
-  float As[DM_STAGES][SUB][BM];
-  float Bs[DM_STAGES][SUB][DM_BN];
-  float Cs[BM * DM_BN];         // the old C tile; after the chunk-0 merge, the rescan targets
-  uint16_t kid[NT][32];         // 0-based k of the last strict improvement, 0xFFFF = none
-  unsigned long long bar[DM_STAGES];
-  unsigned int done[DM_STAGES];  // warps finished with the slot's chunk
-};
-// rescan target slot of (thread, cell): swizzled so the 32 lanes hit 32 banks for a common cell
-__device__ __forceinline__ int dm_tgt(int t, int cell) { return t * 32 + ((cell + t) & 31); }
-
-__global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
-  extern __shared__ __align__(128) unsigned char smraw_dm[];
-  SmemF32DM& sm = *reinterpret_cast<SmemF32DM*>(smraw_dm);
-  int64_t i0, j0;
-  tile_origin(p, BM, DM_BN, i0, j0);
-  if (tile_skipped(p, i0, j0, BM, DM_BN)) return;
-  const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
-  const int64_t nch = p.k / SUB;
-  const float* Ap = reinterpret_cast<const float*>(p.Aprep) + (i0 / BM) * nch * (SUB * BM);
-  const float* Bp = static_cast<const float*>(p.Bprep) + (j0 / DM_BN) * nch * (SUB * DM_BN);
-  auto issue = [&](int64_t c) {
-    const int slot = int(c % DM_STAGES);
-    mbar_expect_tx(&sm.bar[slot], DM_CHUNK_A + DM_CHUNK_B);
-    bulk_g2s(&sm.As[slot][0][0], Ap + c * (SUB * BM), DM_CHUNK_A, &sm.bar[slot]);
-    bulk_g2s(&sm.Bs[slot][0][0], Bp + c * (SUB * DM_BN), DM_CHUNK_B, &sm.bar[slot]);
-  };
-  if (t == 0) {
-    for (int s = 0; s < DM_STAGES; s++) {
-      mbar_init(&sm.bar[s], 1);
-      sm.done[s] = 0;
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int64_t c = 0; c < DM_STAGES && c < nch; c++) issue(c);
-  }
-  __syncthreads();
-  {  // C tile -> smem (merged after chunk 0): row t >> 1, half (t & 1) of 64 floats
-    const int r = t >> 1;
-    const char* src = reinterpret_cast<const char*>(static_cast<const float*>(p.C) + (i0 + r) * p.ldc + j0) +
-                      128 * (t & 1);
-    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r * DM_BN]) + 128 * (t & 1));
-#pragma unroll
-    for (int q = 0; q < 8; q++)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
-#pragma unroll
-  for (int c = 0; c < 32; c++) sm.kid[t][c] = 0xFFFF;
-  float acc[4][8];
-#pragma unroll
-  for (int r = 0; r < 4; r++)
-#pragma unroll
-    for (int q = 0; q < 8; q++) acc[r][q] = __int_as_float(0x7f800000);
-  for (int64_t c = 0; c < nch; c++) {
-    const int slot = int(c % DM_STAGES);
-    mbar_wait(&sm.bar[slot], uint32_t((c / DM_STAGES) & 1));
-    float old[4][8];
-#pragma unroll
-    for (int r = 0; r < 4; r++)
-#pragma unroll
-      for (int q = 0; q < 8; q++) old[r][q] = acc[r][q];
-#pragma unroll 4
-    for (int kk = 0; kk < SUB; kk += 2) {
-      float a0[4], a1[4], b0[8], b1[8];
-      *reinterpret_cast<float4*>(a0) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][4 * ty]);
-      *reinterpret_cast<float4*>(a1) = *reinterpret_cast<const float4*>(&sm.As[slot][kk + 1][4 * ty]);
-      *reinterpret_cast<float4*>(b0) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][8 * tx]);
-      *reinterpret_cast<float4*>(b0 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][8 * tx + 4]);
-      *reinterpret_cast<float4*>(b1) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][8 * tx]);
-      *reinterpret_cast<float4*>(b1 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][8 * tx + 4]);
-#pragma unroll
-      for (int r = 0; r < 4; r++)
-#pragma unroll
-        for (int q = 0; q < 8; q++) acc[r][q] = fmin3(acc[r][q], a0[r] + b0[q], a1[r] + b1[q]);
-    }
-    uint32_t mask = 0;
-    if (c == 0) {   // improvement is against the old C (which wins ties)
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const float4 w0 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 8 * tx]);
-        const float4 w1 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 8 * tx + 4]);
-        const float cv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          if (acc[r][q] < cv[q]) mask |= 1u << (8 * r + q);
-          else acc[r][q] = cv[q];
-        }
-      }
-      __syncthreads();   // the C tile is consumed: its space now holds the rescan targets
-    } else {
-#pragma unroll
-      for (int r = 0; r < 4; r++)
-#pragma unroll
-        for (int q = 0; q < 8; q++)
-          if (acc[r][q] < old[r][q]) mask |= 1u << (8 * r + q);
-    }
-    if (__any_sync(0xffffffffu, mask != 0u)) {
-      if (mask) {
-#pragma unroll
-        for (int r = 0; r < 4; r++)
-#pragma unroll
-          for (int q = 0; q < 8; q++) sm.Cs[dm_tgt(t, 8 * r + q)] = acc[r][q];
-      }
-      const int kb = int(c) * SUB;
-      while (mask) {   // per-lane loop over this lane's improved cells
-        const int cell = __ffs(mask) - 1;
-        mask &= mask - 1;
-        const int row = 4 * ty + (cell >> 3), col = 8 * tx + (cell & 7);
-        const float target = sm.Cs[dm_tgt(t, cell)];
-        int found = 0;
-        for (int kk = 0; kk < SUB; kk++)
-          if (sm.As[slot][kk][row] + sm.Bs[slot][kk][col] == target) {
-            found = kk;
-            break;
-          }
-        sm.kid[t][cell] = uint16_t(kb + found);
-      }
-    }
-    __syncwarp();
-    if ((t & 31) == 0) {   // count this warp out of the slot; the last one refills it
-      __threadfence_block();
-      if (atomicAdd(&sm.done[slot], 1u) == NT / 32 - 1) {
-        __threadfence_block();
-        sm.done[slot] = 0;
-        if (c + DM_STAGES < nch) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(c + DM_STAGES);
-        }
-      }
-    }
-  }
-  bool changed = false;
-  float* Cw = static_cast<float*>(p.C);
-#pragma unroll
-  for (int r = 0; r < 4; r++) {
-    const int64_t i = i0 + 4 * ty + r;
-#pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const uint32_t k = sm.kid[t][8 * r + q];
-      if (k == 0xFFFFu) continue;
-      changed = true;
-      const int64_t j = j0 + 8 * tx + q;
-      Cw[i * p.ldc + j] = acc[r][q];
-      if (p.idx)
-        p.idx[i * p.ldi + j] =
-            (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(k) * p.ldp + j) : int32_t(p.inner_off + k);
-    }
-  }
-  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
-}
-
-// B (k x n) fp32 -> [n/64][k/32][32][64] for the deferred-argmin kernel
-__device__ __forceinline__ void prep_f32_b64_body(const float* B, int64_t ldb, int64_t nch, float* Bprep,
-                                                  int64_t ct, int64_t c) {
-  const int t = threadIdx.x, kk = t >> 3, cb = 8 * (t & 7);
-  const float4* src = reinterpret_cast<const float4*>(B + (c * SUB + kk) * ldb + ct * DM_BN + cb);
-  float4* dst = reinterpret_cast<float4*>(Bprep + (ct * nch + c) * (SUB * DM_BN) + kk * DM_BN + cb);
-  dst[0] = __ldg(src);
-  dst[1] = __ldg(src + 1);
-}
-
-bool f32_deferred() {
-  static const bool on = !getenv("APSP_F32_KERNEL") || std::string(getenv("APSP_F32_KERNEL")) != "nt";
-  return on;
-}
-
-size_t prep_bytes(int64_t m, int64_t n, int64_t k) {   // A keys + B keys (uint32 B keys for w32)
-  return ((size_t(m) * k * 4 + 255) / 256) * 256 + size_t(k) * n * 4 + 256;
-}
-
-// Both panel layouts in ONE launch (one dependent launch fewer on the per-round chain):
-// blockIdx = (chunk, tile, part) with part 0 the A rows and part 1 the B columns.
-enum PrepKind : int { PREP_U8 = 0, PREP_U16 = 1, PREP_W32 = 2, PREP_F32 = 3, PREP_F32_DM = 4 };
-template <int KIND>
-__global__ void __launch_bounds__(NT) prep_pair_kernel(const void* A, int64_t lda, const void* B, int64_t ldb,
-                                                       int64_t nch, int64_t nta, int64_t ntb, uint32_t* Aprep,
-                                                       void* Bprep) {
-  const int64_t c = blockIdx.x, tile = blockIdx.y;
-  if (blockIdx.z == 0) {
-    if (tile >= nta) return;
-    if constexpr (KIND == PREP_U8) prep_nt_a_body<STORE_U8>(static_cast<const uint8_t*>(A), lda, nch, Aprep, tile, c);
-    else if constexpr (KIND == PREP_U16)
-      prep_nt_a_body<STORE_U16>(static_cast<const uint16_t*>(A), lda, nch, Aprep, tile, c);
-    else if constexpr (KIND == PREP_W32) prep_w32_a_body<false>(static_cast<const int32_t*>(A), lda, nch, Aprep, tile, c);
-    else prep_w32_a_body<true>(static_cast<const int32_t*>(A), lda, nch, Aprep, tile, c);
-  } else {
-    if (tile >= ntb) return;
-    if constexpr (KIND == PREP_U8)
-      prep_nt_b_body<STORE_U8>(static_cast<const uint8_t*>(B), ldb, nch, static_cast<uint16_t*>(Bprep), tile, c);
-    else if constexpr (KIND == PREP_U16)
-      prep_nt_b_body<STORE_U16>(static_cast<const uint16_t*>(B), ldb, nch, static_cast<uint16_t*>(Bprep), tile, c);
-    else if constexpr (KIND == PREP_W32)
-      prep_w32_b_body<false>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep), tile, c);
-    else if constexpr (KIND == PREP_F32)
-      prep_w32_b_body<true>(static_cast<const int32_t*>(B), ldb, nch, static_cast<uint32_t*>(Bprep), tile, c);
-    else prep_f32_b64_body(static_cast<const float*>(B), ldb, nch, static_cast<float*>(Bprep), tile, c);
-  }
-}
-
-int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
-                     int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s) {
-  const size_t es = (store == STORE_W32 || store == STORE_F32) ? 4 : store == STORE_U16 ? 2 : 1;
-  if (m % BM || n % BN || k % SUB || (lda * es) % 16 || (ldb * es) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
-      (reinterpret_cast<uintptr_t>(B) & 15))
-    return set_error(2, "panel prep needs 128-multiple m/n, 32-multiple k and 16-byte aligned panels");
-  const int64_t nch = k / SUB, nta = m / BM;
-  const bool dm = store == STORE_F32 && f32_deferred();
-  const int64_t ntb = n / (dm ? DM_BN : BN);
-  const dim3 g(unsigned(nch), unsigned(std::max(nta, ntb)), 2);
-  switch (store) {
-    case STORE_U8: prep_pair_kernel<PREP_U8><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
-    case STORE_U16: prep_pair_kernel<PREP_U16><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
-    case STORE_W32: prep_pair_kernel<PREP_W32><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
-    case STORE_F32:
-      if (dm) prep_pair_kernel<PREP_F32_DM><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep);
-      else prep_pair_kernel<PREP_F32><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep);
-      break;
-    default:
-      return set_error(2, "panel prep is for the u8 / u16 / w32 / f32 tiers");
-  }
-  APSP_CUDA_TRY(cudaGetLastError());
-  count_launches(1);
-  return 0;
-}
-
-static dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
-  if (a.only_lo < a.only_hi) {   // the cross of rows and columns [lo, hi) (tile_origin's enumeration)
-    const int64_t wr = (a.only_hi - a.only_lo) / bm, wc = (a.only_hi - a.only_lo) / bn;
-    const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
-    return dim3(unsigned(wr * nt_c + (nt_r - wr) * wc), 1);
-  }
-  return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
-}
-
-// ------------------------------------------------------------------------------------
-// exact fp32 tier with pre-laid-out panels (continuous weights): compare-select per update,
-// strict < keeps the smallest k.  8 x 8 cells per thread with a 32-bit k per cell; same
-// cp.async.bulk ring as the w32 tier; 1 CTA / SM.
-// ------------------------------------------------------------------------------------
-struct SmemF32NT {
-  float As[W32_STAGES][SUB][BM];
-  float Bs[W32_STAGES][SUB][BN];
-  float Cs[BM][BN];
-  unsigned long long bar[W32_STAGES];
-};
-
-__global__ void __launch_bounds__(NT, 1) minplus_f32nt_kernel(MinplusArgs p) {
-  extern __shared__ __align__(128) unsigned char smraw_f32[];
-  SmemF32NT& sm = *reinterpret_cast<SmemF32NT*>(smraw_f32);
-  int64_t i0, j0;
-  tile_origin(p, BM, BN, i0, j0);
-  if (tile_skipped(p, i0, j0, BM, BN)) return;
-  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  const int64_t nch = p.k / SUB;
-  const float* Ap = reinterpret_cast<const float*>(p.Aprep) + (i0 / BM) * nch * (SUB * BM);
-  const float* Bp = static_cast<const float*>(p.Bprep) + (j0 / BN) * nch * (SUB * BN);
-  if (t == 0) {
-    for (int s = 0; s < W32_STAGES; s++) mbar_init(&sm.bar[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int64_t c) {
-    const int slot = int(c % W32_STAGES);
-    mbar_expect_tx(&sm.bar[slot], 2 * W32_CHUNK);
-    bulk_g2s(&sm.As[slot][0][0], Ap + c * (SUB * BM), W32_CHUNK, &sm.bar[slot]);
-    bulk_g2s(&sm.Bs[slot][0][0], Bp + c * (SUB * BN), W32_CHUNK, &sm.bar[slot]);
-  };
-  if (t == 0)
-    for (int64_t c = 0; c < W32_STAGES && c < nch; c++) issue(c);
-  {  // C tile -> smem (merged after chunk 0)
-    const int r = t >> 1;
-    const char* src = reinterpret_cast<const char*>(static_cast<const float*>(p.C) + (i0 + r) * p.ldc + j0) +
-                      256 * (t & 1);
-    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r][0]) + 256 * (t & 1));
-#pragma unroll
-    for (int q = 0; q < 16; q++)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
-  float acc[8][8];
-  int32_t kid[8][8];
-#pragma unroll
-  for (int r = 0; r < 8; r++)
-#pragma unroll
-    for (int q = 0; q < 8; q++) {
-      acc[r][q] = __int_as_float(0x7f800000);
-      kid[r][q] = -1;
-    }
-  for (int64_t c = 0; c < nch; c++) {
-    const int slot = int(c % W32_STAGES);
-    mbar_wait(&sm.bar[slot], uint32_t((c / W32_STAGES) & 1));
-    const int kb = int(c) * SUB;
-#pragma unroll 4
-    for (int kk = 0; kk < SUB; kk++) {
-      float a[8], b[8];
-      *reinterpret_cast<float4*>(a) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][4 * ty]);
-      *reinterpret_cast<float4*>(a + 4) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][64 + 4 * ty]);
-      *reinterpret_cast<float4*>(b) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][4 * tx]);
-      *reinterpret_cast<float4*>(b + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][64 + 4 * tx]);
-      const int kg = kb + kk;
-#pragma unroll
-      for (int r = 0; r < 8; r++)
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const float sv = a[r] + b[q];
-          if (sv < acc[r][q]) {
-            acc[r][q] = sv;
-            kid[r][q] = kg;
-          }
-        }
-    }
-    if (c == 0) {   // the old C wins ties: strict improvement only
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < 8; r++) {
-        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const float4 w = *reinterpret_cast<const float4*>(&sm.Cs[ri][64 * h + 4 * tx]);
-          const float cv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int q = 0; q < 4; q++)
-            if (!(acc[r][4 * h + q] < cv[q])) {
-              acc[r][4 * h + q] = cv[q];
-              kid[r][4 * h + q] = -1;
-            }
-        }
-      }
-    }
-    __syncthreads();   // every warp is done with this slot
-    if (t == 0 && c + W32_STAGES < nch) issue(c + W32_STAGES);
-  }
-  bool changed = false;
-  float* Cw = static_cast<float*>(p.C);
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-      const int64_t j = j0 + 64 * h + 4 * tx;
-      bool any = false;
-#pragma unroll
-      for (int q = 0; q < 4; q++) any |= kid[r][4 * h + q] >= 0;
-      if (!any) continue;
-      changed = true;
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        const int32_t k = kid[r][4 * h + q];
-        if (k < 0) continue;
-        Cw[i * p.ldc + j + q] = acc[r][4 * h + q];
-        if (p.idx)
-          p.idx[i * p.ldi + j + q] =
-              (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(k) * p.ldp + j + q) : int32_t(p.inner_off + k);
-      }
-    }
-  }
-  if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
-}
-
-static int launch_f32dm(const MinplusArgs& a, cudaStream_t s) {
-  static std::atomic<unsigned long long> attr{0};
-  APSP_CUDA_TRY(smem_optin(minplus_f32dm_kernel, int(sizeof(SmemF32DM)), attr));
-  if (a.m % BM || a.n % DM_BN || a.k % SUB || a.k > 65535 || (reinterpret_cast<uintptr_t>(a.C) & 15) ||
-      (a.ldc * 4) % 16)
-    return set_error(2, "deferred-argmin f32 tiles need 128 x 64 tiles and 32-multiple k");
-  minplus_f32dm_kernel<<<grid_for(a, BM, DM_BN), NT, sizeof(SmemF32DM), s>>>(a);
-  return 0;
-}
-
-static int launch_f32nt(const MinplusArgs& a, cudaStream_t s) {
-  static std::atomic<unsigned long long> attr{0};
-  APSP_CUDA_TRY(smem_optin(minplus_f32nt_kernel, int(sizeof(SmemF32NT)), attr));
-  if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * 4) % 16)
-    return set_error(2, "bulk-staged f32 tiles need full 128 x 128 tiles and 32-multiple k");
-  minplus_f32nt_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemF32NT), s>>>(a);
-  return 0;
-}
-
-static int launch_w32nt(const MinplusArgs& a, cudaStream_t s) {
-  static std::atomic<unsigned long long> attr{0};
-  APSP_CUDA_TRY(smem_optin(minplus_w32nt_kernel, int(sizeof(SmemW32NT)), attr));
-  if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * 4) % 16)
-    return set_error(2, "bulk-staged w32 tiles need full 128 x 128 tiles and 32-multiple k");
-  minplus_w32nt_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemW32NT), s>>>(a);
-  return 0;
-}
-
-template <int S>
-static int launch_nt(const MinplusArgs& a, cudaStream_t s) {
-  static std::atomic<unsigned long long> attr0{0}, attr1{0}, attr2{0};
-  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 0>, int(sizeof(SmemNT<S>)), attr0));
-  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 1>, int(sizeof(SmemNT<S>)), attr1));
-  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 2>, int(sizeof(SmemNT<S>)), attr2));
-  const size_t es = sizeof(typename Narrow<S>::T);
-  if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
-    return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
-  if (a.npeers && a.push_all) {
-    minplus_nt_kernel<S, 2><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
-  } else if (a.npeers) {
-    minplus_nt_kernel<S, 1><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
-  } else if (a.pdl) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid_for(a, BM, BN);
-    cfg.blockDim = dim3(NT);
-    cfg.dynamicSmemBytes = sizeof(SmemNT<S>);
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    APSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, minplus_nt_kernel<S, 0>, a));
-  } else {
-    minplus_nt_kernel<S, 0><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
-  }
-  return 0;
 }
 
 // ------------------------------------------------------------------------------------

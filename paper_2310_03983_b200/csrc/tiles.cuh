@@ -1,0 +1,137 @@
+// Shared device helpers of the min-plus tile kernels (minplus.cu: register-staged and exact
+// kernels plus the dispatch; minplus_bulk.cu: the bulk-staged kernels and their panel layouts).
+#pragma once
+#include <cstdint>
+#include "launch.h"
+
+namespace apsp {
+
+constexpr int BM = 128, BN = 128, NT = 256;
+#ifndef APSP_U8_UNROLL
+#define APSP_U8_UNROLL 32
+#endif
+constexpr int kU8Unroll = APSP_U8_UNROLL;
+
+// Tile origin of this CTA.  Full grid: (blockIdx.y, blockIdx.x).  Cross-list mode
+// (only_lo < only_hi): blockIdx.x enumerates the tiles of rows band + cols band [lo, hi)
+// (band width w tiles): first the w full tile rows, then the remaining rows of the w columns.
+__device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn, int64_t& i0, int64_t& j0) {
+  if (p.only_lo < p.only_hi) {   // tile counts fit 32 bits: 32-bit division (a 64-bit one is ~100 instr)
+    const int wr = int((p.only_hi - p.only_lo) / bm), lo_r = int(p.only_lo / bm);   // row band, in row tiles
+    const int wc = int((p.only_hi - p.only_lo) / bn), lo_c = int(p.only_lo / bn);   // col band, in col tiles
+    const int nt_c = int((p.n + bn - 1) / bn);
+    const int id = int(blockIdx.x);
+    if (id < wr * nt_c) {
+      i0 = int64_t(lo_r + id / nt_c) * bm;
+      j0 = int64_t(id % nt_c) * bn;
+    } else {
+      const int id2 = id - wr * nt_c, rr = id2 / wc, cc = id2 % wc;
+      i0 = int64_t(rr < lo_r ? rr : rr + wr) * bm;
+      j0 = int64_t(lo_c + cc) * bn;
+    }
+  } else {
+    i0 = int64_t(blockIdx.y) * bm;
+    j0 = int64_t(blockIdx.x) * bn;
+  }
+}
+
+__device__ __forceinline__ bool tile_skipped(const MinplusArgs& p, int64_t i0, int64_t j0, int bm, int bn) {
+  const bool rin = i0 >= p.skip_row_lo && i0 + bm <= p.skip_row_hi;
+  const bool cin = j0 >= p.skip_col_lo && j0 + bn <= p.skip_col_hi;
+  const bool r2 = i0 >= p.skip2_lo && i0 + bm <= p.skip2_hi;
+  const bool c2 = j0 >= p.skip2_lo && j0 + bn <= p.skip2_hi;
+  return rin || cin || r2 || c2;
+}
+
+__device__ __forceinline__ void emit_idx(const MinplusArgs& p, int64_t i, int64_t j, uint32_t kk) {
+  if (p.idx == nullptr) return;
+  int32_t v = (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(kk) * p.ldp + j) : int32_t(p.inner_off + kk);
+  p.idx[i * p.ldi + j] = v;
+}
+
+// u8 tier keys: 16-bit UNSIGNED, key = value << 7 | tag, tag = 1..64 over a 64-k decode window
+// (two 32-k chunks).  INF key = 255 << 7 = 32640; the largest sum INF + INF + tag = 65407 < 2^16.
+constexpr int U8_TAG = 7;
+constexpr uint32_t U8_KINF = uint32_t(U8_INF) << U8_TAG;
+constexpr uint32_t U8_TAGMASK2 = 0x007F007Fu;
+
+__device__ __forceinline__ uint32_t viaddmin_u16x2(uint32_t a, uint32_t b, uint32_t c) {
+  return __viaddmin_u16x2(a, b, c);
+}
+
+// 0xFFFF in each 16-bit half whose bit 15 is set, else 0 (PTX prmt sign replication; the
+// CUDA __byte_perm intrinsic masks selectors to 3 bits and cannot express it).
+__device__ __forceinline__ uint32_t prmt_sign_halves(uint32_t x) {
+  uint32_t d;
+  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(x));
+  return d;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// try_wait with a suspend-time hint: the waiting warp sleeps until the phase completes instead
+// of re-issuing the probe (a spinning producer warp steals issue slots from the ALU-bound
+// consumers on its SM sub-partition)
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+inline dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
+  if (a.only_lo < a.only_hi) {   // the cross of rows and columns [lo, hi) (tile_origin's enumeration)
+    const int64_t wr = (a.only_hi - a.only_lo) / bm, wc = (a.only_hi - a.only_lo) / bn;
+    const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
+    return dim3(unsigned(wr * nt_c + (nt_r - wr) * wc), 1);
+  }
+  return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
+}
+
+// 3-input fp32 min (FMNMX3 on sm_100)
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// bulk-staged launchers (minplus_bulk.cu)
+template <int S> int launch_nt(const MinplusArgs& a, cudaStream_t s);
+int launch_w32nt(const MinplusArgs& a, cudaStream_t s);
+int launch_f32nt(const MinplusArgs& a, cudaStream_t s);
+int launch_f32dm(const MinplusArgs& a, cudaStream_t s);
+bool f32_deferred();
+
+}  // namespace apsp
