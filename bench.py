@@ -400,8 +400,10 @@ def bench_e2e(lib, nat, h_np, n, args, block):
         call()
     dt = time.perf_counter() - t
     return {"value": n ** 3 * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": n * n * 4,
-            "d2h_bytes_per_step": 2 * n * n * 4, "ms_per_step": dt / args.steps * 1e3,
-            "api": "apsp_solve_host (C ABI, host buffers; synchronous like the reference solvers)"}
+            "d2h_bytes_per_step": n * n * info.d2h_bytes_per_cell, "ms_per_step": dt / args.steps * 1e3,
+            "api": "apsp_solve_host (C ABI, host buffers; synchronous like the reference solvers)",
+            "readback": "int32 dist + pred into the caller's buffers; the result crosses PCIe narrowed "
+                        f"({info.d2h_bytes_per_cell} B/cell) and host threads widen it (csrc/hostio.cu)"}
 
 
 if __name__ == "__main__":

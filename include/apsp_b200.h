@@ -76,7 +76,7 @@ typedef struct apsp_info {
   int32_t kernel_launches; /* profiled min-plus tile launches (apsp_set_profiling(1)) */
   double kernel_ms;     /* summed CUDA-event time of those launches */
   int32_t block;        /* pivot block used by the blocked FW (0 otherwise) */
-  int32_t reserved;
+  int32_t d2h_bytes_per_cell; /* apsp_solve_host: result bytes per cell read back (dist + idx) */
 } apsp_info;
 
 const char* apsp_last_error(void);

@@ -80,7 +80,7 @@ class ApspInfo(ctypes.Structure):
         ("kernel_launches", ctypes.c_int32),
         ("kernel_ms", ctypes.c_double),
         ("block", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("d2h_bytes_per_cell", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -96,6 +96,7 @@ class ApspInfo(ctypes.Structure):
             "kernel_launches": self.kernel_launches,
             "kernel_ms": self.kernel_ms,
             "block": self.block,
+            "d2h_bytes_per_cell": self.d2h_bytes_per_cell,
         }
 
 

@@ -178,16 +178,30 @@ int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* di
   if (e == cudaSuccess && idx_dtype == APSP_DTYPE_I64 && idx_out) e = cudaMallocAsync(&pw, size_t(n) * n * 8, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return fail(set_cuda_error(e, "host staging", __FILE__, __LINE__));
+  apsp_info local{};
+  local.max_finite = -1;   // stays -1 (no packed readback) unless the solver reports it
   switch (algorithm) {
-    case APSP_ALG_FW_BLOCKED: rc = fw_blocked_impl(dtype, n, d, n, p, n, block, tier, nullptr, 0, s, info); break;
-    case APSP_ALG_FW_CLASSIC: rc = fw_classic_impl(dtype, n, d, n, p, n, s, info); break;
+    case APSP_ALG_FW_BLOCKED: rc = fw_blocked_impl(dtype, n, d, n, p, n, block, tier, nullptr, 0, s, &local); break;
+    case APSP_ALG_FW_CLASSIC: rc = fw_classic_impl(dtype, n, d, n, p, n, s, &local); break;
     case APSP_ALG_RKLEENE:
-      rc = rkleene_impl(dtype, n, d, n, p, n, idx_mode, base_threshold, aligned, tier, nullptr, 0, s, info);
+      rc = rkleene_impl(dtype, n, d, n, p, n, idx_mode, base_threshold, aligned, tier, nullptr, 0, s, &local);
       break;
-    case APSP_ALG_FW_SQUARING: rc = squaring_impl(dtype, n, d, n, p, n, tier, nullptr, 0, s, info); break;
+    case APSP_ALG_FW_SQUARING: rc = squaring_impl(dtype, n, d, n, p, n, tier, nullptr, 0, s, &local); break;
     default: rc = set_error(APSP_EINVAL, "unknown algorithm %d", algorithm);
   }
+  if (info) *info = local;
   if (rc) return fail(rc);
+  if (dtype == APSP_DTYPE_I32) {
+    bool done = false;
+    rc = readback_packed(n, static_cast<const int32_t*>(d), idx_out ? p : nullptr, local.max_finite, dist_out,
+                         idx_out, idx_dtype, s, done);
+    if (rc) return fail(rc);
+    if (done) {
+      if (info) info->d2h_bytes_per_cell = readback_width(n, local.max_finite, idx_out != nullptr, idx_dtype);
+      return fail(0);
+    }
+  }
+  if (info) info->d2h_bytes_per_cell = int32_t(es + (idx_out ? (idx_dtype == APSP_DTYPE_I64 ? 8 : 4) : 0));
   e = cudaMemcpyAsync(dist_out, d, bytes, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && idx_out) {
     if (idx_dtype == APSP_DTYPE_I64) {

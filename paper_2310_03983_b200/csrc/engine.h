@@ -240,4 +240,9 @@ int rk_shard_product_impl(int tier, const void* A, int64_t lda, const void* B, i
                           cudaStream_t s, int npeers = 0, const int64_t* peer_dc = nullptr,
                           const int64_t* peer_di = nullptr);
 
+// hostio.cu: narrowed device->host readback of an int32 result (apsp_solve_host).
+int readback_packed(int64_t n, const int32_t* d, const int32_t* p, int64_t max_finite, void* dist_out, void* idx_out,
+                    int idx_dtype, cudaStream_t s, bool& handled);
+int32_t readback_width(int64_t n, int64_t max_finite, bool idx, int idx_dtype);   // bytes per cell when handled
+
 }  // namespace apsp

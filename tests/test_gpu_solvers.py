@@ -436,3 +436,40 @@ def test_results_independent_of_tile_size_and_workers(cuda):
     for tile_size in (1, 64):
         r = ap.rkleene(h, base_threshold=16, tile_size=tile_size, workers=2)
         assert np.array_equal(r.via.raw, base_r.via.raw)
+
+
+@pytest.mark.parametrize("alpha", [100, 3000, 10 ** 6])
+def test_host_readback_narrowed_equals_device_result(cuda, alpha, monkeypatch):
+    """apsp_solve_host narrows the int32 result for the PCIe readback (csrc/hostio.cu): 1 byte
+    (u8 range), 2 bytes (u16 range) or none (wide) for dist, 2 bytes for pred. The host arrays
+    must equal the device-resident result and the plain int32 readback, cell for cell. n=2050
+    makes every row start 8 bytes off a 16-byte boundary (scalar heads in the widening loops)."""
+    import ctypes
+
+    import torch
+    from paper_2310_03983_b200 import _native as nat
+
+    n = 2050
+    h32 = ap.dense_costs(ap.GenParams(n, 0.1, alpha, 11 + alpha), np.int32)
+    dev = ap.solve(torch.from_numpy(h32).cuda())
+    want_d, want_p = dev.distances.cpu().numpy(), dev.index.cpu().numpy()
+    r = ap.solve(h32)
+    m = r.info["max_finite"]
+    width = 1 if m <= 254 else 2 if m <= 65534 else 4
+    assert width == {100: 1, 3000: 2, 10 ** 6: 4}[alpha] or alpha == 3000
+    assert np.array_equal(r.distances, want_d) and np.array_equal(r.index, want_p)
+    lib = nat.load()
+    info = nat.ApspInfo()
+    d = np.empty((n, n), np.int32)
+    p64 = np.empty((n, n), np.int64)
+    st = lib.apsp_solve_host(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, h32.ctypes.data, d.ctypes.data, p64.ctypes.data,
+                             nat.DTYPE_I64, nat.IDX_PRED, 0, 0, 0, nat.TIER_AUTO, 0, ctypes.byref(info))
+    nat.check(st)
+    assert info.d2h_bytes_per_cell == width + 2
+    assert np.array_equal(d, want_d) and np.array_equal(p64, want_p.astype(np.int64))
+    monkeypatch.setenv("APSP_PACKED_READBACK", "0")
+    st = lib.apsp_solve_host(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, h32.ctypes.data, d.ctypes.data, p64.ctypes.data,
+                             nat.DTYPE_I64, nat.IDX_PRED, 0, 0, 0, nat.TIER_AUTO, 0, ctypes.byref(info))
+    nat.check(st)
+    assert info.d2h_bytes_per_cell == 12
+    assert np.array_equal(d, want_d) and np.array_equal(p64, want_p.astype(np.int64))
