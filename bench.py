@@ -399,11 +399,12 @@ def bench_e2e(lib, nat, h_np, n, args, block):
     for _ in range(args.steps):
         call()
     dt = time.perf_counter() - t
-    return {"value": n ** 3 * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": n * n * 4,
+    return {"value": n ** 3 * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": n * n * info.h2d_bytes_per_cell,
             "d2h_bytes_per_step": n * n * info.d2h_bytes_per_cell, "ms_per_step": dt / args.steps * 1e3,
             "api": "apsp_solve_host (C ABI, host buffers; synchronous like the reference solvers)",
-            "readback": "int32 dist + pred into the caller's buffers; the result crosses PCIe narrowed "
-                        f"({info.d2h_bytes_per_cell} B/cell) and host threads widen it (csrc/hostio.cu)"}
+            "transfers": "int32 costs in, int32 dist + pred out, in the caller's buffers; both cross PCIe "
+                         f"narrowed ({info.h2d_bytes_per_cell} B/cell up, {info.d2h_bytes_per_cell} B/cell down) "
+                         "with host threads packing / widening chunks beside the copies (csrc/hostio.cu)"}
 
 
 if __name__ == "__main__":

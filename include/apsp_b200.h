@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define APSP_ABI_VERSION 1
+#define APSP_ABI_VERSION 2
 
 typedef enum {
   APSP_OK = 0,
@@ -77,6 +77,8 @@ typedef struct apsp_info {
   double kernel_ms;     /* summed CUDA-event time of those launches */
   int32_t block;        /* pivot block used by the blocked FW (0 otherwise) */
   int32_t d2h_bytes_per_cell; /* apsp_solve_host: result bytes per cell read back (dist + idx) */
+  int32_t h2d_bytes_per_cell; /* apsp_solve_host: cost bytes per cell uploaded */
+  int32_t reserved;
 } apsp_info;
 
 const char* apsp_last_error(void);

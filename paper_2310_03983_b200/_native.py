@@ -81,6 +81,8 @@ class ApspInfo(ctypes.Structure):
         ("kernel_ms", ctypes.c_double),
         ("block", ctypes.c_int32),
         ("d2h_bytes_per_cell", ctypes.c_int32),
+        ("h2d_bytes_per_cell", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -97,6 +99,7 @@ class ApspInfo(ctypes.Structure):
             "kernel_ms": self.kernel_ms,
             "block": self.block,
             "d2h_bytes_per_cell": self.d2h_bytes_per_cell,
+            "h2d_bytes_per_cell": self.h2d_bytes_per_cell,
         }
 
 
@@ -173,7 +176,7 @@ def load(require_gpu: bool = True):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.apsp_abi_version() != 1:
+        if lib.apsp_abi_version() != 2:
             raise NativeUnavailableError("libapsp_b200.so ABI version mismatch")
         _lib = lib
     if require_gpu:

@@ -176,7 +176,14 @@ int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* di
   cudaError_t e = cudaMallocAsync(&d, bytes, s);
   if (e == cudaSuccess) e = cudaMallocAsync((void**)&p, size_t(n) * n * 4, s);
   if (e == cudaSuccess && idx_dtype == APSP_DTYPE_I64 && idx_out) e = cudaMallocAsync(&pw, size_t(n) * n * 8, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return fail(set_cuda_error(e, "host staging", __FILE__, __LINE__));
+  bool up = false;
+  int up_width = int(es);
+  if (dtype == APSP_DTYPE_I32) {
+    rc = upload_packed(n, static_cast<const int32_t*>(h), static_cast<int32_t*>(d), s, up, up_width);
+    if (rc) return fail(rc);
+  }
+  if (!up) e = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return fail(set_cuda_error(e, "host staging", __FILE__, __LINE__));
   apsp_info local{};
   local.max_finite = -1;   // stays -1 (no packed readback) unless the solver reports it
@@ -189,6 +196,7 @@ int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* di
     case APSP_ALG_FW_SQUARING: rc = squaring_impl(dtype, n, d, n, p, n, tier, nullptr, 0, s, &local); break;
     default: rc = set_error(APSP_EINVAL, "unknown algorithm %d", algorithm);
   }
+  local.h2d_bytes_per_cell = up ? up_width : int32_t(es);
   if (info) *info = local;
   if (rc) return fail(rc);
   if (dtype == APSP_DTYPE_I32) {

@@ -6,19 +6,19 @@
 // pass packs dist to 1 or 2 bytes (INF32 -> all-ones) and pred to 2 bytes (p + 1, so -1 -> 0).
 // The packed rows then come back in row chunks. Each chunk gets its own event, and a host worker
 // pool widens chunk c while chunk c+1 is still on the wire. The pool writes with streaming stores,
-// so the output lines are not read first. At n=16384 u8 this moves 768 MiB instead of 2 GiB.
+// so the output lines are not read first
+// (hostwiden.cpp, AVX-512 when the host has it). At n=16384 u8 this moves 768 MiB instead of 2 GiB.
 //
 // The pack kernel flags any value outside the promised width. A flagged result falls back to the
 // plain int32 copies, so the output is always the exact device result.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <mutex>
 #include <thread>
 #include <vector>
 #include <sched.h>
-#if defined(__SSE2__)
-#include <emmintrin.h>
-#endif
 #include "engine.h"
 
 namespace apsp {
@@ -56,78 +56,23 @@ __global__ void pack_result_kernel(const int32_t* __restrict__ d, const int32_t*
   if (flag) atomicOr(bad, 1);
 }
 
-// ---- host widening (streaming stores where the target is 16-byte aligned) ------------------
-
-template <typename T>
-inline bool aligned16(const T* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
-void widen_dist(const void* src, int dw, int32_t* dst, size_t cnt) {
-  size_t i = 0;
-  if (dw == 1) {
-    const uint8_t* s = static_cast<const uint8_t*>(src);
-    for (; i < cnt && !aligned16(dst + i); i++) dst[i] = s[i] == 0xFF ? kInf32 : s[i];
-#if defined(__SSE2__)
-    const __m128i z = _mm_setzero_si128(), m = _mm_set1_epi32(0xFF), inf = _mm_set1_epi32(kInf32);
-    for (; i + 16 <= cnt; i += 16) {
-      const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
-      const __m128i lo = _mm_unpacklo_epi8(b, z), hi = _mm_unpackhi_epi8(b, z);
-      const __m128i w[4] = {_mm_unpacklo_epi16(lo, z), _mm_unpackhi_epi16(lo, z), _mm_unpacklo_epi16(hi, z),
-                            _mm_unpackhi_epi16(hi, z)};
-      for (int q = 0; q < 4; q++) {
-        const __m128i e = _mm_cmpeq_epi32(w[q], m);
-        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 4 * q),
-                         _mm_or_si128(_mm_andnot_si128(e, w[q]), _mm_and_si128(e, inf)));
-      }
-    }
-#endif
-    for (; i < cnt; i++) dst[i] = s[i] == 0xFF ? kInf32 : s[i];
-  } else {
-    const uint16_t* s = static_cast<const uint16_t*>(src);
-    for (; i < cnt && !aligned16(dst + i); i++) dst[i] = s[i] == 0xFFFF ? kInf32 : s[i];
-#if defined(__SSE2__)
-    const __m128i z = _mm_setzero_si128(), m = _mm_set1_epi32(0xFFFF), inf = _mm_set1_epi32(kInf32);
-    for (; i + 8 <= cnt; i += 8) {
-      const __m128i h = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
-      const __m128i w[2] = {_mm_unpacklo_epi16(h, z), _mm_unpackhi_epi16(h, z)};
-      for (int q = 0; q < 2; q++) {
-        const __m128i e = _mm_cmpeq_epi32(w[q], m);
-        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 4 * q),
-                         _mm_or_si128(_mm_andnot_si128(e, w[q]), _mm_and_si128(e, inf)));
-      }
-    }
-#endif
-    for (; i < cnt; i++) dst[i] = s[i] == 0xFFFF ? kInf32 : s[i];
-  }
-}
-
-template <typename T>
-void widen_pred(const uint16_t* s, T* dst, size_t cnt) {
-  size_t i = 0;
-  for (; i < cnt && !aligned16(dst + i); i++) dst[i] = T(int32_t(s[i]) - 1);
-#if defined(__SSE2__)
-  const __m128i z = _mm_setzero_si128(), one = _mm_set1_epi32(1);
-  for (; i + 8 <= cnt; i += 8) {
-    const __m128i h = _mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i));
-    const __m128i w[2] = {_mm_sub_epi32(_mm_unpacklo_epi16(h, z), one), _mm_sub_epi32(_mm_unpackhi_epi16(h, z), one)};
-    for (int q = 0; q < 2; q++) {
-      if (sizeof(T) == 4) {
-        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 4 * q), w[q]);
-      } else {
-        const __m128i sg = _mm_srai_epi32(w[q], 31);
-        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 4 * q), _mm_unpacklo_epi32(w[q], sg));
-        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 4 * q + 2), _mm_unpackhi_epi32(w[q], sg));
-      }
-    }
-  }
-#endif
-  for (; i < cnt; i++) dst[i] = T(int32_t(s[i]) - 1);
-}
-
 // ---- pinned staging, grow-only, process-wide ------------------------------------------------
 
-std::mutex g_stage_mu;
-void* g_stage = nullptr;
-size_t g_stage_bytes = 0;
+struct Pinned {
+  std::mutex mu;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t reserve(size_t need) {   // caller holds mu
+    if (bytes >= need) return cudaSuccess;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    const cudaError_t e = cudaHostAlloc(&ptr, need, cudaHostAllocPortable);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+};
+Pinned g_down, g_up;   // readback / upload staging
 
 int host_workers() {
   if (const char* e = std::getenv("APSP_HOST_THREADS")) return std::max(1, std::atoi(e));
@@ -138,11 +83,114 @@ int host_workers() {
   return std::clamp(n, 1, 16);
 }
 
+// row chunks of a transfer: >= 16 of them, each at most 2048 rows
+int64_t chunk_rows(int64_t n) { return std::min<int64_t>(2048, std::max<int64_t>(1, (n + 15) / 16)); }
+
+template <int W>
+__global__ void widen_costs_kernel(const void* __restrict__ src, int32_t* __restrict__ d, int64_t cells) {
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < (cells >> 2);
+       g += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t x[4];
+    if (W == 1) {
+      const uint32_t w = reinterpret_cast<const uint32_t*>(src)[g];
+      for (int q = 0; q < 4; q++) x[q] = (w >> (8 * q)) & 0xFFu;
+    } else {
+      const uint2 w = reinterpret_cast<const uint2*>(src)[g];
+      x[0] = w.x & 0xFFFFu; x[1] = w.x >> 16; x[2] = w.y & 0xFFFFu; x[3] = w.y >> 16;
+    }
+    constexpr uint32_t ALL = W == 1 ? 0xFFu : 0xFFFFu;
+    int32_t o[4];
+    for (int q = 0; q < 4; q++) o[q] = x[q] == ALL ? INF32 : int32_t(x[q]);
+    reinterpret_cast<int4*>(d)[g] = make_int4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 int dist_width(int64_t max_finite) {
   return max_finite >= 0 && max_finite <= 254 ? 1 : max_finite >= 0 && max_finite <= 65534 ? 2 : 0;
 }
 
 }  // namespace
+
+void host_widen_dist(const void* src, int width, int32_t* dst, size_t cnt);   // hostwiden.cpp
+bool host_narrow_i32(const int32_t* src, void* dst, int width, size_t cnt);
+
+// Uploads the n x n int32 cost matrix h into the contiguous device buffer d narrowed: host
+// threads pack row chunks to u8 (or u16) while the previous chunks are on the wire, and one
+// device pass widens them back to int32 (all-ones -> INF32). The width comes from the first
+// rows; a later cell that does not fit aborts the packed upload (handled = false) and the caller
+// copies the int32 matrix as is. The device-side scan then sees exactly the caller's matrix.
+int upload_packed(int64_t n, const int32_t* h, int32_t* d, cudaStream_t s, bool& handled, int& width) {
+  handled = false;
+  width = 4;
+  const char* env = std::getenv("APSP_PACKED_UPLOAD");
+  if (env && env[0] == '0') return 0;
+  const int64_t cells = n * n;
+  if (cells < (int64_t(1) << 22) || cells % 4) return 0;
+  // width from the first rows (a bounded sample; the packing itself checks every cell)
+  const int64_t sample = std::min<int64_t>(n, 64) * n;
+  int32_t mx = 0;
+  for (int64_t i = 0; i < sample; i++) {
+    const int32_t v = h[i];
+    if (v == INF32) continue;
+    if (v < 0) return 0;
+    mx = std::max(mx, v);
+  }
+  const int w = mx <= 254 ? 1 : mx <= 65534 ? 2 : 0;
+  if (!w) return 0;
+  std::unique_lock<std::mutex> lk(g_up.mu);
+  APSP_CUDA_TRY(g_up.reserve(size_t(cells) * w));
+  char* st = static_cast<char*>(g_up.ptr);
+  void* dev = nullptr;
+  APSP_CUDA_TRY(cudaMallocAsync(&dev, size_t(cells) * w, s));
+  const int64_t rows = chunk_rows(n);
+  const int64_t nch = (n + rows - 1) / rows;
+  const int T = host_workers();
+  std::atomic<bool> abort{false};
+  std::atomic<int> cuerr{0};
+  std::vector<std::atomic<int>> pending(static_cast<size_t>(nch));
+  for (auto& x : pending) x = T;
+  auto work = [&](int t) {
+    for (int64_t c = 0; c < nch && !abort; c++) {
+      const int64_t r0 = c * rows, r1 = std::min(n, r0 + rows);
+      const int64_t a = r0 + (r1 - r0) * t / T, b = r0 + (r1 - r0) * (t + 1) / T;
+      if (a < b && !host_narrow_i32(h + a * n, st + size_t(a * n) * w, w, size_t((b - a) * n))) {
+        abort = true;
+        return;
+      }
+      if (pending[size_t(c)].fetch_sub(1) == 1 && !abort) {   // last slice of the chunk: ship it
+        const size_t off = size_t(r0 * n) * w, bytes = size_t((r1 - r0) * n) * w;
+        if (cudaMemcpyAsync(static_cast<char*>(dev) + off, st + off, bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+          cuerr = 1, abort = true;
+      }
+    }
+  };
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 1; t < T; t++) pool.emplace_back(work, t);
+  work(0);
+  for (auto& t : pool) t.join();
+  const auto t1 = std::chrono::steady_clock::now();
+  cudaError_t e = cuerr ? cudaErrorUnknown : cudaSuccess;
+  if (!abort) {
+    if (w == 1) widen_costs_kernel<1><<<148 * 8, 256, 0, s>>>(dev, d, cells);
+    else widen_costs_kernel<2><<<148 * 8, 256, 0, s>>>(dev, d, cells);
+    e = cudaGetLastError();
+    count_launches(1);
+  }
+  cudaFreeAsync(dev, s);
+  // the staging buffer is reused by the next call: its copies must have landed
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
+  if (std::getenv("APSP_READBACK_TRACE"))
+    std::fprintf(stderr, "[upload] n=%lld w=%d threads=%d abort=%d host pack %.2f ms, pack+copies+widen %.2f ms\n",
+                 (long long)n, w, T, int(abort.load()), std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  if (e != cudaSuccess) return set_cuda_error(e, "packed upload", __FILE__, __LINE__);
+  handled = !abort;
+  width = handled ? w : 4;
+  return 0;
+}
+void host_widen_pred(const uint16_t* src, void* dst, bool wide, size_t cnt);
 
 int32_t readback_width(int64_t n, int64_t max_finite, bool idx, int idx_dtype) {
   const int dw = dist_width(max_finite);
@@ -179,20 +227,12 @@ int readback_packed(int64_t n, const int32_t* d, const int32_t* p, int64_t max_f
     e = cudaGetLastError();
     count_launches(1);
   }
-  std::unique_lock<std::mutex> lk(g_stage_mu);
-  const size_t need = dbytes + pbytes + 64;
-  if (e == cudaSuccess && g_stage_bytes < need) {
-    if (g_stage) cudaFreeHost(g_stage);
-    g_stage = nullptr;
-    g_stage_bytes = 0;
-    e = cudaHostAlloc(&g_stage, need, cudaHostAllocPortable);
-    if (e == cudaSuccess) g_stage_bytes = need;
-  }
-  char* st = static_cast<char*>(g_stage);
+  std::unique_lock<std::mutex> lk(g_down.mu);
+  if (e == cudaSuccess) e = g_down.reserve(dbytes + pbytes + 64);
+  char* st = static_cast<char*>(g_down.ptr);
   volatile int* hbad = reinterpret_cast<volatile int*>(st + dbytes + pbytes);
   if (e == cudaSuccess) e = cudaMemcpyAsync((void*)hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
-  // row chunks: >= 16 of them, each at most 2048 rows
-  const int64_t rows = std::min<int64_t>(2048, std::max<int64_t>(1, (n + 15) / 16));
+  const int64_t rows = chunk_rows(n);
   const int64_t nch = (n + rows - 1) / rows;
   std::vector<cudaEvent_t> ev(size_t(nch), nullptr);
   for (int64_t c = 0; e == cudaSuccess && c < nch; c++) {
@@ -218,21 +258,28 @@ int readback_packed(int64_t n, const int32_t* d, const int32_t* p, int64_t max_f
         const int64_t a = r0 + (r1 - r0) * w / T, b = r0 + (r1 - r0) * (w + 1) / T;
         if (a == b) continue;
         const size_t off = size_t(a) * n, cnt = size_t(b - a) * n;
-        if (dw) widen_dist(st + off * dw, dw, static_cast<int32_t*>(dist_out) + off, cnt);
+        if (dw) host_widen_dist(st + off * dw, dw, static_cast<int32_t*>(dist_out) + off, cnt);
         if (pk) {
           const uint16_t* src = reinterpret_cast<const uint16_t*>(st + dbytes) + off;
-          if (idx_dtype == APSP_DTYPE_I64) widen_pred(src, static_cast<int64_t*>(idx_out) + off, cnt);
-          else widen_pred(src, static_cast<int32_t*>(idx_out) + off, cnt);
+          const bool wide = idx_dtype == APSP_DTYPE_I64;
+          host_widen_pred(src, static_cast<char*>(idx_out) + off * (wide ? 8 : 4), wide, cnt);
         }
       }
-#if defined(__SSE2__)
-      _mm_sfence();
-#endif
     };
+    const bool trace = std::getenv("APSP_READBACK_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     std::vector<std::thread> pool;
     for (int w = 1; w < T; w++) pool.emplace_back(work, w);
     work(0);
     for (auto& t : pool) t.join();
+    if (trace) {
+      // last chunk landed vs. widening done: the gap is the host tail
+      const auto t1 = std::chrono::steady_clock::now();
+      cudaEventSynchronize(ev.back());
+      std::fprintf(stderr, "[readback] n=%lld dw=%d pred=%d chunks=%lld threads=%d host wait+widen %.2f ms\n",
+                   (long long)n, dw, int(pk), (long long)nch, T,
+                   std::chrono::duration<double, std::milli>(t1 - t0).count());
+    }
     if (err) e = cudaErrorUnknown;
   }
   const bool flagged = e == cudaSuccess && *hbad;

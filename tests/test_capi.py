@@ -29,7 +29,7 @@ def test_library_loads_and_exports_all_symbols():
     lib = nat.load(require_gpu=False)
     for name in declared_symbols():
         assert hasattr(lib, name), name
-    assert lib.apsp_abi_version() == 1
+    assert lib.apsp_abi_version() == 2
 
 
 def test_workspace_query_is_host_only():

@@ -473,3 +473,45 @@ def test_host_readback_narrowed_equals_device_result(cuda, alpha, monkeypatch):
     nat.check(st)
     assert info.d2h_bytes_per_cell == 12
     assert np.array_equal(d, want_d) and np.array_equal(p64, want_p.astype(np.int64))
+
+
+def test_host_upload_narrowed_and_fallbacks(cuda):
+    """apsp_solve_host narrows the int32 costs for the upload (csrc/hostio.cu): the width comes
+    from the first rows and every cell is checked while packing. A late cell that does not fit
+    (a wide cost, a negative cost) aborts to the plain int32 upload, so results and errors are
+    those of the caller's matrix."""
+    import ctypes
+
+    import torch
+    from paper_2310_03983_b200 import _native as nat
+
+    n = 2048
+    lib = nat.load()
+
+    def host(h):
+        info = nat.ApspInfo()
+        d = np.empty((n, n), np.int32)
+        p = np.empty((n, n), np.int32)
+        st = lib.apsp_solve_host(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, h.ctypes.data, d.ctypes.data, p.ctypes.data,
+                                 nat.DTYPE_I32, nat.IDX_PRED, 0, 0, 0, nat.TIER_AUTO, 0, ctypes.byref(info))
+        return st, d, p, info
+
+    for alpha, width in ((100, 1), (3000, 2), (10 ** 6, 4)):
+        h = ap.dense_costs(ap.GenParams(n, 0.1, alpha, 5 + alpha), np.int32)
+        st, d, p, info = host(h)
+        nat.check(st)
+        dev = ap.solve(torch.from_numpy(h).cuda())
+        assert info.h2d_bytes_per_cell == width
+        assert np.array_equal(d, dev.distances.cpu().numpy()) and np.array_equal(p, dev.index.cpu().numpy())
+    h = ap.dense_costs(ap.GenParams(n, 0.1, 100, 9), np.int32)
+    h[n - 1, 3] = 70000                                   # fits neither u8 nor u16: plain upload
+    st, d, p, info = host(h)
+    nat.check(st)
+    assert info.h2d_bytes_per_cell == 4
+    dev = ap.solve(torch.from_numpy(h).cuda())
+    assert np.array_equal(d, dev.distances.cpu().numpy()) and np.array_equal(p, dev.index.cpu().numpy())
+    h[n - 1, 3] = -5                                      # negative cost: the device scan's error
+    st, _, _, _ = host(h)
+    from paper_2310_03983_b200.core import NegativeWeightError
+    with pytest.raises(NegativeWeightError):
+        nat.check(st)
