@@ -8,6 +8,7 @@
 // during step k (solvers.py:79-81), so one barrier per k suffices.
 #include <cstdlib>
 #include "launch.h"
+#include "tiles.cuh"
 
 namespace apsp {
 
@@ -184,8 +185,9 @@ __global__ void __launch_bounds__(512) block_close_kernel(typename StoreT<S>::T*
 // ------------------------------------------------------------------------------------
 struct CloseU8Smem {
   uint32_t colk[2][MAXB];     // column k as replicated tag-free keys, by row (16-byte lane slots)
-  int32_t P[MAXB][MAXB];      // pred resolution (and the value staging area before it)
-  uint8_t K[MAXB][MAXB];      // 1-based last improving k (0 = none)
+  int32_t P[MAXB][MAXB];      // pred resolution; prefetched by cp.async while the k loop runs
+  uint8_t K[MAXB][MAXB];      // 1-based last improving k (0 = none); value staging before that
+  uint8_t Kpad[MAXB][MAXB];   // second half of the u16 value staging
 };
 
 // Key formats of the packed closure: u8 values << 7 with 64-step tag windows, u16 values << 6
@@ -202,10 +204,11 @@ template <> struct CloseKeys<STORE_U16> {
   static constexpr uint32_t INF = U16_INF;
 };
 
-template <int S>
+template <int S, bool FULL>
 __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo,
                                                               int m, int32_t* idx, int64_t ldi, int mode,
                                                               int64_t via_off) {
+  if (FULL) m = MAXB;   // every FW phase-1 block: the bounds checks fold away
   using CK = CloseKeys<S>;
   using T = typename CK::T;
   constexpr int TAG = CK::TAG, WIN = CK::WIN, VB = int(sizeof(T));
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
   constexpr uint32_t STRIP2 = ~TMASK2;
   extern __shared__ __align__(16) unsigned char smraw_cu8[];
   CloseU8Smem& sm = *reinterpret_cast<CloseU8Smem*>(smraw_cu8);
-  T (*stage)[MAXB] = reinterpret_cast<T (*)[MAXB]>(&sm.P[0][0]);   // value staging (aliases P)
+  T (*stage)[MAXB] = reinterpret_cast<T (*)[MAXB]>(&sm.K[0][0]);   // value staging (aliases K, Kpad)
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
   uint32_t acc[4][4];   // [row r][pair p]: columns (8w + 2p, 8w + 2p + 1)
   uint32_t kst[4][2];   // byte 2 * (p & 1) + h of kst[r][p >> 1] = cell (r, 8w + 2p + h)
@@ -221,6 +224,17 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
   // its 4 rows x 8 bytes
   constexpr int SEG = 16 / VB;   // values per 16-byte segment
   const bool vec = m == MAXB && ((reinterpret_cast<uintptr_t>(D + lo * ld + lo) | uintptr_t(ld * VB)) & 15) == 0;
+  // the predecessors are needed only after the k loop: start their copy now
+  const bool pre = FULL && idx && mode == IDX_PRED &&
+                   ((reinterpret_cast<uintptr_t>(idx + lo * ldi + lo) | uintptr_t(ldi * 4)) & 15) == 0;
+  if (pre) {
+    for (int e = threadIdx.x; e < MAXB * MAXB / 4; e += blockDim.x) {
+      const int i = e >> 5, j = 4 * (e & 31);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&sm.P[i][j])),
+                   "l"(idx + (lo + i) * ldi + lo + j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
   if (vec) {   // full aligned block (every FW phase 1): 16-byte row segments
     for (int e = threadIdx.x; e < MAXB * MAXB / SEG; e += blockDim.x) {
       const int i = e / (MAXB / SEG), j = SEG * (e % (MAXB / SEG));
@@ -251,9 +265,9 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
     }
   }
   // column KC (its low 3 bits KL static) of the owner warp into buffer BUF
-#define CU8_PUBCOL(KC, KL, BUF)                                                                  \
+#define CU8_PUBCOL(OWN, KL, BUF)                                                                 \
   do {                                                                                           \
-    if (w == ((KC) >> 3)) {                                                                      \
+    if (OWN) {                                                                                   \
       const int pp_ = ((KL) & 7) >> 1;                                                       \
       const uint32_t sel_ = ((KL) & 1) ? 0x3232u : 0x1010u; /* replicate the half */        \
       *reinterpret_cast<uint4*>(&sm.colk[BUF][4 * l]) =                                          \
@@ -263,24 +277,28 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
                      __byte_perm(acc[3][pp_], 0, sel_) & STRIP2);                                \
     }                                                                                            \
   } while (0)
-  CU8_PUBCOL(0, 0, 0);
+  CU8_PUBCOL(w == 0, 0, 0);
+  uint32_t tag2 = 0x00010001u;   // tag of step k: 1 + (k mod WIN) in both halves
   for (int k0 = 0; k0 < m; k0 += 8) {
+    const bool own = w == (k0 >> 3), own_next = w == (k0 >> 3) + 1;
+    const bool win_end = ((k0 >> 3) & (WIN / 8 - 1)) == WIN / 8 - 1;   // step k0 + 7 closes a window
 #pragma unroll
     for (int kk = 0; kk < 8; kk++) {
       const int k = k0 + kk;
-      if (k < m) {
+      if (FULL || k < m) {
         __syncthreads();
         const uint4 c4 = *reinterpret_cast<const uint4*>(&sm.colk[kk & 1][4 * l]);
         const uint32_t dik[4] = {c4.x, c4.y, c4.z, c4.w};
-        const uint32_t tag2 = uint32_t((k & (WIN - 1)) + 1) * 0x00010001u;
         uint32_t dkj[4];
 #pragma unroll
-        for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[kk & 3][p], k >> 2) & STRIP2) + tag2;
+        for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[kk & 3][p], k >> 2) & STRIP2) | tag2;
 #pragma unroll
         for (int r = 0; r < 4; r++)
 #pragma unroll
           for (int p = 0; p < 4; p++) acc[r][p] = __viaddmin_u16x2(dik[r], dkj[p], acc[r][p]);
-        if ((k & (WIN - 1)) == WIN - 1 || k + 1 == m) {   // decode this tag window
+        const bool wend = kk == 7 && win_end;
+        tag2 = wend ? 0x00010001u : tag2 + 0x00010001u;
+        if (wend || (!FULL && k + 1 == m)) {   // decode this tag window
           const uint32_t wbase = uint32_t(k & ~(WIN - 1));
 #pragma unroll
           for (int r = 0; r < 4; r++) {
@@ -296,7 +314,7 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
             }
           }
         }
-        if (k + 1 < m) CU8_PUBCOL(k + 1, kk + 1, (kk + 1) & 1);
+        if (k + 1 < m) CU8_PUBCOL(kk == 7 ? own_next : own, kk + 1, (kk + 1) & 1);
       }
     }
   }
@@ -347,13 +365,17 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
     }
     return;
   }
+  if (pre) {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  } else {
 #pragma unroll
-  for (int a = 0; a < 8; a++) {
-    const int i = ty + 16 * a;
+    for (int a = 0; a < 8; a++) {
+      const int i = ty + 16 * a;
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int j = tx + 32 * q;
-      sm.P[i][j] = (i < m && j < m) ? idx[(lo + i) * ldi + lo + j] : -1;
+      for (int q = 0; q < 4; q++) {
+        const int j = tx + 32 * q;
+        sm.P[i][j] = (i < m && j < m) ? idx[(lo + i) * ldi + lo + j] : -1;
+      }
     }
   }
   __syncthreads();
@@ -427,14 +449,24 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
   }
   if ((store == STORE_U8 || store == STORE_U16) && !getenv("APSP_SLOW_CLOSE")) {
     static std::atomic<unsigned long long> attr8{0}, attr16{0};
-    if (store == STORE_U8) {
-      APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8>, int(sizeof(CloseU8Smem)), attr8));
-      block_close_dpx_kernel<STORE_U8><<<1, 512, sizeof(CloseU8Smem), s>>>(static_cast<uint8_t*>(D), ld, lo, int(m),
-                                                                           idx, ldi, mode, via_off);
+    static std::atomic<unsigned long long> attr8f{0}, attr16f{0};
+    const size_t sb = sizeof(CloseU8Smem);
+    if (store == STORE_U8 && m == MAXB) {
+      APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8, true>, int(sb), attr8f));
+      block_close_dpx_kernel<STORE_U8, true><<<1, 512, sb, s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
+                                                                mode, via_off);
+    } else if (store == STORE_U8) {
+      APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8, false>, int(sb), attr8));
+      block_close_dpx_kernel<STORE_U8, false><<<1, 512, sb, s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
+                                                                 mode, via_off);
+    } else if (m == MAXB) {
+      APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16, true>, int(sb), attr16f));
+      block_close_dpx_kernel<STORE_U16, true><<<1, 512, sb, s>>>(static_cast<uint16_t*>(D), ld, lo, int(m), idx,
+                                                                 ldi, mode, via_off);
     } else {
-      APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16>, int(sizeof(CloseU8Smem)), attr16));
-      block_close_dpx_kernel<STORE_U16><<<1, 512, sizeof(CloseU8Smem), s>>>(static_cast<uint16_t*>(D), ld, lo,
-                                                                            int(m), idx, ldi, mode, via_off);
+      APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16, false>, int(sb), attr16));
+      block_close_dpx_kernel<STORE_U16, false><<<1, 512, sb, s>>>(static_cast<uint16_t*>(D), ld, lo, int(m), idx,
+                                                                  ldi, mode, via_off);
     }
     APSP_CUDA_TRY(cudaGetLastError());
     count_launches(1);
