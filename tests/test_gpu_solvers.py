@@ -515,3 +515,19 @@ def test_host_upload_narrowed_and_fallbacks(cuda):
     from paper_2310_03983_b200.core import NegativeWeightError
     with pytest.raises(NegativeWeightError):
         nat.check(st)
+
+
+@pytest.mark.parametrize("algorithm,kw", [("rkleene", {"track": "via"}), ("rkleene", {"track": "pred"}),
+                                          ("fw_squaring", {})])
+def test_host_transfers_other_algorithms(cuda, algorithm, kw):
+    """The narrowed host transfers carry R-Kleene via / pred and squaring via indices too: the
+    host-buffer result equals the device-resident one cell for cell."""
+    import torch
+
+    n = 2048
+    h32 = ap.dense_costs(ap.GenParams(n, 0.1, 100, 77), np.int32)
+    dev = ap.solve(torch.from_numpy(h32).cuda(), algorithm, **kw)
+    r = ap.solve(h32, algorithm, **kw)
+    assert r.info["d2h_bytes_per_cell"] == 3 and r.info["h2d_bytes_per_cell"] == 1
+    assert np.array_equal(r.distances, dev.distances.cpu().numpy())
+    assert np.array_equal(r.index, dev.index.cpu().numpy())
