@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(512) block_close_kernel(typename StoreT<S>::T*
 // ------------------------------------------------------------------------------------
 struct CloseU8Smem {
   uint32_t colk[2][MAXB];     // column k as replicated tag-free keys, by row (16-byte lane slots)
+  uint32_t colk1[2][MAXB];    // column k + 1 likewise (full blocks: two steps per barrier)
   int32_t P[MAXB][MAXB];      // pred resolution; prefetched by cp.async while the k loop runs
   uint8_t K[MAXB][MAXB];      // 1-based last improving k (0 = none); value staging before that
   uint8_t Kpad[MAXB][MAXB];   // second half of the u16 value staging
@@ -277,8 +278,87 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
                      __byte_perm(acc[3][pp_], 0, sel_) & STRIP2);                                \
     }                                                                                            \
   } while (0)
-  CU8_PUBCOL(w == 0, 0, 0);
+  // tag window decode after step k: the last improving k per cell into kst
+  auto decode = [&](int k) {
+    const uint32_t wbase = uint32_t(k & ~(WIN - 1));
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+#pragma unroll
+      for (int p = 0; p < 4; p++) {
+        const uint32_t tg = acc[r][p] & TMASK2;
+        acc[r][p] ^= tg;
+        const uint32_t tlo = tg & 0xFF, thi = tg >> 16;
+        const int sh0 = 8 * (2 * (p & 1)), sh1 = sh0 + 8;
+        uint32_t& ks = kst[r][p >> 1];
+        if (tlo) ks = (ks & ~(0xFFu << sh0)) | ((wbase + tlo) << sh0);
+        if (thi) ks = (ks & ~(0xFFu << sh1)) | ((wbase + thi) << sh1);
+      }
+    }
+  };
   uint32_t tag2 = 0x00010001u;   // tag of step k: 1 + (k mod WIN) in both halves
+  if constexpr (FULL) {
+    // Two steps per CTA barrier. Columns k and k + 1 (k even) form one key pair of one warp, so
+    // the owner publishes the pair (after step k - 1) with a single 16-byte store per lane. Every
+    // warp then advances column k + 1 through step k itself:
+    //   D[i][k+1] <- min(D[i][k+1], D[i][k] + D[k][k+1])
+    // (one packed add+min per row, with D[k][k+1] read from the published pair at row k) and
+    // runs steps k and k + 1 back to back. Row k + 1 comes from the warp's own lanes after its
+    // step k, as before. Only operands are computed redundantly; each cell is still updated by
+    // its owner, so values, tags and k* are those of the one-step loop.
+    // the pair goes out as two replicated, tag-free columns: colk[BUF] = column k,
+    // colk1[BUF] = column k + 1 (both halves of every key equal)
+#define CU8_PUBPAIR(OWN, KL, BUF)                                                                \
+  do {                                                                                           \
+    if (OWN) {                                                                                   \
+      const int pp_ = ((KL) & 7) >> 1;                                                           \
+      *reinterpret_cast<uint4*>(&sm.colk[BUF][4 * l]) = make_uint4(                              \
+          __byte_perm(acc[0][pp_], 0, 0x1010) & STRIP2, __byte_perm(acc[1][pp_], 0, 0x1010) & STRIP2, \
+          __byte_perm(acc[2][pp_], 0, 0x1010) & STRIP2, __byte_perm(acc[3][pp_], 0, 0x1010) & STRIP2); \
+      *reinterpret_cast<uint4*>(&sm.colk1[BUF][4 * l]) = make_uint4(                             \
+          __byte_perm(acc[0][pp_], 0, 0x3232) & STRIP2, __byte_perm(acc[1][pp_], 0, 0x3232) & STRIP2, \
+          __byte_perm(acc[2][pp_], 0, 0x3232) & STRIP2, __byte_perm(acc[3][pp_], 0, 0x3232) & STRIP2); \
+    }                                                                                            \
+  } while (0)
+    CU8_PUBPAIR(w == 0, 0, 0);
+    for (int k0 = 0; k0 < MAXB; k0 += 8) {
+      const bool own = w == (k0 >> 3), own_next = w == (k0 >> 3) + 1;
+      const bool win_end = ((k0 >> 3) & (WIN / 8 - 1)) == WIN / 8 - 1;   // step k0 + 7 closes a window
+#pragma unroll
+      for (int kk = 0; kk < 8; kk += 2) {
+        const int k = k0 + kk;
+        const int buf = (kk >> 1) & 1;
+        __syncthreads();
+        const uint4 c4 = *reinterpret_cast<const uint4*>(&sm.colk[buf][4 * l]);
+        const uint4 c5 = *reinterpret_cast<const uint4*>(&sm.colk1[buf][4 * l]);
+        const uint32_t dkk1 = sm.colk1[buf][k];   // D[k][k+1], replicated
+        const uint32_t ck[4] = {c4.x, c4.y, c4.z, c4.w};
+        uint32_t ck1[4] = {c5.x, c5.y, c5.z, c5.w};
+#pragma unroll
+        for (int r = 0; r < 4; r++) ck1[r] = __viaddmin_u16x2(ck[r], dkk1, ck1[r]);
+        uint32_t dkj[4];
+#pragma unroll
+        for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[kk & 3][p], k >> 2) & STRIP2) | tag2;
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+          for (int p = 0; p < 4; p++) acc[r][p] = __viaddmin_u16x2(ck[r], dkj[p], acc[r][p]);
+        tag2 += 0x00010001u;
+#pragma unroll
+        for (int p = 0; p < 4; p++)
+          dkj[p] = (__shfl_sync(0xffffffffu, acc[(kk + 1) & 3][p], (k + 1) >> 2) & STRIP2) | tag2;
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+          for (int p = 0; p < 4; p++) acc[r][p] = __viaddmin_u16x2(ck1[r], dkj[p], acc[r][p]);
+        const bool wend = kk == 6 && win_end;
+        tag2 = wend ? 0x00010001u : tag2 + 0x00010001u;
+        if (wend) decode(k + 1);
+        if (k + 2 < MAXB) CU8_PUBPAIR(kk == 6 ? own_next : own, kk + 2, buf ^ 1);
+      }
+    }
+#undef CU8_PUBPAIR
+  } else {
+  CU8_PUBCOL(w == 0, 0, 0);
   for (int k0 = 0; k0 < m; k0 += 8) {
     const bool own = w == (k0 >> 3), own_next = w == (k0 >> 3) + 1;
     const bool win_end = ((k0 >> 3) & (WIN / 8 - 1)) == WIN / 8 - 1;   // step k0 + 7 closes a window
@@ -298,25 +378,11 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
           for (int p = 0; p < 4; p++) acc[r][p] = __viaddmin_u16x2(dik[r], dkj[p], acc[r][p]);
         const bool wend = kk == 7 && win_end;
         tag2 = wend ? 0x00010001u : tag2 + 0x00010001u;
-        if (wend || (!FULL && k + 1 == m)) {   // decode this tag window
-          const uint32_t wbase = uint32_t(k & ~(WIN - 1));
-#pragma unroll
-          for (int r = 0; r < 4; r++) {
-#pragma unroll
-            for (int p = 0; p < 4; p++) {
-              const uint32_t tg = acc[r][p] & TMASK2;
-              acc[r][p] ^= tg;
-              const uint32_t tlo = tg & 0xFF, thi = tg >> 16;
-              const int sh0 = 8 * (2 * (p & 1)), sh1 = sh0 + 8;
-              uint32_t& ks = kst[r][p >> 1];
-              if (tlo) ks = (ks & ~(0xFFu << sh0)) | ((wbase + tlo) << sh0);
-              if (thi) ks = (ks & ~(0xFFu << sh1)) | ((wbase + thi) << sh1);
-            }
-          }
-        }
+        if (wend || (!FULL && k + 1 == m)) decode(k);   // close this tag window
         if (k + 1 < m) CU8_PUBCOL(kk == 7 ? own_next : own, kk + 1, (kk + 1) & 1);
       }
     }
+  }
   }
 #undef CU8_PUBCOL
   // values back (through the staging area) and the 1-based k* bytes
