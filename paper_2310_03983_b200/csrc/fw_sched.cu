@@ -191,20 +191,24 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   char* colp = c.D + k0 * c.es;
   const bool nt = bulk_store(c.store, c.b) && c.p2prep;   // bulk-staged tiles (prep = snapshot)
   const bool snap = !nt && b > TILE_ALIGN;
-  if (c.P && c.mode == IDX_PRED) {
+  const bool cross = nt && c.prep[0];
+  const bool psnap = c.P && c.mode == IDX_PRED;
+  if (psnap && !cross) {
     APSP_CUDA_TRY(cudaMemcpy2DAsync(c.predsnap, size_t(m) * 4, c.P + k0 * c.ldp, size_t(c.ldp) * 4, size_t(m) * 4,
                                     size_t(b), cudaMemcpyDeviceToDevice, s));
   }
   int rc = 0;
-  if (nt && c.prep[0]) {
+  if (cross) {
     // Both panels in ONE cross-list launch: the tiles of the pivot row band compute
     // Dg (x) row panel and those of the pivot column band column panel (x) Dg, because the
     // A / B layouts are the full column / row panels (their pivot rows / columns are Dg).  The
     // diagonal tiles compute Dg (x) Dg, which never strictly improves a closed block.  The
     // layouts live in this round's phase-3 slot (free: its last reader, phase 3 two rounds
     // back, is ordered before us) and are rebuilt from the updated panels right after.
+    // the pred snapshot of the pivot rows rides along as the prep launch's third part
     char* slot = c.prep[(k0 / b) & 1];
-    rc = launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
+    rc = launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s,
+                          psnap ? c.P + k0 * c.ldp : nullptr, c.ldp, c.predsnap, m, m);
     if (rc) return rc;
     MinplusArgs x = minplus_args();
     x.A = colp; x.lda = c.ld;

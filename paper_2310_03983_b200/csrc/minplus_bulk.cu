@@ -718,11 +718,36 @@ size_t prep_bytes(int64_t m, int64_t n, int64_t k) {   // A keys + B keys (uint3
 // Both panel layouts in ONE launch (one dependent launch fewer on the per-round chain):
 // blockIdx = (chunk, tile, part) with part 0 the A rows and part 1 the B columns.
 enum PrepKind : int { PREP_U8 = 0, PREP_U16 = 1, PREP_W32 = 2, PREP_F32 = 3, PREP_F32_DM = 4 };
+struct PredCopy {   // optional int32 band copy riding along a prep launch (grid z = 2)
+  const int32_t* src;
+  int64_t lds;
+  int32_t* dst;
+  int64_t ldd, cols;
+  int vec;
+};
 template <int KIND>
 __global__ void __launch_bounds__(NT) prep_pair_kernel(const void* A, int64_t lda, const void* B, int64_t ldb,
                                                        int64_t nch, int64_t nta, int64_t ntb, uint32_t* Aprep,
-                                                       void* Bprep) {
+                                                       void* Bprep, PredCopy pc) {
   const int64_t c = blockIdx.x, tile = blockIdx.y;
+  if (blockIdx.z == 2) {   // pred snapshot rows [32c, 32c + 32) x columns [128 tile, 128 tile + 128)
+    const int64_t j0 = 128 * tile;
+    if (j0 >= pc.cols) return;
+    const int t = threadIdx.x;
+    if (pc.vec) {
+#pragma unroll 4
+      for (int e = t; e < SUB * 32; e += NT) {
+        const int64_t i = SUB * c + (e >> 5), j = j0 + 4 * (e & 31);
+        *reinterpret_cast<int4*>(pc.dst + i * pc.ldd + j) = *reinterpret_cast<const int4*>(pc.src + i * pc.lds + j);
+      }
+    } else {
+      for (int e = t; e < SUB * 128; e += NT) {
+        const int64_t i = SUB * c + (e >> 7), j = j0 + (e & 127);
+        if (j < pc.cols) pc.dst[i * pc.ldd + j] = pc.src[i * pc.lds + j];
+      }
+    }
+    return;
+  }
   if (blockIdx.z == 0) {
     if (tile >= nta) return;
     if constexpr (KIND == PREP_U8) prep_nt_a_body<STORE_U8>(static_cast<const uint8_t*>(A), lda, nch, Aprep, tile, c);
@@ -745,7 +770,8 @@ __global__ void __launch_bounds__(NT) prep_pair_kernel(const void* A, int64_t ld
 }
 
 int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
-                     int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s) {
+                     int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s, const int32_t* psrc, int64_t lds,
+                     int32_t* pdst, int64_t ldd, int64_t pcols) {
   const size_t es = (store == STORE_W32 || store == STORE_F32) ? 4 : store == STORE_U16 ? 2 : 1;
   if (m % BM || n % BN || k % SUB || (lda * es) % 16 || (ldb * es) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
@@ -753,14 +779,21 @@ int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64
   const int64_t nch = k / SUB, nta = m / BM;
   const bool dm = store == STORE_F32 && f32_deferred();
   const int64_t ntb = n / (dm ? DM_BN : BN);
-  const dim3 g(unsigned(nch), unsigned(std::max(nta, ntb)), 2);
+  // optional third part: copy a k x pcols int32 pred band (the phase-2 pred snapshot)
+  PredCopy pc{psrc, lds, pdst, ldd, pcols, 0};
+  if (psrc) {
+    pc.vec = (lds % 4 == 0 && ldd % 4 == 0 && pcols % 128 == 0 &&
+              ((reinterpret_cast<uintptr_t>(psrc) | reinterpret_cast<uintptr_t>(pdst)) & 15) == 0);
+  }
+  const int64_t tiles = std::max(std::max(nta, ntb), psrc ? (pcols + 127) / 128 : int64_t(0));
+  const dim3 g(unsigned(nch), unsigned(tiles), psrc ? 3 : 2);
   switch (store) {
-    case STORE_U8: prep_pair_kernel<PREP_U8><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
-    case STORE_U16: prep_pair_kernel<PREP_U16><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
-    case STORE_W32: prep_pair_kernel<PREP_W32><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep); break;
+    case STORE_U8: prep_pair_kernel<PREP_U8><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep, pc); break;
+    case STORE_U16: prep_pair_kernel<PREP_U16><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep, pc); break;
+    case STORE_W32: prep_pair_kernel<PREP_W32><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep, pc); break;
     case STORE_F32:
-      if (dm) prep_pair_kernel<PREP_F32_DM><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep);
-      else prep_pair_kernel<PREP_F32><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep);
+      if (dm) prep_pair_kernel<PREP_F32_DM><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep, pc);
+      else prep_pair_kernel<PREP_F32><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep, pc);
       break;
     default:
       return set_error(2, "panel prep is for the u8 / u16 / w32 / f32 tiers");
