@@ -548,6 +548,7 @@ struct SmemF32DM {   // 96 KB: 2 CTAs / SM
   float Bs[DM_STAGES][SUB][DM_BN];
   float Cs[BM * DM_BN];         // the old C tile; after the chunk-0 merge, the rescan targets
   uint16_t kid[NT][32];         // 0-based k of the last strict improvement, 0xFFFF = none
+  uint16_t queue[NT / 32][1024];  // per warp: improved (lane, cell) items of the current chunk
   unsigned long long bar[DM_STAGES];
   unsigned int done[DM_STAGES];  // warps finished with the slot's chunk
 };
@@ -648,20 +649,38 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
 #pragma unroll
           for (int q = 0; q < 8; q++) sm.Cs[dm_tgt(t, 8 * r + q)] = acc[r][q];
       }
-      const int kb = int(c) * SUB;
-      while (mask) {   // per-lane loop over this lane's improved cells
+      // The warp's improved cells go into one queue and the 32 lanes share them, so the
+      // rescan costs ceil(items / 32) passes instead of the busiest lane's count. Each pass
+      // scans the whole chunk without branches (independent loads, a select per k), so it is
+      // bound by issue, not by a load-compare chain.
+      const int kb = int(c) * SUB, lane = t & 31;
+      uint16_t* q = sm.queue[t >> 5];
+      const int cnt = __popc(mask);
+      int pre = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += v;
+      }
+      const int total = __shfl_sync(0xffffffffu, pre, 31);
+      pre -= cnt;
+      while (mask) {
         const int cell = __ffs(mask) - 1;
         mask &= mask - 1;
-        const int row = 4 * ty + (cell >> 3), col = 8 * tx + (cell & 7);
-        const float target = sm.Cs[dm_tgt(t, cell)];
-        int found = 0;
-        for (int kk = 0; kk < SUB; kk++)
-          if (sm.As[slot][kk][row] + sm.Bs[slot][kk][col] == target) {
-            found = kk;
-            break;
-          }
-        sm.kid[t][cell] = uint16_t(kb + found);
+        q[pre++] = uint16_t(lane << 5 | cell);
       }
+      __syncwarp();
+      for (int it = lane; it < total; it += 32) {
+        const int e = q[it], tt = (t & ~31) | (e >> 5), cell = e & 31;
+        const int row = 4 * (tt >> 3) + (cell >> 3), col = 8 * (tt & 7) + (cell & 7);
+        const float target = sm.Cs[dm_tgt(tt, cell)];
+        int found = 0;
+#pragma unroll
+        for (int kk = SUB - 1; kk >= 0; kk--)
+          found = sm.As[slot][kk][row] + sm.Bs[slot][kk][col] == target ? kk : found;
+        sm.kid[tt][cell] = uint16_t(kb + found);
+      }
+      __syncwarp();
     }
     __syncwarp();
     if ((t & 31) == 0) {   // count this warp out of the slot; the last one refills it
