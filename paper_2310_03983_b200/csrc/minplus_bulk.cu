@@ -552,8 +552,9 @@ struct SmemF32DM {   // 96 KB: 2 CTAs / SM
   unsigned long long bar[DM_STAGES];
   unsigned int done[DM_STAGES];  // warps finished with the slot's chunk
 };
-// rescan target slot of (thread, cell): swizzled so the 32 lanes hit 32 banks for a common cell
-__device__ __forceinline__ int dm_tgt(int t, int cell) { return t * 32 + ((cell + t) & 31); }
+// rescan target slot of (thread, cell): 4-cell groups stay contiguous (one 16-byte store each),
+// rotated by thread so the 8 lanes of a store phase hit 8 different bank quads
+__device__ __forceinline__ int dm_tgt(int t, int cell) { return t * 32 + ((((cell >> 2) + t) & 7) << 2) + (cell & 3); }
 
 __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
   extern __shared__ __align__(128) unsigned char smraw_dm[];
@@ -647,7 +648,9 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
 #pragma unroll
         for (int r = 0; r < 4; r++)
 #pragma unroll
-          for (int q = 0; q < 8; q++) sm.Cs[dm_tgt(t, 8 * r + q)] = acc[r][q];
+          for (int h = 0; h < 2; h++)
+            *reinterpret_cast<float4*>(&sm.Cs[dm_tgt(t, 8 * r + 4 * h)]) =
+                make_float4(acc[r][4 * h], acc[r][4 * h + 1], acc[r][4 * h + 2], acc[r][4 * h + 3]);
       }
       // The warp's improved cells go into one queue and the 32 lanes share them, so the
       // rescan costs ceil(items / 32) passes instead of the busiest lane's count. Each pass
