@@ -179,8 +179,8 @@ int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* di
   if (e != cudaSuccess) return fail(set_cuda_error(e, "host staging", __FILE__, __LINE__));
   bool up = false;
   int up_width = int(es);
-  if (dtype == APSP_DTYPE_I32) {
-    rc = upload_packed(n, static_cast<const int32_t*>(h), static_cast<int32_t*>(d), s, up, up_width);
+  if (dtype == APSP_DTYPE_I32 || dtype == APSP_DTYPE_I64) {   // integer costs: narrowed upload
+    rc = upload_packed(n, h, int(es), d, s, up, up_width);
     if (rc) return fail(rc);
   }
   if (!up) e = cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s);
@@ -199,13 +199,13 @@ int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* di
   local.h2d_bytes_per_cell = up ? up_width : int32_t(es);
   if (info) *info = local;
   if (rc) return fail(rc);
-  if (dtype == APSP_DTYPE_I32) {
+  if (dtype == APSP_DTYPE_I32 || dtype == APSP_DTYPE_I64) {   // integer results: narrowed readback
     bool done = false;
-    rc = readback_packed(n, static_cast<const int32_t*>(d), idx_out ? p : nullptr, local.max_finite, dist_out,
-                         idx_out, idx_dtype, s, done);
+    rc = readback_packed(n, d, int(es), idx_out ? p : nullptr, local.max_finite, dist_out, idx_out, idx_dtype, s,
+                         done);
     if (rc) return fail(rc);
     if (done) {
-      if (info) info->d2h_bytes_per_cell = readback_width(n, local.max_finite, idx_out != nullptr, idx_dtype);
+      if (info) info->d2h_bytes_per_cell = readback_width(n, local.max_finite, int(es), idx_out != nullptr);
       return fail(0);
     }
   }

@@ -241,9 +241,9 @@ int rk_shard_product_impl(int tier, const void* A, int64_t lda, const void* B, i
                           const int64_t* peer_di = nullptr);
 
 // hostio.cu: narrowed device->host readback of an int32 result (apsp_solve_host).
-int readback_packed(int64_t n, const int32_t* d, const int32_t* p, int64_t max_finite, void* dist_out, void* idx_out,
-                    int idx_dtype, cudaStream_t s, bool& handled);
-int32_t readback_width(int64_t n, int64_t max_finite, bool idx, int idx_dtype);   // bytes per cell when handled
-int upload_packed(int64_t n, const int32_t* h, int32_t* d, cudaStream_t s, bool& handled, int& width);
+int readback_packed(int64_t n, const void* d, int es, const int32_t* p, int64_t max_finite, void* dist_out,
+                    void* idx_out, int idx_dtype, cudaStream_t s, bool& handled);
+int32_t readback_width(int64_t n, int64_t max_finite, int es, bool idx);   // bytes per cell when handled
+int upload_packed(int64_t n, const void* h, int es, void* d, cudaStream_t s, bool& handled, int& width);
 
 }  // namespace apsp

@@ -27,20 +27,34 @@ namespace {
 
 constexpr int32_t kInf32 = INF32;   // the API's int32 "no path" (core.py INF32)
 
-template <int DW, bool PRED>
-__global__ void pack_result_kernel(const int32_t* __restrict__ d, const int32_t* __restrict__ p, int64_t cells,
+template <typename TD> __device__ __forceinline__ TD inf_of() { return sizeof(TD) == 4 ? TD(INF32) : TD(INF_RAW); }
+
+// four consecutive cells as 64-bit lanes (int32 results sign-extend)
+template <typename TD>
+__device__ __forceinline__ void load4(const TD* d, int64_t g, int64_t (&x)[4]) {
+  if constexpr (sizeof(TD) == 4) {
+    const int4 v = reinterpret_cast<const int4*>(d)[g];
+    x[0] = v.x; x[1] = v.y; x[2] = v.z; x[3] = v.w;
+  } else {
+    const longlong2 a = reinterpret_cast<const longlong2*>(d)[2 * g], b = reinterpret_cast<const longlong2*>(d)[2 * g + 1];
+    x[0] = a.x; x[1] = a.y; x[2] = b.x; x[3] = b.y;
+  }
+}
+
+template <int DW, bool PRED, typename TD>
+__global__ void pack_result_kernel(const TD* __restrict__ d, const int32_t* __restrict__ p, int64_t cells,
                                    void* __restrict__ dpk, uint16_t* __restrict__ ppk, int32_t lim,
                                    int* __restrict__ bad) {
   const int64_t groups = cells >> 2;
   int flag = 0;
   for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < groups; g += int64_t(gridDim.x) * blockDim.x) {
     if (DW) {
-      const int4 v = reinterpret_cast<const int4*>(d)[g];
-      const int32_t x[4] = {v.x, v.y, v.z, v.w};
+      int64_t x[4];
+      load4(d, g, x);
       uint32_t o[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const bool inf = x[q] == kInf32;
+        const bool inf = x[q] == int64_t(inf_of<TD>());
         flag |= !inf && (x[q] < 0 || x[q] > lim);
         o[q] = inf ? (DW == 1 ? 0xFFu : 0xFFFFu) : uint32_t(x[q]);
       }
@@ -54,6 +68,19 @@ __global__ void pack_result_kernel(const int32_t* __restrict__ d, const int32_t*
     }
   }
   if (flag) atomicOr(bad, 1);
+}
+
+template <typename TD>
+void launch_pack(int dw, bool pk, const void* d, const int32_t* p, int64_t cells, void* dev, uint16_t* ppk, int* bad,
+                 cudaStream_t s) {
+  const int grid = 148 * 8;
+  const int32_t lim = dw == 1 ? 254 : 65534;
+  const TD* dd = static_cast<const TD*>(d);
+  if (dw == 1 && pk) pack_result_kernel<1, true, TD><<<grid, 256, 0, s>>>(dd, p, cells, dev, ppk, lim, bad);
+  else if (dw == 1) pack_result_kernel<1, false, TD><<<grid, 256, 0, s>>>(dd, p, cells, dev, ppk, lim, bad);
+  else if (dw == 2 && pk) pack_result_kernel<2, true, TD><<<grid, 256, 0, s>>>(dd, p, cells, dev, ppk, lim, bad);
+  else if (dw == 2) pack_result_kernel<2, false, TD><<<grid, 256, 0, s>>>(dd, p, cells, dev, ppk, lim, bad);
+  else pack_result_kernel<0, true, TD><<<grid, 256, 0, s>>>(dd, p, cells, dev, ppk, lim, bad);
 }
 
 // ---- pinned staging, grow-only, process-wide ------------------------------------------------
@@ -86,8 +113,8 @@ int host_workers() {
 // row chunks of a transfer: >= 16 of them, each at most 2048 rows
 int64_t chunk_rows(int64_t n) { return std::min<int64_t>(2048, std::max<int64_t>(1, (n + 15) / 16)); }
 
-template <int W>
-__global__ void widen_costs_kernel(const void* __restrict__ src, int32_t* __restrict__ d, int64_t cells) {
+template <int W, typename TD>
+__global__ void widen_costs_kernel(const void* __restrict__ src, TD* __restrict__ d, int64_t cells) {
   for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < (cells >> 2);
        g += int64_t(gridDim.x) * blockDim.x) {
     uint32_t x[4];
@@ -99,9 +126,14 @@ __global__ void widen_costs_kernel(const void* __restrict__ src, int32_t* __rest
       x[0] = w.x & 0xFFFFu; x[1] = w.x >> 16; x[2] = w.y & 0xFFFFu; x[3] = w.y >> 16;
     }
     constexpr uint32_t ALL = W == 1 ? 0xFFu : 0xFFFFu;
-    int32_t o[4];
-    for (int q = 0; q < 4; q++) o[q] = x[q] == ALL ? INF32 : int32_t(x[q]);
-    reinterpret_cast<int4*>(d)[g] = make_int4(o[0], o[1], o[2], o[3]);
+    TD o[4];
+    for (int q = 0; q < 4; q++) o[q] = x[q] == ALL ? inf_of<TD>() : TD(x[q]);
+    if constexpr (sizeof(TD) == 4) {
+      reinterpret_cast<int4*>(d)[g] = make_int4(o[0], o[1], o[2], o[3]);
+    } else {
+      reinterpret_cast<longlong2*>(d)[2 * g] = make_longlong2(o[0], o[1]);
+      reinterpret_cast<longlong2*>(d)[2 * g + 1] = make_longlong2(o[2], o[3]);
+    }
   }
 }
 
@@ -111,27 +143,28 @@ int dist_width(int64_t max_finite) {
 
 }  // namespace
 
-void host_widen_dist(const void* src, int width, int32_t* dst, size_t cnt);   // hostwiden.cpp
-bool host_narrow_i32(const int32_t* src, void* dst, int width, size_t cnt);
+void host_widen_dist(const void* src, int width, void* dst, bool wide, size_t cnt);   // hostwiden.cpp
+bool host_narrow(const void* src, bool wide, void* dst, int width, size_t cnt);
 
-// Uploads the n x n int32 cost matrix h into the contiguous device buffer d narrowed: host
-// threads pack row chunks to u8 (or u16) while the previous chunks are on the wire, and one
-// device pass widens them back to int32 (all-ones -> INF32). The width comes from the first
+// Uploads the n x n int32 (es 4) or int64 (es 8) cost matrix h into the contiguous device
+// buffer d narrowed: host threads pack row chunks to u8 (or u16) while the previous chunks are
+// on the wire, and one device pass widens them back (all-ones -> INF32 / INF_RAW). The width comes from the first
 // rows; a later cell that does not fit aborts the packed upload (handled = false) and the caller
 // copies the int32 matrix as is. The device-side scan then sees exactly the caller's matrix.
-int upload_packed(int64_t n, const int32_t* h, int32_t* d, cudaStream_t s, bool& handled, int& width) {
+int upload_packed(int64_t n, const void* h, int es, void* d, cudaStream_t s, bool& handled, int& width) {
   handled = false;
-  width = 4;
+  width = es;
+  const bool wide = es == 8;
   const char* env = std::getenv("APSP_PACKED_UPLOAD");
   if (env && env[0] == '0') return 0;
   const int64_t cells = n * n;
   if (cells < (int64_t(1) << 22) || cells % 4) return 0;
   // width from the first rows (a bounded sample; the packing itself checks every cell)
   const int64_t sample = std::min<int64_t>(n, 64) * n;
-  int32_t mx = 0;
+  int64_t mx = 0;
   for (int64_t i = 0; i < sample; i++) {
-    const int32_t v = h[i];
-    if (v == INF32) continue;
+    const int64_t v = wide ? static_cast<const int64_t*>(h)[i] : static_cast<const int32_t*>(h)[i];
+    if (v == (wide ? INF_RAW : int64_t(INF32))) continue;
     if (v < 0) return 0;
     mx = std::max(mx, v);
   }
@@ -153,7 +186,8 @@ int upload_packed(int64_t n, const int32_t* h, int32_t* d, cudaStream_t s, bool&
     for (int64_t c = 0; c < nch && !abort; c++) {
       const int64_t r0 = c * rows, r1 = std::min(n, r0 + rows);
       const int64_t a = r0 + (r1 - r0) * t / T, b = r0 + (r1 - r0) * (t + 1) / T;
-      if (a < b && !host_narrow_i32(h + a * n, st + size_t(a * n) * w, w, size_t((b - a) * n))) {
+      if (a < b && !host_narrow(static_cast<const char*>(h) + size_t(a * n) * es, wide, st + size_t(a * n) * w, w,
+                                size_t((b - a) * n))) {
         abort = true;
         return;
       }
@@ -172,8 +206,10 @@ int upload_packed(int64_t n, const int32_t* h, int32_t* d, cudaStream_t s, bool&
   const auto t1 = std::chrono::steady_clock::now();
   cudaError_t e = cuerr ? cudaErrorUnknown : cudaSuccess;
   if (!abort) {
-    if (w == 1) widen_costs_kernel<1><<<148 * 8, 256, 0, s>>>(dev, d, cells);
-    else widen_costs_kernel<2><<<148 * 8, 256, 0, s>>>(dev, d, cells);
+    if (wide && w == 1) widen_costs_kernel<1><<<148 * 8, 256, 0, s>>>(dev, static_cast<int64_t*>(d), cells);
+    else if (wide) widen_costs_kernel<2><<<148 * 8, 256, 0, s>>>(dev, static_cast<int64_t*>(d), cells);
+    else if (w == 1) widen_costs_kernel<1><<<148 * 8, 256, 0, s>>>(dev, static_cast<int32_t*>(d), cells);
+    else widen_costs_kernel<2><<<148 * 8, 256, 0, s>>>(dev, static_cast<int32_t*>(d), cells);
     e = cudaGetLastError();
     count_launches(1);
   }
@@ -187,20 +223,22 @@ int upload_packed(int64_t n, const int32_t* h, int32_t* d, cudaStream_t s, bool&
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   if (e != cudaSuccess) return set_cuda_error(e, "packed upload", __FILE__, __LINE__);
   handled = !abort;
-  width = handled ? w : 4;
+  width = handled ? w : es;
   return 0;
 }
 void host_widen_pred(const uint16_t* src, void* dst, bool wide, size_t cnt);
 
-int32_t readback_width(int64_t n, int64_t max_finite, bool idx, int idx_dtype) {
+int32_t readback_width(int64_t n, int64_t max_finite, int es, bool idx) {
   const int dw = dist_width(max_finite);
-  return (dw ? dw : 4) + (idx ? 2 : 0);
+  return (dw ? dw : es) + (idx ? 2 : 0);
 }
 
-// Reads back n x n int32 dist (and int32 pred when idx_out) from contiguous device buffers.
-// handled = false when the packed path does not apply; the caller then does the plain copies.
-int readback_packed(int64_t n, const int32_t* d, const int32_t* p, int64_t max_finite, void* dist_out, void* idx_out,
-                    int idx_dtype, cudaStream_t s, bool& handled) {
+// Reads back n x n dist (int32 es 4 / int64 es 8) and the int32 pred (when idx_out; written as
+// idx_dtype) from contiguous device buffers. handled = false when the packed path does not
+// apply; the caller then does the plain copies.
+int readback_packed(int64_t n, const void* d, int es, const int32_t* p, int64_t max_finite, void* dist_out,
+                    void* idx_out, int idx_dtype, cudaStream_t s, bool& handled) {
+  const bool wide = es == 8;
   handled = false;
   const char* env = std::getenv("APSP_PACKED_READBACK");
   if (env && env[0] == '0') return 0;
@@ -216,14 +254,9 @@ int readback_packed(int64_t n, const int32_t* d, const int32_t* p, int64_t max_f
   int* bad = reinterpret_cast<int*>(static_cast<char*>(dev) + dbytes + pbytes);
   uint16_t* ppk = reinterpret_cast<uint16_t*>(static_cast<char*>(dev) + dbytes);
   cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), s);
-  const int grid = 148 * 8;
-  const int32_t lim = dw == 1 ? 254 : 65534;
   if (e == cudaSuccess) {
-    if (dw == 1 && pk) pack_result_kernel<1, true><<<grid, 256, 0, s>>>(d, p, cells, dev, ppk, lim, bad);
-    else if (dw == 1) pack_result_kernel<1, false><<<grid, 256, 0, s>>>(d, p, cells, dev, ppk, lim, bad);
-    else if (dw == 2 && pk) pack_result_kernel<2, true><<<grid, 256, 0, s>>>(d, p, cells, dev, ppk, lim, bad);
-    else if (dw == 2) pack_result_kernel<2, false><<<grid, 256, 0, s>>>(d, p, cells, dev, ppk, lim, bad);
-    else pack_result_kernel<0, true><<<grid, 256, 0, s>>>(d, p, cells, dev, ppk, lim, bad);
+    if (wide) launch_pack<int64_t>(dw, pk, d, p, cells, dev, ppk, bad, s);
+    else launch_pack<int32_t>(dw, pk, d, p, cells, dev, ppk, bad, s);
     e = cudaGetLastError();
     count_launches(1);
   }
@@ -241,7 +274,8 @@ int readback_packed(int64_t n, const int32_t* d, const int32_t* p, int64_t max_f
       e = cudaMemcpyAsync(st + r0 * n * dw, static_cast<char*>(dev) + r0 * n * dw, rc * n * dw,
                           cudaMemcpyDeviceToHost, s);
     else
-      e = cudaMemcpyAsync(static_cast<int32_t*>(dist_out) + r0 * n, d + r0 * n, rc * n * 4, cudaMemcpyDeviceToHost, s);
+      e = cudaMemcpyAsync(static_cast<char*>(dist_out) + r0 * n * es, static_cast<const char*>(d) + r0 * n * es,
+                          rc * n * es, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && pk)
       e = cudaMemcpyAsync(st + dbytes + r0 * n * 2, ppk + r0 * n, rc * n * 2, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[size_t(c)], cudaEventDisableTiming);
@@ -258,7 +292,7 @@ int readback_packed(int64_t n, const int32_t* d, const int32_t* p, int64_t max_f
         const int64_t a = r0 + (r1 - r0) * w / T, b = r0 + (r1 - r0) * (w + 1) / T;
         if (a == b) continue;
         const size_t off = size_t(a) * n, cnt = size_t(b - a) * n;
-        if (dw) host_widen_dist(st + off * dw, dw, static_cast<int32_t*>(dist_out) + off, cnt);
+        if (dw) host_widen_dist(st + off * dw, dw, static_cast<char*>(dist_out) + off * es, wide, cnt);
         if (pk) {
           const uint16_t* src = reinterpret_cast<const uint16_t*>(st + dbytes) + off;
           const bool wide = idx_dtype == APSP_DTYPE_I64;

@@ -13,24 +13,37 @@ namespace {
 
 constexpr int32_t kInf32 = 0x3FFFFFFF;   // common.cuh INF32
 
-template <typename S>
-inline int32_t dist_of(S v) { return v == S(~S(0)) ? kInf32 : int32_t(v); }
+constexpr long long kInfRaw = 1LL << 61;   // common.cuh INF_RAW
+
+template <typename S, typename D = int32_t>
+inline D dist_of(S v) { return v == S(~S(0)) ? (sizeof(D) == 4 ? D(kInf32) : D(kInfRaw)) : D(v); }
 
 // ---- AVX-512 -----------------------------------------------------------------------------
 
-template <typename S>
-__attribute__((target("avx512f,avx512bw"))) void widen_dist_avx512(const S* s, int32_t* d, size_t cnt) {
+template <typename S, typename D>
+__attribute__((target("avx512f,avx512bw"))) void widen_dist_avx512(const S* s, D* d, size_t cnt) {
   size_t i = 0;
-  for (; i < cnt && (reinterpret_cast<uintptr_t>(d + i) & 63); i++) d[i] = dist_of(s[i]);
-  const __m512i all = _mm512_set1_epi32(int(S(~S(0)))), inf = _mm512_set1_epi32(kInf32);
-  for (; i + 16 <= cnt; i += 16) {
-    __m512i v;
-    if (sizeof(S) == 1) v = _mm512_cvtepu8_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i)));
-    else v = _mm512_cvtepu16_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i)));
-    v = _mm512_mask_mov_epi32(v, _mm512_cmpeq_epi32_mask(v, all), inf);
-    _mm512_stream_si512(reinterpret_cast<__m512i*>(d + i), v);
+  for (; i < cnt && (reinterpret_cast<uintptr_t>(d + i) & 63); i++) d[i] = dist_of<S, D>(s[i]);
+  if constexpr (sizeof(D) == 4) {
+    const __m512i all = _mm512_set1_epi32(int(S(~S(0)))), inf = _mm512_set1_epi32(kInf32);
+    for (; i + 16 <= cnt; i += 16) {
+      __m512i v;
+      if (sizeof(S) == 1) v = _mm512_cvtepu8_epi32(_mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i)));
+      else v = _mm512_cvtepu16_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(s + i)));
+      v = _mm512_mask_mov_epi32(v, _mm512_cmpeq_epi32_mask(v, all), inf);
+      _mm512_stream_si512(reinterpret_cast<__m512i*>(d + i), v);
+    }
+  } else {
+    const __m512i all = _mm512_set1_epi64((long long)S(~S(0))), inf = _mm512_set1_epi64(kInfRaw);
+    for (; i + 8 <= cnt; i += 8) {
+      __m512i v;
+      if (sizeof(S) == 1) v = _mm512_cvtepu8_epi64(_mm_loadl_epi64(reinterpret_cast<const __m128i*>(s + i)));
+      else v = _mm512_cvtepu16_epi64(_mm_loadu_si128(reinterpret_cast<const __m128i*>(s + i)));
+      v = _mm512_mask_mov_epi64(v, _mm512_cmpeq_epi64_mask(v, all), inf);
+      _mm512_stream_si512(reinterpret_cast<__m512i*>(d + i), v);
+    }
   }
-  for (; i < cnt; i++) d[i] = dist_of(s[i]);
+  for (; i < cnt; i++) d[i] = dist_of<S, D>(s[i]);
   _mm_sfence();
 }
 
@@ -55,6 +68,11 @@ __attribute__((target("avx512f,avx512bw"))) void widen_pred_avx512(const uint16_
 }
 
 // ---- SSE2 baseline -----------------------------------------------------------------------
+
+template <typename S>
+void widen_dist_scalar64(const S* s, int64_t* d, size_t cnt) {
+  for (size_t i = 0; i < cnt; i++) d[i] = dist_of<S, int64_t>(s[i]);
+}
 
 template <typename S>
 void widen_dist_sse2(const S* s, int32_t* d, size_t cnt) {
@@ -104,8 +122,8 @@ void widen_pred_sse2(const uint16_t* s, T* d, size_t cnt) {
   _mm_sfence();
 }
 
-// int32 costs -> u8/u16 (INF32 -> all-ones). Returns false at the first cell that is neither
-// INF32 nor in [0, lim]; the caller then uploads the int32 matrix as is.
+// int32 / int64 costs -> u8/u16 (INF -> all-ones). Returns false at the first cell that is
+// neither INF nor in [0, lim]; the caller then uploads the matrix as is.
 template <typename S>
 __attribute__((target("avx512f,avx512bw"))) bool narrow_avx512(const int32_t* s, S* d, size_t cnt, int32_t lim) {
   size_t i = 0;
@@ -127,10 +145,32 @@ __attribute__((target("avx512f,avx512bw"))) bool narrow_avx512(const int32_t* s,
 }
 
 template <typename S>
-bool narrow_scalar(const int32_t* s, S* d, size_t cnt, int32_t lim) {
+__attribute__((target("avx512f,avx512bw"))) bool narrow_avx512(const int64_t* s, S* d, size_t cnt, int32_t lim) {
+  size_t i = 0;
+  const __m512i inf = _mm512_set1_epi64(kInfRaw), all = _mm512_set1_epi64((long long)S(~S(0))),
+                l = _mm512_set1_epi64(lim);
+  for (; i + 8 <= cnt; i += 8) {
+    const __m512i v = _mm512_loadu_si512(s + i);
+    const __mmask8 isinf = _mm512_cmpeq_epi64_mask(v, inf);
+    if (_mm512_mask_cmpgt_epu64_mask(__mmask8(~isinf), v, l)) return false;
+    const __m512i w = _mm512_mask_mov_epi64(v, isinf, all);
+    if (sizeof(S) == 1) _mm_storel_epi64(reinterpret_cast<__m128i*>(d + i), _mm512_cvtepi64_epi8(w));
+    else _mm_storeu_si128(reinterpret_cast<__m128i*>(d + i), _mm512_cvtepi64_epi16(w));
+  }
+  for (; i < cnt; i++) {
+    if (s[i] == kInfRaw) d[i] = S(~S(0));
+    else if (uint64_t(s[i]) > uint64_t(lim)) return false;
+    else d[i] = S(s[i]);
+  }
+  return true;
+}
+
+template <typename T, typename S>
+bool narrow_scalar(const T* s, S* d, size_t cnt, int32_t lim) {
+  const T inf = sizeof(T) == 4 ? T(kInf32) : T(kInfRaw);
   for (size_t i = 0; i < cnt; i++) {
-    if (s[i] == kInf32) d[i] = S(~S(0));
-    else if (uint32_t(s[i]) > uint32_t(lim)) return false;
+    if (s[i] == inf) d[i] = S(~S(0));
+    else if (s[i] < 0 || s[i] > T(lim)) return false;
     else d[i] = S(s[i]);
   }
   return true;
@@ -143,13 +183,23 @@ bool has_avx512() {
 
 }  // namespace
 
-void host_widen_dist(const void* src, int width, int32_t* dst, size_t cnt) {
+void host_widen_dist(const void* src, int width, void* dst, bool wide, size_t cnt) {
+  if (wide) {
+    if (width == 1) {
+      if (has_avx512()) widen_dist_avx512(static_cast<const uint8_t*>(src), static_cast<int64_t*>(dst), cnt);
+      else widen_dist_scalar64(static_cast<const uint8_t*>(src), static_cast<int64_t*>(dst), cnt);
+    } else {
+      if (has_avx512()) widen_dist_avx512(static_cast<const uint16_t*>(src), static_cast<int64_t*>(dst), cnt);
+      else widen_dist_scalar64(static_cast<const uint16_t*>(src), static_cast<int64_t*>(dst), cnt);
+    }
+    return;
+  }
   if (width == 1) {
-    if (has_avx512()) widen_dist_avx512(static_cast<const uint8_t*>(src), dst, cnt);
-    else widen_dist_sse2(static_cast<const uint8_t*>(src), dst, cnt);
+    if (has_avx512()) widen_dist_avx512(static_cast<const uint8_t*>(src), static_cast<int32_t*>(dst), cnt);
+    else widen_dist_sse2(static_cast<const uint8_t*>(src), static_cast<int32_t*>(dst), cnt);
   } else {
-    if (has_avx512()) widen_dist_avx512(static_cast<const uint16_t*>(src), dst, cnt);
-    else widen_dist_sse2(static_cast<const uint16_t*>(src), dst, cnt);
+    if (has_avx512()) widen_dist_avx512(static_cast<const uint16_t*>(src), static_cast<int32_t*>(dst), cnt);
+    else widen_dist_sse2(static_cast<const uint16_t*>(src), static_cast<int32_t*>(dst), cnt);
   }
 }
 
@@ -163,12 +213,18 @@ void host_widen_pred(const uint16_t* src, void* dst, bool wide, size_t cnt) {
   }
 }
 
-bool host_narrow_i32(const int32_t* src, void* dst, int width, size_t cnt) {
+template <typename T>
+static bool narrow_any(const T* src, void* dst, int width, size_t cnt) {
   if (width == 1)
     return has_avx512() ? narrow_avx512(src, static_cast<uint8_t*>(dst), cnt, 254)
                         : narrow_scalar(src, static_cast<uint8_t*>(dst), cnt, 254);
   return has_avx512() ? narrow_avx512(src, static_cast<uint16_t*>(dst), cnt, 65534)
                       : narrow_scalar(src, static_cast<uint16_t*>(dst), cnt, 65534);
+}
+
+bool host_narrow(const void* src, bool wide, void* dst, int width, size_t cnt) {
+  return wide ? narrow_any(static_cast<const int64_t*>(src), dst, width, cnt)
+              : narrow_any(static_cast<const int32_t*>(src), dst, width, cnt);
 }
 
 }  // namespace apsp

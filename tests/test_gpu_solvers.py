@@ -531,3 +531,36 @@ def test_host_transfers_other_algorithms(cuda, algorithm, kw):
     assert r.info["d2h_bytes_per_cell"] == 3 and r.info["h2d_bytes_per_cell"] == 1
     assert np.array_equal(r.distances, dev.distances.cpu().numpy())
     assert np.array_equal(r.index, dev.index.cpu().numpy())
+
+
+@pytest.mark.parametrize("alpha", [100, 3000, 10 ** 6])
+def test_int64_api_narrowed_transfers(cuda, alpha):
+    """The reference-facing int64 API (CostMatrix in, int64 ApspSolution out) moves its data
+    narrowed too: int64 costs -> u8/u16 up, dist u8/u16 (INF_RAW = all-ones) and pred u16 down.
+    Results equal the device-resident int64 solve cell for cell; a late wide cell or a negative
+    cost falls back to the plain int64 upload with the reference's error."""
+    import torch
+    from paper_2310_03983_b200.core import NegativeWeightError
+
+    n = 2048
+    h64 = ap.dense_costs(ap.GenParams(n, 0.1, alpha, 21 + alpha), np.int64)
+    s = ap.fw_classic(ap.CostMatrix(h64))
+    dev = ap.solve(torch.from_numpy(h64).cuda())
+    d = np.asarray(s.distances.raw)
+    assert np.array_equal(d, dev.distances.cpu().numpy())
+    assert np.array_equal(np.asarray(s.pred.raw), dev.index.cpu().numpy().astype(np.int64))
+    up = {100: 1, 3000: 2, 10 ** 6: 8}[alpha]
+    m = s.info["max_finite"]
+    down = (1 if m <= 254 else 2 if m <= 65534 else 8) + 2
+    assert s.info["h2d_bytes_per_cell"] == up and s.info["d2h_bytes_per_cell"] == down
+    if alpha == 100:
+        h64 = h64.copy()   # CostMatrix froze the first one
+        h64[n - 1, 5] = 70000
+        s2 = ap.fw_classic(ap.CostMatrix(h64))
+        assert s2.info["h2d_bytes_per_cell"] == 8
+        dev2 = ap.solve(torch.from_numpy(h64).cuda())
+        assert np.array_equal(np.asarray(s2.distances.raw), dev2.distances.cpu().numpy())
+        h64 = h64.copy()
+        h64[n - 1, 5] = -3
+        with pytest.raises(NegativeWeightError):
+            ap.fw_classic(ap.CostMatrix(h64))
