@@ -110,7 +110,7 @@ def fw_classic(h: CostMatrix, *, tile_size: int = DEFAULT_TILE_SIZE, workers: in
     return ApspSolution(
         distances=CostMatrix(dist, _validated=True),
         via=None,
-        pred=PredMatrix(pred),
+        pred=PredMatrix(pred, _validated=True),
         iterations=0,
         relaxation_count=n * n * n,
         algorithm="fw_classic",
@@ -140,8 +140,8 @@ def rkleene(h: CostMatrix, *, base_threshold: int = DEFAULT_BASE_THRESHOLD, tile
                                   aligned=int(split == "aligned"), tier=tier, device=device)
     return ApspSolution(
         distances=CostMatrix(dist, _validated=True),
-        via=ViaMatrix(idx) if track == "via" else None,
-        pred=PredMatrix(idx) if track == "pred" else None,
+        via=ViaMatrix(idx, _validated=True) if track == "via" else None,
+        pred=PredMatrix(idx, _validated=True) if track == "pred" else None,
         iterations=0,
         relaxation_count=n * n * n,
         algorithm="rkleene",
@@ -157,7 +157,7 @@ def fw_squaring(h: CostMatrix, *, tile_size: int = DEFAULT_TILE_SIZE, workers: i
     dist, via, info = _host_solve(nat.ALG_FW_SQUARING, h, idx_mode=nat.IDX_VIA, tier=tier, device=device)
     return ApspSolution(
         distances=CostMatrix(dist, _validated=True),
-        via=ViaMatrix(via),
+        via=ViaMatrix(via, _validated=True),
         pred=None,
         iterations=info.iterations,
         relaxation_count=info.iterations * n * n * n,
