@@ -354,9 +354,10 @@ def bench_single(args):
                                       "achieved_isolated": c["achieved_T"], "frac_isolated": c["frac_of_dpx_ceiling"],
                                       "source": "profiles/ncu_phase3b.json (ncu --set full, round-7 phase-3b launch)"}
 
-    e2e = None
+    e2e = api = None
     if not args.no_e2e:
         e2e = bench_e2e(lib, nat, h_np, n, args, block)
+        api = bench_python_api(h_np, n)
     cpu = nxb = None
     if not args.no_cpu:
         cpu = cpu_baseline(h_np)
@@ -372,9 +373,36 @@ def bench_single(args):
         "fp32_core_peak": FP32_CORE_PEAK,
         "clocks": clk.summary(), "gpu_launches": launches_timed,
         "tier": tier, "max_finite_distance": info.max_finite,
-        "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu, "networkx_baseline": nxb,
+        "roofline": roofline, "e2e": e2e, "python_api_e2e": api, "cpu_baseline": cpu, "networkx_baseline": nxb,
     }
     print(json.dumps(line), flush=True)
+
+
+def bench_python_api(h_np, n, reps=3):
+    """The reference-facing Python call a user of the reference makes: fw_classic on an int64
+    CostMatrix (pageable numpy in, frozen int64 ApspSolution out), wall clock per call."""
+    import paper_2310_03983_b200 as ap
+
+    h64 = h_np.astype(np.int64)
+    h64[h_np == ap.INF32] = ap.INF_RAW   # (np.where with the int32 array would wrap INF_RAW to 0)
+    h = ap.CostMatrix(h64, _validated=True)
+    ap.fw_classic(h)   # warm-up: staging buffers, pool growth
+    ts = []
+    for _ in range(reps):
+        t = time.perf_counter()
+        sol = ap.fw_classic(h)
+        ts.append(time.perf_counter() - t)
+        info = sol.info
+        del sol
+    dt = statistics.median(ts)
+    return {"value": n ** 3 / dt, "unit": UNIT, "ms_per_call": dt * 1e3, "calls": reps,
+            "ms_all": [round(x * 1e3, 1) for x in ts], "device_ms": info.get("device_ms"), "tier": info.get("tier"),
+            "classic_for_zero_edges": info.get("classic_for_zero_edges"),
+            "wire_bytes_per_cell": [info.get("h2d_bytes_per_cell"), info.get("d2h_bytes_per_cell")],
+            "api": "paper_2310_03983_b200.fw_classic(CostMatrix) -> ApspSolution (int64, pageable numpy both ways; "
+                   "reference solvers.py:118-155 signature)",
+            "h2d_bytes_per_call": n * n * 8, "d2h_bytes_per_call": n * n * 16,
+            "note": "bytes are those of the int64 host arrays; on the wire they travel narrowed (csrc/hostio.cu)"}
 
 
 def bench_e2e(lib, nat, h_np, n, args, block):
