@@ -6,6 +6,7 @@
 //
 // Race freedom: with a zero diagonal and nonnegative costs, row k and column k are invariant
 // during step k (solvers.py:79-81), so one barrier per k suffices.
+#include <algorithm>
 #include <cstdlib>
 #include "launch.h"
 #include "tiles.cuh"
@@ -52,8 +53,112 @@ __global__ void __launch_bounds__(256) fw_step_kernel(typename StoreT<S>::T* D, 
   }
 }
 
+// K1 for the narrow stores: HBM-bound, so each thread streams 16-byte row segments (16 u8 or
+// 8 u16 cells) down a band of rows, four rows in flight. The cells are relaxed as packed
+// 16-bit pairs with one VIADDMNMX.U16x2 (min(D[i][k] + D[k][j], D[i][j])) per two cells; the
+// sums stay below 2^16 (u8: <= 510, u16: <= 1022). Row k's pairs stay in registers, column k is
+// one broadcast byte per row, and a row whose D[i][k] is Infinity is skipped unread. Pred row k
+// is read only for improved cells. Same strict-< rule and idx semantics as
+// fw_step_kernel (row and column k are invariant during step k).
+template <int S>
+__device__ __forceinline__ void seg_to_pairs(const uint4& g, uint32_t (&p)[8 / sizeof(typename StoreT<S>::T)]) {
+  const uint32_t w[4] = {g.x, g.y, g.z, g.w};
+  if constexpr (sizeof(typename StoreT<S>::T) == 1) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      p[2 * q] = __byte_perm(w[q], 0, 0x4140);
+      p[2 * q + 1] = __byte_perm(w[q], 0, 0x4342);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; q++) p[q] = w[q];
+  }
+}
+
+template <int S>
+__device__ __forceinline__ uint4 pairs_to_seg(const uint32_t (&p)[8 / sizeof(typename StoreT<S>::T)]) {
+  if constexpr (sizeof(typename StoreT<S>::T) == 1)
+    return make_uint4(__byte_perm(p[0], p[1], 0x6420), __byte_perm(p[2], p[3], 0x6420),
+                      __byte_perm(p[4], p[5], 0x6420), __byte_perm(p[6], p[7], 0x6420));
+  else
+    return make_uint4(p[0], p[1], p[2], p[3]);
+}
+
+template <int S>
+__global__ void __launch_bounds__(256, 3) fw_step_vec_kernel(typename StoreT<S>::T* D, int64_t ld, int64_t n, int64_t k,
+                                                          int32_t* idx, int64_t ldi, int mode, int64_t via_off,
+                                                          Status* st, int rows) {
+  using T = typename StoreT<S>::T;
+  constexpr int V = 16 / int(sizeof(T)), P = V / 2;
+  const uint32_t INF = store_inf<S>();
+  const int64_t j0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) * V;
+  if (j0 >= n) return;
+  uint32_t dkj[P];
+  seg_to_pairs<S>(*reinterpret_cast<const uint4*>(D + k * ld + j0), dkj);
+  bool changed = false;
+  const int64_t i1 = std::min<int64_t>(n, (int64_t(blockIdx.y) + 1) * rows);
+  constexpr int R = 4;   // rows in flight per thread: their loads are issued before any store
+  // column-k bytes run one batch ahead, so a batch's segment loads never wait on them
+  uint32_t dnext[R];
+  const int64_t ib = int64_t(blockIdx.y) * rows;
+#pragma unroll
+  for (int r = 0; r < R; r++) dnext[r] = ib + r < i1 ? uint32_t(D[(ib + r) * ld + k]) : INF;
+  for (int64_t i0 = ib; i0 < i1; i0 += R) {
+    uint32_t dik[R];
+    uint4 seg[R];
+#pragma unroll
+    for (int r = 0; r < R; r++) dik[r] = dnext[r];
+#pragma unroll
+    for (int r = 0; r < R; r++)
+      if (dik[r] != INF) seg[r] = *reinterpret_cast<const uint4*>(D + (i0 + r) * ld + j0);
+#pragma unroll
+    for (int r = 0; r < R; r++) dnext[r] = i0 + R + r < i1 ? uint32_t(D[(i0 + R + r) * ld + k]) : INF;
+#pragma unroll
+    for (int r = 0; r < R; r++) {
+      if (dik[r] == INF) continue;
+      uint32_t v[P], nv[P], diff = 0;
+      seg_to_pairs<S>(seg[r], v);
+      const uint32_t dik2 = dik[r] * 0x00010001u;
+#pragma unroll
+      for (int q = 0; q < P; q++) {
+        nv[q] = __viaddmin_u16x2(dik2, dkj[q], v[q]);
+        diff |= nv[q] ^ v[q];
+      }
+      if (!diff) continue;
+      const int64_t i = i0 + r;
+      changed = true;
+      *reinterpret_cast<uint4*>(D + i * ld + j0) = pairs_to_seg<S>(nv);
+      if (!idx) continue;
+      const int32_t* pk = idx + k * ldi + j0;   // pred row k (invariant in step k; L1/L2-resident)
+#pragma unroll
+      for (int q = 0; q < P; q++) {
+        const uint32_t x = nv[q] ^ v[q];
+        if (x & 0xFFFFu) idx[i * ldi + j0 + 2 * q] = mode == IDX_PRED ? pk[2 * q] : int32_t(via_off + k);
+        if (x >> 16) idx[i * ldi + j0 + 2 * q + 1] = mode == IDX_PRED ? pk[2 * q + 1] : int32_t(via_off + k);
+      }
+    }
+  }
+  if (st && changed) st->changed = 1;
+}
+
 int launch_fw_step(int store, void* D, int64_t ld, int64_t n, int64_t k, int32_t* idx, int64_t ldi, int mode,
                    int64_t via_off, Status* st, cudaStream_t s) {
+  if ((store == STORE_U8 || store == STORE_U16) && !getenv("APSP_K1_SCALAR")) {
+    const int es = int(store_elem_size(store)), V = 16 / es;
+    if (n % V == 0 && (ld * es) % 16 == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0) {
+      const int64_t bx = (n / V + 255) / 256;
+      // one full wave: 148 SMs x 3 resident CTAs (launch bounds), each streaming `rows` rows
+      const int rows = int(std::max<int64_t>(8, (n * bx + 148 * 3 - 1) / (148 * 3)));
+      const dim3 g(unsigned(bx), unsigned((n + rows - 1) / rows));
+      if (store == STORE_U8)
+        fw_step_vec_kernel<STORE_U8><<<g, 256, 0, s>>>((uint8_t*)D, ld, n, k, idx, ldi, mode, via_off, st, rows);
+      else
+        fw_step_vec_kernel<STORE_U16><<<g, 256, 0, s>>>((uint16_t*)D, ld, n, k, idx, ldi, mode, via_off, st, rows);
+      APSP_CUDA_TRY(cudaGetLastError());
+      count_launches(1);
+      return 0;
+    }
+  }
   dim3 grid(unsigned((n + 31) / 32), unsigned((n + 31) / 32));
   switch (store) {
     case STORE_I32: fw_step_kernel<STORE_I32><<<grid, 256, 0, s>>>((int32_t*)D, ld, n, k, idx, ldi, mode, via_off, st); break;

@@ -485,11 +485,16 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
 
 int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, cudaStream_t s,
                     apsp_info* info) {
+  // Classic k order (K1, solvers.py:77-95): n HBM-bound steps, so the narrowest certified
+  // store matters -- a u8 store moves 1 byte per cell per step instead of 4 or 8. The
+  // predecessors are written in place into the caller's matrix.
   if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
   Scratch sc;
-  int rc = sc.acquire(nullptr, 0, header_bytes(), s);
+  const size_t store_off = (header_bytes() + 255) / 256 * 256;
+  int rc = sc.acquire(nullptr, 0, store_off + size_t(n) * n * 2 + 256, s);   // header + u8/u16 store
   if (rc) return rc;
   Header* hdr_dev = static_cast<Header*>(sc.base);
+  char* Dn = static_cast<char*>(sc.base) + store_off;
   Header hdr{};
   Timer tm(s);
   rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
@@ -498,23 +503,45 @@ int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   const ScanResult scan = hdr.scan;
   rc = check_scan(scan);
   if (rc) return rc;
-  const int store = api_store(dtype);
-  APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
-  // pred init in place (to_store with identical in/out is elementwise)
-  rc = launch_to_store(dtype, dist, ld, n, store, dist, ld, n, pred, ldp, 1, s);
-  for (int64_t k = 0; !rc && k < n; k++) rc = launch_fw_step(store, dist, ld, n, k, pred, ldp, IDX_PRED, 0, &hdr_dev->status, s);
-  if (rc) return rc;
-  const int tier = dtype == APSP_DTYPE_I32 ? APSP_TIER_I32 : dtype == APSP_DTYPE_F32 ? APSP_TIER_F32 : APSP_TIER_I64;
-  bool ok = false;
-  rc = certify(tier, store, dist, ld, n, n, scan, hdr_dev, hdr, s, ok);
-  if (rc) return rc;
-  if (!ok) return set_error(APSP_ERANGE, "shortest-path cost left the representable int32 range");
+  const int exact_store = api_store(dtype);
+  const int exact_tier = dtype == APSP_DTYPE_I32 ? APSP_TIER_I32 : dtype == APSP_DTYPE_F32 ? APSP_TIER_F32 : APSP_TIER_I64;
+  std::vector<int> tiers;
+  if (!getenv("APSP_CLASSIC_EXACT"))
+    for (int t : pick_tiers(dtype, scan, -1, true, n))
+      if (t == APSP_TIER_U8 || t == APSP_TIER_U16) tiers.push_back(t);
+  tiers.push_back(exact_tier);
+  int used = -1, tried = 0, launches = 1;
+  for (int tier : tiers) {
+    const bool narrow = tier != exact_tier;
+    const int store = narrow ? tier_store(tier) : exact_store;
+    void* D = narrow ? static_cast<void*>(Dn) : dist;
+    const int64_t ldd = narrow ? n : ld;
+    tried |= 1 << tier;
+    APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
+    // pred init (and the store; in place for the exact store -- to_store is elementwise)
+    rc = launch_to_store(dtype, dist, ld, n, store, D, ldd, n, pred, ldp, 1, s);
+    for (int64_t k = 0; !rc && k < n; k++) rc = launch_fw_step(store, D, ldd, n, k, pred, ldp, IDX_PRED, 0, &hdr_dev->status, s);
+    if (rc) return rc;
+    launches += int(n) + 2;
+    bool ok = false;
+    rc = certify(tier, store, D, ldd, n, n, scan, hdr_dev, hdr, s, ok);
+    if (rc) return rc;
+    if (!ok && !narrow) return set_error(APSP_ERANGE, "shortest-path cost left the representable int32 range");
+    if (!ok) continue;
+    if (narrow) {
+      rc = launch_from_store(store, D, ldd, n, n, dtype, dist, ld, s);
+      if (rc) return rc;
+      launches++;
+    }
+    used = tier;
+    break;
+  }
   const double ms = tm.stop();
   if (info) {
-    info->tier = tier;
-    info->tiers_tried = 1 << tier;
+    info->tier = used;
+    info->tiers_tried = tried;
     info->iterations = 0;
-    info->launches = int32_t(n + 3);
+    info->launches = launches;
     info->max_finite = hdr.cert.max_finite;
     info->relaxations = n * n * n;
     info->device_ms = ms;

@@ -1,0 +1,39 @@
+#!/usr/bin/env python3
+"""Time the classic-k-order path (K1): fw_classic(method="classic") and the zero-cost-edge
+fallback of the blocked solver, at n (default 8192)."""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import paper_2310_03983_b200 as ap  # noqa: E402
+
+
+def main():
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+    h = ap.dense_costs(ap.GenParams(n, 0.1, 100, 7 + n), np.int32)
+    hz = h.copy()
+    rng = np.random.default_rng(1)
+    fin = (hz != ap.INF32) & ~np.eye(n, dtype=bool)
+    zero = fin & (rng.random((n, n)) < 0.05)
+    hz[zero] = 0
+    for label, mat, alg in (("classic order", h, "fw_classic"), ("zero-cost edges (blocked -> classic)", hz, "fw_blocked")):
+        d = torch.from_numpy(mat).cuda()
+        ap.solve(d, alg)
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        r = ap.solve(d, alg)
+        torch.cuda.synchronize()
+        ms = (time.perf_counter() - t) * 1e3
+        print(f"{label} n={n}: {ms:.1f} ms tier={r.info['tier']} tried={r.info['tiers_tried']} "
+              f"zero_edges_flag={r.info.get('classic_for_zero_edges')}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
