@@ -564,3 +564,20 @@ def test_int64_api_narrowed_transfers(cuda, alpha):
         h64[n - 1, 5] = -3
         with pytest.raises(NegativeWeightError):
             ap.fw_classic(ap.CostMatrix(h64))
+
+
+@pytest.mark.parametrize("n", [512, 520, 301])
+@pytest.mark.parametrize("wmax,zero", [(60, 0.0), (60, 0.2), (400, 0.0), (100000, 0.0)])
+def test_classic_order_narrow_stores_bitwise(cuda, n, wmax, zero):
+    """Classic k order (K1) on the narrowest certified store: u8 (small weights), u16 (sums past
+    254) or the exact store, through the packed-pair streaming kernel (n a multiple of 16 / 8)
+    or the scalar one (n = 301). Distances and pred bit-exact with reference fw_classic."""
+    raw = random_graph_raw(n, 0.05, wmax, n + wmax, zero_frac=zero)
+    want_d, want_p = orc.fw_classic(raw)
+    s = ap.fw_classic(ap.CostMatrix(raw), method="classic")
+    assert np.array_equal(s.distances.raw, want_d)
+    assert np.array_equal(s.pred.raw, want_p)
+    if zero:   # the blocked solver falls back to the same classic order
+        b = ap.fw_classic(ap.CostMatrix(raw))
+        assert b.info["classic_for_zero_edges"]
+        assert np.array_equal(b.distances.raw, want_d) and np.array_equal(b.pred.raw, want_p)
