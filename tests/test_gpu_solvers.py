@@ -544,8 +544,8 @@ def test_int64_api_narrowed_transfers(cuda, alpha):
 
     n = 2048
     h64 = ap.dense_costs(ap.GenParams(n, 0.1, alpha, 21 + alpha), np.int64)
+    dev = ap.solve(torch.from_numpy(h64).cuda())   # before CostMatrix freezes h64
     s = ap.fw_classic(ap.CostMatrix(h64))
-    dev = ap.solve(torch.from_numpy(h64).cuda())
     d = np.asarray(s.distances.raw)
     assert np.array_equal(d, dev.distances.cpu().numpy())
     assert np.array_equal(np.asarray(s.pred.raw), dev.index.cpu().numpy().astype(np.int64))
@@ -556,9 +556,9 @@ def test_int64_api_narrowed_transfers(cuda, alpha):
     if alpha == 100:
         h64 = h64.copy()   # CostMatrix froze the first one
         h64[n - 1, 5] = 70000
+        dev2 = ap.solve(torch.from_numpy(h64).cuda())
         s2 = ap.fw_classic(ap.CostMatrix(h64))
         assert s2.info["h2d_bytes_per_cell"] == 8
-        dev2 = ap.solve(torch.from_numpy(h64).cuda())
         assert np.array_equal(np.asarray(s2.distances.raw), dev2.distances.cpu().numpy())
         h64 = h64.copy()
         h64[n - 1, 5] = -3
