@@ -545,7 +545,15 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
     import torch.distributed as dist
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    os.environ.setdefault("NCCL_DEBUG", "WARN")     # keep stdout to the one JSON line
+    # Keep stdout to the one JSON line: the process's fd 1 points at stderr for the whole run
+    # (NCCL prints its version banner with printf at communicator init), and the JSON line goes
+    # to the saved original stdout.
+    import sys
+
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
@@ -640,6 +648,6 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
                     {"block": block, "rows_per_rank": R, "fused_exchange": fused}),
                 "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e, "cpu_baseline": None,
                 "tier": res.info["tier"]}
-        print(json.dumps(line), flush=True)
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
     dist.destroy_process_group()
