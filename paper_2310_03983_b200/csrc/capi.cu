@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include "engine.h"
 
 using namespace apsp;
@@ -187,8 +188,14 @@ int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* di
   if (e != cudaSuccess) return fail(set_cuda_error(e, "host staging", __FILE__, __LINE__));
   apsp_info local{};
   local.max_finite = -1;   // stays -1 (no packed readback) unless the solver reports it
+  // blocked FW: the last round's row bands stream to the host while the rest computes
+  std::unique_ptr<BandSink> bands;
+  if (algorithm == APSP_ALG_FW_BLOCKED && (dtype == APSP_DTYPE_I32 || dtype == APSP_DTYPE_I64))
+    bands = make_band_stream(n, int(es), dist_out, idx_out, idx_dtype, s);
   switch (algorithm) {
-    case APSP_ALG_FW_BLOCKED: rc = fw_blocked_impl(dtype, n, d, n, p, n, block, tier, nullptr, 0, s, &local); break;
+    case APSP_ALG_FW_BLOCKED:
+      rc = fw_blocked_impl(dtype, n, d, n, p, n, block, tier, nullptr, 0, s, &local, bands.get());
+      break;
     case APSP_ALG_FW_CLASSIC: rc = fw_classic_impl(dtype, n, d, n, p, n, s, &local); break;
     case APSP_ALG_RKLEENE:
       rc = rkleene_impl(dtype, n, d, n, p, n, idx_mode, base_threshold, aligned, tier, nullptr, 0, s, &local);
@@ -198,6 +205,14 @@ int apsp_solve_host(int algorithm, int dtype, int64_t n, const void* h, void* di
   }
   local.h2d_bytes_per_cell = up ? up_width : int32_t(es);
   if (info) *info = local;
+  if (bands) {   // the streamed rows stand only if the u8 attempt certified
+    const bool streamed = finish_band_stream(bands.get()) && rc == 0 && local.tier == APSP_TIER_U8;
+    bands.reset();   // releases the readback staging
+    if (streamed) {
+      if (info) info->d2h_bytes_per_cell = 1 + 2;
+      return fail(0);
+    }
+  }
   if (rc) return fail(rc);
   if (dtype == APSP_DTYPE_I32 || dtype == APSP_DTYPE_I64) {   // integer results: narrowed readback
     bool done = false;

@@ -4,6 +4,7 @@
 #pragma once
 #include <atomic>
 #include <cstdint>
+#include <memory>
 #include <vector>
 #include <nvtx3/nvToolsExt.h>
 #include "../../include/apsp_b200.h"
@@ -127,6 +128,16 @@ struct FwCtx {
   char* p2prep = nullptr;        // narrow tiers: bulk-copy layouts of the phase-2 operands
   char* sub = nullptr;           // scratch of the phase-1 sub-run when b > 128
   int launches = 0;
+  struct BandSink* sink = nullptr;   // last round in row bands, each handed to the sink
+};
+
+// Consumer of the final rows of a blocked FW solve: with a sink, the last round's phase 3 runs
+// in row bands and band() is called right after each band's launch on s (rows [r0, r1) of the
+// padded matrix are final once that launch completes; c.store says which value tier produced
+// them -- an attempt that later fails its certificate is followed by another run).
+struct BandSink {
+  virtual ~BandSink() = default;
+  virtual int band(int64_t r0, int64_t r1, const FwCtx& c, cudaStream_t s) = 0;
 };
 
 struct Timer {
@@ -198,7 +209,7 @@ int default_block(int64_t n);
 size_t fw_ws_bytes(int dtype, int64_t n, int block);
 
 int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
-                    void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info);
+                    void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info, BandSink* sink = nullptr);
 
 int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, cudaStream_t s,
                     apsp_info* info);
@@ -245,5 +256,9 @@ int readback_packed(int64_t n, const void* d, int es, const int32_t* p, int64_t 
                     void* idx_out, int idx_dtype, cudaStream_t s, bool& handled);
 int32_t readback_width(int64_t n, int64_t max_finite, int es, bool idx);   // bytes per cell when handled
 int upload_packed(int64_t n, const void* h, int es, void* d, cudaStream_t s, bool& handled, int& width);
+// last-round streaming readback of apsp_solve_host's blocked FW (nullptr when it does not apply)
+std::unique_ptr<BandSink> make_band_stream(int64_t n, int es, void* dist_out, void* idx_out, int idx_dtype,
+                                           cudaStream_t s);
+bool finish_band_stream(BandSink* b);   // true: dist/idx already hold the certified result
 
 }  // namespace apsp

@@ -174,6 +174,7 @@ int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s) {
   sub.b = TILE_ALIGN;
   sub.via_off = c.via_off + k0;
   sub.side = nullptr;
+  sub.sink = nullptr;   // the sub-run's last round is not the solve's
   sub.rowsnap = sub.colsnap = nullptr;
   sub.prep[0] = sub.prep[1] = sub.p2prep = sub.sub = nullptr;
   if (c.sub) fw_carve(sub, c.sub, c.b);
@@ -309,6 +310,31 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   return timed_minplus(c.store, a, s);
 }
 
+// phase 3 of pivot block k0 restricted to output rows [r0, r1) (128-aligned): the last round
+// in bands for a BandSink
+int fw_phase3_rows(FwCtx& c, int64_t k0, int64_t r0, int64_t r1, cudaStream_t s) {
+  NvtxRange r("apsp.fw.phase3band");
+  MinplusArgs a = minplus_args();
+  a.A = c.D + (r0 * c.ld + k0) * c.es; a.lda = c.ld;
+  a.B = c.D + k0 * c.ld * c.es; a.ldb = c.ld;
+  a.C = c.D + r0 * c.ld * c.es; a.ldc = c.ld;
+  a.idx = c.P ? c.P + r0 * c.ldp : nullptr; a.ldi = c.ldp;
+  a.predB = c.P ? c.P + k0 * c.ldp : nullptr; a.ldp = c.ldp;
+  a.m = r1 - r0; a.n = c.m; a.k = c.b;
+  a.inner_off = c.via_off + k0;
+  a.mode = c.mode;
+  a.skip_row_lo = k0 - r0; a.skip_row_hi = k0 + c.b - r0;   // band-relative (may lie outside)
+  a.skip_col_lo = k0; a.skip_col_hi = k0 + c.b;
+  a.status = c.st;
+  if (c.prep[0] && bulk_store(c.store, c.b)) {
+    char* slot = c.prep[(k0 / c.b) & 1];
+    a.Aprep = prep_a(slot) + (r0 / TILE_ALIGN) * (c.b / 32) * (32 * TILE_ALIGN);   // the band's A tiles
+    a.Bprep = prep_b(slot, c.m, c.b);
+  }
+  c.launches++;
+  return timed_minplus(c.store, a, s);
+}
+
 int fw_run(FwCtx& c, cudaStream_t s) {
   const int64_t b = c.b;
   int rc = fw_phase1(c, 0, s);
@@ -325,7 +351,14 @@ int fw_run(FwCtx& c, cudaStream_t s) {
   }
   for (int64_t k0 = 0; !rc && k0 < c.m; k0 += b) {
     const int64_t k1 = k0 + b;
-    if (k1 >= c.m) {
+    if (k1 >= c.m && c.sink) {   // last round in row bands, each final as soon as it lands
+      const int64_t bandr = std::max<int64_t>(TILE_ALIGN, (c.m / 8 + TILE_ALIGN - 1) / TILE_ALIGN * TILE_ALIGN);
+      for (int64_t r0 = 0; !rc && r0 < c.m; r0 += bandr) {
+        const int64_t r1 = std::min(c.m, r0 + bandr);
+        rc = fw_phase3_rows(c, k0, r0, r1, s);
+        if (!rc) rc = c.sink->band(r0, r1, c, s);
+      }
+    } else if (k1 >= c.m) {
       rc = fw_phase3(c, k0, -1, -1, s);
     } else if (c.side) {
       rc = fw_phase3(c, k0, k1, -1, s);                       // 3a: next pivot cross
@@ -383,7 +416,7 @@ size_t fw_ws_bytes(int dtype, int64_t n, int block) {
 }
 
 int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
-                    void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info) {
+                    void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info, BandSink* sink) {
   if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
   if (b <= 0) b = default_block(n);
   if (b % 128 || b < 128 || b > 4096) return set_error(APSP_EINVAL, "blocked FW block must be a multiple of 128 in [128, 4096] (got %d)", b);
@@ -435,12 +468,13 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
       if (getenv("APSP_NO_BULK")) c.prep[0] = c.prep[1] = nullptr;
       // graph replay only where launch gaps dominate (N <= 2048): a graph drops the lookahead
       // stream's priority, which costs more than the gaps at larger N (n=8192 21.6 -> 25 ms)
-      if (N <= 2048) {
+      if (N <= 2048) {   // (no band sink here: the graph holds the whole chain)
         int dev = 0;
         cudaGetDevice(&dev);
         const GraphKey key{dev, 1, store, c.mode, N, b, D, Pw, scratch, c.side, s};
         rc = run_graphed(key, s, [&](cudaStream_t st) { return fw_run(c, st); });
       } else {
+        c.sink = sink;
         rc = fw_run(c, s);
       }
       launches += c.launches;

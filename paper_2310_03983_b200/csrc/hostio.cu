@@ -14,6 +14,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <memory>
 #include <cstdio>
 #include <mutex>
 #include <thread>
@@ -325,5 +327,170 @@ int readback_packed(int64_t n, const void* d, int es, const int32_t* p, int64_t 
   handled = !flagged;   // a value outside the promised width: the caller copies int32 as is
   return 0;
 }
+
+// ---- last-round streaming readback (blocked FW, u8 tier) ----------------------------------
+
+namespace {
+
+__global__ void pack_pred_rows_kernel(const int32_t* __restrict__ P, int64_t ldp, int64_t rows, int64_t n,
+                                      uint16_t* __restrict__ out) {
+  const int64_t q = n >> 2, total = rows * q;
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = g / q, j = 4 * (g - i * q);
+    const int4 v = *reinterpret_cast<const int4*>(P + i * ldp + j);
+    *reinterpret_cast<uint2*>(out + i * n + j) = make_uint2(uint32_t(v.x + 1) | uint32_t(v.y + 1) << 16,
+                                                            uint32_t(v.z + 1) | uint32_t(v.w + 1) << 16);
+  }
+}
+
+// The last FW round's row bands go to the host as they land: the u8 store rows are the dist
+// readback as they are (255 = Infinity), pred rows are packed to u16 on a copy stream, and host
+// workers widen each band into the caller's buffers while later bands are still computing.
+// Valid only if the u8 attempt is the one that certifies; otherwise the caller reads back as
+// usual and overwrites whatever was streamed.
+class BandStream final : public BandSink {
+ public:
+  BandStream(int64_t n, int es, void* dist_out, void* idx_out, int idx_dtype, cudaStream_t s)
+      : n_(n), es_(es), dist_out_(dist_out), idx_out_(idx_out), wide_idx_(idx_dtype == APSP_DTYPE_I64), lk_(g_down.mu) {
+    pbase_ = (size_t(n) * n + 255) & ~size_t(255);
+    if (g_down.reserve(pbase_ + size_t(n) * n * 2 + 64) != cudaSuccess) return;
+    if (cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking) != cudaSuccess) return;
+    if (cudaMallocAsync(&ppk_, size_t(n) * n * 2, s) != cudaSuccess) return;
+    // the copy stream may use ppk_ only after its allocation on s
+    cudaEvent_t e;
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    cudaStreamWaitEvent(cs_, e, 0);
+    cudaEventDestroy(e);
+    st_ = static_cast<char*>(g_down.ptr);
+    const int T = host_workers();
+    for (int t = 0; t < T; t++) pool_.emplace_back([this, t, T] { work(t, T); });
+    ok_ = true;
+  }
+  ~BandStream() override { finish(); }
+
+  bool ready() const { return ok_; }
+
+  int band(int64_t r0, int64_t r1, const FwCtx& c, cudaStream_t s) override {
+    r1 = std::min(r1, n_);
+    if (!ok_ || r0 >= r1) return 0;
+    if (c.store != STORE_U8 || !c.P) {   // not the u8 tier: these rows are not ours to stream
+      invalid_ = true;
+      return 0;
+    }
+    cudaEvent_t landed = nullptr, done = nullptr;
+    APSP_CUDA_TRY(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
+    // workers block on it (no spinning: 16 spinning threads would starve the launching thread)
+    APSP_CUDA_TRY(cudaEventCreateWithFlags(&done, cudaEventDisableTiming | cudaEventBlockingSync));
+    APSP_CUDA_TRY(cudaEventRecord(landed, s));
+    APSP_CUDA_TRY(cudaStreamWaitEvent(cs_, landed, 0));
+    cudaEventDestroy(landed);
+    const int64_t rows = r1 - r0;
+    APSP_CUDA_TRY(cudaMemcpy2DAsync(st_ + size_t(r0) * n_, size_t(n_), c.D + r0 * c.ld, size_t(c.ld), size_t(n_),
+                                    size_t(rows), cudaMemcpyDeviceToHost, cs_));
+    pack_pred_rows_kernel<<<148 * 4, 256, 0, cs_>>>(c.P + r0 * c.ldp, c.ldp, rows, n_, ppk_ + r0 * n_);
+    APSP_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    APSP_CUDA_TRY(cudaMemcpyAsync(st_ + pbase_ + size_t(r0) * n_ * 2, ppk_ + r0 * n_, size_t(rows) * n_ * 2,
+                                  cudaMemcpyDeviceToHost, cs_));
+    APSP_CUDA_TRY(cudaEventRecord(done, cs_));
+    {
+      std::lock_guard<std::mutex> g(qm_);
+      bands_.push_back({r0, r1, done});
+      if (r1 == n_) covered_ = true;
+    }
+    qc_.notify_all();
+    return 0;
+  }
+
+  // stops the workers; true when the streamed rows are the certified u8 result
+  bool finish() {
+    if (trace_)
+      std::fprintf(stderr, "[bandstream] solve returned at %.2f ms (%zu bands)\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count(),
+                   bands_.size());
+    {
+      std::lock_guard<std::mutex> g(qm_);
+      if (finished_) return result_;
+      finished_ = true;
+    }
+    qc_.notify_all();
+    for (auto& t : pool_) t.join();
+    pool_.clear();
+    if (cs_) cudaStreamSynchronize(cs_);
+    for (auto& b : bands_) cudaEventDestroy(b.ev);
+    if (ppk_) cudaFreeAsync(ppk_, cs_);
+    if (cs_) {
+      cudaStreamSynchronize(cs_);
+      cudaStreamDestroy(cs_);
+    }
+    cs_ = nullptr;
+    ppk_ = nullptr;
+    result_ = ok_ && !invalid_ && covered_ && !werr_;
+    if (trace_)
+      std::fprintf(stderr, "[bandstream] widened by %.2f ms, result %d\n",
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count(),
+                   int(result_));
+    return result_;
+  }
+
+ private:
+  struct Band { int64_t r0, r1; cudaEvent_t ev; };
+
+  void work(int t, int T) {
+    size_t next = 0;
+    for (;;) {
+      Band b;
+      {
+        std::unique_lock<std::mutex> g(qm_);
+        qc_.wait(g, [&] { return next < bands_.size() || finished_; });
+        if (next >= bands_.size()) return;   // finished and drained
+        b = bands_[next++];
+      }
+      if (cudaEventSynchronize(b.ev) != cudaSuccess) { werr_ = true; continue; }
+      if (t == 0 && trace_)
+        std::fprintf(stderr, "[bandstream] rows %lld..%lld landed at %.2f ms\n", (long long)b.r0, (long long)b.r1,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_).count());
+      const int64_t a = b.r0 + (b.r1 - b.r0) * t / T, e = b.r0 + (b.r1 - b.r0) * (t + 1) / T;
+      if (a >= e) continue;
+      const size_t off = size_t(a) * n_, cnt = size_t(e - a) * n_;
+      host_widen_dist(st_ + off, 1, static_cast<char*>(dist_out_) + off * es_, es_ == 8, cnt);
+      host_widen_pred(reinterpret_cast<const uint16_t*>(st_ + pbase_) + off,
+                      static_cast<char*>(idx_out_) + off * (wide_idx_ ? 8 : 4), wide_idx_, cnt);
+    }
+  }
+
+  int64_t n_;
+  int es_;
+  void* dist_out_;
+  void* idx_out_;
+  bool wide_idx_;
+  std::unique_lock<std::mutex> lk_;   // the readback staging is ours for the whole solve
+  size_t pbase_ = 0;
+  char* st_ = nullptr;
+  cudaStream_t cs_ = nullptr;
+  uint16_t* ppk_ = nullptr;
+  std::vector<std::thread> pool_;
+  std::mutex qm_;
+  std::condition_variable qc_;
+  std::vector<Band> bands_;
+  bool finished_ = false, covered_ = false, ok_ = false, result_ = false;
+  std::atomic<bool> invalid_{false}, werr_{false};
+  const bool trace_ = std::getenv("APSP_READBACK_TRACE") != nullptr;
+  const std::chrono::steady_clock::time_point t0_ = std::chrono::steady_clock::now();
+};
+
+}  // namespace
+
+std::unique_ptr<BandSink> make_band_stream(int64_t n, int es, void* dist_out, void* idx_out, int idx_dtype,
+                                           cudaStream_t s) {
+  const char* env = std::getenv("APSP_STREAM_READBACK");
+  if ((env && env[0] == '0') || !idx_out || n >= 65535 || n * n < (int64_t(1) << 22) || n % 4) return nullptr;
+  auto b = std::make_unique<BandStream>(n, es, dist_out, idx_out, idx_dtype, s);
+  if (!b->ready()) return nullptr;
+  return b;
+}
+
+bool finish_band_stream(BandSink* b) { return b && static_cast<BandStream*>(b)->finish(); }
 
 }  // namespace apsp

@@ -581,3 +581,23 @@ def test_classic_order_narrow_stores_bitwise(cuda, n, wmax, zero):
         b = ap.fw_classic(ap.CostMatrix(raw))
         assert b.info["classic_for_zero_edges"]
         assert np.array_equal(b.distances.raw, want_d) and np.array_equal(b.pred.raw, want_p)
+
+
+def test_streamed_last_round_readback(cuda):
+    """apsp_solve_host streams the blocked FW's last round to the host band by band (N > 2048,
+    no graph replay). The streamed rows stand only when the u8 attempt certifies: a ring with
+    chords (true max distance ~2n/step > 254) makes the u8 attempt fail, the u16 run follows and
+    the host arrays must still equal the device-resident result."""
+    import torch
+
+    n = 2304
+    for raw, want_tier in ((ring_with_chords(n, 16, 5), "u16"),
+                           (ap.dense_costs(ap.GenParams(n, 0.1, 100, 31), np.int64), "u8")):
+        h32 = np.where(raw == INF_RAW, INF32, raw).astype(np.int32)
+        dev = ap.solve(torch.from_numpy(h32.copy()).cuda())
+        r = ap.solve(h32)
+        assert r.info["tier"] == want_tier and dev.info["tier"] == want_tier
+        if want_tier == "u16":
+            assert "u8" in r.info["tiers_tried"]
+        assert np.array_equal(r.distances, dev.distances.cpu().numpy())
+        assert np.array_equal(r.index, dev.index.cpu().numpy())
