@@ -554,7 +554,19 @@ int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
     // pred init (and the store; in place for the exact store -- to_store is elementwise)
     rc = launch_to_store(dtype, dist, ld, n, store, D, ldd, n, pred, ldp, 1, s);
-    for (int64_t k = 0; !rc && k < n; k++) rc = launch_fw_step(store, D, ldd, n, k, pred, ldp, IDX_PRED, 0, &hdr_dev->status, s);
+    auto steps = [&](cudaStream_t st) {
+      int r = 0;
+      for (int64_t k = 0; !r && k < n; k++) r = launch_fw_step(store, D, ldd, n, k, pred, ldp, IDX_PRED, 0, &hdr_dev->status, st);
+      return r;
+    };
+    if (!rc && n <= 4096) {   // launch-bound sizes: replay the n steps as one graph
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const GraphKey key{dev, 3, store, IDX_PRED, n, ldd, D, pred, &hdr_dev->status, nullptr, s};
+      rc = run_graphed(key, s, steps);
+    } else if (!rc) {
+      rc = steps(s);
+    }
     if (rc) return rc;
     launches += int(n) + 2;
     bool ok = false;

@@ -25,7 +25,8 @@ def main():
     hz[zero] = 0
     for label, mat, alg in (("classic order", h, "fw_classic"), ("zero-cost edges (blocked -> classic)", hz, "fw_blocked")):
         d = torch.from_numpy(mat).cuda()
-        ap.solve(d, alg)
+        for _ in range(3):   # the third solve replays the captured graph (n <= 4096)
+            ap.solve(d, alg)
         torch.cuda.synchronize()
         t = time.perf_counter()
         r = ap.solve(d, alg)
