@@ -176,7 +176,7 @@ size_t rk_ws_bytes(int dtype, int64_t n, int aligned, int thr) {
   const int64_t N = aligned ? round_up(n, TILE_ALIGN) : n;
   const int64_t h = rk_half(N, aligned);
   const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
-  return header_bytes() + size_t(N) * N * (es + 4) + size_t(h + 8) * (h + 8) * (es + 4) + 1024 +
+  return header_bytes() + size_t(N) * N * (es + 4) + size_t(h + 8) * (h + 8) * (es + 4) + 1024 + 5 * 256 +
          rk_extra_bytes(N, aligned, thr);
 }
 
@@ -190,15 +190,20 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
   int rc = sc.acquire(ws, ws_bytes, rk_ws_bytes(dtype, n, aligned, thr), s);
   if (rc) return rc;
   Header* hdr_dev = static_cast<Header*>(sc.base);
-  char* p = static_cast<char*>(sc.base) + header_bytes();
+  // every region starts 256-byte aligned (odd N with the floor split would leave the int64
+  // store 4 bytes off)
+  auto align256 = [](char* q) {
+    return reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(q) + 255) & ~uintptr_t(255));
+  };
+  char* p = align256(static_cast<char*>(sc.base) + header_bytes());
   int32_t* P = reinterpret_cast<int32_t*>(p);
-  p += size_t(N) * N * 4;
+  p = align256(p + size_t(N) * N * 4);
   int32_t* sP = reinterpret_cast<int32_t*>(p);
-  p += size_t(h + 8) * (h + 8) * 4;
+  p = align256(p + size_t(h + 8) * (h + 8) * 4);
   char* D = p;
-  p += size_t(N) * N * (dtype == APSP_DTYPE_I64 ? 8 : 4);
+  p = align256(p + size_t(N) * N * (dtype == APSP_DTYPE_I64 ? 8 : 4));
   char* sV = p;
-  p += size_t(h + 8) * (h + 8) * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 512;
+  p = align256(p + size_t(h + 8) * (h + 8) * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 512);
   char* rkprep = aligned ? p : nullptr;
   char* rkprep2 = aligned ? rkprep + ((prep_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
   char* sV2 = aligned ? rkprep2 + ((prep_bytes(h, h, h) + 511) / 256) * 256 : nullptr;

@@ -601,3 +601,15 @@ def test_streamed_last_round_readback(cuda):
             assert "u8" in r.info["tiers_tried"]
         assert np.array_equal(r.distances, dev.distances.cpu().numpy())
         assert np.array_equal(r.index, dev.index.cpu().numpy())
+
+
+@pytest.mark.parametrize("n", [643, 301])
+def test_rkleene_floor_int64_tier_odd_n(cuda, n):
+    """Floor-split R-Kleene on the exact int64 tier with odd n: the int64 store must start
+    8-byte aligned in the workspace (regression: a 4-byte offset faulted with misaligned
+    address). Found by tools/stress.py."""
+    raw = random_graph_raw(n, 0.002, 10 ** 6, n)
+    want_d, _ = orc.fw_classic(raw)
+    r = ap.rkleene(ap.CostMatrix(raw), tier="i64")
+    assert np.array_equal(r.distances.raw, want_d)
+    assert r.info["tier"] == "i64"

@@ -1,0 +1,86 @@
+#!/usr/bin/env python3
+"""Randomised cross-checks of the product paths (run on a GPU box; not part of the test suite):
+  * small n: every solver entry against the CPU oracle (distances bit-exact, pred certificate);
+  * large n (> 2048, streamed readback, narrowed transfers): host-buffer API == device API.
+usage: tools/stress.py [seconds]"""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+import paper_2310_03983_b200 as ap  # noqa: E402
+from oracle import oracle as orc  # noqa: E402
+from paper_2310_03983_b200.core import INF32, INF_RAW  # noqa: E402
+
+
+def rand_raw(rng, n):
+    dens = float(rng.choice([0.002, 0.01, 0.05, 0.3, 1.0]))
+    wmax = int(rng.choice([1, 5, 100, 254, 300, 5000, 10 ** 6]))
+    raw = rng.integers(1, wmax + 1, size=(n, n)).astype(np.int64)
+    if rng.random() < 0.2:
+        raw[rng.random((n, n)) < 0.1] = 0
+    raw[rng.random((n, n)) >= dens] = INF_RAW
+    np.fill_diagonal(raw, 0)
+    return raw, dens, wmax
+
+
+def main():
+    budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "-v" else int(time.time())
+    print("seed", seed, flush=True)
+    rng = np.random.default_rng(seed)
+    t0 = time.time()
+    cases = fails = 0
+    while time.time() - t0 < budget:
+        small = rng.random() < 0.7
+        n = int(rng.integers(1, 700)) if small else int(rng.choice([2176, 2304, 2560, 3072]))
+        raw, dens, wmax = rand_raw(rng, n)
+        h = ap.CostMatrix(raw.copy(), _validated=True)
+        tag = f"n={n} dens={dens} wmax={wmax} zeros={int((raw == 0).sum()) - n}"
+        if "-v" in sys.argv:
+            print("case", tag, flush=True)
+        try:
+            if small:
+                want_d, want_p = orc.fw_classic(raw)
+                s = ap.fw_classic(h)
+                assert np.array_equal(s.distances.raw, want_d), "fw dist"
+                ok, why = ap.check_pred_tree(raw, s.distances.raw, s.pred.raw, INF_RAW)
+                assert ok, f"fw pred: {why}"
+                c = ap.fw_classic(h, method="classic")
+                assert np.array_equal(c.pred.raw, want_p), "classic pred"
+                r = ap.rkleene(h)
+                assert np.array_equal(r.distances.raw, want_d), "rk dist"
+                rp = ap.rkleene(h, track="pred", split="aligned", base_threshold=128)
+                ok, why = ap.check_pred_tree(raw, rp.distances.raw, rp.pred.raw, INF_RAW)
+                assert ok and np.array_equal(rp.distances.raw, want_d), f"rk pred: {why}"
+            else:
+                h32 = np.where(raw == INF_RAW, INF32, np.minimum(raw, 2 ** 20)).astype(np.int32)
+                dev = ap.solve(torch.from_numpy(h32.copy()).cuda())
+                host = ap.solve(h32)
+                assert np.array_equal(host.distances, dev.distances.cpu().numpy()), "host32 dist"
+                assert np.array_equal(host.index, dev.index.cpu().numpy()), "host32 pred"
+                r64 = ap.fw_classic(ap.CostMatrix(np.where(raw == INF_RAW, INF_RAW, np.minimum(raw, 2 ** 20))))
+                d64 = np.where(host.distances == INF32, INF_RAW, host.distances.astype(np.int64))
+                assert np.array_equal(r64.distances.raw, d64), "int64 api dist"
+        except ap.ApspError as e:   # range errors are legitimate for some draws
+            if "range" not in str(e).lower():
+                fails += 1
+                print(f"FAIL {tag}: {type(e).__name__}: {e}", flush=True)
+        except AssertionError as e:
+            fails += 1
+            print(f"FAIL {tag}: {e}", flush=True)
+        cases += 1
+    print(f"stress: {cases} cases, {fails} failures in {time.time() - t0:.0f}s", flush=True)
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
