@@ -61,6 +61,28 @@ def main():
                 rp = ap.rkleene(h, track="pred", split="aligned", base_threshold=128)
                 ok, why = ap.check_pred_tree(raw, rp.distances.raw, rp.pred.raw, INF_RAW)
                 assert ok and np.array_equal(rp.distances.raw, want_d), f"rk pred: {why}"
+                bt = int(rng.choice([1, 8, 64]))
+                od, ov = orc.rkleene(raw, base_threshold=bt)
+                rv = ap.rkleene(h, base_threshold=bt)
+                assert np.array_equal(rv.via.raw, ov) and np.array_equal(rv.distances.raw, od), "rk via"
+                if n <= 300:
+                    sd, sv, si = orc.fw_squaring(raw)
+                    sq = ap.fw_squaring(h)
+                    assert np.array_equal(sq.distances.raw, sd) and np.array_equal(sq.via.raw, sv), "squaring"
+                    assert sq.iterations == si, "squaring iterations"
+                # rectangular products on sub-blocks, with offsets, then an accumulate into the result
+                n1, n2, n3 = (int(rng.integers(1, n + 1)) for _ in range(3))
+                x, y = raw[:n1, :n2], raw[n - n2:, n - n3:]
+                offs = tuple(int(o) for o in rng.integers(0, 1000, size=3))
+                pd_, pv_ = orc.product(x, y, offs)
+                pr = ap.minplus_product(ap.CostMatrix(x.copy()), ap.CostMatrix(y.copy()), offsets=offs)
+                assert np.array_equal(pr.distances.raw, pd_) and np.array_equal(pr.via.raw, pv_), "product"
+                z = raw[n - n1:, :n3]
+                io = int(rng.integers(0, 1000))
+                ad, av = orc.accumulate(z, x, y, pv_, io)
+                ac = ap.minplus_accumulate(ap.CostMatrix(z.copy()), ap.CostMatrix(x.copy()), ap.CostMatrix(y.copy()),
+                                           pr.via, inner_offset=io)
+                assert np.array_equal(ac.distances.raw, ad) and np.array_equal(ac.via.raw, av), "accumulate"
             else:
                 h32 = np.where(raw == INF_RAW, INF32, np.minimum(raw, 2 ** 20)).astype(np.int32)
                 dev = ap.solve(torch.from_numpy(h32.copy()).cuda())
