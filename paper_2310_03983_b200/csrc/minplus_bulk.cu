@@ -167,13 +167,30 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
       }
     }
     if (wc == WIN - 1 || c + 1 == nch) {
+      const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
+#if APSP_ROW_DECODE
+      // one warp vote per row slot r (2 rows x 128 columns of the warp): once the tile has mostly
+      // converged, only the row slots that improved in this window pay for the decode
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const uint32_t any = (acc[r][0] | acc[r][1] | acc[r][2] | acc[r][3]) & TMASK2;
+        if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const uint32_t tg = acc[r][q] & TMASK2;
+            const uint32_t mask = prmt_sign_halves(tg + 0x7FFF7FFFu);
+            kst[r][q] = (kst[r][q] & ~mask) | ((tg + kb2) & mask);
+            acc[r][q] -= tg;
+          }
+        }
+      }
+#else
       uint32_t any = 0;
 #pragma unroll
       for (int r = 0; r < 8; r++)
 #pragma unroll
         for (int q = 0; q < 4; q++) any |= acc[r][q];
       if (__any_sync(0xffffffffu, any & TMASK2)) {
-        const uint32_t kb2 = uint32_t((c - wc) * SUB) * 0x00010001u;
 #pragma unroll
         for (int r = 0; r < 8; r++)
 #pragma unroll
@@ -184,6 +201,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
             acc[r][q] -= tg;
           }
       }
+#endif
     }
     if (++wc == WIN) wc = 0;
   }

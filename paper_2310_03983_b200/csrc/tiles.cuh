@@ -11,6 +11,9 @@ constexpr int BM = 128, BN = 128, NT = 256;
 #define APSP_U8_UNROLL 32
 #endif
 constexpr int kU8Unroll = APSP_U8_UNROLL;
+#ifndef APSP_ROW_DECODE
+#define APSP_ROW_DECODE 1
+#endif
 
 // Tile origin of this CTA.  Full grid: (blockIdx.y, blockIdx.x).  Cross-list mode
 // (only_lo < only_hi): blockIdx.x enumerates the tiles of rows band + cols band [lo, hi)
