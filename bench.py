@@ -352,7 +352,7 @@ def bench_single(args):
         roofline["traffic"] = c["traffic_bytes"]
         roofline["traffic_launch"] = {"updates": c["updates"], "duration_ms_isolated": c["duration_ms"],
                                       "achieved_isolated": c["achieved_T"], "frac_isolated": c["frac_of_dpx_ceiling"],
-                                      "source": "profiles/ncu_phase3b.json (ncu --set full, round-7 phase-3b launch)"}
+                                      "source": "profiles/ncu_phase3b.json (ncu --set full, round-7 phase-3b launch, tools/p3_capture.sh)"}
 
     e2e = api = None
     if not args.no_e2e:
