@@ -45,6 +45,8 @@ def _load():
         lib.oracle_accumulate.argtypes = [i64, i64, i64, p, i64, p, i64, p, i64, p, i64, p, p, i64, i64]
         lib.oracle_rkleene.argtypes = [i64, p, p, i64, i]
         lib.oracle_fw_squaring.argtypes = [i64, p, p, p, i]
+        lib.oracle_fw_f64.argtypes = [i64, p, i]
+        lib.oracle_fw_f64.restype = None
         _lib = lib
     return _lib
 
@@ -98,6 +100,14 @@ def fw_squaring(h, nthreads: int | None = None):
     return d, via, int(it.value)
 
 
+def fw_f64(h, nthreads: int | None = None) -> np.ndarray:
+    """float64 FW distances (+inf unreachable), bit-identical to networkx floyd_warshall_numpy
+    on the same float64 matrix (the C2 continuous-weight check)."""
+    d = np.ascontiguousarray(np.asarray(h, dtype=np.float64)).copy()
+    _load().oracle_fw_f64(d.shape[0], d.ctypes.data, nthreads or threads())
+    return d
+
+
 def product(x, y, offsets=(0, 0, 0)):
     """(dist, via) of reference minplus_product (minplus.py:166-203)."""
     x, y = _c64(x), _c64(y)
@@ -123,5 +133,6 @@ def accumulate(z, x, y, via=None, inner_offset: int = 0):
     return d, v
 
 
-__all__ = ["INF_RAW", "OracleRangeError", "accumulate", "build", "fw_classic", "fw_squaring", "fw_steps", "product",
+__all__ = ["INF_RAW", "OracleRangeError", "accumulate", "build", "fw_classic", "fw_f64", "fw_squaring", "fw_steps",
+           "product",
            "rkleene", "threads"]

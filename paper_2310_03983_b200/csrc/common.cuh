@@ -62,7 +62,7 @@ template <> __device__ __forceinline__ bool range_overflow<STORE_I64>(int64_t c)
 
 // Index output of a min-plus update (the reference's two artifacts):
 //   IDX_PRED  idx[i][j] <- pred_right[k*][j]   (FW rule, solvers.py:94)
-//   IDX_VIA   idx[i][j] <- inner_off + k*      (global via, minplus.py:405-410)
+//   IDX_VIA   idx[i][j] <- inner_off + k*      (global via, minplus.py:91-97)
 enum IdxMode : int { IDX_PRED = 0, IDX_VIA = 1 };
 
 struct Status {            // device-side status word, one per solve

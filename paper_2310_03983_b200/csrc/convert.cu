@@ -465,7 +465,7 @@ int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_
   return 0;
 }
 
-// ---- minplus_product self-witness via clear (minplus.py:411-423) -----------------------
+// ---- minplus_product self-witness via clear (minplus.py:99-111) -----------------------
 template <int S>
 __global__ void witness_clear_kernel(const typename StoreT<S>::T* X, int64_t ldx, const typename StoreT<S>::T* Y,
                                      int64_t ldy, const typename StoreT<S>::T* Dp, int64_t ldd, int32_t* via,

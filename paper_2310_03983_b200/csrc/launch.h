@@ -126,7 +126,7 @@ int launch_copy_block(int store, const void* src, int64_t lds, void* dst, int64_
                       int64_t rows, int64_t cols, cudaStream_t s);
 int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_t cols,
                       ScanResult* out_dev, cudaStream_t s);
-// Self-witness via clear of minplus_product (minplus.py:411-423).
+// Self-witness via clear of minplus_product (minplus.py:99-111).
 int launch_witness_clear(int store, const void* X, int64_t ldx, const void* Y, int64_t ldy,
                          const void* Dp, int64_t ldd, int32_t* via, int64_t ldv, int64_t n1,
                          int64_t n2, int64_t n3, int64_t row_off, int64_t inner_off,

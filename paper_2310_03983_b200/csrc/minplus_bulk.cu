@@ -610,7 +610,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
     asm volatile("cp.async.commit_group;\n" ::);
   }
 #pragma unroll
-  for (int c = 0; c < 32; c++) sm.kid[t][c] = 0xFFFF;
+  for (int c = 0; c < 4; c++) reinterpret_cast<uint4*>(&sm.kid[t][0])[c] = make_uint4(~0u, ~0u, ~0u, ~0u);
   float acc[4][8];
 #pragma unroll
   for (int r = 0; r < 4; r++)
@@ -716,21 +716,60 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
       }
     }
   }
-  bool changed = false;
-  float* Cw = static_cast<float*>(p.C);
+  // Epilogue: the thread's own 32 k ids (written by any lane of its warp) come back as 4
+  // 16-byte loads; all predecessor gathers of improved cells are issued back to back before
+  // any store, so their latencies overlap instead of serialising per cell.
+  __syncwarp();
+  uint32_t kw[16];
 #pragma unroll
-  for (int r = 0; r < 4; r++) {
-    const int64_t i = i0 + 4 * ty + r;
+  for (int c = 0; c < 4; c++) *reinterpret_cast<uint4*>(&kw[4 * c]) = reinterpret_cast<const uint4*>(&sm.kid[t][0])[c];
+  auto kid_of = [&](int cell) -> uint32_t { return (kw[cell >> 1] >> (16 * (cell & 1))) & 0xFFFFu; };
+  uint32_t anyk = 0;
 #pragma unroll
-    for (int q = 0; q < 8; q++) {
-      const uint32_t k = sm.kid[t][8 * r + q];
-      if (k == 0xFFFFu) continue;
-      changed = true;
-      const int64_t j = j0 + 8 * tx + q;
-      Cw[i * p.ldc + j] = acc[r][q];
-      if (p.idx)
-        p.idx[i * p.ldi + j] =
-            (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(k) * p.ldp + j) : int32_t(p.inner_off + k);
+  for (int c = 0; c < 16; c++) anyk |= ~kw[c];
+  const bool changed = anyk != 0u;
+  if (changed) {
+    float* Cw = static_cast<float*>(p.C);
+    int32_t pv[4][8];
+    const bool pred = p.idx && p.mode == IDX_PRED;
+#pragma unroll
+    for (int r = 0; r < 4; r++)
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const uint32_t k = kid_of(8 * r + q);
+        pv[r][q] = int32_t(p.inner_off + k);
+        if (pred && k != 0xFFFFu) pv[r][q] = __ldg(p.predB + int64_t(k) * p.ldp + j0 + 8 * tx + q);
+      }
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      const int64_t i = i0 + 4 * ty + r;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int64_t j = j0 + 8 * tx + 4 * h;
+        const uint32_t w0 = kw[4 * r + 2 * h], w1 = kw[4 * r + 2 * h + 1];
+        if ((w0 & w1) == 0xFFFFFFFFu) continue;             // none of the 4 cells improved
+        const bool all4 = ((w0 & 0xFFFFu) != 0xFFFFu) && ((w0 >> 16) != 0xFFFFu) &&
+                          ((w1 & 0xFFFFu) != 0xFFFFu) && ((w1 >> 16) != 0xFFFFu);
+        if (all4) {
+          *reinterpret_cast<float4*>(Cw + i * p.ldc + j) =
+              make_float4(acc[r][4 * h], acc[r][4 * h + 1], acc[r][4 * h + 2], acc[r][4 * h + 3]);
+          if (p.idx) {
+            int32_t* dst = p.idx + i * p.ldi + j;
+            if (((reinterpret_cast<uintptr_t>(dst)) & 15) == 0)
+              *reinterpret_cast<int4*>(dst) = make_int4(pv[r][4 * h], pv[r][4 * h + 1], pv[r][4 * h + 2], pv[r][4 * h + 3]);
+            else
+#pragma unroll
+              for (int q = 0; q < 4; q++) dst[q] = pv[r][4 * h + q];
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            if (kid_of(8 * r + 4 * h + q) == 0xFFFFu) continue;
+            Cw[i * p.ldc + j + q] = acc[r][4 * h + q];
+            if (p.idx) p.idx[i * p.ldi + j + q] = pv[r][4 * h + q];
+          }
+        }
+      }
     }
   }
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;

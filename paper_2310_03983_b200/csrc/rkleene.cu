@@ -425,6 +425,19 @@ int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
   const bool integral = dtype != APSP_DTYPE_F32 || !(sx.non_integral || sy.non_integral || sz.non_integral);
   const int64_t sum = std::max<int64_t>(sx.max_finite + sy.max_finite, sz.max_finite);
   int tier = tier_req;
+  if (tier >= 0) {
+    // A forced tier must hold every partial sum exactly: the product has no certificate pass,
+    // so a narrower store would silently wrap a cost (e.g. 300 -> 44 in u8).
+    const bool int_tier = tier == APSP_TIER_U8 || tier == APSP_TIER_U16 || tier == APSP_TIER_W32 ||
+                          tier == APSP_TIER_I32;
+    bool fits = tier == APSP_TIER_F32 ? dtype == APSP_DTYPE_F32
+              : tier == APSP_TIER_I64 ? dtype == APSP_DTYPE_I64
+              : tier == APSP_TIER_I32 ? dtype != APSP_DTYPE_F32 && sum <= tier_limit(tier)
+              : int_tier && integral && sum <= tier_limit(tier);
+    if (!fits)
+      return set_error(APSP_EINVAL, "forced tier %d cannot hold the operands exactly (max partial sum %lld)", tier,
+                       (long long)sum);
+  }
   if (tier < 0) {
     if (integral && sum <= U8_INF - 1) tier = APSP_TIER_U8;
     else if (integral && sum <= W32_INF - 1) tier = APSP_TIER_W32;
@@ -440,7 +453,7 @@ int minplus_impl(int dtype, int accumulate, int64_t n1, int64_t n2, int64_t n3, 
   if (accumulate) {
     rc = launch_to_store_rect(dtype, z, ldz, n1, n3, store, Zs, n3, s);
   } else {
-    // product: C starts at Infinity, via at None (minplus.py:398-400)
+    // product: C starts at Infinity, via at None (_product_band fills dist/via per row, minplus.py:84-88)
     rc = launch_to_store_rect(dtype, nullptr, 0, n1, n3, store, Zs, n3, s);
     if (!rc && via) rc = launch_fill_idx(via, ldv, n1, n3, -1, s);
   }

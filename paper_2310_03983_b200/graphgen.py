@@ -172,3 +172,15 @@ def dense_costs(params: GenParams, dtype=np.int64, chunk_rows: int = 512,
         idx = np.arange(r0, r1)
         block[idx - r0, idx] = 0
     return out
+
+
+def continuous_costs(params: GenParams) -> np.ndarray:
+    """BASELINE config 2's continuous variant: the edge mask of
+    ``generate(params)`` with float32 weights drawn U[1, 100) from ``default_rng(params.seed)``
+    in row-major edge order; zero diagonal, +inf for non-edges."""
+    h = dense_costs(params, np.float32)
+    fin = np.isfinite(h)
+    np.fill_diagonal(fin, False)
+    rng = np.random.default_rng(params.seed)
+    h[fin] = rng.uniform(1.0, 100.0, size=int(fin.sum())).astype(np.float32)
+    return h

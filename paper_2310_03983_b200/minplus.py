@@ -2,7 +2,7 @@
 
 ``minplus_product`` and ``minplus_accumulate`` keep the reference contract: smallest-k argmin
 on ties, strict improvement, via in global vertex numbers through the offsets, the
-self-witness clear of the product (minplus.py:411-423) and ``CostRangeError`` when a finite
+self-witness clear of the product (minplus.py:99-111) and ``CostRangeError`` when a finite
 result leaves the range.  The kernels are the same tile kernels that run R-Kleene.
 """
 

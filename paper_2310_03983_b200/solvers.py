@@ -212,10 +212,17 @@ def solve(h, algorithm: str = "fw_blocked", *, track: str = "pred", base_thresho
 
     numpy input: host-level call (copy in, solve, copy out) -> numpy outputs.
     CUDA torch tensor: device-level call on a copy, on ``stream`` (default: torch's current
-    stream) -> torch outputs; ``workspace`` may be a preallocated uint8 CUDA tensor.
+    stream) -> torch outputs, ready in ``stream`` order; ``stream`` first waits for the current
+    stream (which produced ``h``).  ``workspace`` may be a preallocated uint8 CUDA tensor.
     """
     if algorithm not in _ALGS:
         raise ParameterError(f"unknown algorithm {algorithm!r}; expected one of {sorted(_ALGS)}")
+    if track not in ("via", "pred"):
+        raise ParameterError(f"track must be 'via' or 'pred', got {track!r}")
+    if split not in ("floor", "aligned"):
+        raise ParameterError(f"split must be 'floor' or 'aligned', got {split!r}")
+    if base_threshold < 1:
+        raise ParameterError(f"base_threshold must be >= 1, got {base_threshold}")
     alg = _ALGS[algorithm]
     mode = nat.IDX_VIA if (algorithm == "fw_squaring" or (algorithm == "rkleene" and track == "via")) \
         else nat.IDX_PRED
@@ -243,13 +250,24 @@ def solve(h, algorithm: str = "fw_blocked", *, track: str = "pred", base_thresho
         raise DimensionError(f"expected a non-empty square matrix, got shape {tuple(h.shape)}")
     dt = _dtype_code(h.dtype)
     n = h.shape[0]
-    dist = h.contiguous().clone()
-    idx = torch.empty((n, n), dtype=torch.int32, device=h.device)
-    s = stream if stream is not None else torch.cuda.current_stream(h.device)
+    cur = torch.cuda.current_stream(h.device)
+    s = stream if stream is not None else cur
     sp = ctypes.c_void_p(s.cuda_stream)
     ws_need = lib.apsp_workspace_bytes(alg, dt, n, block)
-    if workspace is None and ws_need:
-        workspace = torch.empty(ws_need, dtype=torch.uint8, device=h.device)
+    # The library runs on `s`; whatever produced `h` (and a caller's `workspace`) was queued on
+    # the current stream, so `s` waits for it, and the copies/allocations below are made on `s`.
+    if s != cur:
+        s.wait_stream(cur)
+    with torch.cuda.stream(s):
+        dist = h.contiguous().clone()
+        idx = torch.empty((n, n), dtype=torch.int32, device=h.device)
+        if workspace is None and ws_need:
+            workspace = torch.empty(ws_need, dtype=torch.uint8, device=h.device)
+    if s != cur:
+        # the outputs are handed back to a caller on `cur` (who syncs with `s` before reading,
+        # as with any side-stream result): their blocks must not be recycled while `cur` uses them
+        for t in (dist, idx):
+            t.record_stream(cur)
     wp = workspace.data_ptr() if workspace is not None else None
     wb = workspace.numel() if workspace is not None else 0
     with torch.cuda.device(h.device):

@@ -71,7 +71,7 @@ def test_idempotence_and_triangle_inequality(cuda, raw):
     assert ap.matrices_equal(again.distances, d)
     dd = d.raw
     fin = dd != INF_RAW
-    # saturated sums exceed INF_RAW but never undercut a finite cell (test_solvers.py:338-345)
+    # saturated sums exceed INF_RAW but never undercut a finite cell (test_solvers.py:175-182)
     for k in range(dd.shape[0]):
         assert (dd <= dd[:, k, None] + dd[None, k, :]).all()
     assert (dd[fin] >= 0).all()

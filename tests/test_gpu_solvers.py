@@ -325,6 +325,12 @@ def test_minplus_tiers_and_errors(cuda):
         ap.minplus_product(m, m)
     with pytest.raises(ap.NegativeWeightError):
         ap.minplus_product(ap.CostMatrix.from_rows([[0, -1], [1, 0]]), ap.minplus_identity(2))
+    # a forced tier that cannot hold the partial sums is refused, never silently narrowed
+    w = ap.CostMatrix.from_rows([[0, 300], [ap.INF, 0]])
+    with pytest.raises(ap.ParameterError):
+        ap.minplus_product(w, w, tier="u8")
+    r8 = ap.minplus_product(ap.CostMatrix.from_rows([[0, 100], [ap.INF, 0]]), ap.minplus_identity(2), tier="u8")
+    assert r8.distances.raw.tolist() == [[0, 100], [INF_RAW, 0]]
 
 
 # ---- larger sizes: size-independent properties ---------------------------------------------

@@ -114,3 +114,21 @@ def test_dense_costs_dtypes():
     fin = a != INF_RAW
     assert np.array_equal(b[fin], a[fin]) and (b[~fin] == INF32).all()
     assert np.array_equal(c[fin], a[fin].astype(np.float32)) and np.isinf(c[~fin]).all()
+
+
+@pytest.mark.parametrize("n,density,seed", [(1, 1.0, 0), (57, 0.3, 1), (300, 0.05, 2), (256, 0.6, 3)])
+def test_f64_fw_matches_networkx(n, density, seed):
+    """oracle.fw_f64 (the C2 continuous-weight reference) is bit-identical to networkx
+    floyd_warshall_numpy on the same float64 weights (SURVEY.md 8(d) C2 variant)."""
+    nx = pytest.importorskip("networkx")
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(1.0, 100.0, size=(n, n)).astype(np.float32).astype(np.float64)
+    present = (rng.random((n, n)) < density) & ~np.eye(n, dtype=bool)
+    g = nx.DiGraph()
+    g.add_nodes_from(range(n))
+    g.add_weighted_edges_from((int(i), int(j), float(w[i, j])) for i, j in zip(*np.nonzero(present)))
+    want = nx.floyd_warshall_numpy(g, nodelist=range(n))
+    h = np.where(present, w, np.inf)
+    np.fill_diagonal(h, 0.0)
+    got = orc.fw_f64(h)
+    assert np.array_equal(got, want)
