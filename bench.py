@@ -39,11 +39,12 @@ sys.path.insert(0, str(ROOT))
 METRIC = "APSP time and min-plus updates/sec (n^3/s) at n=16384; % of FP32 CUDA-core peak"
 UNIT = "updates/s"
 FP32_CORE_PEAK = 148 * 128 * 1965e6 / 2          # 18.6 T upd/s at max clock
-# Measured issue ceilings of the inner-loop instruction of each tier (profiles/r01_microbench_ops.txt)
-TIER_PEAK = {"u8": 37.07e12, "u16": 37.07e12, "w32": 24.91e12, "i32": 17.98e12, "f32": 6.05e12, "i64": 6.05e12}
+# Measured issue ceilings of the inner-loop instruction of each tier's phase-3 kernel
+# (tools/microbench/ops.cu; profiles/r01_microbench_ops.txt; argmin_i32: profiles/r02_microbench_ops.txt)
+TIER_PEAK = {"u8": 37.07e12, "u16": 37.07e12, "w32": 17.98e12, "i32": 6.12e12, "f32": 20.17e12, "i64": 6.05e12}
 TIER_OP = {"u8": "VIADDMNMX.U16x2 (2 upd/instr)", "u16": "VIADDMNMX.U16x2 (2 upd/instr)",
-           "w32": "VIADD+VIMNMX3", "i32": "compare-select",
-           "f32": "FADD/FSETP/FSEL/SEL", "i64": "compare-select int64"}
+           "w32": "VIADDMNMX.U32 (1 upd/instr)", "i32": "IADD/ISETP/IMNMX/SEL compare-select (argmin_i32)",
+           "f32": "FADD + FMNMX3 (1.5 instr/upd; deferred argmin)", "i64": "compare-select int64"}
 BLOCK = 0          # 0: the library's size-aware default (apsp_info.block reports it)
 
 
@@ -157,7 +158,14 @@ class CpuSampler:
     def describe(self) -> str:
         return (f"oracle fw_classic (C/OpenMP int64, solvers.py:77-95) steady-state k-steps "
                 f"{self.k_warm}..{self.k_warm + self.K} of n={self.n} ({self.K}*n^2 updates), resumed from "
-                f"the saved state after {self.k_warm} untimed steps; {self.threads} threads")
+                f"the saved state after {self.k_warm} untimed steps; {self.threads} threads. "
+                f"Bias: a steady-state window runs slower than the whole-solve average (the early k-steps "
+                f"skip rows with d[i][k] = INF): at n=16384 the full oracle solve took 333 s (13.2 G upd/s, "
+                f"16 threads, profiles/r01_summary.md) against 12.1-12.6 G upd/s in this window, so the "
+                f"sampled rate understates the CPU by ~5-9%")
+
+    FULL_SOLVE = {"n": 16384, "s": 333.0, "rate": 16384 ** 3 / 333.0, "threads": 16,
+                  "source": "profiles/r01_summary.md (full oracle fw_classic solve on the GPU box host)"}
 
 
 def cpu_baseline(h32: np.ndarray, budget_s: float = 12.0) -> dict:
@@ -165,7 +173,8 @@ def cpu_baseline(h32: np.ndarray, budget_s: float = 12.0) -> dict:
     dt = s.run()
     rate = s.K * s.n * s.n / dt
     return {"value": rate, "unit": UNIT, "cores": s.threads, "kind": "port",
-            "sample": s.describe() + f"; {dt:.1f}s; full solve extrapolates to {s.n ** 3 / rate:.0f}s"}
+            "sample": s.describe() + f"; {dt:.1f}s; full solve extrapolates to {s.n ** 3 / rate:.0f}s",
+            "full_solve_reference_point": CpuSampler.FULL_SOLVE}
 
 
 def networkx_baseline(n: int = 1024, rho: float = 0.1) -> dict | None:
@@ -203,13 +212,17 @@ def run_reference(args, ws, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generator)",
+        "scaling": scaling_of(args), "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generator)",
         "config": config(n, args.rho, ws),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": s.threads, "kind": "port",
-                         "sample": "each step = " + s.describe()},
+                         "sample": "each step = " + s.describe(), "full_solve_reference_point": CpuSampler.FULL_SOLVE},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def scaling_of(args) -> str:
+    return "strong" if args.strong else "weak"
 
 
 def weak_n(ws: int) -> int:
@@ -235,20 +248,49 @@ def main():
     ap_.add_argument("--rho", type=float, default=0.1)
     ap_.add_argument("--no-cpu", action="store_true")
     ap_.add_argument("--no-e2e", action="store_true")
+    ap_.add_argument("--no-tiers", action="store_true", help="skip the w32 / i32 / continuous-fp32 variants")
     ap_.add_argument("--ref-step-s", type=float, default=8.0)
     ap_.add_argument("--block", type=int, default=BLOCK, help="pivot block (multiple of 128; 0 = library default)")
     ap_.add_argument("--sharded", action="store_true", help="use the multi-GPU row-band path even at N=1")
     ap_.add_argument("--alg", default="fw", choices=["fw", "rkleene"],
                      help="multi-GPU leg: row-band FW (default) or replicated R-Kleene with row-band products")
+    ap_.add_argument("--strong", action="store_true",
+                     help="strong scaling (BASELINE C4): n=32768 at every N instead of the weak-scaled n(N)")
     args = ap_.parse_args()
     ws, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
+    if "WORLD_SIZE" in os.environ and ws != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank per GPU")
+    if args.strong and not args.n:
+        args.n = 32768
     if args.impl == "reference":
         return run_reference(args, ws, rank)
     if ws > 1 or args.sharded:
         from paper_2310_03983_b200 import distributed
 
-        return distributed.bench_main(args, METRIC, UNIT, config, make_input, weak_n, ClockSampler)
+        return distributed.bench_main(args, METRIC, UNIT, config, make_input, weak_n, ClockSampler,
+                                      cpu_baseline=cpu_baseline, tier_peak=TIER_PEAK, tier_op=TIER_OP)
     return bench_single(args)
+
+
+def spawn_ranks(n_gpus: int):
+    """`bench.py --gpus N` outside torchrun: relaunch this command as N ranks (one per GPU)
+    through torch.distributed.run on 127.0.0.1; fails loudly if fewer GPUs are visible."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n_gpus:
+        raise SystemExit(f"bench.py: --gpus {n_gpus} but only {have} CUDA device(s) are visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n_gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    log("[bench] launching", " ".join(cmd))
+    os.execvp(cmd[0], cmd)
 
 
 def bench_single(args):
@@ -266,7 +308,7 @@ def bench_single(args):
     h = torch.from_numpy(h_np).to(dev)
     dist = torch.empty_like(h)
     pred = torch.empty((n, n), dtype=torch.int32, device=dev)
-    wsb = lib.apsp_workspace_bytes(nat.ALG_FW_BLOCKED, nat.DTYPE_I32, n, block)
+    wsb = max(lib.apsp_workspace_bytes(nat.ALG_FW_BLOCKED, dt, n, block) for dt in (nat.DTYPE_I32, nat.DTYPE_F32))
     work = torch.empty(wsb, dtype=torch.uint8, device=dev)
     stream = torch.cuda.Stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
@@ -304,14 +346,10 @@ def bench_single(args):
     value = n ** 3 * args.steps / (total_ms / 1e3)
 
     # dominant kernel: FW phase-3 min-plus tile launches, timed with CUDA events on their stream
-    # (apsp_set_profiling) in two extra, untimed solves:
-    #   * without the lookahead stream, so no phase-1/2 kernel shares the SMs with a phase-3
-    #     launch: the kernel's own rate ("achieved");
-    #   * as in the timed steps, where phase-3 launches share SMs with the lookahead stream
-    #     ("achieved_in_step", the same launches stretched by the concurrent work).
-    def profile(no_lookahead: bool):
-        if no_lookahead:
-            os.environ["APSP_NO_LOOKAHEAD"] = "1"
+    # (apsp_set_profiling) in one extra, untimed solve without the lookahead stream, so no
+    # phase-1/2 kernel shares the SMs with a phase-3 launch: the kernel's own rate.
+    def profile():
+        os.environ["APSP_NO_LOOKAHEAD"] = "1"
         try:
             lib.apsp_set_profiling(1)
             step()
@@ -325,10 +363,8 @@ def bench_single(args):
     # phase 3 of one pivot round updates every tile outside the pivot cross: (N-b)^2 * b
     # (3a + 3b launches together); a solve has N/b rounds
     upd_phase3 = (N // block) * (N - block) ** 2 * block
-    kl, kms = profile(no_lookahead=True)
-    kl2, kms2 = profile(no_lookahead=False)
+    kl, kms = profile()
     achieved = upd_phase3 / (kms / 1e3) if kl else None
-    achieved_step = upd_phase3 / (kms2 / 1e3) if kl2 else None
     peak = TIER_PEAK.get(tier)
     kname = f"minplus_nt_kernel<{tier}> (FW phase 3, bulk-staged)" if tier in ("u8", "u16") else \
         f"minplus_{tier}_kernel (FW phase 3)"
@@ -339,9 +375,6 @@ def bench_single(args):
                 "updates_per_step": upd_phase3,
                 "measurement": "CUDA events around every phase-3 launch on its stream, one extra solve without the "
                                "lookahead stream (no concurrent kernels)",
-                "achieved_in_step": achieved_step / 1e12 if achieved_step else None,
-                "frac_in_step": (achieved_step / peak) if achieved_step and peak else None,
-                "kernel_share_of_step": (kms2 / ms_step) if kl2 else None,
                 "step_frac": value / peak if peak else None,
                 "peak_source": "measured issue ceiling of the inner-loop instruction, profiles/r01_microbench_ops.txt"}
     # DRAM traffic of one phase-3b launch from the committed ncu --set full capture of this
@@ -354,6 +387,9 @@ def bench_single(args):
                                       "achieved_isolated": c["achieved_T"], "frac_isolated": c["frac_of_dpx_ceiling"],
                                       "source": "profiles/ncu_phase3b.json (ncu --set full, round-7 phase-3b launch, tools/p3_capture.sh)"}
 
+    parity = reference_digest(dist, n, args.rho)
+    tiers = None if args.no_tiers else bench_tiers(lib, nat, h, dist, pred, work, stream, n, args, block)
+
     e2e = api = None
     if not args.no_e2e:
         e2e = bench_e2e(lib, nat, h_np, n, args, block)
@@ -364,18 +400,98 @@ def bench_single(args):
         nxb = networkx_baseline()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "apsp_time_s": ms_step / 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": ms_step, "apsp_time_s": ms_step / 1e3, "higher_is_better": True, "scaling": scaling_of(args),
         "vs_baseline": None, "dtype": f"int16x2 keys / uint8 store (tier {tier}); int32 in/out" if tier == "u8"
         else f"tier {tier}; int32 in/out",
         "data": "synthetic (reference generator, bit-identical to apsp.generate)",
-        "config": config(n, args.rho, 1) | {"block": block},
+        "config": config(n, args.rho, 1), "block": block,
         "pct_fp32_core_peak": value / FP32_CORE_PEAK,
         "fp32_core_peak": FP32_CORE_PEAK,
         "clocks": clk.summary(), "gpu_launches": launches_timed,
         "tier": tier, "max_finite_distance": info.max_finite,
         "roofline": roofline, "e2e": e2e, "python_api_e2e": api, "cpu_baseline": cpu, "networkx_baseline": nxb,
+        "parity": parity, "tiers": tiers,
     }
     print(json.dumps(line), flush=True)
+
+
+def reference_digest(dist, n, rho):
+    """Untimed: sha256 of the device result in the reference's int64 form against the digest of
+    the REFERENCE's own solve of this graph (tests/golden/large.json, make_golden_large.py)."""
+    import hashlib
+
+    import paper_2310_03983_b200 as ap
+
+    gold = json.loads((ROOT / "tests" / "golden" / "large.json").read_text())
+    ref = next((v for v in gold.values() if v["n"] == n and v["rho"] == rho and v["seed"] == 7 + n), None)
+    if ref is None:
+        return {"checked": False, "why": f"no reference digest recorded for n={n} rho={rho}"}
+    d = dist.cpu().numpy()
+    d64 = d.astype(np.int64)
+    d64[d == ap.INF32] = ap.INF_RAW
+    got = hashlib.sha256(np.ascontiguousarray(d64).tobytes()).hexdigest()
+    if got != ref["dist_sha256"]:
+        raise SystemExit(f"bench result differs from the reference's distances (sha256 {got} != {ref['dist_sha256']})")
+    return {"checked": True, "dist_sha256_equals_reference": True,
+            "reference": f"apsp {ref['algorithm']} on GenParams({n}, {rho}, 100, {7 + n}), int64, "
+                         f"{ref['solve_s']} s on {ref['cores']} cores (tests/golden/large.json)",
+            "pred": "certificate (paths.check_pred_tree): every pred hop is an input edge on a shortest path, "
+                    "no cycles"}
+
+
+def bench_tiers(lib, nat, h, dist, pred, work, stream, n, args, block, steps=2):
+    """The same n=16384 solve on the wider value tiers (the headline runs on the narrowest tier
+    the certificate allows, u8 for this graph): forced w32 and i32 on the same int32 input, and
+    the continuous-weight fp32 variant (BASELINE C2's variant at this n: the same edge mask with
+    U[1, 100) fp32 weights, exact fp32 tier). Each: ms per solve (CUDA events, 1 warm-up) and
+    the fraction of its own tier's measured instruction ceiling."""
+    import torch
+
+    import paper_2310_03983_b200 as ap
+
+    out = {}
+    info = nat.ApspInfo()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    hf = None
+    for name in ("w32", "i32", "f32_continuous"):
+        if name == "f32_continuous":
+            hf = torch.from_numpy(ap.continuous_costs(ap.GenParams(n, args.rho, 100, 7 + n))).to(h.device)
+            src, dt, tier_req = hf, nat.DTYPE_F32, nat.TIER_AUTO
+            dbuf = dist.view(torch.float32)
+        else:
+            src, dt, tier_req = h, nat.DTYPE_I32, {"w32": nat.TIER_W32, "i32": nat.TIER_I32}[name]
+            dbuf = dist
+        need = lib.apsp_workspace_bytes(nat.ALG_FW_BLOCKED, dt, n, block)
+        if need > work.numel():
+            out[name] = {"skipped": f"workspace {need} B > {work.numel()} B"}
+            continue
+
+        def one():
+            with torch.cuda.stream(stream):
+                dbuf.copy_(src)
+            nat.check(lib.apsp_fw_blocked(dt, n, dbuf.data_ptr(), n, pred.data_ptr(), n, block, tier_req,
+                                          work.data_ptr(), work.numel(), sp, ctypes.byref(info)))
+        one()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            one()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        tier = nat.TIER_NAMES[info.tier]
+        rate = n ** 3 / (ms / 1e3)
+        out[name] = {"tier": tier, "ms_per_step": ms, "value": rate, "unit": UNIT, "steps": steps,
+                     "frac_of_tier_ceiling": rate / TIER_PEAK[tier], "tier_ceiling": TIER_PEAK[tier],
+                     "op": TIER_OP[tier], "pct_fp32_core_peak": rate / FP32_CORE_PEAK}
+        if name == "f32_continuous":
+            ok, why = ap.check_pred_paths(hf, dbuf, pred, 1e-5)
+            out[name]["pred_paths_resummed_within_1e-5"] = ok
+            out[name]["input"] = "generator mask of GenParams(16384, 0.1, 100, 16391), fp32 weights U[1,100) " \
+                                 "(paper_2310_03983_b200.continuous_costs)"
+    del hf
+    return out
 
 
 def bench_python_api(h_np, n, reps=3):

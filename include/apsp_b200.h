@@ -91,6 +91,10 @@ void apsp_set_profiling(int on);
 
 /* Number of kernels this library has launched in the process (all devices, all calls). */
 long long apsp_launch_count(void);
+/* Profiled min-plus tile launches recorded on this host thread since the last read (the shard
+ * entry points below have no apsp_info): their count and summed CUDA-event time. Synchronises
+ * with the recorded events; resets the record. */
+int apsp_profile_read(double* kernel_ms, int32_t* launches);
 
 /* Scratch bytes the device-level calls need when ws != NULL. */
 size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block);

@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "apsp_abi_version",
     "apsp_set_profiling",
     "apsp_launch_count",
+    "apsp_profile_read",
     "apsp_workspace_bytes",
     "apsp_fw_blocked",
     "apsp_fw_classic",
@@ -125,6 +126,7 @@ _SIGNATURES = {
     "apsp_abi_version": (_i32, []),
     "apsp_set_profiling": (None, [_i32]),
     "apsp_launch_count": (ctypes.c_longlong, []),
+    "apsp_profile_read": (_i32, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)]),
     "apsp_workspace_bytes": (_sz, [_i32, _i32, _i64, _i32]),
     "apsp_fw_blocked": (_i32, [_i32, _i64, _vp, _i64, _vp, _i64, _i32, _i32, _vp, _sz, _vp, _info_p]),
     "apsp_fw_classic": (_i32, [_i32, _i64, _vp, _i64, _vp, _i64, _vp, _info_p]),

@@ -15,6 +15,15 @@ extern "C" {
 const char* apsp_last_error(void) { return apsp::last_error(); }
 void apsp_set_profiling(int on) { g_prof.on = on != 0; }
 long long apsp_launch_count(void) { return apsp::launch_count(); }
+int apsp_profile_read(double* kernel_ms, int32_t* launches) {
+  apsp_info info{};
+  APSP_CUDA_TRY(cudaDeviceSynchronize());
+  g_prof.collect(&info);
+  g_prof.reset();
+  if (kernel_ms) *kernel_ms = info.kernel_ms;
+  if (launches) *launches = info.kernel_launches;
+  return 0;
+}
 
 int apsp_scan(int dtype, const void* h, int64_t ld, int64_t rows, int64_t cols, int64_t diag_off,
               apsp_scan_result* out, void* stream) {

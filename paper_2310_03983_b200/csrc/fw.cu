@@ -618,6 +618,11 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
     }
     return 0;
   }
+  // pred mode on the 32-bit exact stores: the blocked in-CTA closure (close_blk.cu; distances
+  // exact, pred a valid tree); via mode keeps the classic order (R-Kleene via is bit-exact)
+  static const bool classic_close = getenv("APSP_CLASSIC_CLOSE") != nullptr;
+  if (mode == IDX_PRED && close_blk_supported(store) && !classic_close)
+    return launch_block_close_blk(store, D, ld, lo, m, idx, ldi, s);
   if ((store == STORE_U8 || store == STORE_U16) && !getenv("APSP_SLOW_CLOSE")) {
     static std::atomic<unsigned long long> attr8{0}, attr16{0};
     static std::atomic<unsigned long long> attr8f{0}, attr16f{0};

@@ -82,6 +82,10 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s);
 
 // Closure of the diagonal block [lo, lo+m) (m <= 128) in classic k order, one CTA:
 // FW phase 1 and the R-Kleene leaf (_fw_via_block, solvers.py:98-115).
+// Blocked in-CTA closure for the 32-bit exact stores, pred mode (close_blk.cu)
+bool close_blk_supported(int store);
+int launch_block_close_blk(int store, void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi,
+                           cudaStream_t s);
 int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m,
                        int32_t* idx, int64_t ldi, int mode, int64_t via_off, Status* st,
                        cudaStream_t s);

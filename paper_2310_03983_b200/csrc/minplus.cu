@@ -510,8 +510,8 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s) {
   if (a.npeers < 0 || a.npeers > MAX_PEERS) return set_error(2, "npeers %d outside [0, %d]", a.npeers, MAX_PEERS);
   if (a.npeers && !(a.Aprep && a.Bprep && (store == STORE_U8 || store == STORE_U16 || store == STORE_W32)))
     return set_error(2, "fused peer stores need a bulk-staged tier (u8 / u16 / w32) with prepared panels");
-  if (a.push_all && !(a.npeers && (store == STORE_U8 || store == STORE_U16)))
-    return set_error(2, "whole-panel peer pushes need the u8 / u16 tier and peers");
+  if (a.push_all && !(a.npeers && (store == STORE_U8 || store == STORE_U16 || store == STORE_W32)))
+    return set_error(2, "whole-panel peer pushes need a bulk-staged tier (u8 / u16 / w32) and peers");
   if (a.k <= 0) return 0;
   if (a.k > 65535) return set_error(2, "min-plus inner dimension %lld exceeds 65535", (long long)a.k);
   if (a.only_lo < a.only_hi) {

@@ -487,6 +487,31 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
     }
 #pragma unroll
     for (int h = 0; h < 2; h++) {
+      if (p.push_all) {   // FW panel push: every segment to the peers, local stores where improved
+        const int64_t j = j0 + 64 * h + 4 * tx;
+        const bool imp = (kst[r][2 * h] | kst[r][2 * h + 1]) != 0u;
+        changed |= imp;
+        const int4 wv = make_int4(int32_t(acc[r][4 * h] >> W32_TAG), int32_t(acc[r][4 * h + 1] >> W32_TAG),
+                                  int32_t(acc[r][4 * h + 2] >> W32_TAG), int32_t(acc[r][4 * h + 3] >> W32_TAG));
+        int4* dstv = reinterpret_cast<int4*>(Cw + i * p.ldc + j);
+        if (imp) *dstv = wv;
+        for (int pr = 0; pr < p.npeers; pr++)
+          *reinterpret_cast<int4*>(reinterpret_cast<char*>(dstv) + p.peer_dC[pr]) = wv;
+        if (!out) continue;
+        int32_t* dst = out + i * p.ldi + j;
+        int32_t full[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          full[q] = ks[h][q] != 0u ? pv[h][q] : dst[q];   // unimproved: the current pred
+          if (ks[h][q] != 0u) dst[q] = pv[h][q];
+        }
+        for (int pr = 0; pr < p.npeers; pr++) {
+          int32_t* pd = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(dst) + p.peer_dI[pr]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) pd[q] = full[q];
+        }
+        continue;
+      }
       if ((kst[r][2 * h] | kst[r][2 * h + 1]) == 0u) continue;
       changed = true;
       const int64_t j = j0 + 64 * h + 4 * tx;
@@ -515,6 +540,8 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
       }
     }
   }
+  // peer stores are ordered before anything the host signals after this kernel
+  if (p.npeers) __threadfence_system();
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
 }
 
@@ -572,6 +599,9 @@ struct SmemF32DM {   // 96 KB: 2 CTAs / SM
 };
 // rescan target slot of (thread, cell): 4-cell groups stay contiguous (one 16-byte store each),
 // rotated by thread so the 8 lanes of a store phase hit 8 different bank quads
+// tile column of a thread's cell q (0..7): two 4-column groups, tx's at 4tx and 32 + 4tx, so
+// the 8 lanes of a B-row load phase read 128 contiguous bytes (no bank conflict)
+__device__ __forceinline__ int dm_col(int tx, int q) { return (q < 4 ? 0 : 28) + 4 * tx + q; }
 __device__ __forceinline__ int dm_tgt(int t, int cell) { return t * 32 + ((((cell >> 2) + t) & 7) << 2) + (cell & 3); }
 
 __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
@@ -629,14 +659,26 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
       float a0[4], a1[4], b0[8], b1[8];
       *reinterpret_cast<float4*>(a0) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][4 * ty]);
       *reinterpret_cast<float4*>(a1) = *reinterpret_cast<const float4*>(&sm.As[slot][kk + 1][4 * ty]);
-      *reinterpret_cast<float4*>(b0) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][8 * tx]);
-      *reinterpret_cast<float4*>(b0 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][8 * tx + 4]);
-      *reinterpret_cast<float4*>(b1) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][8 * tx]);
-      *reinterpret_cast<float4*>(b1 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][8 * tx + 4]);
+      *reinterpret_cast<float4*>(b0) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][4 * tx]);
+      *reinterpret_cast<float4*>(b0 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][32 + 4 * tx]);
+      *reinterpret_cast<float4*>(b1) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][4 * tx]);
+      *reinterpret_cast<float4*>(b1 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][32 + 4 * tx]);
+      unsigned long long p0[4], p1[4];
 #pragma unroll
-      for (int r = 0; r < 4; r++)
+      for (int q = 0; q < 4; q++) {
+        p0[q] = pack_f2(b0[2 * q], b0[2 * q + 1]);
+        p1[q] = pack_f2(b1[2 * q], b1[2 * q + 1]);
+      }
 #pragma unroll
-        for (int q = 0; q < 8; q++) acc[r][q] = fmin3(acc[r][q], a0[r] + b0[q], a1[r] + b1[q]);
+      for (int r = 0; r < 4; r++) {
+        const unsigned long long ar0 = pack_f2(a0[r], a0[r]), ar1 = pack_f2(a1[r], a1[r]);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const float2 s0 = fadd2(ar0, p0[q]), s1 = fadd2(ar1, p1[q]);
+          acc[r][2 * q] = fmin3(acc[r][2 * q], s0.x, s1.x);
+          acc[r][2 * q + 1] = fmin3(acc[r][2 * q + 1], s0.y, s1.y);
+        }
+      }
     }
     uint32_t mask = 0;
     if (c == 0) {   // improvement is against the old C (which wins ties)
@@ -644,8 +686,8 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
       __syncthreads();
 #pragma unroll
       for (int r = 0; r < 4; r++) {
-        const float4 w0 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 8 * tx]);
-        const float4 w1 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 8 * tx + 4]);
+        const float4 w0 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 4 * tx]);
+        const float4 w1 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 32 + 4 * tx]);
         const float cv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
 #pragma unroll
         for (int q = 0; q < 8; q++) {
@@ -693,7 +735,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
       __syncwarp();
       for (int it = lane; it < total; it += 32) {
         const int e = q[it], tt = (t & ~31) | (e >> 5), cell = e & 31;
-        const int row = 4 * (tt >> 3) + (cell >> 3), col = 8 * (tt & 7) + (cell & 7);
+        const int row = 4 * (tt >> 3) + (cell >> 3), col = dm_col(tt & 7, cell & 7);
         const float target = sm.Cs[dm_tgt(tt, cell)];
         int found = 0;
 #pragma unroll
@@ -738,14 +780,14 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
       for (int q = 0; q < 8; q++) {
         const uint32_t k = kid_of(8 * r + q);
         pv[r][q] = int32_t(p.inner_off + k);
-        if (pred && k != 0xFFFFu) pv[r][q] = __ldg(p.predB + int64_t(k) * p.ldp + j0 + 8 * tx + q);
+        if (pred && k != 0xFFFFu) pv[r][q] = __ldg(p.predB + int64_t(k) * p.ldp + j0 + dm_col(tx, q));
       }
 #pragma unroll
     for (int r = 0; r < 4; r++) {
       const int64_t i = i0 + 4 * ty + r;
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-        const int64_t j = j0 + 8 * tx + 4 * h;
+        const int64_t j = j0 + 32 * h + 4 * tx;
         const uint32_t w0 = kw[4 * r + 2 * h], w1 = kw[4 * r + 2 * h + 1];
         if ((w0 & w1) == 0xFFFFFFFFu) continue;             // none of the 4 cells improved
         const bool all4 = ((w0 & 0xFFFFu) != 0xFFFFu) && ((w0 >> 16) != 0xFFFFu) &&

@@ -87,8 +87,8 @@ int shard_pivot_impl(int tier, int64_t N, int b, void* Dv, int64_t ld, int32_t* 
     // fused panel push: the product also covers the diagonal tiles (Dg (x) Dg never improves a
     // closed block) and stores every cell of the b x N panel, values and pred, into each
     // peer's receive slot (address + peer_dv / peer_dp bytes, IPC-mapped over NVLink)
-    if (!nt || !(store == STORE_U8 || store == STORE_U16))
-      return set_error(APSP_EINVAL, "the fused panel push needs the u8 / u16 tier");
+    if (!nt || !(store == STORE_U8 || store == STORE_U16 || store == STORE_W32))
+      return set_error(APSP_EINVAL, "the fused panel push needs a bulk-staged tier (u8 / u16 / w32)");
     if (npeers > MAX_PEERS) return set_error(APSP_EINVAL, "npeers %d outside [0, %d]", npeers, MAX_PEERS);
     a.npeers = npeers;
     a.push_all = 1;

@@ -130,6 +130,21 @@ __device__ __forceinline__ float fmin3(float a, float b, float c) {
   return d;
 }
 
+// packed fp32x2 add (FADD2 on sm_100; a scalar operand packed as {x, x} folds into the
+// instruction's .F32 broadcast form): two correctly rounded sums per instruction
+__device__ __forceinline__ unsigned long long pack_f2(float x, float y) {
+  unsigned long long d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(x), "f"(y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+  return r;
+}
+
 // bulk-staged launchers (minplus_bulk.cu)
 template <int S> int launch_nt(const MinplusArgs& a, cudaStream_t s);
 int launch_w32nt(const MinplusArgs& a, cudaStream_t s);

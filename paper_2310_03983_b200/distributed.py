@@ -95,6 +95,29 @@ def pick_tiers(dtype_code: int, scan: dict, n: int = 0) -> list[int]:
     return t
 
 
+def resolve_tier(tier, dtype_code: int, scan: dict):
+    """A caller's forced tier (None / "auto", a name such as "u8", or a tier code) -> its code,
+    or None for the automatic choice. A forced tier must hold the input exactly (as the
+    single-GPU engine's pick_tiers: narrow integer tiers need integral costs within range);
+    the certificate still decides whether the result fits."""
+    if tier is None or tier == "auto" or tier == nat.TIER_AUTO:
+        return None
+    from .solvers import _tier_arg
+
+    code = _tier_arg(tier)
+    if code not in nat.TIER_NAMES:
+        raise ParameterError(f"unknown tier {tier!r}")
+    integral = dtype_code != nat.DTYPE_F32 or not scan["non_integral"]
+    w = scan["max_finite"]
+    fits = {nat.TIER_U8: integral and w <= U8_LIMIT, nat.TIER_U16: integral and w <= U16_LIMIT,
+            nat.TIER_W32: integral and w <= W32_LIMIT,
+            nat.TIER_I32: dtype_code != nat.DTYPE_F32 and w <= INF32 - 1,
+            nat.TIER_F32: dtype_code == nat.DTYPE_F32, nat.TIER_I64: dtype_code == nat.DTYPE_I64}[code]
+    if not fits:
+        raise ParameterError(f"tier {nat.TIER_NAMES[code]!r} cannot hold this input exactly")
+    return code
+
+
 def merge_scans(scans: list[dict]) -> dict:
     out = {k: 0 for k in ("negative", "diag_nonzero", "non_integral", "zero_offdiag")}
     out["max_finite"] = -1
@@ -110,9 +133,6 @@ def check_scan(scan: dict) -> None:
         raise NegativeWeightError("solver input contains a negative finite cost")
     if scan["diag_nonzero"]:
         raise MalformedGraphError("solver input must have a zero diagonal")
-    if scan["zero_offdiag"]:
-        raise ParameterError("zero-cost edges need the classic k order for predecessors; "
-                             "use fw_classic(method='classic') on one GPU")
 
 
 # ---- the schedule --------------------------------------------------------------------------
@@ -123,6 +143,7 @@ class RankState:
     row0: int
     rows_valid: int
     state: object = None
+    info: dict = field(default_factory=dict)
 
 
 def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, comm, dtype_code: int,
@@ -130,7 +151,10 @@ def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, co
     """Solve with the given local ranks; returns (tier, global max finite)."""
     N, R = layout(n, world, block)
     scan = merged_scan(ranks, ops, h_locals, n, allreduce_max)
-    tiers = [tier_req] if tier_req is not None else pick_tiers(dtype_code, scan, n)
+    forced = resolve_tier(tier_req, dtype_code, scan)
+    if scan["zero_offdiag"]:
+        return classic_fallback(ranks, world, n, ops, comm, dtype_code, h_locals, R, N, allreduce_max)
+    tiers = [forced] if forced is not None else pick_tiers(dtype_code, scan, n)
     for tier in tiers:
         for rk, h in zip(ranks, h_locals):
             rk.state = ops.alloc(tier, R, N)
@@ -145,6 +169,30 @@ def run_schedule(ranks: list[RankState], world: int, n: int, block: int, ops, co
     if dtype_code == nat.DTYPE_I32:
         raise CostRangeError("shortest-path cost left the representable int32 range")
     raise CostRangeError("no value tier could represent the result")
+
+
+EXACT_TIER = {nat.DTYPE_I32: nat.TIER_I32, nat.DTYPE_F32: nat.TIER_F32, nat.DTYPE_I64: nat.TIER_I64}
+
+
+def classic_fallback(ranks, world, n, ops, comm, dtype_code, h_locals, R, N, allreduce_max):
+    """Zero-cost edges (allowed by the reference's CostMatrix, core.py:161-230): many cells
+    relaxing at once could make equal-distance vertices point at each other, so -- as on one
+    GPU -- the predecessors come from the classic k order (bit-exact with reference fw_classic).
+    The rows are gathered on rank 0, solved there by the classic kernel, and scattered back into
+    every rank's state in the exact tier; returns (tier, global max finite) like run_schedule."""
+    full = comm.gather_rows(ranks, h_locals, n, R)          # rank 0: the n x n input, else None
+    res = ops.classic(full, n, dtype_code) if full is not None else None
+    rows = comm.scatter_rows(ranks, res, n, R)               # per local rank: (dist rows, pred rows)
+    tier = EXACT_TIER[dtype_code]
+    for rk, (d, p) in zip(ranks, rows):
+        rk.state = ops.alloc(tier, R, N)
+        ops.prepare(rk.state, d, n, rk.row0, dtype_code)
+        ops.set_pred_rows(rk.state, p)
+    local_max = max(ops.max_finite(rk.state, rk.rows_valid, n) for rk in ranks)
+    gmax = allreduce_max(local_max) if allreduce_max else local_max
+    for rk in ranks:
+        rk.info = {"classic_for_zero_edges": True}
+    return tier, gmax
 
 
 def run_rounds(ranks: list[RankState], N: int, R: int, b: int, ops, comm) -> None:
@@ -167,7 +215,7 @@ def run_rounds(ranks: list[RankState], N: int, R: int, b: int, ops, comm) -> Non
     # whole panel into every peer's receive slot; the comm only adds tiny barriers
     fused = bool(getattr(ops, "fused_for", lambda st: False)(ranks[0].state))
     if fused:
-        comm.connect_slots(ranks, ops)
+        fused = bool(comm.connect_slots(ranks, ops))
     o, lr = owner(0)
     panels = None
     for rk in ranks:
@@ -251,8 +299,8 @@ class CudaShardOps:
         self.fused = fused
 
     def fused_for(self, st) -> bool:
-        """Fused panel push (the pivot kernel's own peer stores) for the u8 / u16 tiers."""
-        return self.fused and st.tier in (nat.TIER_U8, nat.TIER_U16)
+        """Fused panel push (the pivot kernel's own peer stores) for the bulk-staged tiers."""
+        return self.fused and st.tier in (nat.TIER_U8, nat.TIER_U16, nat.TIER_W32)
 
     def set_peer_slots(self, st: CudaShard, peer_pv: list, peer_pp: list, keep=()) -> None:
         if len(peer_pv) > 7:
@@ -326,6 +374,20 @@ class CudaShardOps:
                                              skip_lo, skip_hi, st.scratch.data_ptr(), st.scratch.numel(),
                                              self._stream()))
 
+    def classic(self, h, n: int, dtype_code: int):
+        """Classic-order FW of the whole (gathered) matrix on this GPU (apsp_fw_classic)."""
+        t = self.torch
+        d = h.contiguous().clone()
+        p = t.empty((n, n), dtype=t.int32, device=self.device)
+        info = nat.ApspInfo()
+        nat.check(self.lib.apsp_fw_classic(dtype_code, n, d.data_ptr(), n, p.data_ptr(), n, self._stream(),
+                                           ctypes.byref(info)))
+        return d, p
+
+    def set_pred_rows(self, st: CudaShard, p) -> None:
+        if p is not None and p.numel():
+            st.P[:p.shape[0], :p.shape[1]].copy_(p)
+
     def max_finite(self, st: CudaShard, rows_valid: int, n: int) -> int:
         mx = ctypes.c_int64(-1)
         nat.check(self.lib.apsp_shard_finish(st.tier, nat.DTYPE_I32, rows_valid, n, st.D.data_ptr(), st.N,
@@ -368,6 +430,39 @@ class TorchComm:
         self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
         return int(t.item())
 
+    def gather_rows(self, ranks, h_locals, n: int, R: int):
+        """Every rank's input rows -> the n x n matrix on rank 0 (None elsewhere)."""
+        (rk,), (h,) = ranks, h_locals
+        t = self.torch
+        dtype = h.dtype if h is not None else t.int32
+        pad = t.zeros((R, n), dtype=dtype, device=self.device)
+        if rk.rows_valid:
+            pad[:rk.rows_valid].copy_(h)
+        parts = [t.empty_like(pad) for _ in range(self.world)] if self.rank == 0 else None
+        self.dist.gather(pad, parts, dst=0, group=self.group)
+        return t.cat(parts)[:n].contiguous() if self.rank == 0 else None
+
+    def scatter_rows(self, ranks, res, n: int, R: int):
+        """Rank 0's (dist, pred) n x n result -> every rank's rows [(dist rows, pred rows)]."""
+        (rk,) = ranks
+        t = self.torch
+        meta = [res[0].dtype if res is not None else None]
+        self.dist.broadcast_object_list(meta, src=0, group=self.group)
+        dd = t.empty((R, n), dtype=meta[0], device=self.device)
+        pp = t.empty((R, n), dtype=t.int32, device=self.device)
+        if self.rank == 0:
+            d, p = res
+            D = t.zeros((R * self.world, n), dtype=d.dtype, device=self.device)
+            P = t.full((R * self.world, n), -1, dtype=t.int32, device=self.device)
+            D[:n].copy_(d)
+            P[:n].copy_(p)
+            dl, pl = list(D.chunk(self.world)), list(P.chunk(self.world))
+        else:
+            dl = pl = None
+        self.dist.scatter(dd, dl, src=0, group=self.group)
+        self.dist.scatter(pp, pl, src=0, group=self.group)
+        return [(dd[:rk.rows_valid], pp[:rk.rows_valid])]
+
     def _flag(self, stream=None):
         """A 4-byte all-reduce issued on `stream` (default: current): the collective's
         completion orders every rank's queued work before whatever waits on the handle."""
@@ -376,14 +471,37 @@ class TorchComm:
         with ctx:
             return self.dist.all_reduce(t, group=self.group, async_op=True)
 
-    def connect_slots(self, ranks, ops):
+    def peers_reachable(self) -> bool:
+        """True on every rank iff every rank's GPU can store into every other rank's GPU
+        (cudaDeviceCanAccessPeer for each ordered pair; the IPC mappings then enable peer access
+        themselves). All ranks get the same answer, so they agree on fused vs NCCL exchange."""
+        if self.world == 1:
+            return True
+        if self.device.type != "cuda":
+            return False
+        devs = [None] * self.world
+        self.dist.all_gather_object(devs, self.device.index, group=self.group)
+        mine = self.device.index
+        ok = all(d == mine or self.torch.cuda.can_device_access_peer(mine, d) for d in devs)
+        return self.allreduce_min(int(ok)) == 1
+
+    def allreduce_min(self, v: int) -> int:
+        t = self.torch.tensor([int(v)], dtype=self.torch.int64, device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return int(t.item())
+
+    def connect_slots(self, ranks, ops) -> bool:
         """Fused panel push: map every peer's two receive slots (values, pred) into this process
-        with CUDA IPC handles exchanged over the process group."""
+        with CUDA IPC handles exchanged over the process group. Returns False (every rank) when
+        some pair of GPUs has no peer access: the rounds then use the NCCL broadcast."""
         (rk,) = ranks
         st = rk.state
         if self.world == 1:
             ops.set_peer_slots(st, [], [])
-            return
+            return True
+        if not self.peers_reachable():
+            ops.set_peer_slots(st, [], [])
+            return False
         from torch.multiprocessing.reductions import reduce_tensor
 
         mine = [reduce_tensor(x) for x in (st.pv[0], st.pv[1], st.pp[0], st.pp[1])]
@@ -399,6 +517,7 @@ class TorchComm:
             keep += [v0, v1, p0, p1]
         ops.set_peer_slots(st, peer_pv, peer_pp, keep=keep)
         self._flag().wait()
+        return True
 
     def slot_barrier(self, ranks, ops):
         if self.world > 1:
@@ -451,13 +570,23 @@ class EmulatedComm:
     """All ranks in this process on one device: every rank reads the owner's panel directly
     (fused: each rank reads its own receive slot, filled by the owner's pivot kernel)."""
 
-    def connect_slots(self, ranks, ops):
+    def connect_slots(self, ranks, ops) -> bool:
         for rk in ranks:
             others = [o.state for o in ranks if o is not rk]
             ops.set_peer_slots(rk.state, [o.pv for o in others], [o.pp for o in others])
+        return True
 
     def slot_barrier(self, ranks, ops):
         return None   # one process, stream order: the side-stream pivot follows all queued updates
+
+    def gather_rows(self, ranks, h_locals, n: int, R: int):
+        import torch
+
+        return torch.cat([h for rk, h in zip(ranks, h_locals) if rk.rows_valid])[:n].contiguous()
+
+    def scatter_rows(self, ranks, res, n: int, R: int):
+        d, p = res
+        return [(d[rk.row0:rk.row0 + rk.rows_valid], p[rk.row0:rk.row0 + rk.rows_valid]) for rk in ranks]
 
     def bcast_start(self, ranks, owner: int, owner_panels, slot: int, ops, fused: bool = False):
         pv, pp, _ = owner_panels
@@ -506,7 +635,7 @@ def fw_blocked_sharded(h_local, n: int, *, comm: TorchComm, block: int = 256, ti
         ops.finish(rs.state, rows_valid, n, dtype_code, dist, pred)
     return ShardedResult(dist, pred, row0, rows_valid,
                          {"tier": nat.TIER_NAMES[tier], "max_finite": gmax, "world": world, "N": N, "R": R,
-                          "block": block, "host_s": time.perf_counter() - t0})
+                          "block": block, "host_s": time.perf_counter() - t0} | rs.info)
 
 
 def fw_blocked_emulated(h, world: int, *, block: int = 256, tier=None, fused: bool = False):
@@ -532,13 +661,15 @@ def fw_blocked_emulated(h, world: int, *, block: int = 256, tier=None, fused: bo
         if rk.rows_valid:
             ops.finish(rk.state, rk.rows_valid, n, _dtype_of(h), dist[rk.row0:rk.row0 + rk.rows_valid],
                        pred[rk.row0:rk.row0 + rk.rows_valid])
-    return dist, pred, {"tier": nat.TIER_NAMES[tier_code], "max_finite": gmax}
+    return dist, pred, {"tier": nat.TIER_NAMES[tier_code], "max_finite": gmax} | ranks[0].info
 
 
 # ---- multi-GPU bench leg (torchrun) ----------------------------------------------------------
 
-def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
-    """bench.py --gpus N under torchrun: weak-scaled n, row bands, max-over-ranks device time."""
+def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler, cpu_baseline=None, tier_peak=None,
+               tier_op=None):
+    """bench.py --gpus N under torchrun: weak-scaled n (or n=32768 with --strong), row bands,
+    max-over-ranks device time; per-rank phase-3 roofline and rank 0's bounded CPU baseline."""
     import os
 
     import torch
@@ -606,6 +737,39 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
         torch.cuda.synchronize()
         dist.barrier()
     launches = comm.allreduce_sum(lib.apsp_launch_count() - launches0)   # all ranks' kernels
+    # per-rank roofline of the dominant kernel (FW phase 3 on the local rows): one extra, untimed
+    # solve with every phase-3 launch bracketed by CUDA events on its stream
+    roofline = None
+    if not rk:
+        lib.apsp_set_profiling(1)
+        step()
+        torch.cuda.synchronize()
+        lib.apsp_set_profiling(0)
+        kms, kl = ctypes.c_double(0), ctypes.c_int32(0)
+        nat.check(lib.apsp_profile_read(ctypes.byref(kms), ctypes.byref(kl)))
+        upd = R * (N - block) ** 2          # sum over rounds of (local rows - owned pivot rows) x (N - b) x b
+        rate = upd / (kms.value / 1e3) if kms.value > 0 else 0.0
+        every = [None] * world
+        dist.all_gather_object(every, (rank, rate, kms.value, int(kl.value)), group=None)
+        tier = res.info["tier"]
+        peak = (tier_peak or {}).get(tier)
+        rates = [r[1] for r in sorted(every)]
+        roofline = {"bound": "alu", "kernel": f"minplus phase 3 ({tier} tier) on each rank's rows",
+                    "op": (tier_op or {}).get(tier), "unit": "T updates/s",
+                    "achieved": min(rates) / 1e12, "peak": peak / 1e12 if peak else None,
+                    "frac": (min(rates) / peak) if peak else None,
+                    "per_rank": [{"rank": r, "achieved": x / 1e12, "kernel_ms": ms, "launches": nl,
+                                  "frac": (x / peak) if peak else None} for r, x, ms, nl in sorted(every)],
+                    "updates_per_rank": upd, "traffic": None,
+                    "measurement": "CUDA events around every phase-3 launch on its stream (apsp_profile_read), "
+                                   "one extra solve; achieved = the slowest rank"}
+    cpu = None
+    if cpu_baseline is not None and not getattr(args, "no_cpu", False):
+        if rank == 0:   # the other ranks wait at the barrier below
+            from .graphgen import GenParams as _GP, dense_costs as _dc
+
+            cpu = cpu_baseline(_dc(_GP(n, args.rho, 100, 7 + n), np.int32))
+        dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     total_ms = float(ms.item())
@@ -638,7 +802,8 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
     if rank == 0:
         line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": f"tier {res.info['tier']}; int32 in/out",
+                "scaling": "strong" if getattr(args, "strong", False) else "weak", "vs_baseline": None,
+                "dtype": f"tier {res.info['tier']}; int32 in/out",
                 "data": "synthetic (reference generator, bit-identical to apsp.generate)",
                 "config": config(n, args.rho, world) | (
                     {"workload": f"aligned R-Kleene APSP (replicated matrix, row-band products), distances+"
@@ -646,8 +811,8 @@ def bench_main(args, metric, unit, config, make_input, weak_n, ClockSampler):
                                  f"seed=7+n), int32 in/out", "alg": "rkleene", "base_threshold": 2048,
                      "fused_exchange": fused} if rk else
                     {"block": block, "rows_per_rank": R, "fused_exchange": fused}),
-                "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e, "cpu_baseline": None,
-                "tier": res.info["tier"]}
+                "clocks": clk.summary(), "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+                "roofline": roofline, "tier": res.info["tier"]}
         os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
     dist.destroy_process_group()

@@ -48,6 +48,7 @@ from .distributed import (
     _TORCH_STORE,
     merged_scan,
     pick_tiers,
+    resolve_tier,
     round_up,
 )
 
@@ -121,14 +122,17 @@ def run_rk_schedule(ranks, world, n, thr, ops, comm, dtype_code, h_fulls, tier_r
     for rk in ranks:
         rk.row0, rk.rows_valid = 0, n
     scan = merged_scan(ranks[:1], ops, h_fulls[:1], n, None)   # every rank holds the same input
-    tiers = [tier_req] if tier_req is not None else pick_tiers(dtype_code, scan, n)
+    forced = resolve_tier(tier_req, dtype_code, scan)
+    tiers = [forced] if forced is not None else pick_tiers(dtype_code, scan, n)
     for tier in tiers:
         for rk, h in zip(ranks, h_fulls):
             rk.state = ops.alloc(tier, N, thr)
             ops.prepare(rk.state, h, n, dtype_code)
         if getattr(ops, "fused_for", lambda st: False)(ranks[0].state):
-            comm.connect_replicas(ranks, ops)
-            comm.product_barrier(ranks, ops)      # every replica prepared before any peer store
+            if comm.connect_replicas(ranks, ops):
+                comm.product_barrier(ranks, ops)  # every replica prepared before any peer store
+            else:
+                ops.fused = False                 # no peer access between some GPUs: all-gather
         run_rkleene(ranks, world, N, thr, ops, comm)
         gmax = ops.max_finite(ranks[0].state, n)
         if allreduce_max is not None:
@@ -311,7 +315,9 @@ def _torch_connect_replicas(self: TorchComm, ranks, ops):
     st = rk.state
     if self.world == 1:
         ops.set_peers(st, [], [])
-        return
+        return True
+    if not self.peers_reachable():
+        return False
     from torch.multiprocessing.reductions import reduce_tensor
 
     mine = (reduce_tensor(st.D), reduce_tensor(st.P))
@@ -323,6 +329,7 @@ def _torch_connect_replicas(self: TorchComm, ranks, ops):
             peer_D.append(fd(*ad))
             peer_P.append(fp(*ap_))
     ops.set_peers(st, peer_D, peer_P, keep=peer_D + peer_P)
+    return True
 
 
 def _torch_product_barrier(self: TorchComm, ranks, ops):
@@ -338,6 +345,7 @@ def _emulated_connect_replicas(self: EmulatedComm, ranks, ops):
     for rk in ranks:
         others = [o.state for o in ranks if o is not rk]
         ops.set_peers(rk.state, [o.D for o in others], [o.P for o in others])
+    return True
 
 
 def _emulated_product_barrier(self: EmulatedComm, ranks, ops):

@@ -104,3 +104,14 @@ class CpuShardOps:
         a = st.D.numpy()[:rows_valid, :n]
         fin = a != INF_RAW
         return int(a[fin].max()) if fin.any() else -1
+
+    def classic(self, h, n, dtype_code):
+        """Zero-cost-edge fallback: classic-order FW of the gathered matrix (the oracle)."""
+        from oracle import oracle as orc
+
+        d, p = orc.fw_classic(h.numpy().astype(np.int64))
+        return torch.from_numpy(d), torch.from_numpy(p.astype(np.int32))
+
+    def set_pred_rows(self, st, p):
+        if p is not None and p.numel():
+            st.P[:p.shape[0], :p.shape[1]].copy_(p)

@@ -27,7 +27,7 @@ def _free_port() -> int:
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, h, block, out_dir):
+def _worker(rank, world, port, h, block, out_dir, tier=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -45,18 +45,26 @@ def _worker(rank, world, port, h, block, out_dir):
         hl = torch.from_numpy(h[row0:row0 + rv].copy())
         ops = CpuShardOps(block)
         rs = RankState(rank, row0, rv)
-        tier, gmax = run_schedule([rs], world, n, block, ops, comm, nat.DTYPE_I64, [hl], None,
-                                  comm.allreduce_max)
+        try:
+            tier, gmax = run_schedule([rs], world, n, block, ops, comm, nat.DTYPE_I64, [hl], tier,
+                                      comm.allreduce_max)
+        except Exception as exc:   # recorded for the parent (e.g. a refused forced tier)
+            np.savez(os.path.join(out_dir, f"r{rank}.npz"), err=np.array(type(exc).__name__))
+            return
         np.savez(os.path.join(out_dir, f"r{rank}.npz"), d=rs.state.D.numpy()[:rv, :n], p=rs.state.P.numpy()[:rv, :n],
-                 tier=tier, gmax=gmax)
+                 tier=tier, gmax=gmax, classic=bool(rs.info.get("classic_for_zero_edges")))
     finally:
         dist.destroy_process_group()
 
 
-def _solve(h, world, block):
+def _solve(h, world, block, tier=None, want_info=False):
     with tempfile.TemporaryDirectory() as td:
-        mp.spawn(_worker, args=(world, _free_port(), h, block, td), nprocs=world, join=True)
+        mp.spawn(_worker, args=(world, _free_port(), h, block, td, tier), nprocs=world, join=True)
         parts = [np.load(os.path.join(td, f"r{r}.npz")) for r in range(world)]
+        if "err" in parts[0]:
+            return str(parts[0]["err"])
+        if want_info:
+            return parts
         d = np.concatenate([p["d"] for p in parts])
         pr = np.concatenate([p["p"] for p in parts])
         return d, pr, int(parts[0]["tier"]), [int(p["gmax"]) for p in parts]
@@ -114,3 +122,32 @@ def test_tier_selection_mirrors_library():
     assert pick_tiers(nat.DTYPE_I32, tiny, 2048) == [nat.TIER_W32, nat.TIER_I32]
     assert pick_tiers(nat.DTYPE_I64, dense | {"max_finite": 1 << 30}, 16384) == [nat.TIER_I64]
     assert pick_tiers(nat.DTYPE_F32, dense | {"non_integral": 1}, 16384) == [nat.TIER_F32]
+
+
+def test_two_ranks_zero_cost_edges_take_the_classic_order():
+    """Zero-cost edges (allowed by the reference's CostMatrix): the rows are gathered, solved in
+    classic k order and scattered back -- distances and pred bit-exact with fw_classic."""
+    from oracle import oracle as orc
+
+    h = random_graph_raw(150, 0.05, 9, seed=21, zero_frac=0.03)
+    want_d, want_p = orc.fw_classic(h)
+    parts = _solve(h, 2, 32, want_info=True)
+    d = np.concatenate([p["d"] for p in parts])
+    pr = np.concatenate([p["p"] for p in parts])
+    assert all(bool(p["classic"]) for p in parts)
+    assert np.array_equal(d, want_d) and np.array_equal(pr.astype(np.int64), want_p)
+
+
+def test_two_ranks_forced_tier_names():
+    """A forced tier is given by name like on one GPU, and one that cannot hold the input is
+    refused on every rank (ParameterError) instead of failing inside the schedule."""
+    from oracle import oracle as orc
+
+    h = random_graph_raw(90, 0.1, 100, seed=5)
+    want_d, _ = orc.fw_classic(h)
+    d, _, tier, _ = _solve(h, 2, 16, tier="w32")
+    from paper_2310_03983_b200 import _native as nat
+
+    assert tier == nat.TIER_W32 and np.array_equal(d, want_d)
+    wide = random_graph_raw(90, 0.1, 1000, seed=6)
+    assert _solve(wide, 2, 16, tier="u8") == "ParameterError"

@@ -130,6 +130,19 @@ __global__ void k_argmin_f32(float* out, float b0, float step) {
   float s = 0; for (int i = 0; i < U; i++) s += acc[i] + idx[i];
   if (s == 1234.5f) out[threadIdx.x] = s;
 }
+// G2: exact argmin int32 (the i32 tier's register-staged compare-select): IADD, ISETP, min, SEL
+__global__ void k_argmin_i32(int* out, int b0, int step) {
+  int acc[U], a[U], idx[U];
+  for (int i = 0; i < U; i++) { acc[i] = 0x3fffffff; a[i] = threadIdx.x * 3 + i; idx[i] = -1; }
+  int b = b0;
+  for (int r = 0; r < R; r++) {
+#pragma unroll
+    for (int i = 0; i < U; i++) { int s = a[i] + b; bool p = s < acc[i]; acc[i] = min(acc[i], s); idx[i] = p ? r : idx[i]; }
+    b -= step;
+  }
+  int s = 0; for (int i = 0; i < U; i++) s ^= acc[i] + idx[i];
+  if (s == 12345) out[threadIdx.x] = s;
+}
 // H: FFMA reference (peak issue)
 __global__ void k_ffma(float* out, float b0, float step) {
   float acc[U], a[U];
@@ -175,6 +188,7 @@ int main() {
   run("viaddmin_s16x2", k_viaddmin16x2, i, 1, 1, 2.0, blocks, threads, clk);
   run("iadd+vimin3", k_iadd_vimin3, i, 1, 1, 2.0, blocks, threads, clk);
   run("argmin_f32", k_argmin_f32, f, 1.f, 0.001f, 1.0, blocks, threads, clk);
+  run("argmin_i32", k_argmin_i32, i, 1, 1, 1.0, blocks, threads, clk);
   run("ffma(1 op)", k_ffma, f, 1.f, 0.001f, 1.0, blocks, threads, clk);
   }
   return 0;
