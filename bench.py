@@ -44,7 +44,7 @@ FP32_CORE_PEAK = 148 * 128 * 1965e6 / 2          # 18.6 T upd/s 
 TIER_PEAK = {"u8": 37.07e12, "u16": 37.07e12, "w32": 17.98e12, "i32": 6.12e12, "f32": 20.17e12, "i64": 6.05e12}
 TIER_OP = {"u8": "VIADDMNMX.U16x2 (2 upd/instr)", "u16": "VIADDMNMX.U16x2 (2 upd/instr)",
            "w32": "VIADDMNMX.U32 (1 upd/instr)", "i32": "IADD/ISETP/IMNMX/SEL compare-select (argmin_i32)",
-           "f32": "FADD + FMNMX3 (1.5 instr/upd; deferred argmin)", "i64": "compare-select int64"}
+           "f32": "FADD2 + FMNMX3 (deferred argmin; the FMNMX3 ALU rate bounds it)", "i64": "compare-select int64"}
 BLOCK = 0          # 0: the library's size-aware default (apsp_info.block reports it)
 
 

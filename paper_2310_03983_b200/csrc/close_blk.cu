@@ -18,6 +18,7 @@
 // that (the bit-exact classic pred is fw_classic(method="classic")); zero-cost edges never
 // reach this kernel (fw_sched routes them to the classic order).
 #include <cstdint>
+#include <cstdlib>
 #include "launch.h"
 #include "tiles.cuh"
 
@@ -61,7 +62,7 @@ __device__ __forceinline__ int other(int q, int K) { return q < SB * K ? q : q +
 
 template <int S>
 __global__ void __launch_bounds__(CT, 1) block_close_blk_kernel(typename StoreT<S>::T* D, int64_t ld, int64_t lo,
-                                                                int m, int32_t* idx, int64_t ldi) {
+                                                                int m, int32_t* idx, int64_t ldi, int skip) {
   using O = BlkOps<S>;
   using T = typename O::T;
   extern __shared__ __align__(16) unsigned char smraw_blk[];
@@ -101,7 +102,7 @@ __global__ void __launch_bounds__(CT, 1) block_close_blk_kernel(typename StoreT<
     const int k0 = SB * K;
     const uint8_t tagK = uint8_t(K + 1);
     // (a) diagonal sub-block: warps 0..3, thread (w, l) owns column k0 + l, rows k0 + 8w + r
-    if (w < 4) {
+    if (w < 4 && !(skip & 2)) {
       T c[8], c0[8];
 #pragma unroll
       for (int r = 0; r < 8; r++) c0[r] = c[r] = sm.V[k0 + 8 * w + r][k0 + l];
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(CT, 1) block_close_blk_kernel(typename StoreT<
     // panel is also an operand of its own update):
     //   row panel:    rows k0 + 2w + {0,1}, other columns 3l + {0,1,2}
     //   column panel: other rows 6w + {0..5}, column k0 + l
-    {
+    if (!(skip & 4)) {
       int rrow[2], rcol[3], crow[6];
 #pragma unroll
       for (int a = 0; a < 2; a++) rrow[a] = k0 + 2 * w + a;
@@ -187,7 +188,7 @@ __global__ void __launch_bounds__(CT, 1) block_close_blk_kernel(typename StoreT<
     }
     __syncthreads();
     // (c) the rest: other rows 6w + {0..5} x other columns 3l + {0,1,2}, with the new panels
-    {
+    if (!(skip & 8)) {
       int row[6], col[3];
 #pragma unroll
       for (int a = 0; a < 6; a++) row[a] = other(6 * w + a, K);
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(CT, 1) block_close_blk_kernel(typename StoreT<
     }
     __syncthreads();
   }
-  if (idx) {
+  if (idx && !(skip & 1)) {
     // witness of the last improving sub-round: the first w in it with d[i][w] + d[w][j] == d[i][j].
     // The improved cells are compacted into a queue first (warp-aggregated appends), then each
     // lane scans its cell's 32 candidates branch-free (independent loads, one select per w), so
@@ -318,19 +319,21 @@ int launch_block_close_blk(int store, void* D, int64_t ld, int64_t lo, int64_t m
   if (m <= 0) return 0;
   if (m > CB) return set_error(2, "blocked closure takes m <= %d", CB);
   const int sb = int(sizeof(BlkSmem<float>));
+  // A/B timing only (results wrong): APSP_BLK_SKIP bits 1 witness, 2 diagonal, 4 panels, 8 rest
+  static const int skip = getenv("APSP_BLK_SKIP") ? atoi(getenv("APSP_BLK_SKIP")) : 0;
   static std::atomic<unsigned long long> a0{0}, a1{0}, a2{0};
   switch (store) {
     case STORE_F32:
       APSP_CUDA_TRY(smem_optin(block_close_blk_kernel<STORE_F32>, sb, a0));
-      block_close_blk_kernel<STORE_F32><<<1, CT, sb, s>>>(static_cast<float*>(D), ld, lo, int(m), idx, ldi);
+      block_close_blk_kernel<STORE_F32><<<1, CT, sb, s>>>(static_cast<float*>(D), ld, lo, int(m), idx, ldi, skip);
       break;
     case STORE_W32:
       APSP_CUDA_TRY(smem_optin(block_close_blk_kernel<STORE_W32>, sb, a1));
-      block_close_blk_kernel<STORE_W32><<<1, CT, sb, s>>>(static_cast<int32_t*>(D), ld, lo, int(m), idx, ldi);
+      block_close_blk_kernel<STORE_W32><<<1, CT, sb, s>>>(static_cast<int32_t*>(D), ld, lo, int(m), idx, ldi, skip);
       break;
     case STORE_I32:
       APSP_CUDA_TRY(smem_optin(block_close_blk_kernel<STORE_I32>, sb, a2));
-      block_close_blk_kernel<STORE_I32><<<1, CT, sb, s>>>(static_cast<int32_t*>(D), ld, lo, int(m), idx, ldi);
+      block_close_blk_kernel<STORE_I32><<<1, CT, sb, s>>>(static_cast<int32_t*>(D), ld, lo, int(m), idx, ldi, skip);
       break;
     default:
       return set_error(2, "blocked closure: store %d unsupported", store);

@@ -595,6 +595,7 @@ struct SmemF32DM {   // 96 KB: 2 CTAs / SM
   uint16_t kid[NT][32];         // 0-based k of the last strict improvement, 0xFFFF = none
   uint16_t queue[NT / 32][1024];  // per warp: improved (lane, cell) items of the current chunk
   unsigned long long bar[DM_STAGES];
+  unsigned long long cbar;       // the old C tile (128 row copies)
   unsigned int done[DM_STAGES];  // warps finished with the slot's chunk
 };
 // rescan target slot of (thread, cell): 4-cell groups stay contiguous (one 16-byte store each),
@@ -625,20 +626,14 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
       mbar_init(&sm.bar[s], 1);
       sm.done[s] = 0;
     }
+    mbar_init(&sm.cbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int64_t c = 0; c < DM_STAGES && c < nch; c++) issue(c);
+    mbar_expect_tx(&sm.cbar, BM * DM_BN * 4);
   }
   __syncthreads();
-  {  // C tile -> smem (merged after chunk 0): row t >> 1, half (t & 1) of 64 floats
-    const int r = t >> 1;
-    const char* src = reinterpret_cast<const char*>(static_cast<const float*>(p.C) + (i0 + r) * p.ldc + j0) +
-                      128 * (t & 1);
-    const uint32_t dst = smem_u32(reinterpret_cast<const char*>(&sm.Cs[r * DM_BN]) + 128 * (t & 1));
-#pragma unroll
-    for (int q = 0; q < 8; q++)
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst + 16 * q), "l"(src + 16 * q));
-    asm volatile("cp.async.commit_group;\n" ::);
-  }
+  if (t < BM)   // C tile -> smem (merged after chunk 0): one 256-byte bulk copy per row
+    bulk_g2s(&sm.Cs[t * DM_BN], static_cast<const float*>(p.C) + (i0 + t) * p.ldc + j0, DM_BN * 4, &sm.cbar);
 #pragma unroll
   for (int c = 0; c < 4; c++) reinterpret_cast<uint4*>(&sm.kid[t][0])[c] = make_uint4(~0u, ~0u, ~0u, ~0u);
   float acc[4][8];
@@ -649,11 +644,14 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
   for (int64_t c = 0; c < nch; c++) {
     const int slot = int(c % DM_STAGES);
     mbar_wait(&sm.bar[slot], uint32_t((c / DM_STAGES) & 1));
-    float old[4][8];
+    if (c > 0) {   // the pre-chunk values go to the thread's own target slots (not registers)
 #pragma unroll
-    for (int r = 0; r < 4; r++)
+      for (int r = 0; r < 4; r++)
 #pragma unroll
-      for (int q = 0; q < 8; q++) old[r][q] = acc[r][q];
+        for (int h = 0; h < 2; h++)
+          *reinterpret_cast<float4*>(&sm.Cs[dm_tgt(t, 8 * r + 4 * h)]) =
+              make_float4(acc[r][4 * h], acc[r][4 * h + 1], acc[r][4 * h + 2], acc[r][4 * h + 3]);
+    }
 #pragma unroll 4
     for (int kk = 0; kk < SUB; kk += 2) {
       float a0[4], a1[4], b0[8], b1[8];
@@ -682,8 +680,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
     }
     uint32_t mask = 0;
     if (c == 0) {   // improvement is against the old C (which wins ties)
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
-      __syncthreads();
+      mbar_wait(&sm.cbar, 0);
 #pragma unroll
       for (int r = 0; r < 4; r++) {
         const float4 w0 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 4 * tx]);
@@ -700,8 +697,13 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
 #pragma unroll
       for (int r = 0; r < 4; r++)
 #pragma unroll
-        for (int q = 0; q < 8; q++)
-          if (acc[r][q] < old[r][q]) mask |= 1u << (8 * r + q);
+        for (int h = 0; h < 2; h++) {
+          const float4 o = *reinterpret_cast<const float4*>(&sm.Cs[dm_tgt(t, 8 * r + 4 * h)]);
+          const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+          for (int q = 0; q < 4; q++)
+            if (acc[r][4 * h + q] < ov[q]) mask |= 1u << (8 * r + 4 * h + q);
+        }
     }
     if (__any_sync(0xffffffffu, mask != 0u)) {
       if (mask) {
@@ -795,20 +797,32 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
         if (all4) {
           *reinterpret_cast<float4*>(Cw + i * p.ldc + j) =
               make_float4(acc[r][4 * h], acc[r][4 * h + 1], acc[r][4 * h + 2], acc[r][4 * h + 3]);
-          if (p.idx) {
-            int32_t* dst = p.idx + i * p.ldi + j;
-            if (((reinterpret_cast<uintptr_t>(dst)) & 15) == 0)
-              *reinterpret_cast<int4*>(dst) = make_int4(pv[r][4 * h], pv[r][4 * h + 1], pv[r][4 * h + 2], pv[r][4 * h + 3]);
-            else
-#pragma unroll
-              for (int q = 0; q < 4; q++) dst[q] = pv[r][4 * h + q];
-          }
         } else {
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            if (kid_of(8 * r + 4 * h + q) == 0xFFFFu) continue;
-            Cw[i * p.ldc + j + q] = acc[r][4 * h + q];
-            if (p.idx) p.idx[i * p.ldi + j + q] = pv[r][4 * h + q];
+          for (int q = 0; q < 4; q++)
+            if (kid_of(8 * r + 4 * h + q) != 0xFFFFu) Cw[i * p.ldc + j + q] = acc[r][4 * h + q];
+        }
+      }
+    }
+    // predecessor stores last: the value stores above do not wait for the gathers
+    if (p.idx) {
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const int64_t i = i0 + 4 * ty + r;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          const int64_t j = j0 + 32 * h + 4 * tx;
+          const uint32_t w0 = kw[4 * r + 2 * h], w1 = kw[4 * r + 2 * h + 1];
+          if ((w0 & w1) == 0xFFFFFFFFu) continue;
+          const bool all4 = ((w0 & 0xFFFFu) != 0xFFFFu) && ((w0 >> 16) != 0xFFFFu) &&
+                            ((w1 & 0xFFFFu) != 0xFFFFu) && ((w1 >> 16) != 0xFFFFu);
+          int32_t* dst = p.idx + i * p.ldi + j;
+          if (all4 && ((reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+            *reinterpret_cast<int4*>(dst) = make_int4(pv[r][4 * h], pv[r][4 * h + 1], pv[r][4 * h + 2], pv[r][4 * h + 3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              if (kid_of(8 * r + 4 * h + q) != 0xFFFFu) dst[q] = pv[r][4 * h + q];
           }
         }
       }

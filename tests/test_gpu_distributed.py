@@ -17,7 +17,8 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import INF_RAW
+from conftest import INF_RAW, random_graph_raw
+from oracle import oracle as orc
 
 import paper_2310_03983_b200 as ap
 from paper_2310_03983_b200.core import INF32
@@ -187,6 +188,38 @@ def test_fused_panel_push_emulated(cuda, n, world, block):
     d, p, info = fw_blocked_emulated(h, world, block=block, fused=True)
     assert info["tier"] == single.info["tier"]
     assert torch.equal(d, single.distances) and torch.equal(p, single.index)
+
+
+@pytest.mark.parametrize("world,block", [(3, 128), (2, 256)])
+def test_fused_panel_push_w32_emulated(cuda, world, block):
+    """The fused push on the w32 tier (weights past the u16 range): minplus_w32nt_kernel's
+    whole-panel peer stores, bitwise equal to one GPU."""
+    from paper_2310_03983_b200.distributed import fw_blocked_emulated
+
+    n = 900
+    h = torch.from_numpy(ap.dense_costs(ap.GenParams(n, 0.05, 50000, 17), np.int32)).cuda()
+    single = ap.solve(h, "fw_blocked", block=block)
+    assert single.info["tier"] == "w32"
+    d, p, info = fw_blocked_emulated(h, world, block=block, fused=True)
+    assert info["tier"] == "w32"
+    assert torch.equal(d, single.distances) and torch.equal(p, single.index)
+
+
+def test_sharded_zero_cost_edges_classic_order(cuda):
+    """Zero-cost edges on the sharded path: gathered, solved in classic k order on one GPU,
+    scattered back -- bit-exact with reference fw_classic (the oracle)."""
+    from paper_2310_03983_b200.distributed import fw_blocked_emulated
+
+    raw = random_graph_raw(500, 0.03, 9, 77, zero_frac=0.02)
+    want_d, want_p = orc.fw_classic(raw)
+    h32 = raw.astype(np.int64)
+    h32[raw == INF_RAW] = INF32
+    h = torch.from_numpy(h32.astype(np.int32)).cuda()
+    d, p, info = fw_blocked_emulated(h, 3, block=128)
+    assert info.get("classic_for_zero_edges")
+    dd = d.cpu().numpy().astype(np.int64)
+    dd[dd == INF32] = INF_RAW
+    assert np.array_equal(dd, want_d) and np.array_equal(p.cpu().numpy().astype(np.int64), want_p)
 
 
 def _fw_ipc_worker(rank, world, port, out):
