@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(CT, 1) block_close_blk_kernel(typename StoreT<
 #pragma unroll
       for (int k = 0; k < SB; k++) {
         if (w == (k >> 3)) sm.V[k0 + k][k0 + l] = c[k & 7];   // publish row k (final for this step)
+        APSP_JITTER_POINT(k0 + k);
         asm volatile("bar.sync 1, 128;" ::: "memory");
         const T rk = sm.V[k0 + k][k0 + l];
 #pragma unroll
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(CT, 1) block_close_blk_kernel(typename StoreT<
 #pragma unroll
         for (int a = 0; a < 6; a++) ca[a] = O::min3(ca[a], O::add(pa[a][0], db[0]), O::add(pa[a][1], db[1]));
       }
+      APSP_JITTER_POINT(K + 500);
       __syncthreads();
 #pragma unroll
       for (int a = 0; a < 2; a++)

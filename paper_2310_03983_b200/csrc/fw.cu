@@ -7,9 +7,13 @@
 // Race freedom: with a zero diagonal and nonnegative costs, row k and column k are invariant
 // during step k (solvers.py:79-81), so one barrier per k suffices.
 #include <algorithm>
+#include <mutex>
+#include <vector>
+#include <cstdio>
 #include <cstdlib>
 #include "launch.h"
 #include "tiles.cuh"
+#include "engine.h"
 
 namespace apsp {
 
@@ -310,17 +314,18 @@ template <> struct CloseKeys<STORE_U16> {
   static constexpr uint32_t INF = U16_INF;
 };
 
+// The closure body is a device function so the persistent small-n kernel (fw_persist.cu) can
+// run it as one of its tasks; block_close_dpx_kernel below is the stand-alone launch.
 template <int S, bool FULL>
-__global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo,
-                                                              int m, int32_t* idx, int64_t ldi, int mode,
-                                                              int64_t via_off) {
+__device__ __forceinline__ void close_dpx_body(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo, int m,
+                                               int32_t* idx, int64_t ldi, int mode, int64_t via_off,
+                                               unsigned char* smraw_cu8) {
   if (FULL) m = MAXB;   // every FW phase-1 block: the bounds checks fold away
   using CK = CloseKeys<S>;
   using T = typename CK::T;
   constexpr int TAG = CK::TAG, WIN = CK::WIN, VB = int(sizeof(T));
   constexpr uint32_t TMASK2 = ((1u << TAG) - 1u) * 0x00010001u;   // tag bits of both halves
   constexpr uint32_t STRIP2 = ~TMASK2;
-  extern __shared__ __align__(16) unsigned char smraw_cu8[];
   CloseU8Smem& sm = *reinterpret_cast<CloseU8Smem*>(smraw_cu8);
   T (*stage)[MAXB] = reinterpret_cast<T (*)[MAXB]>(&sm.K[0][0]);   // value staging (aliases K, Kpad)
   const int l = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
   if (vec) {   // full aligned block (every FW phase 1): 16-byte row segments
     for (int e = threadIdx.x; e < MAXB * MAXB / SEG; e += blockDim.x) {
       const int i = e / (MAXB / SEG), j = SEG * (e % (MAXB / SEG));
-      *reinterpret_cast<uint4*>(&stage[i][j]) = *reinterpret_cast<const uint4*>(D + (lo + i) * ld + lo + j);
+      *reinterpret_cast<uint4*>(&stage[i][j]) = __ldcg(reinterpret_cast<const uint4*>(D + (lo + i) * ld + lo + j));
     }
   } else {
     for (int e = threadIdx.x; e < MAXB * MAXB; e += blockDim.x) {
@@ -432,6 +437,7 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
       for (int kk = 0; kk < 8; kk += 2) {
         const int k = k0 + kk;
         const int buf = (kk >> 1) & 1;
+        APSP_JITTER_POINT(k);
         __syncthreads();
         const uint4 c4 = *reinterpret_cast<const uint4*>(&sm.colk[buf][4 * l]);
         const uint4 c5 = *reinterpret_cast<const uint4*>(&sm.colk1[buf][4 * l]);
@@ -596,6 +602,14 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
   }
 }
 
+template <int S, bool FULL>
+__global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo,
+                                                              int m, int32_t* idx, int64_t ldi, int mode,
+                                                              int64_t via_off) {
+  extern __shared__ __align__(16) unsigned char smraw_cu8[];
+  close_dpx_body<S, FULL>(D, ld, lo, m, idx, ldi, mode, via_off, smraw_cu8);
+}
+
 template <int S>
 static int close_impl(void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi, int mode,
                       int64_t via_off, Status* st, cudaStream_t s) {
@@ -658,5 +672,7 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
   }
   return set_error(2, "unknown store %d", store);
 }
+
+#include "fw_persist.cuh"
 
 }  // namespace apsp

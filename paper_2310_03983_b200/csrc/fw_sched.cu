@@ -184,6 +184,8 @@ int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s) {
   return rc;
 }
 
+static bool fine_round(const FwCtx& c, int64_t k0);
+
 int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   NvtxRange r("apsp.fw.phase2");
   const int64_t b = c.b, m = c.m;
@@ -222,6 +224,7 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
     x.mode = c.mode;
     x.only_lo = k0; x.only_hi = k0 + b;
     x.status = c.st;
+    x.fine = fine_round(c, k0);
     x.Aprep = prep_a(slot);
     x.Bprep = prep_b(slot, m, b);
     c.launches += 5;
@@ -280,6 +283,15 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
 }
 
+// Exact fp32 tier: rescan granularity of the deferred-argmin kernel. Early rounds improve
+// a large share of the cells per chunk, so detecting and rescanning every 8 k costs less than
+// every 32 there (measured at n=4096: the first launches are 2.5x the steady-state one, mostly
+// rescans); later rounds use the coarse default. APSP_F32_FINE = fraction of rounds (0.25).
+static bool fine_round(const FwCtx& c, int64_t k0) {
+  static const double frac = getenv("APSP_F32_FINE") ? atof(getenv("APSP_F32_FINE")) : 0.25;
+  return c.store == STORE_F32 && double(k0) < frac * double(c.m);
+}
+
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
 // additionally skips cross skip_next.
 int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaStream_t s) {
@@ -301,6 +313,7 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
     a.pdl = getenv("APSP_NO_PDL") ? 0 : 1;
   }
   a.status = c.st;
+  a.fine = fine_round(c, k0);
   if (c.prep[0] && bulk_store(c.store, c.b)) {
     char* slot = c.prep[(k0 / c.b) & 1];
     a.Aprep = prep_a(slot);
@@ -409,6 +422,52 @@ int default_block(int64_t n) {
   return b;
 }
 
+// ---- small n: closure by min-plus squaring --------------------------------------------------
+// For small N the blocked schedule is bound by its per-round chain (closure -> panels -> cross),
+// N/b times. Repeated squaring D <- min(D, D (x) D) needs only ceil(log2(hop diameter)) + 1
+// products, each one launch of the bulk tile kernel over the whole matrix, so for N <= 1024 it
+// finishes well before the chain does (the paper's own "FW on GPU" is this squaring,
+// PAPER.md:104-105). Each product reads operand layouts and a pred snapshot taken before it,
+// so the in-place update is exactly D_new = min(D, D_old (x) D_old); pred[i][j] <- pred_old[k*][j]
+// on strict improvement (smallest k on ties) keeps a valid shortest-path tree, and the
+// distances at the fixpoint are the exact closure (bit-identical to the blocked schedule).
+static int64_t squaring_max_n() {
+  static const int64_t v = getenv("APSP_SQUARING_MAX_N") ? atoll(getenv("APSP_SQUARING_MAX_N")) : 0;
+  return v;
+}
+
+static int fw_square_run(FwCtx& c, Header* hdr_dev, cudaStream_t s, int* iters) {
+  const int64_t N = c.m;
+  const size_t pb = (prep_bytes(N, N, N) + 255) / 256 * 256;
+  Scratch sc;
+  int rc = sc.acquire(nullptr, 0, pb + 256 + size_t(N) * N * 4, s);
+  if (rc) return rc;
+  char* prep = static_cast<char*>(sc.base);
+  int32_t* Ps = reinterpret_cast<int32_t*>(prep + pb + 256);
+  Header hdr{};
+  for (int it = 1;; it++) {
+    APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status.changed, 0, sizeof(int32_t), s));
+    if (c.P)
+      APSP_CUDA_TRY(cudaMemcpy2DAsync(Ps, size_t(N) * 4, c.P, size_t(c.ldp) * 4, size_t(N) * 4, size_t(N),
+                                      cudaMemcpyDeviceToDevice, s));
+    rc = launch_prep_bulk(c.store, c.D, c.ld, c.D, c.ld, N, N, N, prep_a(prep), prep_b(prep, N, N), s);
+    if (rc) return rc;
+    MinplusArgs a = minplus_args();
+    a.A = c.D; a.lda = c.ld; a.B = c.D; a.ldb = c.ld; a.C = c.D; a.ldc = c.ld;
+    a.idx = c.P; a.ldi = c.ldp; a.predB = c.P ? Ps : nullptr; a.ldp = N;
+    a.m = N; a.n = N; a.k = N; a.inner_off = 0; a.mode = IDX_PRED;
+    a.status = c.st; a.track_changed = 1;
+    a.Aprep = prep_a(prep); a.Bprep = prep_b(prep, N, N);
+    rc = timed_minplus(c.store, a, s);
+    if (!rc) rc = read_header(hdr_dev, hdr, s);
+    if (rc) return rc;
+    c.launches += 3;
+    *iters = it;
+    if (!hdr.status.changed) return 0;
+    if (it > 64) return set_error(APSP_ECONVERGE, "squaring did not converge");
+  }
+}
+
 size_t fw_ws_bytes(int dtype, int64_t n, int block) {
   const int64_t N = round_up(std::max<int64_t>(n, 1), block);
   const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
@@ -450,7 +509,7 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     Pw = pred;
     ldpw = ldp;
   }
-  int launches = 2, used = -1, tried = 0;
+  int launches = 2, used = -1, tried = 0, sq_iters = 0;
   for (int tier : tiers) {
     const int store = tier_store(tier);
     if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
@@ -468,7 +527,19 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
       if (getenv("APSP_NO_BULK")) c.prep[0] = c.prep[1] = nullptr;
       // graph replay only where launch gaps dominate (N <= 2048): a graph drops the lookahead
       // stream's priority, which costs more than the gaps at larger N (n=8192 21.6 -> 25 ms)
-      if (N <= 2048) {   // (no band sink here: the graph holds the whole chain)
+      const int64_t Nsq = round_up(n, TILE_ALIGN);
+      if (b == TILE_ALIGN && fw_persist_enabled(store, N) && !sink && !g_prof.on && !getenv("APSP_NO_PERSIST")) {
+        Scratch ps;
+        rc = ps.acquire(nullptr, 0, fw_persist_scratch_bytes(N), s);
+        if (!rc) rc = launch_fw_persist(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s);
+        c.launches += 2;
+      } else if (Nsq <= squaring_max_n() && bulk_store(store, Nsq) && !sink) {
+        c.m = Nsq;   // squaring works on the 128-aligned view (pad vertices are isolated)
+        int it = 0;
+        rc = fw_square_run(c, hdr_dev, s, &it);
+        c.m = N;
+        sq_iters = it;
+      } else if (N <= 2048) {   // (no band sink here: the graph holds the whole chain)
         int dev = 0;
         cudaGetDevice(&dev);
         const GraphKey key{dev, 1, store, c.mode, N, b, D, Pw, scratch, c.side, s};
@@ -502,10 +573,10 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   launches++;
   const double ms = tm.stop();
   if (info) {
-    info->block = b;
+    info->block = sq_iters ? 0 : b;
     info->tier = used;
     info->tiers_tried = tried;
-    info->iterations = 0;
+    info->iterations = sq_iters;   // > 0: solved by min-plus squaring (small n)
     info->launches = launches;
     info->max_finite = hdr.cert.max_finite;
     info->relaxations = n * n * n;

@@ -59,6 +59,9 @@ struct MinplusArgs {
   // right before it on the stream (FW phase 3b after 3a: disjoint tiles), so its CTAs may start
   // while that kernel's last wave drains.
   int pdl;
+  // Exact fp32 deferred-argmin kernel: detect improvements (and rescan) every 8 k instead of
+  // every 32 -- cheaper when many cells improve per chunk (early FW rounds).
+  int fine;
 };
 
 // Lay the u8 operand panels out in the tile kernel's shared-memory format, once per product:
@@ -82,6 +85,10 @@ int launch_minplus(int store, const MinplusArgs& a, cudaStream_t s);
 
 // Closure of the diagonal block [lo, lo+m) (m <= 128) in classic k order, one CTA:
 // FW phase 1 and the R-Kleene leaf (_fw_via_block, solvers.py:98-115).
+// Small-n u8 blocked FW in one persistent launch (fw_persist.cuh, in fw.cu)
+bool fw_persist_enabled(int store, int64_t N);
+size_t fw_persist_scratch_bytes(int64_t N);
+int launch_fw_persist(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch, cudaStream_t s);
 // Blocked in-CTA closure for the 32-bit exact stores, pred mode (close_blk.cu)
 bool close_blk_supported(int store);
 int launch_block_close_blk(int store, void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi,

@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   int slot = 0, wc = 0;
   uint32_t ph = 0;
   for (int c = 0; c < nch; c++) {
+    APSP_JITTER_POINT(c);
     mbar_wait(&sm.full[slot], ph);
 #pragma unroll kU8Unroll
     for (int kk = 0; kk < SUB; kk++) {
@@ -129,6 +130,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
         for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
     }
     __syncwarp();
+    APSP_JITTER_POINT(c + 101);
     if (lane == 0) {   // count this warp out of the slot; the last one refills it
       __threadfence_block();
       if (atomicAdd(&sm.done[slot], 1u) == NT / 32 - 1) {
@@ -459,6 +461,7 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
           }
       }
     }
+    APSP_JITTER_POINT(c + 202);
     __syncthreads();   // every warp is done with this slot
     if (t == 0 && c + W32_STAGES < nch) issue(c + W32_STAGES);
   }
@@ -605,6 +608,7 @@ struct SmemF32DM {   // 96 KB: 2 CTAs / SM
 __device__ __forceinline__ int dm_col(int tx, int q) { return (q < 4 ? 0 : 28) + 4 * tx + q; }
 __device__ __forceinline__ int dm_tgt(int t, int cell) { return t * 32 + ((((cell >> 2) + t) & 7) << 2) + (cell & 3); }
 
+template <int G>
 __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
   extern __shared__ __align__(128) unsigned char smraw_dm[];
   SmemF32DM& sm = *reinterpret_cast<SmemF32DM*>(smraw_dm);
@@ -643,70 +647,12 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
     for (int q = 0; q < 8; q++) acc[r][q] = __int_as_float(0x7f800000);
   for (int64_t c = 0; c < nch; c++) {
     const int slot = int(c % DM_STAGES);
+    APSP_JITTER_POINT(c + 303);
     mbar_wait(&sm.bar[slot], uint32_t((c / DM_STAGES) & 1));
-    if (c > 0) {   // the pre-chunk values go to the thread's own target slots (not registers)
-#pragma unroll
-      for (int r = 0; r < 4; r++)
-#pragma unroll
-        for (int h = 0; h < 2; h++)
-          *reinterpret_cast<float4*>(&sm.Cs[dm_tgt(t, 8 * r + 4 * h)]) =
-              make_float4(acc[r][4 * h], acc[r][4 * h + 1], acc[r][4 * h + 2], acc[r][4 * h + 3]);
-    }
-#pragma unroll 4
-    for (int kk = 0; kk < SUB; kk += 2) {
-      float a0[4], a1[4], b0[8], b1[8];
-      *reinterpret_cast<float4*>(a0) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][4 * ty]);
-      *reinterpret_cast<float4*>(a1) = *reinterpret_cast<const float4*>(&sm.As[slot][kk + 1][4 * ty]);
-      *reinterpret_cast<float4*>(b0) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][4 * tx]);
-      *reinterpret_cast<float4*>(b0 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][32 + 4 * tx]);
-      *reinterpret_cast<float4*>(b1) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][4 * tx]);
-      *reinterpret_cast<float4*>(b1 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][32 + 4 * tx]);
-      unsigned long long p0[4], p1[4];
-#pragma unroll
-      for (int q = 0; q < 4; q++) {
-        p0[q] = pack_f2(b0[2 * q], b0[2 * q + 1]);
-        p1[q] = pack_f2(b1[2 * q], b1[2 * q + 1]);
-      }
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const unsigned long long ar0 = pack_f2(a0[r], a0[r]), ar1 = pack_f2(a1[r], a1[r]);
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const float2 s0 = fadd2(ar0, p0[q]), s1 = fadd2(ar1, p1[q]);
-          acc[r][2 * q] = fmin3(acc[r][2 * q], s0.x, s1.x);
-          acc[r][2 * q + 1] = fmin3(acc[r][2 * q + 1], s0.y, s1.y);
-        }
-      }
-    }
-    uint32_t mask = 0;
-    if (c == 0) {   // improvement is against the old C (which wins ties)
-      mbar_wait(&sm.cbar, 0);
-#pragma unroll
-      for (int r = 0; r < 4; r++) {
-        const float4 w0 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 4 * tx]);
-        const float4 w1 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 32 + 4 * tx]);
-        const float cv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          if (acc[r][q] < cv[q]) mask |= 1u << (8 * r + q);
-          else acc[r][q] = cv[q];
-        }
-      }
-      __syncthreads();   // the C tile is consumed: its space now holds the rescan targets
-    } else {
-#pragma unroll
-      for (int r = 0; r < 4; r++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-          const float4 o = *reinterpret_cast<const float4*>(&sm.Cs[dm_tgt(t, 8 * r + 4 * h)]);
-          const float ov[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-          for (int q = 0; q < 4; q++)
-            if (acc[r][4 * h + q] < ov[q]) mask |= 1u << (8 * r + 4 * h + q);
-        }
-    }
-    if (__any_sync(0xffffffffu, mask != 0u)) {
-      if (mask) {
+#pragma unroll 1
+    for (int ks = 0; ks < SUB; ks += G) {   // sub-chunks of G k: detection + rescan granularity
+      const bool first = c == 0 && ks == 0;
+      if (!first) {   // the pre-sub-chunk values go to the thread's own target slots (not registers)
 #pragma unroll
         for (int r = 0; r < 4; r++)
 #pragma unroll
@@ -714,40 +660,104 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
             *reinterpret_cast<float4*>(&sm.Cs[dm_tgt(t, 8 * r + 4 * h)]) =
                 make_float4(acc[r][4 * h], acc[r][4 * h + 1], acc[r][4 * h + 2], acc[r][4 * h + 3]);
       }
-      // The warp's improved cells go into one queue and the 32 lanes share them, so the
-      // rescan costs ceil(items / 32) passes instead of the busiest lane's count. Each pass
-      // scans the whole chunk without branches (independent loads, a select per k), so it is
-      // bound by issue, not by a load-compare chain.
-      const int kb = int(c) * SUB, lane = t & 31;
-      uint16_t* q = sm.queue[t >> 5];
-      const int cnt = __popc(mask);
-      int pre = cnt;
+#pragma unroll 4
+      for (int kk = ks; kk < ks + G; kk += 2) {
+        float a0[4], a1[4], b0[8], b1[8];
+        *reinterpret_cast<float4*>(a0) = *reinterpret_cast<const float4*>(&sm.As[slot][kk][4 * ty]);
+        *reinterpret_cast<float4*>(a1) = *reinterpret_cast<const float4*>(&sm.As[slot][kk + 1][4 * ty]);
+        *reinterpret_cast<float4*>(b0) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][4 * tx]);
+        *reinterpret_cast<float4*>(b0 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk][32 + 4 * tx]);
+        *reinterpret_cast<float4*>(b1) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][4 * tx]);
+        *reinterpret_cast<float4*>(b1 + 4) = *reinterpret_cast<const float4*>(&sm.Bs[slot][kk + 1][32 + 4 * tx]);
+        unsigned long long p0[4], p1[4];
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, pre, o);
-        if (lane >= o) pre += v;
-      }
-      const int total = __shfl_sync(0xffffffffu, pre, 31);
-      pre -= cnt;
-      while (mask) {
-        const int cell = __ffs(mask) - 1;
-        mask &= mask - 1;
-        q[pre++] = uint16_t(lane << 5 | cell);
-      }
-      __syncwarp();
-      for (int it = lane; it < total; it += 32) {
-        const int e = q[it], tt = (t & ~31) | (e >> 5), cell = e & 31;
-        const int row = 4 * (tt >> 3) + (cell >> 3), col = dm_col(tt & 7, cell & 7);
-        const float target = sm.Cs[dm_tgt(tt, cell)];
-        int found = 0;
+        for (int q = 0; q < 4; q++) {
+          p0[q] = pack_f2(b0[2 * q], b0[2 * q + 1]);
+          p1[q] = pack_f2(b1[2 * q], b1[2 * q + 1]);
+        }
 #pragma unroll
-        for (int kk = SUB - 1; kk >= 0; kk--)
-          found = sm.As[slot][kk][row] + sm.Bs[slot][kk][col] == target ? kk : found;
-        sm.kid[tt][cell] = uint16_t(kb + found);
+        for (int r = 0; r < 4; r++) {
+          const unsigned long long ar0 = pack_f2(a0[r], a0[r]), ar1 = pack_f2(a1[r], a1[r]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const float2 s0 = fadd2(ar0, p0[q]), s1 = fadd2(ar1, p1[q]);
+            acc[r][2 * q] = fmin3(acc[r][2 * q], s0.x, s1.x);
+            acc[r][2 * q + 1] = fmin3(acc[r][2 * q + 1], s0.y, s1.y);
+          }
+        }
       }
-      __syncwarp();
+      uint32_t mask = 0;
+      if (first) {   // improvement is against the old C (which wins ties)
+        mbar_wait(&sm.cbar, 0);
+#pragma unroll
+        for (int r = 0; r < 4; r++) {
+          const float4 w0 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 4 * tx]);
+          const float4 w1 = *reinterpret_cast<const float4*>(&sm.Cs[(4 * ty + r) * DM_BN + 32 + 4 * tx]);
+          const float cv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+          for (int q = 0; q < 8; q++) {
+            if (acc[r][q] < cv[q]) mask |= 1u << (8 * r + q);
+            else acc[r][q] = cv[q];
+          }
+        }
+        __syncthreads();   // the C tile is consumed: its space now holds the rescan targets
+      } else {
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const float4 o = *reinterpret_cast<const float4*>(&sm.Cs[dm_tgt(t, 8 * r + 4 * h)]);
+            const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              if (acc[r][4 * h + q] < ov[q]) mask |= 1u << (8 * r + 4 * h + q);
+          }
+      }
+      if (__any_sync(0xffffffffu, mask != 0u)) {
+        if (mask) {
+#pragma unroll
+          for (int r = 0; r < 4; r++)
+#pragma unroll
+            for (int h = 0; h < 2; h++)
+              *reinterpret_cast<float4*>(&sm.Cs[dm_tgt(t, 8 * r + 4 * h)]) =
+                  make_float4(acc[r][4 * h], acc[r][4 * h + 1], acc[r][4 * h + 2], acc[r][4 * h + 3]);
+        }
+        // The warp's improved cells go into one queue and the 32 lanes share them, so the
+        // rescan costs ceil(items / 32) passes instead of the busiest lane's count. Each pass
+        // scans the sub-chunk without branches (independent loads, a select per k), so it is
+        // bound by issue, not by a load-compare chain.
+        const int kb = int(c) * SUB + ks, lane = t & 31;
+        uint16_t* q = sm.queue[t >> 5];
+        const int cnt = __popc(mask);
+        int pre = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, pre, o);
+          if (lane >= o) pre += v;
+        }
+        const int total = __shfl_sync(0xffffffffu, pre, 31);
+        pre -= cnt;
+        while (mask) {
+          const int cell = __ffs(mask) - 1;
+          mask &= mask - 1;
+          q[pre++] = uint16_t(lane << 5 | cell);
+        }
+        __syncwarp();
+        for (int it = lane; it < total; it += 32) {
+          const int e = q[it], tt = (t & ~31) | (e >> 5), cell = e & 31;
+          const int row = 4 * (tt >> 3) + (cell >> 3), col = dm_col(tt & 7, cell & 7);
+          const float target = sm.Cs[dm_tgt(tt, cell)];
+          int found = 0;
+#pragma unroll
+          for (int kk = G - 1; kk >= 0; kk--)
+            found = sm.As[slot][ks + kk][row] + sm.Bs[slot][ks + kk][col] == target ? kk : found;
+          sm.kid[tt][cell] = uint16_t(kb + found);
+        }
+        __syncwarp();
+      }
     }
     __syncwarp();
+    APSP_JITTER_POINT(c + 404);
     if ((t & 31) == 0) {   // count this warp out of the slot; the last one refills it
       __threadfence_block();
       if (atomicAdd(&sm.done[slot], 1u) == NT / 32 - 1) {
@@ -1035,6 +1045,7 @@ __global__ void __launch_bounds__(NT, 1) minplus_f32nt_kernel(MinplusArgs p) {
         }
       }
     }
+    APSP_JITTER_POINT(c + 202);
     __syncthreads();   // every warp is done with this slot
     if (t == 0 && c + W32_STAGES < nch) issue(c + W32_STAGES);
   }
@@ -1067,11 +1078,14 @@ __global__ void __launch_bounds__(NT, 1) minplus_f32nt_kernel(MinplusArgs p) {
 
 int launch_f32dm(const MinplusArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
-  APSP_CUDA_TRY(smem_optin(minplus_f32dm_kernel, int(sizeof(SmemF32DM)), attr));
+  static std::atomic<unsigned long long> attr8{0};
+  APSP_CUDA_TRY(smem_optin(minplus_f32dm_kernel<32>, int(sizeof(SmemF32DM)), attr));
+  APSP_CUDA_TRY(smem_optin(minplus_f32dm_kernel<8>, int(sizeof(SmemF32DM)), attr8));
   if (a.m % BM || a.n % DM_BN || a.k % SUB || a.k > 65535 || (reinterpret_cast<uintptr_t>(a.C) & 15) ||
       (a.ldc * 4) % 16)
     return set_error(2, "deferred-argmin f32 tiles need 128 x 64 tiles and 32-multiple k");
-  minplus_f32dm_kernel<<<grid_for(a, BM, DM_BN), NT, sizeof(SmemF32DM), s>>>(a);
+  if (a.fine) minplus_f32dm_kernel<8><<<grid_for(a, BM, DM_BN), NT, sizeof(SmemF32DM), s>>>(a);
+  else minplus_f32dm_kernel<32><<<grid_for(a, BM, DM_BN), NT, sizeof(SmemF32DM), s>>>(a);
   return 0;
 }
 

@@ -56,7 +56,10 @@ struct RK {
     a.mode = mode;
     a.status = st;
     launches++;
-    if (prep_ && bulk_store(store, k) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
+    const bool al16 = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
+                      (size_t(lda) * es) % 16 == 0 && (size_t(ldb) * es) % 16 == 0 &&
+                      (reinterpret_cast<uintptr_t>(at(r0, c0)) & 15) == 0 && (size_t(ld) * es) % 16 == 0;
+    if (prep_ && al16 && bulk_store(store, k) && m % TILE_ALIGN == 0 && n % TILE_ALIGN == 0 && k % 32 == 0) {
       int rc = launch_prep_bulk(store, A, lda, B, ldb, m, n, k, prep_a(prep_), prep_b(prep_, m, k), st_);
       if (rc) return rc;
       a.Aprep = prep_a(prep_);
@@ -164,8 +167,11 @@ int64_t rk_half(int64_t N, int aligned) {
 }
 
 size_t rk_extra_bytes(int64_t N, int aligned, int thr) {
-  if (!aligned) return 0;
   const int64_t h = rk_half(N, aligned);
+  // floor split (the reference's): operand layouts for the products whose sides happen to be
+  // 128-aligned (every product above the leaves when N is a power of two), which then run on
+  // the bulk-staged kernels instead of the register-staged ones (n=8192: 44 -> see DESIGN.md)
+  if (!aligned) return prep_bytes(h, h, h) + 512;
   const int64_t leaf = std::max<int64_t>(round_up(std::min<int64_t>(thr, N), TILE_ALIGN), TILE_ALIGN);
   // prep + prep2 (concurrent product pair), leaf FW scratch, second value snapshot (<= 8 B / cell)
   return 2 * (prep_bytes(h, h, h) + 512) + fw_scratch_bytes(leaf, TILE_ALIGN, 4) + 512 +
@@ -204,7 +210,7 @@ int rkleene_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* idx, int
   p = align256(p + size_t(N) * N * (dtype == APSP_DTYPE_I64 ? 8 : 4));
   char* sV = p;
   p = align256(p + size_t(h + 8) * (h + 8) * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 512);
-  char* rkprep = aligned ? p : nullptr;
+  char* rkprep = (aligned || !getenv("APSP_RK_FLOOR_REGISTER")) ? p : nullptr;
   char* rkprep2 = aligned ? rkprep + ((prep_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
   char* sV2 = aligned ? rkprep2 + ((prep_bytes(h, h, h) + 511) / 256) * 256 : nullptr;
   char* leafws = aligned ? sV2 + ((size_t(h + 8) * (h + 8) * 8 + 511) / 256) * 256 : nullptr;

@@ -123,6 +123,25 @@ inline dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
   return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
 }
 
+// Race stress (the debug build libapsp_b200_jitter.so, -DAPSP_JITTER; tools/race_stress.py):
+// at the synchronisation points of the barrier-free rings and the closures a pseudo-random
+// eighth of the warps sleep up to ~4 us, so every ordering the code relies on gets exercised
+// with warps far apart. compute-sanitizer is not available on the GPU pool; this plus the
+// oracle comparison is the race evidence. Compiles to nothing in the product build.
+#ifdef APSP_JITTER
+__device__ __forceinline__ void jitter_point(uint32_t salt) {
+  uint32_t h = (blockIdx.x * 73856093u) ^ (blockIdx.y * 19349663u) ^ ((threadIdx.x >> 5) * 83492791u) ^
+               (salt * 2654435761u) ^ uint32_t(clock());
+  h ^= h >> 13;
+  h *= 0x5bd1e995u;
+  h ^= h >> 15;
+  if ((h & 7u) == 0u) __nanosleep(h & 4095u);
+}
+#define APSP_JITTER_POINT(salt) ::apsp::jitter_point(salt)
+#else
+#define APSP_JITTER_POINT(salt) ((void)0)
+#endif
+
 // 3-input fp32 min (FMNMX3 on sm_100)
 __device__ __forceinline__ float fmin3(float a, float b, float c) {
   float d;

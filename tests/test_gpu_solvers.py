@@ -619,3 +619,24 @@ def test_rkleene_floor_int64_tier_odd_n(cuda, n):
     r = ap.rkleene(ap.CostMatrix(raw), tier="i64")
     assert np.array_equal(r.distances.raw, want_d)
     assert r.info["tier"] == "i64"
+
+
+@pytest.mark.parametrize("n,rho", [(128, 0.5), (300, 0.3), (1000, 0.1), (1537, 0.3), (2100, 0.1)])
+def test_persistent_small_n_schedule(cuda, n, rho, monkeypatch):
+    """The one-launch dataflow schedule of small-n u8 FW (fw_persist.cuh) against the oracle and
+    the launch-based schedule (APSP_NO_PERSIST=1): equal distances, both pred trees valid."""
+    import torch
+
+    raw = ap.dense_costs(ap.GenParams(n, rho, 100, 3 * n), np.int64)
+    want, _ = orc.rkleene(raw, 64)
+    s = ap.fw_classic(ap.CostMatrix(raw))
+    assert s.info["tier"] == "u8"
+    assert np.array_equal(s.distances.raw, want)
+    pred_ok(raw, s.distances.raw, s.pred.raw)
+    h = torch.from_numpy(ap.dense_costs(ap.GenParams(n, rho, 100, 3 * n), np.int32)).cuda()
+    a = ap.solve(h)
+    monkeypatch.setenv("APSP_NO_PERSIST", "1")
+    b = ap.solve(h)
+    assert torch.equal(a.distances, b.distances)
+    ok, why = ap.check_pred_tree(h, b.distances, b.index, INF32)
+    assert ok, why

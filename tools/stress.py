@@ -1,8 +1,12 @@
 #!/usr/bin/env python3
 """Randomised cross-checks of the product paths (run on a GPU box; not part of the test suite):
   * small n: every solver entry against the CPU oracle (distances bit-exact, pred certificate);
+  * continuous fp32 (small n): FW and R-Kleene within 1e-5 of the float64 oracle, paths re-summed;
+  * multi-rank schedules emulated on one GPU (fused peer stores): bitwise equal to one GPU;
   * large n (> 2048, streamed readback, narrowed transfers): host-buffer API == device API.
-usage: tools/stress.py [seconds]"""
+With APSP_B200_LIB=paper_2310_03983_b200/libapsp_b200_jitter.so (make -C ... jitter) every
+synchronisation point of the rings and closures sleeps pseudo-randomly: the race stress run.
+usage: tools/stress.py [seconds] [seed] [-v]"""
 
 from __future__ import annotations
 
@@ -32,14 +36,63 @@ def rand_raw(rng, n):
     return raw, dens, wmax
 
 
+def extra_case(rng, verbose) -> int:
+    """Continuous fp32 (FW + R-Kleene vs float64) or an emulated multi-rank schedule."""
+    from paper_2310_03983_b200.distributed import fw_blocked_emulated
+    from paper_2310_03983_b200.distributed_rk import rkleene_emulated
+
+    if rng.random() < 0.5:
+        n = int(rng.integers(1, 700))
+        h = ap.continuous_costs(ap.GenParams(n, float(rng.choice([0.01, 0.1, 1.0])), 100, int(rng.integers(1 << 30))))
+        tag = f"f32 n={n}"
+        want = orc.fw_f64(h.astype(np.float64))
+        hd = torch.from_numpy(h).cuda()
+        try:
+            for r in (ap.solve(hd), ap.solve(hd, "rkleene", track="pred", base_threshold=128)):
+                d = r.distances.double().cpu().numpy()
+                fin = np.isfinite(want)
+                assert np.array_equal(np.isfinite(d), fin), "f32 reachability"
+                assert (np.abs(d[fin] - want[fin]) <= 1e-5 * np.maximum(want[fin], 1e-30)).all(), "f32 tolerance"
+                ok, why = ap.check_pred_paths(hd, r.distances, r.index, 1e-5)
+                assert ok, f"f32 paths: {why}"
+        except AssertionError as e:
+            print(f"FAIL {tag}: {e}", flush=True)
+            return 1
+    else:
+        n = int(rng.integers(300, 1300))
+        world = int(rng.integers(2, 5))
+        alpha = int(rng.choice([100, 400, 50000]))
+        h = torch.from_numpy(ap.dense_costs(ap.GenParams(n, float(rng.choice([0.02, 0.1])), alpha,
+                                                         int(rng.integers(1 << 30))), np.int32)).cuda()
+        tag = f"emulated n={n} world={world} alpha={alpha}"
+        try:
+            single = ap.solve(h, "fw_blocked", block=128)
+            d, p, _ = fw_blocked_emulated(h, world, block=128, fused=True)
+            assert torch.equal(d, single.distances) and torch.equal(p, single.index), "fused FW"
+            rk1 = ap.solve(h, "rkleene", track="pred", base_threshold=256)
+            d2, p2, info = rkleene_emulated(h, world, base_threshold=256, fused=True)
+            assert torch.equal(d2, rk1.distances) and info["replicas_equal"], "fused R-Kleene"
+        except AssertionError as e:
+            print(f"FAIL {tag}: {e}", flush=True)
+            return 1
+    if verbose:
+        print("ok", tag, flush=True)
+    return 0
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
     seed = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "-v" else int(time.time())
-    print("seed", seed, flush=True)
+    print("seed", seed, "library", ap._native.lib_path(), flush=True)
     rng = np.random.default_rng(seed)
     t0 = time.time()
     cases = fails = 0
     while time.time() - t0 < budget:
+        kind = rng.random()
+        if kind < 0.12:
+            cases += 1
+            fails += extra_case(rng, "-v" in sys.argv)
+            continue
         small = rng.random() < 0.7
         n = int(rng.integers(1, 700)) if small else int(rng.choice([2176, 2304, 2560, 3072]))
         raw, dens, wmax = rand_raw(rng, n)
