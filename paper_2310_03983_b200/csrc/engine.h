@@ -124,7 +124,9 @@ struct FwCtx {
   int32_t* predsnap = nullptr;   // b x m
   char* rowsnap = nullptr;       // b x m values (b > 128 only)
   char* colsnap = nullptr;       // m x b values (b > 128 only)
-  char* prep[2] = {nullptr, nullptr};  // narrow tiers: bulk-copy layouts of the panels, by round parity
+  char* prep[3] = {nullptr, nullptr, nullptr};  // bulk tiers: layouts of the panels, by round mod 3
+  int32_t* predsnap3[3] = {nullptr, nullptr, nullptr};  // pivot-row pred after phase 2, by round mod 3
+  bool deep = false;             // two-deep lookahead (the next cross on the side stream)
   char* p2prep = nullptr;        // narrow tiers: bulk-copy layouts of the phase-2 operands
   char* sub = nullptr;           // scratch of the phase-1 sub-run when b > 128
   int launches = 0;

@@ -15,7 +15,8 @@ namespace apsp {
 size_t fw_scratch_bytes(int64_t m, int b, size_t es) {
   size_t v = size_t(b) * m * 4 + 256;                      // pred row-panel snapshot
   if (b > TILE_ALIGN) v += 2 * size_t(b) * m * es + 256;   // value snapshots (non-narrow tiers)
-  v += 2 * (prep_bytes(m, m, b) + 256);                 // phase-3 panel layouts (double buffered)
+  v += 3 * (prep_bytes(m, m, b) + 256);                 // phase-3 panel layouts (by round mod 3)
+  v += 3 * (size_t(b) * m * 4 + 256);                   // phase-3 pivot-row pred snapshots (mod 3)
   v += prep_bytes(m, b, b) + 256;                       // phase-2 layouts (max of row/col product)
   if (b > TILE_ALIGN) v += fw_scratch_bytes(b, TILE_ALIGN, es) + 256;   // phase-1 sub-run
   return v;
@@ -31,9 +32,13 @@ void fw_carve(FwCtx& c, char* scratch, int64_t N) {
     c.colsnap = p + size_t(c.b) * N * c.es + 128;
     p += 2 * size_t(c.b) * N * c.es + 256;
   }
-  for (int q = 0; q < 2; q++) {
+  for (int q = 0; q < 3; q++) {
     c.prep[q] = p;
     p += prep_bytes(N, N, c.b) + 256;
+  }
+  for (int q = 0; q < 3; q++) {
+    c.predsnap3[q] = reinterpret_cast<int32_t*>(p);
+    p += size_t(c.b) * N * 4 + 256;
   }
   c.p2prep = p;
   p += prep_bytes(N, c.b, c.b) + 256;
@@ -176,7 +181,8 @@ int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s) {
   sub.side = nullptr;
   sub.sink = nullptr;   // the sub-run's last round is not the solve's
   sub.rowsnap = sub.colsnap = nullptr;
-  sub.prep[0] = sub.prep[1] = sub.p2prep = sub.sub = nullptr;
+  sub.prep[0] = sub.prep[1] = sub.prep[2] = sub.p2prep = sub.sub = nullptr;
+  sub.deep = false;
   if (c.sub) fw_carve(sub, c.sub, c.b);
   sub.launches = 0;
   const int rc = fw_run(sub, s);
@@ -209,7 +215,7 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
     // layouts live in this round's phase-3 slot (free: its last reader, phase 3 two rounds
     // back, is ordered before us) and are rebuilt from the updated panels right after.
     // the pred snapshot of the pivot rows rides along as the prep launch's third part
-    char* slot = c.prep[(k0 / b) & 1];
+    char* slot = c.prep[(k0 / b) % 3];
     rc = launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s,
                           psnap ? c.P + k0 * c.ldp : nullptr, c.ldp, c.predsnap, m, m);
     if (rc) return rc;
@@ -230,7 +236,11 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
     c.launches += 5;
     rc = launch_minplus(c.store, x, s);
     if (rc) return rc;
-    return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
+    // the phase-3 layouts; with the two-deep lookahead also the pivot rows' final pred (the next
+    // cross, updated on the side stream while this round's phase 3 still gathers, writes them)
+    const int q3 = int((k0 / b) % 3);
+    return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s,
+                            c.deep && c.P ? c.P + k0 * c.ldp : nullptr, c.ldp, c.predsnap3[q3], m, m);
   }
   if (snap) {
     rc = launch_copy_block(c.store, rowp, c.ld, c.rowsnap, m, b, m, s);
@@ -278,23 +288,26 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
   c.launches += 2;
   rc = launch_minplus(c.store, q, s);
   if (rc || !c.prep[0] || !bulk_store(c.store, c.b)) return rc;
-  char* slot = c.prep[(k0 / b) & 1];
+  char* slot = c.prep[(k0 / b) % 3];
   c.launches += 2;
-  return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s);
+  const int q3 = int((k0 / b) % 3);
+  return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s,
+                          c.deep && c.P ? c.P + k0 * c.ldp : nullptr, c.ldp, c.predsnap3[q3], m, m);
 }
 
 // Exact fp32 tier: rescan granularity of the deferred-argmin kernel. Early rounds improve
 // a large share of the cells per chunk, so detecting and rescanning every 8 k costs less than
 // every 32 there (measured at n=4096: the first launches are 2.5x the steady-state one, mostly
-// rescans); later rounds use the coarse default. APSP_F32_FINE = fraction of rounds (0.25).
+// rescans); later rounds use the coarse default. APSP_F32_FINE = fraction of rounds (0.125).
 static bool fine_round(const FwCtx& c, int64_t k0) {
-  static const double frac = getenv("APSP_F32_FINE") ? atof(getenv("APSP_F32_FINE")) : 0.25;
+  static const double frac = getenv("APSP_F32_FINE") ? atof(getenv("APSP_F32_FINE")) : 0.125;
   return c.store == STORE_F32 && double(k0) < frac * double(c.m);
 }
 
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
 // additionally skips cross skip_next.
-int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaStream_t s) {
+int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaStream_t s, int64_t skip_next2 = -1,
+              bool pdl = true) {
   NvtxRange r(only_next >= 0 ? "apsp.fw.phase3a" : skip_next >= 0 ? "apsp.fw.phase3b" : "apsp.fw.phase3");
   MinplusArgs a = minplus_args();
   a.A = c.D + k0 * c.es; a.lda = c.ld;
@@ -302,6 +315,10 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   a.C = c.D; a.ldc = c.ld;
   a.idx = c.P; a.ldi = c.ldp;
   a.predB = c.P ? c.P + k0 * c.ldp : nullptr; a.ldp = c.ldp;
+  if (c.deep && c.P) {   // the pivot rows' pred as of the end of phase 2 (see fw_phase2)
+    a.predB = c.predsnap3[(k0 / c.b) % 3];
+    a.ldp = c.m;
+  }
   a.m = c.m; a.n = c.m; a.k = c.b;
   a.inner_off = c.via_off + k0;
   a.mode = c.mode;
@@ -310,12 +327,13 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   if (only_next >= 0) { a.only_lo = only_next; a.only_hi = only_next + c.b; }
   if (skip_next >= 0) {   // 3b: disjoint from the 3a launch queued just before it
     a.skip2_lo = skip_next; a.skip2_hi = skip_next + c.b;
-    a.pdl = getenv("APSP_NO_PDL") ? 0 : 1;
+    a.pdl = (pdl && !getenv("APSP_NO_PDL")) ? 1 : 0;
   }
+  if (skip_next2 >= 0) { a.skip3_lo = skip_next2; a.skip3_hi = skip_next2 + c.b; }
   a.status = c.st;
   a.fine = fine_round(c, k0);
   if (c.prep[0] && bulk_store(c.store, c.b)) {
-    char* slot = c.prep[(k0 / c.b) & 1];
+    char* slot = c.prep[(k0 / c.b) % 3];
     a.Aprep = prep_a(slot);
     a.Bprep = prep_b(slot, c.m, c.b);
   }
@@ -333,6 +351,10 @@ int fw_phase3_rows(FwCtx& c, int64_t k0, int64_t r0, int64_t r1, cudaStream_t s)
   a.C = c.D + r0 * c.ld * c.es; a.ldc = c.ld;
   a.idx = c.P ? c.P + r0 * c.ldp : nullptr; a.ldi = c.ldp;
   a.predB = c.P ? c.P + k0 * c.ldp : nullptr; a.ldp = c.ldp;
+  if (c.deep && c.P) {
+    a.predB = c.predsnap3[(k0 / c.b) % 3];
+    a.ldp = c.m;
+  }
   a.m = r1 - r0; a.n = c.m; a.k = c.b;
   a.inner_off = c.via_off + k0;
   a.mode = c.mode;
@@ -340,7 +362,7 @@ int fw_phase3_rows(FwCtx& c, int64_t k0, int64_t r0, int64_t r1, cudaStream_t s)
   a.skip_col_lo = k0; a.skip_col_hi = k0 + c.b;
   a.status = c.st;
   if (c.prep[0] && bulk_store(c.store, c.b)) {
-    char* slot = c.prep[(k0 / c.b) & 1];
+    char* slot = c.prep[(k0 / c.b) % 3];
     a.Aprep = prep_a(slot) + (r0 / TILE_ALIGN) * (c.b / 32) * (32 * TILE_ALIGN);   // the band's A tiles
     a.Bprep = prep_b(slot, c.m, c.b);
   }
@@ -348,8 +370,82 @@ int fw_phase3_rows(FwCtx& c, int64_t k0, int64_t r0, int64_t r1, cudaStream_t s)
   return timed_minplus(c.store, a, s);
 }
 
+// Two-deep lookahead (bulk tiers): round K's phase 3 is split into X(K) = the tiles of the cross
+// of K+1 (needed by the next closure), Y(K) = the tiles of the cross of K+2 outside it, and
+// Z(K) = the rest. The side stream runs the critical chain
+//     X(K+1) -> closure(K+2) -> panels(K+2)
+// as soon as Y(K) and panels(K+1) are done, while the main stream runs Y(K), Z(K), Y(K+1), ...
+// back to back: the next cross no longer sits between two rest launches. Every launch reads
+// its panels from layouts / pred snapshots taken at the end of its round's phase 2 (round mod 3
+// buffers), so the side stream's writes to the pivot rows of later rounds never race with them.
+static int fw_run_deep(FwCtx& c, cudaStream_t s) {
+  const int64_t b = c.b, m = c.m;
+  cudaEvent_t ev[5] = {};
+  for (auto& e : ev)
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      for (auto& f : ev)
+        if (f) cudaEventDestroy(f);
+      return set_error(APSP_ECUDA, "lookahead events");
+    }
+  cudaEvent_t* evP2 = ev;        // [2]: panels(K) issued, by K parity
+  cudaEvent_t* evY = ev + 2;     // [2]: Y(K) done, by K parity
+  cudaEvent_t evX0 = ev[4];
+  auto fail = [](const char* what) { return set_error(APSP_ECUDA, "%s", what); };
+  int rc = fw_phase1(c, 0, s);
+  if (!rc) rc = fw_phase2(c, 0, s);
+  if (!rc && b < m) {   // X(0) on the main stream, then closure(1) + panels(1) on the side
+    rc = fw_phase3(c, 0, b, -1, s);
+    if (!rc && cudaEventRecord(evX0, s) != cudaSuccess) rc = fail("event record");
+    if (!rc && cudaStreamWaitEvent(c.side, evX0, 0) != cudaSuccess) rc = fail("stream wait");
+    if (!rc) rc = fw_phase1(c, b, c.side);
+    if (!rc) rc = fw_phase2(c, b, c.side);
+    if (!rc && cudaEventRecord(evP2[1], c.side) != cudaSuccess) rc = fail("event record");
+  }
+  for (int64_t k0 = 0, K = 0; !rc && k0 < m; k0 += b, K++) {
+    const int64_t k1 = k0 + b, k2 = k1 + b;
+    if (K > 0 && cudaStreamWaitEvent(s, evP2[K & 1], 0) != cudaSuccess) rc = fail("stream wait");
+    if (rc) break;
+    if (k1 >= m) {   // last round: every tile
+      if (c.sink) {
+        const int64_t bandr = std::max<int64_t>(TILE_ALIGN, (m / 8 + TILE_ALIGN - 1) / TILE_ALIGN * TILE_ALIGN);
+        for (int64_t r0 = 0; !rc && r0 < m; r0 += bandr) {
+          const int64_t r1 = std::min(m, r0 + bandr);
+          rc = fw_phase3_rows(c, k0, r0, r1, s);
+          if (!rc) rc = c.sink->band(r0, r1, c, s);
+        }
+      } else {
+        rc = fw_phase3(c, k0, -1, -1, s);
+      }
+      break;
+    }
+    if (k2 < m) {
+      rc = fw_phase3(c, k0, k2, k1, s, -1, false);              // Y(K)
+      if (!rc && cudaEventRecord(evY[K & 1], s) != cudaSuccess) rc = fail("event record");
+      if (!rc) rc = fw_phase3(c, k0, -1, k1, s, k2);          // Z(K)
+      // side: X(K+1) (needs panels(K+1), already queued there, and Y(K)), then closure and
+      // panels of K+2
+      if (!rc && cudaStreamWaitEvent(c.side, evY[K & 1], 0) != cudaSuccess) rc = fail("stream wait");
+      if (!rc) rc = fw_phase3(c, k1, k2, -1, c.side);         // X(K+1)
+      if (!rc) rc = fw_phase1(c, k2, c.side);
+      if (!rc) rc = fw_phase2(c, k2, c.side);
+      if (!rc && cudaEventRecord(evP2[K & 1], c.side) != cudaSuccess) rc = fail("event record");
+    } else {
+      rc = fw_phase3(c, k0, -1, k1, s, -1, false);             // Z(K): no cross of K+2
+    }
+  }
+  // the side stream's last work (panels of the last round) is ordered before the last phase 3
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+static bool deep_enabled(const FwCtx& c) {
+  return c.side && c.prep[0] && bulk_store(c.store, c.b) && getenv("APSP_DEEP") && c.m >= 3 * c.b;
+}
+
 int fw_run(FwCtx& c, cudaStream_t s) {
   const int64_t b = c.b;
+  c.deep = deep_enabled(c);
+  if (c.deep) return fw_run_deep(c, s);
   int rc = fw_phase1(c, 0, s);
   if (!rc) rc = fw_phase2(c, 0, s);
   if (rc) return rc;

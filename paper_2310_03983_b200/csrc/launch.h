@@ -40,6 +40,7 @@ struct MinplusArgs {
   int64_t skip_row_lo, skip_row_hi;  // rows [lo,hi) and cols [lo,hi) form the FW pivot cross;
   int64_t skip_col_lo, skip_col_hi;  // tiles entirely inside either band are skipped
   int64_t skip2_lo, skip2_hi;     // a second cross (rows and cols [lo,hi)) to skip (lookahead rest)
+  int64_t skip3_lo, skip3_hi;     // a third cross to skip (two-deep lookahead rest)
   int64_t only_lo, only_hi;       // if lo < hi: the grid enumerates only the tiles of this cross
   Status* status;                 // optional: overflow flag (+ changed flag if track_changed)
   int track_changed;              // set status->changed on any strict improvement (squaring)
@@ -77,6 +78,7 @@ inline MinplusArgs minplus_args() {
   MinplusArgs a{};
   a.skip_row_lo = a.skip_row_hi = a.skip_col_lo = a.skip_col_hi = -1;
   a.skip2_lo = a.skip2_hi = -1;
+  a.skip3_lo = a.skip3_hi = -1;
   a.only_lo = a.only_hi = -1;
   return a;
 }

@@ -43,7 +43,9 @@ __device__ __forceinline__ bool tile_skipped(const MinplusArgs& p, int64_t i0, i
   const bool cin = j0 >= p.skip_col_lo && j0 + bn <= p.skip_col_hi;
   const bool r2 = i0 >= p.skip2_lo && i0 + bm <= p.skip2_hi;
   const bool c2 = j0 >= p.skip2_lo && j0 + bn <= p.skip2_hi;
-  return rin || cin || r2 || c2;
+  const bool r3 = i0 >= p.skip3_lo && i0 + bm <= p.skip3_hi;
+  const bool c3 = j0 >= p.skip3_lo && j0 + bn <= p.skip3_hi;
+  return rin || cin || r2 || c2 || r3 || c3;
 }
 
 __device__ __forceinline__ void emit_idx(const MinplusArgs& p, int64_t i, int64_t j, uint32_t kk) {

@@ -84,13 +84,11 @@ def main():
     h = gen(4096, 1.0, np.float32)
     ms, r = timed(lambda: ap.solve(h, "fw_blocked"), a.reps)
     row(rows, "C2", 4096, 1.0, "fw_blocked fp32 (integral)", ms, r.info)
-    rng = np.random.default_rng(4096)
-    hc = h.cpu().numpy().copy()
-    fin = np.isfinite(hc) & (hc > 0)
-    hc[fin] = rng.uniform(1.0, 100.0, size=int(fin.sum())).astype(np.float32)
-    hc = torch.from_numpy(hc).cuda()
+    hc = torch.from_numpy(ap.continuous_costs(ap.GenParams(4096, 1.0, 100, 7 + 4096))).cuda()
     ms, r = timed(lambda: ap.solve(hc, "fw_blocked"), a.reps)
     row(rows, "C2", 4096, 1.0, "fw_blocked fp32 continuous", ms, r.info)
+    ms, r = timed(lambda: ap.solve(hc, "rkleene", track="pred", base_threshold=512), a.reps)
+    row(rows, "C2", 4096, 1.0, "rkleene fp32 continuous (aligned)", ms, r.info)
     ms, r = timed(lambda: ap.solve(h, "rkleene", track="pred", split="aligned", base_threshold=1024), a.reps)
     row(rows, "C2", 4096, 1.0, "rkleene fp32 (aligned, pred)", ms, r.info)
     # C3
@@ -100,6 +98,14 @@ def main():
         row(rows, "C3", 8192, 1.0, f"rkleene fp32 aligned thr={thr}", ms, r.info)
     ms, r = timed(lambda: ap.solve(h, "fw_blocked"), a.reps)
     row(rows, "C3", 8192, 1.0, "fw_blocked fp32", ms, r.info)
+    ms, r = timed(lambda: ap.solve(h, "rkleene", track="via", split="floor", base_threshold=64), a.reps)
+    row(rows, "C3", 8192, 1.0, "rkleene fp32 reference defaults (floor, via, thr=64)", ms, r.info)
+    hc = torch.from_numpy(ap.continuous_costs(ap.GenParams(8192, 1.0, 100, 7 + 8192))).cuda()
+    ms, r = timed(lambda: ap.solve(hc, "rkleene", track="pred", base_threshold=1024), a.reps)
+    row(rows, "C3", 8192, 1.0, "rkleene fp32 continuous (aligned, pred)", ms, r.info)
+    ms, r = timed(lambda: ap.solve(hc, "fw_blocked"), a.reps)
+    row(rows, "C3", 8192, 1.0, "fw_blocked fp32 continuous", ms, r.info)
+    del hc
     # C5
     for n in (1024, 2048, 4096, 8192, 16384):
         if n > a.sweep_max:
