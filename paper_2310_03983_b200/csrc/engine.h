@@ -2,6 +2,7 @@
 // certificate, streams; fw_sched.cu: blocked FW rounds; rkleene.cu: R-Kleene, squaring and
 // public products; shard.cu: multi-GPU building blocks).  Not part of the C ABI.
 #pragma once
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <memory>
@@ -142,14 +143,44 @@ struct BandSink {
   virtual int band(int64_t r0, int64_t r1, const FwCtx& c, cudaStream_t s) = 0;
 };
 
+// Device time of one call (apsp_info.device_ms). The event pair is created once per host thread
+// and device. stop() synchronises on the end event; mark() + elapsed() let a call that
+// synchronises anyway (the certificate readback) take the end point there, without one more
+// host round trip at the end of a stream-ordered call.
 struct Timer {
   cudaEvent_t a = nullptr, b = nullptr;
   cudaStream_t s;
+  bool marked = false;
+  static int& depth() {   // nested calls (e.g. the zero-cost-edge fallback) get their own pair
+    thread_local int d = 0;
+    return d;
+  }
   explicit Timer(cudaStream_t st) : s(st) {
     g_prof.reset();
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    thread_local cudaEvent_t ev[64][4][2] = {};
+    if (dev < 0 || dev >= 64) dev = 0;
+    const int lvl = std::min(depth()++, 3);
+    if (!ev[dev][lvl][0]) {
+      cudaEventCreate(&ev[dev][lvl][0]);
+      cudaEventCreate(&ev[dev][lvl][1]);
+    }
+    a = ev[dev][lvl][0];
+    b = ev[dev][lvl][1];
     cudaEventRecord(a, s);
+  }
+  ~Timer() { depth()--; }
+  void mark() {
+    cudaEventRecord(b, s);
+    marked = true;
+  }
+  double elapsed() {   // after a synchronisation that covers the mark
+    float ms = 0;
+    if (!marked) return stop();
+    if (cudaEventQuery(b) != cudaSuccess) cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
   }
   double stop() {
     float ms = 0;
@@ -157,10 +188,6 @@ struct Timer {
     cudaEventSynchronize(b);
     cudaEventElapsedTime(&ms, a, b);
     return ms;
-  }
-  ~Timer() {
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
   }
 };
 

@@ -14,8 +14,9 @@
 // tiles reached K+1 (panels) and its own tile reached K, then publishes K+1 (release after a CTA
 // barrier; acquire spin by one thread; all tile data is read through L2, ld.global.cg / cp.async.cg,
 // so no SM reads a stale L1 line). The claim order
-//     C(0) P(0) A(0) | C(1) P(1) B(0) A(1) | C(2) P(2) B(1) A(2) | ... | B(nb-1)
-// (P = the panels, A(K) = the round-K updates of the tiles in the cross of K+1, B(K) = the rest)
+//     C(0) P(0) A(0) | C(1) P(1) B'(0) A(1) B''(0) | C(2) P(2) B'(1) A(2) B''(1) | ... | B(nb-1)
+// (P = the panels, A(K) = the round-K updates of the tiles in the cross of K+1, B(K) = the rest,
+// split into B'(K), its tiles in the cross of K+2, and B''(K), the others)
 // is the lookahead schedule, and every dependency of a task is claimed before it: with every CTA
 // resident (grid = SM count, one CTA per SM), the spin-waits always end.
 //
@@ -26,13 +27,19 @@
 // gathered from the B rows' pred for improved cells only. The row-panel task reads its own tile
 // as B and its pred rows, so every gather of a task completes before any of its stores (barrier).
 
+// APSP_PERSIST_TRACE: summed globaltimer ns of the 64-wide closure's phases (load, k loop, pred
+// resolution, stores) over all closure tasks, printed with the trace
+__device__ unsigned long long g_close64_phase[5];
+
 namespace persist {
 
 constexpr int PT = 512;            // threads
 constexpr int PB = 128;            // tile
 constexpr uint32_t KINF2 = (uint32_t(U8_INF) << 7) * 0x00010001u;
 constexpr uint32_t TMASK2 = 0x007F007Fu;
-enum Task : int { T_CLOSE = 0, T_ROW = 1, T_COL = 2, T_UPD = 3 };
+// T_UCLOSE(K): round K-1's update of the diagonal tile (K,K) fused into its closure -- one task
+// hop fewer on the per-round chain (closure -> panel -> cross tile -> closure)
+enum Task : int { T_CLOSE = 0, T_ROW = 1, T_COL = 2, T_UPD = 3, T_UCLOSE = 4 };
 
 struct TileSmem {
   uint32_t As[2][SUB][PB];   // replicated key pairs (v << 7 in both halves), by k then row
@@ -196,6 +203,10 @@ __global__ void __launch_bounds__(PT, 1) fw_persist_kernel(uint8_t* D, int64_t l
     if (t == 0) {
       if (w.x == T_CLOSE) {
         wait_at_least(&done[K * nb + K], K);
+      } else if (w.x == T_UCLOSE) {
+        wait_at_least(&done[K * nb + K - 1], K);
+        wait_at_least(&done[(K - 1) * nb + K], K);
+        wait_at_least(&done[K * nb + K], K - 1);
       } else if (w.x == T_ROW) {
         wait_at_least(&done[K * nb + K], K + 1);
         wait_at_least(&done[K * nb + J], K);
@@ -211,7 +222,13 @@ __global__ void __launch_bounds__(PT, 1) fw_persist_kernel(uint8_t* D, int64_t l
     __syncthreads();
     if (trace && t == 0) t_ready = gtimer();
     const int64_t k0 = int64_t(K) * PB;
-    if (w.x == T_CLOSE) {
+    if (w.x == T_CLOSE || w.x == T_UCLOSE) {
+      if (w.x == T_UCLOSE) {   // round K-1 on the tile first (pivot block K-1)
+        const int64_t kp = k0 - PB;
+        tile_task(sm.tile, D + k0 * ld + k0, ld, D + k0 * ld + kp, ld, D + kp * ld + k0, ld,
+                  P ? P + k0 * ldp + k0 : nullptr, ldp, P ? P + kp * ldp + k0 : nullptr, ldp);
+        __syncthreads();
+      }
       close_dpx_body<STORE_U8, true>(D, ld, k0, PB, P, ldp, IDX_PRED, k0,
                                      reinterpret_cast<unsigned char*>(&sm.close));
     } else {
@@ -222,8 +239,8 @@ __global__ void __launch_bounds__(PT, 1) fw_persist_kernel(uint8_t* D, int64_t l
     __syncthreads();   // the task's stores precede the release
     if (t == 0) {
       __threadfence();
-      const int ti = w.x == T_CLOSE ? K : w.x == T_ROW ? K : I;
-      const int tj = w.x == T_CLOSE ? K : w.x == T_COL ? K : J;
+      const int ti = (w.x == T_CLOSE || w.x == T_UCLOSE || w.x == T_ROW) ? K : I;
+      const int tj = (w.x == T_CLOSE || w.x == T_UCLOSE || w.x == T_COL) ? K : J;
       release_st(&done[ti * nb + tj], K + 1);
       if (trace) {   // APSP_PERSIST_TRACE: claim / dependencies met / done (globaltimer ns), SM
         unsigned int smid;
@@ -240,29 +257,36 @@ __global__ void __launch_bounds__(PT, 1) fw_persist_kernel(uint8_t* D, int64_t l
 }  // namespace persist
 
 // The claim order of the persistent schedule (see above), built once per (device, block count).
-static const int4* persist_items(int nb, int* nitems) {
-  struct Entry { int dev, nb, n; int4* d; };
+static const int4* persist_items(int nb, int* nitems, bool fuse_diag) {
+  struct Entry { int dev, nb, fuse, n; int4* d; };
   static std::mutex mu;
   static std::vector<Entry> cache;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lock(mu);
   for (const Entry& e : cache)
-    if (e.dev == dev && e.nb == nb) {
+    if (e.dev == dev && e.nb == nb && e.fuse == int(fuse_diag)) {
       *nitems = e.n;
       return e.d;
     }
   std::vector<int4> v;
-  auto updates = [&](int K, bool next_cross) {   // round-K updates in / outside the cross of K+1
+  // round-K updates inside (part 0) / outside (part 1) the cross of K+1; part 1 optionally only
+  // the tiles in (sel = 1) or outside (sel = 2) the cross of K+2, so the rest of round K-1 that
+  // the next cross needs is claimed before that cross, and the remainder after it
+  auto updates = [&](int K, bool next_cross, int sel = 0) {
     for (int I = 0; I < nb; I++)
       for (int J = 0; J < nb; J++) {
         if (I == K || J == K) continue;
         const bool nx = K + 1 < nb && (I == K + 1 || J == K + 1);
-        if (nx == next_cross) v.push_back(make_int4(persist::T_UPD, K, I, J));
+        if (nx != next_cross) continue;
+        const bool nx2 = K + 2 < nb && (I == K + 2 || J == K + 2);
+        if ((sel == 1 && !nx2) || (sel == 2 && nx2)) continue;
+        if (fuse_diag && I == K + 1 && J == K + 1) continue;   // fused into T_UCLOSE(K+1)
+        v.push_back(make_int4(persist::T_UPD, K, I, J));
       }
   };
   auto close_and_panels = [&](int K) {
-    v.push_back(make_int4(persist::T_CLOSE, K, K, K));
+    v.push_back(make_int4(K && fuse_diag ? persist::T_UCLOSE : persist::T_CLOSE, K, K, K));
     for (int q = 1; q < nb; q++) {   // the next pivot's panel tiles first
       const int X = (K + q) % nb;
       v.push_back(make_int4(persist::T_ROW, K, K, X));
@@ -273,17 +297,20 @@ static const int4* persist_items(int nb, int* nitems) {
   updates(0, true);
   for (int K = 1; K < nb; K++) {
     close_and_panels(K);
-    updates(K - 1, false);
-    updates(K, true);
+    updates(K - 1, false, 1);   // round K-1 tiles of the cross of K+1 (needed by A(K))
+    updates(K, true);           // A(K): round K on the cross of K+1 (needed by the next closure)
+    updates(K - 1, false, 2);   // the rest of round K-1
   }
   updates(nb - 1, false);
   int4* d = nullptr;
   if (cudaMalloc(&d, v.size() * sizeof(int4)) != cudaSuccess) return nullptr;
   if (cudaMemcpy(d, v.data(), v.size() * sizeof(int4), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-  cache.push_back({dev, nb, int(v.size()), d});
+  cache.push_back({dev, nb, int(fuse_diag), int(v.size()), d});
   *nitems = int(v.size());
   return d;
 }
+
+static int persist_dump_trace(unsigned long long* trace, const int4* items, int nitems, cudaStream_t s);
 
 size_t fw_persist_scratch_bytes(int64_t N) {
   const int64_t nb = N / TILE_ALIGN;
@@ -299,7 +326,8 @@ bool fw_persist_enabled(int store, int64_t N) {
 int launch_fw_persist(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch, cudaStream_t s) {
   const int nb = int(N / TILE_ALIGN);
   int nitems = 0;
-  const int4* items = persist_items(nb, &nitems);
+  // (the 128-wide closure is long: fusing the diagonal update into it measured slower at n=3072)
+  const int4* items = persist_items(nb, &nitems, false);
   if (!items) return set_error(APSP_ECUDA, "persistent schedule table allocation failed");
   int* done = static_cast<int*>(scratch);
   int* counter = done + nb * nb;
@@ -311,14 +339,18 @@ int launch_fw_persist(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N
   APSP_CUDA_TRY(cudaGetDevice(&dev));
   APSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int grid = std::min(sms, nitems);
-  // APSP_PERSIST_TRACE=file: per task (kind, K, I, J, claim, ready, done ns, SM) as CSV, for the
-  // schedule's critical path (tools/persist_trace.py)
-  const char* tpath = getenv("APSP_PERSIST_TRACE");
   unsigned long long* trace = nullptr;
-  if (tpath) APSP_CUDA_TRY(cudaMalloc(&trace, size_t(nitems) * 4 * sizeof(unsigned long long)));
+  if (getenv("APSP_PERSIST_TRACE")) APSP_CUDA_TRY(cudaMalloc(&trace, size_t(nitems) * 4 * sizeof(unsigned long long)));
   persist::fw_persist_kernel<<<grid, persist::PT, sb, s>>>(D, ld, P, ldp, nb, items, nitems, done, counter, trace);
   APSP_CUDA_TRY(cudaGetLastError());
   count_launches(1);
+  return persist_dump_trace(trace, items, nitems, s);
+}
+
+// APSP_PERSIST_TRACE=file: per task (kind, K, I, J, claim, ready, done ns, SM) as CSV, for the
+// schedule's critical path (tools/persist_trace.py)
+static int persist_dump_trace(unsigned long long* trace, const int4* items, int nitems, cudaStream_t s) {
+  const char* tpath = getenv("APSP_PERSIST_TRACE");
   if (trace) {
     std::vector<unsigned long long> h(size_t(nitems) * 4);
     std::vector<int4> it(nitems);
@@ -327,6 +359,10 @@ int launch_fw_persist(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N
     APSP_CUDA_TRY(cudaStreamSynchronize(s));
     cudaFree(trace);
     if (FILE* f = fopen(tpath, "w")) {
+      unsigned long long ph[5] = {};
+      if (cudaMemcpyFromSymbol(ph, g_close64_phase, sizeof(ph)) == cudaSuccess && ph[4])
+        fprintf(stderr, "[persist64] close64 phases (mean ns over %llu): load %llu, k loop %llu, pred %llu, store %llu\n",
+                ph[4], ph[0] / ph[4], ph[1] / ph[4], ph[2] / ph[4], ph[3] / ph[4]);
       fprintf(f, "kind,K,I,J,claim,ready,done,sm\n");
       for (int i = 0; i < nitems; i++)
         fprintf(f, "%d,%d,%d,%d,%llu,%llu,%llu,%llu\n", it[i].x, it[i].y, it[i].z, it[i].w, h[4 * i], h[4 * i + 1],
@@ -335,4 +371,383 @@ int launch_fw_persist(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N
     }
   }
   return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// 64-wide pivot blocks (N <= APSP_PERSIST64_MAX_N): the per-round chain is what bounds small n,
+// and a 64 x 64 closure is ~8x cheaper than a 128 x 128 one (64 steps over 4096 cells instead
+// of 128 over 16384), so halving b halves the chain even though the rounds double. Same
+// dataflow schedule and semantics as above with 64 x 64 tiles: 256-thread CTAs, several per SM
+// (all resident: grid = occupancy x SMs), k = 64 per task in one shot (tags 1..64, one decode).
+// ------------------------------------------------------------------------------------------
+namespace persist64 {
+
+constexpr int QT = 256;   // threads
+constexpr int QB = 64;    // tile / pivot block
+using persist::TMASK2;
+
+struct TileSmem {
+  uint32_t As[QB][QB];    // [k][row] replicated key pairs
+  uint16_t Bs[QB][QB];    // [k][col] tagged keys
+  int32_t Pb[QB][QB];     // pred rows of B (cp.async during the k loop: the gathers hit smem)
+};
+struct CloseSmem {
+  uint32_t colk[2][QB];   // column k as replicated tag-free keys, by row
+  uint32_t colk1[2][QB];  // column k+1 likewise (two steps per barrier)
+  int32_t P[QB][QB];      // pred resolution
+  uint8_t K[QB][QB];      // 1-based last improving k (0 = none)
+};
+union Smem {
+  TileSmem tile;
+  CloseSmem close;
+};
+
+// 64 x 64 closure in classic k order (values, pred bit-exact with the classic in-block loop).
+// Warp w owns columns 8w..8w+7 (4 key pairs), lane l rows 2l, 2l+1: row k comes by shuffle from
+// lane k/2 of the same warp, column k from its owner warp through shared memory (double
+// buffered, one barrier per step). The last improving k rides in the 7-bit tag (k + 1 <= 64).
+__device__ void close64(CloseSmem& sm, uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, bool prof) {
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  unsigned long long tp0 = prof && t == 0 ? persist::gtimer() : 0, tp1 = 0, tp2 = 0, tp3 = 0;
+  constexpr uint32_t STRIP2 = ~TMASK2;
+  uint32_t acc[2][4];
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(D + int64_t(2 * l + r) * ld + 8 * w));
+    acc[r][0] = __byte_perm(v.x, 0, 0x4140) << 7;
+    acc[r][1] = __byte_perm(v.x, 0, 0x4342) << 7;
+    acc[r][2] = __byte_perm(v.y, 0, 0x4140) << 7;
+    acc[r][3] = __byte_perm(v.y, 0, 0x4342) << 7;
+  }
+  if (P) {   // the input pred block, for the resolution after the k loop: in flight meanwhile
+    for (int e = t; e < QB * QB / 4; e += QT) {
+      const int i = e >> 4, j = 4 * (e & 15);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&sm.P[i][j])),
+                   "l"(P + int64_t(i) * ldp + j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  // Two steps per barrier: columns k and k+1 (k even) are one key pair of one warp, published
+  // together as two replicated tag-free columns; every warp advances column k+1 through step k
+  // itself, D[i][k+1] <- min(D[i][k+1], D[i][k] + D[k][k+1]), then runs steps k and k+1 back to
+  // back (row k+1 comes from its owner lane after that lane's own step-k update). Each cell is
+  // still updated by its owner in k order, so values and tags are those of the one-step loop.
+#define P64_PUBPAIR(PP, BUF)                                                                \
+  do {                                                                                      \
+    *reinterpret_cast<uint2*>(&sm.colk[BUF][2 * l]) =                                       \
+        make_uint2(__byte_perm(acc[0][PP], 0, 0x1010) & STRIP2, __byte_perm(acc[1][PP], 0, 0x1010) & STRIP2); \
+    *reinterpret_cast<uint2*>(&sm.colk1[BUF][2 * l]) =                                      \
+        make_uint2(__byte_perm(acc[0][PP], 0, 0x3232) & STRIP2, __byte_perm(acc[1][PP], 0, 0x3232) & STRIP2); \
+  } while (0)
+  if (w == 0) P64_PUBPAIR(0, 0);
+  if (prof) {
+    __syncthreads();
+    if (t == 0) tp1 = persist::gtimer();
+  }
+#pragma unroll 1
+  for (int k0 = 0; k0 < QB; k0 += 8) {
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 2) {
+      const int k = k0 + kk, buf = (kk >> 1) & 1;
+      __syncthreads();
+      const uint2 c2 = *reinterpret_cast<const uint2*>(&sm.colk[buf][2 * l]);
+      const uint2 c3 = *reinterpret_cast<const uint2*>(&sm.colk1[buf][2 * l]);
+      const uint32_t dkk1 = sm.colk1[buf][k];   // D[k][k+1], replicated
+      const uint32_t ck1x = __viaddmin_u16x2(c2.x, dkk1, c3.x), ck1y = __viaddmin_u16x2(c2.y, dkk1, c3.y);
+      uint32_t dkj[4];
+      const uint32_t tag2 = uint32_t(k + 1) * 0x00010001u;
+#pragma unroll
+      for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[0][p], k >> 1) & STRIP2) | tag2;
+#pragma unroll
+      for (int p = 0; p < 4; p++) {
+        acc[0][p] = __viaddmin_u16x2(c2.x, dkj[p], acc[0][p]);
+        acc[1][p] = __viaddmin_u16x2(c2.y, dkj[p], acc[1][p]);
+      }
+#pragma unroll
+      for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[1][p], (k + 1) >> 1) & STRIP2) | (tag2 + 0x00010001u);
+#pragma unroll
+      for (int p = 0; p < 4; p++) {
+        acc[0][p] = __viaddmin_u16x2(ck1x, dkj[p], acc[0][p]);
+        acc[1][p] = __viaddmin_u16x2(ck1y, dkj[p], acc[1][p]);
+      }
+      // the next pair (k+2, k+3): pair ((kk+2) & 7) >> 1 of warp (k+2) >> 3
+      if (k + 2 < QB) {
+        if (kk == 6) {
+          if (w == (k0 >> 3) + 1) P64_PUBPAIR(0, buf ^ 1);
+        } else if (w == (k0 >> 3)) {
+          P64_PUBPAIR(((kk + 2) & 7) >> 1, buf ^ 1);
+        }
+      }
+    }
+  }
+#undef P64_PUBPAIR
+  __syncthreads();   // every warp is past its last read of colk
+  if (prof && t == 0) tp2 = persist::gtimer();
+  uint32_t kst[2][4];
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      kst[r][p] = acc[r][p] & TMASK2;   // one window: the tag is k* + 1 (0 = never improved)
+      acc[r][p] -= kst[r][p];
+    }
+  // values back (improved pairs only change; writing all is simpler and equally final)
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    const uint32_t v0 = __byte_perm(acc[r][0] >> 7, acc[r][1] >> 7, 0x6420);
+    const uint32_t v1 = __byte_perm(acc[r][2] >> 7, acc[r][3] >> 7, 0x6420);
+    *reinterpret_cast<uint2*>(D + int64_t(2 * l + r) * ld + 8 * w) = make_uint2(v0, v1);
+  }
+  if (!P) return;
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      sm.K[2 * l + r][8 * w + 2 * p] = uint8_t(kst[r][p] & 0xFFu);
+      sm.K[2 * l + r][8 * w + 2 * p + 1] = uint8_t(kst[r][p] >> 16);
+    }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  // pred[i][j] = pred_final[k*][j]: pointer jumping (chains strictly shorten: < 64 = 2^6 hops)
+  for (int round = 0; round < 6; round++) {
+    int32_t np[16];
+    uint8_t nk[16];
+    bool live = false;
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      const int e = t + QT * c, i = e >> 6, j = e & 63;
+      const uint8_t kk = sm.K[i][j];
+      np[c] = sm.P[i][j];
+      nk[c] = kk;
+      if (kk) {
+        np[c] = sm.P[kk - 1][j];
+        nk[c] = sm.K[kk - 1][j];
+        live |= nk[c] != 0;
+      }
+    }
+    const bool more = __syncthreads_or(live);
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      const int e = t + QT * c, i = e >> 6, j = e & 63;
+      sm.P[i][j] = np[c];
+      sm.K[i][j] = nk[c];
+    }
+    __syncthreads();
+    if (!more) break;
+  }
+  if (prof && t == 0) tp3 = persist::gtimer();
+  for (int e = t; e < QB * QB / 4; e += QT) {
+    const int i = e >> 4, j = 4 * (e & 15);
+    *reinterpret_cast<int4*>(P + int64_t(i) * ldp + j) = *reinterpret_cast<const int4*>(&sm.P[i][j]);
+  }
+  if (prof && t == 0) {
+    const unsigned long long tp4 = persist::gtimer();
+    atomicAdd(&g_close64_phase[0], tp1 - tp0);
+    atomicAdd(&g_close64_phase[1], tp2 - tp1);
+    atomicAdd(&g_close64_phase[2], tp3 - tp2);
+    atomicAdd(&g_close64_phase[3], tp4 - tp3);
+    atomicAdd(&g_close64_phase[4], 1ull);
+  }
+}
+
+// C <- min(C, A (x) B) on a 64 x 64 tile, k = 64. Thread t: rows 2*(t>>3) + {0,1}, columns
+// 8*(t&7) .. + 7 (4 key pairs).
+__device__ void tile64(TileSmem& sm, uint8_t* C, int64_t ldc, const uint8_t* A, int64_t lda, const uint8_t* B,
+                       int64_t ldb, int32_t* P, int64_t ldp, const int32_t* PB_, int64_t ldpb) {
+  const int t = threadIdx.x, ty = t >> 3, tx = t & 7;
+  if (P) {   // B's pred rows, in flight while the tile computes (L2 only: cp.async.cg)
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int e = t + QT * q, i = e >> 4, j = 4 * (e & 15);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&sm.Pb[i][j])),
+                   "l"(PB_ + int64_t(i) * ldpb + j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  {  // stage A (64 rows x 64 k) and B (64 k x 64 cols): 16 bytes of each per thread
+    const int ra = t >> 2, ka = 16 * (t & 3);
+    const uint4 va = __ldcg(reinterpret_cast<const uint4*>(A + int64_t(ra) * lda + ka));
+    const uint32_t wa[4] = {va.x, va.y, va.z, va.w};
+#pragma unroll
+    for (int q = 0; q < 16; q++) sm.As[ka + q][ra] = ((wa[q >> 2] >> (8 * (q & 3))) & 0xFFu) * 0x00800080u;
+    const int kb = t >> 2, cb = 16 * (t & 3);
+    const uint4 vb = __ldcg(reinterpret_cast<const uint4*>(B + int64_t(kb) * ldb + cb));
+    const uint32_t wb[4] = {vb.x, vb.y, vb.z, vb.w};
+    const uint32_t tag = uint32_t(kb + 1) * 0x00010001u;
+    uint32_t o[8];
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      o[2 * q] = (__byte_perm(wb[q], 0, 0x4140) << 7) | tag;
+      o[2 * q + 1] = (__byte_perm(wb[q], 0, 0x4342) << 7) | tag;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(&sm.Bs[kb][cb]);
+    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+  uint32_t acc[2][4];
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(C + int64_t(2 * ty + r) * ldc + 8 * tx));
+    acc[r][0] = __byte_perm(v.x, 0, 0x4140) << 7;
+    acc[r][1] = __byte_perm(v.x, 0, 0x4342) << 7;
+    acc[r][2] = __byte_perm(v.y, 0, 0x4140) << 7;
+    acc[r][3] = __byte_perm(v.y, 0, 0x4342) << 7;
+  }
+  __syncthreads();
+#pragma unroll 16
+  for (int k = 0; k < QB; k++) {
+    const uint2 a = *reinterpret_cast<const uint2*>(&sm.As[k][2 * ty]);
+    const uint4 b = *reinterpret_cast<const uint4*>(&sm.Bs[k][8 * tx]);
+    const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      acc[0][p] = __viaddmin_u16x2(a.x, bv[p], acc[0][p]);
+      acc[1][p] = __viaddmin_u16x2(a.y, bv[p], acc[1][p]);
+    }
+  }
+  uint32_t kst[2][4];
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int p = 0; p < 4; p++) {
+      kst[r][p] = acc[r][p] & TMASK2;
+      acc[r][p] -= kst[r][p];
+    }
+  // the gathers read the smem snapshot of B's pred rows (taken before any store of this task,
+  // so the row-panel task, whose B is its own tile, needs no barrier before its stores)
+  if (P) {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
+  int32_t pv[2][8];
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int p = 0; p < 4; p++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint32_t k1 = (kst[r][p] >> (16 * h)) & 0xFFFFu;
+        pv[r][2 * p + h] = (P && k1) ? sm.Pb[k1 - 1][8 * tx + 2 * p + h] : 0;
+      }
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    if ((kst[r][0] | kst[r][1] | kst[r][2] | kst[r][3]) == 0u) continue;
+    const uint32_t v0 = __byte_perm(acc[r][0] >> 7, acc[r][1] >> 7, 0x6420);
+    const uint32_t v1 = __byte_perm(acc[r][2] >> 7, acc[r][3] >> 7, 0x6420);
+    *reinterpret_cast<uint2*>(C + int64_t(2 * ty + r) * ldc + 8 * tx) = make_uint2(v0, v1);
+    if (!P) continue;
+    int32_t* prow = P + int64_t(2 * ty + r) * ldp + 8 * tx;
+#pragma unroll
+    for (int p = 0; p < 4; p++)
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+        if ((kst[r][p] >> (16 * h)) & 0xFFFFu) prow[2 * p + h] = pv[r][2 * p + h];
+  }
+}
+
+__global__ void __launch_bounds__(QT, 3) fw_persist64_kernel(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int nb,
+                                                             const int4* items, int nitems, int* done, int* counter,
+                                                             unsigned long long* trace) {
+  __shared__ Smem sm;
+  __shared__ int s_item;
+  const int t = threadIdx.x;
+  for (;;) {
+    if (t == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int it = s_item;
+    if (it >= nitems) break;
+    const int4 w = items[it];   // (task, K, I, J)
+    const int K = w.y, I = w.z, J = w.w;
+    unsigned long long t_claim = 0, t_ready = 0;
+    if (trace && t == 0) t_claim = persist::gtimer();
+    if (t == 0) {
+      if (w.x == persist::T_CLOSE) {
+        persist::wait_at_least(&done[K * nb + K], K);
+      } else if (w.x == persist::T_UCLOSE) {
+        persist::wait_at_least(&done[K * nb + K - 1], K);
+        persist::wait_at_least(&done[(K - 1) * nb + K], K);
+        persist::wait_at_least(&done[K * nb + K], K - 1);
+      } else if (w.x == persist::T_ROW) {
+        persist::wait_at_least(&done[K * nb + K], K + 1);
+        persist::wait_at_least(&done[K * nb + J], K);
+      } else if (w.x == persist::T_COL) {
+        persist::wait_at_least(&done[K * nb + K], K + 1);
+        persist::wait_at_least(&done[I * nb + K], K);
+      } else {
+        persist::wait_at_least(&done[I * nb + K], K + 1);
+        persist::wait_at_least(&done[K * nb + J], K + 1);
+        persist::wait_at_least(&done[I * nb + J], K);
+      }
+    }
+    __syncthreads();
+    if (trace && t == 0) t_ready = persist::gtimer();
+    const int64_t k0 = int64_t(K) * QB;
+    if (w.x == persist::T_CLOSE || w.x == persist::T_UCLOSE) {
+      if (w.x == persist::T_UCLOSE) {   // round K-1 on the tile first (pivot block K-1)
+        const int64_t kp = k0 - QB;
+        tile64(sm.tile, D + k0 * ld + k0, ld, D + k0 * ld + kp, ld, D + kp * ld + k0, ld,
+               P ? P + k0 * ldp + k0 : nullptr, ldp, P ? P + kp * ldp + k0 : nullptr, ldp);
+        __syncthreads();
+      }
+      close64(sm.close, D + k0 * ld + k0, ld, P ? P + k0 * ldp + k0 : nullptr, ldp, trace != nullptr);
+    } else {
+      const int64_t i0 = int64_t(w.x == persist::T_ROW ? K : I) * QB;
+      const int64_t j0 = int64_t(w.x == persist::T_COL ? K : J) * QB;
+      tile64(sm.tile, D + i0 * ld + j0, ld, D + i0 * ld + k0, ld, D + k0 * ld + j0, ld,
+             P ? P + i0 * ldp + j0 : nullptr, ldp, P ? P + k0 * ldp + j0 : nullptr, ldp);
+    }
+    __syncthreads();
+    if (t == 0) {
+      __threadfence();
+      const bool cl = w.x == persist::T_CLOSE || w.x == persist::T_UCLOSE;
+      const int ti = (cl || w.x == persist::T_ROW) ? K : I;
+      const int tj = (cl || w.x == persist::T_COL) ? K : J;
+      persist::release_st(&done[ti * nb + tj], K + 1);
+      if (trace) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        trace[4 * it] = t_claim;
+        trace[4 * it + 1] = t_ready;
+        trace[4 * it + 2] = persist::gtimer();
+        trace[4 * it + 3] = smid;
+      }
+    }
+  }
+}
+
+}  // namespace persist64
+
+bool fw_persist64_enabled(int store, int64_t N) {
+  static const int64_t max_n = getenv("APSP_PERSIST64_MAX_N") ? atoll(getenv("APSP_PERSIST64_MAX_N")) : 2048;
+  // N = 128 is one classic-order closure (pred bit-exact with the reference, test-pinned): the
+  // 128-wide schedule handles it
+  return store == STORE_U8 && N % 64 == 0 && N <= max_n && N >= 256;
+}
+
+size_t fw_persist64_scratch_bytes(int64_t N) {
+  const int64_t nb = N / 64;
+  return size_t(nb * nb + 64) * sizeof(int);
+}
+
+int launch_fw_persist64(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch, cudaStream_t s) {
+  const int nb = int(N / 64);
+  int nitems = 0;
+  const int4* items = persist_items(nb, &nitems, true);
+  if (!items) return set_error(APSP_ECUDA, "persistent schedule table allocation failed");
+  int* done = static_cast<int*>(scratch);
+  int* counter = done + nb * nb;
+  APSP_CUDA_TRY(cudaMemsetAsync(scratch, 0, fw_persist64_scratch_bytes(N), s));
+  int dev = 0, sms = 0, per_sm = 0;
+  APSP_CUDA_TRY(cudaGetDevice(&dev));
+  APSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  APSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist64::fw_persist64_kernel, persist64::QT, 0));
+  if (per_sm < 1) return set_error(APSP_ECUDA, "persistent kernel does not fit an SM");
+  const int grid = std::min(sms * per_sm, nitems);   // every CTA resident: the spin-waits end
+  unsigned long long* trace = nullptr;
+  if (getenv("APSP_PERSIST_TRACE")) APSP_CUDA_TRY(cudaMalloc(&trace, size_t(nitems) * 4 * sizeof(unsigned long long)));
+  persist64::fw_persist64_kernel<<<grid, persist64::QT, 0, s>>>(D, ld, P, ldp, nb, items, nitems, done, counter,
+                                                                trace);
+  APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
+  return persist_dump_trace(trace, items, nitems, s);
 }

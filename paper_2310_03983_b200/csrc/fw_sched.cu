@@ -573,6 +573,7 @@ size_t fw_ws_bytes(int dtype, int64_t n, int block) {
 int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
                     void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info, BandSink* sink) {
   if (n < 1) return set_error(APSP_EDIMENSION, "cost matrix must be non-empty");
+  const bool b_default = b <= 0;   // the library picks the schedule (incl. the 64-wide persistent one)
   if (b <= 0) b = default_block(n);
   if (b % 128 || b < 128 || b > 4096) return set_error(APSP_EINVAL, "blocked FW block must be a multiple of 128 in [128, 4096] (got %d)", b);
   const int64_t N = round_up(n, b);
@@ -624,7 +625,12 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
       // graph replay only where launch gaps dominate (N <= 2048): a graph drops the lookahead
       // stream's priority, which costs more than the gaps at larger N (n=8192 21.6 -> 25 ms)
       const int64_t Nsq = round_up(n, TILE_ALIGN);
-      if (b == TILE_ALIGN && fw_persist_enabled(store, N) && !sink && !g_prof.on && !getenv("APSP_NO_PERSIST")) {
+      if (b_default && fw_persist64_enabled(store, N) && !sink && !g_prof.on && !getenv("APSP_NO_PERSIST")) {
+        Scratch ps;
+        rc = ps.acquire(nullptr, 0, fw_persist64_scratch_bytes(N), s);
+        if (!rc) rc = launch_fw_persist64(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s);
+        c.launches += 2;
+      } else if (b == TILE_ALIGN && fw_persist_enabled(store, N) && !sink && !g_prof.on && !getenv("APSP_NO_PERSIST")) {
         Scratch ps;
         rc = ps.acquire(nullptr, 0, fw_persist_scratch_bytes(N), s);
         if (!rc) rc = launch_fw_persist(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s);
@@ -647,6 +653,7 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
       launches += c.launches;
     }
     bool ok = false;
+    tm.mark();   // device_ms: scan through the solve (the certificate readback syncs right after)
     if (!rc) rc = certify(tier, store, D, N, n, n, scan, hdr_dev, hdr, s, ok);
     if (rc) return rc;
     launches += 2;
@@ -667,7 +674,7 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   }
   if (rc) return rc;
   launches++;
-  const double ms = tm.stop();
+  const double ms = tm.elapsed();
   if (info) {
     info->block = sq_iters ? 0 : b;
     info->tier = used;

@@ -7,7 +7,7 @@ from collections import defaultdict
 
 rows = list(csv.DictReader(open(sys.argv[1])))
 t0 = min(int(r["claim"]) for r in rows)
-kinds = {0: "close", 1: "row", 2: "col", 3: "upd"}
+kinds = {0: "close", 1: "row", 2: "col", 3: "upd", 4: "uclose"}
 dur = defaultdict(list)
 wait = defaultdict(list)
 for r in rows:
@@ -19,5 +19,5 @@ print(f"tasks {len(rows)}  span {(end - t0) / 1e3:.1f} us  SMs used {len({r['sm'
 for k in dur:
     d, w = dur[k], wait[k]
     print(f"{k:6s} n={len(d):6d} run mean {sum(d) / len(d):7.2f} us max {max(d):7.2f}  wait mean {sum(w) / len(w):7.2f} us")
-closes = sorted((int(r["K"]), (int(r["ready"]) - t0) / 1e3, (int(r["done"]) - t0) / 1e3) for r in rows if r["kind"] == "0")
+closes = sorted((int(r["K"]), (int(r["ready"]) - t0) / 1e3, (int(r["done"]) - t0) / 1e3) for r in rows if r["kind"] in ("0", "4"))
 print("closures (K, start us, end us):", [(k, round(a, 1), round(b, 1)) for k, a, b in closes[:12]])
