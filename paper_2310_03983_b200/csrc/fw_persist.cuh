@@ -17,8 +17,10 @@
 //     C(0) P(0) A(0) | C(1) P(1) B'(0) A(1) B''(0) | C(2) P(2) B'(1) A(2) B''(1) | ... | B(nb-1)
 // (P = the panels, A(K) = the round-K updates of the tiles in the cross of K+1, B(K) = the rest,
 // split into B'(K), its tiles in the cross of K+2, and B''(K), the others)
-// is the lookahead schedule, and every dependency of a task is claimed before it: with every CTA
-// resident (grid = SM count, one CTA per SM), the spin-waits always end.
+// is the lookahead schedule, and every dependency of a task is claimed before it. Tasks are
+// claimed only by CTAs that are running (an atomic counter), and a running CTA finishes its task,
+// so by induction over the claim order every spin-wait ends -- whether or not every CTA of the
+// grid is resident (the grid is sized to the SMs / occupancy only to use them all).
 //
 // Tile tasks use 512 threads on a 128 x 128 tile (4 rows x 8 columns each), k = 128 in four
 // 32-k chunks staged through registers into shared memory as packed 16-bit keys
@@ -378,7 +380,7 @@ static int persist_dump_trace(unsigned long long* trace, const int4* items, int 
 // and a 64 x 64 closure is ~8x cheaper than a 128 x 128 one (64 steps over 4096 cells instead
 // of 128 over 16384), so halving b halves the chain even though the rounds double. Same
 // dataflow schedule and semantics as above with 64 x 64 tiles: 256-thread CTAs, several per SM
-// (all resident: grid = occupancy x SMs), k = 64 per task in one shot (tags 1..64, one decode).
+// (grid = occupancy x SMs), k = 64 per task in one shot (tags 1..64, one decode).
 // ------------------------------------------------------------------------------------------
 namespace persist64 {
 
@@ -742,7 +744,7 @@ int launch_fw_persist64(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t
   APSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   APSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist64::fw_persist64_kernel, persist64::QT, 0));
   if (per_sm < 1) return set_error(APSP_ECUDA, "persistent kernel does not fit an SM");
-  const int grid = std::min(sms * per_sm, nitems);   // every CTA resident: the spin-waits end
+  const int grid = std::min(sms * per_sm, nitems);
   unsigned long long* trace = nullptr;
   if (getenv("APSP_PERSIST_TRACE")) APSP_CUDA_TRY(cudaMalloc(&trace, size_t(nitems) * 4 * sizeof(unsigned long long)));
   persist64::fw_persist64_kernel<<<grid, persist64::QT, 0, s>>>(D, ld, P, ldp, nb, items, nitems, done, counter,

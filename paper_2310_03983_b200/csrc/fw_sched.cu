@@ -625,15 +625,26 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
       // graph replay only where launch gaps dominate (N <= 2048): a graph drops the lookahead
       // stream's priority, which costs more than the gaps at larger N (n=8192 21.6 -> 25 ms)
       const int64_t Nsq = round_up(n, TILE_ALIGN);
-      if (b_default && fw_persist64_enabled(store, N) && !sink && !g_prof.on && !getenv("APSP_NO_PERSIST")) {
+      // the persistent small-n schedules finish every row at once: a host-buffer call's band
+      // sink then gets all bands right after the kernel (same schedule, so the host and device
+      // APIs return identical pred)
+      auto sink_all = [&](int rc0) {
+        if (rc0 || !sink) return rc0;
+        const int64_t bandr = std::max<int64_t>(TILE_ALIGN, (N / 8 + TILE_ALIGN - 1) / TILE_ALIGN * TILE_ALIGN);
+        int r = 0;
+        for (int64_t r0 = 0; !r && r0 < N; r0 += bandr) r = sink->band(r0, std::min(N, r0 + bandr), c, s);
+        return r;
+      };
+      const bool persist_ok = !g_prof.on && !getenv("APSP_NO_PERSIST");
+      if (b_default && persist_ok && fw_persist64_enabled(store, N)) {
         Scratch ps;
         rc = ps.acquire(nullptr, 0, fw_persist64_scratch_bytes(N), s);
-        if (!rc) rc = launch_fw_persist64(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s);
+        if (!rc) rc = sink_all(launch_fw_persist64(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s));
         c.launches += 2;
-      } else if (b == TILE_ALIGN && fw_persist_enabled(store, N) && !sink && !g_prof.on && !getenv("APSP_NO_PERSIST")) {
+      } else if (b == TILE_ALIGN && persist_ok && fw_persist_enabled(store, N)) {
         Scratch ps;
         rc = ps.acquire(nullptr, 0, fw_persist_scratch_bytes(N), s);
-        if (!rc) rc = launch_fw_persist(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s);
+        if (!rc) rc = sink_all(launch_fw_persist(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s));
         c.launches += 2;
       } else if (Nsq <= squaring_max_n() && bulk_store(store, Nsq) && !sink) {
         c.m = Nsq;   // squaring works on the 128-aligned view (pad vertices are isolated)
