@@ -32,19 +32,58 @@ template <> struct Api<API_I64> { using T = int64_t; __device__ static bool fin(
   for (int64_t i = blockIdx.y; i < (rows); i += gridDim.y)                                               \
     for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < (cols); j += int64_t(gridDim.x) * blockDim.x)
 
-static dim3 grid_2d(int64_t rows, int64_t cols) {
+static dim3 grid_2d(int64_t rows, int64_t cols, int64_t ctas = 148 * 16) {
   int64_t gx = (cols + 255) / 256;
   if (gx > 16) gx = 16;
   if (gx < 1) gx = 1;
-  int64_t gy = (148 * 16 + gx - 1) / gx;
+  int64_t gy = (ctas + gx - 1) / gx;
   if (gy > rows) gy = rows;
   if (gy > 65535) gy = 65535;
   if (gy < 1) gy = 1;
   return dim3(unsigned(gx), unsigned(gy));
 }
 
-__device__ __forceinline__ void warp_or(int32_t* dst, bool v) {
-  if (__any_sync(0xffffffffu, v) && (threadIdx.x & 31) == 0) atomicOr(dst, 1);
+// Reductions (scan, certificate) run on 4 CTAs per SM and combine per CTA before one atomic
+// per field: per-warp atomics on the same few addresses serialise in L2 (2368 CTAs x 8 warps
+// made the n=2048 scan 40 us).
+constexpr int64_t kReduceCtas = 148 * 4;
+enum : uint32_t { F_NEG = 1, F_DIAG = 2, F_NONINT = 4, F_ANYFIN = 8, F_ZERO = 16 };
+
+__device__ __forceinline__ void block_commit(ScanResult* out, uint32_t flags, long long mx, float mxf,
+                                             unsigned long long edges) {
+  __shared__ uint32_t s_fl[32];
+  __shared__ long long s_mx[32];
+  __shared__ float s_mf[32];
+  __shared__ unsigned long long s_ed[32];
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  for (int o = 16; o; o >>= 1) {
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+    edges += __shfl_xor_sync(0xffffffffu, edges, o);
+  }
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    s_fl[w] = flags;
+    s_mx[w] = mx;
+    s_mf[w] = mxf;
+    s_ed[w] = edges;
+  }
+  __syncthreads();
+  if (threadIdx.x) return;
+  for (int q = 1; q < nw; q++) {
+    flags |= s_fl[q];
+    mx = max(mx, s_mx[q]);
+    mxf = fmaxf(mxf, s_mf[q]);
+    edges += s_ed[q];
+  }
+  if (flags & F_NEG) atomicOr(&out->negative, 1);
+  if (flags & F_DIAG) atomicOr(&out->diag_nonzero, 1);
+  if (flags & F_NONINT) atomicOr(&out->non_integral, 1);
+  if (flags & F_ANYFIN) atomicOr(&out->any_finite, 1);
+  if (flags & F_ZERO) atomicOr(&out->zero_offdiag, 1);
+  if (mx >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&out->max_finite), (unsigned long long)mx);
+  if (mxf >= 0.f) atomicMax(reinterpret_cast<int*>(&out->max_finite_f), __float_as_int(mxf));
+  if (edges) atomicAdd(&out->finite_offdiag, edges);
 }
 
 template <int D>
@@ -100,24 +139,9 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
   if (!vec || sizeof(T) != 4) {
     FOR_2D(i, j, rows, cols) a.add(h[i * ld + j], diag_off >= 0 && j == i + diag_off);
   }
-  warp_or(&out->negative, a.neg);
-  warp_or(&out->diag_nonzero, a.diag);
-  warp_or(&out->non_integral, a.nonint);
-  warp_or(&out->any_finite, a.anyfin);
-  warp_or(&out->zero_offdiag, a.zero);
-  long long mx = a.mx;
-  float mxf = a.mxf;
-  unsigned long long edges = a.edges;
-  for (int o = 16; o; o >>= 1) {
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
-    edges += __shfl_xor_sync(0xffffffffu, edges, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (mx >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&out->max_finite), (unsigned long long)mx);
-    if (mxf >= 0.f) atomicMax(reinterpret_cast<int*>(&out->max_finite_f), __float_as_int(mxf));
-    if (edges) atomicAdd(&out->finite_offdiag, edges);
-  }
+  const uint32_t flags = (a.neg ? F_NEG : 0u) | (a.diag ? F_DIAG : 0u) | (a.nonint ? F_NONINT : 0u) |
+                         (a.anyfin ? F_ANYFIN : 0u) | (a.zero ? F_ZERO : 0u);
+  block_commit(out, flags, a.mx, a.mxf, a.edges);
 }
 
 static bool vec4_ok(const void* p, int64_t ld, int64_t cols, size_t es) {
@@ -129,7 +153,7 @@ int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t c
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
   // max fields start at 0 after memset; negative sentinel not needed (values are >= 0)
   const int vec = vec4_ok(h, ld, cols, in_dtype == API_I64 ? 8 : 4);
-  const dim3 g = grid_2d(rows, vec ? cols / 4 : cols);
+  const dim3 g = grid_2d(rows, vec ? cols / 4 : cols, kReduceCtas);
   switch (in_dtype) {
     case API_I32: scan_kernel<API_I32><<<g, 256, 0, s>>>((const int32_t*)h, ld, rows, cols, diag_off, out_dev, vec); break;
     case API_F32: scan_kernel<API_F32><<<g, 256, 0, s>>>((const float*)h, ld, rows, cols, diag_off, out_dev, vec); break;
@@ -436,21 +460,14 @@ __global__ void max_finite_kernel(const typename StoreT<S>::T* D, int64_t ld, in
       else mx = max(mx, (long long)v);
     }
   }
-  for (int o = 16; o; o >>= 1) {
-    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    mxf = fmaxf(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (mx >= 0) atomicMax(reinterpret_cast<unsigned long long*>(&out->max_finite), (unsigned long long)mx);
-    if (mxf >= 0.f) atomicMax(reinterpret_cast<int*>(&out->max_finite_f), __float_as_int(mxf));
-  }
+  block_commit(out, 0u, mx, mxf, 0ull);
 }
 
 int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_t cols, ScanResult* out_dev,
                       cudaStream_t s) {
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
   const int vec = store == STORE_U8 && cols % 16 == 0 && ld % 16 == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0;
-  const dim3 g = grid_2d(rows, vec ? cols / 16 : cols);
+  const dim3 g = grid_2d(rows, vec ? cols / 16 : cols, kReduceCtas);
   switch (store) {
     case STORE_U8: max_finite_kernel<STORE_U8><<<g, 256, 0, s>>>((const uint8_t*)D, ld, rows, cols, out_dev, vec); break;
     case STORE_W32: max_finite_kernel<STORE_W32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev, vec); break;

@@ -214,6 +214,7 @@ std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced, bool al
 
 int certify(int tier, int store, const void* D, int64_t ld, int64_t rows, int64_t cols, const ScanResult& sc,
             Header* hdr_dev, Header& hdr, cudaStream_t s, bool& ok);
+int certify_check(int tier, const ScanResult& sc, const Header& hdr, bool& ok);
 
 int api_store(int dtype);
 

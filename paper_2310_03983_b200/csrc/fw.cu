@@ -316,11 +316,20 @@ template <> struct CloseKeys<STORE_U16> {
 
 // The closure body is a device function so the persistent small-n kernel (fw_persist.cu) can
 // run it as one of its tasks; block_close_dpx_kernel below is the stand-alone launch.
+__device__ unsigned long long g_close128_phase[6];   // APSP_CLOSE_PROF: summed ns per phase + count
+__device__ __forceinline__ unsigned long long close_gtimer() {
+  unsigned long long v;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(v));
+  return v;
+}
+
 template <int S, bool FULL>
 __device__ __forceinline__ void close_dpx_body(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo, int m,
                                                int32_t* idx, int64_t ldi, int mode, int64_t via_off,
-                                               unsigned char* smraw_cu8) {
+                                               unsigned char* smraw_cu8, bool prof = false) {
   if (FULL) m = MAXB;   // every FW phase-1 block: the bounds checks fold away
+  unsigned long long tp[5] = {};
+  if (prof && threadIdx.x == 0) tp[0] = close_gtimer();
   using CK = CloseKeys<S>;
   using T = typename CK::T;
   constexpr int TAG = CK::TAG, WIN = CK::WIN, VB = int(sizeof(T));
@@ -406,6 +415,7 @@ __device__ __forceinline__ void close_dpx_body(typename CloseKeys<S>::T* D, int6
     }
   };
   uint32_t tag2 = 0x00010001u;   // tag of step k: 1 + (k mod WIN) in both halves
+  if (prof && threadIdx.x == 0) tp[1] = close_gtimer();
   if constexpr (FULL) {
     // Two steps per CTA barrier. Columns k and k + 1 (k even) form one key pair of one warp, so
     // the owner publishes the pair (after step k - 1) with a single 16-byte store per lane. Every
@@ -498,6 +508,7 @@ __device__ __forceinline__ void close_dpx_body(typename CloseKeys<S>::T* D, int6
 #undef CU8_PUBCOL
   // values back (through the staging area) and the 1-based k* bytes
   __syncthreads();   // every thread has read its cells and column k of the last step
+  if (prof && threadIdx.x == 0) tp[2] = close_gtimer();
 #pragma unroll
   for (int r = 0; r < 4; r++) {
     if constexpr (VB == 1) {
@@ -521,6 +532,7 @@ __device__ __forceinline__ void close_dpx_body(typename CloseKeys<S>::T* D, int6
       if (i < m && j < m) D[(lo + i) * ld + lo + j] = stage[i][j];
     }
   }
+  if (prof && threadIdx.x == 0) tp[3] = close_gtimer();
   if (!idx) return;
   __syncthreads();
 #pragma unroll
@@ -591,6 +603,7 @@ __device__ __forceinline__ void close_dpx_body(typename CloseKeys<S>::T* D, int6
     __syncthreads();
     if (!more) break;
   }
+  if (prof && threadIdx.x == 0) tp[4] = close_gtimer();
 #pragma unroll
   for (int a = 0; a < 8; a++) {
     const int i = ty + 16 * a;
@@ -600,14 +613,40 @@ __device__ __forceinline__ void close_dpx_body(typename CloseKeys<S>::T* D, int6
       if (i < m && j < m) idx[(lo + i) * ldi + lo + j] = sm.P[i][j];
     }
   }
+  if (prof && threadIdx.x == 0) {   // load, k loop, values out, pred resolution, pred out
+    const unsigned long long t5 = close_gtimer();
+    atomicAdd(&g_close128_phase[0], tp[1] - tp[0]);
+    atomicAdd(&g_close128_phase[1], tp[2] - tp[1]);
+    atomicAdd(&g_close128_phase[2], tp[3] - tp[2]);
+    atomicAdd(&g_close128_phase[3], tp[4] - tp[3]);
+    atomicAdd(&g_close128_phase[4], t5 - tp[4]);
+    atomicAdd(&g_close128_phase[5], 1ull);
+  }
 }
 
 template <int S, bool FULL>
 __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo,
                                                               int m, int32_t* idx, int64_t ldi, int mode,
-                                                              int64_t via_off) {
+                                                              int64_t via_off, int prof) {
   extern __shared__ __align__(16) unsigned char smraw_cu8[];
-  close_dpx_body<S, FULL>(D, ld, lo, m, idx, ldi, mode, via_off, smraw_cu8);
+  close_dpx_body<S, FULL>(D, ld, lo, m, idx, ldi, mode, via_off, smraw_cu8, prof != 0);
+}
+
+static bool close_prof_on() {
+  static const bool on = getenv("APSP_CLOSE_PROF") != nullptr;
+  return on;
+}
+
+// APSP_CLOSE_PROF=1: every 32nd u8 closure launch prints the mean phase split (syncs the device;
+// diagnostics only)
+static void close_prof_report() {
+  static std::atomic<long long> calls{0};
+  if (++calls % 32) return;
+  unsigned long long ph[6] = {};
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpyFromSymbol(ph, g_close128_phase, sizeof(ph)) != cudaSuccess || !ph[5])
+    return;
+  fprintf(stderr, "[close128] mean ns over %llu: load %llu, k loop %llu, values out %llu, pred resolve %llu, pred out %llu\n",
+          ph[5], ph[0] / ph[5], ph[1] / ph[5], ph[2] / ph[5], ph[3] / ph[5], ph[4] / ph[5]);
 }
 
 template <int S>
@@ -644,19 +683,20 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
     if (store == STORE_U8 && m == MAXB) {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8, true>, int(sb), attr8f));
       block_close_dpx_kernel<STORE_U8, true><<<1, 512, sb, s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
-                                                                mode, via_off);
+                                                                mode, via_off, int(close_prof_on()));
+      if (close_prof_on()) close_prof_report();
     } else if (store == STORE_U8) {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8, false>, int(sb), attr8));
       block_close_dpx_kernel<STORE_U8, false><<<1, 512, sb, s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
-                                                                 mode, via_off);
+                                                                 mode, via_off, 0);
     } else if (m == MAXB) {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16, true>, int(sb), attr16f));
       block_close_dpx_kernel<STORE_U16, true><<<1, 512, sb, s>>>(static_cast<uint16_t*>(D), ld, lo, int(m), idx,
-                                                                 ldi, mode, via_off);
+                                                                 ldi, mode, via_off, 0);
     } else {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16, false>, int(sb), attr16));
       block_close_dpx_kernel<STORE_U16, false><<<1, 512, sb, s>>>(static_cast<uint16_t*>(D), ld, lo, int(m), idx,
-                                                                  ldi, mode, via_off);
+                                                                  ldi, mode, via_off, 0);
     }
     APSP_CUDA_TRY(cudaGetLastError());
     count_launches(1);

@@ -325,6 +325,35 @@ bool fw_persist_enabled(int store, int64_t N) {
 }
 
 // One persistent launch for the whole u8 blocked FW of an N x N view (N a multiple of 128).
+// co-resident CTAs of a persistent kernel on the current device (SMs x CTAs per SM), cached per
+// (device, kernel): the occupancy query is not free on a small-n call path
+template <typename K>
+static cudaError_t persist_slots(K kernel, int threads, int smem, int& slots) {
+  struct Entry { int dev; const void* fn; int slots; };
+  static std::mutex mu;
+  static std::vector<Entry> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const void* fn = reinterpret_cast<const void*>(kernel);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Entry& c : cache)
+      if (c.dev == dev && c.fn == fn) {
+        slots = c.slots;
+        return cudaSuccess;
+      }
+  }
+  int sms = 0, per_sm = 0;
+  e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+  if (e != cudaSuccess) return e;
+  slots = sms * per_sm;
+  std::lock_guard<std::mutex> lock(mu);
+  cache.push_back({dev, fn, slots});
+  return cudaSuccess;
+}
+
 int launch_fw_persist(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch, cudaStream_t s) {
   const int nb = int(N / TILE_ALIGN);
   int nitems = 0;
@@ -337,9 +366,8 @@ int launch_fw_persist(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N
   static std::atomic<unsigned long long> attr{0};
   const int sb = int(sizeof(persist::Smem));
   APSP_CUDA_TRY(smem_optin(persist::fw_persist_kernel, sb, attr));
-  int dev = 0, sms = 0;
-  APSP_CUDA_TRY(cudaGetDevice(&dev));
-  APSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int sms = 0;
+  APSP_CUDA_TRY(persist_slots(persist::fw_persist_kernel, persist::PT, sb, sms));
   const int grid = std::min(sms, nitems);
   unsigned long long* trace = nullptr;
   if (getenv("APSP_PERSIST_TRACE")) APSP_CUDA_TRY(cudaMalloc(&trace, size_t(nitems) * 4 * sizeof(unsigned long long)));
@@ -739,12 +767,10 @@ int launch_fw_persist64(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t
   int* done = static_cast<int*>(scratch);
   int* counter = done + nb * nb;
   APSP_CUDA_TRY(cudaMemsetAsync(scratch, 0, fw_persist64_scratch_bytes(N), s));
-  int dev = 0, sms = 0, per_sm = 0;
-  APSP_CUDA_TRY(cudaGetDevice(&dev));
-  APSP_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  APSP_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, persist64::fw_persist64_kernel, persist64::QT, 0));
-  if (per_sm < 1) return set_error(APSP_ECUDA, "persistent kernel does not fit an SM");
-  const int grid = std::min(sms * per_sm, nitems);
+  int slots = 0;
+  APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel, persist64::QT, 0, slots));
+  if (slots < 1) return set_error(APSP_ECUDA, "persistent kernel does not fit an SM");
+  const int grid = std::min(slots, nitems);
   unsigned long long* trace = nullptr;
   if (getenv("APSP_PERSIST_TRACE")) APSP_CUDA_TRY(cudaMalloc(&trace, size_t(nitems) * 4 * sizeof(unsigned long long)));
   persist64::fw_persist64_kernel<<<grid, persist64::QT, 0, s>>>(D, ld, P, ldp, nb, items, nitems, done, counter,

@@ -564,11 +564,65 @@ static int fw_square_run(FwCtx& c, Header* hdr_dev, cudaStream_t s, int* iters) 
   }
 }
 
+// scratch of the persistent small-n schedules (done counters + claim counter), carved from the
+// workspace after fw_scratch_bytes: no allocation on the small-n call path
+static size_t persist_ws_bytes(int64_t N) {
+  if (!fw_persist64_enabled(STORE_U8, N) && !fw_persist_enabled(STORE_U8, N)) return 0;
+  return std::max(N % TILE_ALIGN ? size_t(0) : fw_persist_scratch_bytes(N), fw_persist64_scratch_bytes(N)) + 256;
+}
+
 size_t fw_ws_bytes(int dtype, int64_t n, int block) {
   const int64_t N = round_up(std::max<int64_t>(n, 1), block);
   const size_t es = dtype == APSP_DTYPE_I64 ? 8 : 4;
-  return header_bytes() + size_t(N) * N * (es + 4) + 256 + fw_scratch_bytes(N, block, es);
+  return header_bytes() + size_t(N) * N * (es + 4) + 256 + fw_scratch_bytes(N, block, es) + 256 + persist_ws_bytes(N);
 }
+
+namespace {
+// ---- speculative tier --------------------------------------------------------------------
+// Picking a tier needs the input scan on the host: one stream sync before the solve and one
+// for the certificate after it. A repeated call of the same shape (iterative workloads, the
+// benchmark) instead starts the tier that certified last time right behind the scan and reads
+// the scan, the status and the certificate back in ONE sync. The result is used only if the
+// scan then picks that same tier first and the certificate holds; otherwise the attempt is
+// discarded (the caller's dist is only written after a certified tier, the input is intact)
+// and the normal tier loop runs. APSP_NO_SPECULATE=1 disables it.
+struct SpecKey {
+  int dev, dtype, b, tier_req, flags;
+  int64_t n;
+  bool operator==(const SpecKey& o) const {
+    return dev == o.dev && dtype == o.dtype && b == o.b && tier_req == o.tier_req && flags == o.flags && n == o.n;
+  }
+};
+struct SpecEntry {
+  SpecKey key{};
+  int tier = -1;
+};
+constexpr int SPEC_SLOTS = 16;
+std::mutex g_spec_mu;
+SpecEntry g_spec[SPEC_SLOTS];
+int g_spec_next = 0;
+
+int spec_lookup(const SpecKey& k) {
+  static const bool off = getenv("APSP_NO_SPECULATE") != nullptr;
+  if (off) return -1;
+  std::lock_guard<std::mutex> lock(g_spec_mu);
+  for (auto& e : g_spec)
+    if (e.tier >= 0 && e.key == k) return e.tier;
+  return -1;
+}
+
+void spec_remember(const SpecKey& k, int tier) {
+  std::lock_guard<std::mutex> lock(g_spec_mu);
+  for (auto& e : g_spec)
+    if (e.tier >= 0 && e.key == k) {
+      e.tier = tier;
+      return;
+    }
+  if (tier < 0) return;
+  g_spec[g_spec_next] = SpecEntry{k, tier};
+  g_spec_next = (g_spec_next + 1) % SPEC_SLOTS;
+}
+}  // namespace
 
 int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int b, int tier_req,
                     void* ws, size_t ws_bytes, cudaStream_t s, apsp_info* info, BandSink* sink) {
@@ -577,28 +631,19 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   if (b <= 0) b = default_block(n);
   if (b % 128 || b < 128 || b > 4096) return set_error(APSP_EINVAL, "blocked FW block must be a multiple of 128 in [128, 4096] (got %d)", b);
   const int64_t N = round_up(n, b);
+  const size_t es_api = dtype == APSP_DTYPE_I64 ? 8 : 4;
   Scratch sc;
   int rc = sc.acquire(ws, ws_bytes, fw_ws_bytes(dtype, n, b), s);
   if (rc) return rc;
   Header* hdr_dev = static_cast<Header*>(sc.base);
   int32_t* P = reinterpret_cast<int32_t*>(static_cast<char*>(sc.base) + header_bytes());
   char* D = reinterpret_cast<char*>(P) + size_t(N) * N * 4;
-  char* scratch = D + size_t(N) * N * (dtype == APSP_DTYPE_I64 ? 8 : 4) + 256;
+  char* scratch = D + size_t(N) * N * es_api + 256;
+  char* pscratch = scratch + (fw_scratch_bytes(N, b, es_api) + 255) / 256 * 256 + 256;
   Header hdr{};
   Timer tm(s);
   rc = launch_scan(dtype, dist, ld, n, n, 0, &hdr_dev->scan, s);
-  if (!rc) rc = read_header(hdr_dev, hdr, s);
   if (rc) return rc;
-  const ScanResult scan = hdr.scan;
-  rc = check_scan(scan);
-  if (rc) return rc;
-  if (scan.zero_offdiag && pred) {
-    rc = fw_classic_impl(dtype, n, dist, ld, pred, ldp, s, info);
-    if (!rc && info) info->flags |= FLAG_CLASSIC_FOR_ZERO_EDGES;
-    return rc;
-  }
-  std::vector<int> tiers = pick_tiers(dtype, scan, tier_req, true, n);
-  if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
   // no padding: solve straight into the caller's pred matrix (saves an N^2 int32 copy)
   int32_t* Pw = P;
   int64_t ldpw = N;
@@ -607,77 +652,118 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     ldpw = ldp;
   }
   int launches = 2, used = -1, tried = 0, sq_iters = 0;
-  for (int tier : tiers) {
+  // one tier: the store conversion and the schedule (no host reads)
+  auto attempt = [&](int tier) -> int {
     const int store = tier_store(tier);
     if (store < 0) return set_error(APSP_EINVAL, "unknown tier %d", tier);
     if (store == STORE_I64 && dtype != APSP_DTYPE_I64) return set_error(APSP_EINVAL, "int64 tier needs int64 input");
     tried |= 1 << tier;
     APSP_CUDA_TRY(cudaMemsetAsync(&hdr_dev->status, 0, sizeof(Status), s));
-    rc = launch_to_store(dtype, dist, ld, n, store, D, N, N, Pw, ldpw, 1, s);
-    if (!rc) {
-      FwCtx c;
-      c.store = store; c.es = store_elem_size(store);
-      c.D = D; c.ld = N; c.P = Pw; c.ldp = ldpw; c.m = N; c.b = b; c.mode = IDX_PRED; c.via_off = 0;
-      c.st = &hdr_dev->status;
-      c.side = getenv("APSP_NO_LOOKAHEAD") ? nullptr : side_stream();
-      fw_carve(c, scratch, N);
-      if (getenv("APSP_NO_BULK")) c.prep[0] = c.prep[1] = nullptr;
-      // graph replay only where launch gaps dominate (N <= 2048): a graph drops the lookahead
-      // stream's priority, which costs more than the gaps at larger N (n=8192 21.6 -> 25 ms)
-      const int64_t Nsq = round_up(n, TILE_ALIGN);
-      // the persistent small-n schedules finish every row at once: a host-buffer call's band
-      // sink then gets all bands right after the kernel (same schedule, so the host and device
-      // APIs return identical pred)
-      auto sink_all = [&](int rc0) {
-        if (rc0 || !sink) return rc0;
-        const int64_t bandr = std::max<int64_t>(TILE_ALIGN, (N / 8 + TILE_ALIGN - 1) / TILE_ALIGN * TILE_ALIGN);
-        int r = 0;
-        for (int64_t r0 = 0; !r && r0 < N; r0 += bandr) r = sink->band(r0, std::min(N, r0 + bandr), c, s);
-        return r;
-      };
-      const bool persist_ok = !g_prof.on && !getenv("APSP_NO_PERSIST");
-      if (b_default && persist_ok && fw_persist64_enabled(store, N)) {
-        Scratch ps;
-        rc = ps.acquire(nullptr, 0, fw_persist64_scratch_bytes(N), s);
-        if (!rc) rc = sink_all(launch_fw_persist64(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s));
-        c.launches += 2;
-      } else if (b == TILE_ALIGN && persist_ok && fw_persist_enabled(store, N)) {
-        Scratch ps;
-        rc = ps.acquire(nullptr, 0, fw_persist_scratch_bytes(N), s);
-        if (!rc) rc = sink_all(launch_fw_persist(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, ps.base, s));
-        c.launches += 2;
-      } else if (Nsq <= squaring_max_n() && bulk_store(store, Nsq) && !sink) {
-        c.m = Nsq;   // squaring works on the 128-aligned view (pad vertices are isolated)
-        int it = 0;
-        rc = fw_square_run(c, hdr_dev, s, &it);
-        c.m = N;
-        sq_iters = it;
-      } else if (N <= 2048) {   // (no band sink here: the graph holds the whole chain)
-        int dev = 0;
-        cudaGetDevice(&dev);
-        const GraphKey key{dev, 1, store, c.mode, N, b, D, Pw, scratch, c.side, s};
-        rc = run_graphed(key, s, [&](cudaStream_t st) { return fw_run(c, st); });
-      } else {
-        c.sink = sink;
-        rc = fw_run(c, s);
-      }
-      launches += c.launches;
+    int r = launch_to_store(dtype, dist, ld, n, store, D, N, N, Pw, ldpw, 1, s);
+    if (r) return r;
+    FwCtx c;
+    c.store = store; c.es = store_elem_size(store);
+    c.D = D; c.ld = N; c.P = Pw; c.ldp = ldpw; c.m = N; c.b = b; c.mode = IDX_PRED; c.via_off = 0;
+    c.st = &hdr_dev->status;
+    c.side = getenv("APSP_NO_LOOKAHEAD") ? nullptr : side_stream();
+    fw_carve(c, scratch, N);
+    if (getenv("APSP_NO_BULK")) c.prep[0] = c.prep[1] = nullptr;
+    // graph replay only where launch gaps dominate (N <= 2048): a graph drops the lookahead
+    // stream's priority, which costs more than the gaps at larger N (n=8192 21.6 -> 25 ms)
+    const int64_t Nsq = round_up(n, TILE_ALIGN);
+    // the persistent small-n schedules finish every row at once: a host-buffer call's band
+    // sink then gets all bands right after the kernel (same schedule, so the host and device
+    // APIs return identical pred)
+    auto sink_all = [&](int rc0) {
+      if (rc0 || !sink) return rc0;
+      const int64_t bandr = std::max<int64_t>(TILE_ALIGN, (N / 8 + TILE_ALIGN - 1) / TILE_ALIGN * TILE_ALIGN);
+      int q = 0;
+      for (int64_t r0 = 0; !q && r0 < N; r0 += bandr) q = sink->band(r0, std::min(N, r0 + bandr), c, s);
+      return q;
+    };
+    const bool persist_ok = !g_prof.on && !getenv("APSP_NO_PERSIST");
+    if (b_default && persist_ok && fw_persist64_enabled(store, N)) {
+      r = sink_all(launch_fw_persist64(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, pscratch, s));
+      c.launches += 2;
+    } else if (b == TILE_ALIGN && persist_ok && fw_persist_enabled(store, N)) {
+      r = sink_all(launch_fw_persist(reinterpret_cast<uint8_t*>(D), N, Pw, ldpw, N, pscratch, s));
+      c.launches += 2;
+    } else if (Nsq <= squaring_max_n() && bulk_store(store, Nsq) && !sink) {
+      c.m = Nsq;   // squaring works on the 128-aligned view (pad vertices are isolated)
+      int it = 0;
+      r = fw_square_run(c, hdr_dev, s, &it);
+      c.m = N;
+      sq_iters = it;
+    } else if (N <= 2048) {   // (no band sink here: the graph holds the whole chain)
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const GraphKey key{dev, 1, store, c.mode, N, b, D, Pw, scratch, c.side, s};
+      r = run_graphed(key, s, [&](cudaStream_t st) { return fw_run(c, st); });
+    } else {
+      c.sink = sink;
+      r = fw_run(c, s);
     }
-    bool ok = false;
-    tm.mark();   // device_ms: scan through the solve (the certificate readback syncs right after)
-    if (!rc) rc = certify(tier, store, D, N, n, n, scan, hdr_dev, hdr, s, ok);
+    launches += c.launches;
+    return r;
+  };
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const SpecKey skey{dev, dtype, b_default ? 0 : b, tier_req, (pred ? 1 : 0) | (sink ? 2 : 0) | (Pw == pred ? 4 : 0), n};
+  // the squaring schedule reads the header itself (its stop test): no speculation around it
+  const int guess = round_up(n, TILE_ALIGN) <= squaring_max_n() ? -1 : spec_lookup(skey);
+  std::vector<int> tiers;
+  bool spec_done = false;
+  if (guess >= 0) {
+    rc = attempt(guess);
+    if (!rc) {
+      tm.mark();
+      rc = launch_max_finite(tier_store(guess), D, N, n, n, &hdr_dev->cert, s);
+    }
+    if (!rc) rc = read_header(hdr_dev, hdr, s);
     if (rc) return rc;
     launches += 2;
-    if (ok) {
-      used = tier;
-      break;
-    }
+    spec_done = true;
+  } else {
+    rc = read_header(hdr_dev, hdr, s);
+    if (rc) return rc;
+  }
+  const ScanResult scan = hdr.scan;
+  rc = check_scan(scan);
+  if (rc) return rc;
+  if (scan.zero_offdiag && pred) {
+    rc = fw_classic_impl(dtype, n, dist, ld, pred, ldp, s, info);
+    if (!rc && info) info->flags |= FLAG_CLASSIC_FOR_ZERO_EDGES;
+    return rc;
+  }
+  tiers = pick_tiers(dtype, scan, tier_req, true, n);
+  if (tiers.empty()) return set_error(APSP_EINVAL, "tier %d cannot hold this input", tier_req);
+  const int first = tiers[0];
+  if (spec_done && first != guess) tried = 0;   // discarded: the loop below starts over
+  if (spec_done && tiers[0] == guess) {
+    bool ok = false;
+    rc = certify_check(guess, scan, hdr, ok);
+    if (rc) return rc;
+    tiers.erase(tiers.begin());
+    if (ok) used = guess;
+  }
+  for (size_t q = 0; used < 0 && q < tiers.size(); q++) {
+    const int tier = tiers[q];
+    rc = attempt(tier);
+    bool ok = false;
+    tm.mark();   // device_ms: scan through the solve (the certificate readback syncs right after)
+    if (!rc) rc = certify(tier, tier_store(tier), D, N, n, n, scan, hdr_dev, hdr, s, ok);
+    if (rc) return rc;
+    launches += 2;
+    if (ok) used = tier;
   }
   if (used < 0) {
     if (dtype == APSP_DTYPE_I32)
       return set_error(APSP_ERANGE, "shortest-path cost left the representable int32 range");
     return set_error(APSP_ERANGE, "no value tier could represent the result");
   }
+  // only a tier that was the scan's first pick is worth guessing (long-path graphs whose narrow
+  // certificates keep failing would otherwise waste a solve every call)
+  spec_remember(skey, used == first ? used : -1);
   rc = launch_from_store(tier_store(used), D, N, n, n, dtype, dist, ld, s);
   if (!rc && pred && Pw != pred) {
     rc = launch_copy_idx(P, N, n, n, APSP_DTYPE_I32, pred, ldp, s);
