@@ -2,6 +2,7 @@
 // result certificate (max finite), index copies and the minplus_product witness clear.
 // All are HBM-bound elementwise kernels: 2D grid-stride sweeps (rows over blockIdx.y, columns
 // over threads) -- no per-element 64-bit index division, coalesced along rows.
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -31,6 +32,38 @@ template <> struct Api<API_I64> { using T = int64_t; __device__ static bool fin(
 #define FOR_2D(i, j, rows, cols)                                                                         \
   for (int64_t i = blockIdx.y; i < (rows); i += gridDim.y)                                               \
     for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < (cols); j += int64_t(gridDim.x) * blockDim.x)
+
+// Unrolled vector sweep for the HBM-bound reductions: rows over blockIdx.y (grid-stride); in a
+// row each thread takes U segments blockDim.x apart per step and issues all U loads before using
+// any, so enough bytes are in flight on 4 CTAs per SM (one load per thread reached ~2 TB/s).
+template <int U, typename V, typename F>
+__device__ __forceinline__ void sweep_vec(const V* base, int64_t ldv, int64_t rows, int64_t cv, F&& f) {
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    const V* row = base + i * ldv;
+    for (int64_t jb = int64_t(blockIdx.x) * blockDim.x * U + threadIdx.x; jb < cv;
+         jb += int64_t(gridDim.x) * blockDim.x * U) {
+      V w[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t j = jb + int64_t(u) * blockDim.x;
+        if (j < cv) w[u] = __ldg(row + j);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t j = jb + int64_t(u) * blockDim.x;
+        if (j < cv) f(i, j, w[u]);
+      }
+    }
+  }
+}
+constexpr int kSweepU = 4;
+
+static dim3 grid_vec(int64_t rows, int64_t cv, int64_t ctas) {
+  int64_t gx = (cv + 256 * kSweepU - 1) / (256 * kSweepU);
+  gx = std::min<int64_t>(std::max<int64_t>(gx, 1), 16);
+  const int64_t gy = std::max<int64_t>(1, std::min<int64_t>({(ctas + gx - 1) / gx, rows, 65535}));
+  return dim3(unsigned(gx), unsigned(gy));
+}
 
 static dim3 grid_2d(int64_t rows, int64_t cols, int64_t ctas = 148 * 16) {
   int64_t gx = (cols + 255) / 256;
@@ -87,33 +120,41 @@ __device__ __forceinline__ void block_commit(ScanResult* out, uint32_t flags, lo
 }
 
 template <int D>
-struct ScanAcc {
+struct ScanAcc {   // per-thread flags as a bit set, the max in the input type (widened once, at the end)
   using T = typename Api<D>::T;
-  bool neg = false, diag = false, nonint = false, anyfin = false, zero = false;
-  unsigned long long edges = 0;
-  long long mx = -1;
-  float mxf = -1.f;
+  uint32_t flags = 0;
+  uint32_t edges = 0;   // a thread sees far fewer than 2^32 cells
+  T mx = T(-1);
   __device__ __forceinline__ void add(T v, bool on_diag) {
-    if (on_diag && v != T(0)) diag = true;
+    if (on_diag && v != T(0)) flags |= F_DIAG;
     if (!Api<D>::fin(v)) return;
-    anyfin = true;
-    if (!on_diag) edges++;
-    if (v == T(0) && !on_diag) zero = true;
+    flags |= F_ANYFIN;
+    if (!on_diag) {
+      edges++;
+      if (v == T(0)) flags |= F_ZERO;
+    }
     if constexpr (D == API_F32) {
       if (isnan(v) || v < 0.f) {
-        neg = true;
+        flags |= F_NEG;
         return;
       }
-      if (v != floorf(v)) nonint = true;
-      mxf = fmaxf(mxf, v);
-      mx = max(mx, (long long)fminf(v, 9.0e18f));
+      if (v != floorf(v)) flags |= F_NONINT;
+      mx = fmaxf(mx, v);
     } else {
       if (v < 0) {
-        neg = true;
+        flags |= F_NEG;
         return;
       }
-      mx = max(mx, (long long)v);
+      mx = max(mx, v);
     }
+  }
+  __device__ __forceinline__ long long max_ll() const {
+    if constexpr (D == API_F32) return mx < 0.f ? -1 : (long long)fminf(mx, 9.0e18f);
+    else return (long long)mx;
+  }
+  __device__ __forceinline__ float max_f() const {
+    if constexpr (D == API_F32) return mx;
+    else return -1.f;
   }
 };
 
@@ -126,22 +167,19 @@ __global__ void scan_kernel(const typename Api<D>::T* h, int64_t ld, int64_t row
   ScanAcc<D> a;
   if constexpr (sizeof(T) == 4) {
     if (vec) {
-      FOR_2D(i, j4, rows, cols / 4) {
-        const int4 w = __ldg(reinterpret_cast<const int4*>(h + i * ld) + j4);
+      sweep_vec<kSweepU>(reinterpret_cast<const int4*>(h), ld / 4, rows, cols / 4, [&](int64_t i, int64_t j4, int4 w) {
         const int64_t j = 4 * j4, dj = diag_off >= 0 ? i + diag_off - j : -1;
         a.add(__builtin_bit_cast(T, w.x), dj == 0);
         a.add(__builtin_bit_cast(T, w.y), dj == 1);
         a.add(__builtin_bit_cast(T, w.z), dj == 2);
         a.add(__builtin_bit_cast(T, w.w), dj == 3);
-      }
+      });
     }
   }
   if (!vec || sizeof(T) != 4) {
     FOR_2D(i, j, rows, cols) a.add(h[i * ld + j], diag_off >= 0 && j == i + diag_off);
   }
-  const uint32_t flags = (a.neg ? F_NEG : 0u) | (a.diag ? F_DIAG : 0u) | (a.nonint ? F_NONINT : 0u) |
-                         (a.anyfin ? F_ANYFIN : 0u) | (a.zero ? F_ZERO : 0u);
-  block_commit(out, flags, a.mx, a.mxf, a.edges);
+  block_commit(out, a.flags, a.max_ll(), a.max_f(), a.edges);
 }
 
 static bool vec4_ok(const void* p, int64_t ld, int64_t cols, size_t es) {
@@ -153,7 +191,7 @@ int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t c
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
   // max fields start at 0 after memset; negative sentinel not needed (values are >= 0)
   const int vec = vec4_ok(h, ld, cols, in_dtype == API_I64 ? 8 : 4);
-  const dim3 g = grid_2d(rows, vec ? cols / 4 : cols, kReduceCtas);
+  const dim3 g = vec ? grid_vec(rows, cols / 4, kReduceCtas) : grid_2d(rows, cols, kReduceCtas);
   switch (in_dtype) {
     case API_I32: scan_kernel<API_I32><<<g, 256, 0, s>>>((const int32_t*)h, ld, rows, cols, diag_off, out_dev, vec); break;
     case API_F32: scan_kernel<API_F32><<<g, 256, 0, s>>>((const float*)h, ld, rows, cols, diag_off, out_dev, vec); break;
@@ -367,6 +405,14 @@ template <int S>
 static int from_store_s(const void* in, int64_t ld, int64_t rows, int64_t cols, int out_dtype, void* out, int64_t ldo,
                         cudaStream_t s) {
   using TI = typename StoreT<S>::T;
+  // same representation on both sides (fp32 -> fp32, exact int32 -> int32, int64 -> int64):
+  // a strided copy
+  if ((S == STORE_F32 && out_dtype == API_F32) || (S == STORE_I32 && out_dtype == API_I32) ||
+      (S == STORE_I64 && out_dtype == API_I64)) {
+    APSP_CUDA_TRY(cudaMemcpy2DAsync(out, size_t(ldo) * sizeof(TI), in, size_t(ld) * sizeof(TI), size_t(cols) * sizeof(TI),
+                                    size_t(rows), cudaMemcpyDeviceToDevice, s));
+    return 0;
+  }
   const int vec = sizeof(TI) <= 2 && out_dtype != API_I64 && cols % 4 == 0 && ld % 4 == 0 && ldo % 4 == 0 &&
                   (reinterpret_cast<uintptr_t>(in) & (4 * sizeof(TI) - 1)) == 0 &&
                   (reinterpret_cast<uintptr_t>(out) & 15) == 0;
@@ -443,16 +489,28 @@ __global__ void max_finite_kernel(const typename StoreT<S>::T* D, int64_t ld, in
     if (vec) {   // 16 cells per step: INF bytes zeroed, then a packed byte max (the diagonal is 0,
                  // so a finite value always exists)
       uint32_t m4 = 0;
-      FOR_2D(i, j16, rows, cols / 16) {
-        const uint4 w = *reinterpret_cast<const uint4*>(D + i * ld + 16 * j16);
+      sweep_vec<kSweepU>(reinterpret_cast<const uint4*>(D), ld / 16, rows, cols / 16, [&](int64_t, int64_t, uint4 w) {
         const uint32_t x[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int q = 0; q < 4; q++) m4 = __vmaxu4(m4, x[q] & ~__vcmpeq4(x[q], 0xFFFFFFFFu));
-      }
+      });
       mx = max(max(m4 & 0xFF, (m4 >> 8) & 0xFF), max((m4 >> 16) & 0xFF, m4 >> 24));
     }
+  } else if constexpr (sizeof(typename StoreT<S>::T) == 4) {
+    if (vec) {   // 4 cells per 16-byte segment
+      sweep_vec<kSweepU>(reinterpret_cast<const uint4*>(D), ld / 4, rows, cols / 4, [&](int64_t, int64_t, uint4 w) {
+        const uint32_t x[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const auto v = __builtin_bit_cast(typename StoreT<S>::T, x[q]);
+          if (v == inf) continue;
+          if constexpr (S == STORE_F32) mxf = fmaxf(mxf, v);
+          else mx = max(mx, (long long)v);
+        }
+      });
+    }
   }
-  if (!(S == STORE_U8 && vec)) {
+  if (!vec || (S != STORE_U8 && sizeof(typename StoreT<S>::T) != 4)) {
     FOR_2D(i, j, rows, cols) {
       const auto v = D[i * ld + j];
       if (v == inf) continue;
@@ -466,8 +524,10 @@ __global__ void max_finite_kernel(const typename StoreT<S>::T* D, int64_t ld, in
 int launch_max_finite(int store, const void* D, int64_t ld, int64_t rows, int64_t cols, ScanResult* out_dev,
                       cudaStream_t s) {
   APSP_CUDA_TRY(cudaMemsetAsync(out_dev, 0, sizeof(ScanResult), s));
-  const int vec = store == STORE_U8 && cols % 16 == 0 && ld % 16 == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0;
-  const dim3 g = grid_2d(rows, vec ? cols / 16 : cols, kReduceCtas);
+  const size_t es = store_elem_size(store);
+  const int per = es == 1 ? 16 : 4;   // cells per 16-byte segment (u8, or the 4-byte stores)
+  const int vec = (es == 1 || es == 4) && cols % per == 0 && ld % per == 0 && (reinterpret_cast<uintptr_t>(D) & 15) == 0;
+  const dim3 g = vec ? grid_vec(rows, cols / per, kReduceCtas) : grid_2d(rows, cols, kReduceCtas);
   switch (store) {
     case STORE_U8: max_finite_kernel<STORE_U8><<<g, 256, 0, s>>>((const uint8_t*)D, ld, rows, cols, out_dev, vec); break;
     case STORE_W32: max_finite_kernel<STORE_W32><<<g, 256, 0, s>>>((const int32_t*)D, ld, rows, cols, out_dev, vec); break;

@@ -130,6 +130,7 @@ struct FwCtx {
   bool deep = false;             // two-deep lookahead (the next cross on the side stream)
   char* p2prep = nullptr;        // narrow tiers: bulk-copy layouts of the phase-2 operands
   char* sub = nullptr;           // scratch of the phase-1 sub-run when b > 128
+  int* spin = nullptr;           // 3a exit count the next closure waits for on the device
   int launches = 0;
   struct BandSink* sink = nullptr;   // last round in row bands, each handed to the sink
 };
@@ -226,7 +227,7 @@ size_t fw_scratch_bytes(int64_t m, int b, size_t es);
 
 void fw_carve(FwCtx& c, char* scratch, int64_t N);
 
-int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s);
+int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count = nullptr, int wait_target = 0);
 
 int fw_run(FwCtx& c, cudaStream_t s);
 

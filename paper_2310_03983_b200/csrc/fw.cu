@@ -627,8 +627,20 @@ __device__ __forceinline__ void close_dpx_body(typename CloseKeys<S>::T* D, int6
 template <int S, bool FULL>
 __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo,
                                                               int m, int32_t* idx, int64_t ldi, int mode,
-                                                              int64_t via_off, int prof) {
+                                                              int64_t via_off, int prof, const int* wait_count,
+                                                              int wait_target) {
   extern __shared__ __align__(16) unsigned char smraw_cu8[];
+  if (wait_count) {   // started ahead of its producer (fw_sched.cu): wait for the 3a count
+    if (threadIdx.x == 0) {
+      int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(wait_count) : "memory");
+        if (v >= wait_target) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
   close_dpx_body<S, FULL>(D, ld, lo, m, idx, ldi, mode, via_off, smraw_cu8, prof != 0);
 }
 
@@ -660,8 +672,10 @@ static int close_impl(void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, 
 }
 
 int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi, int mode,
-                       int64_t via_off, Status* st, cudaStream_t s) {
+                       int64_t via_off, Status* st, cudaStream_t s, const int* wait_count, int wait_target) {
   if (m <= 0) return 0;
+  if (wait_count && !((store == STORE_U8 || store == STORE_U16) && m == MAXB))
+    return set_error(APSP_EINVAL, "device-signalled closure start needs a full u8 / u16 block");
   if (m > MAXB) {
     // classic order over a larger block: per-k steps on the sub-view
     for (int64_t k = 0; k < m; k++) {
@@ -676,6 +690,8 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
   static const bool classic_close = getenv("APSP_CLASSIC_CLOSE") != nullptr;
   if (mode == IDX_PRED && close_blk_supported(store) && !classic_close)
     return launch_block_close_blk(store, D, ld, lo, m, idx, ldi, s);
+  if (wait_count && getenv("APSP_SLOW_CLOSE"))
+    return set_error(APSP_EINVAL, "device-signalled closure start needs the packed closure kernel");
   if ((store == STORE_U8 || store == STORE_U16) && !getenv("APSP_SLOW_CLOSE")) {
     static std::atomic<unsigned long long> attr8{0}, attr16{0};
     static std::atomic<unsigned long long> attr8f{0}, attr16f{0};
@@ -683,20 +699,21 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
     if (store == STORE_U8 && m == MAXB) {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8, true>, int(sb), attr8f));
       block_close_dpx_kernel<STORE_U8, true><<<1, 512, sb, s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
-                                                                mode, via_off, int(close_prof_on()));
+                                                                mode, via_off, int(close_prof_on()), wait_count,
+                                                                wait_target);
       if (close_prof_on()) close_prof_report();
     } else if (store == STORE_U8) {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8, false>, int(sb), attr8));
       block_close_dpx_kernel<STORE_U8, false><<<1, 512, sb, s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
-                                                                 mode, via_off, 0);
+                                                                 mode, via_off, 0, nullptr, 0);
     } else if (m == MAXB) {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16, true>, int(sb), attr16f));
       block_close_dpx_kernel<STORE_U16, true><<<1, 512, sb, s>>>(static_cast<uint16_t*>(D), ld, lo, int(m), idx,
-                                                                 ldi, mode, via_off, 0);
+                                                                 ldi, mode, via_off, 0, wait_count, wait_target);
     } else {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16, false>, int(sb), attr16));
       block_close_dpx_kernel<STORE_U16, false><<<1, 512, sb, s>>>(static_cast<uint16_t*>(D), ld, lo, int(m), idx,
-                                                                  ldi, mode, via_off, 0);
+                                                                  ldi, mode, via_off, 0, nullptr, 0);
     }
     APSP_CUDA_TRY(cudaGetLastError());
     count_launches(1);

@@ -18,6 +18,7 @@ size_t fw_scratch_bytes(int64_t m, int b, size_t es) {
   v += 3 * (prep_bytes(m, m, b) + 256);                 // phase-3 panel layouts (by round mod 3)
   v += 3 * (size_t(b) * m * 4 + 256);                   // phase-3 pivot-row pred snapshots (mod 3)
   v += prep_bytes(m, b, b) + 256;                       // phase-2 layouts (max of row/col product)
+  v += 256;                                             // 3a exit count (device-signalled closure)
   if (b > TILE_ALIGN) v += fw_scratch_bytes(b, TILE_ALIGN, es) + 256;   // phase-1 sub-run
   return v;
 }
@@ -42,6 +43,8 @@ void fw_carve(FwCtx& c, char* scratch, int64_t N) {
   }
   c.p2prep = p;
   p += prep_bytes(N, c.b, c.b) + 256;
+  c.spin = reinterpret_cast<int*>(p);
+  p += 256;
   if (c.b > TILE_ALIGN) c.sub = p;
 }
 
@@ -167,11 +170,13 @@ int run_graphed(const GraphKey& key, cudaStream_t s, F&& body) {
 
 }  // namespace
 
-int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s) {
+int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count, int wait_target) {
   NvtxRange r("apsp.fw.phase1");
   c.launches++;
   if (c.b <= TILE_ALIGN)
-    return launch_block_close(c.store, c.D, c.ld, k0, c.b, c.P, c.ldp, c.mode, c.via_off + k0, c.st, s);
+    return launch_block_close(c.store, c.D, c.ld, k0, c.b, c.P, c.ldp, c.mode, c.via_off + k0, c.st, s, wait_count,
+                              wait_target);
+  if (wait_count) return set_error(APSP_EINVAL, "device-signalled closure start needs b = 128");
   FwCtx sub = c;
   sub.D = c.D + (k0 * c.ld + k0) * c.es;
   sub.P = c.P ? c.P + k0 * c.ldp + k0 : nullptr;
@@ -307,7 +312,7 @@ static bool fine_round(const FwCtx& c, int64_t k0) {
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
 // additionally skips cross skip_next.
 int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaStream_t s, int64_t skip_next2 = -1,
-              bool pdl = true) {
+              bool pdl = true, int* exit_count = nullptr) {
   NvtxRange r(only_next >= 0 ? "apsp.fw.phase3a" : skip_next >= 0 ? "apsp.fw.phase3b" : "apsp.fw.phase3");
   MinplusArgs a = minplus_args();
   a.A = c.D + k0 * c.es; a.lda = c.ld;
@@ -332,6 +337,7 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   if (skip_next2 >= 0) { a.skip3_lo = skip_next2; a.skip3_hi = skip_next2 + c.b; }
   a.status = c.st;
   a.fine = fine_round(c, k0);
+  a.exit_count = exit_count;
   if (c.prep[0] && bulk_store(c.store, c.b)) {
     char* slot = c.prep[(k0 / c.b) % 3];
     a.Aprep = prep_a(slot);
@@ -438,6 +444,12 @@ static int fw_run_deep(FwCtx& c, cudaStream_t s) {
   return rc;
 }
 
+// CTAs of a 3a launch (grid_for's cross enumeration with 128 x 128 tiles, band width b)
+static int cross_ctas(int64_t m, int64_t b) {
+  const int64_t nt = m / TILE_ALIGN, w = b / TILE_ALIGN;
+  return int(w * nt + (nt - w) * w);
+}
+
 static bool deep_enabled(const FwCtx& c) {
   return c.side && c.prep[0] && bulk_store(c.store, c.b) && getenv("APSP_DEEP") && c.m >= 3 * c.b;
 }
@@ -458,6 +470,19 @@ int fw_run(FwCtx& c, cudaStream_t s) {
       return set_cuda_error(e, "lookahead events", __FILE__, __LINE__);
     }
   }
+  // Device-signalled closure start (packed u8 / u16 closure, b = 128, bulk 3a): the closure of
+  // K+1 waits for the 3a exit count instead of an event. Behind an event it was queued after 3b
+  // had filled every SM and waited ~10 us for a free slot (n=4096 timeline). The side stream is
+  // first ordered after the count's reset.
+  const bool spin = c.side && c.spin && b == TILE_ALIGN && (c.store == STORE_U8 || c.store == STORE_U16) &&
+                    c.prep[0] && bulk_store(c.store, b) && !getenv("APSP_NO_SPIN_CLOSE") && !getenv("APSP_SLOW_CLOSE");
+  int spin_target = 0;
+  if (spin) {
+    cudaError_t e = cudaMemsetAsync(c.spin, 0, sizeof(int), s);
+    if (e == cudaSuccess) e = cudaEventRecord(evA, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, evA, 0);
+    if (e != cudaSuccess) rc = set_cuda_error(e, "lookahead count reset", __FILE__, __LINE__);
+  }
   for (int64_t k0 = 0; !rc && k0 < c.m; k0 += b) {
     const int64_t k1 = k0 + b;
     if (k1 >= c.m && c.sink) {   // last round in row bands, each final as soon as it lands
@@ -469,6 +494,16 @@ int fw_run(FwCtx& c, cudaStream_t s) {
       }
     } else if (k1 >= c.m) {
       rc = fw_phase3(c, k0, -1, -1, s);
+    } else if (c.side && spin) {
+      // 3a counts its CTAs out; the next closure is queued on the side stream right behind the
+      // previous panels, so its CTA is resident before 3b fills the SMs, and starts on the count
+      rc = fw_phase3(c, k0, k1, -1, s, -1, true, c.spin);      // 3a: next pivot cross
+      spin_target += cross_ctas(c.m, b);
+      if (!rc) rc = fw_phase1(c, k1, c.side, c.spin, spin_target);
+      if (!rc) rc = fw_phase2(c, k1, c.side);
+      if (!rc && cudaEventRecord(evB, c.side) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
+      if (!rc) rc = fw_phase3(c, k0, -1, k1, s);               // 3b: the rest
+      if (!rc && cudaStreamWaitEvent(s, evB, 0) != cudaSuccess) rc = set_error(APSP_ECUDA, "stream wait");
     } else if (c.side) {
       rc = fw_phase3(c, k0, k1, -1, s);                       // 3a: next pivot cross
       if (!rc && cudaEventRecord(evA, s) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");

@@ -63,6 +63,10 @@ struct MinplusArgs {
   // Exact fp32 deferred-argmin kernel: detect improvements (and rescan) every 8 k instead of
   // every 32 -- cheaper when many cells improve per chunk (early FW rounds).
   int fine;
+  // Optional exit count (u8 / u16 bulk-staged kernels): every CTA, skipped or not, adds 1 here
+  // after its stores are fenced, so a kernel on another stream can start on the device as soon
+  // as this launch's count is reached (the FW closure after the 3a cross, fw_sched.cu).
+  int* exit_count;
 };
 
 // Lay the u8 operand panels out in the tile kernel's shared-memory format, once per product:
@@ -98,9 +102,11 @@ int launch_fw_persist64(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t
 bool close_blk_supported(int store);
 int launch_block_close_blk(int store, void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi,
                            cudaStream_t s);
+// wait_count (u8 / u16 full 128-blocks only): the closure kernel starts on the device once
+// *wait_count >= wait_target (acquire), instead of behind a stream event
 int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m,
                        int32_t* idx, int64_t ldi, int mode, int64_t via_off, Status* st,
-                       cudaStream_t s);
+                       cudaStream_t s, const int* wait_count = nullptr, int wait_target = 0);
 
 // Classic per-k Floyd-Warshall step (K1): bit-exact pred/via parity with fw_classic
 // (solvers.py:77-95).  One launch per k; row k / column k are invariant in step k.

@@ -62,7 +62,10 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int64_t i0, j0;
   tile_origin(p, BM, BN, i0, j0);
-  if (tile_skipped(p, i0, j0, BM, BN)) return;
+  if (tile_skipped(p, i0, j0, BM, BN)) {
+    if (p.exit_count && threadIdx.x == 0) atomicAdd(p.exit_count, 1);
+    return;
+  }
   const int t = threadIdx.x;
   const int nch = int(p.k / SUB);
   const uint32_t* Ap = p.Aprep + (i0 / BM) * int64_t(nch) * (SUB * BM);
@@ -304,6 +307,11 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   if constexpr (PEERS != 0) __threadfence_system();
   // one flag write per warp that changed (no CTA barrier needed)
   if (p.status && p.track_changed && __any_sync(0xffffffffu, changed) && lane == 0) p.status->changed = 1;
+  if (p.exit_count) {   // every thread's stores fenced, then one count per CTA
+    __threadfence();
+    __syncthreads();
+    if (t == 0) atomicAdd(p.exit_count, 1);
+  }
 }
 
 // panel layout kernels (one CTA per (tile, chunk); thread = one row x 16 k, or one k x 16 columns)
