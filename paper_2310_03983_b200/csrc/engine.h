@@ -227,7 +227,8 @@ size_t fw_scratch_bytes(int64_t m, int b, size_t es);
 
 void fw_carve(FwCtx& c, char* scratch, int64_t N);
 
-int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count = nullptr, int wait_target = 0);
+int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count = nullptr, int wait_target = 0,
+              uint32_t* nxA = nullptr, uint16_t* nxB = nullptr, int32_t* nxPred = nullptr, int64_t nxPredLd = 0);
 
 int fw_run(FwCtx& c, cudaStream_t s);
 

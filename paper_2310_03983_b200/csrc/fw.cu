@@ -628,7 +628,8 @@ template <int S, bool FULL>
 __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys<S>::T* D, int64_t ld, int64_t lo,
                                                               int m, int32_t* idx, int64_t ldi, int mode,
                                                               int64_t via_off, int prof, const int* wait_count,
-                                                              int wait_target) {
+                                                              int wait_target, uint32_t* nxA, uint16_t* nxB,
+                                                              int32_t* nxPred, int64_t nxPredLd) {
   extern __shared__ __align__(16) unsigned char smraw_cu8[];
   if (wait_count) {   // started ahead of its producer (fw_sched.cu): wait for the 3a count
     if (threadIdx.x == 0) {
@@ -642,6 +643,25 @@ __global__ void __launch_bounds__(512) block_close_dpx_kernel(typename CloseKeys
     __syncthreads();
   }
   close_dpx_body<S, FULL>(D, ld, lo, m, idx, ldi, mode, via_off, smraw_cu8, prof != 0);
+  if constexpr (FULL) {
+    if (nxA) {   // the closed block's layouts and pred rows for the next phase-2 launch (tiles.cuh)
+      using T = typename CloseKeys<S>::T;
+      __syncthreads();   // this CTA's value and pred stores are visible to all its threads
+      const T* Dg = D + lo * ld + lo;
+      auto get = [&](int r, int c0, T (&v)[16]) { load16_global(Dg + int64_t(r) * ld + c0, v); };
+      constexpr int NCH = MAXB / SUB;
+      const int64_t t0 = lo / MAXB;   // the diagonal tile's index in the panels
+      emit_layout_a<T, NtFormat<S>::TAG, NCH, 512>(get, nxA + t0 * NCH * (SUB * MAXB));
+      emit_layout_b<T, NtFormat<S>::TAG, NtFormat<S>::WIN, NCH, 512>(get, nxB + t0 * NCH * (SUB * MAXB));
+      if (nxPred && idx) {
+        CloseU8Smem& sm = *reinterpret_cast<CloseU8Smem*>(smraw_cu8);
+        for (int e = threadIdx.x; e < MAXB * MAXB; e += blockDim.x) {
+          const int i = e >> 7, j = e & 127;
+          nxPred[int64_t(i) * nxPredLd + lo + j] = sm.P[i][j];
+        }
+      }
+    }
+  }
 }
 
 static bool close_prof_on() {
@@ -672,9 +692,10 @@ static int close_impl(void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, 
 }
 
 int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi, int mode,
-                       int64_t via_off, Status* st, cudaStream_t s, const int* wait_count, int wait_target) {
+                       int64_t via_off, Status* st, cudaStream_t s, const int* wait_count, int wait_target,
+                       uint32_t* nxA, uint16_t* nxB, int32_t* nxPred, int64_t nxPredLd) {
   if (m <= 0) return 0;
-  if (wait_count && !((store == STORE_U8 || store == STORE_U16) && m == MAXB))
+  if ((wait_count || nxA) && !((store == STORE_U8 || store == STORE_U16) && m == MAXB && lo % MAXB == 0))
     return set_error(APSP_EINVAL, "device-signalled closure start needs a full u8 / u16 block");
   if (m > MAXB) {
     // classic order over a larger block: per-k steps on the sub-view
@@ -690,7 +711,7 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
   static const bool classic_close = getenv("APSP_CLASSIC_CLOSE") != nullptr;
   if (mode == IDX_PRED && close_blk_supported(store) && !classic_close)
     return launch_block_close_blk(store, D, ld, lo, m, idx, ldi, s);
-  if (wait_count && getenv("APSP_SLOW_CLOSE"))
+  if ((wait_count || nxA) && getenv("APSP_SLOW_CLOSE"))
     return set_error(APSP_EINVAL, "device-signalled closure start needs the packed closure kernel");
   if ((store == STORE_U8 || store == STORE_U16) && !getenv("APSP_SLOW_CLOSE")) {
     static std::atomic<unsigned long long> attr8{0}, attr16{0};
@@ -700,20 +721,21 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m, in
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8, true>, int(sb), attr8f));
       block_close_dpx_kernel<STORE_U8, true><<<1, 512, sb, s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
                                                                 mode, via_off, int(close_prof_on()), wait_count,
-                                                                wait_target);
+                                                                wait_target, nxA, nxB, nxPred, nxPredLd);
       if (close_prof_on()) close_prof_report();
     } else if (store == STORE_U8) {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U8, false>, int(sb), attr8));
       block_close_dpx_kernel<STORE_U8, false><<<1, 512, sb, s>>>(static_cast<uint8_t*>(D), ld, lo, int(m), idx, ldi,
-                                                                 mode, via_off, 0, nullptr, 0);
+                                                                 mode, via_off, 0, nullptr, 0, nullptr, nullptr, nullptr, 0);
     } else if (m == MAXB) {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16, true>, int(sb), attr16f));
       block_close_dpx_kernel<STORE_U16, true><<<1, 512, sb, s>>>(static_cast<uint16_t*>(D), ld, lo, int(m), idx,
-                                                                 ldi, mode, via_off, 0, wait_count, wait_target);
+                                                                 ldi, mode, via_off, 0, wait_count, wait_target, nxA, nxB,
+                                                                 nxPred, nxPredLd);
     } else {
       APSP_CUDA_TRY(smem_optin(block_close_dpx_kernel<STORE_U16, false>, int(sb), attr16));
       block_close_dpx_kernel<STORE_U16, false><<<1, 512, sb, s>>>(static_cast<uint16_t*>(D), ld, lo, int(m), idx,
-                                                                  ldi, mode, via_off, 0, nullptr, 0);
+                                                                  ldi, mode, via_off, 0, nullptr, 0, nullptr, nullptr, nullptr, 0);
     }
     APSP_CUDA_TRY(cudaGetLastError());
     count_launches(1);

@@ -170,13 +170,14 @@ int run_graphed(const GraphKey& key, cudaStream_t s, F&& body) {
 
 }  // namespace
 
-int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count, int wait_target) {
+int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count, int wait_target, uint32_t* nxA,
+              uint16_t* nxB, int32_t* nxPred, int64_t nxPredLd) {
   NvtxRange r("apsp.fw.phase1");
   c.launches++;
   if (c.b <= TILE_ALIGN)
     return launch_block_close(c.store, c.D, c.ld, k0, c.b, c.P, c.ldp, c.mode, c.via_off + k0, c.st, s, wait_count,
-                              wait_target);
-  if (wait_count) return set_error(APSP_EINVAL, "device-signalled closure start needs b = 128");
+                              wait_target, nxA, nxB, nxPred, nxPredLd);
+  if (wait_count || nxA) return set_error(APSP_EINVAL, "device-signalled closure start needs b = 128");
   FwCtx sub = c;
   sub.D = c.D + (k0 * c.ld + k0) * c.es;
   sub.P = c.P ? c.P + k0 * c.ldp + k0 : nullptr;
@@ -197,7 +198,12 @@ int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count, int w
 
 static bool fine_round(const FwCtx& c, int64_t k0);
 
-int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
+// prelaid: the cross launch's layouts and pred snapshot were already written by 3a and the
+// closure (fw_run's device-signalled schedule)
+// emit3: the cross launch writes the phase-3 layouts of its own tiles in place (the prep after
+// it goes away) and counts its CTAs out on emit3 (fw_run's device-signalled schedule)
+int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s, bool prelaid = false, const int* wait_count = nullptr,
+              int wait_target = 0, int* emit3 = nullptr) {
   NvtxRange r("apsp.fw.phase2");
   const int64_t b = c.b, m = c.m;
   char* Dg = c.D + (k0 * c.ld + k0) * c.es;
@@ -221,8 +227,9 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
     // back, is ordered before us) and are rebuilt from the updated panels right after.
     // the pred snapshot of the pivot rows rides along as the prep launch's third part
     char* slot = c.prep[(k0 / b) % 3];
-    rc = launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s,
-                          psnap ? c.P + k0 * c.ldp : nullptr, c.ldp, c.predsnap, m, m);
+    if (!prelaid)
+      rc = launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s,
+                            psnap ? c.P + k0 * c.ldp : nullptr, c.ldp, c.predsnap, m, m);
     if (rc) return rc;
     MinplusArgs x = minplus_args();
     x.A = colp; x.lda = c.ld;
@@ -238,9 +245,17 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s) {
     x.fine = fine_round(c, k0);
     x.Aprep = prep_a(slot);
     x.Bprep = prep_b(slot, m, b);
+    x.wait_count = wait_count;   // prelaid: 3a's layouts complete
+    x.wait_target = wait_target;
+    if (emit3) {   // in place: each layout tile is read only by the CTA that rewrites it (the
+                   // diagonal's, read by all, does not change: Dg (x) Dg never improves)
+      x.nxA = prep_a(slot);
+      x.nxB = prep_b(slot, m, b);
+      x.exit_count = emit3;
+    }
     c.launches += 5;
     rc = launch_minplus(c.store, x, s);
-    if (rc) return rc;
+    if (rc || emit3) return rc;
     // the phase-3 layouts; with the two-deep lookahead also the pivot rows' final pred (the next
     // cross, updated on the side stream while this round's phase 3 still gathers, writes them)
     const int q3 = int((k0 / b) % 3);
@@ -312,7 +327,9 @@ static bool fine_round(const FwCtx& c, int64_t k0) {
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
 // additionally skips cross skip_next.
 int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaStream_t s, int64_t skip_next2 = -1,
-              bool pdl = true, int* exit_count = nullptr) {
+              bool pdl = true, int* exit_count = nullptr, uint32_t* nxA = nullptr, uint16_t* nxB = nullptr,
+              int32_t* nxPred = nullptr, int64_t nxPredLd = 0, int* diag_flag = nullptr, int diag_value = 0,
+              const int* wait_count = nullptr, int wait_target = 0) {
   NvtxRange r(only_next >= 0 ? "apsp.fw.phase3a" : skip_next >= 0 ? "apsp.fw.phase3b" : "apsp.fw.phase3");
   MinplusArgs a = minplus_args();
   a.A = c.D + k0 * c.es; a.lda = c.ld;
@@ -338,6 +355,9 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   a.status = c.st;
   a.fine = fine_round(c, k0);
   a.exit_count = exit_count;
+  a.nxA = nxA; a.nxB = nxB; a.nxPred = nxPred; a.nxPredLd = nxPredLd;
+  a.diag_flag = diag_flag; a.diag_value = diag_value;
+  a.wait_count = wait_count; a.wait_target = wait_target;
   if (c.prep[0] && bulk_store(c.store, c.b)) {
     char* slot = c.prep[(k0 / c.b) % 3];
     a.Aprep = prep_a(slot);
@@ -476,15 +496,23 @@ int fw_run(FwCtx& c, cudaStream_t s) {
   // first ordered after the count's reset.
   const bool spin = c.side && c.spin && b == TILE_ALIGN && (c.store == STORE_U8 || c.store == STORE_U16) &&
                     c.prep[0] && bulk_store(c.store, b) && !getenv("APSP_NO_SPIN_CLOSE") && !getenv("APSP_SLOW_CLOSE");
-  int spin_target = 0;
+  int spin_target = 0, p2_target = 0;
+  const bool prelay = spin && c.p2prep && !getenv("APSP_NO_PRELAY");
+  const bool chain = prelay && c.mode == IDX_PRED && !c.deep && !getenv("APSP_NO_DEVCHAIN");
   if (spin) {
-    cudaError_t e = cudaMemsetAsync(c.spin, 0, sizeof(int), s);
+    // [0] 3a exit count, [1] diagonal flag, [2] cross-launch exit count
+    cudaError_t e = cudaMemsetAsync(c.spin, 0, 3 * sizeof(int), s);
     if (e == cudaSuccess) e = cudaEventRecord(evA, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, evA, 0);
     if (e != cudaSuccess) rc = set_cuda_error(e, "lookahead count reset", __FILE__, __LINE__);
   }
   for (int64_t k0 = 0; !rc && k0 < c.m; k0 += b) {
     const int64_t k1 = k0 + b;
+    if (k1 >= c.m && chain && k0 > 0) {   // the last round's panels: joined by a plain event
+      if (cudaEventRecord(evB, c.side) != cudaSuccess || cudaStreamWaitEvent(s, evB, 0) != cudaSuccess)
+        rc = set_error(APSP_ECUDA, "lookahead join");
+      if (rc) break;
+    }
     if (k1 >= c.m && c.sink) {   // last round in row bands, each final as soon as it lands
       const int64_t bandr = std::max<int64_t>(TILE_ALIGN, (c.m / 8 + TILE_ALIGN - 1) / TILE_ALIGN * TILE_ALIGN);
       for (int64_t r0 = 0; !rc && r0 < c.m; r0 += bandr) {
@@ -497,13 +525,32 @@ int fw_run(FwCtx& c, cudaStream_t s) {
     } else if (c.side && spin) {
       // 3a counts its CTAs out; the next closure is queued on the side stream right behind the
       // previous panels, so its CTA is resident before 3b fills the SMs, and starts on the count
-      rc = fw_phase3(c, k0, k1, -1, s, -1, true, c.spin);      // 3a: next pivot cross
+      // 3a and the closure also lay out the next cross launch's operands (no prep launch there)
+      char* nslot = c.prep[(k1 / b) % 3];
+      uint32_t* nxA = prelay ? prep_a(nslot) : nullptr;
+      uint16_t* nxB = prelay ? prep_b(nslot, c.m, b) : nullptr;
+      int32_t* nxP = prelay && c.P && c.mode == IDX_PRED ? c.predsnap : nullptr;
+      // The closure waits only for 3a's diagonal tile (its flag: round number), the cross launch
+      // for every 3a CTA (the exit count, once their layouts are out).
+      const int round = int(k1 / b);
+      // With the layouts pre-laid the cross launch also writes the phase-3 layouts (no prep after
+      // it), and the next 3a waits for its count on the device instead of an event (a stream
+      // event cost ~8 us per round). Only 3a's 2N/b - 1 CTAs ever spin for it: 3b is released
+      // by 3a's launch_dependents, which each 3a CTA issues after its wait.
+      const int* w3a = chain && k0 > 0 ? c.spin + 2 : nullptr;
+      rc = fw_phase3(c, k0, k1, -1, s, -1, true, c.spin, nxA, nxB, nxP, c.m, c.spin + 1, round, w3a, p2_target);
       spin_target += cross_ctas(c.m, b);
-      if (!rc) rc = fw_phase1(c, k1, c.side, c.spin, spin_target);
-      if (!rc) rc = fw_phase2(c, k1, c.side);
-      if (!rc && cudaEventRecord(evB, c.side) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
-      if (!rc) rc = fw_phase3(c, k0, -1, k1, s);               // 3b: the rest
-      if (!rc && cudaStreamWaitEvent(s, evB, 0) != cudaSuccess) rc = set_error(APSP_ECUDA, "stream wait");
+      if (!rc && prelay) rc = fw_phase1(c, k1, c.side, c.spin + 1, round, nxA, nxB, nxP, c.m);
+      else if (!rc) rc = fw_phase1(c, k1, c.side, c.spin, spin_target);   // the prep launch reads all of 3a
+      if (!rc) rc = fw_phase2(c, k1, c.side, prelay, prelay ? c.spin : nullptr, spin_target, chain ? c.spin + 2 : nullptr);
+      if (chain) {
+        p2_target += cross_ctas(c.m, b);
+        if (!rc) rc = fw_phase3(c, k0, -1, k1, s);             // 3b: the rest
+      } else {
+        if (!rc && cudaEventRecord(evB, c.side) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
+        if (!rc) rc = fw_phase3(c, k0, -1, k1, s);             // 3b: the rest
+        if (!rc && cudaStreamWaitEvent(s, evB, 0) != cudaSuccess) rc = set_error(APSP_ECUDA, "stream wait");
+      }
     } else if (c.side) {
       rc = fw_phase3(c, k0, k1, -1, s);                       // 3a: next pivot cross
       if (!rc && cudaEventRecord(evA, s) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
@@ -744,8 +791,11 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
   int dev = 0;
   cudaGetDevice(&dev);
   const SpecKey skey{dev, dtype, b_default ? 0 : b, tier_req, (pred ? 1 : 0) | (sink ? 2 : 0) | (Pw == pred ? 4 : 0), n};
-  // the squaring schedule reads the header itself (its stop test): no speculation around it
-  const int guess = round_up(n, TILE_ALIGN) <= squaring_max_n() ? -1 : spec_lookup(skey);
+  // No speculation around the squaring schedule (it reads the header itself: its stop test) or
+  // with a band sink: the sink streams the attempt's last round to the host as final rows, and
+  // an input that then turns out to need another path (zero-cost edges: the classic order)
+  // would leave them standing.
+  const int guess = round_up(n, TILE_ALIGN) <= squaring_max_n() || sink ? -1 : spec_lookup(skey);
   std::vector<int> tiers;
   bool spec_done = false;
   if (guess >= 0) {

@@ -67,6 +67,21 @@ struct MinplusArgs {
   // after its stores are fenced, so a kernel on another stream can start on the device as soon
   // as this launch's count is reached (the FW closure after the 3a cross, fw_sched.cu).
   int* exit_count;
+  // Optional next-round layouts (FW 3a with b = 128, u8 / u16 bulk kernel): the tiles of the
+  // cross [only_lo, only_hi) other than the diagonal also write themselves in the prep formats
+  // of the next phase-2 launch -- column-band tiles as A row tile i0/128 of nxA, row-band tiles
+  // as B column tile j0/128 of nxB plus their final pred rows into nxPred (ld nxPredLd).
+  uint32_t* nxA;
+  uint16_t* nxB;
+  int32_t* nxPred;
+  int64_t nxPredLd;
+  // Optional (same kernels): the CTA of the cross's diagonal tile stores diag_value to diag_flag
+  // (release) right after its own stores, ahead of the rest of the launch; and every CTA waits
+  // (acquire) until *wait_count >= wait_target before reading anything.
+  int* diag_flag;
+  int diag_value;
+  const int* wait_count;
+  int wait_target;
 };
 
 // Lay the u8 operand panels out in the tile kernel's shared-memory format, once per product:
@@ -104,9 +119,13 @@ int launch_block_close_blk(int store, void* D, int64_t ld, int64_t lo, int64_t m
                            cudaStream_t s);
 // wait_count (u8 / u16 full 128-blocks only): the closure kernel starts on the device once
 // *wait_count >= wait_target (acquire), instead of behind a stream event
+// nx* (same conditions): the closed block also writes its layouts / pred rows for the next
+// phase-2 launch (see MinplusArgs::nxA)
 int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m,
                        int32_t* idx, int64_t ldi, int mode, int64_t via_off, Status* st,
-                       cudaStream_t s, const int* wait_count = nullptr, int wait_target = 0);
+                       cudaStream_t s, const int* wait_count = nullptr, int wait_target = 0,
+                       uint32_t* nxA = nullptr, uint16_t* nxB = nullptr, int32_t* nxPred = nullptr,
+                       int64_t nxPredLd = 0);
 
 // Classic per-k Floyd-Warshall step (K1): bit-exact pred/via parity with fw_classic
 // (solvers.py:77-95).  One launch per k; row k / column k are invariant in step k.

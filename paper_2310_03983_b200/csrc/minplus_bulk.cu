@@ -20,12 +20,12 @@ namespace apsp {
 template <int S> struct Narrow;
 template <> struct Narrow<STORE_U8> {
   using T = uint8_t;
-  static constexpr int TAG = 7, WIN = 3, STAGES = 3;
+  static constexpr int TAG = NtFormat<STORE_U8>::TAG, WIN = NtFormat<STORE_U8>::WIN, STAGES = 3;
   static constexpr uint32_t INF = U8_INF;
 };
 template <> struct Narrow<STORE_U16> {
   using T = uint16_t;
-  static constexpr int TAG = 6, WIN = 1, STAGES = 3;
+  static constexpr int TAG = NtFormat<STORE_U16>::TAG, WIN = NtFormat<STORE_U16>::WIN, STAGES = 3;
   static constexpr uint32_t INF = U16_INF;
 };
 
@@ -34,7 +34,9 @@ template <int S>
 struct SmemNT {   // u8: 4 x 24 KB ring + 16 KB C = 112 KB (2 CTAs / SM); u16: 3 x 24 KB + 32 KB
   uint32_t As[Narrow<S>::STAGES][SUB][BM];
   uint16_t Bs[Narrow<S>::STAGES][SUB][BN];
-  typename Narrow<S>::T Cs[BM][BN];
+  // C staging; rows padded by 4 cells (u8: 4 bytes, u16: 8 bytes, keeping 8-byte alignment) so a warp reading one column segment of 32 rows hits 32
+  // banks (the next-round layout emission reads the tile transposed)
+  typename Narrow<S>::T Cs[BM][BN + 4];
   unsigned long long full[Narrow<S>::STAGES];   // bulk copy landed (tx count)
   unsigned int done[Narrow<S>::STAGES];         // warps finished with the slot's chunk
 };
@@ -58,11 +60,57 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   constexpr int CW = 4 * int(sizeof(T));          // bytes of one 4-cell C segment
   extern __shared__ __align__(128) unsigned char smraw_nt[];
   SmemNT<S>& sm = *reinterpret_cast<SmemNT<S>*>(smraw_nt);
-  // a dependent launch queued behind this kernel (pdl) may start as soon as every CTA is running
+  if (p.wait_count) {   // operands produced by a kernel on another stream (fw_sched.cu)
+    if (threadIdx.x == 0) {
+      int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.wait_count) : "memory");
+        if (v >= p.wait_target) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
+  // A dependent launch queued behind this kernel (pdl) may start as soon as every CTA is running
+  // -- and past its wait above: the dependent (FW 3b) reads what that wait guards.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int64_t i0, j0;
   tile_origin(p, BM, BN, i0, j0);
+  // next-round layouts (see MinplusArgs::nxA): this CTA's part, from a value getter
+  const bool nx_a = p.nxA && p.only_lo < p.only_hi && j0 == p.only_lo && i0 != p.only_lo;
+  const bool nx_b = p.nxA && p.only_lo < p.only_hi && i0 == p.only_lo && j0 != p.only_lo;
+  auto emit_next = [&](auto&& get) {
+    constexpr int NCHX = BN / SUB;
+    if (nx_a) {
+      emit_layout_a<T, TAG, NCHX, NT>(get, p.nxA + (i0 / BM) * int64_t(NCHX) * (SUB * BM));
+    } else {
+      emit_layout_b<T, TAG, WIN, NCHX, NT>(get, p.nxB + (j0 / BN) * int64_t(NCHX) * (SUB * BN));
+      if (p.nxPred && p.idx) {   // next pivot rows' pred: all 16 loads in flight, then the stores
+        constexpr int PER = BM * BN / 4 / NT;
+        int4 buf[PER];
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+          const int e = threadIdx.x + u * NT, r = e >> 5, q4 = 4 * (e & 31);
+          buf[u] = *reinterpret_cast<const int4*>(p.idx + (i0 + r) * p.ldi + j0 + q4);
+        }
+#pragma unroll
+        for (int u = 0; u < PER; u++) {
+          const int e = threadIdx.x + u * NT, r = e >> 5, q4 = 4 * (e & 31);
+          *reinterpret_cast<int4*>(p.nxPred + int64_t(r) * p.nxPredLd + j0 + q4) = buf[u];
+        }
+      }
+    }
+  };
   if (tile_skipped(p, i0, j0, BM, BN)) {
+    // a cross tile inside the current pivot's bands: final since phase 2, laid out from memory
+    if (nx_a || nx_b) {
+      const T* Cg = static_cast<const T*>(p.C) + i0 * p.ldc + j0;
+      emit_next([&](int r, int c0, T (&v)[16]) { load16_global(Cg + int64_t(r) * p.ldc + c0, v); });
+      if (p.exit_count) {
+        __threadfence();
+        __syncthreads();
+      }
+    }
     if (p.exit_count && threadIdx.x == 0) atomicAdd(p.exit_count, 1);
     return;
   }
@@ -307,6 +355,35 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   if constexpr (PEERS != 0) __threadfence_system();
   // one flag write per warp that changed (no CTA barrier needed)
   if (p.status && p.track_changed && __any_sync(0xffffffffu, changed) && lane == 0) p.status->changed = 1;
+  if (p.diag_flag && i0 == p.only_lo && j0 == p.only_lo) {   // the next closure's input is final
+    __threadfence();
+    __syncthreads();
+    if (t == 0) atomicExch(p.diag_flag, p.diag_value);
+  }
+  if (nx_a || nx_b) {   // uniform per CTA
+    {
+      // final values of every cell (acc = min(old, new) << TAG) -> the C staging tile
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+          if constexpr (sizeof(T) == 1)
+            *reinterpret_cast<uint32_t*>(&sm.Cs[ri][64 * h + 4 * tx]) =
+                __byte_perm(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG, 0x6420);
+          else
+            *reinterpret_cast<uint2*>(&sm.Cs[ri][64 * h + 4 * tx]) =
+                make_uint2(acc[r][2 * h] >> TAG, acc[r][2 * h + 1] >> TAG);
+        }
+      }
+      __syncthreads();   // also orders this CTA's pred stores before the pred copy
+      emit_next([&](int r, int c0, T (&v)[16]) {   // 4-byte words of a padded row: no bank conflict
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&sm.Cs[r][c0]);
+#pragma unroll
+        for (int q = 0; q < 4 * int(sizeof(T)); q++) reinterpret_cast<uint32_t*>(v)[q] = w[q];
+      });
+    }
+  }
   if (p.exit_count) {   // every thread's stores fenced, then one count per CTA
     __threadfence();
     __syncthreads();

@@ -48,6 +48,69 @@ __device__ __forceinline__ bool tile_skipped(const MinplusArgs& p, int64_t i0, i
   return rin || cin || r2 || c2 || r3 || c3;
 }
 
+// key format of the bulk-staged narrow tiles (minplus_bulk.cu Narrow<S>): key = v << TAG | tag,
+// tags 1..32*WIN per decode window
+template <int S> struct NtFormat;
+template <> struct NtFormat<STORE_U8> { static constexpr int TAG = 7, WIN = 3; };
+template <> struct NtFormat<STORE_U16> { static constexpr int TAG = 6, WIN = 1; };
+
+// ---- next-round operand layouts written by their producers (FW b = 128, u8 / u16) ----------
+// The phase-2 cross launch of round K+1 reads the column and row panels of pivot K+1 in the
+// prep_pair_kernel formats. All of them but the diagonal block are final when 3a(K) writes
+// them, the diagonal when the closure does; so the producers lay them out directly and the
+// separate prep launch (which waited for SM slots behind 3b) goes away. get(r, c) returns the
+// tile value at row r, column c (0..127); the layouts are those of prep_nt_a_body /
+// prep_nt_b_body: A = replicated key pairs [chunk][k][row], B = tagged keys [chunk][k][col].
+// load16(r, c0, v) fills v[0..15] with the tile row r, columns c0..c0+15 (c0 % 16 == 0).
+// NCH chunks of 32 k; every thread first loads all its segments (global sources: the loads
+// overlap instead of one L2 round trip per segment), then stores them
+template <typename T, int TAG, int NCH, int NTHR, typename L>
+__device__ __forceinline__ void emit_layout_a(L&& load16, uint32_t* Atile) {
+  constexpr int PER = NCH * 256 / NTHR;
+  T v[PER][16];
+#pragma unroll
+  for (int u = 0; u < PER; u++) {
+    const int e = threadIdx.x + u * NTHR, c = e >> 8, tt = e & 255, r = tt & 127, kb = 16 * (tt >> 7);
+    load16(r, c * SUB + kb, v[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; u++) {
+    const int e = threadIdx.x + u * NTHR, c = e >> 8, tt = e & 255, r = tt & 127, kb = 16 * (tt >> 7);
+    uint32_t* dst = Atile + int64_t(c) * (SUB * 128);
+#pragma unroll
+    for (int q = 0; q < 16; q++) dst[(kb + q) * 128 + r] = (uint32_t(v[u][q]) << TAG) * 0x00010001u;
+  }
+}
+template <typename T, int TAG, int WIN, int NCH, int NTHR, typename L>
+__device__ __forceinline__ void emit_layout_b(L&& load16, uint16_t* Btile) {
+  constexpr int PER = NCH * 256 / NTHR;
+  T v[PER][16];
+#pragma unroll
+  for (int u = 0; u < PER; u++) {
+    const int e = threadIdx.x + u * NTHR, c = e >> 8, tt = e & 255, kk = tt >> 3, cb = 16 * (tt & 7);
+    load16(c * SUB + kk, cb, v[u]);
+  }
+#pragma unroll
+  for (int u = 0; u < PER; u++) {
+    const int e = threadIdx.x + u * NTHR, c = e >> 8, tt = e & 255, kk = tt >> 3, cb = 16 * (tt & 7);
+    const uint32_t tag = uint32_t(SUB * (c % WIN) + kk + 1);
+    uint32_t o[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+      o[q] = ((uint32_t(v[u][2 * q]) << TAG) | tag) | (((uint32_t(v[u][2 * q + 1]) << TAG) | tag) << 16);
+    uint4* dst = reinterpret_cast<uint4*>(Btile + int64_t(c) * (SUB * 128) + kk * 128 + cb);
+    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+// 16 values of a row-major tile in global memory (16-byte aligned rows), for load16
+template <typename T>
+__device__ __forceinline__ void load16_global(const T* row, T (&v)[16]) {
+  const uint4* src = reinterpret_cast<const uint4*>(row);
+  reinterpret_cast<uint4*>(v)[0] = src[0];
+  if constexpr (sizeof(T) == 2) reinterpret_cast<uint4*>(v)[1] = src[1];
+}
+
 __device__ __forceinline__ void emit_idx(const MinplusArgs& p, int64_t i, int64_t j, uint32_t kk) {
   if (p.idx == nullptr) return;
   int32_t v = (p.mode == IDX_PRED) ? __ldg(p.predB + int64_t(kk) * p.ldp + j) : int32_t(p.inner_off + kk);

@@ -690,3 +690,11 @@ def test_speculative_tier_follows_the_input(cuda):
     assert np.array_equal(got, want_d) and np.array_equal(s.index.cpu().numpy().astype(np.int64), want_p)
     s = ap.solve(dev(narrow))
     assert np.array_equal(s.distances.cpu().numpy(), first["narrow"][0])
+    # host-buffer calls (band sink; no speculation) after same-shape calls match the device path,
+    # zero-cost edges (classic order) included
+    for raw in (narrow, narrow, zero, narrow):
+        h32 = dev(raw).cpu().numpy()
+        host = ap.solve(h32)
+        d = ap.solve(torch.from_numpy(h32).cuda())
+        assert np.array_equal(host.distances, d.distances.cpu().numpy())
+        assert np.array_equal(host.index, d.index.cpu().numpy())

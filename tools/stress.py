@@ -94,7 +94,7 @@ def main():
             fails += extra_case(rng, "-v" in sys.argv)
             continue
         small = rng.random() < 0.7
-        n = int(rng.integers(1, 700)) if small else int(rng.choice([2176, 2304, 2560, 3072]))
+        n = int(rng.integers(1, 700)) if small else int(rng.choice([2176, 2304, 2560, 3072, 3200, 4096]))
         raw, dens, wmax = rand_raw(rng, n)
         h = ap.CostMatrix(raw.copy(), _validated=True)
         tag = f"n={n} dens={dens} wmax={wmax} zeros={int((raw == 0).sum()) - n}"
@@ -142,6 +142,12 @@ def main():
                 host = ap.solve(h32)
                 assert np.array_equal(host.distances, dev.distances.cpu().numpy()), "host32 dist"
                 assert np.array_equal(host.index, dev.index.cpu().numpy()), "host32 pred"
+                # an independent schedule (R-Kleene) and the pred certificate on the device
+                hd = torch.from_numpy(h32.copy()).cuda()
+                rk = ap.solve(hd, "rkleene", track="pred", base_threshold=1024)
+                assert torch.equal(rk.distances, dev.distances), "fw == rkleene"
+                ok, why = ap.check_pred_tree(hd, dev.distances, dev.index, INF32)
+                assert ok, f"large pred: {why}"
                 r64 = ap.fw_classic(ap.CostMatrix(np.where(raw == INF_RAW, INF_RAW, np.minimum(raw, 2 ** 20))))
                 d64 = np.where(host.distances == INF32, INF_RAW, host.distances.astype(np.int64))
                 assert np.array_equal(r64.distances.raw, d64), "int64 api dist"
