@@ -130,7 +130,8 @@ struct FwCtx {
   bool deep = false;             // two-deep lookahead (the next cross on the side stream)
   char* p2prep = nullptr;        // narrow tiers: bulk-copy layouts of the phase-2 operands
   char* sub = nullptr;           // scratch of the phase-1 sub-run when b > 128
-  int* spin = nullptr;           // 3a exit count the next closure waits for on the device
+  int* spin = nullptr;           // device-signalled chain: exit counts and the diagonal flag
+  int* tflags = nullptr;         // per-tile round flags of the device-signalled chain
   int launches = 0;
   struct BandSink* sink = nullptr;   // last round in row bands, each handed to the sink
 };

@@ -18,7 +18,8 @@ size_t fw_scratch_bytes(int64_t m, int b, size_t es) {
   v += 3 * (prep_bytes(m, m, b) + 256);                 // phase-3 panel layouts (by round mod 3)
   v += 3 * (size_t(b) * m * 4 + 256);                   // phase-3 pivot-row pred snapshots (mod 3)
   v += prep_bytes(m, b, b) + 256;                       // phase-2 layouts (max of row/col product)
-  v += 256;                                             // 3a exit count (device-signalled closure)
+  v += 256;                                             // device-signalled chain: counts and flags
+  v += size_t(m / TILE_ALIGN) * (m / TILE_ALIGN) * 4 + 256;   // per-tile round flags
   if (b > TILE_ALIGN) v += fw_scratch_bytes(b, TILE_ALIGN, es) + 256;   // phase-1 sub-run
   return v;
 }
@@ -45,6 +46,8 @@ void fw_carve(FwCtx& c, char* scratch, int64_t N) {
   p += prep_bytes(N, c.b, c.b) + 256;
   c.spin = reinterpret_cast<int*>(p);
   p += 256;
+  c.tflags = reinterpret_cast<int*>(p);
+  p += size_t(N / TILE_ALIGN) * (N / TILE_ALIGN) * 4 + 256;
   if (c.b > TILE_ALIGN) c.sub = p;
 }
 
@@ -170,6 +173,36 @@ int run_graphed(const GraphKey& key, cudaStream_t s, F&& body) {
 
 }  // namespace
 
+// Device-side signals of one product launch in the b = 128 device-signalled round chain (see
+// fw_run and the MinplusArgs fields of the same names).
+struct FwSignals {
+  int* exit_count = nullptr;
+  uint32_t* nxA = nullptr;
+  uint16_t* nxB = nullptr;
+  int32_t* nxPred = nullptr;
+  int64_t nxPredLd = 0;
+  int* diag_flag = nullptr;
+  int diag_value = 0;
+  const int* wait_count = nullptr;
+  int wait_target = 0;
+  int* tile_flags = nullptr;
+  int tile_ld = 0;
+  int tile_round = 0;
+  int64_t first_lo = -1;   // 3b: enumerate this pivot cross first (width b)
+  bool pdl = false;        // launch behind the previous kernel with programmatic serialization
+};
+
+static void apply_signals(MinplusArgs& a, const FwSignals* g, int64_t b) {
+  if (!g) return;
+  a.exit_count = g->exit_count;
+  a.nxA = g->nxA; a.nxB = g->nxB; a.nxPred = g->nxPred; a.nxPredLd = g->nxPredLd;
+  a.diag_flag = g->diag_flag; a.diag_value = g->diag_value;
+  a.wait_count = g->wait_count; a.wait_target = g->wait_target;
+  a.tile_flags = g->tile_flags; a.tile_ld = g->tile_ld; a.tile_round = g->tile_round;
+  if (g->first_lo >= 0) { a.first_lo = g->first_lo; a.first_hi = g->first_lo + b; }
+  if (g->pdl && !getenv("APSP_NO_PDL")) a.pdl = 1;
+}
+
 int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count, int wait_target, uint32_t* nxA,
               uint16_t* nxB, int32_t* nxPred, int64_t nxPredLd) {
   NvtxRange r("apsp.fw.phase1");
@@ -202,8 +235,8 @@ static bool fine_round(const FwCtx& c, int64_t k0);
 // closure (fw_run's device-signalled schedule)
 // emit3: the cross launch writes the phase-3 layouts of its own tiles in place (the prep after
 // it goes away) and counts its CTAs out on emit3 (fw_run's device-signalled schedule)
-int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s, bool prelaid = false, const int* wait_count = nullptr,
-              int wait_target = 0, int* emit3 = nullptr) {
+int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s, bool prelaid = false, const FwSignals* sig = nullptr,
+              bool emit3 = false) {
   NvtxRange r("apsp.fw.phase2");
   const int64_t b = c.b, m = c.m;
   char* Dg = c.D + (k0 * c.ld + k0) * c.es;
@@ -245,13 +278,11 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s, bool prelaid = false, const 
     x.fine = fine_round(c, k0);
     x.Aprep = prep_a(slot);
     x.Bprep = prep_b(slot, m, b);
-    x.wait_count = wait_count;   // prelaid: 3a's layouts complete
-    x.wait_target = wait_target;
+    apply_signals(x, sig, b);   // prelaid: waits for 3a's layouts; chain: counts out, tile flags
     if (emit3) {   // in place: each layout tile is read only by the CTA that rewrites it (the
                    // diagonal's, read by all, does not change: Dg (x) Dg never improves)
       x.nxA = prep_a(slot);
       x.nxB = prep_b(slot, m, b);
-      x.exit_count = emit3;
     }
     c.launches += 5;
     rc = launch_minplus(c.store, x, s);
@@ -327,9 +358,7 @@ static bool fine_round(const FwCtx& c, int64_t k0) {
 // phase 3 of pivot block k0; only_next >= 0 restricts to cross only_next, skip_next >= 0
 // additionally skips cross skip_next.
 int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaStream_t s, int64_t skip_next2 = -1,
-              bool pdl = true, int* exit_count = nullptr, uint32_t* nxA = nullptr, uint16_t* nxB = nullptr,
-              int32_t* nxPred = nullptr, int64_t nxPredLd = 0, int* diag_flag = nullptr, int diag_value = 0,
-              const int* wait_count = nullptr, int wait_target = 0) {
+              bool pdl = true, const FwSignals* sig = nullptr) {
   NvtxRange r(only_next >= 0 ? "apsp.fw.phase3a" : skip_next >= 0 ? "apsp.fw.phase3b" : "apsp.fw.phase3");
   MinplusArgs a = minplus_args();
   a.A = c.D + k0 * c.es; a.lda = c.ld;
@@ -354,10 +383,7 @@ int fw_phase3(FwCtx& c, int64_t k0, int64_t only_next, int64_t skip_next, cudaSt
   if (skip_next2 >= 0) { a.skip3_lo = skip_next2; a.skip3_hi = skip_next2 + c.b; }
   a.status = c.st;
   a.fine = fine_round(c, k0);
-  a.exit_count = exit_count;
-  a.nxA = nxA; a.nxB = nxB; a.nxPred = nxPred; a.nxPredLd = nxPredLd;
-  a.diag_flag = diag_flag; a.diag_value = diag_value;
-  a.wait_count = wait_count; a.wait_target = wait_target;
+  apply_signals(a, sig, c.b);
   if (c.prep[0] && bulk_store(c.store, c.b)) {
     char* slot = c.prep[(k0 / c.b) % 3];
     a.Aprep = prep_a(slot);
@@ -478,8 +504,29 @@ int fw_run(FwCtx& c, cudaStream_t s) {
   const int64_t b = c.b;
   c.deep = deep_enabled(c);
   if (c.deep) return fw_run_deep(c, s);
+  // Device-signalled round chain (packed u8 / u16 closure, b = 128, bulk tiles):
+  //   spin    the closure of K+1 starts on a device flag instead of behind a stream event (queued
+  //           on the side stream early, its CTA is resident before 3b fills the SMs);
+  //   prelay  3a and the closure lay out the next cross launch's operands (no prep launch);
+  //   chain   the cross launch writes the phase-3 layouts in place, every product launch waits
+  //           on per-tile round flags / exit counts instead of events, 3a runs behind the
+  //           previous 3b with programmatic serialization and 3b enumerates the next 3a's
+  //           tiles first, so a round starts while the previous one's last wave drains.
+  const bool spin = c.side && c.spin && c.tflags && b == TILE_ALIGN && (c.store == STORE_U8 || c.store == STORE_U16) &&
+                    c.prep[0] && bulk_store(c.store, b) && !getenv("APSP_NO_SPIN_CLOSE") && !getenv("APSP_SLOW_CLOSE");
+  const bool prelay = spin && c.p2prep && !getenv("APSP_NO_PRELAY");
+  const bool chain = prelay && c.mode == IDX_PRED && !getenv("APSP_NO_DEVCHAIN");
+  const int nt = int(c.m / TILE_ALIGN);
+  if (spin) {   // [0] 3a exit count, [1] diagonal flag, [2] cross-launch exit count; tile flags
+    APSP_CUDA_TRY(cudaMemsetAsync(c.spin, 0, 3 * sizeof(int), s));
+    if (chain) APSP_CUDA_TRY(cudaMemsetAsync(c.tflags, 0, size_t(nt) * nt * sizeof(int), s));
+  }
+  FwSignals sig0;
+  if (chain) {   // round 0's panels also release their tiles' flags
+    sig0.tile_flags = c.tflags; sig0.tile_ld = nt; sig0.tile_round = 0;
+  }
   int rc = fw_phase1(c, 0, s);
-  if (!rc) rc = fw_phase2(c, 0, s);
+  if (!rc) rc = fw_phase2(c, 0, s, false, chain ? &sig0 : nullptr);
   if (rc) return rc;
   cudaEvent_t evA = nullptr, evB = nullptr;
   if (c.side) {
@@ -490,24 +537,14 @@ int fw_run(FwCtx& c, cudaStream_t s) {
       return set_cuda_error(e, "lookahead events", __FILE__, __LINE__);
     }
   }
-  // Device-signalled closure start (packed u8 / u16 closure, b = 128, bulk 3a): the closure of
-  // K+1 waits for the 3a exit count instead of an event. Behind an event it was queued after 3b
-  // had filled every SM and waited ~10 us for a free slot (n=4096 timeline). The side stream is
-  // first ordered after the count's reset.
-  const bool spin = c.side && c.spin && b == TILE_ALIGN && (c.store == STORE_U8 || c.store == STORE_U16) &&
-                    c.prep[0] && bulk_store(c.store, b) && !getenv("APSP_NO_SPIN_CLOSE") && !getenv("APSP_SLOW_CLOSE");
   int spin_target = 0, p2_target = 0;
-  const bool prelay = spin && c.p2prep && !getenv("APSP_NO_PRELAY");
-  const bool chain = prelay && c.mode == IDX_PRED && !c.deep && !getenv("APSP_NO_DEVCHAIN");
-  if (spin) {
-    // [0] 3a exit count, [1] diagonal flag, [2] cross-launch exit count
-    cudaError_t e = cudaMemsetAsync(c.spin, 0, 3 * sizeof(int), s);
-    if (e == cudaSuccess) e = cudaEventRecord(evA, s);
+  if (spin) {   // the side stream starts after the resets and round 0's panels
+    cudaError_t e = cudaEventRecord(evA, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, evA, 0);
-    if (e != cudaSuccess) rc = set_cuda_error(e, "lookahead count reset", __FILE__, __LINE__);
+    if (e != cudaSuccess) rc = set_cuda_error(e, "lookahead start", __FILE__, __LINE__);
   }
   for (int64_t k0 = 0; !rc && k0 < c.m; k0 += b) {
-    const int64_t k1 = k0 + b;
+    const int64_t k1 = k0 + b, k2 = k1 + b;
     if (k1 >= c.m && chain && k0 > 0) {   // the last round's panels: joined by a plain event
       if (cudaEventRecord(evB, c.side) != cudaSuccess || cudaStreamWaitEvent(s, evB, 0) != cudaSuccess)
         rc = set_error(APSP_ECUDA, "lookahead join");
@@ -523,29 +560,42 @@ int fw_run(FwCtx& c, cudaStream_t s) {
     } else if (k1 >= c.m) {
       rc = fw_phase3(c, k0, -1, -1, s);
     } else if (c.side && spin) {
-      // 3a counts its CTAs out; the next closure is queued on the side stream right behind the
-      // previous panels, so its CTA is resident before 3b fills the SMs, and starts on the count
-      // 3a and the closure also lay out the next cross launch's operands (no prep launch there)
+      const int round = int(k0 / b);
       char* nslot = c.prep[(k1 / b) % 3];
-      uint32_t* nxA = prelay ? prep_a(nslot) : nullptr;
-      uint16_t* nxB = prelay ? prep_b(nslot, c.m, b) : nullptr;
-      int32_t* nxP = prelay && c.P && c.mode == IDX_PRED ? c.predsnap : nullptr;
-      // The closure waits only for 3a's diagonal tile (its flag: round number), the cross launch
-      // for every 3a CTA (the exit count, once their layouts are out).
-      const int round = int(k1 / b);
-      // With the layouts pre-laid the cross launch also writes the phase-3 layouts (no prep after
-      // it), and the next 3a waits for its count on the device instead of an event (a stream
-      // event cost ~8 us per round). Only 3a's 2N/b - 1 CTAs ever spin for it: 3b is released
-      // by 3a's launch_dependents, which each 3a CTA issues after its wait.
-      const int* w3a = chain && k0 > 0 ? c.spin + 2 : nullptr;
-      rc = fw_phase3(c, k0, k1, -1, s, -1, true, c.spin, nxA, nxB, nxP, c.m, c.spin + 1, round, w3a, p2_target);
+      // 3a(K): the cross of K+1. It releases the diagonal flag (the closure of K+1 reads only that
+      // tile) and counts out once its layouts for the cross launch are written. In the chain it
+      // waits for the cross launch of K (count) and its tiles' flags, and runs behind 3b(K-1).
+      FwSignals g3a;
+      g3a.exit_count = c.spin;
+      g3a.diag_flag = c.spin + 1; g3a.diag_value = round + 1;
+      if (prelay) {
+        g3a.nxA = prep_a(nslot); g3a.nxB = prep_b(nslot, c.m, b);
+        g3a.nxPred = c.P && c.mode == IDX_PRED ? c.predsnap : nullptr; g3a.nxPredLd = c.m;
+      }
+      if (chain) {
+        g3a.tile_flags = c.tflags; g3a.tile_ld = nt; g3a.tile_round = round;
+        if (k0 > 0) { g3a.wait_count = c.spin + 2; g3a.wait_target = p2_target; g3a.pdl = true; }
+      }
+      rc = fw_phase3(c, k0, k1, -1, s, -1, true, &g3a);
       spin_target += cross_ctas(c.m, b);
-      if (!rc && prelay) rc = fw_phase1(c, k1, c.side, c.spin + 1, round, nxA, nxB, nxP, c.m);
-      else if (!rc) rc = fw_phase1(c, k1, c.side, c.spin, spin_target);   // the prep launch reads all of 3a
-      if (!rc) rc = fw_phase2(c, k1, c.side, prelay, prelay ? c.spin : nullptr, spin_target, chain ? c.spin + 2 : nullptr);
+      // closure(K+1) on the side stream: the diagonal flag (prelay) or all of 3a (the prep reads it)
+      if (!rc && prelay) rc = fw_phase1(c, k1, c.side, c.spin + 1, round + 1, g3a.nxA, g3a.nxB, g3a.nxPred, c.m);
+      else if (!rc) rc = fw_phase1(c, k1, c.side, c.spin, spin_target);
+      // the cross launch of K+1: waits for 3a's count; in the chain it also writes the phase-3
+      // layouts in place and counts out for the next 3a
+      FwSignals gp2;
+      if (prelay) { gp2.wait_count = c.spin; gp2.wait_target = spin_target; }
+      if (chain) {
+        gp2.exit_count = c.spin + 2;
+        gp2.tile_flags = c.tflags; gp2.tile_ld = nt; gp2.tile_round = round + 1;
+      }
+      if (!rc) rc = fw_phase2(c, k1, c.side, prelay, prelay ? &gp2 : nullptr, chain);
       if (chain) {
         p2_target += cross_ctas(c.m, b);
-        if (!rc) rc = fw_phase3(c, k0, -1, k1, s);             // 3b: the rest
+        FwSignals g3b;   // 3b(K): tile flags, the next 3a's tiles (cross of K+2) first
+        g3b.tile_flags = c.tflags; g3b.tile_ld = nt; g3b.tile_round = round;
+        if (k2 < c.m) g3b.first_lo = k2;
+        if (!rc) rc = fw_phase3(c, k0, -1, k1, s, -1, true, &g3b);
       } else {
         if (!rc && cudaEventRecord(evB, c.side) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
         if (!rc) rc = fw_phase3(c, k0, -1, k1, s);             // 3b: the rest

@@ -82,6 +82,16 @@ struct MinplusArgs {
   int diag_value;
   const int* wait_count;
   int wait_target;
+  // Optional per-tile round flags (FW b = 128 device-signalled chain, u8 / u16 bulk kernel): the
+  // CTA of tile (I, J) waits until tile_flags[I * tile_ld + J] >= tile_round (the previous round
+  // has updated it), and releases tile_round + 1 after its stores. Lets a launch start while the
+  // previous round's last wave drains.
+  int* tile_flags;
+  int tile_ld;
+  int tile_round;
+  // Full-grid launches: if first_lo < first_hi the (1D) grid enumerates the tiles of the cross
+  // [first_lo, first_hi) first, then the rest row-major (FW 3b: the next 3a's inputs first).
+  int64_t first_lo, first_hi;
 };
 
 // Lay the u8 operand panels out in the tile kernel's shared-memory format, once per product:
@@ -99,6 +109,7 @@ inline MinplusArgs minplus_args() {
   a.skip2_lo = a.skip2_hi = -1;
   a.skip3_lo = a.skip3_hi = -1;
   a.only_lo = a.only_hi = -1;
+  a.first_lo = a.first_hi = -1;
   return a;
 }
 

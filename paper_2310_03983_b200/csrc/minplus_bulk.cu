@@ -71,11 +71,24 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
     }
     __syncthreads();
   }
-  // A dependent launch queued behind this kernel (pdl) may start as soon as every CTA is running
-  // -- and past its wait above: the dependent (FW 3b) reads what that wait guards.
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   int64_t i0, j0;
   tile_origin(p, BM, BN, i0, j0);
+  int* tflag = nullptr;   // this tile's round flag (see MinplusArgs::tile_flags)
+  if (p.tile_flags && !tile_skipped(p, i0, j0, BM, BN)) {
+    tflag = p.tile_flags + (i0 / BM) * p.tile_ld + j0 / BN;
+    if (threadIdx.x == 0) {
+      int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(tflag) : "memory");
+        if (v >= p.tile_round) break;
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+  }
+  // A dependent launch queued behind this kernel (pdl) may start as soon as every CTA is running
+  // -- and past its waits above: the dependent (FW 3b) reads what those waits guard.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // next-round layouts (see MinplusArgs::nxA): this CTA's part, from a value getter
   const bool nx_a = p.nxA && p.only_lo < p.only_hi && j0 == p.only_lo && i0 != p.only_lo;
   const bool nx_b = p.nxA && p.only_lo < p.only_hi && i0 == p.only_lo && j0 != p.only_lo;
@@ -359,6 +372,11 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
     __threadfence();
     __syncthreads();
     if (t == 0) atomicExch(p.diag_flag, p.diag_value);
+  }
+  if (tflag) {   // this round's update of the tile is stored
+    __threadfence();
+    __syncthreads();
+    if (t == 0) atomicExch(tflag, p.tile_round + 1);
   }
   if (nx_a || nx_b) {   // uniform per CTA
     {

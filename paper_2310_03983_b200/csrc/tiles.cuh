@@ -32,6 +32,24 @@ __device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn
       i0 = int64_t(rr < lo_r ? rr : rr + wr) * bm;
       j0 = int64_t(lo_c + cc) * bn;
     }
+  } else if (p.first_lo < p.first_hi) {   // 1D: the cross of [first_lo, first_hi) first, then the rest
+    const int w = int((p.first_hi - p.first_lo) / bm), lo_t = int(p.first_lo / bm);   // square tiles
+    const int nt_r = int((p.m + bm - 1) / bm), nt_c = int((p.n + bn - 1) / bn);
+    const int id = int(blockIdx.x), ncross = w * nt_c + (nt_r - w) * w;
+    if (id < ncross) {
+      if (id < w * nt_c) {
+        i0 = int64_t(lo_t + id / nt_c) * bm;
+        j0 = int64_t(id % nt_c) * bn;
+      } else {
+        const int id2 = id - w * nt_c, rr = id2 / w, cc = id2 % w;
+        i0 = int64_t(rr < lo_t ? rr : rr + w) * bm;
+        j0 = int64_t(lo_t + cc) * bn;
+      }
+    } else {
+      const int id3 = id - ncross, rr = id3 / (nt_c - w), cc = id3 % (nt_c - w);
+      i0 = int64_t(rr < lo_t ? rr : rr + w) * bm;
+      j0 = int64_t(cc < lo_t ? cc : cc + w) * bn;
+    }
   } else {
     i0 = int64_t(blockIdx.y) * bm;
     j0 = int64_t(blockIdx.x) * bn;
@@ -185,6 +203,7 @@ inline dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
     const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
     return dim3(unsigned(wr * nt_c + (nt_r - wr) * wc), 1);
   }
+  if (a.first_lo < a.first_hi) return dim3(unsigned(((a.n + bn - 1) / bn) * ((a.m + bm - 1) / bm)), 1);
   return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
 }
 
