@@ -190,6 +190,7 @@ struct FwSignals {
   int tile_round = 0;
   int64_t first_lo = -1;   // 3b: enumerate this pivot cross first (width b)
   bool pdl = false;        // launch behind the previous kernel with programmatic serialization
+  bool split_rows = false; // two half-row CTAs per tile (the latency-bound cross launches)
 };
 
 static void apply_signals(MinplusArgs& a, const FwSignals* g, int64_t b) {
@@ -201,6 +202,7 @@ static void apply_signals(MinplusArgs& a, const FwSignals* g, int64_t b) {
   a.tile_flags = g->tile_flags; a.tile_ld = g->tile_ld; a.tile_round = g->tile_round;
   if (g->first_lo >= 0) { a.first_lo = g->first_lo; a.first_hi = g->first_lo + b; }
   if (g->pdl && !getenv("APSP_NO_PDL")) a.pdl = 1;
+  a.split_rows = g->split_rows ? 1 : 0;
 }
 
 int fw_phase1(FwCtx& c, int64_t k0, cudaStream_t s, const int* wait_count, int wait_target, uint32_t* nxA,
@@ -516,6 +518,14 @@ int fw_run(FwCtx& c, cudaStream_t s) {
                     c.prep[0] && bulk_store(c.store, b) && !getenv("APSP_NO_SPIN_CLOSE") && !getenv("APSP_SLOW_CLOSE");
   const bool prelay = spin && c.p2prep && !getenv("APSP_NO_PRELAY");
   const bool chain = prelay && c.mode == IDX_PRED && !getenv("APSP_NO_DEVCHAIN");
+  // The chain's cross launches (3a, the panels) are latency-bound single waves: two half-row
+  // CTAs per tile halve each CTA's work (flags count half-tiles either way). That pays where the
+  // rounds are chain-bound (n=3200: 2.36 -> 1.98 ms, 3840: 2.92 -> 2.77 ms, u16 n=2048: 1.51 ->
+  // 1.21 ms); from n=4096 on, where 3b is the bound, the doubled A traffic and the resident
+  // waiting CTAs cost more (4096: 3.12 -> 3.20 ms).
+  static const int64_t split_max = getenv("APSP_SPLIT_ROWS_MAX_N") ? atoll(getenv("APSP_SPLIT_ROWS_MAX_N")) : 3840;
+  const bool split = chain && c.m <= split_max;
+  const int xmul = split ? 2 : 1;
   const int nt = int(c.m / TILE_ALIGN);
   if (spin) {   // [0] 3a exit count, [1] diagonal flag, [2] cross-launch exit count; tile flags
     APSP_CUDA_TRY(cudaMemsetAsync(c.spin, 0, 3 * sizeof(int), s));
@@ -574,12 +584,14 @@ int fw_run(FwCtx& c, cudaStream_t s) {
       }
       if (chain) {
         g3a.tile_flags = c.tflags; g3a.tile_ld = nt; g3a.tile_round = round;
+        g3a.split_rows = split;
         if (k0 > 0) { g3a.wait_count = c.spin + 2; g3a.wait_target = p2_target; g3a.pdl = true; }
       }
       rc = fw_phase3(c, k0, k1, -1, s, -1, true, &g3a);
-      spin_target += cross_ctas(c.m, b);
-      // closure(K+1) on the side stream: the diagonal flag (prelay) or all of 3a (the prep reads it)
-      if (!rc && prelay) rc = fw_phase1(c, k1, c.side, c.spin + 1, round + 1, g3a.nxA, g3a.nxB, g3a.nxPred, c.m);
+      spin_target += cross_ctas(c.m, b) * xmul;
+      // closure(K+1) on the side stream: the diagonal flag (prelay; it counts half-tiles, two per
+      // round) or all of 3a (the prep reads it)
+      if (!rc && prelay) rc = fw_phase1(c, k1, c.side, c.spin + 1, 2 * (round + 1), g3a.nxA, g3a.nxB, g3a.nxPred, c.m);
       else if (!rc) rc = fw_phase1(c, k1, c.side, c.spin, spin_target);
       // the cross launch of K+1: waits for 3a's count; in the chain it also writes the phase-3
       // layouts in place and counts out for the next 3a
@@ -588,10 +600,11 @@ int fw_run(FwCtx& c, cudaStream_t s) {
       if (chain) {
         gp2.exit_count = c.spin + 2;
         gp2.tile_flags = c.tflags; gp2.tile_ld = nt; gp2.tile_round = round + 1;
+        gp2.split_rows = split;
       }
       if (!rc) rc = fw_phase2(c, k1, c.side, prelay, prelay ? &gp2 : nullptr, chain);
       if (chain) {
-        p2_target += cross_ctas(c.m, b);
+        p2_target += cross_ctas(c.m, b) * xmul;
         FwSignals g3b;   // 3b(K): tile flags, the next 3a's tiles (cross of K+2) first
         g3b.tile_flags = c.tflags; g3b.tile_ld = nt; g3b.tile_round = round;
         if (k2 < c.m) g3b.first_lo = k2;

@@ -92,6 +92,10 @@ struct MinplusArgs {
   // Full-grid launches: if first_lo < first_hi the (1D) grid enumerates the tiles of the cross
   // [first_lo, first_hi) first, then the rest row-major (FW 3b: the next 3a's inputs first).
   int64_t first_lo, first_hi;
+  // Cross-list launches of the u8 / u16 bulk kernel: two CTAs per tile, each owning 64 rows
+  // (half the work each: the latency-bound FW 3a / cross launches use twice the SMs). Round
+  // flags and the diagonal flag then count halves: a whole-tile CTA adds 2, a half adds 1.
+  int split_rows;
 };
 
 // Lay the u8 operand panels out in the tile kernel's shared-memory format, once per product:

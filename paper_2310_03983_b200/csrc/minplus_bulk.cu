@@ -50,7 +50,9 @@ struct SmemNT {   // u8: 4 x 24 KB ring + 16 KB C = 112 KB (2 CTAs / SM); u16: 3
 // PEERS: 0 no peer stores; 1 improved segments also stored into the peer replicas (R-Kleene);
 // 2 every cell of the tile (values and pred, improved or not) stored into the peers' receive
 // slots (the FW pivot panel push).
-template <int S, int PEERS>
+// HR: half-row CTAs (MinplusArgs::split_rows; PEERS = 0 only): rows [64 h, 64 h + 64) of the
+// tile, h = blockIdx.x & 1, 4 rows per thread instead of 8.
+template <int S, int PEERS, int HR = 0>
 __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   using NR = Narrow<S>;
   using T = typename NR::T;
@@ -58,6 +60,11 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   constexpr uint32_t KINF2 = (NR::INF << TAG) * 0x00010001u;
   constexpr uint32_t TMASK2 = ((1u << TAG) - 1u) * 0x00010001u;
   constexpr int CW = 4 * int(sizeof(T));          // bytes of one 4-cell C segment
+  constexpr int R = HR ? 4 : 8;                    // rows per thread
+  const int half = HR ? int(blockIdx.x & 1) : 0;
+  const int ty_ = int(threadIdx.x) >> 4;
+  auto row_of = [&](int r) { return HR ? 64 * half + 4 * ty_ + r : (r < 4 ? 4 * ty_ + r : 64 + 4 * ty_ + r - 4); };
+  constexpr int UNITS = HR ? 1 : 2;                // this CTA's share of a tile, in half-tiles
   extern __shared__ __align__(128) unsigned char smraw_nt[];
   SmemNT<S>& sm = *reinterpret_cast<SmemNT<S>*>(smraw_nt);
   if (p.wait_count) {   // operands produced by a kernel on another stream (fw_sched.cu)
@@ -80,7 +87,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
       int v;
       for (;;) {
         asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(tflag) : "memory");
-        if (v >= p.tile_round) break;
+        if (v >= 2 * p.tile_round) break;
         __nanosleep(32);
       }
     }
@@ -94,21 +101,22 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   const bool nx_b = p.nxA && p.only_lo < p.only_hi && i0 == p.only_lo && j0 != p.only_lo;
   auto emit_next = [&](auto&& get) {
     constexpr int NCHX = BN / SUB;
+    constexpr int ROWS = HR ? 64 : 128;
     if (nx_a) {
-      emit_layout_a<T, TAG, NCHX, NT>(get, p.nxA + (i0 / BM) * int64_t(NCHX) * (SUB * BM));
+      emit_layout_a<T, TAG, NCHX, NT, ROWS>(get, p.nxA + (i0 / BM) * int64_t(NCHX) * (SUB * BM), 64 * half);
     } else {
-      emit_layout_b<T, TAG, WIN, NCHX, NT>(get, p.nxB + (j0 / BN) * int64_t(NCHX) * (SUB * BN));
-      if (p.nxPred && p.idx) {   // next pivot rows' pred: all 16 loads in flight, then the stores
-        constexpr int PER = BM * BN / 4 / NT;
+      emit_layout_b<T, TAG, WIN, NCHX, NT, ROWS>(get, p.nxB + (j0 / BN) * int64_t(NCHX) * (SUB * BN), 64 * half);
+      if (p.nxPred && p.idx) {   // next pivot rows' pred: all loads in flight, then the stores
+        constexpr int PER = ROWS * BN / 4 / NT;
         int4 buf[PER];
 #pragma unroll
         for (int u = 0; u < PER; u++) {
-          const int e = threadIdx.x + u * NT, r = e >> 5, q4 = 4 * (e & 31);
+          const int e = threadIdx.x + u * NT, r = 64 * half + (e >> 5), q4 = 4 * (e & 31);
           buf[u] = *reinterpret_cast<const int4*>(p.idx + (i0 + r) * p.ldi + j0 + q4);
         }
 #pragma unroll
         for (int u = 0; u < PER; u++) {
-          const int e = threadIdx.x + u * NT, r = e >> 5, q4 = 4 * (e & 31);
+          const int e = threadIdx.x + u * NT, r = 64 * half + (e >> 5), q4 = 4 * (e & 31);
           *reinterpret_cast<int4*>(p.nxPred + int64_t(r) * p.nxPredLd + j0 + q4) = buf[u];
         }
       }
@@ -149,8 +157,8 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   {  // own C cells -> smem (cp.async, 4 or 8 bytes per 4-cell segment)
     const char* C = static_cast<const char*>(p.C);
 #pragma unroll
-    for (int r = 0; r < 8; r++) {
-      const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+    for (int r = 0; r < R; r++) {
+      const int ri = row_of(r);
 #pragma unroll
       for (int h = 0; h < 2; h++) {
         const char* src = C + ((i0 + ri) * p.ldc + j0 + 64 * h + 4 * tx) * int64_t(sizeof(T));
@@ -166,10 +174,10 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   T* Cw = static_cast<T*>(p.C);
   const bool idx_vec = out && ((reinterpret_cast<uintptr_t>(out) & 15) == 0) && ((p.ldi & 3) == 0);
 
-  uint32_t acc[8][4];
-  uint32_t kst[8][4];
+  uint32_t acc[R][4];
+  uint32_t kst[R][4];
 #pragma unroll
-  for (int r = 0; r < 8; r++)
+  for (int r = 0; r < R; r++)
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       acc[r][q] = KINF2;
@@ -182,14 +190,21 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
     mbar_wait(&sm.full[slot], ph);
 #pragma unroll kU8Unroll
     for (int kk = 0; kk < SUB; kk++) {
-      const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
-      const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
       const uint2 b0 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][4 * tx]);
       const uint2 b1 = *reinterpret_cast<const uint2*>(&sm.Bs[slot][kk][64 + 4 * tx]);
-      const uint32_t a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      uint32_t a[R];
+      if constexpr (HR) {
+        const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 * half + 4 * ty]);
+        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      } else {
+        const uint4 a0 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][4 * ty]);
+        const uint4 a1 = *reinterpret_cast<const uint4*>(&sm.As[slot][kk][64 + 4 * ty]);
+        a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+        a[4 % R] = a1.x; a[5 % R] = a1.y; a[6 % R] = a1.z; a[7 % R] = a1.w;
+      }
       const uint32_t b[4] = {b0.x, b0.y, b1.x, b1.y};
 #pragma unroll
-      for (int r = 0; r < 8; r++)
+      for (int r = 0; r < R; r++)
 #pragma unroll
         for (int q = 0; q < 4; q++) acc[r][q] = viaddmin_u16x2(a[r], b[q], acc[r][q]);
     }
@@ -213,8 +228,8 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
     if (c == 0) {   // merge the old C (own cells only: no barrier)
       asm volatile("cp.async.wait_all;\n" ::: "memory");
 #pragma unroll
-      for (int r = 0; r < 8; r++) {
-        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+      for (int r = 0; r < R; r++) {
+        const int ri = row_of(r);
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           uint32_t p0, p1;   // old values of the two column pairs, as key pairs
@@ -238,7 +253,7 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
       // one warp vote per row slot r (2 rows x 128 columns of the warp): once the tile has mostly
       // converged, only the row slots that improved in this window pay for the decode
 #pragma unroll
-      for (int r = 0; r < 8; r++) {
+      for (int r = 0; r < R; r++) {
         const uint32_t any = (acc[r][0] | acc[r][1] | acc[r][2] | acc[r][3]) & TMASK2;
         if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
@@ -253,12 +268,12 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
 #else
       uint32_t any = 0;
 #pragma unroll
-      for (int r = 0; r < 8; r++)
+      for (int r = 0; r < R; r++)
 #pragma unroll
         for (int q = 0; q < 4; q++) any |= acc[r][q];
       if (__any_sync(0xffffffffu, any & TMASK2)) {
 #pragma unroll
-        for (int r = 0; r < 8; r++)
+        for (int r = 0; r < R; r++)
 #pragma unroll
           for (int q = 0; q < 4; q++) {
             const uint32_t tg = acc[r][q] & TMASK2;
@@ -273,8 +288,8 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   }
   // epilogue
 #pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const int64_t i = i0 + (r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4);
+  for (int r = 0; r < R; r++) {
+    const int64_t i = i0 + row_of(r);
     int32_t pv[2][4];
     uint32_t ks[2][4];
 #pragma unroll
@@ -371,19 +386,19 @@ __global__ void __launch_bounds__(NT, 2) minplus_nt_kernel(MinplusArgs p) {
   if (p.diag_flag && i0 == p.only_lo && j0 == p.only_lo) {   // the next closure's input is final
     __threadfence();
     __syncthreads();
-    if (t == 0) atomicExch(p.diag_flag, p.diag_value);
+    if (t == 0) atomicAdd(p.diag_flag, UNITS);   // the closure waits for 2 (K + 1)
   }
   if (tflag) {   // this round's update of the tile is stored
     __threadfence();
     __syncthreads();
-    if (t == 0) atomicExch(tflag, p.tile_round + 1);
+    if (t == 0) atomicAdd(tflag, UNITS);   // 2 (round + 1) once every row of the tile is stored
   }
   if (nx_a || nx_b) {   // uniform per CTA
     {
       // final values of every cell (acc = min(old, new) << TAG) -> the C staging tile
 #pragma unroll
-      for (int r = 0; r < 8; r++) {
-        const int ri = r < 4 ? 4 * ty + r : 64 + 4 * ty + r - 4;
+      for (int r = 0; r < R; r++) {
+        const int ri = row_of(r);
 #pragma unroll
         for (int h = 0; h < 2; h++) {
           if constexpr (sizeof(T) == 1)
@@ -1212,13 +1227,29 @@ int launch_w32nt(const MinplusArgs& a, cudaStream_t s) {
 
 template <int S>
 int launch_nt(const MinplusArgs& a, cudaStream_t s) {
-  static std::atomic<unsigned long long> attr0{0}, attr1{0}, attr2{0};
+  static std::atomic<unsigned long long> attr0{0}, attr1{0}, attr2{0}, attr3{0};
   APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 0>, int(sizeof(SmemNT<S>)), attr0));
   APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 1>, int(sizeof(SmemNT<S>)), attr1));
   APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 2>, int(sizeof(SmemNT<S>)), attr2));
+  APSP_CUDA_TRY(smem_optin(minplus_nt_kernel<S, 0, 1>, int(sizeof(SmemNT<S>)), attr3));
   const size_t es = sizeof(typename Narrow<S>::T);
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
     return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
+  if (a.split_rows) {   // half-row CTAs: cross-list launches without peers only
+    if (a.npeers || !(a.only_lo < a.only_hi)) return set_error(2, "half-row tiles are for cross-list launches");
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid_for(a, BM, BN);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = sizeof(SmemNT<S>);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.pdl ? 1 : 0;
+    APSP_CUDA_TRY(cudaLaunchKernelEx(&cfg, minplus_nt_kernel<S, 0, 1>, a));
+    return 0;
+  }
   if (a.npeers && a.push_all) {
     minplus_nt_kernel<S, 2><<<grid_for(a, BM, BN), NT, sizeof(SmemNT<S>), s>>>(a);
   } else if (a.npeers) {

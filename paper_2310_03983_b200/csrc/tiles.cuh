@@ -23,7 +23,7 @@ __device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn
     const int wr = int((p.only_hi - p.only_lo) / bm), lo_r = int(p.only_lo / bm);   // row band, in row tiles
     const int wc = int((p.only_hi - p.only_lo) / bn), lo_c = int(p.only_lo / bn);   // col band, in col tiles
     const int nt_c = int((p.n + bn - 1) / bn);
-    const int id = int(blockIdx.x);
+    const int id = int(blockIdx.x) >> (p.split_rows ? 1 : 0);   // half-row CTAs: two per tile
     if (id < wr * nt_c) {
       i0 = int64_t(lo_r + id / nt_c) * bm;
       j0 = int64_t(id % nt_c) * bn;
@@ -82,35 +82,40 @@ template <> struct NtFormat<STORE_U16> { static constexpr int TAG = 6, WIN = 1; 
 // load16(r, c0, v) fills v[0..15] with the tile row r, columns c0..c0+15 (c0 % 16 == 0).
 // NCH chunks of 32 k; every thread first loads all its segments (global sources: the loads
 // overlap instead of one L2 round trip per segment), then stores them
-template <typename T, int TAG, int NCH, int NTHR, typename L>
-__device__ __forceinline__ void emit_layout_a(L&& load16, uint32_t* Atile) {
-  constexpr int PER = NCH * 256 / NTHR;
+// ROWS = 128 (whole tile) or 64 (rows [row_lo, row_lo + 64) of it: a half-tile CTA). For B the
+// tile rows are the k index, so a half covers chunks [row_lo / 32, row_lo / 32 + NCH / 2).
+template <typename T, int TAG, int NCH, int NTHR, int ROWS = 128, typename L>
+__device__ __forceinline__ void emit_layout_a(L&& load16, uint32_t* Atile, int row_lo = 0) {
+  constexpr int PER = NCH * 2 * ROWS / NTHR;   // items: chunk x row x 16-k half
   T v[PER][16];
 #pragma unroll
   for (int u = 0; u < PER; u++) {
-    const int e = threadIdx.x + u * NTHR, c = e >> 8, tt = e & 255, r = tt & 127, kb = 16 * (tt >> 7);
+    const int e = threadIdx.x + u * NTHR, c = e / (2 * ROWS), tt = e % (2 * ROWS);
+    const int r = row_lo + tt % ROWS, kb = 16 * (tt / ROWS);
     load16(r, c * SUB + kb, v[u]);
   }
 #pragma unroll
   for (int u = 0; u < PER; u++) {
-    const int e = threadIdx.x + u * NTHR, c = e >> 8, tt = e & 255, r = tt & 127, kb = 16 * (tt >> 7);
+    const int e = threadIdx.x + u * NTHR, c = e / (2 * ROWS), tt = e % (2 * ROWS);
+    const int r = row_lo + tt % ROWS, kb = 16 * (tt / ROWS);
     uint32_t* dst = Atile + int64_t(c) * (SUB * 128);
 #pragma unroll
     for (int q = 0; q < 16; q++) dst[(kb + q) * 128 + r] = (uint32_t(v[u][q]) << TAG) * 0x00010001u;
   }
 }
-template <typename T, int TAG, int WIN, int NCH, int NTHR, typename L>
-__device__ __forceinline__ void emit_layout_b(L&& load16, uint16_t* Btile) {
-  constexpr int PER = NCH * 256 / NTHR;
+template <typename T, int TAG, int WIN, int NCH, int NTHR, int ROWS = 128, typename L>
+__device__ __forceinline__ void emit_layout_b(L&& load16, uint16_t* Btile, int row_lo = 0) {
+  constexpr int PER = NCH * 256 * ROWS / 128 / NTHR;
+  const int c0 = row_lo / SUB;
   T v[PER][16];
 #pragma unroll
   for (int u = 0; u < PER; u++) {
-    const int e = threadIdx.x + u * NTHR, c = e >> 8, tt = e & 255, kk = tt >> 3, cb = 16 * (tt & 7);
+    const int e = threadIdx.x + u * NTHR, c = c0 + (e >> 8), tt = e & 255, kk = tt >> 3, cb = 16 * (tt & 7);
     load16(c * SUB + kk, cb, v[u]);
   }
 #pragma unroll
   for (int u = 0; u < PER; u++) {
-    const int e = threadIdx.x + u * NTHR, c = e >> 8, tt = e & 255, kk = tt >> 3, cb = 16 * (tt & 7);
+    const int e = threadIdx.x + u * NTHR, c = c0 + (e >> 8), tt = e & 255, kk = tt >> 3, cb = 16 * (tt & 7);
     const uint32_t tag = uint32_t(SUB * (c % WIN) + kk + 1);
     uint32_t o[8];
 #pragma unroll
@@ -201,7 +206,7 @@ inline dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
   if (a.only_lo < a.only_hi) {   // the cross of rows and columns [lo, hi) (tile_origin's enumeration)
     const int64_t wr = (a.only_hi - a.only_lo) / bm, wc = (a.only_hi - a.only_lo) / bn;
     const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
-    return dim3(unsigned(wr * nt_c + (nt_r - wr) * wc), 1);
+    return dim3(unsigned((wr * nt_c + (nt_r - wr) * wc) << (a.split_rows ? 1 : 0)), 1);
   }
   if (a.first_lo < a.first_hi) return dim3(unsigned(((a.n + bn - 1) / bn) * ((a.m + bm - 1) / bm)), 1);
   return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
