@@ -204,6 +204,23 @@ int launch_scan(int in_dtype, const void* h, int64_t ld, int64_t rows, int64_t c
 }
 
 // ---- conversion into a padded store ------------------------------------------------
+// A finite input value into store S. The narrow stores saturate (negative -> 0, beyond the
+// tier -> its Infinity): a speculative attempt (fw_sched.cu) may run a tier before the scan that
+// rejects it is read back, and its kernels must still see keys inside the tier's range (a wrapped
+// u16 key would carry garbage tag bits into the argmin decode). Admissible inputs are unchanged.
+template <int S, typename V>
+__device__ __forceinline__ typename StoreT<S>::T store_val(V v) {
+  using T = typename StoreT<S>::T;
+  if constexpr (S == STORE_U8 || S == STORE_U16 || S == STORE_W32) {
+    const auto inf = store_inf<S>();
+    if (!(v >= V(0))) return T(0);          // negative (and NaN): rejected by the scan anyway
+    if (v >= V(inf)) return inf;
+    return T(v);
+  } else {
+    return T(v);
+  }
+}
+
 // rows [row0, row0 + R) of the padded N x N matrix (R = N, row0 = 0 for a whole matrix)
 template <int D, int S>
 __device__ __forceinline__ typename StoreT<S>::T store_cell(const typename Api<D>::T* h, int64_t ldh, int64_t n,
@@ -212,7 +229,7 @@ __device__ __forceinline__ typename StoreT<S>::T store_cell(const typename Api<D
   if (i < n && j < n) {
     const typename Api<D>::T v = h[il * ldh + j];
     fin = Api<D>::fin(v);
-    return fin ? T(v) : store_inf<S>();
+    return fin ? store_val<S>(v) : store_inf<S>();
   }
   fin = (i == j);
   return fin ? T(0) : store_inf<S>();
@@ -240,7 +257,7 @@ __global__ void to_store_kernel(const typename Api<D>::T* h, int64_t ldh, int64_
 #pragma unroll
           for (int q = 0; q < 4; q++) {
             fin[q] = Api<D>::fin(v[q]);
-            o[q] = fin[q] ? T(v[q]) : store_inf<S>();
+            o[q] = fin[q] ? store_val<S>(v[q]) : store_inf<S>();
           }
         } else {
 #pragma unroll
@@ -325,7 +342,7 @@ __global__ void to_store_rect_kernel(const typename Api<D>::T* h, int64_t ldh, i
     T o = store_inf<S>();
     if (h) {
       const typename Api<D>::T v = h[i * ldh + j];
-      if (Api<D>::fin(v)) o = T(v);
+      if (Api<D>::fin(v)) o = store_val<S>(v);
     }
     out[i * ldo + j] = o;
   }

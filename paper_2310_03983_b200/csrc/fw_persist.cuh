@@ -416,7 +416,57 @@ namespace persist64 {
 
 constexpr int QT = 256;   // threads
 constexpr int QB = 64;    // tile / pivot block
-using persist::TMASK2;
+
+// Key formats: u8 values << 7 with one 64-k tag window per task; u16 values (<= 510) << 6 with
+// two 32-k windows (INF + INF + tag < 2^16 in both), decoded after k = 31.
+template <int S> struct K64;
+template <> struct K64<STORE_U8> {
+  using T = uint8_t;
+  static constexpr int TAG = 7, WIN = 64;
+};
+template <> struct K64<STORE_U16> {
+  using T = uint16_t;
+  static constexpr int TAG = 6, WIN = 32;
+};
+template <int S> __device__ __forceinline__ constexpr uint32_t tmask2() {
+  return ((1u << K64<S>::TAG) - 1u) * 0x00010001u;
+}
+// 8 consecutive cells (16-byte aligned for u16, 8 for u8) as 4 key pairs
+template <int S>
+__device__ __forceinline__ void load_pairs(const typename K64<S>::T* src, uint32_t (&a)[4]) {
+  constexpr int TAG = K64<S>::TAG;
+  if constexpr (S == STORE_U8) {
+    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(src));
+    a[0] = __byte_perm(v.x, 0, 0x4140) << TAG;
+    a[1] = __byte_perm(v.x, 0, 0x4342) << TAG;
+    a[2] = __byte_perm(v.y, 0, 0x4140) << TAG;
+    a[3] = __byte_perm(v.y, 0, 0x4342) << TAG;
+  } else {
+    const uint4 v = __ldcg(reinterpret_cast<const uint4*>(src));
+    a[0] = v.x << TAG;
+    a[1] = v.y << TAG;
+    a[2] = v.z << TAG;
+    a[3] = v.w << TAG;
+  }
+}
+// 4 tag-free key pairs back as 8 cells
+template <int S>
+__device__ __forceinline__ void store_pairs(typename K64<S>::T* dst, const uint32_t (&a)[4]) {
+  constexpr int TAG = K64<S>::TAG;
+  if constexpr (S == STORE_U8) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(a[0] >> TAG, a[1] >> TAG, 0x6420),
+                                                __byte_perm(a[2] >> TAG, a[3] >> TAG, 0x6420));
+  } else {
+    *reinterpret_cast<uint4*>(dst) = make_uint4(a[0] >> TAG, a[1] >> TAG, a[2] >> TAG, a[3] >> TAG);
+  }
+}
+// close a tag window: the last improving k (1-based, window base wb) of each half into kst
+__device__ __forceinline__ void decode_pair(uint32_t& acc, uint32_t& kst, uint32_t tmask, uint32_t wb) {
+  const uint32_t tg = acc & tmask;
+  acc -= tg;
+  if (tg & 0xFFFFu) kst = (kst & 0xFFFF0000u) | ((tg & 0xFFFFu) + wb);
+  if (tg >> 16) kst = (kst & 0x0000FFFFu) | (((tg >> 16) + wb) << 16);
+}
 
 struct TileSmem {
   uint32_t As[QB][QB];    // [k][row] replicated key pairs
@@ -438,19 +488,16 @@ union Smem {
 // Warp w owns columns 8w..8w+7 (4 key pairs), lane l rows 2l, 2l+1: row k comes by shuffle from
 // lane k/2 of the same warp, column k from its owner warp through shared memory (double
 // buffered, one barrier per step). The last improving k rides in the 7-bit tag (k + 1 <= 64).
-__device__ void close64(CloseSmem& sm, uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, bool prof) {
+template <int S>
+__device__ void close64(CloseSmem& sm, typename K64<S>::T* D, int64_t ld, int32_t* P, int64_t ldp, bool prof) {
   const int t = threadIdx.x, w = t >> 5, l = t & 31;
   unsigned long long tp0 = prof && t == 0 ? persist::gtimer() : 0, tp1 = 0, tp2 = 0, tp3 = 0;
-  constexpr uint32_t STRIP2 = ~TMASK2;
+  constexpr uint32_t TMASK2 = tmask2<S>(), STRIP2 = ~TMASK2;
+  constexpr int WIN = K64<S>::WIN;
   uint32_t acc[2][4];
+  uint32_t kst[2][4] = {};
 #pragma unroll
-  for (int r = 0; r < 2; r++) {
-    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(D + int64_t(2 * l + r) * ld + 8 * w));
-    acc[r][0] = __byte_perm(v.x, 0, 0x4140) << 7;
-    acc[r][1] = __byte_perm(v.x, 0, 0x4342) << 7;
-    acc[r][2] = __byte_perm(v.y, 0, 0x4140) << 7;
-    acc[r][3] = __byte_perm(v.y, 0, 0x4342) << 7;
-  }
+  for (int r = 0; r < 2; r++) load_pairs<S>(D + int64_t(2 * l + r) * ld + 8 * w, acc[r]);
   if (P) {   // the input pred block, for the resolution after the k loop: in flight meanwhile
     for (int e = t; e < QB * QB / 4; e += QT) {
       const int i = e >> 4, j = 4 * (e & 15);
@@ -487,7 +534,7 @@ __device__ void close64(CloseSmem& sm, uint8_t* D, int64_t ld, int32_t* P, int64
       const uint32_t dkk1 = sm.colk1[buf][k];   // D[k][k+1], replicated
       const uint32_t ck1x = __viaddmin_u16x2(c2.x, dkk1, c3.x), ck1y = __viaddmin_u16x2(c2.y, dkk1, c3.y);
       uint32_t dkj[4];
-      const uint32_t tag2 = uint32_t(k + 1) * 0x00010001u;
+      const uint32_t tag2 = uint32_t(k % WIN + 1) * 0x00010001u;
 #pragma unroll
       for (int p = 0; p < 4; p++) dkj[p] = (__shfl_sync(0xffffffffu, acc[0][p], k >> 1) & STRIP2) | tag2;
 #pragma unroll
@@ -502,6 +549,12 @@ __device__ void close64(CloseSmem& sm, uint8_t* D, int64_t ld, int32_t* P, int64
         acc[0][p] = __viaddmin_u16x2(ck1x, dkj[p], acc[0][p]);
         acc[1][p] = __viaddmin_u16x2(ck1y, dkj[p], acc[1][p]);
       }
+      if (WIN < QB && k + 2 == WIN) {   // u16: the first 32-k window closes after step k + 1
+#pragma unroll
+        for (int r = 0; r < 2; r++)
+#pragma unroll
+          for (int p = 0; p < 4; p++) decode_pair(acc[r][p], kst[r][p], TMASK2, 0u);
+      }
       // the next pair (k+2, k+3): pair ((kk+2) & 7) >> 1 of warp (k+2) >> 3
       if (k + 2 < QB) {
         if (kk == 6) {
@@ -515,21 +568,14 @@ __device__ void close64(CloseSmem& sm, uint8_t* D, int64_t ld, int32_t* P, int64
 #undef P64_PUBPAIR
   __syncthreads();   // every warp is past its last read of colk
   if (prof && t == 0) tp2 = persist::gtimer();
-  uint32_t kst[2][4];
+  // the (last) window: its tag is k* + 1 - base (0 = no improvement in it)
 #pragma unroll
   for (int r = 0; r < 2; r++)
 #pragma unroll
-    for (int p = 0; p < 4; p++) {
-      kst[r][p] = acc[r][p] & TMASK2;   // one window: the tag is k* + 1 (0 = never improved)
-      acc[r][p] -= kst[r][p];
-    }
+    for (int p = 0; p < 4; p++) decode_pair(acc[r][p], kst[r][p], TMASK2, uint32_t(QB - WIN));
   // values back (improved pairs only change; writing all is simpler and equally final)
 #pragma unroll
-  for (int r = 0; r < 2; r++) {
-    const uint32_t v0 = __byte_perm(acc[r][0] >> 7, acc[r][1] >> 7, 0x6420);
-    const uint32_t v1 = __byte_perm(acc[r][2] >> 7, acc[r][3] >> 7, 0x6420);
-    *reinterpret_cast<uint2*>(D + int64_t(2 * l + r) * ld + 8 * w) = make_uint2(v0, v1);
-  }
+  for (int r = 0; r < 2; r++) store_pairs<S>(D + int64_t(2 * l + r) * ld + 8 * w, acc[r]);
   if (!P) return;
 #pragma unroll
   for (int r = 0; r < 2; r++)
@@ -584,8 +630,13 @@ __device__ void close64(CloseSmem& sm, uint8_t* D, int64_t ld, int32_t* P, int64
 
 // C <- min(C, A (x) B) on a 64 x 64 tile, k = 64. Thread t: rows 2*(t>>3) + {0,1}, columns
 // 8*(t&7) .. + 7 (4 key pairs).
-__device__ void tile64(TileSmem& sm, uint8_t* C, int64_t ldc, const uint8_t* A, int64_t lda, const uint8_t* B,
-                       int64_t ldb, int32_t* P, int64_t ldp, const int32_t* PB_, int64_t ldpb) {
+template <int S>
+__device__ void tile64(TileSmem& sm, typename K64<S>::T* C, int64_t ldc, const typename K64<S>::T* A, int64_t lda,
+                       const typename K64<S>::T* B, int64_t ldb, int32_t* P, int64_t ldp, const int32_t* PB_,
+                       int64_t ldpb) {
+  using T = typename K64<S>::T;
+  constexpr int TAG = K64<S>::TAG, WIN = K64<S>::WIN;
+  constexpr uint32_t TMASK2 = tmask2<S>();
   const int t = threadIdx.x, ty = t >> 3, tx = t & 7;
   if (P) {   // B's pred rows, in flight while the tile computes (L2 only: cp.async.cg)
 #pragma unroll
@@ -596,55 +647,51 @@ __device__ void tile64(TileSmem& sm, uint8_t* C, int64_t ldc, const uint8_t* A, 
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
-  {  // stage A (64 rows x 64 k) and B (64 k x 64 cols): 16 bytes of each per thread
+  {  // stage A (64 rows x 64 k) and B (64 k x 64 cols): 16 values of each per thread
     const int ra = t >> 2, ka = 16 * (t & 3);
-    const uint4 va = __ldcg(reinterpret_cast<const uint4*>(A + int64_t(ra) * lda + ka));
-    const uint32_t wa[4] = {va.x, va.y, va.z, va.w};
+    T va[16];
+    reinterpret_cast<uint4*>(va)[0] = __ldcg(reinterpret_cast<const uint4*>(A + int64_t(ra) * lda + ka));
+    if constexpr (sizeof(T) == 2)
+      reinterpret_cast<uint4*>(va)[1] = __ldcg(reinterpret_cast<const uint4*>(A + int64_t(ra) * lda + ka) + 1);
 #pragma unroll
-    for (int q = 0; q < 16; q++) sm.As[ka + q][ra] = ((wa[q >> 2] >> (8 * (q & 3))) & 0xFFu) * 0x00800080u;
+    for (int q = 0; q < 16; q++) sm.As[ka + q][ra] = (uint32_t(va[q]) << TAG) * 0x00010001u;
     const int kb = t >> 2, cb = 16 * (t & 3);
-    const uint4 vb = __ldcg(reinterpret_cast<const uint4*>(B + int64_t(kb) * ldb + cb));
-    const uint32_t wb[4] = {vb.x, vb.y, vb.z, vb.w};
-    const uint32_t tag = uint32_t(kb + 1) * 0x00010001u;
+    T vb[16];
+    reinterpret_cast<uint4*>(vb)[0] = __ldcg(reinterpret_cast<const uint4*>(B + int64_t(kb) * ldb + cb));
+    if constexpr (sizeof(T) == 2)
+      reinterpret_cast<uint4*>(vb)[1] = __ldcg(reinterpret_cast<const uint4*>(B + int64_t(kb) * ldb + cb) + 1);
+    const uint32_t tag = uint32_t(kb % WIN + 1);
     uint32_t o[8];
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      o[2 * q] = (__byte_perm(wb[q], 0, 0x4140) << 7) | tag;
-      o[2 * q + 1] = (__byte_perm(wb[q], 0, 0x4342) << 7) | tag;
-    }
+    for (int q = 0; q < 8; q++)
+      o[q] = ((uint32_t(vb[2 * q]) << TAG) | tag) | (((uint32_t(vb[2 * q + 1]) << TAG) | tag) << 16);
     uint4* dst = reinterpret_cast<uint4*>(&sm.Bs[kb][cb]);
     dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
     dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
   }
   uint32_t acc[2][4];
 #pragma unroll
-  for (int r = 0; r < 2; r++) {
-    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(C + int64_t(2 * ty + r) * ldc + 8 * tx));
-    acc[r][0] = __byte_perm(v.x, 0, 0x4140) << 7;
-    acc[r][1] = __byte_perm(v.x, 0, 0x4342) << 7;
-    acc[r][2] = __byte_perm(v.y, 0, 0x4140) << 7;
-    acc[r][3] = __byte_perm(v.y, 0, 0x4342) << 7;
-  }
+  for (int r = 0; r < 2; r++) load_pairs<S>(C + int64_t(2 * ty + r) * ldc + 8 * tx, acc[r]);
   __syncthreads();
+  uint32_t kst[2][4] = {};
+#pragma unroll
+  for (int w0 = 0; w0 < QB; w0 += WIN) {   // one tag window per WIN k
 #pragma unroll 16
-  for (int k = 0; k < QB; k++) {
-    const uint2 a = *reinterpret_cast<const uint2*>(&sm.As[k][2 * ty]);
-    const uint4 b = *reinterpret_cast<const uint4*>(&sm.Bs[k][8 * tx]);
-    const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
+    for (int k = w0; k < w0 + WIN; k++) {
+      const uint2 a = *reinterpret_cast<const uint2*>(&sm.As[k][2 * ty]);
+      const uint4 b = *reinterpret_cast<const uint4*>(&sm.Bs[k][8 * tx]);
+      const uint32_t bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int p = 0; p < 4; p++) {
-      acc[0][p] = __viaddmin_u16x2(a.x, bv[p], acc[0][p]);
-      acc[1][p] = __viaddmin_u16x2(a.y, bv[p], acc[1][p]);
+      for (int p = 0; p < 4; p++) {
+        acc[0][p] = __viaddmin_u16x2(a.x, bv[p], acc[0][p]);
+        acc[1][p] = __viaddmin_u16x2(a.y, bv[p], acc[1][p]);
+      }
     }
+#pragma unroll
+    for (int r = 0; r < 2; r++)
+#pragma unroll
+      for (int p = 0; p < 4; p++) decode_pair(acc[r][p], kst[r][p], TMASK2, uint32_t(w0));
   }
-  uint32_t kst[2][4];
-#pragma unroll
-  for (int r = 0; r < 2; r++)
-#pragma unroll
-    for (int p = 0; p < 4; p++) {
-      kst[r][p] = acc[r][p] & TMASK2;
-      acc[r][p] -= kst[r][p];
-    }
   // the gathers read the smem snapshot of B's pred rows (taken before any store of this task,
   // so the row-panel task, whose B is its own tile, needs no barrier before its stores)
   if (P) {
@@ -664,9 +711,7 @@ __device__ void tile64(TileSmem& sm, uint8_t* C, int64_t ldc, const uint8_t* A, 
 #pragma unroll
   for (int r = 0; r < 2; r++) {
     if ((kst[r][0] | kst[r][1] | kst[r][2] | kst[r][3]) == 0u) continue;
-    const uint32_t v0 = __byte_perm(acc[r][0] >> 7, acc[r][1] >> 7, 0x6420);
-    const uint32_t v1 = __byte_perm(acc[r][2] >> 7, acc[r][3] >> 7, 0x6420);
-    *reinterpret_cast<uint2*>(C + int64_t(2 * ty + r) * ldc + 8 * tx) = make_uint2(v0, v1);
+    store_pairs<S>(C + int64_t(2 * ty + r) * ldc + 8 * tx, acc[r]);
     if (!P) continue;
     int32_t* prow = P + int64_t(2 * ty + r) * ldp + 8 * tx;
 #pragma unroll
@@ -677,7 +722,8 @@ __device__ void tile64(TileSmem& sm, uint8_t* C, int64_t ldc, const uint8_t* A, 
   }
 }
 
-__global__ void __launch_bounds__(QT, 3) fw_persist64_kernel(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int nb,
+template <int S>
+__global__ void __launch_bounds__(QT, 3) fw_persist64_kernel(typename K64<S>::T* D, int64_t ld, int32_t* P, int64_t ldp, int nb,
                                                              const int4* items, int nitems, int* done, int* counter,
                                                              unsigned long long* trace) {
   __shared__ Smem sm;
@@ -717,15 +763,15 @@ __global__ void __launch_bounds__(QT, 3) fw_persist64_kernel(uint8_t* D, int64_t
     if (w.x == persist::T_CLOSE || w.x == persist::T_UCLOSE) {
       if (w.x == persist::T_UCLOSE) {   // round K-1 on the tile first (pivot block K-1)
         const int64_t kp = k0 - QB;
-        tile64(sm.tile, D + k0 * ld + k0, ld, D + k0 * ld + kp, ld, D + kp * ld + k0, ld,
+        tile64<S>(sm.tile, D + k0 * ld + k0, ld, D + k0 * ld + kp, ld, D + kp * ld + k0, ld,
                P ? P + k0 * ldp + k0 : nullptr, ldp, P ? P + kp * ldp + k0 : nullptr, ldp);
         __syncthreads();
       }
-      close64(sm.close, D + k0 * ld + k0, ld, P ? P + k0 * ldp + k0 : nullptr, ldp, trace != nullptr);
+      close64<S>(sm.close, D + k0 * ld + k0, ld, P ? P + k0 * ldp + k0 : nullptr, ldp, trace != nullptr);
     } else {
       const int64_t i0 = int64_t(w.x == persist::T_ROW ? K : I) * QB;
       const int64_t j0 = int64_t(w.x == persist::T_COL ? K : J) * QB;
-      tile64(sm.tile, D + i0 * ld + j0, ld, D + i0 * ld + k0, ld, D + k0 * ld + j0, ld,
+      tile64<S>(sm.tile, D + i0 * ld + j0, ld, D + i0 * ld + k0, ld, D + k0 * ld + j0, ld,
              P ? P + i0 * ldp + j0 : nullptr, ldp, P ? P + k0 * ldp + j0 : nullptr, ldp);
     }
     __syncthreads();
@@ -753,7 +799,7 @@ bool fw_persist64_enabled(int store, int64_t N) {
   static const int64_t max_n = getenv("APSP_PERSIST64_MAX_N") ? atoll(getenv("APSP_PERSIST64_MAX_N")) : 2048;
   // N = 128 is one classic-order closure (pred bit-exact with the reference, test-pinned): the
   // 128-wide schedule handles it
-  return store == STORE_U8 && N % 64 == 0 && N <= max_n && N >= 256;
+  return (store == STORE_U8 || store == STORE_U16) && N % 64 == 0 && N <= max_n && N >= 256;
 }
 
 size_t fw_persist64_scratch_bytes(int64_t N) {
@@ -761,7 +807,9 @@ size_t fw_persist64_scratch_bytes(int64_t N) {
   return size_t(nb * nb + 64) * sizeof(int);
 }
 
-int launch_fw_persist64(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch, cudaStream_t s) {
+int launch_fw_persist64(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch,
+                        cudaStream_t s) {
+  if (store != STORE_U8 && store != STORE_U16) return set_error(APSP_EINVAL, "the 64-wide schedule is u8 / u16");
   const int nb = int(N / 64);
   int nitems = 0;
   const int4* items = persist_items(nb, &nitems, true);
@@ -770,13 +818,18 @@ int launch_fw_persist64(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t
   int* counter = done + nb * nb;
   APSP_CUDA_TRY(cudaMemsetAsync(scratch, 0, fw_persist64_scratch_bytes(N), s));
   int slots = 0;
-  APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel, persist64::QT, 0, slots));
+  if (store == STORE_U8) APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel<STORE_U8>, persist64::QT, 0, slots));
+  else APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel<STORE_U16>, persist64::QT, 0, slots));
   if (slots < 1) return set_error(APSP_ECUDA, "persistent kernel does not fit an SM");
   const int grid = std::min(slots, nitems);
   unsigned long long* trace = nullptr;
   if (getenv("APSP_PERSIST_TRACE")) APSP_CUDA_TRY(cudaMalloc(&trace, size_t(nitems) * 4 * sizeof(unsigned long long)));
-  persist64::fw_persist64_kernel<<<grid, persist64::QT, 0, s>>>(D, ld, P, ldp, nb, items, nitems, done, counter,
-                                                                trace);
+  if (store == STORE_U8)
+    persist64::fw_persist64_kernel<STORE_U8><<<grid, persist64::QT, 0, s>>>(static_cast<uint8_t*>(D), ld, P, ldp, nb,
+                                                                            items, nitems, done, counter, trace);
+  else
+    persist64::fw_persist64_kernel<STORE_U16><<<grid, persist64::QT, 0, s>>>(static_cast<uint16_t*>(D), ld, P, ldp,
+                                                                             nb, items, nitems, done, counter, trace);
   APSP_CUDA_TRY(cudaGetLastError());
   count_launches(1);
   return persist_dump_trace(trace, items, nitems, s);

@@ -127,7 +127,8 @@ size_t fw_persist_scratch_bytes(int64_t N);
 int launch_fw_persist(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch, cudaStream_t s);
 bool fw_persist64_enabled(int store, int64_t N);
 size_t fw_persist64_scratch_bytes(int64_t N);
-int launch_fw_persist64(uint8_t* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch, cudaStream_t s);
+int launch_fw_persist64(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch,
+                        cudaStream_t s);
 // Blocked in-CTA closure for the 32-bit exact stores, pred mode (close_blk.cu)
 bool close_blk_supported(int store);
 int launch_block_close_blk(int store, void* D, int64_t ld, int64_t lo, int64_t m, int32_t* idx, int64_t ldi,
