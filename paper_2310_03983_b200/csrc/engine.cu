@@ -140,6 +140,11 @@ std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced, bool al
 
 size_t header_bytes() { return 256; }
 
+int raster_group() {
+  static const int g = getenv("APSP_RASTER_G") ? atoi(getenv("APSP_RASTER_G")) : 8;
+  return g;
+}
+
 // High-priority side stream of the current device (created once per device, thread-safe).
 cudaStream_t side_stream() {
   static cudaStream_t streams[64] = {};

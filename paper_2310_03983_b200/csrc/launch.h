@@ -96,6 +96,8 @@ struct MinplusArgs {
   // (half the work each: the latency-bound FW 3a / cross launches use twice the SMs). Round
   // flags and the diagonal flag then count halves: a whole-tile CTA adds 2, a half adds 1.
   int split_rows;
+  // Full-grid launches: grouped tile order (row tiles per group; <= 1: row-major), see tile_origin
+  int raster;
 };
 
 // Lay the u8 operand panels out in the tile kernel's shared-memory format, once per product:
@@ -106,6 +108,9 @@ int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64
                      int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s, const int32_t* psrc = nullptr,
                      int64_t lds = 0, int32_t* pdst = nullptr, int64_t ldd = 0, int64_t pcols = 0);
 
+// Row tiles per rasterisation group of full-grid launches (APSP_RASTER_G, default 8; 1 = row-major).
+int raster_group();
+
 // Default-initialised args: nothing skipped, full grid.
 inline MinplusArgs minplus_args() {
   MinplusArgs a{};
@@ -114,6 +119,7 @@ inline MinplusArgs minplus_args() {
   a.skip3_lo = a.skip3_hi = -1;
   a.only_lo = a.only_hi = -1;
   a.first_lo = a.first_hi = -1;
+  a.raster = raster_group();
   return a;
 }
 

@@ -50,6 +50,15 @@ __device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn
       i0 = int64_t(rr < lo_t ? rr : rr + w) * bm;
       j0 = int64_t(cc < lo_t ? cc : cc + w) * bn;
     }
+  } else if (p.raster > 1) {
+    // Grouped rasterisation: CTAs launch in linear blockIdx order, so consecutive CTAs take the
+    // tiles of `raster` row tiles column by column -- the row panels of the group stay hot in L2
+    // while each column panel is read once per group instead of once per row tile.
+    const int nt_c = int(gridDim.x), nt_r = int(gridDim.y), g = p.raster;
+    const int id = int(blockIdx.y) * nt_c + int(blockIdx.x);
+    const int grp = id / (g * nt_c), r0 = grp * g, gs = min(nt_r - r0, g), in = id - grp * g * nt_c;
+    i0 = int64_t(r0 + in % gs) * bm;
+    j0 = int64_t(in / gs) * bn;
   } else {
     i0 = int64_t(blockIdx.y) * bm;
     j0 = int64_t(blockIdx.x) * bn;
