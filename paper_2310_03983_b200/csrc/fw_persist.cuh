@@ -1,3 +1,4 @@
+#include <type_traits>
 // Small-n blocked Floyd-Warshall in ONE persistent launch (u8 tier), included by fw.cu.
 //
 // For N <= a few thousand the launch-based schedule is bound by its per-round chain -- closure
@@ -428,6 +429,11 @@ template <> struct K64<STORE_U16> {
   using T = uint16_t;
   static constexpr int TAG = 6, WIN = 32;
 };
+// w32: unsigned 32-bit keys v << 7 | tag, one per cell, one 64-k window (INF + INF + tag < 2^32)
+template <> struct K64<STORE_W32> {
+  using T = int32_t;
+  static constexpr int TAG = 7, WIN = 64;
+};
 template <int S> __device__ __forceinline__ constexpr uint32_t tmask2() {
   return ((1u << K64<S>::TAG) - 1u) * 0x00010001u;
 }
@@ -481,6 +487,15 @@ struct CloseSmem {
 };
 union Smem {
   TileSmem tile;
+  CloseSmem close;
+};
+struct TileSmemW {        // w32 tile task: 32-bit keys for both operands
+  uint32_t As[QB][QB];    // [k][row]
+  uint32_t Bs[QB][QB];    // [k][col] tagged
+  int32_t Pb[QB][QB];
+};
+union SmemW {
+  TileSmemW tile;
   CloseSmem close;
 };
 
@@ -722,13 +737,223 @@ __device__ void tile64(TileSmem& sm, typename K64<S>::T* C, int64_t ldc, const t
   }
 }
 
+// ---- w32 tier: one unsigned 32-bit key per cell (v << 7 | tag), VIADDMNMX.U32 ----------------
+// Same thread mapping as the packed tasks: a thread owns 2 rows x 8 columns, now 16 keys.
+constexpr uint32_t W_TMASK = 0x7Fu, W_STRIP = ~0x7Fu;
+
+__device__ __forceinline__ void load8_w32(const int32_t* src, uint32_t (&a)[8]) {
+  const uint4 v0 = __ldcg(reinterpret_cast<const uint4*>(src)), v1 = __ldcg(reinterpret_cast<const uint4*>(src) + 1);
+  a[0] = v0.x << 7; a[1] = v0.y << 7; a[2] = v0.z << 7; a[3] = v0.w << 7;
+  a[4] = v1.x << 7; a[5] = v1.y << 7; a[6] = v1.z << 7; a[7] = v1.w << 7;
+}
+__device__ __forceinline__ void store8_w32(int32_t* dst, const uint32_t (&a)[8]) {
+  reinterpret_cast<uint4*>(dst)[0] = make_uint4(a[0] >> 7, a[1] >> 7, a[2] >> 7, a[3] >> 7);
+  reinterpret_cast<uint4*>(dst)[1] = make_uint4(a[4] >> 7, a[5] >> 7, a[6] >> 7, a[7] >> 7);
+}
+
+// 64 x 64 w32 closure, classic k order, two steps per barrier (as close64): warp w owns columns
+// 8w..8w+7, lane l rows 2l, 2l+1; the tag (k + 1, one window) is the last improving k.
+__device__ void close64_w32(CloseSmem& sm, int32_t* D, int64_t ld, int32_t* P, int64_t ldp) {
+  const int t = threadIdx.x, w = t >> 5, l = t & 31;
+  uint32_t acc[2][8];
+#pragma unroll
+  for (int r = 0; r < 2; r++) load8_w32(D + int64_t(2 * l + r) * ld + 8 * w, acc[r]);
+  if (P) {
+    for (int e = t; e < QB * QB / 4; e += QT) {
+      const int i = e >> 4, j = 4 * (e & 15);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&sm.P[i][j])),
+                   "l"(P + int64_t(i) * ldp + j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  // columns k, k+1 (tag-free) of the owner warp into buffer BUF
+#define W64_PUB(C0, BUF)                                                                            \
+  do {                                                                                              \
+    *reinterpret_cast<uint2*>(&sm.colk[BUF][2 * l]) = make_uint2(acc[0][C0] & W_STRIP, acc[1][C0] & W_STRIP); \
+    *reinterpret_cast<uint2*>(&sm.colk1[BUF][2 * l]) =                                              \
+        make_uint2(acc[0][(C0) + 1] & W_STRIP, acc[1][(C0) + 1] & W_STRIP);                         \
+  } while (0)
+  if (w == 0) W64_PUB(0, 0);
+#pragma unroll 1
+  for (int k0 = 0; k0 < QB; k0 += 8) {
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 2) {
+      const int k = k0 + kk, buf = (kk >> 1) & 1;
+      __syncthreads();
+      const uint2 c2 = *reinterpret_cast<const uint2*>(&sm.colk[buf][2 * l]);
+      const uint2 c3 = *reinterpret_cast<const uint2*>(&sm.colk1[buf][2 * l]);
+      const uint32_t dkk1 = sm.colk1[buf][k];   // D[k][k+1]
+      const uint32_t ck1x = min(c3.x, c2.x + dkk1), ck1y = min(c3.y, c2.y + dkk1);
+      uint32_t dkj[8];
+#pragma unroll
+      for (int c = 0; c < 8; c++) dkj[c] = (__shfl_sync(0xffffffffu, acc[kk & 1][c], k >> 1) & W_STRIP) | uint32_t(k + 1);
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        acc[0][c] = min(acc[0][c], c2.x + dkj[c]);
+        acc[1][c] = min(acc[1][c], c2.y + dkj[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 8; c++)
+        dkj[c] = (__shfl_sync(0xffffffffu, acc[(kk + 1) & 1][c], (k + 1) >> 1) & W_STRIP) | uint32_t(k + 2);
+#pragma unroll
+      for (int c = 0; c < 8; c++) {
+        acc[0][c] = min(acc[0][c], ck1x + dkj[c]);
+        acc[1][c] = min(acc[1][c], ck1y + dkj[c]);
+      }
+      if (k + 2 < QB) {
+        if (kk == 6) {
+          if (w == (k0 >> 3) + 1) W64_PUB(0, buf ^ 1);
+        } else if (w == (k0 >> 3)) {
+          W64_PUB((kk + 2) & 7, buf ^ 1);
+        }
+      }
+    }
+  }
+#undef W64_PUB
+  __syncthreads();
+  uint32_t kst[2][8];
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      kst[r][c] = acc[r][c] & W_TMASK;
+      acc[r][c] -= kst[r][c];
+    }
+#pragma unroll
+  for (int r = 0; r < 2; r++) store8_w32(D + int64_t(2 * l + r) * ld + 8 * w, acc[r]);
+  if (!P) return;
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int c = 0; c < 8; c++) sm.K[2 * l + r][8 * w + c] = uint8_t(kst[r][c]);
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  for (int round = 0; round < 6; round++) {
+    int32_t np[16];
+    uint8_t nk[16];
+    bool live = false;
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      const int e = t + QT * c, i = e >> 6, j = e & 63;
+      const uint8_t kk = sm.K[i][j];
+      np[c] = sm.P[i][j];
+      nk[c] = kk;
+      if (kk) {
+        np[c] = sm.P[kk - 1][j];
+        nk[c] = sm.K[kk - 1][j];
+        live |= nk[c] != 0;
+      }
+    }
+    const bool more = __syncthreads_or(live);
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      const int e = t + QT * c, i = e >> 6, j = e & 63;
+      sm.P[i][j] = np[c];
+      sm.K[i][j] = nk[c];
+    }
+    __syncthreads();
+    if (!more) break;
+  }
+  for (int e = t; e < QB * QB / 4; e += QT) {
+    const int i = e >> 4, j = 4 * (e & 15);
+    *reinterpret_cast<int4*>(P + int64_t(i) * ldp + j) = *reinterpret_cast<const int4*>(&sm.P[i][j]);
+  }
+}
+
+// C <- min(C, A (x) B) on a 64 x 64 w32 tile, k = 64 (one tag window)
+__device__ void tile64_w32(TileSmemW& sm, int32_t* C, int64_t ldc, const int32_t* A, int64_t lda, const int32_t* B,
+                           int64_t ldb, int32_t* P, int64_t ldp, const int32_t* PB_, int64_t ldpb) {
+  const int t = threadIdx.x, ty = t >> 3, tx = t & 7;
+  if (P) {
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int e = t + QT * q, i = e >> 4, j = 4 * (e & 15);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&sm.Pb[i][j])),
+                   "l"(PB_ + int64_t(i) * ldpb + j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  {  // A (64 rows x 64 k) transposed to [k][row]; B (64 k x 64 cols) tagged: 16 values each per thread
+    const int ra = t >> 2, ka = 16 * (t & 3);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; q4++) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(A + int64_t(ra) * lda + ka) + q4);
+      sm.As[ka + 4 * q4][ra] = v.x << 7;
+      sm.As[ka + 4 * q4 + 1][ra] = v.y << 7;
+      sm.As[ka + 4 * q4 + 2][ra] = v.z << 7;
+      sm.As[ka + 4 * q4 + 3][ra] = v.w << 7;
+    }
+    const int kb = t >> 2, cb = 16 * (t & 3);
+    const uint32_t tag = uint32_t(kb + 1);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; q4++) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(B + int64_t(kb) * ldb + cb) + q4);
+      reinterpret_cast<uint4*>(&sm.Bs[kb][cb])[q4] =
+          make_uint4((v.x << 7) | tag, (v.y << 7) | tag, (v.z << 7) | tag, (v.w << 7) | tag);
+    }
+  }
+  uint32_t acc[2][8];
+#pragma unroll
+  for (int r = 0; r < 2; r++) load8_w32(C + int64_t(2 * ty + r) * ldc + 8 * tx, acc[r]);
+  __syncthreads();
+#pragma unroll 8
+  for (int k = 0; k < QB; k++) {
+    const uint2 a = *reinterpret_cast<const uint2*>(&sm.As[k][2 * ty]);
+    const uint4 b0 = reinterpret_cast<const uint4*>(&sm.Bs[k][8 * tx])[0];
+    const uint4 b1 = reinterpret_cast<const uint4*>(&sm.Bs[k][8 * tx])[1];
+    const uint32_t bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      acc[0][c] = min(acc[0][c], a.x + bv[c]);
+      acc[1][c] = min(acc[1][c], a.y + bv[c]);
+    }
+  }
+  uint32_t kst[2][8];
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int c = 0; c < 8; c++) {
+      kst[r][c] = acc[r][c] & W_TMASK;
+      acc[r][c] -= kst[r][c];
+    }
+  if (P) {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
+  int32_t pv[2][8];
+#pragma unroll
+  for (int r = 0; r < 2; r++)
+#pragma unroll
+    for (int c = 0; c < 8; c++) pv[r][c] = (P && kst[r][c]) ? sm.Pb[kst[r][c] - 1][8 * tx + c] : 0;
+#pragma unroll
+  for (int r = 0; r < 2; r++) {
+    uint32_t any = 0;
+#pragma unroll
+    for (int c = 0; c < 8; c++) any |= kst[r][c];
+    if (!any) continue;
+    store8_w32(C + int64_t(2 * ty + r) * ldc + 8 * tx, acc[r]);
+    if (!P) continue;
+    int32_t* prow = P + int64_t(2 * ty + r) * ldp + 8 * tx;
+#pragma unroll
+    for (int c = 0; c < 8; c++)
+      if (kst[r][c]) prow[c] = pv[r][c];
+  }
+}
+
 template <int S>
 __global__ void __launch_bounds__(QT, 3) fw_persist64_kernel(typename K64<S>::T* D, int64_t ld, int32_t* P, int64_t ldp, int nb,
                                                              const int4* items, int nitems, int* done, int* counter,
                                                              unsigned long long* trace) {
-  __shared__ Smem sm;
+  using SmemT = typename std::conditional<S == STORE_W32, SmemW, Smem>::type;
+  extern __shared__ __align__(16) unsigned char smraw_p64[];   // sizeof(SmemT) (w32: 48 KB, opt-in)
+  SmemT& sm = *reinterpret_cast<SmemT*>(smraw_p64);
   __shared__ int s_item;
   const int t = threadIdx.x;
+  auto tile = [&](typename K64<S>::T* C, int64_t ldc, const typename K64<S>::T* A, const typename K64<S>::T* B,
+                  int32_t* Pc, const int32_t* Pb_) {
+    if constexpr (S == STORE_W32) tile64_w32(sm.tile, C, ldc, A, ld, B, ld, Pc, ldp, Pb_, ldp);
+    else tile64<S>(sm.tile, C, ldc, A, ld, B, ld, Pc, ldp, Pb_, ldp);
+  };
   for (;;) {
     if (t == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
@@ -763,16 +988,17 @@ __global__ void __launch_bounds__(QT, 3) fw_persist64_kernel(typename K64<S>::T*
     if (w.x == persist::T_CLOSE || w.x == persist::T_UCLOSE) {
       if (w.x == persist::T_UCLOSE) {   // round K-1 on the tile first (pivot block K-1)
         const int64_t kp = k0 - QB;
-        tile64<S>(sm.tile, D + k0 * ld + k0, ld, D + k0 * ld + kp, ld, D + kp * ld + k0, ld,
-               P ? P + k0 * ldp + k0 : nullptr, ldp, P ? P + kp * ldp + k0 : nullptr, ldp);
+        tile(D + k0 * ld + k0, ld, D + k0 * ld + kp, D + kp * ld + k0, P ? P + k0 * ldp + k0 : nullptr,
+             P ? P + kp * ldp + k0 : nullptr);
         __syncthreads();
       }
-      close64<S>(sm.close, D + k0 * ld + k0, ld, P ? P + k0 * ldp + k0 : nullptr, ldp, trace != nullptr);
+      if constexpr (S == STORE_W32) close64_w32(sm.close, D + k0 * ld + k0, ld, P ? P + k0 * ldp + k0 : nullptr, ldp);
+      else close64<S>(sm.close, D + k0 * ld + k0, ld, P ? P + k0 * ldp + k0 : nullptr, ldp, trace != nullptr);
     } else {
       const int64_t i0 = int64_t(w.x == persist::T_ROW ? K : I) * QB;
       const int64_t j0 = int64_t(w.x == persist::T_COL ? K : J) * QB;
-      tile64<S>(sm.tile, D + i0 * ld + j0, ld, D + i0 * ld + k0, ld, D + k0 * ld + j0, ld,
-             P ? P + i0 * ldp + j0 : nullptr, ldp, P ? P + k0 * ldp + j0 : nullptr, ldp);
+      tile(D + i0 * ld + j0, ld, D + i0 * ld + k0, D + k0 * ld + j0, P ? P + i0 * ldp + j0 : nullptr,
+           P ? P + k0 * ldp + j0 : nullptr);
     }
     __syncthreads();
     if (t == 0) {
@@ -799,7 +1025,7 @@ bool fw_persist64_enabled(int store, int64_t N) {
   static const int64_t max_n = getenv("APSP_PERSIST64_MAX_N") ? atoll(getenv("APSP_PERSIST64_MAX_N")) : 2048;
   // N = 128 is one classic-order closure (pred bit-exact with the reference, test-pinned): the
   // 128-wide schedule handles it
-  return (store == STORE_U8 || store == STORE_U16) && N % 64 == 0 && N <= max_n && N >= 256;
+  return (store == STORE_U8 || store == STORE_U16 || store == STORE_W32) && N % 64 == 0 && N <= max_n && N >= 256;
 }
 
 size_t fw_persist64_scratch_bytes(int64_t N) {
@@ -809,7 +1035,8 @@ size_t fw_persist64_scratch_bytes(int64_t N) {
 
 int launch_fw_persist64(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t N, void* scratch,
                         cudaStream_t s) {
-  if (store != STORE_U8 && store != STORE_U16) return set_error(APSP_EINVAL, "the 64-wide schedule is u8 / u16");
+  if (store != STORE_U8 && store != STORE_U16 && store != STORE_W32)
+    return set_error(APSP_EINVAL, "the 64-wide schedule is u8 / u16 / w32");
   const int nb = int(N / 64);
   int nitems = 0;
   const int4* items = persist_items(nb, &nitems, true);
@@ -818,17 +1045,30 @@ int launch_fw_persist64(int store, void* D, int64_t ld, int32_t* P, int64_t ldp,
   int* counter = done + nb * nb;
   APSP_CUDA_TRY(cudaMemsetAsync(scratch, 0, fw_persist64_scratch_bytes(N), s));
   int slots = 0;
-  if (store == STORE_U8) APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel<STORE_U8>, persist64::QT, 0, slots));
-  else APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel<STORE_U16>, persist64::QT, 0, slots));
+  constexpr int sb = int(sizeof(persist64::Smem)), sbw = int(sizeof(persist64::SmemW));
+  static std::atomic<unsigned long long> a8{0}, a16{0}, a32{0};
+  if (store == STORE_U8) {
+    APSP_CUDA_TRY(smem_optin(persist64::fw_persist64_kernel<STORE_U8>, sb, a8));
+    APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel<STORE_U8>, persist64::QT, sb, slots));
+  } else if (store == STORE_U16) {
+    APSP_CUDA_TRY(smem_optin(persist64::fw_persist64_kernel<STORE_U16>, sb, a16));
+    APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel<STORE_U16>, persist64::QT, sb, slots));
+  } else {
+    APSP_CUDA_TRY(smem_optin(persist64::fw_persist64_kernel<STORE_W32>, sbw, a32));
+    APSP_CUDA_TRY(persist_slots(persist64::fw_persist64_kernel<STORE_W32>, persist64::QT, sbw, slots));
+  }
   if (slots < 1) return set_error(APSP_ECUDA, "persistent kernel does not fit an SM");
   const int grid = std::min(slots, nitems);
   unsigned long long* trace = nullptr;
   if (getenv("APSP_PERSIST_TRACE")) APSP_CUDA_TRY(cudaMalloc(&trace, size_t(nitems) * 4 * sizeof(unsigned long long)));
   if (store == STORE_U8)
-    persist64::fw_persist64_kernel<STORE_U8><<<grid, persist64::QT, 0, s>>>(static_cast<uint8_t*>(D), ld, P, ldp, nb,
+    persist64::fw_persist64_kernel<STORE_U8><<<grid, persist64::QT, sb, s>>>(static_cast<uint8_t*>(D), ld, P, ldp, nb,
                                                                             items, nitems, done, counter, trace);
+  else if (store == STORE_U16)
+    persist64::fw_persist64_kernel<STORE_U16><<<grid, persist64::QT, sb, s>>>(static_cast<uint16_t*>(D), ld, P, ldp,
+                                                                             nb, items, nitems, done, counter, trace);
   else
-    persist64::fw_persist64_kernel<STORE_U16><<<grid, persist64::QT, 0, s>>>(static_cast<uint16_t*>(D), ld, P, ldp,
+    persist64::fw_persist64_kernel<STORE_W32><<<grid, persist64::QT, sbw, s>>>(static_cast<int32_t*>(D), ld, P, ldp,
                                                                              nb, items, nitems, done, counter, trace);
   APSP_CUDA_TRY(cudaGetLastError());
   count_launches(1);

@@ -766,3 +766,29 @@ def test_speculative_skip_ahead_u8_to_u16(cuda):
     raw[raw == INF32] = INF_RAW
     want, _ = orc.fw_classic(h64)
     assert np.array_equal(raw, want)
+
+
+@pytest.mark.parametrize("n,rho,wmax", [(300, 0.05, 50000), (1000, 0.01, 3000), (2048, 0.002, 100)])
+def test_persistent_small_n_w32(cuda, n, rho, wmax, monkeypatch):
+    """The 64-wide persistent schedule on the w32 tier (one unsigned 32-bit key per cell,
+    VIADDMNMX.U32): equal to the oracle, valid pred tree, equal distances to the launch-based
+    schedule."""
+    import torch
+
+    raw = random_graph_raw(n, rho, wmax, n + wmax) if wmax > 500 else ap.dense_costs(
+        ap.GenParams(n, rho, wmax, 7 + n), np.int64)
+    want, _ = orc.fw_classic(raw)
+    s = ap.fw_classic(ap.CostMatrix(raw))
+    assert s.info["tier"] == "w32"
+    assert np.array_equal(s.distances.raw, want)
+    pred_ok(raw, s.distances.raw, s.pred.raw)
+    h32 = raw.copy()
+    h32[raw == INF_RAW] = INF32
+    h = torch.from_numpy(h32.astype(np.int32)).cuda()
+    a = ap.solve(h)
+    assert a.info["tier"] == "w32"
+    monkeypatch.setenv("APSP_NO_PERSIST", "1")
+    b = ap.solve(h)
+    assert torch.equal(a.distances, b.distances)
+    ok, why = ap.check_pred_tree(h, a.distances, a.index, INF32)
+    assert ok, why
