@@ -640,6 +640,14 @@ int fw_run(FwCtx& c, cudaStream_t s) {
 int fw_blocked_view(int store, void* D, int64_t ld, int32_t* P, int64_t ldp, int64_t m, int b, int mode,
                     int64_t via_off, Status* st, cudaStream_t s, int* launches, int32_t* predsnap,
                     char* scratch, cudaStream_t side) {
+  // R-Kleene leaves (pred mode, 128-aligned, <= 2048): the 64-wide persistent schedule, as for a
+  // small FW solve; its done counters reuse the start of the leaf scratch. The single-GPU and the
+  // sharded recursions both come through here, so their leaves stay bitwise equal.
+  if (mode == IDX_PRED && scratch && b == TILE_ALIGN && fw_persist64_enabled(store, m) && !g_prof.on &&
+      !getenv("APSP_NO_PERSIST") && fw_scratch_bytes(m, b, store_elem_size(store)) >= fw_persist64_scratch_bytes(m)) {
+    *launches += 2;
+    return launch_fw_persist64(store, D, ld, P, ldp, m, scratch, s);
+  }
   FwCtx c;
   c.store = store; c.es = store_elem_size(store);
   c.D = static_cast<char*>(D); c.ld = ld; c.P = P; c.ldp = ldp;
