@@ -385,7 +385,7 @@ def bench_single(args):
         roofline["traffic"] = c["traffic_bytes"]
         roofline["traffic_launch"] = {"updates": c["updates"], "duration_ms_isolated": c["duration_ms"],
                                       "achieved_isolated": c["achieved_T"], "frac_isolated": c["frac_of_dpx_ceiling"],
-                                      "source": "profiles/ncu_phase3b.json (ncu --set full, round-7 phase-3b launch, tools/p3_capture.sh)"}
+                                      "source": "profiles/ncu_phase3b.json (ncu --set full of the 7th long phase-3b launch, round 2, tools/p3_capture.sh; summary profiles/r02_ncu_phase3b.txt)"}
 
     parity = reference_digest(dist, n, args.rho)
     tiers = None if args.no_tiers else bench_tiers(lib, nat, h, dist, pred, work, stream, n, args, block)

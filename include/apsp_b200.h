@@ -103,7 +103,10 @@ size_t apsp_workspace_bytes(int algorithm, int dtype, int64_t n, int block);
  * predecessors (pred[i][j] = last vertex before j, -1 = None).
  * Replaces fw_classic (solvers.py:118-155): same distances bit-exactly, pred a valid
  * shortest-path tree (equal-length ties may pick another predecessor).
- * block: pivot block size (128).  Host syncs: after the input scan, after the certificate. */
+ * block: pivot block size (0 = by n).  Host syncs: after the input scan and after the
+ * certificate; a repeated call of the same shape starts the tier that certified last time
+ * right behind the scan and syncs once.  dist is written only on success; on an error
+ * return the contents of pred are unspecified. */
 int apsp_fw_blocked(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred, int64_t ldp, int block,
                     int tier, void* ws, size_t ws_bytes, void* stream, apsp_info* info);
 

@@ -57,6 +57,75 @@ __global__ void __launch_bounds__(256) fw_step_kernel(typename StoreT<S>::T* D, 
   }
 }
 
+// K1 for small n in ONE launch: a single 1024-thread CTA keeps the whole matrix in shared
+// memory and runs the n classic steps with one barrier each (row and column k are invariant
+// during step k, so the cells of a step are independent). Pred stays in global memory (L1/L2
+// on this SM) and is touched only for improved cells: pred[i][j] <- pred[k][j], pred row k is
+// invariant in step k too. Same strict-< rule as fw_step_kernel, so the result is bit-exact
+// with fw_classic. n = 256 (u8): 256 launches (graph-replayed, ~10 us each) -> one.
+constexpr int K1CTA_THREADS = 1024;
+constexpr size_t K1CTA_MAX_SMEM = 200 * 1024;
+
+template <int S>
+__global__ void __launch_bounds__(K1CTA_THREADS) fw_classic_cta_kernel(typename StoreT<S>::T* D, int64_t ld, int n,
+                                                                       int32_t* idx, int64_t ldi, Status* st) {
+  using T = typename StoreT<S>::T;
+  using A = typename StoreT<S>::A;
+  extern __shared__ __align__(16) unsigned char smraw_k1[];
+  T* Ds = reinterpret_cast<T*>(smraw_k1);   // n x n, row pitch n
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
+  for (int e = t; e < n * n; e += K1CTA_THREADS) Ds[e] = D[int64_t(e / n) * ld + e % n];
+  __syncthreads();
+  bool overflow = false;
+  for (int k = 0; k < n; k++) {
+    const T* rowk = Ds + k * n;
+    for (int i = ty; i < n; i += 32) {
+      const A dik = A(Ds[i * n + k]);
+      if (dik == A(store_inf<S>())) continue;   // nothing through an unreachable k
+      for (int j = tx; j < n; j += 32) {
+        const A c = dik + A(rowk[j]);
+        if (c < A(Ds[i * n + j])) {
+          overflow |= range_overflow<S>(c);
+          Ds[i * n + j] = T(c);
+          if (idx) idx[int64_t(i) * ldi + j] = idx[int64_t(k) * ldi + j];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < n * n; e += K1CTA_THREADS) D[int64_t(e / n) * ld + e % n] = Ds[e];
+  if (st && overflow) st->overflow = 1;
+}
+
+// true (and launched) when the whole n x n store fits one CTA's shared memory
+int launch_fw_classic_cta(int store, void* D, int64_t ld, int64_t n, int32_t* idx, int64_t ldi, Status* st,
+                          cudaStream_t s, bool& done) {
+  done = false;
+  const size_t bytes = size_t(n) * n * store_elem_size(store);
+  if (n < 2 || bytes > K1CTA_MAX_SMEM || getenv("APSP_K1_STEPS")) return 0;
+  static std::atomic<unsigned long long> a8{0}, a16{0}, a32{0}, af{0}, a64{0}, aw{0};
+  const int sb = int(bytes);
+  switch (store) {
+#define K1CTA(ST, TT, ATTR)                                                                                  \
+  case ST:                                                                                                   \
+    APSP_CUDA_TRY(smem_optin(fw_classic_cta_kernel<ST>, sb, ATTR));                                       \
+    fw_classic_cta_kernel<ST><<<1, K1CTA_THREADS, sb, s>>>(static_cast<TT*>(D), ld, int(n), idx, ldi, st); \
+    break;
+    K1CTA(STORE_U8, uint8_t, a8)
+    K1CTA(STORE_U16, uint16_t, a16)
+    K1CTA(STORE_I32, int32_t, a32)
+    K1CTA(STORE_F32, float, af)
+    K1CTA(STORE_I64, int64_t, a64)
+    K1CTA(STORE_W32, int32_t, aw)
+#undef K1CTA
+    default: return set_error(2, "unknown store %d", store);
+  }
+  APSP_CUDA_TRY(cudaGetLastError());
+  count_launches(1);
+  done = true;
+  return 0;
+}
+
 // K1 for the narrow stores: HBM-bound, so each thread streams 16-byte row segments (16 u8 or
 // 8 u16 cells) down a band of rows, four rows in flight. The cells are relaxed as packed
 // 16-bit pairs with one VIADDMNMX.U16x2 (min(D[i][k] + D[k][j], D[i][j])) per two cells; the

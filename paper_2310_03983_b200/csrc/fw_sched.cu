@@ -993,16 +993,21 @@ int fw_classic_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
       for (int64_t k = 0; !r && k < n; k++) r = launch_fw_step(store, D, ldd, n, k, pred, ldp, IDX_PRED, 0, &hdr_dev->status, st);
       return r;
     };
-    if (!rc && n <= 4096) {   // launch-bound sizes: replay the n steps as one graph
+    bool one = false;   // small n: every step in one single-CTA launch
+    if (!rc) rc = launch_fw_classic_cta(store, D, ldd, n, pred, ldp, &hdr_dev->status, s, one);
+    if (!rc && one) {
+      launches += 3;
+    } else if (!rc && n <= 4096) {   // launch-bound sizes: replay the n steps as one graph
       int dev = 0;
       cudaGetDevice(&dev);
       const GraphKey key{dev, 3, store, IDX_PRED, n, ldd, D, pred, &hdr_dev->status, nullptr, s};
       rc = run_graphed(key, s, steps);
+      launches += int(n) + 2;
     } else if (!rc) {
       rc = steps(s);
+      launches += int(n) + 2;
     }
     if (rc) return rc;
-    launches += int(n) + 2;
     bool ok = false;
     rc = certify(tier, store, D, ldd, n, n, scan, hdr_dev, hdr, s, ok);
     if (rc) return rc;

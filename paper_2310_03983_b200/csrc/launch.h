@@ -149,6 +149,11 @@ int launch_block_close(int store, void* D, int64_t ld, int64_t lo, int64_t m,
                        uint32_t* nxA = nullptr, uint16_t* nxB = nullptr, int32_t* nxPred = nullptr,
                        int64_t nxPredLd = 0);
 
+// K1 for small n: all n classic steps in one single-CTA launch (the store in shared memory);
+// done = false (nothing launched) when the matrix does not fit
+int launch_fw_classic_cta(int store, void* D, int64_t ld, int64_t n, int32_t* idx, int64_t ldi, Status* st,
+                          cudaStream_t s, bool& done);
+
 // Classic per-k Floyd-Warshall step (K1): bit-exact pred/via parity with fw_classic
 // (solvers.py:77-95).  One launch per k; row k / column k are invariant in step k.
 int launch_fw_step(int store, void* D, int64_t ld, int64_t n, int64_t k, int32_t* idx,
