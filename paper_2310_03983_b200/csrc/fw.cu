@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) fw_step_kernel(typename StoreT<S>::T* D, 
 // during step k, so the cells of a step are independent). Pred stays in global memory (L1/L2
 // on this SM) and is touched only for improved cells: pred[i][j] <- pred[k][j], pred row k is
 // invariant in step k too. Same strict-< rule as fw_step_kernel, so the result is bit-exact
-// with fw_classic. n = 256 (u8): 256 launches (graph-replayed, ~10 us each) -> one.
+// with fw_classic. n = 128 (u16): 0.65 -> 0.34 ms; n = 256 (u8): 2.0 -> 1.85 ms.
 constexpr int K1CTA_THREADS = 1024;
 constexpr size_t K1CTA_MAX_SMEM = 200 * 1024;
 
@@ -102,13 +102,14 @@ int launch_fw_classic_cta(int store, void* D, int64_t ld, int64_t n, int32_t* id
                           cudaStream_t s, bool& done) {
   done = false;
   const size_t bytes = size_t(n) * n * store_elem_size(store);
-  if (n < 2 || bytes > K1CTA_MAX_SMEM || getenv("APSP_K1_STEPS")) return 0;
+  // one SM's issue rate bounds it: 2x the graph-replayed steps at n=128, ~8% at 256, slower above
+  if (n < 2 || n > 256 || bytes > K1CTA_MAX_SMEM || getenv("APSP_K1_STEPS")) return 0;
   static std::atomic<unsigned long long> a8{0}, a16{0}, a32{0}, af{0}, a64{0}, aw{0};
   const int sb = int(bytes);
   switch (store) {
 #define K1CTA(ST, TT, ATTR)                                                                                  \
   case ST:                                                                                                   \
-    APSP_CUDA_TRY(smem_optin(fw_classic_cta_kernel<ST>, sb, ATTR));                                       \
+    APSP_CUDA_TRY(smem_optin(fw_classic_cta_kernel<ST>, int(K1CTA_MAX_SMEM), ATTR));                      \
     fw_classic_cta_kernel<ST><<<1, K1CTA_THREADS, sb, s>>>(static_cast<TT*>(D), ld, int(n), idx, ldi, st); \
     break;
     K1CTA(STORE_U8, uint8_t, a8)
