@@ -925,8 +925,14 @@ int fw_blocked_impl(int dtype, int64_t n, void* dist, int64_t ld, int32_t* pred,
     return set_error(APSP_ERANGE, "no value tier could represent the result");
   }
   // only a tier that was the scan's first pick (or u16 after u8) is worth guessing: long-path
-  // graphs whose narrow certificates keep failing would otherwise waste a solve every call
-  spec_remember(skey, used == first || (first == APSP_TIER_U8 && used == APSP_TIER_U16) ? used : -1);
+  // graphs whose narrow certificates keep failing would otherwise waste a solve every call. A
+  // skip-ahead u16 result whose certificate shows u8 would have held goes back to guessing u8
+  // (a same-shape sweep over different graphs must not stay on the wider tier).
+  int remember = used == first || (first == APSP_TIER_U8 && used == APSP_TIER_U16) ? used : -1;
+  if (remember == APSP_TIER_U16 && first == APSP_TIER_U8 && hdr.cert.max_finite >= 0 &&
+      hdr.cert.max_finite + scan.max_finite <= tier_limit(APSP_TIER_U8))
+    remember = APSP_TIER_U8;
+  spec_remember(skey, remember);
   rc = launch_from_store(tier_store(used), D, N, n, n, dtype, dist, ld, s);
   if (!rc && pred && Pw != pred) {
     rc = launch_copy_idx(P, N, n, n, APSP_DTYPE_I32, pred, ldp, s);

@@ -792,3 +792,19 @@ def test_persistent_small_n_w32(cuda, n, rho, wmax, monkeypatch):
     assert torch.equal(a.distances, b.distances)
     ok, why = ap.check_pred_tree(h, a.distances, a.index, INF32)
     assert ok, why
+
+
+def test_skip_ahead_returns_to_u8(cuda):
+    """After a shape needed u16, a same-shape input that fits u8 may run once on u16 (skip-ahead,
+    same bits), but its certificate shows u8 would have held: the next call is u8 again."""
+    import torch
+
+    n = 1024
+    need16 = torch.from_numpy(ap.dense_costs(ap.GenParams(n, 0.02, 100, 7 + n), np.int32)).cuda()
+    dense = torch.from_numpy(ap.dense_costs(ap.GenParams(n, 1.0, 100, 5), np.int32)).cuda()
+    assert ap.solve(need16).info["tier"] == "u16"
+    assert ap.solve(need16).info["tier"] == "u16"
+    a = ap.solve(dense)
+    b = ap.solve(dense)
+    assert a.info["tier"] in ("u8", "u16") and b.info["tier"] == "u8"
+    assert torch.equal(a.distances, b.distances) and torch.equal(a.index, b.index)
