@@ -140,8 +140,10 @@ std::vector<int> pick_tiers(int dtype, const ScanResult& sc, int forced, bool al
 
 size_t header_bytes() { return 256; }
 
+// Off by default: grouping cuts phase-3b DRAM reads by 15 % at n=16384 with the same time, but
+// costs 1.5 % at n=8192 (profiles/r02_raster_ab.txt); the kernel is ALU-bound either way.
 int raster_group() {
-  static const int g = getenv("APSP_RASTER_G") ? atoi(getenv("APSP_RASTER_G")) : 8;
+  static const int g = getenv("APSP_RASTER_G") ? atoi(getenv("APSP_RASTER_G")) : 1;
   return g;
 }
 

@@ -108,7 +108,7 @@ int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64
                      int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s, const int32_t* psrc = nullptr,
                      int64_t lds = 0, int32_t* pdst = nullptr, int64_t ldd = 0, int64_t pcols = 0);
 
-// Row tiles per rasterisation group of full-grid launches (APSP_RASTER_G, default 8; 1 = row-major).
+// Row tiles per rasterisation group of full-grid launches (APSP_RASTER_G, default 1 = row-major).
 int raster_group();
 
 // Default-initialised args: nothing skipped, full grid.
