@@ -69,7 +69,10 @@ def back64(t):
 
 
 @pytest.mark.parametrize("n,wmax,tier,block", [(300, 9, "u8", 128), (257, 400, "auto", 128), (333, 50000, "w32", 256),
-                                               (129, 9, "u8", 256), (700, 9, "auto", 0), (1100, 9, "auto", 128)])
+                                               (129, 9, "u8", 256), (700, 9, "auto", 0), (1100, 9, "auto", 128),
+                                               # persistent 64-wide u16 / w32 tasks, the device-signalled
+                                               # chain with half-row cross launches (n > 2560)
+                                               (640, 300, "u16", 0), (520, 50000, "w32", 0), (2600, 9, "u8", 0)])
 def test_fw_blocked_guarded(cuda, n, wmax, tier, block):
     lib = nat.load()
     raw = random_graph_raw(n, 0.05, wmax, n + wmax)
