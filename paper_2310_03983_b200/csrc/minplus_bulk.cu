@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
   constexpr uint32_t TMASK = (1u << W32_TAG) - 1u;
   extern __shared__ __align__(128) unsigned char smraw_w32[];
   SmemW32NT& sm = *reinterpret_cast<SmemW32NT*>(smraw_w32);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // (FW 3b behind 3a: see minplus_nt_kernel)
   int64_t i0, j0;
   tile_origin(p, BM, BN, i0, j0);
   if (tile_skipped(p, i0, j0, BM, BN)) return;
@@ -730,6 +731,7 @@ template <int G>
 __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
   extern __shared__ __align__(128) unsigned char smraw_dm[];
   SmemF32DM& sm = *reinterpret_cast<SmemF32DM*>(smraw_dm);
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // (FW 3b behind 3a: see minplus_nt_kernel)
   int64_t i0, j0;
   tile_origin(p, BM, DM_BN, i0, j0);
   if (tile_skipped(p, i0, j0, BM, DM_BN)) return;
@@ -1194,6 +1196,23 @@ __global__ void __launch_bounds__(NT, 1) minplus_f32nt_kernel(MinplusArgs p) {
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
 }
 
+// <<<grid, NT, smem, s>>>, with programmatic stream serialization when a.pdl (FW 3b: no data
+// dependency on the 3a launch queued right before it)
+template <typename K>
+static cudaError_t launch_maybe_pdl(K* kernel, dim3 grid, size_t smem, cudaStream_t s, const MinplusArgs& a) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 int launch_f32dm(const MinplusArgs& a, cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
   static std::atomic<unsigned long long> attr8{0};
@@ -1202,8 +1221,8 @@ int launch_f32dm(const MinplusArgs& a, cudaStream_t s) {
   if (a.m % BM || a.n % DM_BN || a.k % SUB || a.k > 65535 || (reinterpret_cast<uintptr_t>(a.C) & 15) ||
       (a.ldc * 4) % 16)
     return set_error(2, "deferred-argmin f32 tiles need 128 x 64 tiles and 32-multiple k");
-  if (a.fine) minplus_f32dm_kernel<8><<<grid_for(a, BM, DM_BN), NT, sizeof(SmemF32DM), s>>>(a);
-  else minplus_f32dm_kernel<32><<<grid_for(a, BM, DM_BN), NT, sizeof(SmemF32DM), s>>>(a);
+  if (a.fine) APSP_CUDA_TRY(launch_maybe_pdl(minplus_f32dm_kernel<8>, grid_for(a, BM, DM_BN), sizeof(SmemF32DM), s, a));
+  else APSP_CUDA_TRY(launch_maybe_pdl(minplus_f32dm_kernel<32>, grid_for(a, BM, DM_BN), sizeof(SmemF32DM), s, a));
   return 0;
 }
 
@@ -1221,7 +1240,7 @@ int launch_w32nt(const MinplusArgs& a, cudaStream_t s) {
   APSP_CUDA_TRY(smem_optin(minplus_w32nt_kernel, int(sizeof(SmemW32NT)), attr));
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * 4) % 16)
     return set_error(2, "bulk-staged w32 tiles need full 128 x 128 tiles and 32-multiple k");
-  minplus_w32nt_kernel<<<grid_for(a, BM, BN), NT, sizeof(SmemW32NT), s>>>(a);
+  APSP_CUDA_TRY(launch_maybe_pdl(minplus_w32nt_kernel, grid_for(a, BM, BN), sizeof(SmemW32NT), s, a));
   return 0;
 }
 
