@@ -238,7 +238,7 @@ static bool fine_round(const FwCtx& c, int64_t k0);
 // emit3: the cross launch writes the phase-3 layouts of its own tiles in place (the prep after
 // it goes away) and counts its CTAs out on emit3 (fw_run's device-signalled schedule)
 int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s, bool prelaid = false, const FwSignals* sig = nullptr,
-              bool emit3 = false) {
+              bool emit3 = false, int* prep3_count = nullptr, int* prep3_ctas = nullptr) {
   NvtxRange r("apsp.fw.phase2");
   const int64_t b = c.b, m = c.m;
   char* Dg = c.D + (k0 * c.ld + k0) * c.es;
@@ -293,7 +293,8 @@ int fw_phase2(FwCtx& c, int64_t k0, cudaStream_t s, bool prelaid = false, const 
     // cross, updated on the side stream while this round's phase 3 still gathers, writes them)
     const int q3 = int((k0 / b) % 3);
     return launch_prep_bulk(c.store, colp, c.ld, rowp, c.ld, m, m, b, prep_a(slot), prep_b(slot, m, b), s,
-                            c.deep && c.P ? c.P + k0 * c.ldp : nullptr, c.ldp, c.predsnap3[q3], m, m);
+                            c.deep && c.P ? c.P + k0 * c.ldp : nullptr, c.ldp, c.predsnap3[q3], m, m,
+                            prep3_count, prep3_ctas);
   }
   if (snap) {
     rc = launch_copy_block(c.store, rowp, c.ld, c.rowsnap, m, b, m, s);
@@ -527,16 +528,22 @@ int fw_run(FwCtx& c, cudaStream_t s) {
   const bool split = chain && c.m <= split_max;
   const int xmul = split ? 2 : 1;
   const int nt = int(c.m / TILE_ALIGN);
-  if (spin) {   // [0] 3a exit count, [1] diagonal flag, [2] cross-launch exit count; tile flags
+  // The exact fp32 tier's round overlap (its 3b is the bound at n=4096: 6.5 waves of 128 x 64
+  // tiles): 3a(K+1) runs behind 3b(K) on per-tile flags and waits on the device for the phase-3
+  // prep of K+1 (its exit count) instead of a stream event; 3b enumerates the next cross first.
+  // The closure and the panels stay event-ordered on the side stream.
+  const bool f32chain = !spin && c.side && c.spin && c.tflags && b == TILE_ALIGN && c.store == STORE_F32 &&
+                        c.prep[0] && bulk_store(c.store, b) && c.p2prep && !getenv("APSP_NO_DEVCHAIN");
+  if (spin || f32chain) {   // [0] 3a exit count, [1] diagonal flag, [2] cross / prep exit count; tile flags
     APSP_CUDA_TRY(cudaMemsetAsync(c.spin, 0, 3 * sizeof(int), s));
-    if (chain) APSP_CUDA_TRY(cudaMemsetAsync(c.tflags, 0, size_t(nt) * nt * sizeof(int), s));
+    if (chain || f32chain) APSP_CUDA_TRY(cudaMemsetAsync(c.tflags, 0, size_t(nt) * nt * sizeof(int), s));
   }
   FwSignals sig0;
-  if (chain) {   // round 0's panels also release their tiles' flags
+  if (chain || f32chain) {   // round 0's panels also release their tiles' flags
     sig0.tile_flags = c.tflags; sig0.tile_ld = nt; sig0.tile_round = 0;
   }
   int rc = fw_phase1(c, 0, s);
-  if (!rc) rc = fw_phase2(c, 0, s, false, chain ? &sig0 : nullptr);
+  if (!rc) rc = fw_phase2(c, 0, s, false, (chain || f32chain) ? &sig0 : nullptr);
   if (rc) return rc;
   cudaEvent_t evA = nullptr, evB = nullptr;
   if (c.side) {
@@ -548,14 +555,14 @@ int fw_run(FwCtx& c, cudaStream_t s) {
     }
   }
   int spin_target = 0, p2_target = 0;
-  if (spin) {   // the side stream starts after the resets and round 0's panels
+  if (spin || f32chain) {   // the side stream starts after the resets and round 0's panels
     cudaError_t e = cudaEventRecord(evA, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.side, evA, 0);
     if (e != cudaSuccess) rc = set_cuda_error(e, "lookahead start", __FILE__, __LINE__);
   }
   for (int64_t k0 = 0; !rc && k0 < c.m; k0 += b) {
     const int64_t k1 = k0 + b, k2 = k1 + b;
-    if (k1 >= c.m && chain && k0 > 0) {   // the last round's panels: joined by a plain event
+    if (k1 >= c.m && (chain || f32chain) && k0 > 0) {   // the last round's panels: joined by a plain event
       if (cudaEventRecord(evB, c.side) != cudaSuccess || cudaStreamWaitEvent(s, evB, 0) != cudaSuccess)
         rc = set_error(APSP_ECUDA, "lookahead join");
       if (rc) break;
@@ -614,6 +621,24 @@ int fw_run(FwCtx& c, cudaStream_t s) {
         if (!rc) rc = fw_phase3(c, k0, -1, k1, s);             // 3b: the rest
         if (!rc && cudaStreamWaitEvent(s, evB, 0) != cudaSuccess) rc = set_error(APSP_ECUDA, "stream wait");
       }
+    } else if (c.side && f32chain) {
+      const int round = int(k0 / b);
+      FwSignals g3a;
+      g3a.tile_flags = c.tflags; g3a.tile_ld = nt; g3a.tile_round = round;
+      if (k0 > 0) { g3a.wait_count = c.spin + 2; g3a.wait_target = p2_target; g3a.pdl = true; }
+      rc = fw_phase3(c, k0, k1, -1, s, -1, true, &g3a);     // 3a: next pivot cross
+      if (!rc && cudaEventRecord(evA, s) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
+      if (!rc && cudaStreamWaitEvent(c.side, evA, 0) != cudaSuccess) rc = set_error(APSP_ECUDA, "stream wait");
+      if (!rc) rc = fw_phase1(c, k1, c.side);
+      FwSignals gp2;
+      gp2.tile_flags = c.tflags; gp2.tile_ld = nt; gp2.tile_round = round + 1;
+      int pctas = 0;
+      if (!rc) rc = fw_phase2(c, k1, c.side, false, &gp2, false, c.spin + 2, &pctas);
+      p2_target += pctas;
+      FwSignals g3b;
+      g3b.tile_flags = c.tflags; g3b.tile_ld = nt; g3b.tile_round = round;
+      if (k2 < c.m) g3b.first_lo = k2;
+      if (!rc) rc = fw_phase3(c, k0, -1, k1, s, -1, true, &g3b);   // 3b: the rest
     } else if (c.side) {
       rc = fw_phase3(c, k0, k1, -1, s);                       // 3a: next pivot cross
       if (!rc && cudaEventRecord(evA, s) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");

@@ -106,7 +106,8 @@ struct MinplusArgs {
 size_t prep_bytes(int64_t m, int64_t n, int64_t k);
 int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
                      int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s, const int32_t* psrc = nullptr,
-                     int64_t lds = 0, int32_t* pdst = nullptr, int64_t ldd = 0, int64_t pcols = 0);
+                     int64_t lds = 0, int32_t* pdst = nullptr, int64_t ldd = 0, int64_t pcols = 0,
+                     int* exit_count = nullptr, int* ctas = nullptr);
 
 // Row tiles per rasterisation group of full-grid launches (APSP_RASTER_G, default 1 = row-major).
 int raster_group();

@@ -731,9 +731,34 @@ template <int G>
 __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
   extern __shared__ __align__(128) unsigned char smraw_dm[];
   SmemF32DM& sm = *reinterpret_cast<SmemF32DM*>(smraw_dm);
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // (FW 3b behind 3a: see minplus_nt_kernel)
+  if (p.wait_count) {   // operands produced by a kernel on another stream (fw_sched.cu f32 chain)
+    if (threadIdx.x == 0) {
+      int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.wait_count) : "memory");
+        if (v >= p.wait_target) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
   int64_t i0, j0;
   tile_origin(p, BM, DM_BN, i0, j0);
+  int* tflag = nullptr;   // round flag of the 128 x 128 tile this half belongs to (2 per round)
+  if (p.tile_flags && !tile_skipped(p, i0, j0, BM, DM_BN)) {
+    tflag = p.tile_flags + (i0 / BM) * p.tile_ld + j0 / BM;
+    if (threadIdx.x == 0) {
+      int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(tflag) : "memory");
+        if (v >= 2 * p.tile_round) break;
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+  }
+  // (FW 3b behind 3a: see minplus_nt_kernel; issued after the waits)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tile_skipped(p, i0, j0, BM, DM_BN)) return;
   const int t = threadIdx.x, tx = t & 7, ty = t >> 3;
   const int64_t nch = p.k / SUB;
@@ -959,6 +984,11 @@ __global__ void __launch_bounds__(NT, 2) minplus_f32dm_kernel(MinplusArgs p) {
     }
   }
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+  if (tflag) {   // this half-tile's update is stored
+    __threadfence();
+    __syncthreads();
+    if (t == 0) atomicAdd(tflag, 1);
+  }
 }
 
 // B (k x n) fp32 -> [n/64][k/32][32][64] for the deferred-argmin kernel
@@ -989,11 +1019,27 @@ struct PredCopy {   // optional int32 band copy riding along a prep launch (grid
   int32_t* dst;
   int64_t ldd, cols;
   int vec;
+  int* exit_count;   // optional: every CTA adds 1 once its stores are fenced (fw_sched.cu f32 chain)
 };
+template <int KIND>
+__device__ __forceinline__ void prep_pair_body(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t nch,
+                                               int64_t nta, int64_t ntb, uint32_t* Aprep, void* Bprep,
+                                               const PredCopy& pc);
 template <int KIND>
 __global__ void __launch_bounds__(NT) prep_pair_kernel(const void* A, int64_t lda, const void* B, int64_t ldb,
                                                        int64_t nch, int64_t nta, int64_t ntb, uint32_t* Aprep,
                                                        void* Bprep, PredCopy pc) {
+  prep_pair_body<KIND>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep, pc);
+  if (pc.exit_count) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(pc.exit_count, 1);
+  }
+}
+template <int KIND>
+__device__ __forceinline__ void prep_pair_body(const void* A, int64_t lda, const void* B, int64_t ldb, int64_t nch,
+                                               int64_t nta, int64_t ntb, uint32_t* Aprep, void* Bprep,
+                                               const PredCopy& pc) {
   const int64_t c = blockIdx.x, tile = blockIdx.y;
   if (blockIdx.z == 2) {   // pred snapshot rows [32c, 32c + 32) x columns [128 tile, 128 tile + 128)
     const int64_t j0 = 128 * tile;
@@ -1036,7 +1082,7 @@ __global__ void __launch_bounds__(NT) prep_pair_kernel(const void* A, int64_t ld
 
 int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64_t ldb, int64_t m, int64_t n,
                      int64_t k, uint32_t* Aprep, void* Bprep, cudaStream_t s, const int32_t* psrc, int64_t lds,
-                     int32_t* pdst, int64_t ldd, int64_t pcols) {
+                     int32_t* pdst, int64_t ldd, int64_t pcols, int* exit_count, int* ctas) {
   const size_t es = (store == STORE_W32 || store == STORE_F32) ? 4 : store == STORE_U16 ? 2 : 1;
   if (m % BM || n % BN || k % SUB || (lda * es) % 16 || (ldb * es) % 16 || (reinterpret_cast<uintptr_t>(A) & 15) ||
       (reinterpret_cast<uintptr_t>(B) & 15))
@@ -1045,13 +1091,14 @@ int launch_prep_bulk(int store, const void* A, int64_t lda, const void* B, int64
   const bool dm = store == STORE_F32 && f32_deferred();
   const int64_t ntb = n / (dm ? DM_BN : BN);
   // optional third part: copy a k x pcols int32 pred band (the phase-2 pred snapshot)
-  PredCopy pc{psrc, lds, pdst, ldd, pcols, 0};
+  PredCopy pc{psrc, lds, pdst, ldd, pcols, 0, exit_count};
   if (psrc) {
     pc.vec = (lds % 4 == 0 && ldd % 4 == 0 && pcols % 128 == 0 &&
               ((reinterpret_cast<uintptr_t>(psrc) | reinterpret_cast<uintptr_t>(pdst)) & 15) == 0);
   }
   const int64_t tiles = std::max(std::max(nta, ntb), psrc ? (pcols + 127) / 128 : int64_t(0));
   const dim3 g(unsigned(nch), unsigned(tiles), psrc ? 3 : 2);
+  if (ctas) *ctas = int(g.x * g.y * g.z);
   switch (store) {
     case STORE_U8: prep_pair_kernel<PREP_U8><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep, pc); break;
     case STORE_U16: prep_pair_kernel<PREP_U16><<<g, NT, 0, s>>>(A, lda, B, ldb, nch, nta, ntb, Aprep, Bprep, pc); break;

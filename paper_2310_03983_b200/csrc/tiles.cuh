@@ -33,22 +33,23 @@ __device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn
       j0 = int64_t(lo_c + cc) * bn;
     }
   } else if (p.first_lo < p.first_hi) {   // 1D: the cross of [first_lo, first_hi) first, then the rest
-    const int w = int((p.first_hi - p.first_lo) / bm), lo_t = int(p.first_lo / bm);   // square tiles
+    const int wr = int((p.first_hi - p.first_lo) / bm), lo_r = int(p.first_lo / bm);
+    const int wc = int((p.first_hi - p.first_lo) / bn), lo_c = int(p.first_lo / bn);
     const int nt_r = int((p.m + bm - 1) / bm), nt_c = int((p.n + bn - 1) / bn);
-    const int id = int(blockIdx.x), ncross = w * nt_c + (nt_r - w) * w;
+    const int id = int(blockIdx.x), ncross = wr * nt_c + (nt_r - wr) * wc;
     if (id < ncross) {
-      if (id < w * nt_c) {
-        i0 = int64_t(lo_t + id / nt_c) * bm;
+      if (id < wr * nt_c) {
+        i0 = int64_t(lo_r + id / nt_c) * bm;
         j0 = int64_t(id % nt_c) * bn;
       } else {
-        const int id2 = id - w * nt_c, rr = id2 / w, cc = id2 % w;
-        i0 = int64_t(rr < lo_t ? rr : rr + w) * bm;
-        j0 = int64_t(lo_t + cc) * bn;
+        const int id2 = id - wr * nt_c, rr = id2 / wc, cc = id2 % wc;
+        i0 = int64_t(rr < lo_r ? rr : rr + wr) * bm;
+        j0 = int64_t(lo_c + cc) * bn;
       }
     } else {
-      const int id3 = id - ncross, rr = id3 / (nt_c - w), cc = id3 % (nt_c - w);
-      i0 = int64_t(rr < lo_t ? rr : rr + w) * bm;
-      j0 = int64_t(cc < lo_t ? cc : cc + w) * bn;
+      const int id3 = id - ncross, rr = id3 / (nt_c - wc), cc = id3 % (nt_c - wc);
+      i0 = int64_t(rr < lo_r ? rr : rr + wr) * bm;
+      j0 = int64_t(cc < lo_c ? cc : cc + wc) * bn;
     }
   } else if (p.raster > 1) {
     // Grouped rasterisation: CTAs launch in linear blockIdx order, so consecutive CTAs take the
