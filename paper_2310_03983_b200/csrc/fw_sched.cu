@@ -528,12 +528,13 @@ int fw_run(FwCtx& c, cudaStream_t s) {
   const bool split = chain && c.m <= split_max;
   const int xmul = split ? 2 : 1;
   const int nt = int(c.m / TILE_ALIGN);
-  // The exact fp32 tier's round overlap (its 3b is the bound at n=4096: 6.5 waves of 128 x 64
-  // tiles): 3a(K+1) runs behind 3b(K) on per-tile flags and waits on the device for the phase-3
+  // The exact fp32 and w32 tiers' round overlap (their 3b is the bound at n=4096: 6.5 waves of
+  // 128 x 64 fp32 tiles, of 1-CTA/SM w32 tiles): 3a(K+1) runs behind 3b(K) on per-tile flags and waits on the device for the phase-3
   // prep of K+1 (its exit count) instead of a stream event; 3b enumerates the next cross first.
   // The closure and the panels stay event-ordered on the side stream.
-  const bool f32chain = !spin && c.side && c.spin && c.tflags && b == TILE_ALIGN && c.store == STORE_F32 &&
-                        c.prep[0] && bulk_store(c.store, b) && c.p2prep && !getenv("APSP_NO_DEVCHAIN");
+  const bool f32chain = !spin && c.side && c.spin && c.tflags && b == TILE_ALIGN &&
+                        (c.store == STORE_F32 || c.store == STORE_W32) && c.prep[0] && bulk_store(c.store, b) &&
+                        c.p2prep && !getenv("APSP_NO_DEVCHAIN");
   if (spin || f32chain) {   // [0] 3a exit count, [1] diagonal flag, [2] cross / prep exit count; tile flags
     APSP_CUDA_TRY(cudaMemsetAsync(c.spin, 0, 3 * sizeof(int), s));
     if (chain || f32chain) APSP_CUDA_TRY(cudaMemsetAsync(c.tflags, 0, size_t(nt) * nt * sizeof(int), s));

@@ -483,9 +483,34 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
   constexpr uint32_t TMASK = (1u << W32_TAG) - 1u;
   extern __shared__ __align__(128) unsigned char smraw_w32[];
   SmemW32NT& sm = *reinterpret_cast<SmemW32NT*>(smraw_w32);
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // (FW 3b behind 3a: see minplus_nt_kernel)
+  if (p.wait_count) {   // operands produced by a kernel on another stream (fw_sched.cu round overlap)
+    if (threadIdx.x == 0) {
+      int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p.wait_count) : "memory");
+        if (v >= p.wait_target) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
   int64_t i0, j0;
   tile_origin(p, BM, BN, i0, j0);
+  int* tflag = nullptr;   // this tile's round flag (a whole tile: 2 per round)
+  if (p.tile_flags && !tile_skipped(p, i0, j0, BM, BN)) {
+    tflag = p.tile_flags + (i0 / BM) * p.tile_ld + j0 / BN;
+    if (threadIdx.x == 0) {
+      int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(tflag) : "memory");
+        if (v >= 2 * p.tile_round) break;
+        __nanosleep(32);
+      }
+    }
+    __syncthreads();
+  }
+  // (FW 3b behind 3a: see minplus_nt_kernel; issued after the waits)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (tile_skipped(p, i0, j0, BM, BN)) return;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
   const int64_t nch = p.k / SUB;
@@ -665,6 +690,11 @@ __global__ void __launch_bounds__(NT, 1) minplus_w32nt_kernel(MinplusArgs p) {
   // peer stores are ordered before anything the host signals after this kernel
   if (p.npeers) __threadfence_system();
   if (p.status && p.track_changed && __syncthreads_or(changed) && t == 0) p.status->changed = 1;
+  if (tflag) {   // this round's update of the tile is stored
+    __threadfence();
+    __syncthreads();
+    if (t == 0) atomicAdd(tflag, 2);
+  }
 }
 
 // RAW: plain 32-bit copies in the same layout (the exact fp32 tier); else w32 keys v << 7
