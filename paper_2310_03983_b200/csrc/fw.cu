@@ -97,6 +97,45 @@ __global__ void __launch_bounds__(K1CTA_THREADS) fw_classic_cta_kernel(typename 
   if (st && overflow) st->overflow = 1;
 }
 
+// The narrow stores (n even): cells as 16-bit values in shared memory, relaxed two at a time --
+// one packed add (VADD2) and one packed compare per column pair, row k's pairs in registers.
+// Sums stay below 2^16 (u8 <= 510, u16 <= 1022) and a stored sum is below the tier's Infinity,
+// so there is nothing to flag. Same strict-< rule and pred copy as above.
+template <int S>
+__global__ void __launch_bounds__(K1CTA_THREADS) fw_classic_cta_packed_kernel(typename StoreT<S>::T* D, int64_t ld,
+                                                                              int n, int32_t* idx, int64_t ldi) {
+  using T = typename StoreT<S>::T;
+  extern __shared__ __align__(16) unsigned char smraw_k1p[];
+  uint16_t* Ds = reinterpret_cast<uint16_t*>(smraw_k1p);   // n x n, row pitch n (even)
+  const int t = threadIdx.x, tx = t & 31, ty = t >> 5, np = n >> 1;
+  const uint32_t inf = uint32_t(store_inf<S>());
+  for (int e = t; e < n * n; e += K1CTA_THREADS) Ds[e] = uint16_t(D[int64_t(e / n) * ld + e % n]);
+  __syncthreads();
+  for (int k = 0; k < n; k++) {
+    const uint32_t* rowk = reinterpret_cast<const uint32_t*>(Ds + k * n);
+    for (int i = ty; i < n; i += 32) {
+      const uint32_t dik = Ds[i * n + k];
+      if (dik == inf) continue;   // nothing through an unreachable k
+      const uint32_t dik2 = dik * 0x00010001u;
+      uint32_t* rowi = reinterpret_cast<uint32_t*>(Ds + i * n);
+      for (int q = tx; q < np; q += 32) {
+        const uint32_t cur = rowi[q], cand = __vadd2(dik2, rowk[q]);
+        const uint32_t lt = __vcmpltu2(cand, cur);   // 0xFFFF in each half that strictly improves
+        if (lt) {
+          rowi[q] = (cand & lt) | (cur & ~lt);
+          if (idx) {
+            const int64_t j = 2 * q;
+            if (lt & 0xFFFFu) idx[int64_t(i) * ldi + j] = idx[int64_t(k) * ldi + j];
+            if (lt >> 16) idx[int64_t(i) * ldi + j + 1] = idx[int64_t(k) * ldi + j + 1];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = t; e < n * n; e += K1CTA_THREADS) D[int64_t(e / n) * ld + e % n] = T(Ds[e]);
+}
+
 // true (and launched) when the whole n x n store fits one CTA's shared memory
 int launch_fw_classic_cta(int store, void* D, int64_t ld, int64_t n, int32_t* idx, int64_t ldi, Status* st,
                           cudaStream_t s, bool& done) {
@@ -104,8 +143,24 @@ int launch_fw_classic_cta(int store, void* D, int64_t ld, int64_t n, int32_t* id
   const size_t bytes = size_t(n) * n * store_elem_size(store);
   // one SM's issue rate bounds it: 2x the graph-replayed steps at n=128, ~8% at 256, slower above
   if (n < 2 || n > 256 || bytes > K1CTA_MAX_SMEM || getenv("APSP_K1_STEPS")) return 0;
-  static std::atomic<unsigned long long> a8{0}, a16{0}, a32{0}, af{0}, a64{0}, aw{0};
+  static std::atomic<unsigned long long> a8{0}, a16{0}, a32{0}, af{0}, a64{0}, aw{0}, p8{0}, p16{0};
   const int sb = int(bytes);
+  if ((store == STORE_U8 || store == STORE_U16) && n % 2 == 0 && size_t(n) * n * 2 <= K1CTA_MAX_SMEM &&
+      !getenv("APSP_K1_SCALAR")) {
+    const int sp = int(size_t(n) * n * 2);
+    if (store == STORE_U8) {
+      APSP_CUDA_TRY(smem_optin(fw_classic_cta_packed_kernel<STORE_U8>, int(K1CTA_MAX_SMEM), p8));
+      fw_classic_cta_packed_kernel<STORE_U8><<<1, K1CTA_THREADS, sp, s>>>(static_cast<uint8_t*>(D), ld, int(n), idx, ldi);
+    } else {
+      APSP_CUDA_TRY(smem_optin(fw_classic_cta_packed_kernel<STORE_U16>, int(K1CTA_MAX_SMEM), p16));
+      fw_classic_cta_packed_kernel<STORE_U16><<<1, K1CTA_THREADS, sp, s>>>(static_cast<uint16_t*>(D), ld, int(n), idx,
+                                                                            ldi);
+    }
+    APSP_CUDA_TRY(cudaGetLastError());
+    count_launches(1);
+    done = true;
+    return 0;
+  }
   switch (store) {
 #define K1CTA(ST, TT, ATTR)                                                                                  \
   case ST:                                                                                                   \
