@@ -73,11 +73,16 @@ __global__ void __launch_bounds__(K1CTA_THREADS) fw_classic_cta_kernel(typename 
   using A = typename StoreT<S>::A;
   extern __shared__ __align__(16) unsigned char smraw_k1[];
   T* Ds = reinterpret_cast<T*>(smraw_k1);   // n x n, row pitch n
+  int32_t* prow = reinterpret_cast<int32_t*>(smraw_k1 + ((size_t(n) * n * sizeof(T) + 15) / 16) * 16);
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5;
   for (int e = t; e < n * n; e += K1CTA_THREADS) Ds[e] = D[int64_t(e / n) * ld + e % n];
   __syncthreads();
   bool overflow = false;
   for (int k = 0; k < n; k++) {
+    if (idx) {   // pred row k (invariant in step k) into shared memory first
+      for (int j = t; j < n; j += K1CTA_THREADS) prow[j] = idx[int64_t(k) * ldi + j];
+      __syncthreads();
+    }
     const T* rowk = Ds + k * n;
     for (int i = ty; i < n; i += 32) {
       const A dik = A(Ds[i * n + k]);
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(K1CTA_THREADS) fw_classic_cta_kernel(typename 
         if (c < A(Ds[i * n + j])) {
           overflow |= range_overflow<S>(c);
           Ds[i * n + j] = T(c);
-          if (idx) idx[int64_t(i) * ldi + j] = idx[int64_t(k) * ldi + j];
+          if (idx) idx[int64_t(i) * ldi + j] = prow[j];
         }
       }
     }
@@ -107,11 +112,18 @@ __global__ void __launch_bounds__(K1CTA_THREADS) fw_classic_cta_packed_kernel(ty
   using T = typename StoreT<S>::T;
   extern __shared__ __align__(16) unsigned char smraw_k1p[];
   uint16_t* Ds = reinterpret_cast<uint16_t*>(smraw_k1p);   // n x n, row pitch n (even)
+  int32_t* prow = reinterpret_cast<int32_t*>(Ds + n * n);  // pred row k of the current step
   const int t = threadIdx.x, tx = t & 31, ty = t >> 5, np = n >> 1;
   const uint32_t inf = uint32_t(store_inf<S>());
   for (int e = t; e < n * n; e += K1CTA_THREADS) Ds[e] = uint16_t(D[int64_t(e / n) * ld + e % n]);
   __syncthreads();
   for (int k = 0; k < n; k++) {
+    // pred row k (invariant in step k) into shared memory first: an improved cell then copies
+    // it from there instead of waiting on a global load (the loop was bound by those)
+    if (idx) {
+      for (int j = t; j < n; j += K1CTA_THREADS) prow[j] = idx[int64_t(k) * ldi + j];
+      __syncthreads();
+    }
     const uint32_t* rowk = reinterpret_cast<const uint32_t*>(Ds + k * n);
     for (int i = ty; i < n; i += 32) {
       const uint32_t dik = Ds[i * n + k];
@@ -125,8 +137,8 @@ __global__ void __launch_bounds__(K1CTA_THREADS) fw_classic_cta_packed_kernel(ty
           rowi[q] = (cand & lt) | (cur & ~lt);
           if (idx) {
             const int64_t j = 2 * q;
-            if (lt & 0xFFFFu) idx[int64_t(i) * ldi + j] = idx[int64_t(k) * ldi + j];
-            if (lt >> 16) idx[int64_t(i) * ldi + j + 1] = idx[int64_t(k) * ldi + j + 1];
+            if (lt & 0xFFFFu) idx[int64_t(i) * ldi + j] = prow[j];
+            if (lt >> 16) idx[int64_t(i) * ldi + j + 1] = prow[j + 1];
           }
         }
       }
@@ -140,14 +152,14 @@ __global__ void __launch_bounds__(K1CTA_THREADS) fw_classic_cta_packed_kernel(ty
 int launch_fw_classic_cta(int store, void* D, int64_t ld, int64_t n, int32_t* idx, int64_t ldi, Status* st,
                           cudaStream_t s, bool& done) {
   done = false;
-  const size_t bytes = size_t(n) * n * store_elem_size(store);
+  const size_t bytes = (size_t(n) * n * store_elem_size(store) + 15) / 16 * 16 + size_t(n) * 4;   // + pred row
   // one SM's issue rate bounds it: 2x the graph-replayed steps at n=128, ~8% at 256, slower above
   if (n < 2 || n > 256 || bytes > K1CTA_MAX_SMEM || getenv("APSP_K1_STEPS")) return 0;
   static std::atomic<unsigned long long> a8{0}, a16{0}, a32{0}, af{0}, a64{0}, aw{0}, p8{0}, p16{0};
   const int sb = int(bytes);
-  if ((store == STORE_U8 || store == STORE_U16) && n % 2 == 0 && size_t(n) * n * 2 <= K1CTA_MAX_SMEM &&
+  if ((store == STORE_U8 || store == STORE_U16) && n % 2 == 0 && size_t(n) * n * 2 + size_t(n) * 4 <= K1CTA_MAX_SMEM &&
       !getenv("APSP_K1_SCALAR")) {
-    const int sp = int(size_t(n) * n * 2);
+    const int sp = int(size_t(n) * n * 2 + size_t(n) * 4);
     if (store == STORE_U8) {
       APSP_CUDA_TRY(smem_optin(fw_classic_cta_packed_kernel<STORE_U8>, int(K1CTA_MAX_SMEM), p8));
       fw_classic_cta_packed_kernel<STORE_U8><<<1, K1CTA_THREADS, sp, s>>>(static_cast<uint8_t*>(D), ld, int(n), idx, ldi);
