@@ -19,6 +19,7 @@ Dense int32 / fp32 arrays (numpy or CUDA torch tensors) go through ``solve``.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 from dataclasses import dataclass, field
 
@@ -256,21 +257,24 @@ def solve(h, algorithm: str = "fw_blocked", *, track: str = "pred", base_thresho
     ws_need = lib.apsp_workspace_bytes(alg, dt, n, block)
     # The library runs on `s`; whatever produced `h` (and a caller's `workspace`) was queued on
     # the current stream, so `s` waits for it, and the copies/allocations below are made on `s`.
-    if s != cur:
+    side = s != cur
+    if side:
         s.wait_stream(cur)
-    with torch.cuda.stream(s):
+    # (the stream / device context managers cost ~10 us per call at small n: entered only when
+    # they change something)
+    with torch.cuda.stream(s) if side else contextlib.nullcontext():
         dist = h.contiguous().clone()
         idx = torch.empty((n, n), dtype=torch.int32, device=h.device)
         if workspace is None and ws_need:
             workspace = torch.empty(ws_need, dtype=torch.uint8, device=h.device)
-    if s != cur:
+    if side:
         # the outputs are handed back to a caller on `cur` (who syncs with `s` before reading,
         # as with any side-stream result): their blocks must not be recycled while `cur` uses them
         for t in (dist, idx):
             t.record_stream(cur)
     wp = workspace.data_ptr() if workspace is not None else None
     wb = workspace.numel() if workspace is not None else 0
-    with torch.cuda.device(h.device):
+    with torch.cuda.device(h.device) if h.device.index != torch.cuda.current_device() else contextlib.nullcontext():
         if alg == nat.ALG_FW_BLOCKED:
             st = lib.apsp_fw_blocked(dt, n, dist.data_ptr(), n, idx.data_ptr(), n, block, _tier_arg(tier), wp, wb,
                                      sp, ctypes.byref(info))
