@@ -189,6 +189,7 @@ struct FwSignals {
   int tile_ld = 0;
   int tile_round = 0;
   int64_t first_lo = -1;   // 3b: enumerate this pivot cross first (width b)
+  int id_begin = 0, id_count = 0;   // first mode: a sub-range of the enumeration
   bool pdl = false;        // launch behind the previous kernel with programmatic serialization
   bool split_rows = false; // two half-row CTAs per tile (the latency-bound cross launches)
 };
@@ -201,6 +202,7 @@ static void apply_signals(MinplusArgs& a, const FwSignals* g, int64_t b) {
   a.wait_count = g->wait_count; a.wait_target = g->wait_target;
   a.tile_flags = g->tile_flags; a.tile_ld = g->tile_ld; a.tile_round = g->tile_round;
   if (g->first_lo >= 0) { a.first_lo = g->first_lo; a.first_hi = g->first_lo + b; }
+  a.id_begin = g->id_begin; a.id_count = g->id_count;
   if (g->pdl && !getenv("APSP_NO_PDL")) a.pdl = 1;
   a.split_rows = g->split_rows ? 1 : 0;
 }
@@ -499,6 +501,43 @@ static int cross_ctas(int64_t m, int64_t b) {
   return int(w * nt + (nt - w) * w);
 }
 
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Where to cut the enumeration of 3b(K) (cross of K2 first, then the rest row-major; tiles in the
+// crosses of K and K+1 are skipped) so that the ids after the cut hold the active tiles of the
+// last, partial wave of `slots` CTAs; -1 when that wave is at least half full (nothing to gain).
+// Mirrors tile_origin's cross-first mapping with b = 128 (one tile per band).
+static int tail_split(int nt, int K, int K2, int slots) {
+  const int total = nt * nt, active = (nt - 2) * (nt - 2);
+  const int tail = active % slots;
+  if (tail == 0 || 2 * tail >= slots || active < slots) return -1;
+  auto tile_of = [&](int id, int& I, int& J) {
+    const int ncross = nt + (nt - 1);
+    if (id < nt) { I = K2; J = id; return; }
+    if (id < ncross) { const int rr = id - nt; I = rr < K2 ? rr : rr + 1; J = K2; return; }
+    const int id3 = id - ncross, rr = id3 / (nt - 1), cc = id3 % (nt - 1);
+    I = rr < K2 ? rr : rr + 1;
+    J = cc < K2 ? cc : cc + 1;
+  };
+  int seen = 0;
+  for (int id = total - 1; id >= 0; id--) {
+    int I = 0, J = 0;
+    tile_of(id, I, J);
+    const bool skipped = I == K || J == K || I == K + 1 || J == K + 1;
+    if (!skipped && ++seen == tail) return id;
+  }
+  return -1;
+}
+
 static bool deep_enabled(const FwCtx& c) {
   return c.side && c.prep[0] && bulk_store(c.store, c.b) && getenv("APSP_DEEP") && c.m >= 3 * c.b;
 }
@@ -616,7 +655,23 @@ int fw_run(FwCtx& c, cudaStream_t s) {
         FwSignals g3b;   // 3b(K): tile flags, the next 3a's tiles (cross of K+2) first
         g3b.tile_flags = c.tflags; g3b.tile_ld = nt; g3b.tile_round = round;
         if (k2 < c.m) g3b.first_lo = k2;
-        if (!rc) rc = fw_phase3(c, k0, -1, k1, s, -1, true, &g3b);
+        // A last wave that would run mostly empty goes out as half-row CTAs in a second launch
+        // behind the first: twice the CTAs at half the work each fill it twice as fast. Only in
+        // the chain-bound sizes (with the half-row cross launches): n=3584 2.38 -> 2.30 ms; from
+        // n=4096 on the next round already fills that wave (4096: 3.16 -> 3.18, 6144: 9.78 -> 9.89).
+        const int cut = split && k2 < c.m ? tail_split(nt, int(k0 / b), int(k2 / b), 2 * sm_count()) : -1;
+        if (cut > 0 && !getenv("APSP_NO_TAIL_SPLIT")) {
+          g3b.id_count = cut;
+          if (!rc) rc = fw_phase3(c, k0, -1, k1, s, -1, true, &g3b);
+          FwSignals g3t = g3b;
+          g3t.id_begin = cut;
+          g3t.id_count = 0;
+          g3t.split_rows = true;
+          g3t.pdl = true;
+          if (!rc) rc = fw_phase3(c, k0, -1, k1, s, -1, true, &g3t);
+        } else if (!rc) {
+          rc = fw_phase3(c, k0, -1, k1, s, -1, true, &g3b);
+        }
       } else {
         if (!rc && cudaEventRecord(evB, c.side) != cudaSuccess) rc = set_error(APSP_ECUDA, "event record");
         if (!rc) rc = fw_phase3(c, k0, -1, k1, s);             // 3b: the rest

@@ -96,6 +96,10 @@ struct MinplusArgs {
   // (half the work each: the latency-bound FW 3a / cross launches use twice the SMs). Round
   // flags and the diagonal flag then count halves: a whole-tile CTA adds 2, a half adds 1.
   int split_rows;
+  // First-mode launches (first_lo < first_hi): this launch covers CTA ids [id_begin, id_begin +
+  // grid) of the enumeration (a launch split in two: whole tiles, then the tail as half rows)
+  int id_begin;
+  int id_count;   // 0: to the end of the enumeration
   // Full-grid launches: grouped tile order (row tiles per group; <= 1: row-major), see tile_origin
   int raster;
 };

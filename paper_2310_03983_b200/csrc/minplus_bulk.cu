@@ -1331,8 +1331,9 @@ int launch_nt(const MinplusArgs& a, cudaStream_t s) {
   const size_t es = sizeof(typename Narrow<S>::T);
   if (a.m % BM || a.n % BN || a.k % SUB || (reinterpret_cast<uintptr_t>(a.C) & 15) || (a.ldc * es) % 16)
     return set_error(2, "bulk-staged narrow tiles need full 128 x 128 tiles and 32-multiple k");
-  if (a.split_rows) {   // half-row CTAs: cross-list launches without peers only
-    if (a.npeers || !(a.only_lo < a.only_hi)) return set_error(2, "half-row tiles are for cross-list launches");
+  if (a.split_rows) {   // half-row CTAs: cross-list or first-mode launches without peers only
+    if (a.npeers || !(a.only_lo < a.only_hi || a.first_lo < a.first_hi))
+      return set_error(2, "half-row tiles are for cross-list / cross-first launches");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid_for(a, BM, BN);
     cfg.blockDim = dim3(NT);

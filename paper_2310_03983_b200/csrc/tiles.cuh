@@ -36,7 +36,7 @@ __device__ __forceinline__ void tile_origin(const MinplusArgs& p, int bm, int bn
     const int wr = int((p.first_hi - p.first_lo) / bm), lo_r = int(p.first_lo / bm);
     const int wc = int((p.first_hi - p.first_lo) / bn), lo_c = int(p.first_lo / bn);
     const int nt_r = int((p.m + bm - 1) / bm), nt_c = int((p.n + bn - 1) / bn);
-    const int id = int(blockIdx.x), ncross = wr * nt_c + (nt_r - wr) * wc;
+    const int id = (int(blockIdx.x) >> (p.split_rows ? 1 : 0)) + p.id_begin, ncross = wr * nt_c + (nt_r - wr) * wc;
     if (id < ncross) {
       if (id < wr * nt_c) {
         i0 = int64_t(lo_r + id / nt_c) * bm;
@@ -218,7 +218,11 @@ inline dim3 grid_for(const MinplusArgs& a, int bm, int bn) {
     const int64_t nt_r = (a.m + bm - 1) / bm, nt_c = (a.n + bn - 1) / bn;
     return dim3(unsigned((wr * nt_c + (nt_r - wr) * wc) << (a.split_rows ? 1 : 0)), 1);
   }
-  if (a.first_lo < a.first_hi) return dim3(unsigned(((a.n + bn - 1) / bn) * ((a.m + bm - 1) / bm)), 1);
+  if (a.first_lo < a.first_hi) {
+    const int64_t total = ((a.n + bn - 1) / bn) * ((a.m + bm - 1) / bm);
+    const int64_t cnt = a.id_count > 0 ? a.id_count : total - a.id_begin;
+    return dim3(unsigned(cnt << (a.split_rows ? 1 : 0)), 1);
+  }
   return dim3(unsigned((a.n + bn - 1) / bn), unsigned((a.m + bm - 1) / bm));
 }
 
